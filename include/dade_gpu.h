@@ -1,0 +1,177 @@
+/*
+ * dade_gpu.h — C ABI of the B200-native DADE distance-comparison hot path.
+ *
+ * One handle = one GPU context holding device-resident copies of the
+ * artifacts the reference's search path reads (transform, IVF lists or flat
+ * base rows, strategy tables). Calls on one handle are externally serialised
+ * (SURVEY.md §8b "Threading"); every entry point returns a status code and
+ * never throws. The C++ mirror of the reference API over this ABI is
+ * include/dade_gpu.hpp; the Python mirror is paper_2411_17229_b200/.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference):
+ *   dade_gpu_set_transform   OrthoTransform fields      proj/include/dade/transform.hpp:42-64
+ *   dade_gpu_rotate          apply_transform            proj/src/transform.cpp:221-228, 295-304
+ *   dade_gpu_set_ivf         IvfIndex (DIVF field order) proj/src/ivf.cpp:233-247, 249-279
+ *   dade_gpu_set_base        linear_scan's VectorSet    proj/src/knn.cpp:31-41
+ *   dade_gpu_set_strategy    DadeStrategy / AdsamplingStrategy / FdScanningStrategy
+ *                            precomputed tables         proj/src/estimator.cpp:99-177
+ *   dade_gpu_set_strategy_dade  DadeStrategy ctor incl. its ConfigError checks
+ *                                                       proj/src/estimator.cpp:115-152
+ *   dade_gpu_ivf_search      IvfIndex::search, batched  proj/src/ivf.cpp:207-231
+ *   dade_gpu_flat_search     linear_scan, batched       proj/src/knn.cpp:31-41
+ *   dade_gpu_dco_evaluate    DcoStrategy::evaluate      proj/include/dade/estimator.hpp:64-74
+ *   dade_gpu_partial_sums    partial_sqdist at every checkpoint
+ *                                                       proj/src/estimator.cpp:74-82
+ *   dade_gpu_calibrate       calibrate                  proj/src/calibration.cpp:109-146
+ *
+ * Status codes mirror the reference's exception split
+ * (proj/include/dade/error.hpp:10-19, proj/tools/dade_cli.cpp:407-419).
+ */
+#ifndef DADE_GPU_H_
+#define DADE_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    DADE_GPU_OK = 0,
+    DADE_GPU_RUNTIME_ERROR = 1, /* std::runtime_error (IO / corruption)           */
+    DADE_GPU_CONFIG_ERROR = 2,  /* dade::ConfigError (mismatched artifacts)        */
+    DADE_GPU_INVALID_INPUT = 3, /* dade::InvalidInput (precondition violated)      */
+    DADE_GPU_CUDA_ERROR = 4     /* CUDA runtime / launch failure                   */
+};
+
+/* strategy kinds (proj/include/dade/bench.hpp:19 DcoKind, hot-path subset) */
+enum { DADE_GPU_FD = 0, DADE_GPU_ADS = 1, DADE_GPU_DADE = 2 };
+
+/* search flags */
+enum {
+    DADE_GPU_QUERIES_RAW = 1u << 0, /* queries are in the raw basis: rotate on device first   */
+    DADE_GPU_DEVICE_PTRS = 1u << 1  /* every array argument is a device pointer; the call is
+                                       asynchronous on the handle's stream (no H2D/D2H)      */
+};
+
+typedef struct dade_gpu_ctx dade_gpu_ctx;
+
+/* DcoStats counters (proj/include/dade/estimator.hpp:24-49); accumulated into. */
+typedef struct {
+    uint64_t total_dco;
+    uint64_t dims_accumulated;
+    uint64_t eligible;
+    uint64_t failures;
+} dade_gpu_stats;
+
+const char* dade_gpu_last_error(void);
+const char* dade_gpu_version(void);
+
+int dade_gpu_create(int device, dade_gpu_ctx** out);
+int dade_gpu_destroy(dade_gpu_ctx* ctx);
+/* Work on a caller-owned cudaStream_t (NULL = the handle's own stream). */
+int dade_gpu_set_stream(dade_gpu_ctx* ctx, void* cuda_stream);
+int dade_gpu_synchronize(dade_gpu_ctx* ctx);
+
+/* Column-major f64 D x D matrix (column k = k-th direction) + nonincreasing
+ * variances; the lambda prefix sums are derived exactly as on load
+ * (proj/src/transform.cpp:21-25, 338-342). */
+int dade_gpu_set_transform(dade_gpu_ctx* ctx, uint32_t dim, const double* matrix,
+                           const double* eigenvalues);
+
+/* IVF lists in DIVF field order. layout 0 = contiguous (split == dim),
+ * 1 = split (per-list head block [len x split] then tail block). Host pointers. */
+int dade_gpu_set_ivf(dade_gpu_ctx* ctx, uint32_t dim, uint32_t count, uint32_t n_clusters,
+                     uint32_t layout, uint32_t split, const float* centroids,
+                     const uint32_t* offsets, const uint32_t* ids, const float* storage);
+
+/* Multi-GPU list sharding: keep only lists with mask[c] != 0
+ * on this device. Centroids stay replicated so coarse ranking is global. */
+int dade_gpu_set_ivf_shard(dade_gpu_ctx* ctx, const uint8_t* list_mask);
+
+/* Flat base rows (linear_scan). Returned ids are row + id_base, so a row shard
+ * of a larger base reports global ids. Host pointer. */
+int dade_gpu_set_base(dade_gpu_ctx* ctx, uint32_t dim, uint32_t count, const float* data,
+                      uint32_t id_base);
+
+/* Precomputed strategy tables: n checkpoints (ascending, < dim), reject_coeff[i]
+ * (reject iff partial > coeff * r^2), est_scale[i]. n == 0 (or kind == FD) is
+ * FdScanningStrategy. */
+int dade_gpu_set_strategy(dade_gpu_ctx* ctx, uint32_t kind, uint32_t dim, uint32_t n,
+                          const uint32_t* checkpoints, const double* reject_coeff,
+                          const double* est_scale);
+
+/* DadeStrategy(t, cal, delta_d) on the handle's transform, with the
+ * reference's validation (ConfigError on step / grid mismatch). */
+int dade_gpu_set_strategy_dade(dade_gpu_ctx* ctx, uint32_t delta_d, uint32_t cal_delta_d,
+                               uint32_t n, const uint32_t* cal_checkpoints,
+                               const double* cal_epsilons);
+
+/* AdsamplingStrategy(dim, delta_d, eps0). */
+int dade_gpu_set_strategy_ads(dade_gpu_ctx* ctx, uint32_t dim, uint32_t delta_d, double eps0);
+
+/* apply_transform: out = rotate(in), n rows of the handle's dim. */
+int dade_gpu_rotate(dade_gpu_ctx* ctx, const float* in, uint32_t n, float* out, uint32_t flags);
+
+/* Batched IvfIndex::search. Per query: up to k results ascending by
+ * (distance, id) in out_ids/out_dists [nq x k]; out_counts[q] < k means
+ * truncated. stats (nullable) accumulates. */
+int dade_gpu_ivf_search(dade_gpu_ctx* ctx, const float* queries, uint32_t nq, uint32_t k,
+                        uint32_t n_probe, uint32_t flags, uint32_t* out_ids, float* out_dists,
+                        uint32_t* out_counts, dade_gpu_stats* stats);
+
+/* Batched linear_scan over the flat base. */
+int dade_gpu_flat_search(dade_gpu_ctx* ctx, const float* queries, uint32_t nq, uint32_t k,
+                         uint32_t flags, uint32_t* out_ids, float* out_dists,
+                         uint32_t* out_counts, dade_gpu_stats* stats);
+
+/* Like the two searches, but leave the packed per-query top-K keys
+ * ((float_bits(dist) << 32) | id, ascending; UINT64_MAX = empty) in
+ * out_keys [nq x k] for a cross-GPU merge. Device pointers only. */
+int dade_gpu_ivf_search_keys(dade_gpu_ctx* ctx, const float* d_queries, uint32_t nq, uint32_t k,
+                             uint32_t n_probe, uint32_t flags, uint64_t* d_out_keys,
+                             dade_gpu_stats* stats);
+int dade_gpu_flat_search_keys(dade_gpu_ctx* ctx, const float* d_queries, uint32_t nq,
+                              uint32_t k, uint32_t flags, uint64_t* d_out_keys,
+                              dade_gpu_stats* stats);
+
+/* Merge G gathered key blocks [G x nq x k] (e.g. an NCCL all-gather) into the
+ * global top-K: ids/dists/counts as dade_gpu_ivf_search. Device pointers. */
+int dade_gpu_merge_keys(dade_gpu_ctx* ctx, const uint64_t* d_keys, uint32_t n_blocks,
+                        uint32_t nq, uint32_t k, uint32_t* d_out_ids, float* d_out_dists,
+                        uint32_t* d_out_counts);
+
+/* DcoStrategy::evaluate for n independent (o_i, q_i, r_i) with the current
+ * strategy. Host pointers unless DEVICE_PTRS. */
+int dade_gpu_dco_evaluate(dade_gpu_ctx* ctx, const float* o, const float* q, const float* r,
+                          uint32_t n, uint32_t flags, uint8_t* pruned, float* distance,
+                          uint8_t* distance_exact, uint32_t* dims_used, dade_gpu_stats* stats);
+
+/* Running partial sums of every pair at each checkpoint of the current
+ * strategy and at the full dim: out [n x (n_ckpt + 1)] f32. The estimator
+ * value of step i is est_scale[i] * out[p, i] (dade_estimate). */
+int dade_gpu_partial_sums(dade_gpu_ctx* ctx, const float* o, const float* q, uint32_t n,
+                          uint32_t flags, float* out);
+
+/* calibrate(t, data, p_s, delta_d, n_pairs, seed) over n rotated rows with
+ * the handle's transform: writes the checkpoint grid and epsilons (arrays of
+ * at least dim / delta_d entries) and returns the count in *n_out. */
+int dade_gpu_calibrate(dade_gpu_ctx* ctx, const float* data, uint32_t n, double p_s,
+                       uint32_t delta_d, uint64_t n_pairs, uint64_t seed, uint32_t flags,
+                       uint32_t* checkpoints, double* epsilons, uint32_t* n_out);
+
+/* Number of CUDA kernels this handle launched so far (bench evidence). */
+uint64_t dade_gpu_launch_count(dade_gpu_ctx* ctx);
+
+/* Measured device time (ms) of the DCO scan kernel(s) in the last search
+ * call, via CUDA events on the launching stream, and its algorithmic bytes
+ * (slice bytes read + list metadata). Requires dade_gpu_set_profiling(1). */
+int dade_gpu_set_profiling(dade_gpu_ctx* ctx, int on);
+int dade_gpu_last_scan_profile(dade_gpu_ctx* ctx, double* scan_ms, double* scan_bytes,
+                               double* total_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DADE_GPU_H_ */

@@ -1,0 +1,429 @@
+"""Python mirror of the reference's search API over the C ABI.
+
+Names, argument meaning and error behaviour follow proj/include/dade/*.hpp:
+``OrthoTransform``, ``CalibrationTable``, ``FdScanningStrategy``,
+``DadeStrategy``, ``AdsamplingStrategy``, ``IvfIndex.search``,
+``linear_scan``, ``DcoStats``, ``SearchResult``; batched variants
+(``search_batch``) are the GPU-native granularity. Every compute call goes to
+libdade_gpu.so; there is no host fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import ConfigError, InvalidInput, check, ptr
+
+__all__ = [
+    "Device", "OrthoTransform", "CalibrationTable", "FdScanningStrategy", "DadeStrategy",
+    "AdsamplingStrategy", "IvfIndex", "FlatIndex", "linear_scan", "DcoStats", "DcoOutcome",
+    "SearchResult", "Neighbor", "ConfigError", "InvalidInput", "expected_checkpoints",
+]
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _u32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def expected_checkpoints(dim: int, delta_d: int) -> list[int]:
+    """CalibrationTable::expected_checkpoints (proj/src/calibration.cpp:74-81)."""
+    if delta_d == 0:
+        raise InvalidInput("delta_d must be positive")
+    return list(range(delta_d, dim, delta_d))
+
+
+class Device:
+    """One GPU context (dade_gpu_ctx): owns device copies of the artifacts."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(_capi.lib.dade_gpu_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+        self._strategy_token = None
+
+    def close(self):
+        if self.h:
+            _capi.lib.dade_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None):
+        check(_capi.lib.dade_gpu_set_stream(self.h, C.c_void_p(stream_ptr)))
+
+    def synchronize(self):
+        check(_capi.lib.dade_gpu_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(_capi.lib.dade_gpu_launch_count(self.h))
+
+    def set_profiling(self, on: bool):
+        check(_capi.lib.dade_gpu_set_profiling(self.h, int(on)))
+
+    def last_scan_profile(self):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        check(_capi.lib.dade_gpu_last_scan_profile(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    # -- strategy plumbing ---------------------------------------------------
+    def apply(self, dco) -> None:
+        if self._strategy_token is dco:
+            return
+        dco._apply(self)
+        self._strategy_token = dco
+
+
+@dataclass
+class OrthoTransform:
+    """proj/include/dade/transform.hpp:42-64 (column-major f64 matrix)."""
+    dim: int
+    kind: int  # 0 pca, 1 random
+    mean: np.ndarray
+    eigenvalues: np.ndarray
+    matrix: np.ndarray  # D*D column-major (column k = k-th direction)
+
+    @property
+    def lambda_prefix(self) -> np.ndarray:
+        ev = np.maximum(self.eigenvalues, 0.0)
+        out = np.zeros(self.dim + 1)
+        acc = 0.0
+        for i, v in enumerate(ev):  # sequential sums, as prefix_sums()
+            acc = acc + float(v)
+            out[i + 1] = acc
+        return out
+
+    def scale_factor(self, d: int) -> float:
+        """OrthoTransform::scale_factor (proj/src/transform.cpp:209-214)."""
+        if d == 0 or d > self.dim:
+            raise InvalidInput("scale_factor: d out of range")
+        pre = self.lambda_prefix
+        return 1.0 if pre[d] <= 0.0 else pre[self.dim] / pre[d]
+
+    def upload(self, dev: Device):
+        check(_capi.lib.dade_gpu_set_transform(dev.h, self.dim, ptr(_f64(self.matrix)),
+                                               ptr(_f64(self.eigenvalues))))
+
+    def apply(self, dev: Device, rows: np.ndarray) -> np.ndarray:
+        """apply_transform (proj/src/transform.cpp:295-304) on the GPU."""
+        rows = _f32(rows)
+        if rows.ndim != 2 or rows.shape[1] != self.dim:
+            raise InvalidInput("apply_transform: dimension mismatch")
+        self.upload(dev)
+        out = np.empty_like(rows)
+        check(_capi.lib.dade_gpu_rotate(dev.h, ptr(rows), rows.shape[0], ptr(out), 0))
+        return out
+
+
+@dataclass
+class CalibrationTable:
+    """proj/include/dade/calibration.hpp:20-40."""
+    p_s: float
+    delta_d: int
+    checkpoints: list
+    epsilons: list
+
+    @staticmethod
+    def expected_checkpoints(dim: int, delta_d: int) -> list[int]:
+        return expected_checkpoints(dim, delta_d)
+
+    @staticmethod
+    def unbounded(dim: int, delta_d: int) -> "CalibrationTable":
+        cps = expected_checkpoints(dim, delta_d)
+        return CalibrationTable(0.0, delta_d, cps, [math.inf] * len(cps))
+
+    @staticmethod
+    def calibrate(dev: Device, t: OrthoTransform, transformed_data, p_s: float, delta_d: int,
+                  n_pairs: int, seed: int, device_ptr: bool = False, count: int | None = None):
+        """calibrate (proj/src/calibration.cpp:109-146), partial sums on the GPU.
+        With device_ptr, ``transformed_data`` is a CUDA tensor [count, dim]."""
+        t.upload(dev)
+        n = count if count is not None else int(transformed_data.shape[0])
+        data = transformed_data if device_ptr else _f32(transformed_data)
+        cps = np.zeros(max(1, t.dim // max(delta_d, 1) + 1), dtype=np.uint32)
+        eps = np.zeros(len(cps), dtype=np.float64)
+        nout = C.c_uint32()
+        check(_capi.lib.dade_gpu_calibrate(dev.h, ptr(data), n, float(p_s), delta_d, int(n_pairs),
+                                           int(seed), _capi.DEVICE_PTRS if device_ptr else 0,
+                                           ptr(cps), ptr(eps), C.byref(nout)))
+        m = nout.value
+        return CalibrationTable(float(p_s), delta_d, [int(x) for x in cps[:m]],
+                                [float(x) for x in eps[:m]])
+
+
+class _Strategy:
+    kind = _capi.FD
+    dim = 0
+
+    @property
+    def n_ckpt(self) -> int:
+        if isinstance(self, DadeStrategy):
+            return len(self.cal.checkpoints)
+        if isinstance(self, AdsamplingStrategy):
+            return len(expected_checkpoints(self.dim, self.delta_d))
+        return 0
+
+
+class FdScanningStrategy(_Strategy):
+    """proj/src/estimator.cpp:99-113: exact distance, prune iff > r."""
+    kind = _capi.FD
+
+    def __init__(self, dim: int):
+        self.dim = dim
+        self.checkpoints, self.reject_coeff, self.est_scale = [], [], []
+
+    def _apply(self, dev: Device):
+        check(_capi.lib.dade_gpu_set_strategy(dev.h, _capi.FD, self.dim, 0, None, None, None))
+
+
+class DadeStrategy(_Strategy):
+    """DadeStrategy(t, cal, delta_d) (proj/src/estimator.cpp:115-152); the
+    table derivation and its ConfigError checks run in the C ABI."""
+    kind = _capi.DADE
+
+    def __init__(self, t: OrthoTransform, cal: CalibrationTable, delta_d: int, dev: Device | None = None):
+        self.t, self.cal, self.delta_d, self.dim = t, cal, delta_d, t.dim
+        self._dev = dev or _default_device()
+        self._apply(self._dev)  # validate eagerly, like the reference ctor
+        self._dev._strategy_token = self
+
+    def _apply(self, dev: Device):
+        self.t.upload(dev)
+        cps = _u32(self.cal.checkpoints)
+        eps = _f64(self.cal.epsilons)
+        check(_capi.lib.dade_gpu_set_strategy_dade(dev.h, self.delta_d, self.cal.delta_d, len(cps),
+                                                   ptr(cps), ptr(eps)))
+
+
+class AdsamplingStrategy(_Strategy):
+    """proj/src/estimator.cpp:158-177."""
+    kind = _capi.ADS
+
+    def __init__(self, dim: int, delta_d: int, eps0: float, dev: Device | None = None):
+        self.dim, self.delta_d, self.eps0 = dim, delta_d, eps0
+        d = dev or _default_device()
+        self._apply(d)
+        d._strategy_token = self
+
+    def _apply(self, dev: Device):
+        check(_capi.lib.dade_gpu_set_strategy_ads(dev.h, self.dim, self.delta_d, float(self.eps0)))
+
+
+_DEFAULT = None
+
+
+def _default_device() -> Device:
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = Device(0)
+    return _DEFAULT
+
+
+@dataclass
+class DcoStats:
+    """proj/include/dade/estimator.hpp:24-49."""
+    total_dco: int = 0
+    dims_accumulated: int = 0
+    measure_failures: bool = False
+    eligible: int = 0
+    failures: int = 0
+
+    def _add(self, s: _capi.Stats):
+        self.total_dco += s.total_dco
+        self.dims_accumulated += s.dims_accumulated
+        self.eligible += s.eligible
+        self.failures += s.failures
+
+    def dim_fraction(self, dim: int) -> float:
+        return 0.0 if self.total_dco == 0 else self.dims_accumulated / (self.total_dco * dim)
+
+    def failure_rate(self) -> float:
+        return 0.0 if self.eligible == 0 else self.failures / self.eligible
+
+
+@dataclass
+class DcoOutcome:
+    pruned: bool
+    distance: float
+    distance_exact: bool
+    dims_used: int
+
+
+@dataclass(order=True)
+class Neighbor:
+    distance: float
+    id: int
+
+
+@dataclass
+class SearchResult:
+    neighbors: list = field(default_factory=list)
+    truncated: bool = False
+
+    def ids(self):
+        return [n.id for n in self.neighbors]
+
+
+def _results(ids, dists, counts, k):
+    out = []
+    for q in range(ids.shape[0]):
+        c = int(counts[q])
+        out.append(SearchResult([Neighbor(float(dists[q, i]), int(ids[q, i])) for i in range(c)], c < k))
+    return out
+
+
+def evaluate_batch(dev: Device, dco, o, q, r, stats: DcoStats | None = None):
+    """DcoStrategy::evaluate over n independent (o_i, q_i, r_i) on the GPU."""
+    dev.apply(dco)
+    o, q, r = _f32(o), _f32(q), _f32(np.atleast_1d(r))
+    n = r.shape[0]
+    pr = np.zeros(n, np.uint8)
+    di = np.zeros(n, np.float32)
+    ex = np.zeros(n, np.uint8)
+    du = np.zeros(n, np.uint32)
+    st = _capi.Stats()
+    check(_capi.lib.dade_gpu_dco_evaluate(dev.h, ptr(o), ptr(q), ptr(r), n, 0, ptr(pr), ptr(di),
+                                          ptr(ex), ptr(du), C.byref(st)))
+    if stats is not None:
+        stats.total_dco += st.total_dco
+        stats.dims_accumulated += st.dims_accumulated
+        if stats.measure_failures:
+            stats.eligible += st.eligible
+            stats.failures += st.failures
+    return pr.astype(bool), di, ex.astype(bool), du
+
+
+def partial_sums(dev: Device, dco, o, q) -> np.ndarray:
+    """Running partial squared distances at each checkpoint and at dim."""
+    dev.apply(dco)
+    o, q = _f32(o), _f32(q)
+    n = o.shape[0]
+    out = np.zeros((n, dco.n_ckpt + 1), np.float32)
+    check(_capi.lib.dade_gpu_partial_sums(dev.h, ptr(o), ptr(q), n, 0, ptr(out)))
+    return out
+
+
+class IvfIndex:
+    """Device-resident IVF index in the reference's DIVF field order
+    (proj/include/dade/ivf.hpp:62-70; proj/src/ivf.cpp:233-279)."""
+
+    def __init__(self, dev: Device, dim, count, n_clusters, centroids, offsets, ids, storage,
+                 layout: int = 0, split: int | None = None):
+        self.dev = dev
+        self._dim, self._count, self._nc = int(dim), int(count), int(n_clusters)
+        self.layout = layout
+        self.split = dim if split is None else split
+        self.offsets = _u32(offsets)
+        check(_capi.lib.dade_gpu_set_ivf(dev.h, self._dim, self._count, self._nc, layout, self.split,
+                                         ptr(_f32(centroids)), ptr(self.offsets), ptr(_u32(ids)),
+                                         ptr(_f32(storage))))
+
+    @staticmethod
+    def from_divf(dev: Device, divf) -> "IvfIndex":
+        return IvfIndex(dev, divf.dim, divf.count, divf.n_clusters, divf.centroids, divf.offsets,
+                        divf.ids, divf.storage, divf.layout, divf.split)
+
+    def dim(self):
+        return self._dim
+
+    def count(self):
+        return self._count
+
+    def n_clusters(self):
+        return self._nc
+
+    def shard(self, list_mask) -> None:
+        m = np.ascontiguousarray(list_mask, dtype=np.uint8)
+        check(_capi.lib.dade_gpu_set_ivf_shard(self.dev.h, ptr(m)))
+
+    def search_batch(self, queries, k: int, n_probe: int, dco, stats: DcoStats | None = None,
+                     raw: bool = False):
+        """Batched IvfIndex::search; returns (ids [nq,k], dists [nq,k], counts [nq])."""
+        q = _f32(queries)
+        if q.ndim == 1:
+            q = q[None, :]
+        if q.shape[1] != self._dim:
+            raise InvalidInput("IvfIndex::search: query dim mismatch")
+        if dco.dim != self._dim:
+            raise InvalidInput("IvfIndex::search: strategy dim mismatch")
+        self.dev.apply(dco)
+        nq = q.shape[0]
+        kk = max(k, 1)
+        ids = np.zeros((nq, kk), np.uint32)
+        dists = np.zeros((nq, kk), np.float32)
+        counts = np.zeros(nq, np.uint32)
+        st = _capi.Stats()
+        check(_capi.lib.dade_gpu_ivf_search(self.dev.h, ptr(q), nq, k, n_probe,
+                                            _capi.QUERIES_RAW if raw else 0, ptr(ids), ptr(dists),
+                                            ptr(counts), C.byref(st)))
+        if stats is not None:
+            stats._add(st)
+        return ids, dists, counts
+
+    def search(self, query, k: int, n_probe: int, dco, stats: DcoStats | None = None) -> SearchResult:
+        """IvfIndex::search (proj/src/ivf.cpp:207-231) for one rotated query."""
+        ids, dists, counts = self.search_batch(query, k, n_probe, dco, stats)
+        return _results(ids, dists, counts, k)[0]
+
+    def search_many(self, queries, k, n_probe, dco, stats=None):
+        ids, dists, counts = self.search_batch(queries, k, n_probe, dco, stats)
+        return _results(ids, dists, counts, k)
+
+
+class FlatIndex:
+    """Device-resident base rows for linear_scan (proj/src/knn.cpp:31-41)."""
+
+    def __init__(self, dev: Device, data, id_base: int = 0):
+        self.dev = dev
+        d = _f32(data)
+        if d.ndim != 2 or d.shape[1] == 0:
+            raise InvalidInput("VectorSet: dim must be positive")
+        self.dim, self.count = d.shape[1], d.shape[0]
+        check(_capi.lib.dade_gpu_set_base(dev.h, self.dim, self.count, ptr(d), id_base))
+
+    def search_batch(self, queries, k: int, dco, stats: DcoStats | None = None, raw: bool = False):
+        q = _f32(queries)
+        if q.ndim == 1:
+            q = q[None, :]
+        if dco.dim != self.dim:
+            raise InvalidInput("linear_scan: strategy dim mismatch")
+        self.dev.apply(dco)
+        nq = q.shape[0]
+        kk = max(k, 1)
+        ids = np.zeros((nq, kk), np.uint32)
+        dists = np.zeros((nq, kk), np.float32)
+        counts = np.zeros(nq, np.uint32)
+        st = _capi.Stats()
+        check(_capi.lib.dade_gpu_flat_search(self.dev.h, ptr(q), nq, k, _capi.QUERIES_RAW if raw else 0,
+                                             ptr(ids), ptr(dists), ptr(counts), C.byref(st)))
+        if stats is not None:
+            stats._add(st)
+        return ids, dists, counts
+
+
+def linear_scan(data_or_index, query, k: int, dco, stats: DcoStats | None = None,
+                dev: Device | None = None) -> SearchResult:
+    """linear_scan (proj/src/knn.cpp:31-41) for one query."""
+    if isinstance(data_or_index, FlatIndex):
+        fi = data_or_index
+    else:
+        fi = FlatIndex(dev or _default_device(), data_or_index)
+    ids, dists, counts = fi.search_batch(query, k, dco, stats)
+    return _results(ids, dists, counts, k)[0]

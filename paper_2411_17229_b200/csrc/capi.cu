@@ -1,0 +1,1005 @@
+// Host runtime + C ABI of libdade_gpu.so (include/dade_gpu.h).
+//
+// The handle owns every device buffer (grow-only workspaces, so steady-state
+// searches allocate nothing) and one CUDA stream. A search is a fixed,
+// host-sync-free launch sequence on that stream:
+//   [rotate] -> coarse scan (centroids, K = n_probe) -> segment merge ->
+//   group probes into per-list query buckets -> DCO scan -> segment merge
+// so it is capturable in a CUDA graph; the host only synchronises when it has
+// to copy results or counters back.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dade_gpu.h"
+#include "kernels.h"
+
+using namespace dade_gpu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct ApiError : std::runtime_error {
+    int code;
+    ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw ApiError(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(DADE_GPU_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return DADE_GPU_OK;
+    } catch (const ApiError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = std::string("host allocation failed: ") + e.what();
+        return DADE_GPU_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return DADE_GPU_RUNTIME_ERROR;
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* ensure(size_t bytes) {
+        if (bytes <= cap && p) return p;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 256);
+        cuda_check(cudaMalloc(&p, want), "cudaMalloc");
+        cap = want;
+        return p;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Checkpoint grid rule of CalibrationTable::expected_checkpoints
+// (proj/src/calibration.cpp:74-81).
+std::vector<uint32_t> expected_checkpoints(uint32_t dim, uint32_t delta_d) {
+    std::vector<uint32_t> cps;
+    for (uint64_t d = delta_d; d + 1 <= dim && d < dim; d += delta_d) cps.push_back((uint32_t)d);
+    return cps;
+}
+
+// Dimension chunks: boundaries at every checkpoint and every kCH dims.
+ChunkTable make_chunks(uint32_t dim, const std::vector<uint32_t>& cps) {
+    ChunkTable ct{};
+    ct.n_ckpt = (int)cps.size();
+    uint32_t k = 0;
+    size_t ci = 0;
+    int n = 0;
+    while (k < dim) {
+        uint32_t e = std::min(dim, k + (uint32_t)kCH);
+        int ck = -1;
+        if (ci < cps.size() && cps[ci] <= e) {
+            e = cps[ci];
+            ck = (int)ci;
+            ++ci;
+        }
+        if (n >= kMaxChunks) fail(DADE_GPU_INVALID_INPUT, "dimension too large for the chunk table");
+        ct.end[n] = (uint16_t)e;
+        ct.ckpt[n] = (int16_t)ck;
+        ++n;
+        k = e;
+    }
+    ct.n_chunks = n;
+    return ct;
+}
+
+}  // namespace
+
+struct dade_gpu_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+
+    // transform
+    uint32_t t_dim = 0;
+    DevBuf W;
+    std::vector<double> lambda_prefix;
+
+    // ivf
+    bool has_ivf = false;
+    uint32_t dim = 0, count = 0, n_clusters = 0;
+    DevBuf centroids, storage, ids, offsets;
+    std::vector<uint32_t> h_offsets;  // full index offsets (host)
+    std::vector<uint32_t> dev_offsets;
+
+    // flat base
+    bool has_base = false;
+    uint32_t b_dim = 0, b_count = 0, b_id_base = 0;
+    DevBuf base;
+
+    // strategy
+    bool has_strategy = false;
+    uint32_t s_kind = DADE_GPU_FD, s_dim = 0;
+    std::vector<uint32_t> cps;
+    std::vector<double> coeff, scale;
+    DevBuf d_cps, d_coeff, d_scale;
+
+    // workspaces
+    DevBuf q_in, q_rot, probes, probe_count, c_seg_keys, c_seg_count, c_r;
+    DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
+    DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts;
+    DevBuf counters;
+
+    // profiling
+    bool profiling = false;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+    double last_scan_ms = 0, last_bytes = 0, last_total_ms = 0;
+
+    void use_device() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
+};
+
+namespace {
+
+void upload(DevBuf& b, const void* src, size_t bytes, cudaStream_t s) {
+    b.ensure(bytes);
+    if (bytes) cuda_check(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, s), "H2D copy");
+}
+
+void require_strategy(const dade_gpu_ctx* c, uint32_t dim, const char* who) {
+    if (!c->has_strategy) fail(DADE_GPU_CONFIG_ERROR, std::string(who) + ": no strategy set");
+    if (c->s_dim != dim) fail(DADE_GPU_INVALID_INPUT, std::string(who) + ": strategy dim mismatch");
+}
+
+void set_tables(dade_gpu_ctx* c, uint32_t kind, uint32_t dim, std::vector<uint32_t> cps,
+                std::vector<double> coeff, std::vector<double> scale) {
+    if (dim == 0) fail(DADE_GPU_INVALID_INPUT, "strategy: dim must be positive");
+    for (size_t i = 0; i < cps.size(); ++i) {
+        if (cps[i] == 0 || cps[i] >= dim || (i && cps[i] <= cps[i - 1]))
+            fail(DADE_GPU_INVALID_INPUT, "strategy: checkpoints must ascend within [1, dim)");
+    }
+    c->s_kind = kind;
+    c->s_dim = dim;
+    c->cps = std::move(cps);
+    c->coeff = std::move(coeff);
+    c->scale = std::move(scale);
+    c->use_device();
+    upload(c->d_cps, c->cps.data(), c->cps.size() * 4, c->stream);
+    upload(c->d_coeff, c->coeff.data(), c->coeff.size() * 8, c->stream);
+    upload(c->d_scale, c->scale.data(), c->scale.size() * 8, c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "strategy upload");
+    c->has_strategy = true;
+}
+
+// Coarse ranking (K2): exact l2_sq to every centroid, K = n_probe smallest by
+// (dist^2, cluster id) (proj/src/ivf.cpp:215-219), as a flat FD scan in
+// squared-distance key space.
+void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_probe) {
+    cudaStream_t s = c->stream;
+    const uint32_t qchunks = (nq + kQC - 1) / kQC;
+    const uint32_t max_blocks = (c->n_clusters + kRT - 1) / kRT;
+    uint32_t nb = std::max<uint32_t>(1, std::min<uint32_t>(max_blocks, (1184 + qchunks - 1) / qchunks));
+    uint32_t block = (c->n_clusters + nb - 1) / nb;
+    block = (block + kRT - 1) / kRT * kRT;
+    nb = (c->n_clusters + block - 1) / block;
+    const size_t nseg = (size_t)nq * nb;
+    c->c_seg_keys.ensure(nseg * n_probe * 8);
+    c->c_seg_count.ensure(nseg * 4);
+    c->c_r.ensure((size_t)nq * 4);
+    c->probes.ensure((size_t)nq * n_probe * 8);
+    c->probe_count.ensure((size_t)nq * 4);
+    cuda_check(cudaMemsetAsync(c->c_seg_count.p, 0, nseg * 4, s), "memset");
+    cuda_check(launch_fill_u32(c->c_r.as<uint32_t>(), 0x7f800000u, nq, s), "fill");
+    ScanArgs a{};
+    a.storage = c->centroids.as<float>();
+    a.row_ids = nullptr;
+    a.id_base = 0;
+    a.dim = c->dim;
+    a.queries = d_q;
+    a.items = nullptr;
+    a.flat_rows = c->n_clusters;
+    a.flat_block = block;
+    a.flat_nq = nq;
+    a.flat_qchunks = qchunks;
+    a.r_global = c->c_r.as<uint32_t>();
+    a.seg_keys = c->c_seg_keys.as<uint64_t>();
+    a.seg_count = c->c_seg_count.as<uint32_t>();
+    a.n_slots = nb;
+    a.K = n_probe;
+    a.coeff = nullptr;
+    a.neg_zero2 = 0x8000000080000000ull;
+    a.counters = nullptr;
+    const ChunkTable ct = make_chunks(c->dim, {});
+    cuda_check(launch_scan(a, ct, nb * qchunks, /*sqrt_key=*/false, s), "coarse scan");
+    cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, nb, n_probe, c->probes.as<uint64_t>(),
+                                     c->probe_count.as<uint32_t>(), s),
+               "coarse merge");
+    c->launches += 3;
+}
+
+void record(dade_gpu_ctx* c, cudaEvent_t e) {
+    if (c->profiling) cuda_check(cudaEventRecord(e, c->stream), "event");
+}
+
+void finish_profile(dade_gpu_ctx* c) {
+    if (!c->profiling) return;
+    cuda_check(cudaEventSynchronize(c->e3), "event sync");
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, c->e1, c->e2), "elapsed");
+    c->last_scan_ms = ms;
+    cuda_check(cudaEventElapsedTime(&ms, c->e0, c->e3), "elapsed");
+    c->last_total_ms = ms;
+    unsigned long long h[3] = {0, 0, 0};
+    cuda_check(cudaMemcpy(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost), "D2H counters");
+    c->last_bytes = (double)h[2];
+}
+
+// Rotated device queries -> packed top-K keys [nq x k] + counts in
+// out_keys/out_count (device). Stats counters left in c->counters.
+void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint32_t n_probe,
+                       uint64_t* out_keys, uint32_t* out_count) {
+    cudaStream_t s = c->stream;
+    coarse_rank(c, d_q, nq, n_probe);
+    // K3 grouping
+    GroupArgs g{};
+    g.probes = c->probes.as<uint64_t>();
+    g.nq = nq;
+    g.n_probe = n_probe;
+    g.n_lists = c->n_clusters;
+    g.list_offsets = c->offsets.as<uint32_t>();
+    // rank buckets: nearest list first, then ranks 1-3, then the rest, so
+    // every query's radius is established before its far lists are scanned
+    uint32_t ends[3] = {1, 4, n_probe};
+    uint32_t nrb = 0;
+    for (uint32_t e : ends) {
+        const uint32_t v = std::min(e, n_probe);
+        if (nrb == 0 || v > g.rb_end[nrb - 1]) g.rb_end[nrb++] = v;
+    }
+    g.n_rb = nrb;
+    const size_t ne = (size_t)nrb * c->n_clusters;
+    const size_t max_items = ((size_t)nq * n_probe + kQC - 1) / kQC + ne;
+    c->g_counts.ensure(ne * 4);
+    c->g_cursor.ensure(ne * 4);
+    c->g_boff.ensure(ne * 4);
+    c->g_ioff.ensure(ne * 4);
+    c->bucket_q.ensure((size_t)nq * n_probe * 4);
+    c->bucket_slot.ensure((size_t)nq * n_probe * 4);
+    c->items.ensure(max_items * sizeof(WorkItem));
+    c->n_items.ensure(4);
+    g.counts = c->g_counts.as<uint32_t>();
+    g.cursor = c->g_cursor.as<uint32_t>();
+    g.bucket_off = c->g_boff.as<uint32_t>();
+    g.item_off = c->g_ioff.as<uint32_t>();
+    g.bucket_q = c->bucket_q.as<uint32_t>();
+    g.bucket_slot = c->bucket_slot.as<uint32_t>();
+    g.items = c->items.as<WorkItem>();
+    g.n_items = c->n_items.as<uint32_t>();
+    cuda_check(launch_group(g, s), "group");
+    c->launches += 4;
+    // K4 scan
+    const size_t nseg = (size_t)nq * n_probe;
+    c->seg_keys.ensure(nseg * k * 8);
+    c->seg_count.ensure(nseg * 4);
+    c->r_global.ensure((size_t)nq * 4);
+    cuda_check(cudaMemsetAsync(c->seg_count.p, 0, nseg * 4, s), "memset");
+    cuda_check(launch_fill_u32(c->r_global.as<uint32_t>(), 0x7f800000u, nq, s), "fill");
+    ScanArgs a{};
+    a.storage = c->storage.as<float>();
+    a.row_ids = c->ids.as<uint32_t>();
+    a.id_base = 0;
+    a.dim = c->dim;
+    a.queries = d_q;
+    a.items = g.items;
+    a.n_items = g.n_items;
+    a.bucket_q = g.bucket_q;
+    a.bucket_slot = g.bucket_slot;
+    a.r_global = c->r_global.as<uint32_t>();
+    a.seg_keys = c->seg_keys.as<uint64_t>();
+    a.seg_count = c->seg_count.as<uint32_t>();
+    a.n_slots = n_probe;
+    a.K = k;
+    a.coeff = c->d_coeff.as<double>();
+    a.neg_zero2 = 0x8000000080000000ull;
+    a.counters = c->counters.as<unsigned long long>();
+    const ChunkTable ct = make_chunks(c->dim, c->cps);
+    record(c, c->e1);
+    cuda_check(launch_scan(a, ct, (uint32_t)max_items, true, s), "dco scan");
+    record(c, c->e2);
+    cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, n_probe, k, out_keys, out_count, s),
+               "merge");
+    c->launches += 3;
+}
+
+void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint64_t* out_keys,
+                        uint32_t* out_count) {
+    cudaStream_t s = c->stream;
+    const uint32_t qchunks = (nq + kQC - 1) / kQC;
+    const uint32_t max_blocks = (c->b_count + kRT - 1) / kRT;
+    uint32_t nb = std::max<uint32_t>(1, std::min<uint32_t>(max_blocks, (1184 + qchunks - 1) / qchunks));
+    uint32_t block = (c->b_count + nb - 1) / nb;
+    block = (block + kRT - 1) / kRT * kRT;
+    nb = (c->b_count + block - 1) / block;
+    const size_t nseg = (size_t)nq * nb;
+    c->seg_keys.ensure(nseg * k * 8);
+    c->seg_count.ensure(nseg * 4);
+    c->r_global.ensure((size_t)nq * 4);
+    cuda_check(cudaMemsetAsync(c->seg_count.p, 0, nseg * 4, s), "memset");
+    cuda_check(launch_fill_u32(c->r_global.as<uint32_t>(), 0x7f800000u, nq, s), "fill");
+    ScanArgs a{};
+    a.storage = c->base.as<float>();
+    a.row_ids = nullptr;
+    a.id_base = c->b_id_base;
+    a.dim = c->b_dim;
+    a.queries = d_q;
+    a.items = nullptr;
+    a.flat_rows = c->b_count;
+    a.flat_block = block;
+    a.flat_nq = nq;
+    a.flat_qchunks = qchunks;
+    a.r_global = c->r_global.as<uint32_t>();
+    a.seg_keys = c->seg_keys.as<uint64_t>();
+    a.seg_count = c->seg_count.as<uint32_t>();
+    a.n_slots = nb;
+    a.K = k;
+    a.coeff = c->d_coeff.as<double>();
+    a.neg_zero2 = 0x8000000080000000ull;
+    a.counters = c->counters.as<unsigned long long>();
+    const ChunkTable ct = make_chunks(c->b_dim, c->cps);
+    record(c, c->e1);
+    cuda_check(launch_scan(a, ct, nb * qchunks, true, s), "flat scan");
+    record(c, c->e2);
+    cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, nb, k, out_keys, out_count, s), "merge");
+    c->launches += 3;
+}
+
+// Query staging shared by the two searches: H2D (host path) and rotation.
+const float* stage_queries(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t dim,
+                           uint32_t flags) {
+    const size_t bytes = (size_t)nq * dim * 4;
+    const float* d_in = queries;
+    if (!(flags & DADE_GPU_DEVICE_PTRS)) {
+        c->q_in.ensure(bytes);
+        cuda_check(cudaMemcpyAsync(c->q_in.p, queries, bytes, cudaMemcpyHostToDevice, c->stream), "H2D queries");
+        d_in = c->q_in.as<float>();
+    }
+    if (flags & DADE_GPU_QUERIES_RAW) {
+        if (c->t_dim != dim) fail(DADE_GPU_CONFIG_ERROR, "raw queries need a transform of the index dim");
+        c->q_rot.ensure(bytes);
+        cuda_check(launch_rotate(c->W.as<double>(), dim, d_in, nq, c->q_rot.as<float>(), c->stream), "rotate");
+        ++c->launches;
+        return c->q_rot.as<float>();
+    }
+    return d_in;
+}
+
+void collect_stats(dade_gpu_ctx* c, dade_gpu_stats* stats) {
+    if (!stats) return;
+    unsigned long long h[3] = {0, 0, 0};
+    cuda_check(cudaMemcpyAsync(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream), "D2H stats");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    stats->total_dco += h[0];
+    stats->dims_accumulated += h[1];
+}
+
+// Common driver: results as ids/dists/counts (host or device).
+void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t dim, uint32_t k,
+                   uint32_t flags, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
+                   dade_gpu_stats* stats, const std::function<void(const float*, uint64_t*, uint32_t*)>& run) {
+    c->use_device();
+    cudaStream_t s = c->stream;
+    c->counters.ensure(64);
+    cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
+    record(c, c->e0);
+    if (nq == 0) return;
+    const float* d_q = stage_queries(c, queries, nq, dim, flags);
+    c->out_keys.ensure((size_t)nq * k * 8);
+    c->out_count.ensure((size_t)nq * 4);
+    run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
+    const bool dev = flags & DADE_GPU_DEVICE_PTRS;
+    uint32_t* ids = out_ids;
+    float* dists = out_dists;
+    uint32_t* cnts = out_counts;
+    if (!dev) {
+        c->out_ids.ensure((size_t)nq * k * 4);
+        c->out_dists.ensure((size_t)nq * k * 4);
+        c->out_counts.ensure((size_t)nq * 4);
+        ids = c->out_ids.as<uint32_t>();
+        dists = c->out_dists.as<float>();
+        cnts = c->out_counts.as<uint32_t>();
+    }
+    cuda_check(launch_keys_to_results(c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), nq, k, ids,
+                                      dists, cnts, s),
+               "keys_to_results");
+    ++c->launches;
+    if (!dev) {
+        cuda_check(cudaMemcpyAsync(out_ids, ids, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, s), "D2H ids");
+        cuda_check(cudaMemcpyAsync(out_dists, dists, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, s), "D2H dists");
+        if (out_counts)
+            cuda_check(cudaMemcpyAsync(out_counts, cnts, (size_t)nq * 4, cudaMemcpyDeviceToHost, s), "D2H counts");
+    }
+    record(c, c->e3);
+    if (!dev) cuda_check(cudaStreamSynchronize(s), "search");
+    collect_stats(c, stats);
+    finish_profile(c);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dade_gpu_last_error(void) { return g_last_error.c_str(); }
+const char* dade_gpu_version(void) { return "dade_gpu 0.1 sm_100a"; }
+
+int dade_gpu_create(int device, dade_gpu_ctx** out) {
+    return guarded([&] {
+        if (!out) fail(DADE_GPU_INVALID_INPUT, "create: out is null");
+        int n = 0;
+        cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n) fail(DADE_GPU_INVALID_INPUT, "create: no such device");
+        auto* c = new dade_gpu_ctx;
+        c->device = device;
+        c->use_device();
+        cuda_check(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "stream");
+        c->stream = c->own_stream;
+        cuda_check(cudaEventCreate(&c->e0), "event");
+        cuda_check(cudaEventCreate(&c->e1), "event");
+        cuda_check(cudaEventCreate(&c->e2), "event");
+        cuda_check(cudaEventCreate(&c->e3), "event");
+        *out = c;
+    });
+}
+
+int dade_gpu_destroy(dade_gpu_ctx* c) {
+    return guarded([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        DevBuf* bufs[] = {&c->W, &c->centroids, &c->storage, &c->ids, &c->offsets, &c->base,
+                          &c->d_cps, &c->d_coeff, &c->d_scale, &c->q_in, &c->q_rot, &c->probes,
+                          &c->probe_count, &c->c_seg_keys, &c->c_seg_count, &c->c_r, &c->g_counts,
+                          &c->g_cursor, &c->g_boff, &c->g_ioff, &c->bucket_q, &c->bucket_slot,
+                          &c->items, &c->n_items, &c->seg_keys, &c->seg_count, &c->r_global,
+                          &c->out_keys, &c->out_count, &c->out_ids, &c->out_dists, &c->out_counts,
+                          &c->counters};
+        for (DevBuf* b : bufs) b->release();
+        cudaEventDestroy(c->e0);
+        cudaEventDestroy(c->e1);
+        cudaEventDestroy(c->e2);
+        cudaEventDestroy(c->e3);
+        cudaStreamDestroy(c->own_stream);
+        delete c;
+    });
+}
+
+int dade_gpu_set_stream(dade_gpu_ctx* c, void* stream) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    });
+}
+
+int dade_gpu_synchronize(dade_gpu_ctx* c) {
+    return guarded([&] {
+        c->use_device();
+        cuda_check(cudaStreamSynchronize(c->stream), "synchronize");
+    });
+}
+
+int dade_gpu_set_transform(dade_gpu_ctx* c, uint32_t dim, const double* matrix, const double* eig) {
+    return guarded([&] {
+        if (!c || !matrix || !eig) fail(DADE_GPU_INVALID_INPUT, "set_transform: null argument");
+        if (dim == 0) fail(DADE_GPU_INVALID_INPUT, "set_transform: dim must be positive");
+        // prefix sums of the clamped variances (transform.cpp:21-36)
+        std::vector<double> pre(dim + 1, 0.0);
+        for (uint32_t i = 0; i < dim; ++i) {
+            double v = eig[i];
+            if (v < -1e-6) fail(DADE_GPU_RUNTIME_ERROR, "eigenvalue below tolerance; not a covariance");
+            if (v < 0.0) v = 0.0;
+            pre[i + 1] = pre[i] + v;
+        }
+        c->use_device();
+        upload(c->W, matrix, (size_t)dim * dim * 8, c->stream);
+        cuda_check(cudaStreamSynchronize(c->stream), "transform upload");
+        c->t_dim = dim;
+        c->lambda_prefix = std::move(pre);
+    });
+}
+
+int dade_gpu_set_ivf(dade_gpu_ctx* c, uint32_t dim, uint32_t count, uint32_t n_clusters, uint32_t layout,
+                     uint32_t split, const float* centroids, const uint32_t* offsets, const uint32_t* ids,
+                     const float* storage) {
+    return guarded([&] {
+        if (!c || !centroids || !offsets || (count && (!ids || !storage)))
+            fail(DADE_GPU_INVALID_INPUT, "set_ivf: null argument");
+        if (dim == 0 || n_clusters == 0) fail(DADE_GPU_RUNTIME_ERROR, "inconsistent ivf header");
+        if (layout > 1) fail(DADE_GPU_RUNTIME_ERROR, "bad ivf layout byte");
+        if (layout == 1 && (split == 0 || split > dim)) fail(DADE_GPU_RUNTIME_ERROR, "inconsistent ivf header");
+        if (offsets[0] != 0 || offsets[n_clusters] != count)
+            fail(DADE_GPU_RUNTIME_ERROR, "inconsistent ivf posting offsets");
+        for (uint32_t i = 0; i < n_clusters; ++i)
+            if (offsets[i + 1] < offsets[i]) fail(DADE_GPU_RUNTIME_ERROR, "inconsistent ivf posting offsets");
+        c->use_device();
+        // Device layout = contiguous rows in posting order (ivf.cpp:195-205);
+        // a split payload is re-interleaved row by row on the host.
+        const float* rows = storage;
+        std::vector<float> tmp;
+        if (layout == 1 && split != dim) {
+            tmp.resize((size_t)count * dim);
+            for (uint32_t cl = 0; cl < n_clusters; ++cl) {
+                const uint32_t b = offsets[cl], len = offsets[cl + 1] - b;
+                const float* blk = storage + (size_t)b * dim;
+                for (uint32_t pos = 0; pos < len; ++pos) {
+                    float* dst = tmp.data() + (size_t)(b + pos) * dim;
+                    std::memcpy(dst, blk + (size_t)pos * split, sizeof(float) * split);
+                    std::memcpy(dst + split, blk + (size_t)len * split + (size_t)pos * (dim - split),
+                                sizeof(float) * (dim - split));
+                }
+            }
+            rows = tmp.data();
+        }
+        upload(c->centroids, centroids, (size_t)n_clusters * dim * 4, c->stream);
+        upload(c->storage, rows, (size_t)count * dim * 4, c->stream);
+        upload(c->ids, ids, (size_t)count * 4, c->stream);
+        upload(c->offsets, offsets, (size_t)(n_clusters + 1) * 4, c->stream);
+        cuda_check(cudaStreamSynchronize(c->stream), "ivf upload");
+        c->dim = dim;
+        c->count = count;
+        c->n_clusters = n_clusters;
+        c->h_offsets.assign(offsets, offsets + n_clusters + 1);
+        c->dev_offsets = c->h_offsets;
+        c->has_ivf = true;
+    });
+}
+
+int dade_gpu_set_ivf_shard(dade_gpu_ctx* c, const uint8_t* mask) {
+    return guarded([&] {
+        if (!c || !mask) fail(DADE_GPU_INVALID_INPUT, "set_ivf_shard: null argument");
+        if (!c->has_ivf) fail(DADE_GPU_CONFIG_ERROR, "set_ivf_shard: no ivf index");
+        c->use_device();
+        // Compact the kept lists' rows on the device, keep global offsets for
+        // removed lists at zero length.
+        const uint32_t nl = c->n_clusters;
+        std::vector<uint32_t> dev(nl + 1, 0);
+        size_t rows = 0;
+        for (uint32_t l = 0; l < nl; ++l) {
+            dev[l] = (uint32_t)rows;
+            if (mask[l]) rows += c->dev_offsets[l + 1] - c->dev_offsets[l];
+        }
+        dev[nl] = (uint32_t)rows;
+        DevBuf ns, ni;
+        ns.ensure(rows * c->dim * 4);
+        ni.ensure(rows * 4);
+        for (uint32_t l = 0; l < nl; ++l) {
+            if (!mask[l]) continue;
+            const uint32_t src = c->dev_offsets[l], len = c->dev_offsets[l + 1] - src;
+            if (!len) continue;
+            cuda_check(cudaMemcpyAsync(ns.as<float>() + (size_t)dev[l] * c->dim,
+                                       c->storage.as<float>() + (size_t)src * c->dim,
+                                       (size_t)len * c->dim * 4, cudaMemcpyDeviceToDevice, c->stream),
+                       "shard copy");
+            cuda_check(cudaMemcpyAsync(ni.as<uint32_t>() + dev[l], c->ids.as<uint32_t>() + src, (size_t)len * 4,
+                                       cudaMemcpyDeviceToDevice, c->stream),
+                       "shard copy");
+        }
+        cuda_check(cudaStreamSynchronize(c->stream), "shard");
+        c->storage.release();
+        c->ids.release();
+        c->storage = ns;
+        c->ids = ni;
+        ns.p = nullptr;
+        ni.p = nullptr;
+        upload(c->offsets, dev.data(), (size_t)(nl + 1) * 4, c->stream);
+        cuda_check(cudaStreamSynchronize(c->stream), "shard");
+        c->dev_offsets = dev;
+        c->count = (uint32_t)rows;
+    });
+}
+
+int dade_gpu_set_base(dade_gpu_ctx* c, uint32_t dim, uint32_t count, const float* data, uint32_t id_base) {
+    return guarded([&] {
+        if (!c || (count && !data)) fail(DADE_GPU_INVALID_INPUT, "set_base: null argument");
+        if (dim == 0) fail(DADE_GPU_INVALID_INPUT, "VectorSet: dim must be positive");
+        c->use_device();
+        upload(c->base, data, (size_t)count * dim * 4, c->stream);
+        cuda_check(cudaStreamSynchronize(c->stream), "base upload");
+        c->b_dim = dim;
+        c->b_count = count;
+        c->b_id_base = id_base;
+        c->has_base = true;
+    });
+}
+
+int dade_gpu_set_strategy(dade_gpu_ctx* c, uint32_t kind, uint32_t dim, uint32_t n, const uint32_t* cps,
+                          const double* coeff, const double* scale) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (kind > DADE_GPU_DADE) fail(DADE_GPU_INVALID_INPUT, "unknown strategy kind");
+        if (kind == DADE_GPU_FD) n = 0;
+        if (n && (!cps || !coeff || !scale)) fail(DADE_GPU_INVALID_INPUT, "set_strategy: null tables");
+        set_tables(c, kind, dim, std::vector<uint32_t>(cps, cps + n), std::vector<double>(coeff, coeff + n),
+                   std::vector<double>(scale, scale + n));
+    });
+}
+
+// DadeStrategy::DadeStrategy (proj/src/estimator.cpp:115-152).
+int dade_gpu_set_strategy_dade(dade_gpu_ctx* c, uint32_t delta_d, uint32_t cal_delta_d, uint32_t n,
+                               const uint32_t* cal_cps, const double* cal_eps) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (c->t_dim == 0) fail(DADE_GPU_CONFIG_ERROR, "DadeStrategy: no transform set");
+        const uint32_t dim = c->t_dim;
+        if (delta_d == 0) fail(DADE_GPU_INVALID_INPUT, "DadeStrategy: delta_d must be positive");
+        if (cal_delta_d != delta_d)
+            fail(DADE_GPU_CONFIG_ERROR, "calibration step " + std::to_string(cal_delta_d) +
+                                            " does not match requested step " + std::to_string(delta_d));
+        const auto expected = expected_checkpoints(dim, delta_d);
+        std::vector<uint32_t> have(cal_cps, cal_cps + n);
+        if (have != expected) {
+            std::string msg = "calibration table does not cover checkpoints for dim " + std::to_string(dim) +
+                              " step " + std::to_string(delta_d);
+            for (uint32_t d : expected)
+                if (std::find(have.begin(), have.end(), d) == have.end()) {
+                    msg += "; first missing checkpoint " + std::to_string(d);
+                    break;
+                }
+            fail(DADE_GPU_CONFIG_ERROR, msg);
+        }
+        const auto& pre = c->lambda_prefix;
+        std::vector<double> coeff(n), scale(n);
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t d = have[i];
+            const double ope = 1.0 + cal_eps[i];
+            if (!(pre[d] > 0.0)) {
+                coeff[i] = std::numeric_limits<double>::infinity();
+                scale[i] = 1.0;
+            } else {
+                const double s = pre[dim] / pre[d];
+                coeff[i] = ope * ope / s;
+                scale[i] = s;
+            }
+        }
+        set_tables(c, DADE_GPU_DADE, dim, have, coeff, scale);
+    });
+}
+
+// AdsamplingStrategy::AdsamplingStrategy (proj/src/estimator.cpp:158-172).
+int dade_gpu_set_strategy_ads(dade_gpu_ctx* c, uint32_t dim, uint32_t delta_d, double eps0) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (dim == 0) fail(DADE_GPU_INVALID_INPUT, "AdsamplingStrategy: dim must be positive");
+        if (delta_d == 0) fail(DADE_GPU_INVALID_INPUT, "AdsamplingStrategy: delta_d must be positive");
+        if (eps0 < 0.0) fail(DADE_GPU_INVALID_INPUT, "AdsamplingStrategy: eps0 must be nonnegative");
+        const auto cps = expected_checkpoints(dim, delta_d);
+        std::vector<double> coeff(cps.size()), scale(cps.size());
+        for (size_t i = 0; i < cps.size(); ++i) {
+            const double d = cps[i];
+            const double ope = 1.0 + eps0 / std::sqrt(d);
+            coeff[i] = d / dim * ope * ope;
+            scale[i] = dim / d;
+        }
+        set_tables(c, DADE_GPU_ADS, dim, cps, coeff, scale);
+    });
+}
+
+int dade_gpu_rotate(dade_gpu_ctx* c, const float* in, uint32_t n, float* out, uint32_t flags) {
+    return guarded([&] {
+        if (!c || (n && (!in || !out))) fail(DADE_GPU_INVALID_INPUT, "rotate: null argument");
+        if (c->t_dim == 0) fail(DADE_GPU_CONFIG_ERROR, "rotate: no transform set");
+        c->use_device();
+        const size_t bytes = (size_t)n * c->t_dim * 4;
+        if (flags & DADE_GPU_DEVICE_PTRS) {
+            cuda_check(launch_rotate(c->W.as<double>(), c->t_dim, in, n, out, c->stream), "rotate");
+            ++c->launches;
+            return;
+        }
+        c->q_in.ensure(bytes);
+        c->q_rot.ensure(bytes);
+        cuda_check(cudaMemcpyAsync(c->q_in.p, in, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+        cuda_check(launch_rotate(c->W.as<double>(), c->t_dim, c->q_in.as<float>(), n, c->q_rot.as<float>(), c->stream),
+                   "rotate");
+        ++c->launches;
+        cuda_check(cudaMemcpyAsync(out, c->q_rot.p, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(c->stream), "rotate");
+    });
+}
+
+// IvfIndex::search argument checks (proj/src/ivf.cpp:209-213).
+static void check_ivf_args(dade_gpu_ctx* c, uint32_t k, uint32_t n_probe) {
+    if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+    if (!c->has_ivf) fail(DADE_GPU_CONFIG_ERROR, "IvfIndex::search: no ivf index uploaded");
+    if (k == 0) fail(DADE_GPU_INVALID_INPUT, "IvfIndex::search: k must be positive");
+    if (n_probe == 0 || n_probe > c->n_clusters)
+        fail(DADE_GPU_INVALID_INPUT,
+             "IvfIndex::search: n_probe must be in [1, n_clusters], got " + std::to_string(n_probe));
+    require_strategy(c, c->dim, "IvfIndex::search");
+}
+
+static void check_flat_args(dade_gpu_ctx* c, uint32_t k) {
+    if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+    if (!c->has_base) fail(DADE_GPU_CONFIG_ERROR, "linear_scan: no base vectors uploaded");
+    if (k == 0) fail(DADE_GPU_INVALID_INPUT, "linear_scan: k must be positive");
+    require_strategy(c, c->b_dim, "linear_scan");
+}
+
+int dade_gpu_ivf_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint32_t n_probe,
+                        uint32_t flags, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
+                        dade_gpu_stats* stats) {
+    return guarded([&] {
+        check_ivf_args(c, k, n_probe);
+        if (nq && (!queries || !out_ids || !out_dists)) fail(DADE_GPU_INVALID_INPUT, "ivf_search: null argument");
+        search_common(c, queries, nq, c->dim, k, flags, out_ids, out_dists, out_counts, stats,
+                      [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
+                          ivf_search_device(c, d_q, nq, k, n_probe, ok, oc);
+                      });
+    });
+}
+
+int dade_gpu_flat_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t k, uint32_t flags,
+                         uint32_t* out_ids, float* out_dists, uint32_t* out_counts, dade_gpu_stats* stats) {
+    return guarded([&] {
+        check_flat_args(c, k);
+        if (nq && (!queries || !out_ids || !out_dists)) fail(DADE_GPU_INVALID_INPUT, "flat_search: null argument");
+        search_common(c, queries, nq, c->b_dim, k, flags, out_ids, out_dists, out_counts, stats,
+                      [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
+                          flat_search_device(c, d_q, nq, k, ok, oc);
+                      });
+    });
+}
+
+int dade_gpu_ivf_search_keys(dade_gpu_ctx* c, const float* d_queries, uint32_t nq, uint32_t k, uint32_t n_probe,
+                             uint32_t flags, uint64_t* d_out_keys, dade_gpu_stats* stats) {
+    return guarded([&] {
+        check_ivf_args(c, k, n_probe);
+        c->use_device();
+        c->counters.ensure(64);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+        if (nq == 0) return;
+        const float* d_q = stage_queries(c, d_queries, nq, c->dim, flags | DADE_GPU_DEVICE_PTRS);
+        c->out_count.ensure((size_t)nq * 4);
+        ivf_search_device(c, d_q, nq, k, n_probe, d_out_keys, c->out_count.as<uint32_t>());
+        collect_stats(c, stats);
+    });
+}
+
+int dade_gpu_flat_search_keys(dade_gpu_ctx* c, const float* d_queries, uint32_t nq, uint32_t k, uint32_t flags,
+                              uint64_t* d_out_keys, dade_gpu_stats* stats) {
+    return guarded([&] {
+        check_flat_args(c, k);
+        c->use_device();
+        c->counters.ensure(64);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+        if (nq == 0) return;
+        const float* d_q = stage_queries(c, d_queries, nq, c->b_dim, flags | DADE_GPU_DEVICE_PTRS);
+        c->out_count.ensure((size_t)nq * 4);
+        flat_search_device(c, d_q, nq, k, d_out_keys, c->out_count.as<uint32_t>());
+        collect_stats(c, stats);
+    });
+}
+
+int dade_gpu_merge_keys(dade_gpu_ctx* c, const uint64_t* d_keys, uint32_t G, uint32_t nq, uint32_t k,
+                        uint32_t* d_ids, float* d_dists, uint32_t* d_counts) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (k == 0) fail(DADE_GPU_INVALID_INPUT, "merge_keys: k must be positive");
+        c->use_device();
+        c->out_keys.ensure((size_t)nq * k * 8);
+        c->out_count.ensure((size_t)nq * 4);
+        cuda_check(launch_merge_blocks(d_keys, G, nq, k, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(),
+                                       c->stream),
+                   "merge_blocks");
+        cuda_check(launch_keys_to_results(c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), nq, k, d_ids,
+                                          d_dists, d_counts, c->stream),
+                   "keys_to_results");
+        c->launches += 2;
+    });
+}
+
+int dade_gpu_dco_evaluate(dade_gpu_ctx* c, const float* o, const float* q, const float* r, uint32_t n,
+                          uint32_t flags, uint8_t* pruned, float* distance, uint8_t* exact, uint32_t* dims_used,
+                          dade_gpu_stats* stats) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (!c->has_strategy) fail(DADE_GPU_CONFIG_ERROR, "evaluate: no strategy set");
+        c->use_device();
+        const uint32_t dim = c->s_dim;
+        cudaStream_t s = c->stream;
+        c->counters.ensure(64);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
+        if (n == 0) return;
+        const bool dev = flags & DADE_GPU_DEVICE_PTRS;
+        const size_t vb = (size_t)n * dim * 4;
+        const float *d_o = o, *d_q = q, *d_r = r;
+        uint8_t *d_p = pruned, *d_e = exact;
+        float* d_d = distance;
+        uint32_t* d_u = dims_used;
+        DevBuf bo, bq, br, bp, bd, be, bu;
+        if (!dev) {
+            upload(bo, o, vb, s);
+            upload(bq, q, vb, s);
+            upload(br, r, (size_t)n * 4, s);
+            d_o = bo.as<float>();
+            d_q = bq.as<float>();
+            d_r = br.as<float>();
+            d_p = static_cast<uint8_t*>(bp.ensure(n));
+            d_d = static_cast<float*>(bd.ensure((size_t)n * 4));
+            d_e = static_cast<uint8_t*>(be.ensure(n));
+            d_u = static_cast<uint32_t*>(bu.ensure((size_t)n * 4));
+        }
+        cuda_check(launch_evaluate(d_o, d_q, d_r, n, dim, c->d_cps.as<uint32_t>(), c->d_coeff.as<double>(),
+                                   c->d_scale.as<double>(), (uint32_t)c->cps.size(), d_p, d_d, d_e, d_u,
+                                   c->counters.as<unsigned long long>(), s),
+                   "evaluate");
+        ++c->launches;
+        if (!dev) {
+            cuda_check(cudaMemcpyAsync(pruned, d_p, n, cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_check(cudaMemcpyAsync(distance, d_d, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_check(cudaMemcpyAsync(exact, d_e, n, cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_check(cudaMemcpyAsync(dims_used, d_u, (size_t)n * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        }
+        unsigned long long h[4] = {0, 0, 0, 0};
+        cuda_check(cudaMemcpyAsync(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaStreamSynchronize(s), "evaluate");
+        if (stats) {
+            stats->total_dco += h[0];
+            stats->dims_accumulated += h[1];
+            stats->eligible += h[2];
+            stats->failures += h[3];
+        }
+        for (DevBuf* b : {&bo, &bq, &br, &bp, &bd, &be, &bu}) b->release();
+    });
+}
+
+int dade_gpu_partial_sums(dade_gpu_ctx* c, const float* o, const float* q, uint32_t n, uint32_t flags, float* out) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (!c->has_strategy) fail(DADE_GPU_CONFIG_ERROR, "partial_sums: no strategy set");
+        c->use_device();
+        if (n == 0) return;
+        const uint32_t dim = c->s_dim, nc = (uint32_t)c->cps.size();
+        cudaStream_t s = c->stream;
+        const size_t ob = (size_t)n * (nc + 1) * 4;
+        if (flags & DADE_GPU_DEVICE_PTRS) {
+            cuda_check(launch_partial_sums(o, q, n, dim, c->d_cps.as<uint32_t>(), nc, out, s), "partial_sums");
+            ++c->launches;
+            return;
+        }
+        DevBuf bo, bq, bout;
+        upload(bo, o, (size_t)n * dim * 4, s);
+        upload(bq, q, (size_t)n * dim * 4, s);
+        bout.ensure(ob);
+        cuda_check(launch_partial_sums(bo.as<float>(), bq.as<float>(), n, dim, c->d_cps.as<uint32_t>(), nc,
+                                       bout.as<float>(), s),
+                   "partial_sums");
+        ++c->launches;
+        cuda_check(cudaMemcpyAsync(out, bout.p, ob, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaStreamSynchronize(s), "partial_sums");
+        bo.release();
+        bq.release();
+        bout.release();
+    });
+}
+
+// calibrate (proj/src/calibration.cpp:92-146): pairs drawn on the host with
+// the reference's generator and rejection sampler (std::mt19937_64 +
+// rng::bounded, proj/include/dade/rng.hpp:20-25), running partial sums on the
+// GPU (bit-exact), ratios / order statistic / running min on the host.
+int dade_gpu_calibrate(dade_gpu_ctx* c, const float* data, uint32_t n, double p_s, uint32_t delta_d,
+                       uint64_t n_pairs, uint64_t seed, uint32_t flags, uint32_t* out_cps, double* out_eps,
+                       uint32_t* n_out) {
+    return guarded([&] {
+        if (!c || !data || !n_out) fail(DADE_GPU_INVALID_INPUT, "calibrate: null argument");
+        if (!(p_s > 0.0 && p_s < 1.0)) fail(DADE_GPU_INVALID_INPUT, "calibrate: p_s must be in (0, 1)");
+        if (n_pairs == 0) fail(DADE_GPU_INVALID_INPUT, "calibrate: n_pairs must be positive");
+        if (c->t_dim == 0) fail(DADE_GPU_CONFIG_ERROR, "calibrate: no transform set");
+        if (delta_d == 0) fail(DADE_GPU_INVALID_INPUT, "delta_d must be positive");
+        if (n < 2) fail(DADE_GPU_INVALID_INPUT, "sample_pairs: need at least 2 vectors");
+        const uint32_t dim = c->t_dim;
+        c->use_device();
+        cudaStream_t s = c->stream;
+        std::mt19937_64 gen(seed);
+        auto bounded = [&](uint64_t m) {
+            const uint64_t limit = (0 - m) % m;
+            uint64_t r = gen();
+            while (r < limit) r = gen();
+            return r % m;
+        };
+        std::vector<uint32_t> pi(n_pairs), pj(n_pairs);
+        for (uint64_t p = 0; p < n_pairs; ++p) {
+            const uint32_t i = (uint32_t)bounded(n);
+            uint32_t j = (uint32_t)bounded(n - 1);
+            if (j >= i) ++j;
+            pi[p] = i;
+            pj[p] = j;
+        }
+        const auto cps = expected_checkpoints(dim, delta_d);
+        const uint32_t nc = (uint32_t)cps.size();
+        DevBuf bdata, bpi, bpj, bcps, bout;
+        const float* d_data = data;
+        if (!(flags & DADE_GPU_DEVICE_PTRS)) {
+            upload(bdata, data, (size_t)n * dim * 4, s);
+            d_data = bdata.as<float>();
+        }
+        upload(bpi, pi.data(), n_pairs * 4, s);
+        upload(bpj, pj.data(), n_pairs * 4, s);
+        upload(bcps, cps.data(), cps.size() * 4, s);
+        bout.ensure(n_pairs * (nc + 1) * 4);
+        cuda_check(launch_pair_partials(d_data, dim, bpi.as<uint32_t>(), bpj.as<uint32_t>(), n_pairs,
+                                        bcps.as<uint32_t>(), nc, bout.as<float>(), s),
+                   "pair_partials");
+        ++c->launches;
+        std::vector<float> part(n_pairs * (nc + 1));
+        cuda_check(cudaMemcpyAsync(part.data(), bout.p, part.size() * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaStreamSynchronize(s), "calibrate");
+        for (DevBuf* b : {&bdata, &bpi, &bpj, &bcps, &bout}) b->release();
+        const auto& pre = c->lambda_prefix;
+        std::vector<double> scale(nc);
+        for (uint32_t ci = 0; ci < nc; ++ci) scale[ci] = pre[cps[ci]] <= 0.0 ? 1.0 : pre[dim] / pre[cps[ci]];
+        std::vector<std::vector<double>> ratios(nc);
+        for (auto& r : ratios) r.reserve(n_pairs);
+        uint64_t skipped = 0;
+        for (uint64_t p = 0; p < n_pairs; ++p) {
+            const float* row = part.data() + p * (nc + 1);
+            const float acc = row[nc];
+            if (acc == 0.0f) {
+                ++skipped;
+                continue;
+            }
+            const double dis = std::sqrt(static_cast<double>(acc));
+            for (uint32_t ci = 0; ci < nc; ++ci)
+                ratios[ci].push_back(std::sqrt(scale[ci] * static_cast<double>(row[ci])) / dis - 1.0);
+        }
+        const uint64_t kept = n_pairs - skipped;
+        if (nc > 0) {
+            if (skipped * 2 > n_pairs)
+                fail(DADE_GPU_RUNTIME_ERROR,
+                     "calibrate: over half the sampled pairs are at zero distance; data is too degenerate to calibrate");
+            if (kept == 0) fail(DADE_GPU_RUNTIME_ERROR, "calibrate: no usable pairs");
+            const auto rank = static_cast<uint64_t>(std::ceil((1.0 - p_s) * static_cast<double>(kept)));
+            for (uint32_t ci = 0; ci < nc; ++ci) {
+                auto& r = ratios[ci];
+                std::sort(r.begin(), r.end());
+                out_eps[ci] = r[rank - 1];
+            }
+            for (uint32_t ci = 1; ci < nc; ++ci) out_eps[ci] = std::min(out_eps[ci], out_eps[ci - 1]);
+        }
+        for (uint32_t ci = 0; ci < nc; ++ci) out_cps[ci] = cps[ci];
+        *n_out = nc;
+    });
+}
+
+uint64_t dade_gpu_launch_count(dade_gpu_ctx* c) { return c ? c->launches : 0; }
+
+int dade_gpu_set_profiling(dade_gpu_ctx* c, int on) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        c->profiling = on != 0;
+    });
+}
+
+int dade_gpu_last_scan_profile(dade_gpu_ctx* c, double* scan_ms, double* scan_bytes, double* total_ms) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (scan_ms) *scan_ms = c->last_scan_ms;
+        if (scan_bytes) *scan_bytes = c->last_bytes;
+        if (total_ms) *total_ms = c->last_total_ms;
+    });
+}
+
+}  // extern "C"

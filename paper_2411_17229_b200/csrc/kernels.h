@@ -1,0 +1,81 @@
+// Host-visible launchers of the sm_100a kernels (internal to libdade_gpu.so).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace dade_gpu {
+
+struct ScanArgs {
+    const float* storage;    // device rows [*, dim], contiguous
+    const uint32_t* row_ids; // nullable: ids = id_base + row
+    uint32_t id_base;
+    uint32_t dim;
+    const float* queries;    // rotated [nq, dim]
+    // explicit work items (IVF) ...
+    const WorkItem* items;
+    const uint32_t* n_items;
+    const uint32_t* bucket_q;
+    const uint32_t* bucket_slot;
+    // ... or an implicit (row block x query chunk) grid (flat scans)
+    uint32_t flat_rows, flat_block, flat_nq, flat_qchunks;
+    uint32_t* r_global;      // [nq] radius as float bits (key space)
+    uint64_t* seg_keys;      // [nq * n_slots * K]
+    uint32_t* seg_count;     // [nq * n_slots]
+    uint32_t n_slots;
+    uint32_t K;
+    const double* coeff;     // [n_ckpt] reject coefficients
+    uint64_t neg_zero2;      // 0x8000000080000000 (opaque to ptxas)
+    unsigned long long* counters;  // [3] total_dco, dims_accumulated, bytes
+};
+
+size_t scan_smem_bytes(int n_ckpt);
+cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, uint32_t grid, bool sqrt_key,
+                        cudaStream_t s);
+cudaError_t launch_merge_segments(const uint64_t* seg_keys, const uint32_t* seg_count, uint32_t nq,
+                                  uint32_t n_slots, uint32_t K, uint64_t* out_keys,
+                                  uint32_t* out_count, cudaStream_t s);
+cudaError_t launch_merge_blocks(const uint64_t* keys, uint32_t G, uint32_t nq, uint32_t K,
+                                uint64_t* out_keys, uint32_t* out_count, cudaStream_t s);
+cudaError_t launch_keys_to_results(const uint64_t* keys, const uint32_t* count, uint32_t nq,
+                                   uint32_t K, uint32_t* ids, float* dists, uint32_t* counts_out,
+                                   cudaStream_t s);
+
+// prep.cu
+cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s);
+cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
+                          cudaStream_t s);
+// Probe grouping (K3): probe keys [nq x nprobe] (low 32 bits = list id) ->
+// per (rank bucket, list) query buckets and work items, ordered by rank bucket.
+struct GroupArgs {
+    const uint64_t* probes;
+    uint32_t nq, n_probe, n_lists;
+    const uint32_t* list_offsets;   // [n_lists + 1] device row prefix sums (a list absent
+                                    // from this shard has zero length)
+    uint32_t n_rb;                  // rank buckets
+    uint32_t rb_end[8];             // exclusive probe-rank bound of each bucket
+    uint32_t* counts;               // [n_rb * n_lists]
+    uint32_t* cursor;               // [n_rb * n_lists]
+    uint32_t* bucket_off;           // [n_rb * n_lists]
+    uint32_t* item_off;             // [n_rb * n_lists]
+    uint32_t* bucket_q;             // [nq * n_probe]
+    uint32_t* bucket_slot;          // [nq * n_probe]
+    WorkItem* items;                // [max_items]
+    uint32_t* n_items;              // [1]
+};
+cudaError_t launch_group(const GroupArgs& g, cudaStream_t s);
+
+cudaError_t launch_evaluate(const float* o, const float* q, const float* r, uint32_t n, uint32_t dim,
+                            const uint32_t* cps, const double* coeff, const double* scale,
+                            uint32_t n_ckpt, uint8_t* pruned, float* dist, uint8_t* exact,
+                            uint32_t* dims_used, unsigned long long* counters, cudaStream_t s);
+cudaError_t launch_partial_sums(const float* o, const float* q, uint32_t n, uint32_t dim,
+                                const uint32_t* cps, uint32_t n_ckpt, float* out, cudaStream_t s);
+cudaError_t launch_pair_partials(const float* data, uint32_t dim, const uint32_t* pi,
+                                 const uint32_t* pj, uint64_t n, const uint32_t* cps,
+                                 uint32_t n_ckpt, float* out, cudaStream_t s);
+
+}  // namespace dade_gpu

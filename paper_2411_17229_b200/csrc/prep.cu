@@ -1,0 +1,285 @@
+// Query rotation (K1), probe grouping (K3) and the per-pair DCO kernels that
+// mirror DcoStrategy::evaluate / partial_sqdist / calibration's ratio walk.
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dade_gpu {
+
+namespace {
+
+// ---- K1: out[i][k] = (float) sum_r W[k*D + r] * in[i][r] --------------------
+// f64 accumulation in r order with separately rounded DMUL/DADD, exactly
+// OrthoTransform::transform_vector (proj/src/transform.cpp:221-228).
+constexpr int kRotTile = 32;  // outputs (cols) and rows per CTA
+constexpr int kRotK = 32;     // r chunk
+
+__global__ void __launch_bounds__(256)
+rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in, uint32_t n,
+              float* __restrict__ out) {
+    __shared__ double ws[kRotTile][kRotK + 1];
+    __shared__ double xs[kRotTile][kRotK + 1];
+    const int tx = threadIdx.x & 31;  // output column within tile
+    const int ty = threadIdx.x >> 5;  // 0..7 -> rows ty*4 .. ty*4+3
+    const uint32_t col0 = blockIdx.x * kRotTile;
+    const uint32_t row0 = blockIdx.y * kRotTile;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (uint32_t r0 = 0; r0 < dim; r0 += kRotK) {
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < kRotTile * kRotK; idx += 256) {
+            const int a = idx / kRotK, b = idx % kRotK;
+            const uint32_t col = col0 + a, r = r0 + b;
+            ws[a][b] = (col < dim && r < dim) ? W[(size_t)col * dim + r] : 0.0;
+            const uint32_t row = row0 + a;
+            xs[a][b] = (row < n && r < dim) ? (double)in[(size_t)row * dim + r] : 0.0;
+        }
+        __syncthreads();
+        const int kmax = (int)min((uint32_t)kRotK, dim - r0);
+        for (int b = 0; b < kmax; ++b) {
+            const double w = ws[tx][b];
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) acc[ii] = __dadd_rn(acc[ii], __dmul_rn(w, xs[ty * 4 + ii][b]));
+        }
+    }
+    const uint32_t col = col0 + tx;
+    if (col < dim) {
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+            const uint32_t row = row0 + ty * 4 + ii;
+            if (row < n) out[(size_t)row * dim + col] = __double2float_rn(acc[ii]);
+        }
+    }
+}
+
+// ---- K3: grouping ------------------------------------------------------------
+__device__ __forceinline__ uint32_t rank_bucket(const GroupArgs& g, uint32_t p) {
+    uint32_t b = 0;
+    while (b + 1 < g.n_rb && p >= g.rb_end[b]) ++b;
+    return b;
+}
+
+__global__ void group_count_kernel(const GroupArgs g) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)g.nq * g.n_probe) return;
+    const uint32_t p = (uint32_t)(i % g.n_probe);
+    const uint32_t list = (uint32_t)g.probes[i];
+    if (list >= g.n_lists) return;
+    if (g.list_offsets[list + 1] == g.list_offsets[list]) return;  // empty / not on this shard
+    atomicAdd(&g.counts[rank_bucket(g, p) * g.n_lists + list], 1u);
+}
+
+// Single-CTA exclusive scans of the bucket sizes and item counts.
+__global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
+    __shared__ uint32_t s_b[1024], s_i[1024];
+    const uint32_t n = g.n_rb * g.n_lists;
+    const uint32_t per = (n + 1023) / 1024;
+    const uint32_t lo = threadIdx.x * per, hi = min(n, lo + per);
+    uint32_t sb = 0, si = 0;
+    for (uint32_t e = lo; e < hi; ++e) {
+        const uint32_t c = g.counts[e];
+        sb += c;
+        si += (c + kQC - 1) / kQC;
+    }
+    s_b[threadIdx.x] = sb;
+    s_i[threadIdx.x] = si;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const uint32_t vb = threadIdx.x >= (unsigned)off ? s_b[threadIdx.x - off] : 0;
+        const uint32_t vi = threadIdx.x >= (unsigned)off ? s_i[threadIdx.x - off] : 0;
+        __syncthreads();
+        s_b[threadIdx.x] += vb;
+        s_i[threadIdx.x] += vi;
+        __syncthreads();
+    }
+    uint32_t rb = s_b[threadIdx.x] - sb, ri = s_i[threadIdx.x] - si;
+    for (uint32_t e = lo; e < hi; ++e) {
+        const uint32_t c = g.counts[e];
+        g.bucket_off[e] = rb;
+        g.item_off[e] = ri;
+        rb += c;
+        ri += (c + kQC - 1) / kQC;
+    }
+    if (threadIdx.x == 1023) *g.n_items = s_i[1023];
+}
+
+__global__ void group_scatter_kernel(const GroupArgs g) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)g.nq * g.n_probe) return;
+    const uint32_t q = (uint32_t)(i / g.n_probe), p = (uint32_t)(i % g.n_probe);
+    const uint32_t list = (uint32_t)g.probes[i];
+    if (list >= g.n_lists) return;
+    if (g.list_offsets[list + 1] == g.list_offsets[list]) return;
+    const uint32_t e = rank_bucket(g, p) * g.n_lists + list;
+    const uint32_t pos = g.bucket_off[e] + atomicAdd(&g.cursor[e], 1u);
+    g.bucket_q[pos] = q;
+    g.bucket_slot[pos] = p;
+}
+
+__global__ void group_items_kernel(const GroupArgs g) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= g.n_rb * g.n_lists) return;
+    const uint32_t c = g.counts[e];
+    if (c == 0) return;
+    const uint32_t list = e % g.n_lists;
+    const uint32_t start = g.list_offsets[list], len = g.list_offsets[list + 1] - start;
+    const uint32_t ni = (c + kQC - 1) / kQC;
+    for (uint32_t t = 0; t < ni; ++t) {
+        WorkItem w;
+        w.row_start = start;
+        w.row_count = len;
+        w.bucket_start = g.bucket_off[e] + t * kQC;
+        w.bucket_count = min((uint32_t)kQC, c - t * kQC);
+        g.items[g.item_off[e] + t] = w;
+    }
+}
+
+// ---- per-pair DCO: checkpointed_scan (proj/src/estimator.cpp:24-70) ------------
+__global__ void evaluate_kernel(const float* __restrict__ o, const float* __restrict__ q,
+                                const float* __restrict__ r, uint32_t n, uint32_t dim,
+                                const uint32_t* __restrict__ cps, const double* __restrict__ coeff,
+                                const double* __restrict__ scale, uint32_t n_ckpt, uint8_t* pruned,
+                                float* dist, uint8_t* exact, uint32_t* dims_used,
+                                unsigned long long* counters) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* oi = o + (size_t)i * dim;
+    const float* qi = q + (size_t)i * dim;
+    const float ri = r[i];
+    const double r2 = __dmul_rn((double)ri, (double)ri);
+    float acc = 0.f;
+    uint32_t prev = 0;
+    bool pr = false, ex = true;
+    float d_out = 0.f;
+    uint32_t used = dim;
+    for (uint32_t ci = 0; ci < n_ckpt; ++ci) {
+        const uint32_t d = cps[ci];
+        for (uint32_t k = prev; k < d; ++k) acc = sq_step(acc, oi[k], qi[k]);
+        prev = d;
+        if ((double)acc > __dmul_rn(coeff[ci], r2)) {
+            pr = true;
+            ex = false;
+            d_out = __double2float_rn(__dsqrt_rn(__dmul_rn(scale[ci], (double)acc)));
+            used = d;
+            break;
+        }
+    }
+    float full = acc;
+    const uint32_t from = pr ? used : prev;
+    for (uint32_t k = from; k < dim; ++k) full = sq_step(full, oi[k], qi[k]);
+    if (!pr) {
+        d_out = __fsqrt_rn(full);
+        pr = d_out > ri;
+    }
+    pruned[i] = pr;
+    dist[i] = d_out;
+    exact[i] = ex;
+    dims_used[i] = used;
+    if (counters) {
+        atomicAdd(counters + 0, 1ull);
+        atomicAdd(counters + 1, (unsigned long long)used);
+        // failure accounting (record_failure_check, estimator.cpp:24-33)
+        if (__fsqrt_rn(full) <= ri) {
+            atomicAdd(counters + 2, 1ull);
+            if (pr) atomicAdd(counters + 3, 1ull);
+        }
+    }
+}
+
+__global__ void partial_sums_kernel(const float* __restrict__ o, const float* __restrict__ q, uint32_t n,
+                                    uint32_t dim, const uint32_t* __restrict__ cps, uint32_t n_ckpt,
+                                    float* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* oi = o + (size_t)i * dim;
+    const float* qi = q + (size_t)i * dim;
+    float acc = 0.f;
+    uint32_t prev = 0;
+    for (uint32_t ci = 0; ci <= n_ckpt; ++ci) {
+        const uint32_t d = ci < n_ckpt ? cps[ci] : dim;
+        for (uint32_t k = prev; k < d; ++k) acc = sq_step(acc, oi[k], qi[k]);
+        prev = d;
+        out[(size_t)i * (n_ckpt + 1) + ci] = acc;
+    }
+}
+
+// collect_ratios' running accumulator (proj/src/calibration.cpp:40-50) on
+// sampled pairs (i, j): out[p][ci] = partial at checkpoint ci, out[p][n] = full.
+__global__ void pair_partials_kernel(const float* __restrict__ data, uint32_t dim,
+                                     const uint32_t* __restrict__ pi, const uint32_t* __restrict__ pj,
+                                     uint64_t n, const uint32_t* __restrict__ cps, uint32_t n_ckpt,
+                                     float* out) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const float* a = data + (size_t)pi[p] * dim;
+    const float* b = data + (size_t)pj[p] * dim;
+    float acc = 0.f;
+    uint32_t prev = 0;
+    for (uint32_t ci = 0; ci <= n_ckpt; ++ci) {
+        const uint32_t d = ci < n_ckpt ? cps[ci] : dim;
+        for (uint32_t k = prev; k < d; ++k) acc = sq_step(acc, a[k], b[k]);
+        prev = d;
+        out[p * (n_ckpt + 1) + ci] = acc;
+    }
+}
+
+__global__ void fill_u32_kernel(uint32_t* p, uint32_t v, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+}  // namespace
+
+cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    fill_u32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, v, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
+                          cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    dim3 grid((dim + kRotTile - 1) / kRotTile, (n + kRotTile - 1) / kRotTile);
+    rotate_kernel<<<grid, 256, 0, s>>>(W, dim, in, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_group(const GroupArgs& g, cudaStream_t s) {
+    const size_t pairs = (size_t)g.nq * g.n_probe;
+    const uint32_t ne = g.n_rb * g.n_lists;
+    DADE_CUDA_TRY(cudaMemsetAsync(g.counts, 0, sizeof(uint32_t) * ne, s));
+    DADE_CUDA_TRY(cudaMemsetAsync(g.cursor, 0, sizeof(uint32_t) * ne, s));
+    const unsigned gp = (unsigned)((pairs + 255) / 256);
+    if (pairs) group_count_kernel<<<gp, 256, 0, s>>>(g);
+    group_scan_kernel<<<1, 1024, 0, s>>>(g);
+    if (pairs) group_scatter_kernel<<<gp, 256, 0, s>>>(g);
+    group_items_kernel<<<(ne + 255) / 256, 256, 0, s>>>(g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_evaluate(const float* o, const float* q, const float* r, uint32_t n, uint32_t dim,
+                            const uint32_t* cps, const double* coeff, const double* scale,
+                            uint32_t n_ckpt, uint8_t* pruned, float* dist, uint8_t* exact,
+                            uint32_t* dims_used, unsigned long long* counters, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    evaluate_kernel<<<(n + 127) / 128, 128, 0, s>>>(o, q, r, n, dim, cps, coeff, scale, n_ckpt, pruned,
+                                                    dist, exact, dims_used, counters);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_partial_sums(const float* o, const float* q, uint32_t n, uint32_t dim,
+                                const uint32_t* cps, uint32_t n_ckpt, float* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    partial_sums_kernel<<<(n + 127) / 128, 128, 0, s>>>(o, q, n, dim, cps, n_ckpt, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pair_partials(const float* data, uint32_t dim, const uint32_t* pi,
+                                 const uint32_t* pj, uint64_t n, const uint32_t* cps,
+                                 uint32_t n_ckpt, float* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    pair_partials_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(data, dim, pi, pj, n, cps, n_ckpt, out);
+    return cudaGetLastError();
+}
+
+}  // namespace dade_gpu
