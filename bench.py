@@ -212,7 +212,8 @@ def run_ours(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     dev = gp.Device(local)
-    stream = torch.cuda.current_stream(device)
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)  # torch ops, CUDA events and the C ABI share one stream
 
     nq_total = cfg.nq * world
     art = W.build(cfg, dev, device, with_gt=(rank == 0), nq=nq_total, log=log if rank == 0 else (lambda *a: None))

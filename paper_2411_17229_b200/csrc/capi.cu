@@ -107,6 +107,17 @@ ChunkTable make_chunks(uint32_t dim, const std::vector<uint32_t>& cps) {
         k = e;
     }
     ct.n_chunks = n;
+    ct.n_dense = n;
+    for (int c = 0; c < n; ++c)
+        if (ct.ckpt[c] >= 0) {
+            ct.n_dense = c + 1;
+            break;
+        }
+    bool al = (dim & 3u) == 0;
+    for (int c = 0; c < n; ++c) al = al && (ct.end[c] & 3u) == 0;
+    ct.vec_ok = al ? 1 : 0;
+    const uint32_t dense_dims = ct.end[ct.n_dense - 1];
+    ct.d_res = (al && dense_dims * kQC * 4 <= (uint32_t)kMaxResidentQBytes) ? (int)dense_dims : 0;
     return ct;
 }
 
@@ -456,7 +467,8 @@ int dade_gpu_create(int device, dade_gpu_ctx** out) {
         auto* c = new dade_gpu_ctx;
         c->device = device;
         c->use_device();
-        cuda_check(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "stream");
+        // blocking stream: orders with the legacy default stream callers use
+        cuda_check(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamDefault), "stream");
         c->stream = c->own_stream;
         cuda_check(cudaEventCreate(&c->e0), "event");
         cuda_check(cudaEventCreate(&c->e1), "event");

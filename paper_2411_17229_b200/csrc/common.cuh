@@ -30,12 +30,20 @@ struct WorkItem {
 
 // Chunk table: chunk c covers dims [c_begin, end[c]); ckpt[c] = checkpoint
 // index tested after the chunk, or -1.
+// Chunks [0, n_dense) form the dense phase (up to and including the first
+// checkpoint; all chunks without checkpoints). d_res > 0: the queries' first
+// d_res dims stay resident in shared memory. vec_ok: every boundary is a
+// multiple of 4 (16-byte staging and loads).
 struct ChunkTable {
     int n_chunks;
     int n_ckpt;
+    int n_dense;
+    int d_res;
+    int vec_ok;
     uint16_t end[kMaxChunks];
     int16_t ckpt[kMaxChunks];
 };
+constexpr int kMaxResidentQBytes = 64 * 1024;
 
 // ---- exact fp32 arithmetic -------------------------------------------------
 // The reference accumulates acc += (o - q)^2 with three separately rounded

@@ -1,20 +1,30 @@
 // DCO scan kernel (K4/K6/K2 of SURVEY.md §2) and top-K merges (K5).
 //
-// One CTA = one work item: a contiguous row range (an IVF posting list or a
-// flat row block) x up to kQC queries. Rows are swept in kRT-row tiles; each
-// tile is swept in dimension chunks of <= kCH dims, with checkpoint tests at
-// the strategy's checkpoints (proj/src/estimator.cpp:39-70):
-//   * dense phase: every (row, query) pair of the tile in registers, 4 rows x
-//     8 queries per thread, packed FADD2/FFMA2 math (bit-exact, see
-//     common.cuh), queries broadcast from shared memory;
-//   * after a checkpoint leaves <= kSparseCap pairs alive, the survivors are
-//     compacted (warp ballot + prefix) into a shared list and only they are
-//     advanced through the remaining chunks;
-//   * exact full-D survivors with distance <= r become candidates and are
-//     merged into the per-(query, slot) top-K segment in global memory, which
-//     tightens the CTA's radius within the list (the reference's live heap
-//     threshold, proj/src/ivf.cpp:221-229) and, via atomicMin, the query's
-//     global radius seen by every later tile of every CTA.
+// One CTA = one work item: a contiguous row range (an IVF posting list, or a
+// flat row block) x up to kQC queries. The range is swept in kRT-row tiles.
+//
+//   dense phase  the chunks up to and including the first checkpoint
+//                (every chunk in FD mode): all kRT x kQC pairs of the tile in
+//                registers, 4 rows x 8 queries per thread, packed FADD2/FFMA2
+//                (bit-exact, see common.cuh). The o tile of the next
+//                (tile, chunk) step is prefetched with cp.async while the
+//                current one is computed (double buffer); the queries' dense
+//                dims stay resident in shared memory for the whole item.
+//   sparse phase pairs that pass the first checkpoint are compacted per warp
+//                (ballot + prefix) and advanced one pair per lane straight
+//                from global memory (L2) through the remaining chunks and
+//                checkpoints (proj/src/estimator.cpp:39-70).
+//   top-K        exact full-D survivors with distance <= r are merged by the
+//                warp that owns the query into its (query, slot) top-K
+//                segment in global memory. The K-th key tightens the
+//                CTA's radius for the rest of the list (the reference's live
+//                heap threshold, proj/src/ivf.cpp:221-229) and, by atomicMin,
+//                the query's global radius read by every later tile of every
+//                CTA.
+//
+// Warp w owns queries [8w, 8w+8) of the chunk for the whole item, so after
+// the per-step __syncthreads that guards the o-tile double buffer, all
+// survivor / candidate / merge work is warp-local.
 #include <cfloat>
 #include <cstdio>
 
@@ -25,28 +35,27 @@ namespace dade_gpu {
 
 namespace {
 
+constexpr int kWarpList = 256;  // survivor-list entries per warp per round
+
 struct SmemLayout {
-    size_t o_t, q_k, q_j, r_s, thr_s, qidx, slot, la_meta, la_acc, lb_meta, lb_acc, keys, cnt, total;
+    size_t o_buf, q_res, q_stage, r_s, thr_s, qidx, slot, wl_meta, wl_acc, keys, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline SmemLayout smem_layout(int n_ckpt) {
+__host__ __device__ inline SmemLayout smem_layout(int n_ckpt, int d_res) {
     SmemLayout L;
     size_t off = 0;
-    L.o_t = off; off = align16(off + sizeof(float) * kRT * kOStride);
-    L.q_k = off; off = align16(off + sizeof(float) * kCH * kQC);
-    L.q_j = off; off = align16(off + sizeof(float) * kQC * kOStride);
+    L.o_buf = off; off = align16(off + sizeof(float) * 2 * kRT * kOStride);
+    L.q_res = off; off = align16(off + sizeof(float) * (size_t)d_res * kQC);
+    L.q_stage = off; off = align16(off + (d_res == 0 ? sizeof(float) * kCH * kQC : 0));
     L.r_s = off; off = align16(off + sizeof(float) * kQC);
     L.thr_s = off; off = align16(off + sizeof(float) * kQC * (n_ckpt > 0 ? n_ckpt : 1));
     L.qidx = off; off = align16(off + sizeof(uint32_t) * kQC);
     L.slot = off; off = align16(off + sizeof(uint32_t) * kQC);
-    L.la_meta = off; off = align16(off + sizeof(uint32_t) * kSparseCap);
-    L.la_acc = off; off = align16(off + sizeof(float) * kSparseCap);
-    L.lb_meta = off; off = align16(off + sizeof(uint32_t) * kSparseCap);
-    L.lb_acc = off; off = align16(off + sizeof(float) * kSparseCap);
+    L.wl_meta = off; off = align16(off + sizeof(uint32_t) * kWarps * kWarpList);
+    L.wl_acc = off; off = align16(off + sizeof(float) * kWarps * kWarpList);
     L.keys = off; off = align16(off + sizeof(uint64_t) * kWarps * kRT);
-    L.cnt = off; off = align16(off + sizeof(uint32_t) * (3 * kQC + 16));
     L.total = off;
     return L;
 }
@@ -55,6 +64,14 @@ __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
     return *reinterpret_cast<const volatile uint32_t*>(p);
 }
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    const int n = valid ? 16 : 0;  // src-size 0 -> zero fill
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
 // Recompute query j's per-checkpoint float thresholds from r_s[j].
 __device__ __forceinline__ void refresh_thr(float* thr_s, const float* r_s, const double* coeff,
                                             int n_ckpt, int j, int lane_in, int lanes) {
@@ -62,32 +79,51 @@ __device__ __forceinline__ void refresh_thr(float* thr_s, const float* r_s, cons
     for (int c = lane_in; c < n_ckpt; c += lanes) thr_s[j * n_ckpt + c] = prune_threshold(coeff[c], r);
 }
 
+// Warp-level: merge the m candidate keys of query j (in kb) into its segment,
+// then tighten r_s[j] / thr_s / the global radius from the new K-th key.
+__device__ __forceinline__ void merge_query(const ScanArgs& a, uint64_t* kb, uint32_t m, uint32_t j,
+                                            const uint32_t* qidx_s, const uint32_t* slot_s, float* r_s,
+                                            float* thr_s, int n_ckpt, int lane) {
+    const size_t seg = (size_t)qidx_s[j] * a.n_slots + slot_s[j];
+    uint64_t* A = a.seg_keys + seg * a.K;
+    const uint32_t nc = warp_merge(A, a.seg_count + seg, a.K, kb, m, false);
+    if (nc == a.K) {
+        const float rn = hi_f(A[a.K - 1]);
+        if (rn < r_s[j]) {
+            __syncwarp();
+            if (lane == 0) {
+                r_s[j] = rn;
+                atomicMin(a.r_global + qidx_s[j], __float_as_uint(rn));
+            }
+            __syncwarp();
+            refresh_thr(thr_s, r_s, a.coeff, n_ckpt, j, lane, 32);
+        }
+    }
+    __syncwarp();
+}
+
 template <bool kSqrtKey>
 __global__ void __launch_bounds__(kThreads, 2)
 dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int n_ckpt = ct.n_ckpt;
-    const SmemLayout L = smem_layout(n_ckpt);
-    float* o_t = reinterpret_cast<float*>(smem + L.o_t);
-    float* q_k = reinterpret_cast<float*>(smem + L.q_k);
-    float* q_j = reinterpret_cast<float*>(smem + L.q_j);
+    const int d_res = ct.d_res;  // resident query dims (0 -> stage per chunk)
+    const SmemLayout L = smem_layout(n_ckpt, d_res);
+    float* o_buf = reinterpret_cast<float*>(smem + L.o_buf);
+    float* q_res = reinterpret_cast<float*>(smem + L.q_res);
+    float* q_stage = reinterpret_cast<float*>(smem + L.q_stage);
     float* r_s = reinterpret_cast<float*>(smem + L.r_s);
     float* thr_s = reinterpret_cast<float*>(smem + L.thr_s);
     uint32_t* qidx_s = reinterpret_cast<uint32_t*>(smem + L.qidx);
     uint32_t* slot_s = reinterpret_cast<uint32_t*>(smem + L.slot);
-    uint32_t* lmeta[2] = {reinterpret_cast<uint32_t*>(smem + L.la_meta),
-                          reinterpret_cast<uint32_t*>(smem + L.lb_meta)};
-    float* lacc[2] = {reinterpret_cast<float*>(smem + L.la_acc), reinterpret_cast<float*>(smem + L.lb_acc)};
-    uint64_t* keys_s = reinterpret_cast<uint64_t*>(smem + L.keys);
-    uint32_t* qcnt = reinterpret_cast<uint32_t*>(smem + L.cnt);  // [kQC] candidate counts
-    uint32_t* qoff = qcnt + kQC;                                 // [kQC] offsets in round
-    uint32_t* qcur = qoff + kQC;                                 // [kQC] scatter cursors
-    uint32_t* misc = qcur + kQC;                                 // [16]
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const uint32_t dim = a.dim;
+    uint32_t* wl_meta = reinterpret_cast<uint32_t*>(smem + L.wl_meta) + warp * kWarpList;
+    float* wl_acc = reinterpret_cast<float*>(smem + L.wl_acc) + warp * kWarpList;
+    uint64_t* kb = reinterpret_cast<uint64_t*>(smem + L.keys) + warp * kRT;
 
     // ---- decode the work item ------------------------------------------------
     uint32_t row_start, row_count, qcount;
@@ -112,344 +148,300 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
             slot_s[tid] = rb;
         }
     }
-    if (tid < kQC) r_s[tid] = __int_as_float(0x7f800000);
     if (tid < kQC && tid >= (int)qcount) { qidx_s[tid] = 0; slot_s[tid] = 0; }
+    if (tid < kQC) r_s[tid] = __int_as_float(0x7f800000);
+    __syncthreads();
+    // resident queries, k-major [d_res][kQC]
+    for (uint32_t idx = tid; idx < (uint32_t)d_res * kQC; idx += kThreads) {
+        const uint32_t j = idx / d_res, k = idx - j * d_res;
+        q_res[k * kQC + j] = j < qcount ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k) : 0.f;
+    }
 
     unsigned long long st_dco = 0, st_dims = 0, st_bytes = 0;
-    if (tid == 0) st_bytes += sizeof(WorkItem) + 8ull * qcount;
+    if (tid == 0) st_bytes += sizeof(WorkItem) + 8ull * qcount + 4ull * d_res * qcount;
     const uint64_t nz2 = a.neg_zero2;
+    const int c_dense = ct.n_dense;
+    const bool has_sparse = c_dense < ct.n_chunks;
+    const uint32_t n_tiles = (row_count + kRT - 1) / kRT;
+    const uint32_t n_steps = n_tiles * c_dense;
+    const bool vec = (dim & 3u) == 0 && ct.vec_ok;
 
-    for (uint32_t tile_base = 0; tile_base < row_count; tile_base += kRT) {
-        const uint32_t nrows = min((uint32_t)kRT, row_count - tile_base);
-        __syncthreads();  // previous tile's merges finished with r_s / thr_s
-        // Pick up radii tightened by other CTAs (or our own earlier tiles).
-        if (tid < (int)qcount) {
-            const float rg = __uint_as_float(ld_volatile_u32(a.r_global + qidx_s[tid]));
-            const bool first = tile_base == 0;
-            if (rg < r_s[tid] || first) {
-                r_s[tid] = fminf(rg, r_s[tid]);
-                refresh_thr(thr_s, r_s, a.coeff, n_ckpt, tid, 0, 1);
+    // stage the o tile of step s into buffer (s & 1)
+    auto issue = [&](uint32_t s) {
+        const uint32_t t = s / c_dense, c = s - t * c_dense;
+        const uint32_t tb = t * kRT, nrows = min((uint32_t)kRT, row_count - tb);
+        const uint32_t k0 = c == 0 ? 0u : ct.end[c - 1];
+        const uint32_t w = ct.end[c] - k0;
+        float* buf = o_buf + (s & 1) * (kRT * kOStride);
+        if (vec) {
+            const uint32_t v4 = w >> 2;
+            for (uint32_t idx = tid; idx < kRT * v4; idx += kThreads) {
+                const uint32_t r = idx / v4, c4 = idx - r * v4;
+                const bool ok = r < nrows;
+                const float* src = a.storage + (size_t)(row_start + tb + (ok ? r : 0)) * dim + k0 + 4 * c4;
+                cp_async16(buf + r * kOStride + 4 * c4, src, ok);
+            }
+        } else {
+            const uint32_t w4 = (w + 3) & ~3u;
+            for (uint32_t idx = tid; idx < kRT * w4; idx += kThreads) {
+                const uint32_t r = idx / w4, cc = idx - r * w4;
+                float v = 0.f;
+                if (r < nrows && cc < w) v = __ldg(a.storage + (size_t)(row_start + tb + r) * dim + k0 + cc);
+                buf[r * kOStride + cc] = v;
             }
         }
+        cp_async_commit();
+        if (tid == 0) st_bytes += 4ull * w * nrows;
+    };
 
-        // ---- dense state -------------------------------------------------------
-        uint64_t acc[4][4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
-        uint32_t alive = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-                if ((uint32_t)(lane + 32 * i) < nrows && (uint32_t)(warp * 8 + jj) < qcount)
-                    alive |= 1u << (i * 8 + jj);
-        st_dco += __popc(alive);
-        bool dense = true;
-        int cur = 0;              // active sparse list
-        uint32_t cand = 0;        // dense candidate bits (final chunk)
+    if (n_steps > 0) issue(0);
 
-        for (int c = 0; c < ct.n_chunks; ++c) {
-            const uint32_t k0 = c == 0 ? 0u : ct.end[c - 1];
-            const uint32_t w = ct.end[c] - k0;
-            const uint32_t w4 = (w + 3) & ~3u;
-            __syncthreads();  // everyone done with the previous chunk's tiles
-            // ---- stage the o tile [kRT x w4] and q tiles ------------------------
-            const bool vec = ((dim | k0 | w) & 3u) == 0;
-            if (vec) {
-                const uint32_t v4 = w >> 2;
-                for (uint32_t idx = tid; idx < kRT * v4; idx += kThreads) {
-                    const uint32_t r = idx / v4, c4 = idx - r * v4;
-                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (r < nrows)
-                        v = __ldg(reinterpret_cast<const float4*>(
-                            a.storage + (size_t)(row_start + tile_base + r) * dim + k0) + c4);
-                    *reinterpret_cast<float4*>(o_t + r * kOStride + 4 * c4) = v;
-                }
-            } else {
-                for (uint32_t idx = tid; idx < kRT * w4; idx += kThreads) {
-                    const uint32_t r = idx / w4, cc = idx - r * w4;
-                    float v = 0.f;
-                    if (r < nrows && cc < w) v = __ldg(a.storage + (size_t)(row_start + tile_base + r) * dim + k0 + cc);
-                    o_t[r * kOStride + cc] = v;
+    uint64_t acc[4][4];
+    uint32_t alive = 0;
+    for (uint32_t s = 0; s < n_steps; ++s) {
+        const uint32_t t = s / c_dense;
+        const int c = (int)(s - t * c_dense);
+        const uint32_t tb = t * kRT, nrows = min((uint32_t)kRT, row_count - tb);
+        const uint32_t k0 = c == 0 ? 0u : ct.end[c - 1];
+        const uint32_t w = ct.end[c] - k0;
+        const uint32_t w4 = (w + 3) & ~3u;
+        if (c == 0) {
+            // tile start: pick up radii tightened by other CTAs; reset the pairs
+            if (lane < 8) {
+                const int j = warp * 8 + lane;
+                if (j < (int)qcount) {
+                    const float rg = __uint_as_float(ld_volatile_u32(a.r_global + qidx_s[j]));
+                    if (rg < r_s[j] || t == 0) {
+                        r_s[j] = fminf(rg, r_s[j]);
+                        refresh_thr(thr_s, r_s, a.coeff, n_ckpt, j, 0, 1);
+                    }
                 }
             }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
+            alive = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj)
+                    if ((uint32_t)(lane + 32 * i) < nrows && (uint32_t)(warp * 8 + jj) < qcount)
+                        alive |= 1u << (i * 8 + jj);
+            st_dco += __popc(alive);
+        }
+        cp_async_wait_all();
+        __syncthreads();  // tile s visible to all; everyone done with tile s-1's buffer
+        if (s + 1 < n_steps) issue(s + 1);
+        const float* buf = o_buf + (s & 1) * (kRT * kOStride);
+        const float* qk;
+        if (d_res > 0) {
+            qk = q_res + k0 * kQC;
+        } else {
+            // non-resident queries: stage this chunk's slice (k-major)
             for (uint32_t idx = tid; idx < kQC * w4; idx += kThreads) {
                 const uint32_t j = idx / w4, cc = idx - j * w4;
-                float v = 0.f;
-                if (j < qcount && cc < w) v = __ldg(a.queries + (size_t)qidx_s[j] * dim + k0 + cc);
-                q_k[cc * kQC + j] = v;
-                q_j[j * kOStride + cc] = v;
+                q_stage[cc * kQC + j] =
+                    (j < qcount && cc < w) ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k0 + cc) : 0.f;
             }
-            if (tid == 0) st_bytes += 4ull * w * (nrows + qcount);
             __syncthreads();
+            qk = q_stage;
+            if (tid == 0) st_bytes += 4ull * w * qcount;
+        }
 
-            const int ck = ct.ckpt[c];
-            const bool last = c == ct.n_chunks - 1;
-            if (dense) {
-                // ---- dense register-tiled update -------------------------------
-                if (__any_sync(0xffffffffu, alive != 0)) {
-                    for (uint32_t k4 = 0; k4 < w4; k4 += 4) {
-                        float4 o[4];
+        // ---- dense register-tiled update -------------------------------------
+        if (__any_sync(0xffffffffu, alive != 0)) {
+            for (uint32_t k4 = 0; k4 < w4; k4 += 4) {
+                float4 o[4];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            o[i] = *reinterpret_cast<const float4*>(o_t + (lane + 32 * i) * kOStride + k4);
+                for (int i = 0; i < 4; ++i)
+                    o[i] = *reinterpret_cast<const float4*>(buf + (lane + 32 * i) * kOStride + k4);
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const ulonglong2 qa = *reinterpret_cast<const ulonglong2*>(q_k + (k4 + kk) * kQC + warp * 8);
-                            const ulonglong2 qb = *reinterpret_cast<const ulonglong2*>(q_k + (k4 + kk) * kQC + warp * 8 + 4);
-                            const uint64_t qp[4] = {qa.x, qa.y, qb.x, qb.y};
+                for (int kk = 0; kk < 4; ++kk) {
+                    const ulonglong2 qa = *reinterpret_cast<const ulonglong2*>(qk + (k4 + kk) * kQC + warp * 8);
+                    const ulonglong2 qb = *reinterpret_cast<const ulonglong2*>(qk + (k4 + kk) * kQC + warp * 8 + 4);
+                    const uint64_t qp[4] = {qa.x, qa.y, qb.x, qb.y};
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const float ov = kk == 0 ? o[i].x : kk == 1 ? o[i].y : kk == 2 ? o[i].z : o[i].w;
+                    for (int i = 0; i < 4; ++i) {
+                        const float ov = kk == 0 ? o[i].x : kk == 1 ? o[i].y : kk == 2 ? o[i].z : o[i].w;
 #pragma unroll
-                                for (int p = 0; p < 4; ++p) acc[i][p] = sq_step2(acc[i][p], ov, qp[p], nz2);
-                            }
-                        }
+                        for (int p = 0; p < 4; ++p) acc[i][p] = sq_step2(acc[i][p], ov, qp[p], nz2);
                     }
                 }
-                if (ck >= 0) {
-                    // checkpoint test on every live pair
-                    uint32_t dead = 0;
+            }
+        }
+        if (c != c_dense - 1) continue;
+
+        // ---- end of the dense phase for this tile (warp-local from here) ------
+        const int ck = ct.ckpt[c];
+        uint32_t cand = 0;  // dense candidate bits (FD: no sparse phase)
+        if (has_sparse) {
+            uint32_t dead = 0;
 #pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) {
-                        const float t = thr_s[(warp * 8 + jj) * n_ckpt + ck];
+            for (int jj = 0; jj < 8; ++jj) {
+                const float th = thr_s[(warp * 8 + jj) * n_ckpt + ck];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
+                for (int i = 0; i < 4; ++i) {
+                    const uint64_t v = acc[i][jj >> 1];
+                    const float x = (jj & 1) ? hi_f(v) : lo_f(v);
+                    if (x > th) dead |= 1u << (i * 8 + jj);
+                }
+            }
+            dead &= alive;
+            alive &= ~dead;
+            st_dims += (unsigned long long)__popc(dead) * ct.end[c];
+        } else {
+            st_dims += (unsigned long long)__popc(alive) * dim;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const float r = r_s[warp * 8 + jj];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint64_t v = acc[i][jj >> 1];
+                    const float x = (jj & 1) ? hi_f(v) : lo_f(v);
+                    const float key = kSqrtKey ? __fsqrt_rn(x) : x;
+                    if (((alive >> (i * 8 + jj)) & 1u) && !(key > r)) cand |= 1u << (i * 8 + jj);
+                }
+            }
+            alive = 0;
+        }
+
+        if (!has_sparse) {
+            // FD: candidates straight from registers, one query at a time
+            if (__any_sync(0xffffffffu, cand != 0)) {
+                for (int jj = 0; jj < 8; ++jj) {
+                    const uint32_t j = warp * 8 + jj;
+                    uint32_t m = 0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const bool is = (cand >> (i * 8 + jj)) & 1u;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, is);
+                        if (is) {
                             const uint64_t v = acc[i][jj >> 1];
                             const float x = (jj & 1) ? hi_f(v) : lo_f(v);
-                            if (x > t) dead |= 1u << (i * 8 + jj);
+                            const uint32_t g = row_start + tb + lane + 32 * i;
+                            const uint32_t id = a.row_ids ? __ldg(a.row_ids + g) : a.id_base + g;
+                            kb[m + __popc(bal & ((1u << lane) - 1u))] = make_key(kSqrtKey ? __fsqrt_rn(x) : x, id);
                         }
+                        m += __popc(bal);
                     }
-                    dead &= alive;
-                    alive &= ~dead;
-                    st_dims += (unsigned long long)__popc(dead) * ct.end[c];
-                    if (tid == 0) misc[0] = 0;
-                    __syncthreads();
-                    uint32_t wsum = __reduce_add_sync(0xffffffffu, __popc(alive));
-                    if (lane == 0) atomicAdd(&misc[0], wsum);
-                    __syncthreads();
-                    const uint32_t total_alive = misc[0];
-                    if (total_alive <= (uint32_t)kSparseCap && !last) {
-                        // ---- switch to the sparse survivor list -------------------
-                        if (tid == 0) misc[1] = 0;
-                        __syncthreads();
-                        const uint32_t mine = __popc(alive);
-                        uint32_t incl = mine;
-#pragma unroll
-                        for (int off = 1; off < 32; off <<= 1) {
-                            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-                            if (lane >= off) incl += y;
-                        }
-                        uint32_t base = 0;
-                        if (lane == 31) base = atomicAdd(&misc[1], incl);
-                        base = __shfl_sync(0xffffffffu, base, 31);
-                        uint32_t pos = base + incl - mine;
-                        uint32_t bits = alive;
-                        while (bits) {
-                            const int b = __ffs(bits) - 1;
-                            bits &= bits - 1;
-                            const int i = b >> 3, jj = b & 7;
-                            const uint64_t v = acc[i][jj >> 1];
-                            lmeta[0][pos] = (uint32_t)(lane + 32 * i) | ((uint32_t)(warp * 8 + jj) << 8);
-                            lacc[0][pos] = (jj & 1) ? hi_f(v) : lo_f(v);
-                            ++pos;
-                        }
-                        dense = false;
-                        cur = 0;
-                        __syncthreads();
-                        if (tid == 0) misc[2] = misc[1];  // list length
-                        __syncthreads();
+                    __syncwarp();
+                    if (m) {
+                        if (a.row_ids && lane == 0) st_bytes += 4ull * m;
+                        merge_query(a, kb, m, j, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane);
                     }
                 }
-                if (last) {
-                    st_dims += (unsigned long long)__popc(alive) * dim;
+            }
+            continue;
+        }
+
+        // ---- sparse rounds: compact, advance from global, merge ---------------
+        uint32_t pending = alive;
+        while (__any_sync(0xffffffffu, pending != 0)) {
+            const uint32_t mine = __popc(pending);
+            uint32_t incl = mine;
 #pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) {
-                        const float r = r_s[warp * 8 + jj];
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const uint64_t v = acc[i][jj >> 1];
-                            const float x = (jj & 1) ? hi_f(v) : lo_f(v);
-                            const float key = kSqrtKey ? __fsqrt_rn(x) : x;
-                            if (((alive >> (i * 8 + jj)) & 1u) && !(key > r)) cand |= 1u << (i * 8 + jj);
-                        }
-                    }
-                }
-            } else {
-                // ---- sparse survivor update -----------------------------------
-                const uint32_t n = misc[2];
-                uint32_t* meta_in = lmeta[cur];
-                float* acc_in = lacc[cur];
-                uint32_t* meta_out = lmeta[cur ^ 1];
-                float* acc_out = lacc[cur ^ 1];
-                if (ck >= 0 && tid == 0) misc[1] = 0;
-                if (ck >= 0) __syncthreads();
-                const uint32_t n_round = (n + kThreads - 1) / kThreads * kThreads;
-                for (uint32_t e = tid; e < n_round; e += kThreads) {
-                    bool keep = false;
-                    uint32_t meta = 0;
-                    float x = 0.f;
-                    if (e < n) {
-                        meta = meta_in[e];
-                        x = acc_in[e];
-                        const uint32_t row = meta & 0xffu, j = meta >> 8;
-                        const float* orow = o_t + row * kOStride;
-                        const float* qrow = q_j + j * kOStride;
-                        for (uint32_t k4 = 0; k4 < w4; k4 += 4) {
-                            const float4 o4 = *reinterpret_cast<const float4*>(orow + k4);
-                            const float4 q4 = *reinterpret_cast<const float4*>(qrow + k4);
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            uint32_t pos = incl - mine;
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            const uint32_t n = min(total, (uint32_t)kWarpList);
+            uint32_t bits = pending;
+            while (bits && pos < (uint32_t)kWarpList) {
+                const int b = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int i = b >> 3, jj = b & 7;
+                const uint64_t v = acc[i][jj >> 1];
+                wl_meta[pos] = (uint32_t)(lane + 32 * i) | ((uint32_t)jj << 8);
+                wl_acc[pos] = (jj & 1) ? hi_f(v) : lo_f(v);
+                pending &= ~(1u << b);
+                ++pos;
+            }
+            __syncwarp();
+            // advance each survivor through the remaining chunks (one per lane)
+            for (uint32_t e = lane; e < n; e += 32) {
+                uint32_t meta = wl_meta[e];
+                float x = wl_acc[e];
+                const uint32_t row = meta & 0xffu, jj = (meta >> 8) & 0xffu, j = warp * 8 + jj;
+                const float* orow = a.storage + (size_t)(row_start + tb + row) * dim;
+                const float* qrow = a.queries + (size_t)qidx_s[j] * dim;
+                bool live = true;
+                for (int cc = c_dense; cc < ct.n_chunks; ++cc) {
+                    const uint32_t lo = ct.end[cc - 1], hi = ct.end[cc];
+                    if (vec) {
+                        for (uint32_t kk = lo; kk < hi; kk += 4) {
+                            const float4 o4 = __ldg(reinterpret_cast<const float4*>(orow + kk));
+                            const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + kk));
                             x = sq_step(x, o4.x, q4.x);
                             x = sq_step(x, o4.y, q4.y);
                             x = sq_step(x, o4.z, q4.z);
                             x = sq_step(x, o4.w, q4.w);
                         }
-                        if (ck >= 0) {
-                            keep = !(x > thr_s[j * n_ckpt + ck]);
-                            if (!keep) st_dims += ct.end[c];
-                        } else if (last) {
-                            st_dims += dim;
-                            const float key = kSqrtKey ? __fsqrt_rn(x) : x;
-                            const bool is_cand = !(key > r_s[j]);
-                            meta_in[e] = meta | (is_cand ? 0x80000000u : 0u);
-                            acc_in[e] = key;
-                        } else {
-                            acc_in[e] = x;
-                        }
+                    } else {
+                        for (uint32_t kk = lo; kk < hi; ++kk) x = sq_step(x, __ldg(orow + kk), __ldg(qrow + kk));
                     }
-                    if (ck >= 0) {
-                        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-                        uint32_t base = 0;
-                        if (lane == 0 && bal) base = atomicAdd(&misc[1], __popc(bal));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        if (keep) {
-                            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
-                            meta_out[pos] = meta;
-                            acc_out[pos] = x;
-                        }
+                    st_bytes += 8ull * (hi - lo);
+                    const int k2 = ct.ckpt[cc];
+                    if (k2 >= 0 && x > thr_s[j * n_ckpt + k2]) {
+                        st_dims += hi;
+                        live = false;
+                        break;
                     }
                 }
-                if (ck >= 0) {
-                    __syncthreads();
-                    if (tid == 0) misc[2] = misc[1];
-                    cur ^= 1;
-                    __syncthreads();
+                bool is_cand = false;
+                if (live) {
+                    st_dims += dim;
+                    const float key = kSqrtKey ? __fsqrt_rn(x) : x;
+                    is_cand = !(key > r_s[j]);
+                    x = key;
                 }
+                wl_meta[e] = meta | (is_cand ? 0x80000000u : 0u);
+                wl_acc[e] = x;
             }
-        }  // chunks
-
-        // ---- candidates -> per-(query, slot) top-K segments ----------------------
-        if (tid < kQC) { qcnt[tid] = 0; qcur[tid] = 0; }
-        __syncthreads();
-        const uint32_t n_sp = dense ? 0u : misc[2];
-        const uint32_t* sp_meta = lmeta[cur];
-        const float* sp_key = lacc[cur];
-        if (dense) {
-            uint32_t bits = cand;
-            while (bits) {
-                const int b = __ffs(bits) - 1;
-                bits &= bits - 1;
-                atomicAdd(&qcnt[warp * 8 + (b & 7)], 1u);
-            }
-        } else {
-            for (uint32_t e = tid; e < n_sp; e += kThreads) {
-                const uint32_t m = sp_meta[e];
-                if (m & 0x80000000u) atomicAdd(&qcnt[(m >> 8) & 0xffu], 1u);
-            }
-        }
-        __syncthreads();
-        // Rounds of consecutive queries whose candidates fit the scratch list.
-        uint32_t* cmeta = lmeta[dense ? 0 : (cur ^ 1)];
-        float* ckey = lacc[dense ? 0 : (cur ^ 1)];
-        uint32_t j_lo = 0;
-        while (j_lo < qcount) {
-            // every thread computes the same round end (qcnt is small)
-            uint32_t j_hi = j_lo, tot = 0;
-            while (j_hi < qcount && tot + qcnt[j_hi] <= (uint32_t)kSparseCap) {
-                tot += qcnt[j_hi];
-                ++j_hi;
-            }
-            if (tot == 0) { j_lo = j_hi; continue; }
-            if (tid < kQC) {
-                uint32_t o = 0;
-                for (uint32_t j = j_lo; j < (uint32_t)tid && j < j_hi; ++j) o += qcnt[j];
-                qoff[tid] = o;
-                qcur[tid] = 0;
-            }
-            __syncthreads();
-            if (dense) {
-                uint32_t bits = cand;
-                while (bits) {
-                    const int b = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    const int i = b >> 3, jj = b & 7;
-                    const uint32_t j = warp * 8 + jj;
-                    if (j < j_lo || j >= j_hi) continue;
-                    const uint64_t v = acc[i][jj >> 1];
-                    const float x = (jj & 1) ? hi_f(v) : lo_f(v);
-                    const uint32_t pos = qoff[j] + atomicAdd(&qcur[j], 1u);
-                    cmeta[pos] = (uint32_t)(lane + 32 * i);
-                    ckey[pos] = kSqrtKey ? __fsqrt_rn(x) : x;
-                }
-            } else {
-                for (uint32_t e = tid; e < n_sp; e += kThreads) {
-                    const uint32_t m = sp_meta[e];
-                    const uint32_t j = (m >> 8) & 0xffu;
-                    if (!(m & 0x80000000u) || j < j_lo || j >= j_hi) continue;
-                    const uint32_t pos = qoff[j] + atomicAdd(&qcur[j], 1u);
-                    cmeta[pos] = m & 0xffu;
-                    ckey[pos] = sp_key[e];
-                }
-            }
-            __syncthreads();
-            // warp w merges queries j == w (mod kWarps)
-            for (uint32_t j = j_lo + ((warp - j_lo % kWarps + kWarps) % kWarps); j < j_hi; j += kWarps) {
-                const uint32_t m = qcnt[j];
-                if (m == 0) continue;
-                uint64_t* kb = keys_s + warp * kRT;
-                for (uint32_t e = lane; e < m; e += 32) {
-                    const uint32_t row = cmeta[qoff[j] + e];
-                    const uint32_t g = row_start + tile_base + row;
-                    const uint32_t id = a.row_ids ? __ldg(a.row_ids + g) : a.id_base + g;
-                    kb[e] = make_key(ckey[qoff[j] + e], id);
-                }
-                st_bytes += a.row_ids ? 4ull * (m > lane ? (m - lane + 31) / 32 : 0) : 0ull;
-                __syncwarp();
-                const size_t seg = (size_t)qidx_s[j] * a.n_slots + slot_s[j];
-                uint64_t* A = a.seg_keys + seg * a.K;
-                const uint32_t nc = warp_merge(A, a.seg_count + seg, a.K, kb, m, false);
-                if (nc == a.K) {
-                    const float rn = hi_f(A[a.K - 1]);
-                    if (rn < r_s[j]) {
-                        __syncwarp();
-                        if (lane == 0) {
-                            r_s[j] = rn;
-                            atomicMin(a.r_global + qidx_s[j], __float_as_uint(rn));
-                        }
-                        __syncwarp();
-                        refresh_thr(thr_s, r_s, a.coeff, n_ckpt, j, lane, 32);
+            __syncwarp();
+            // per query: gather candidate keys, merge
+            for (int jj = 0; jj < 8; ++jj) {
+                uint32_t m = 0;
+                for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+                    const uint32_t e = e0 + lane;
+                    bool is = false;
+                    uint32_t meta = 0;
+                    if (e < n) {
+                        meta = wl_meta[e];
+                        is = (meta & 0x80000000u) && ((meta >> 8) & 0xffu) == (uint32_t)jj;
                     }
+                    const uint32_t bal = __ballot_sync(0xffffffffu, is);
+                    if (is) {
+                        const uint32_t g = row_start + tb + (meta & 0xffu);
+                        const uint32_t id = a.row_ids ? __ldg(a.row_ids + g) : a.id_base + g;
+                        kb[m + __popc(bal & ((1u << lane) - 1u))] = make_key(wl_acc[e], id);
+                    }
+                    m += __popc(bal);
                 }
                 __syncwarp();
+                if (m) {
+                    if (a.row_ids && lane == 0) st_bytes += 4ull * m;
+                    merge_query(a, kb, m, warp * 8 + jj, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane);
+                }
             }
-            __syncthreads();
-            j_lo = j_hi;
         }
-    }  // tiles
+    }  // steps
 
     // ---- counters -------------------------------------------------------------
-    st_dco = __reduce_add_sync(0xffffffffu, (unsigned)st_dco);
-    unsigned long long d = st_dims;
+    unsigned long long v0 = st_dco, v1 = st_dims, v2 = st_bytes;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
-    unsigned long long b = st_bytes;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) b += __shfl_xor_sync(0xffffffffu, b, off);
+    for (int off = 16; off > 0; off >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, off);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, off);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, off);
+    }
     if (lane == 0 && a.counters) {
-        atomicAdd(a.counters + 0, st_dco);
-        atomicAdd(a.counters + 1, d);
-        atomicAdd(a.counters + 2, b);
+        atomicAdd(a.counters + 0, v0);
+        atomicAdd(a.counters + 1, v1);
+        atomicAdd(a.counters + 2, v2);
     }
 }
 
@@ -474,9 +466,8 @@ merge_segments_kernel(const uint64_t* __restrict__ seg_keys, const uint32_t* __r
         const uint64_t* src = seg_keys + seg * K;
         for (uint32_t b0 = 0; b0 < cnt; b0 += 256) {
             const uint32_t m = min(256u, cnt - b0);
-            // early out: the batch starts above a full list's worst key
             const uint32_t cur = *reinterpret_cast<volatile uint32_t*>(cA);
-            if (cur == K && src[b0] > A[K - 1]) break;
+            if (cur == K && src[b0] > A[K - 1]) break;  // batch starts above a full list's worst
             for (uint32_t e = lane; e < m; e += 32) B[e] = src[b0 + e];
             __syncwarp();
             warp_merge(A, cA, K, B, m, true);
@@ -504,16 +495,14 @@ merge_blocks_kernel(const uint64_t* __restrict__ keys, uint32_t G, uint32_t nq, 
         const uint64_t* src = keys + ((size_t)g * nq + q) * K;
         for (uint32_t b0 = 0; b0 < K; b0 += 256) {
             const uint32_t m0 = min(256u, K - b0);
-            uint32_t m = 0;
+            uint32_t nonempty = 0;
             for (uint32_t e = lane; e < m0; e += 32) {
                 const uint64_t v = src[b0 + e];
                 B[e] = v;
+                nonempty += v != kEmptyKey;
             }
             __syncwarp();
-            // count of non-empty keys (sorted, empties at the end)
-            uint32_t nonempty = 0;
-            for (uint32_t e = lane; e < m0; e += 32) nonempty += B[e] != kEmptyKey;
-            m = __reduce_add_sync(0xffffffffu, nonempty);
+            const uint32_t m = __reduce_add_sync(0xffffffffu, nonempty);
             if (m == 0) break;
             warp_merge(A, cA, K, B, m, true);
             __syncwarp();
@@ -544,11 +533,11 @@ __global__ void keys_to_results_kernel(const uint64_t* __restrict__ keys, const 
 
 }  // namespace
 
-size_t scan_smem_bytes(int n_ckpt) { return smem_layout(n_ckpt).total; }
+size_t scan_smem_bytes(int n_ckpt, int d_res) { return smem_layout(n_ckpt, d_res).total; }
 
 cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, uint32_t grid, bool sqrt_key,
                         cudaStream_t s) {
-    const size_t smem = scan_smem_bytes(ct.n_ckpt);
+    const size_t smem = scan_smem_bytes(ct.n_ckpt, ct.d_res);
     if (grid == 0) return cudaSuccess;
     if (sqrt_key) {
         DADE_CUDA_TRY(cudaFuncSetAttribute(dco_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
