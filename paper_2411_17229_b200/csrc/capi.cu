@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -117,7 +118,18 @@ ChunkTable make_chunks(uint32_t dim, const std::vector<uint32_t>& cps) {
     for (int c = 0; c < n; ++c) al = al && (ct.end[c] & 3u) == 0;
     ct.vec_ok = al ? 1 : 0;
     const uint32_t dense_dims = ct.end[ct.n_dense - 1];
-    ct.d_res = (al && dense_dims * kQC * 4 <= (uint32_t)kMaxResidentQBytes) ? (int)dense_dims : 0;
+    ct.d_res = (al && dense_dims * kQS * 4 <= (uint32_t)kMaxResidentQBytes) ? (int)dense_dims : 0;
+    // Tensor-core first-slice filter: needs checkpoints, resident queries and
+    // dense chunk widths that are multiples of the MMA k (8).
+    bool tc = ct.n_dense < ct.n_chunks && ct.d_res > 0;
+    for (int c = 0; c < ct.n_dense; ++c) {
+        const uint32_t lo = c == 0 ? 0u : ct.end[c - 1];
+        tc = tc && ((ct.end[c] - lo) % 8u) == 0;
+    }
+    const char* env = std::getenv("DADE_GPU_NO_TC");
+    if (env && env[0] == '1') tc = false;
+    ct.use_tc = tc ? 1 : 0;
+    ct.n_buf = tc ? ct.n_dense + 1 : 2;
     return ct;
 }
 
@@ -344,6 +356,10 @@ void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t
     const uint32_t qchunks = (nq + kQC - 1) / kQC;
     const uint32_t max_blocks = (c->b_count + kRT - 1) / kRT;
     uint32_t nb = std::max<uint32_t>(1, std::min<uint32_t>(max_blocks, (1184 + qchunks - 1) / qchunks));
+    // test hook: a fixed row-block count (1 => each query's scan is one
+    // sequential CTA, hence deterministic)
+    if (const char* fb = std::getenv("DADE_GPU_FLAT_BLOCKS"))
+        nb = std::max<uint32_t>(1, std::min<uint32_t>(max_blocks, (uint32_t)std::atoi(fb)));
     uint32_t block = (c->b_count + nb - 1) / nb;
     block = (block + kRT - 1) / kRT * kRT;
     nb = (c->b_count + block - 1) / block;

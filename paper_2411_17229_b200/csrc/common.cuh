@@ -13,6 +13,7 @@ constexpr int kRT = 128;       // candidate rows per tile
 constexpr int kQC = 64;        // queries per work item (query chunk)
 constexpr int kCH = 32;        // dims per staged chunk
 constexpr int kOStride = kCH + 4;  // padded o-tile row (floats): conflict-free LDS.128
+constexpr int kQS = kQC + 8;       // padded k-major query row: conflict-free MMA B loads
 constexpr int kSparseCap = 2048;   // survivor-list capacity (25 % of kRT * kQC)
 constexpr int kMaxChunks = 256;    // dim up to ~4096 with kCH = 32 plus checkpoints
 
@@ -34,12 +35,16 @@ struct WorkItem {
 // checkpoint; all chunks without checkpoints). d_res > 0: the queries' first
 // d_res dims stay resident in shared memory. vec_ok: every boundary is a
 // multiple of 4 (16-byte staging and loads).
+// use_tc: the dense phase runs as a TF32 tensor-core filter (see scan.cu);
+// n_buf: o-tile ring depth (n_dense + 1 with the filter, else 2).
 struct ChunkTable {
     int n_chunks;
     int n_ckpt;
     int n_dense;
     int d_res;
     int vec_ok;
+    int use_tc;
+    int n_buf;
     uint16_t end[kMaxChunks];
     int16_t ckpt[kMaxChunks];
 };

@@ -32,7 +32,7 @@ struct ScanArgs {
     unsigned long long* counters;  // [3] total_dco, dims_accumulated, bytes
 };
 
-size_t scan_smem_bytes(int n_ckpt, int d_res);
+size_t scan_smem_bytes(int n_ckpt, int d_res, int n_buf);
 cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, uint32_t grid, bool sqrt_key,
                         cudaStream_t s);
 cudaError_t launch_merge_segments(const uint64_t* seg_keys, const uint32_t* seg_count, uint32_t nq,

@@ -37,18 +37,28 @@ namespace {
 
 constexpr int kWarpList = 256;  // survivor-list entries per warp per round
 
+// Relative error budget of the TF32 filter: |p~ - acc| <= kTcDelta * (|o|^2 + |q|^2)
+// over the first slice. Derivation: TF32 inputs (cvt.rna,
+// 2^-11 relative each) give a dot-product error <= (2^-10 + 2^-22) sum|o_k q_k|
+// <= 5e-4 (|o|^2 + |q|^2); tensor-core fp32 accumulation of 8-term steps and
+// the fp32 norms / combination add < 1e-5; the exact sequential fp32 partial
+// differs from the real distance by < 32 * 3 * 2^-24 relative (< 1e-5 of
+// (|o| + |q|)^2). 2e-3 leaves a > 3x margin.
+constexpr float kTcDelta = 2e-3f;
+
 struct SmemLayout {
-    size_t o_buf, q_res, q_stage, r_s, thr_s, qidx, slot, wl_meta, wl_acc, keys, total;
+    size_t o_buf, q_res, q_stage, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, keys, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline SmemLayout smem_layout(int n_ckpt, int d_res) {
+__host__ __device__ inline SmemLayout smem_layout(int n_ckpt, int d_res, int n_buf) {
     SmemLayout L;
     size_t off = 0;
-    L.o_buf = off; off = align16(off + sizeof(float) * 2 * kRT * kOStride);
-    L.q_res = off; off = align16(off + sizeof(float) * (size_t)d_res * kQC);
-    L.q_stage = off; off = align16(off + (d_res == 0 ? sizeof(float) * kCH * kQC : 0));
+    L.o_buf = off; off = align16(off + sizeof(float) * (size_t)n_buf * kRT * kOStride);
+    L.q_res = off; off = align16(off + sizeof(float) * (size_t)d_res * kQS);
+    L.q_stage = off; off = align16(off + (d_res == 0 ? sizeof(float) * kCH * kQS : 0));
+    L.n_q = off; off = align16(off + sizeof(float) * kQC);
     L.r_s = off; off = align16(off + sizeof(float) * kQC);
     L.thr_s = off; off = align16(off + sizeof(float) * kQC * (n_ckpt > 0 ? n_ckpt : 1));
     L.qidx = off; off = align16(off + sizeof(uint32_t) * kQC);
@@ -71,6 +81,22 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, boo
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+// D += A(16x8, row) * B(8x8, col), TF32 in, FP32 accumulate.
+__device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 
 // Recompute query j's per-checkpoint float thresholds from r_s[j].
 __device__ __forceinline__ void refresh_thr(float* thr_s, const float* r_s, const double* coeff,
@@ -102,16 +128,80 @@ __device__ __forceinline__ void merge_query(const ScanArgs& a, uint64_t* kb, uin
     __syncwarp();
 }
 
-template <bool kSqrtKey>
+// Gather query jj's candidates of the warp list (meta bit 31) into kb and merge.
+__device__ __forceinline__ void merge_list_candidates(const ScanArgs& a, const uint32_t* wl_meta,
+                                                      const float* wl_acc, uint32_t n, uint64_t* kb,
+                                                      uint32_t row_base, int warp, int lane,
+                                                      const uint32_t* qidx_s, const uint32_t* slot_s,
+                                                      float* r_s, float* thr_s, int n_ckpt,
+                                                      unsigned long long& st_bytes) {
+    for (int jj = 0; jj < 8; ++jj) {
+        uint32_t m = 0;
+        for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            bool is = false;
+            uint32_t meta = 0;
+            if (e < n) {
+                meta = wl_meta[e];
+                is = (meta & 0x80000000u) && ((meta >> 8) & 0xffu) == (uint32_t)jj;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, is);
+            if (is) {
+                const uint32_t g = row_base + (meta & 0xffu);
+                const uint32_t id = a.row_ids ? __ldg(a.row_ids + g) : a.id_base + g;
+                kb[m + __popc(bal & ((1u << lane) - 1u))] = make_key(wl_acc[e], id);
+            }
+            m += __popc(bal);
+        }
+        __syncwarp();
+        if (m) {
+            if (a.row_ids && lane == 0) st_bytes += 4ull * m;
+            merge_query(a, kb, m, warp * 8 + jj, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane);
+        }
+    }
+}
+
+// Compact this lane's `pending` pair bits into the warp list (up to kWarpList
+// per round); pair bit b -> (row, jj) via decode. Returns the round size.
+template <class Decode, class AccOf>
+__device__ __forceinline__ uint32_t compact_round(uint32_t& pending, uint32_t* wl_meta, float* wl_acc, int lane,
+                                                  Decode decode, AccOf acc_of) {
+    const uint32_t mine = __popc(pending);
+    uint32_t incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+    }
+    uint32_t pos = incl - mine;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t bits = pending;
+    while (bits && pos < (uint32_t)kWarpList) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        uint32_t row, jj;
+        decode(b, row, jj);
+        wl_meta[pos] = row | (jj << 8);
+        wl_acc[pos] = acc_of(b);
+        pending &= ~(1u << b);
+        ++pos;
+    }
+    __syncwarp();
+    return min(total, (uint32_t)kWarpList);
+}
+
+template <bool kSqrtKey, bool kTC>
 __global__ void __launch_bounds__(kThreads, 2)
 dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int n_ckpt = ct.n_ckpt;
     const int d_res = ct.d_res;  // resident query dims (0 -> stage per chunk)
-    const SmemLayout L = smem_layout(n_ckpt, d_res);
+    const int n_buf = ct.n_buf;
+    const SmemLayout L = smem_layout(n_ckpt, d_res, n_buf);
     float* o_buf = reinterpret_cast<float*>(smem + L.o_buf);
     float* q_res = reinterpret_cast<float*>(smem + L.q_res);
     float* q_stage = reinterpret_cast<float*>(smem + L.q_stage);
+    float* n_q = reinterpret_cast<float*>(smem + L.n_q);
     float* r_s = reinterpret_cast<float*>(smem + L.r_s);
     float* thr_s = reinterpret_cast<float*>(smem + L.thr_s);
     uint32_t* qidx_s = reinterpret_cast<uint32_t*>(smem + L.qidx);
@@ -151,10 +241,16 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
     if (tid < kQC && tid >= (int)qcount) { qidx_s[tid] = 0; slot_s[tid] = 0; }
     if (tid < kQC) r_s[tid] = __int_as_float(0x7f800000);
     __syncthreads();
-    // resident queries, k-major [d_res][kQC]
+    // resident queries, k-major [d_res][kQS]
     for (uint32_t idx = tid; idx < (uint32_t)d_res * kQC; idx += kThreads) {
         const uint32_t j = idx / d_res, k = idx - j * d_res;
-        q_res[k * kQC + j] = j < qcount ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k) : 0.f;
+        q_res[k * kQS + j] = j < qcount ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k) : 0.f;
+    }
+    __syncthreads();
+    if (kTC && tid < kQC) {  // first-slice query norms for the filter bound
+        float nq = 0.f;
+        for (int k = 0; k < d_res; ++k) nq = fmaf(q_res[k * kQS + tid], q_res[k * kQS + tid], nq);
+        n_q[tid] = nq;
     }
 
     unsigned long long st_dco = 0, st_dims = 0, st_bytes = 0;
@@ -162,17 +258,19 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
     const uint64_t nz2 = a.neg_zero2;
     const int c_dense = ct.n_dense;
     const bool has_sparse = c_dense < ct.n_chunks;
+    const uint32_t d0 = ct.end[c_dense - 1];
     const uint32_t n_tiles = (row_count + kRT - 1) / kRT;
     const uint32_t n_steps = n_tiles * c_dense;
-    const bool vec = (dim & 3u) == 0 && ct.vec_ok;
+    const bool vec = ct.vec_ok != 0;
+    const int g = lane >> 2, tq = lane & 3;  // MMA fragment coordinates
 
-    // stage the o tile of step s into buffer (s & 1)
+    // stage the o tile of step s into ring slot (s % n_buf)
     auto issue = [&](uint32_t s) {
         const uint32_t t = s / c_dense, c = s - t * c_dense;
         const uint32_t tb = t * kRT, nrows = min((uint32_t)kRT, row_count - tb);
         const uint32_t k0 = c == 0 ? 0u : ct.end[c - 1];
         const uint32_t w = ct.end[c] - k0;
-        float* buf = o_buf + (s & 1) * (kRT * kOStride);
+        float* buf = o_buf + (s % n_buf) * (kRT * kOStride);
         if (vec) {
             const uint32_t v4 = w >> 2;
             for (uint32_t idx = tid; idx < kRT * v4; idx += kThreads) {
@@ -196,7 +294,8 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
 
     if (n_steps > 0) issue(0);
 
-    uint64_t acc[4][4];
+    uint64_t acc[4][4];      // SIMT dense accumulators (kTC == false)
+    float tcd[8][4];         // MMA accumulators: 8 m-tiles of 16 rows x this warp's 8 queries
     uint32_t alive = 0;
     for (uint32_t s = 0; s < n_steps; ++s) {
         const uint32_t t = s / c_dense;
@@ -205,6 +304,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
         const uint32_t k0 = c == 0 ? 0u : ct.end[c - 1];
         const uint32_t w = ct.end[c] - k0;
         const uint32_t w4 = (w + 3) & ~3u;
+        const uint32_t my_q = (uint32_t)max(0, min(8, (int)qcount - warp * 8));
         if (c == 0) {
             // tile start: pick up radii tightened by other CTAs; reset the pairs
             if (lane < 8) {
@@ -218,31 +318,38 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                 }
             }
             __syncwarp();
+            if (lane == 0) st_dco += (unsigned long long)nrows * my_q;
+            if constexpr (kTC) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+                for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
-                for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
-            alive = 0;
+                    for (int v = 0; v < 4; ++v) tcd[mt][v] = 0.f;
+            } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj)
-                    if ((uint32_t)(lane + 32 * i) < nrows && (uint32_t)(warp * 8 + jj) < qcount)
-                        alive |= 1u << (i * 8 + jj);
-            st_dco += __popc(alive);
+                    for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
+                alive = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj)
+                        if ((uint32_t)(lane + 32 * i) < nrows && (uint32_t)jj < my_q)
+                            alive |= 1u << (i * 8 + jj);
+            }
         }
         cp_async_wait_all();
-        __syncthreads();  // tile s visible to all; everyone done with tile s-1's buffer
+        __syncthreads();  // tile s visible to all; everyone done with the slot being refilled
         if (s + 1 < n_steps) issue(s + 1);
-        const float* buf = o_buf + (s & 1) * (kRT * kOStride);
+        const float* buf = o_buf + (s % n_buf) * (kRT * kOStride);
         const float* qk;
         if (d_res > 0) {
-            qk = q_res + k0 * kQC;
+            qk = q_res + k0 * kQS;
         } else {
             // non-resident queries: stage this chunk's slice (k-major)
             for (uint32_t idx = tid; idx < kQC * w4; idx += kThreads) {
                 const uint32_t j = idx / w4, cc = idx - j * w4;
-                q_stage[cc * kQC + j] =
+                q_stage[cc * kQS + j] =
                     (j < qcount && cc < w) ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k0 + cc) : 0.f;
             }
             __syncthreads();
@@ -250,23 +357,39 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
             if (tid == 0) st_bytes += 4ull * w * qcount;
         }
 
-        // ---- dense register-tiled update -------------------------------------
-        if (__any_sync(0xffffffffu, alive != 0)) {
-            for (uint32_t k4 = 0; k4 < w4; k4 += 4) {
-                float4 o[4];
+        if constexpr (kTC) {
+            // ---- tensor-core dot products o . q over this chunk ----------------
+            if (my_q > 0) {
+                for (uint32_t ks = 0; ks < w; ks += 8) {
+                    const uint32_t b0 = to_tf32(qk[(ks + tq) * kQS + warp * 8 + g]);
+                    const uint32_t b1 = to_tf32(qk[(ks + tq + 4) * kQS + warp * 8 + g]);
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    o[i] = *reinterpret_cast<const float4*>(buf + (lane + 32 * i) * kOStride + k4);
+                    for (int mt = 0; mt < 8; ++mt) {
+                        const float* r0 = buf + (mt * 16 + g) * kOStride + ks + tq;
+                        const float* r1 = r0 + 8 * kOStride;
+                        mma_tf32(tcd[mt], to_tf32(r0[0]), to_tf32(r1[0]), to_tf32(r0[4]), to_tf32(r1[4]), b0, b1);
+                    }
+                }
+            }
+        } else {
+            // ---- dense register-tiled exact update ----------------------------
+            if (__any_sync(0xffffffffu, alive != 0)) {
+                for (uint32_t k4 = 0; k4 < w4; k4 += 4) {
+                    float4 o[4];
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const ulonglong2 qa = *reinterpret_cast<const ulonglong2*>(qk + (k4 + kk) * kQC + warp * 8);
-                    const ulonglong2 qb = *reinterpret_cast<const ulonglong2*>(qk + (k4 + kk) * kQC + warp * 8 + 4);
-                    const uint64_t qp[4] = {qa.x, qa.y, qb.x, qb.y};
+                    for (int i = 0; i < 4; ++i)
+                        o[i] = *reinterpret_cast<const float4*>(buf + (lane + 32 * i) * kOStride + k4);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float ov = kk == 0 ? o[i].x : kk == 1 ? o[i].y : kk == 2 ? o[i].z : o[i].w;
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const ulonglong2 qa = *reinterpret_cast<const ulonglong2*>(qk + (k4 + kk) * kQS + warp * 8);
+                        const ulonglong2 qb = *reinterpret_cast<const ulonglong2*>(qk + (k4 + kk) * kQS + warp * 8 + 4);
+                        const uint64_t qp[4] = {qa.x, qa.y, qb.x, qb.y};
 #pragma unroll
-                        for (int p = 0; p < 4; ++p) acc[i][p] = sq_step2(acc[i][p], ov, qp[p], nz2);
+                        for (int i = 0; i < 4; ++i) {
+                            const float ov = kk == 0 ? o[i].x : kk == 1 ? o[i].y : kk == 2 ? o[i].z : o[i].w;
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) acc[i][p] = sq_step2(acc[i][p], ov, qp[p], nz2);
+                        }
                     }
                 }
             }
@@ -275,8 +398,52 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
 
         // ---- end of the dense phase for this tile (warp-local from here) ------
         const int ck = ct.ckpt[c];
-        uint32_t cand = 0;  // dense candidate bits (FD: no sparse phase)
-        if (has_sparse) {
+        const uint32_t row_base = row_start + tb;
+        uint32_t pending = 0;  // pairs needing the exact / sparse path
+        bool from_prefix = false;
+        if constexpr (kTC) {
+            // first-slice squared norms of this lane's rows l + 32i (exact enough: fma)
+            float no_reg[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) no_reg[i] = 0.f;
+            for (int cc = 0; cc < c_dense; ++cc) {
+                const float* bc = o_buf + ((s - (c_dense - 1) + cc) % n_buf) * (kRT * kOStride);
+                const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], wc = ct.end[cc] - lo;
+                for (uint32_t k4 = 0; k4 < wc; k4 += 4) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float4 v = *reinterpret_cast<const float4*>(bc + (lane + 32 * i) * kOStride + k4);
+                        no_reg[i] = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, no_reg[i]))));
+                    }
+                }
+            }
+            // filter: prune for sure iff p~ - delta > thr; everything else is decided exactly
+            uint32_t valid = 0;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int rb = mt * 16 + 8 * h;
+                    const float no = __shfl_sync(0xffffffffu, no_reg[rb >> 5], (rb + g) & 31);
+                    const uint32_t row = rb + g;
+#pragma unroll
+                    for (int cq = 0; cq < 2; ++cq) {
+                        const uint32_t jj = 2 * tq + cq;
+                        if (row < nrows && jj < my_q) {
+                            const int j = warp * 8 + jj;
+                            const float nq = n_q[j];
+                            const float pt = no + nq - 2.f * tcd[mt][2 * h + cq];
+                            const float delta = kTcDelta * (no + nq);
+                            const uint32_t bit = 1u << (mt * 4 + h * 2 + cq);
+                            valid |= bit;
+                            if (!(pt - delta > thr_s[j * n_ckpt + ck])) pending |= bit;
+                        }
+                    }
+                }
+            }
+            st_dims += (unsigned long long)__popc(valid & ~pending) * d0;
+            from_prefix = true;
+        } else if (has_sparse) {
             uint32_t dead = 0;
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
@@ -291,8 +458,11 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
             dead &= alive;
             alive &= ~dead;
             st_dims += (unsigned long long)__popc(dead) * ct.end[c];
+            pending = alive;
         } else {
+            // FD: candidates straight from registers, one query at a time
             st_dims += (unsigned long long)__popc(alive) * dim;
+            uint32_t cand = 0;
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
                 const float r = r_s[warp * 8 + jj];
@@ -304,11 +474,6 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                     if (((alive >> (i * 8 + jj)) & 1u) && !(key > r)) cand |= 1u << (i * 8 + jj);
                 }
             }
-            alive = 0;
-        }
-
-        if (!has_sparse) {
-            // FD: candidates straight from registers, one query at a time
             if (__any_sync(0xffffffffu, cand != 0)) {
                 for (int jj = 0; jj < 8; ++jj) {
                     const uint32_t j = warp * 8 + jj;
@@ -320,8 +485,8 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                         if (is) {
                             const uint64_t v = acc[i][jj >> 1];
                             const float x = (jj & 1) ? hi_f(v) : lo_f(v);
-                            const uint32_t g = row_start + tb + lane + 32 * i;
-                            const uint32_t id = a.row_ids ? __ldg(a.row_ids + g) : a.id_base + g;
+                            const uint32_t gr = row_base + lane + 32 * i;
+                            const uint32_t id = a.row_ids ? __ldg(a.row_ids + gr) : a.id_base + gr;
                             kb[m + __popc(bal & ((1u << lane) - 1u))] = make_key(kSqrtKey ? __fsqrt_rn(x) : x, id);
                         }
                         m += __popc(bal);
@@ -336,59 +501,76 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
             continue;
         }
 
-        // ---- sparse rounds: compact, advance from global, merge ---------------
-        uint32_t pending = alive;
+        // ---- sparse rounds: compact, advance exactly, merge --------------------
         while (__any_sync(0xffffffffu, pending != 0)) {
-            const uint32_t mine = __popc(pending);
-            uint32_t incl = mine;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += y;
+            uint32_t n;
+            if constexpr (kTC) {
+                n = compact_round(
+                    pending, wl_meta, wl_acc, lane,
+                    [&](int b, uint32_t& row, uint32_t& jj) {
+                        row = (b >> 2) * 16 + ((b >> 1) & 1) * 8 + g;
+                        jj = 2 * tq + (b & 1);
+                    },
+                    [&](int) { return 0.f; });
+            } else {
+                n = compact_round(
+                    pending, wl_meta, wl_acc, lane,
+                    [&](int b, uint32_t& row, uint32_t& jj) {
+                        row = lane + 32 * (b >> 3);
+                        jj = b & 7;
+                    },
+                    [&](int b) {
+                        const uint64_t v = acc[b >> 3][(b & 7) >> 1];
+                        return (b & 1) ? hi_f(v) : lo_f(v);
+                    });
             }
-            uint32_t pos = incl - mine;
-            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-            const uint32_t n = min(total, (uint32_t)kWarpList);
-            uint32_t bits = pending;
-            while (bits && pos < (uint32_t)kWarpList) {
-                const int b = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const int i = b >> 3, jj = b & 7;
-                const uint64_t v = acc[i][jj >> 1];
-                wl_meta[pos] = (uint32_t)(lane + 32 * i) | ((uint32_t)jj << 8);
-                wl_acc[pos] = (jj & 1) ? hi_f(v) : lo_f(v);
-                pending &= ~(1u << b);
-                ++pos;
-            }
-            __syncwarp();
-            // advance each survivor through the remaining chunks (one per lane)
+            // one pair per lane: [exact dense prefix from smem] + remaining chunks from L2
             for (uint32_t e = lane; e < n; e += 32) {
-                uint32_t meta = wl_meta[e];
+                const uint32_t meta = wl_meta[e];
                 float x = wl_acc[e];
                 const uint32_t row = meta & 0xffu, jj = (meta >> 8) & 0xffu, j = warp * 8 + jj;
-                const float* orow = a.storage + (size_t)(row_start + tb + row) * dim;
-                const float* qrow = a.queries + (size_t)qidx_s[j] * dim;
                 bool live = true;
-                for (int cc = c_dense; cc < ct.n_chunks; ++cc) {
-                    const uint32_t lo = ct.end[cc - 1], hi = ct.end[cc];
-                    if (vec) {
-                        for (uint32_t kk = lo; kk < hi; kk += 4) {
-                            const float4 o4 = __ldg(reinterpret_cast<const float4*>(orow + kk));
-                            const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + kk));
-                            x = sq_step(x, o4.x, q4.x);
-                            x = sq_step(x, o4.y, q4.y);
-                            x = sq_step(x, o4.z, q4.z);
-                            x = sq_step(x, o4.w, q4.w);
+                if (from_prefix) {
+                    for (int cc = 0; cc < c_dense; ++cc) {
+                        const float* bc = o_buf + ((s - (c_dense - 1) + cc) % n_buf) * (kRT * kOStride) + row * kOStride;
+                        const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
+                        for (uint32_t k = lo; k < hi; k += 4) {
+                            const float4 o4 = *reinterpret_cast<const float4*>(bc + (k - lo));
+                            x = sq_step(x, o4.x, q_res[(k + 0) * kQS + j]);
+                            x = sq_step(x, o4.y, q_res[(k + 1) * kQS + j]);
+                            x = sq_step(x, o4.z, q_res[(k + 2) * kQS + j]);
+                            x = sq_step(x, o4.w, q_res[(k + 3) * kQS + j]);
                         }
-                    } else {
-                        for (uint32_t kk = lo; kk < hi; ++kk) x = sq_step(x, __ldg(orow + kk), __ldg(qrow + kk));
                     }
-                    st_bytes += 8ull * (hi - lo);
-                    const int k2 = ct.ckpt[cc];
-                    if (k2 >= 0 && x > thr_s[j * n_ckpt + k2]) {
-                        st_dims += hi;
+                    if (x > thr_s[j * n_ckpt + ck]) {
+                        st_dims += d0;
                         live = false;
-                        break;
+                    }
+                }
+                if (live) {
+                    const float* orow = a.storage + (size_t)(row_base + row) * dim;
+                    const float* qrow = a.queries + (size_t)qidx_s[j] * dim;
+                    for (int cc = c_dense; cc < ct.n_chunks; ++cc) {
+                        const uint32_t lo = ct.end[cc - 1], hi = ct.end[cc];
+                        if (vec) {
+                            for (uint32_t kk = lo; kk < hi; kk += 4) {
+                                const float4 o4 = __ldg(reinterpret_cast<const float4*>(orow + kk));
+                                const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + kk));
+                                x = sq_step(x, o4.x, q4.x);
+                                x = sq_step(x, o4.y, q4.y);
+                                x = sq_step(x, o4.z, q4.z);
+                                x = sq_step(x, o4.w, q4.w);
+                            }
+                        } else {
+                            for (uint32_t kk = lo; kk < hi; ++kk) x = sq_step(x, __ldg(orow + kk), __ldg(qrow + kk));
+                        }
+                        st_bytes += 8ull * (hi - lo);
+                        const int k2 = ct.ckpt[cc];
+                        if (k2 >= 0 && x > thr_s[j * n_ckpt + k2]) {
+                            st_dims += hi;
+                            live = false;
+                            break;
+                        }
                     }
                 }
                 bool is_cand = false;
@@ -402,31 +584,8 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                 wl_acc[e] = x;
             }
             __syncwarp();
-            // per query: gather candidate keys, merge
-            for (int jj = 0; jj < 8; ++jj) {
-                uint32_t m = 0;
-                for (uint32_t e0 = 0; e0 < n; e0 += 32) {
-                    const uint32_t e = e0 + lane;
-                    bool is = false;
-                    uint32_t meta = 0;
-                    if (e < n) {
-                        meta = wl_meta[e];
-                        is = (meta & 0x80000000u) && ((meta >> 8) & 0xffu) == (uint32_t)jj;
-                    }
-                    const uint32_t bal = __ballot_sync(0xffffffffu, is);
-                    if (is) {
-                        const uint32_t g = row_start + tb + (meta & 0xffu);
-                        const uint32_t id = a.row_ids ? __ldg(a.row_ids + g) : a.id_base + g;
-                        kb[m + __popc(bal & ((1u << lane) - 1u))] = make_key(wl_acc[e], id);
-                    }
-                    m += __popc(bal);
-                }
-                __syncwarp();
-                if (m) {
-                    if (a.row_ids && lane == 0) st_bytes += 4ull * m;
-                    merge_query(a, kb, m, warp * 8 + jj, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane);
-                }
-            }
+            merge_list_candidates(a, wl_meta, wl_acc, n, kb, row_base, warp, lane, qidx_s, slot_s, r_s, thr_s,
+                                  n_ckpt, st_bytes);
         }
     }  // steps
 
@@ -533,20 +692,24 @@ __global__ void keys_to_results_kernel(const uint64_t* __restrict__ keys, const 
 
 }  // namespace
 
-size_t scan_smem_bytes(int n_ckpt, int d_res) { return smem_layout(n_ckpt, d_res).total; }
+size_t scan_smem_bytes(int n_ckpt, int d_res, int n_buf) { return smem_layout(n_ckpt, d_res, n_buf).total; }
+
+template <bool kSqrtKey, bool kTC>
+static cudaError_t launch_scan_t(const ScanArgs& a, const ChunkTable& ct, uint32_t grid, size_t smem, cudaStream_t s) {
+    DADE_CUDA_TRY(cudaFuncSetAttribute(dco_scan_kernel<kSqrtKey, kTC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    dco_scan_kernel<kSqrtKey, kTC><<<grid, kThreads, smem, s>>>(a, ct);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, uint32_t grid, bool sqrt_key,
                         cudaStream_t s) {
-    const size_t smem = scan_smem_bytes(ct.n_ckpt, ct.d_res);
     if (grid == 0) return cudaSuccess;
-    if (sqrt_key) {
-        DADE_CUDA_TRY(cudaFuncSetAttribute(dco_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dco_scan_kernel<true><<<grid, kThreads, smem, s>>>(a, ct);
-    } else {
-        DADE_CUDA_TRY(cudaFuncSetAttribute(dco_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dco_scan_kernel<false><<<grid, kThreads, smem, s>>>(a, ct);
-    }
-    return cudaGetLastError();
+    const size_t smem = scan_smem_bytes(ct.n_ckpt, ct.d_res, ct.n_buf);
+    if (sqrt_key) return ct.use_tc ? launch_scan_t<true, true>(a, ct, grid, smem, s)
+                                   : launch_scan_t<true, false>(a, ct, grid, smem, s);
+    return ct.use_tc ? launch_scan_t<false, true>(a, ct, grid, smem, s)
+                     : launch_scan_t<false, false>(a, ct, grid, smem, s);
 }
 
 cudaError_t launch_merge_segments(const uint64_t* seg_keys, const uint32_t* seg_count, uint32_t nq,
