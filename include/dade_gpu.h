@@ -161,6 +161,10 @@ int dade_gpu_calibrate(dade_gpu_ctx* ctx, const float* data, uint32_t n, double 
                        uint32_t delta_d, uint64_t n_pairs, uint64_t seed, uint32_t flags,
                        uint32_t* checkpoints, double* epsilons, uint32_t* n_out);
 
+/* Debug: the last scan's device counters [0..7] (total_dco, dims, bytes, ...)
+ * and, with DADE_GPU_PHASES=1 in the environment, per-phase clock sums [8..15]. */
+int dade_gpu_debug_counters(dade_gpu_ctx* ctx, uint64_t* out16);
+
 /* Number of CUDA kernels this handle launched so far (bench evidence). */
 uint64_t dade_gpu_launch_count(dade_gpu_ctx* ctx);
 

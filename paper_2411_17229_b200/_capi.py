@@ -74,6 +74,7 @@ def _load():
         "dade_gpu_partial_sums": ([P, P, P, U32, U32, P], I),
         "dade_gpu_calibrate": ([P, P, U32, D, U32, U64, U64, U32, P, P, P], I),
         "dade_gpu_launch_count": ([P], U64),
+        "dade_gpu_debug_counters": ([P, P], I),
         "dade_gpu_set_profiling": ([P, I], I),
         "dade_gpu_last_scan_profile": ([P, P, P, P], I),
     }
@@ -94,7 +95,7 @@ EXPORTED = [
     "dade_gpu_ivf_search", "dade_gpu_flat_search", "dade_gpu_ivf_search_keys",
     "dade_gpu_flat_search_keys", "dade_gpu_merge_keys", "dade_gpu_dco_evaluate",
     "dade_gpu_partial_sums", "dade_gpu_calibrate", "dade_gpu_launch_count",
-    "dade_gpu_set_profiling", "dade_gpu_last_scan_profile",
+    "dade_gpu_set_profiling", "dade_gpu_last_scan_profile", "dade_gpu_debug_counters",
 ]
 
 

@@ -129,6 +129,8 @@ ChunkTable make_chunks(uint32_t dim, const std::vector<uint32_t>& cps) {
     const char* env = std::getenv("DADE_GPU_NO_TC");
     if (env && env[0] == '1') tc = false;
     ct.use_tc = tc ? 1 : 0;
+    const char* dbg = std::getenv("DADE_GPU_DEBUG");
+    ct.debug = (dbg && dbg[0] == '1') ? 1 : 0;
     ct.n_buf = tc ? ct.n_dense + 1 : 2;
     return ct;
 }
@@ -169,7 +171,7 @@ struct dade_gpu_ctx {
     DevBuf q_in, q_rot, probes, probe_count, c_seg_keys, c_seg_count, c_r;
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts;
-    DevBuf counters;
+    DevBuf counters, phase;
 
     // profiling
     bool profiling = false;
@@ -257,6 +259,14 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
     c->launches += 3;
 }
 
+unsigned long long* phase_ptr(dade_gpu_ctx* c) {
+    const char* e = std::getenv("DADE_GPU_PHASES");
+    if (!(e && e[0] == '1')) return nullptr;
+    c->phase.ensure(64);
+    cuda_check(cudaMemsetAsync(c->phase.p, 0, 64, c->stream), "memset");
+    return c->phase.as<unsigned long long>();
+}
+
 void record(dade_gpu_ctx* c, cudaEvent_t e) {
     if (c->profiling) cuda_check(cudaEventRecord(e, c->stream), "event");
 }
@@ -341,6 +351,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     a.coeff = c->d_coeff.as<double>();
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
+    a.phase = phase_ptr(c);
     const ChunkTable ct = make_chunks(c->dim, c->cps);
     record(c, c->e1);
     cuda_check(launch_scan(a, ct, (uint32_t)max_items, true, s), "dco scan");
@@ -388,6 +399,7 @@ void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t
     a.coeff = c->d_coeff.as<double>();
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
+    a.phase = phase_ptr(c);
     const ChunkTable ct = make_chunks(c->b_dim, c->cps);
     record(c, c->e1);
     cuda_check(launch_scan(a, ct, nb * qchunks, true, s), "flat scan");
@@ -1013,6 +1025,18 @@ int dade_gpu_calibrate(dade_gpu_ctx* c, const float* data, uint32_t n, double p_
 }
 
 uint64_t dade_gpu_launch_count(dade_gpu_ctx* c) { return c ? c->launches : 0; }
+
+// Debug: the last scan's counters [0..7] and per-phase clocks [8..15].
+int dade_gpu_debug_counters(dade_gpu_ctx* c, uint64_t* out16) {
+    return guarded([&] {
+        if (!c || !out16) fail(DADE_GPU_INVALID_INPUT, "null argument");
+        c->use_device();
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        std::memset(out16, 0, 16 * sizeof(uint64_t));
+        if (c->counters.p) cuda_check(cudaMemcpy(out16, c->counters.p, 64, cudaMemcpyDeviceToHost), "D2H");
+        if (c->phase.p) cuda_check(cudaMemcpy(out16 + 8, c->phase.p, 64, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
 
 int dade_gpu_set_profiling(dade_gpu_ctx* c, int on) {
     return guarded([&] {

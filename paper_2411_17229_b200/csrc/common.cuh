@@ -45,6 +45,7 @@ struct ChunkTable {
     int vec_ok;
     int use_tc;
     int n_buf;
+    int debug;
     uint16_t end[kMaxChunks];
     int16_t ckpt[kMaxChunks];
 };

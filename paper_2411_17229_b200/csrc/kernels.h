@@ -30,6 +30,7 @@ struct ScanArgs {
     const double* coeff;     // [n_ckpt] reject coefficients
     uint64_t neg_zero2;      // 0x8000000080000000 (opaque to ptxas)
     unsigned long long* counters;  // [3] total_dco, dims_accumulated, bytes
+    unsigned long long* phase;     // nullable: per-phase clocks (debug)
 };
 
 size_t scan_smem_bytes(int n_ckpt, int d_res, int n_buf);

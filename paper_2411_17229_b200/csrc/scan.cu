@@ -109,11 +109,11 @@ __device__ __forceinline__ void refresh_thr(float* thr_s, const float* r_s, cons
 // then tighten r_s[j] / thr_s / the global radius from the new K-th key.
 __device__ __forceinline__ void merge_query(const ScanArgs& a, uint64_t* kb, uint32_t m, uint32_t j,
                                             const uint32_t* qidx_s, const uint32_t* slot_s, float* r_s,
-                                            float* thr_s, int n_ckpt, int lane) {
+                                            float* thr_s, int n_ckpt, int lane, bool tighten = true) {
     const size_t seg = (size_t)qidx_s[j] * a.n_slots + slot_s[j];
     uint64_t* A = a.seg_keys + seg * a.K;
     const uint32_t nc = warp_merge(A, a.seg_count + seg, a.K, kb, m, false);
-    if (nc == a.K) {
+    if (tighten && nc == a.K) {
         const float rn = hi_f(A[a.K - 1]);
         if (rn < r_s[j]) {
             __syncwarp();
@@ -156,9 +156,30 @@ __device__ __forceinline__ void merge_list_candidates(const ScanArgs& a, const u
         __syncwarp();
         if (m) {
             if (a.row_ids && lane == 0) st_bytes += 4ull * m;
-            merge_query(a, kb, m, warp * 8 + jj, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane);
+            merge_query(a, kb, m, warp * 8 + jj, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane, false);
         }
     }
+}
+
+// After a tile's survivor rounds: tighten the warp's 8 radii from their
+// segments' K-th keys. Decisions inside a tile all use the tile-start radii,
+// so they do not depend on how pairs were split into rounds.
+__device__ __forceinline__ void tighten_warp_radii(const ScanArgs& a, int warp, int lane, uint32_t my_q,
+                                                   const uint32_t* qidx_s, const uint32_t* slot_s, float* r_s,
+                                                   float* thr_s, int n_ckpt) {
+    if (lane < (int)my_q) {
+        const int j = warp * 8 + lane;
+        const size_t seg = (size_t)qidx_s[j] * a.n_slots + slot_s[j];
+        if (ld_volatile_u32(a.seg_count + seg) == a.K) {
+            const float rn = hi_f(*reinterpret_cast<const volatile uint64_t*>(a.seg_keys + seg * a.K + a.K - 1));
+            if (rn < r_s[j]) {
+                r_s[j] = rn;
+                atomicMin(a.r_global + qidx_s[j], __float_as_uint(rn));
+                refresh_thr(thr_s, r_s, a.coeff, n_ckpt, j, 0, 1);
+            }
+        }
+    }
+    __syncwarp();
 }
 
 // Compact this lane's `pending` pair bits into the warp list (up to kWarpList
@@ -189,6 +210,12 @@ __device__ __forceinline__ uint32_t compact_round(uint32_t& pending, uint32_t* w
     __syncwarp();
     return min(total, (uint32_t)kWarpList);
 }
+
+// Optional per-phase clock accounting (DADE_GPU_PHASES=1): lane 0 of every
+// warp adds its clock64 deltas into a.phase[0..4] = {wait+barrier, dense,
+// epilogue, survivors, merges}.
+#define PH_MARK(t) const long long t = a.phase ? clock64() : 0
+#define PH_ADD(i, t0, t1) do { if (a.phase && lane == 0) atomicAdd(a.phase + (i), (unsigned long long)((t1) - (t0))); } while (0)
 
 template <bool kSqrtKey, bool kTC>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -338,8 +365,11 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                             alive |= 1u << (i * 8 + jj);
             }
         }
+        PH_MARK(t_w0);
         cp_async_wait_all();
         __syncthreads();  // tile s visible to all; everyone done with the slot being refilled
+        PH_MARK(t_w1);
+        PH_ADD(0, t_w0, t_w1);
         if (s + 1 < n_steps) issue(s + 1);
         const float* buf = o_buf + (s % n_buf) * (kRT * kOStride);
         const float* qk;
@@ -394,6 +424,8 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                 }
             }
         }
+        PH_MARK(t_d1);
+        PH_ADD(1, t_w1, t_d1);
         if (c != c_dense - 1) continue;
 
         // ---- end of the dense phase for this tile (warp-local from here) ------
@@ -437,6 +469,23 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                             const uint32_t bit = 1u << (mt * 4 + h * 2 + cq);
                             valid |= bit;
                             if (!(pt - delta > thr_s[j * n_ckpt + ck])) pending |= bit;
+                            else if (ct.debug) {
+                                // debug: the filter's prune must agree with the exact prefix
+                                float xx = 0.f;
+                                for (int cc = 0; cc < c_dense; ++cc) {
+                                    const float* bc = o_buf + ((s - (c_dense - 1) + cc) % n_buf) * (kRT * kOStride) + row * kOStride;
+                                    const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
+                                    for (uint32_t k = lo; k < hi; ++k) xx = sq_step(xx, bc[k - lo], q_res[k * kQS + j]);
+                                }
+                                if (!(xx > thr_s[j * n_ckpt + ck])) {
+                                    atomicAdd(a.counters + 3, 1ull);
+                                    if (a.counters[4] == 0) {
+                                        a.counters[4] = 1;
+                                        printf("TC VIOLATION row %u j %d pt %.6g delta %.6g exact %.6g thr %.6g no %.6g nq %.6g dot %.6g\n",
+                                               row, j, pt, delta, xx, thr_s[j * n_ckpt + ck], no, nq, tcd[mt][2 * h + cq]);
+                                    }
+                                }
+                            }
                         }
                     }
                 }
@@ -501,8 +550,11 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
             continue;
         }
 
+        PH_MARK(t_e1);
+        PH_ADD(2, t_d1, t_e1);
         // ---- sparse rounds: compact, advance exactly, merge --------------------
         while (__any_sync(0xffffffffu, pending != 0)) {
+            PH_MARK(t_r0);
             uint32_t n;
             if constexpr (kTC) {
                 n = compact_round(
@@ -584,9 +636,14 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                 wl_acc[e] = x;
             }
             __syncwarp();
+            PH_MARK(t_r1);
+            PH_ADD(3, t_r0, t_r1);
             merge_list_candidates(a, wl_meta, wl_acc, n, kb, row_base, warp, lane, qidx_s, slot_s, r_s, thr_s,
                                   n_ckpt, st_bytes);
+            PH_MARK(t_r2);
+            PH_ADD(4, t_r1, t_r2);
         }
+        tighten_warp_radii(a, warp, lane, my_q, qidx_s, slot_s, r_s, thr_s, n_ckpt);
     }  // steps
 
     // ---- counters -------------------------------------------------------------
