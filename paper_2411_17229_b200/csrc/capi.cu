@@ -21,6 +21,7 @@
 
 #include "../../include/dade_gpu.h"
 #include "kernels.h"
+#include <cudaTypedefs.h>
 
 using namespace dade_gpu;
 
@@ -129,11 +130,54 @@ ChunkTable make_chunks(uint32_t dim, const std::vector<uint32_t>& cps) {
     const char* env = std::getenv("DADE_GPU_NO_TC");
     if (env && env[0] == '1') tc = false;
     ct.use_tc = tc ? 1 : 0;
+    // ring depth: the filter holds a tile's boxes through its exact phase
+    ct.n_buf = tc ? std::max(4, 2 * ct.n_dense + 2) : 4;
+    ct.use_tma = 0;  // decided per launch (needs a tensor map of the rows)
     const char* dbg = std::getenv("DADE_GPU_DEBUG");
     ct.debug = (dbg && dbg[0] == '1') ? 1 : 0;
-    ct.n_buf = tc ? ct.n_dense + 1 : 2;
     return ct;
 }
+
+// 2D tensor map over row-major fp32 rows [rows][dim]: box [kRT rows][kBox
+// dims], 128-byte swizzle (matches swz() in scan.cu), OOB -> zeros.
+bool make_row_tmap(CUtensorMap* m, const float* base, uint64_t rows, uint32_t dim) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                    &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            encode = nullptr;
+        if (!encode) return false;
+    }
+    if (dim % 4 != 0 || dim < (uint32_t)kBox || rows == 0 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    cuuint64_t gdim[2] = {dim, rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)dim * 4};
+    cuuint32_t box[2] = {(cuuint32_t)kBox, (cuuint32_t)kRT};
+    cuuint32_t estride[2] = {1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct TmapCache {
+    const float* base = nullptr;
+    uint64_t rows = 0;
+    uint32_t dim = 0;
+    bool ok = false;
+    CUtensorMap map{};
+    const CUtensorMap& get(const float* b, uint64_t r, uint32_t d, bool& usable) {
+        if (b != base || r != rows || d != dim) {
+            base = b;
+            rows = r;
+            dim = d;
+            ok = make_row_tmap(&map, b, r, d);
+        }
+        const char* env = std::getenv("DADE_GPU_NO_TMA");
+        usable = ok && !(env && env[0] == '1');
+        return map;
+    }
+};
 
 }  // namespace
 
@@ -172,6 +216,7 @@ struct dade_gpu_ctx {
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts;
     DevBuf counters, phase;
+    TmapCache tm_centroids, tm_storage, tm_base;
 
     // profiling
     bool profiling = false;
@@ -251,8 +296,11 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
     a.coeff = nullptr;
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = nullptr;
-    const ChunkTable ct = make_chunks(c->dim, {});
-    cuda_check(launch_scan(a, ct, nb * qchunks, /*sqrt_key=*/false, s), "coarse scan");
+    ChunkTable ct = make_chunks(c->dim, {});
+    bool tma = false;
+    const CUtensorMap& tm = c->tm_centroids.get(a.storage, c->n_clusters, c->dim, tma);
+    ct.use_tma = (tma && ct.vec_ok) ? 1 : 0;
+    cuda_check(launch_scan(a, ct, tm, nb * qchunks, /*sqrt_key=*/false, s), "coarse scan");
     cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, nb, n_probe, c->probes.as<uint64_t>(),
                                      c->probe_count.as<uint32_t>(), s),
                "coarse merge");
@@ -352,9 +400,12 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
     a.phase = phase_ptr(c);
-    const ChunkTable ct = make_chunks(c->dim, c->cps);
+    ChunkTable ct = make_chunks(c->dim, c->cps);
+    bool tma = false;
+    const CUtensorMap& tm = c->tm_storage.get(a.storage, std::max<uint32_t>(c->count, 1), c->dim, tma);
+    ct.use_tma = (tma && ct.vec_ok && c->count > 0) ? 1 : 0;
     record(c, c->e1);
-    cuda_check(launch_scan(a, ct, (uint32_t)max_items, true, s), "dco scan");
+    cuda_check(launch_scan(a, ct, tm, (uint32_t)max_items, true, s), "dco scan");
     record(c, c->e2);
     cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, n_probe, k, out_keys, out_count, s),
                "merge");
@@ -400,9 +451,12 @@ void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
     a.phase = phase_ptr(c);
-    const ChunkTable ct = make_chunks(c->b_dim, c->cps);
+    ChunkTable ct = make_chunks(c->b_dim, c->cps);
+    bool tma = false;
+    const CUtensorMap& tm = c->tm_base.get(a.storage, std::max<uint32_t>(c->b_count, 1), c->b_dim, tma);
+    ct.use_tma = (tma && ct.vec_ok && c->b_count > 0) ? 1 : 0;
     record(c, c->e1);
-    cuda_check(launch_scan(a, ct, nb * qchunks, true, s), "flat scan");
+    cuda_check(launch_scan(a, ct, tm, nb * qchunks, true, s), "flat scan");
     record(c, c->e2);
     cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, nb, k, out_keys, out_count, s), "merge");
     c->launches += 3;

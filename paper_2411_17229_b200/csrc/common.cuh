@@ -2,13 +2,16 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace dade_gpu {
 
 // ---- scan geometry ---------------------------------------------------------
 constexpr int kThreads = 256;  // 8 warps
-constexpr int kWarps = kThreads / 32;
+constexpr int kWarps = kThreads / 32;     // consumer warps
+constexpr int kThreadsTotal = kThreads + 32;  // + one TMA producer warp
+constexpr int kBox = 32;        // dims per TMA box (128 B rows, 128B swizzle)
 constexpr int kRT = 128;       // candidate rows per tile
 constexpr int kQC = 64;        // queries per work item (query chunk)
 constexpr int kCH = 32;        // dims per staged chunk
@@ -46,6 +49,7 @@ struct ChunkTable {
     int use_tc;
     int n_buf;
     int debug;
+    int use_tma;
     uint16_t end[kMaxChunks];
     int16_t ckpt[kMaxChunks];
 };

@@ -34,8 +34,8 @@ struct ScanArgs {
 };
 
 size_t scan_smem_bytes(int n_ckpt, int d_res, int n_buf);
-cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, uint32_t grid, bool sqrt_key,
-                        cudaStream_t s);
+cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tmap, uint32_t grid,
+                        bool sqrt_key, cudaStream_t s);
 cudaError_t launch_merge_segments(const uint64_t* seg_keys, const uint32_t* seg_count, uint32_t nq,
                                   uint32_t n_slots, uint32_t K, uint64_t* out_keys,
                                   uint32_t* out_count, cudaStream_t s);

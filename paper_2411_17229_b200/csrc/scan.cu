@@ -47,17 +47,24 @@ constexpr int kWarpList = 256;  // survivor-list entries per warp per round
 constexpr float kTcDelta = 2e-3f;
 
 struct SmemLayout {
-    size_t o_buf, q_res, q_stage, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, keys, total;
+    size_t slots, q_res, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, keys, bars, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Ring slot = one TMA box [kRT rows][32 dims] (128B-swizzled, 16 KB) plus, when
+// the queries are not resident, that chunk's query tile [32][kQS].
+__host__ __device__ inline size_t slot_bytes(int d_res) {
+    return (size_t)kRT * kBox * 4 + (d_res == 0 ? (size_t)kBox * kQS * 4 : 0);
+}
+
+// Offsets are relative to a 1024-byte aligned base (128B swizzle atoms).
 __host__ __device__ inline SmemLayout smem_layout(int n_ckpt, int d_res, int n_buf) {
     SmemLayout L;
     size_t off = 0;
-    L.o_buf = off; off = align16(off + sizeof(float) * (size_t)n_buf * kRT * kOStride);
+    L.slots = off; off = align16(off + slot_bytes(d_res) * n_buf);
+    off = (off + 1023) & ~size_t(1023);
     L.q_res = off; off = align16(off + sizeof(float) * (size_t)d_res * kQS);
-    L.q_stage = off; off = align16(off + (d_res == 0 ? sizeof(float) * kCH * kQS : 0));
     L.n_q = off; off = align16(off + sizeof(float) * kQC);
     L.r_s = off; off = align16(off + sizeof(float) * kQC);
     L.thr_s = off; off = align16(off + sizeof(float) * kQC * (n_ckpt > 0 ? n_ckpt : 1));
@@ -66,21 +73,50 @@ __host__ __device__ inline SmemLayout smem_layout(int n_ckpt, int d_res, int n_b
     L.wl_meta = off; off = align16(off + sizeof(uint32_t) * kWarps * kWarpList);
     L.wl_acc = off; off = align16(off + sizeof(float) * kWarps * kWarpList);
     L.keys = off; off = align16(off + sizeof(uint64_t) * kWarps * kRT);
-    L.total = off;
+    L.bars = off; off = align16(off + sizeof(uint64_t) * 2 * n_buf);
+    L.total = off + 1024;  // slack for aligning the dynamic smem base
     return L;
+}
+
+// Element (row, k) of a 128B-swizzled [rows][32] fp32 box: 16-byte chunk k/4 of
+// row r lives at chunk (k/4) ^ (r % 8) (CU_TENSOR_MAP_SWIZZLE_128B).
+__device__ __forceinline__ int swz(int row, int k) { return row * kBox + ((((k >> 2) ^ (row & 7))) << 2) + (k & 3); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
     return *reinterpret_cast<const volatile uint32_t*>(p);
 }
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
-    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
-    const int n = valid ? 16 : 0;  // src-size 0 -> zero fill
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 __device__ __forceinline__ uint32_t to_tf32(float x) {
     uint32_t r;
@@ -212,35 +248,44 @@ __device__ __forceinline__ uint32_t compact_round(uint32_t& pending, uint32_t* w
 }
 
 // Optional per-phase clock accounting (DADE_GPU_PHASES=1): lane 0 of every
-// warp adds its clock64 deltas into a.phase[0..4] = {wait+barrier, dense,
-// epilogue, survivors, merges}.
+// consumer warp adds its clock64 deltas into a.phase[0..4] = {wait full slot,
+// dense, epilogue, survivors, merges}.
 #define PH_MARK(t) const long long t = a.phase ? clock64() : 0
 #define PH_ADD(i, t0, t1) do { if (a.phase && lane == 0) atomicAdd(a.phase + (i), (unsigned long long)((t1) - (t0))); } while (0)
 
+// Warp-specialised: warps 0..7 consume (each owns 8 queries of the item for
+// the whole item), warp 8 produces. The producer streams the item's
+// (tile, dense chunk) boxes through an n_buf-deep ring: one TMA
+// (cp.async.bulk.tensor, 128B swizzle) per box into a slot whose `full`
+// mbarrier completes on the transaction bytes; consumers wait on `full`,
+// compute, and arrive on the slot's `empty` mbarrier (count 8) when done with
+// it, so warps drift freely within the ring depth instead of meeting at a
+// CTA barrier every step.
 template <bool kSqrtKey, bool kTC>
-__global__ void __launch_bounds__(kThreads, 2)
-dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
-    extern __shared__ __align__(16) unsigned char smem[];
+__global__ void __launch_bounds__(kThreadsTotal, 2)
+dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int n_ckpt = ct.n_ckpt;
-    const int d_res = ct.d_res;  // resident query dims (0 -> stage per chunk)
+    const int d_res = ct.d_res;  // resident query dims (0 -> staged per box by the producer)
     const int n_buf = ct.n_buf;
     const SmemLayout L = smem_layout(n_ckpt, d_res, n_buf);
-    float* o_buf = reinterpret_cast<float*>(smem + L.o_buf);
+    const size_t sbytes = slot_bytes(d_res);
     float* q_res = reinterpret_cast<float*>(smem + L.q_res);
-    float* q_stage = reinterpret_cast<float*>(smem + L.q_stage);
     float* n_q = reinterpret_cast<float*>(smem + L.n_q);
     float* r_s = reinterpret_cast<float*>(smem + L.r_s);
     float* thr_s = reinterpret_cast<float*>(smem + L.thr_s);
     uint32_t* qidx_s = reinterpret_cast<uint32_t*>(smem + L.qidx);
     uint32_t* slot_s = reinterpret_cast<uint32_t*>(smem + L.slot);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* empty_bar = full_bar + n_buf;
+    auto slot_o = [&](uint32_t sl) { return reinterpret_cast<float*>(smem + L.slots + sl * sbytes); };
+    auto slot_q = [&](uint32_t sl) { return reinterpret_cast<float*>(smem + L.slots + sl * sbytes + (size_t)kRT * kBox * 4); };
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const uint32_t dim = a.dim;
-    uint32_t* wl_meta = reinterpret_cast<uint32_t*>(smem + L.wl_meta) + warp * kWarpList;
-    float* wl_acc = reinterpret_cast<float*>(smem + L.wl_acc) + warp * kWarpList;
-    uint64_t* kb = reinterpret_cast<uint64_t*>(smem + L.keys) + warp * kRT;
 
     // ---- decode the work item ------------------------------------------------
     uint32_t row_start, row_count, qcount;
@@ -267,59 +312,85 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
     }
     if (tid < kQC && tid >= (int)qcount) { qidx_s[tid] = 0; slot_s[tid] = 0; }
     if (tid < kQC) r_s[tid] = __int_as_float(0x7f800000);
+    if (tid == 0) {
+        for (int i = 0; i < n_buf; ++i) {
+            mbar_init(full_bar + i, 1);
+            mbar_init(empty_bar + i, kWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        if (ct.use_tma) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    }
     __syncthreads();
     // resident queries, k-major [d_res][kQS]
-    for (uint32_t idx = tid; idx < (uint32_t)d_res * kQC; idx += kThreads) {
+    for (uint32_t idx = tid; idx < (uint32_t)d_res * kQC; idx += kThreadsTotal) {
         const uint32_t j = idx / d_res, k = idx - j * d_res;
         q_res[k * kQS + j] = j < qcount ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k) : 0.f;
     }
     __syncthreads();
-    if (kTC && tid < kQC) {  // first-slice query norms for the filter bound
-        float nq = 0.f;
-        for (int k = 0; k < d_res; ++k) nq = fmaf(q_res[k * kQS + tid], q_res[k * kQS + tid], nq);
-        n_q[tid] = nq;
-    }
 
-    unsigned long long st_dco = 0, st_dims = 0, st_bytes = 0;
-    if (tid == 0) st_bytes += sizeof(WorkItem) + 8ull * qcount + 4ull * d_res * qcount;
-    const uint64_t nz2 = a.neg_zero2;
     const int c_dense = ct.n_dense;
-    const bool has_sparse = c_dense < ct.n_chunks;
-    const uint32_t d0 = ct.end[c_dense - 1];
     const uint32_t n_tiles = (row_count + kRT - 1) / kRT;
     const uint32_t n_steps = n_tiles * c_dense;
+
+    // =========================== producer warp ===================================
+    if (warp == kWarps) {
+        unsigned long long st_bytes = 0;
+        for (uint32_t s = 0; s < n_steps; ++s) {
+            const uint32_t sl = s % n_buf;
+            if (s >= (uint32_t)n_buf) mbar_wait(empty_bar + sl, ((s / n_buf) - 1) & 1);
+            const uint32_t t = s / c_dense, c = s - t * c_dense;
+            const uint32_t tb = t * kRT, nrows = min((uint32_t)kRT, row_count - tb);
+            const uint32_t k0 = c == 0 ? 0u : ct.end[c - 1];
+            const uint32_t w = ct.end[c] - k0;
+            if (d_res == 0) {
+                // stage this chunk's query slice (zero beyond w) next to the box
+                float* qs = slot_q(sl);
+                for (uint32_t idx = lane; idx < (uint32_t)kQC * kBox; idx += 32) {
+                    const uint32_t j = idx / kBox, cc = idx - j * kBox;
+                    qs[cc * kQS + j] = (j < qcount && cc < w) ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k0 + cc) : 0.f;
+                }
+                st_bytes += 4ull * w * qcount;
+            }
+            float* ob = slot_o(sl);
+            if (ct.use_tma) {
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(full_bar + sl, kRT * kBox * 4);
+                    tma_load_2d(ob, &tmap, (int)k0, (int)(row_start + tb), full_bar + sl);
+                }
+            } else {
+                for (uint32_t idx = lane; idx < (uint32_t)kRT * kBox; idx += 32) {
+                    const uint32_t r = idx / kBox, cc = idx - r * kBox;
+                    ob[swz(r, cc)] = (r < nrows && cc < w) ? __ldg(a.storage + (size_t)(row_start + tb + r) * dim + k0 + cc) : 0.f;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(full_bar + sl);
+            }
+            st_bytes += 4ull * w * nrows;
+        }
+        if (lane == 0 && a.counters) atomicAdd(a.counters + 2, st_bytes + sizeof(WorkItem) + 8ull * qcount + 4ull * d_res * qcount);
+        return;
+    }
+
+    // =========================== consumer warps ==================================
+    uint32_t* wl_meta = reinterpret_cast<uint32_t*>(smem + L.wl_meta) + warp * kWarpList;
+    float* wl_acc = reinterpret_cast<float*>(smem + L.wl_acc) + warp * kWarpList;
+    uint64_t* kb = reinterpret_cast<uint64_t*>(smem + L.keys) + warp * kRT;
+    const uint32_t my_q = (uint32_t)max(0, min(8, (int)qcount - warp * 8));
+    if (kTC && lane < (int)my_q) {  // first-slice query norms for the filter bound
+        const int j = warp * 8 + lane;
+        float nq = 0.f;
+        for (int k = 0; k < d_res; ++k) nq = fmaf(q_res[k * kQS + j], q_res[k * kQS + j], nq);
+        n_q[j] = nq;
+    }
+    __syncwarp();
+
+    unsigned long long st_dco = 0, st_dims = 0, st_bytes = 0;
+    const uint64_t nz2 = a.neg_zero2;
+    const uint32_t d0 = ct.end[c_dense - 1];
+    const bool has_sparse = c_dense < ct.n_chunks;
     const bool vec = ct.vec_ok != 0;
     const int g = lane >> 2, tq = lane & 3;  // MMA fragment coordinates
-
-    // stage the o tile of step s into ring slot (s % n_buf)
-    auto issue = [&](uint32_t s) {
-        const uint32_t t = s / c_dense, c = s - t * c_dense;
-        const uint32_t tb = t * kRT, nrows = min((uint32_t)kRT, row_count - tb);
-        const uint32_t k0 = c == 0 ? 0u : ct.end[c - 1];
-        const uint32_t w = ct.end[c] - k0;
-        float* buf = o_buf + (s % n_buf) * (kRT * kOStride);
-        if (vec) {
-            const uint32_t v4 = w >> 2;
-            for (uint32_t idx = tid; idx < kRT * v4; idx += kThreads) {
-                const uint32_t r = idx / v4, c4 = idx - r * v4;
-                const bool ok = r < nrows;
-                const float* src = a.storage + (size_t)(row_start + tb + (ok ? r : 0)) * dim + k0 + 4 * c4;
-                cp_async16(buf + r * kOStride + 4 * c4, src, ok);
-            }
-        } else {
-            const uint32_t w4 = (w + 3) & ~3u;
-            for (uint32_t idx = tid; idx < kRT * w4; idx += kThreads) {
-                const uint32_t r = idx / w4, cc = idx - r * w4;
-                float v = 0.f;
-                if (r < nrows && cc < w) v = __ldg(a.storage + (size_t)(row_start + tb + r) * dim + k0 + cc);
-                buf[r * kOStride + cc] = v;
-            }
-        }
-        cp_async_commit();
-        if (tid == 0) st_bytes += 4ull * w * nrows;
-    };
-
-    if (n_steps > 0) issue(0);
 
     uint64_t acc[4][4];      // SIMT dense accumulators (kTC == false)
     float tcd[8][4];         // MMA accumulators: 8 m-tiles of 16 rows x this warp's 8 queries
@@ -331,17 +402,15 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
         const uint32_t k0 = c == 0 ? 0u : ct.end[c - 1];
         const uint32_t w = ct.end[c] - k0;
         const uint32_t w4 = (w + 3) & ~3u;
-        const uint32_t my_q = (uint32_t)max(0, min(8, (int)qcount - warp * 8));
+        const uint32_t sl = s % n_buf;
         if (c == 0) {
             // tile start: pick up radii tightened by other CTAs; reset the pairs
-            if (lane < 8) {
+            if (lane < (int)my_q) {
                 const int j = warp * 8 + lane;
-                if (j < (int)qcount) {
-                    const float rg = __uint_as_float(ld_volatile_u32(a.r_global + qidx_s[j]));
-                    if (rg < r_s[j] || t == 0) {
-                        r_s[j] = fminf(rg, r_s[j]);
-                        refresh_thr(thr_s, r_s, a.coeff, n_ckpt, j, 0, 1);
-                    }
+                const float rg = __uint_as_float(ld_volatile_u32(a.r_global + qidx_s[j]));
+                if (rg < r_s[j] || t == 0) {
+                    r_s[j] = fminf(rg, r_s[j]);
+                    refresh_thr(thr_s, r_s, a.coeff, n_ckpt, j, 0, 1);
                 }
             }
             __syncwarp();
@@ -366,26 +435,11 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
             }
         }
         PH_MARK(t_w0);
-        cp_async_wait_all();
-        __syncthreads();  // tile s visible to all; everyone done with the slot being refilled
+        mbar_wait(full_bar + sl, (s / n_buf) & 1);
         PH_MARK(t_w1);
         PH_ADD(0, t_w0, t_w1);
-        if (s + 1 < n_steps) issue(s + 1);
-        const float* buf = o_buf + (s % n_buf) * (kRT * kOStride);
-        const float* qk;
-        if (d_res > 0) {
-            qk = q_res + k0 * kQS;
-        } else {
-            // non-resident queries: stage this chunk's slice (k-major)
-            for (uint32_t idx = tid; idx < kQC * w4; idx += kThreads) {
-                const uint32_t j = idx / w4, cc = idx - j * w4;
-                q_stage[cc * kQS + j] =
-                    (j < qcount && cc < w) ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k0 + cc) : 0.f;
-            }
-            __syncthreads();
-            qk = q_stage;
-            if (tid == 0) st_bytes += 4ull * w * qcount;
-        }
+        const float* ob = slot_o(sl);
+        const float* qk = d_res > 0 ? q_res + k0 * kQS : slot_q(sl);
 
         if constexpr (kTC) {
             // ---- tensor-core dot products o . q over this chunk ----------------
@@ -395,9 +449,9 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                     const uint32_t b1 = to_tf32(qk[(ks + tq + 4) * kQS + warp * 8 + g]);
 #pragma unroll
                     for (int mt = 0; mt < 8; ++mt) {
-                        const float* r0 = buf + (mt * 16 + g) * kOStride + ks + tq;
-                        const float* r1 = r0 + 8 * kOStride;
-                        mma_tf32(tcd[mt], to_tf32(r0[0]), to_tf32(r1[0]), to_tf32(r0[4]), to_tf32(r1[4]), b0, b1);
+                        const int r0 = mt * 16 + g;
+                        mma_tf32(tcd[mt], to_tf32(ob[swz(r0, ks + tq)]), to_tf32(ob[swz(r0 + 8, ks + tq)]),
+                                 to_tf32(ob[swz(r0, ks + tq + 4)]), to_tf32(ob[swz(r0 + 8, ks + tq + 4)]), b0, b1);
                     }
                 }
             }
@@ -408,7 +462,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                     float4 o[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
-                        o[i] = *reinterpret_cast<const float4*>(buf + (lane + 32 * i) * kOStride + k4);
+                        o[i] = *reinterpret_cast<const float4*>(ob + swz(lane + 32 * i, k4));
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const ulonglong2 qa = *reinterpret_cast<const ulonglong2*>(qk + (k4 + kk) * kQS + warp * 8);
@@ -423,6 +477,9 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                     }
                 }
             }
+            // the exact path keeps its partials in registers: free the slot now
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_bar + sl);
         }
         PH_MARK(t_d1);
         PH_ADD(1, t_w1, t_d1);
@@ -434,17 +491,17 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
         uint32_t pending = 0;  // pairs needing the exact / sparse path
         bool from_prefix = false;
         if constexpr (kTC) {
-            // first-slice squared norms of this lane's rows l + 32i (exact enough: fma)
+            // first-slice squared norms of this lane's rows l + 32i
             float no_reg[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) no_reg[i] = 0.f;
             for (int cc = 0; cc < c_dense; ++cc) {
-                const float* bc = o_buf + ((s - (c_dense - 1) + cc) % n_buf) * (kRT * kOStride);
+                const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
                 const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], wc = ct.end[cc] - lo;
                 for (uint32_t k4 = 0; k4 < wc; k4 += 4) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const float4 v = *reinterpret_cast<const float4*>(bc + (lane + 32 * i) * kOStride + k4);
+                        const float4 v = *reinterpret_cast<const float4*>(bc + swz(lane + 32 * i, k4));
                         no_reg[i] = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, no_reg[i]))));
                     }
                 }
@@ -473,18 +530,11 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                                 // debug: the filter's prune must agree with the exact prefix
                                 float xx = 0.f;
                                 for (int cc = 0; cc < c_dense; ++cc) {
-                                    const float* bc = o_buf + ((s - (c_dense - 1) + cc) % n_buf) * (kRT * kOStride) + row * kOStride;
+                                    const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
                                     const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
-                                    for (uint32_t k = lo; k < hi; ++k) xx = sq_step(xx, bc[k - lo], q_res[k * kQS + j]);
+                                    for (uint32_t k = lo; k < hi; ++k) xx = sq_step(xx, bc[swz(row, k - lo)], q_res[k * kQS + j]);
                                 }
-                                if (!(xx > thr_s[j * n_ckpt + ck])) {
-                                    atomicAdd(a.counters + 3, 1ull);
-                                    if (a.counters[4] == 0) {
-                                        a.counters[4] = 1;
-                                        printf("TC VIOLATION row %u j %d pt %.6g delta %.6g exact %.6g thr %.6g no %.6g nq %.6g dot %.6g\n",
-                                               row, j, pt, delta, xx, thr_s[j * n_ckpt + ck], no, nq, tcd[mt][2 * h + cq]);
-                                    }
-                                }
+                                if (!(xx > thr_s[j * n_ckpt + ck])) atomicAdd(a.counters + 3, 1ull);
                             }
                         }
                     }
@@ -584,10 +634,10 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                 bool live = true;
                 if (from_prefix) {
                     for (int cc = 0; cc < c_dense; ++cc) {
-                        const float* bc = o_buf + ((s - (c_dense - 1) + cc) % n_buf) * (kRT * kOStride) + row * kOStride;
+                        const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
                         const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
                         for (uint32_t k = lo; k < hi; k += 4) {
-                            const float4 o4 = *reinterpret_cast<const float4*>(bc + (k - lo));
+                            const float4 o4 = *reinterpret_cast<const float4*>(bc + swz(row, k - lo));
                             x = sq_step(x, o4.x, q_res[(k + 0) * kQS + j]);
                             x = sq_step(x, o4.y, q_res[(k + 1) * kQS + j]);
                             x = sq_step(x, o4.z, q_res[(k + 2) * kQS + j]);
@@ -604,7 +654,22 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
                     const float* qrow = a.queries + (size_t)qidx_s[j] * dim;
                     for (int cc = c_dense; cc < ct.n_chunks; ++cc) {
                         const uint32_t lo = ct.end[cc - 1], hi = ct.end[cc];
-                        if (vec) {
+                        if (vec && hi - lo == (uint32_t)kCH) {
+                            // whole chunk in flight at once: one L2 round trip
+                            float4 o8[kCH / 4], q8[kCH / 4];
+#pragma unroll
+                            for (int v = 0; v < kCH / 4; ++v) {
+                                o8[v] = __ldg(reinterpret_cast<const float4*>(orow + lo) + v);
+                                q8[v] = __ldg(reinterpret_cast<const float4*>(qrow + lo) + v);
+                            }
+#pragma unroll
+                            for (int v = 0; v < kCH / 4; ++v) {
+                                x = sq_step(x, o8[v].x, q8[v].x);
+                                x = sq_step(x, o8[v].y, q8[v].y);
+                                x = sq_step(x, o8[v].z, q8[v].z);
+                                x = sq_step(x, o8[v].w, q8[v].w);
+                            }
+                        } else if (vec) {
                             for (uint32_t kk = lo; kk < hi; kk += 4) {
                                 const float4 o4 = __ldg(reinterpret_cast<const float4*>(orow + kk));
                                 const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + kk));
@@ -644,6 +709,12 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct) {
             PH_ADD(4, t_r1, t_r2);
         }
         tighten_warp_radii(a, warp, lane, my_q, qidx_s, slot_s, r_s, thr_s, n_ckpt);
+        if constexpr (kTC) {
+            // the tile's boxes were read by the exact prefix: release them now
+            __syncwarp();
+            if (lane == 0)
+                for (int cc = 0; cc < c_dense; ++cc) mbar_arrive(empty_bar + (s - (c_dense - 1) + cc) % n_buf);
+        }
     }  // steps
 
     // ---- counters -------------------------------------------------------------
@@ -752,21 +823,22 @@ __global__ void keys_to_results_kernel(const uint64_t* __restrict__ keys, const 
 size_t scan_smem_bytes(int n_ckpt, int d_res, int n_buf) { return smem_layout(n_ckpt, d_res, n_buf).total; }
 
 template <bool kSqrtKey, bool kTC>
-static cudaError_t launch_scan_t(const ScanArgs& a, const ChunkTable& ct, uint32_t grid, size_t smem, cudaStream_t s) {
+static cudaError_t launch_scan_t(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tm, uint32_t grid,
+                                 size_t smem, cudaStream_t s) {
     DADE_CUDA_TRY(cudaFuncSetAttribute(dco_scan_kernel<kSqrtKey, kTC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    dco_scan_kernel<kSqrtKey, kTC><<<grid, kThreads, smem, s>>>(a, ct);
+    dco_scan_kernel<kSqrtKey, kTC><<<grid, kThreadsTotal, smem, s>>>(a, ct, tm);
     return cudaGetLastError();
 }
 
-cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, uint32_t grid, bool sqrt_key,
-                        cudaStream_t s) {
+cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tm, uint32_t grid,
+                        bool sqrt_key, cudaStream_t s) {
     if (grid == 0) return cudaSuccess;
     const size_t smem = scan_smem_bytes(ct.n_ckpt, ct.d_res, ct.n_buf);
-    if (sqrt_key) return ct.use_tc ? launch_scan_t<true, true>(a, ct, grid, smem, s)
-                                   : launch_scan_t<true, false>(a, ct, grid, smem, s);
-    return ct.use_tc ? launch_scan_t<false, true>(a, ct, grid, smem, s)
-                     : launch_scan_t<false, false>(a, ct, grid, smem, s);
+    if (sqrt_key) return ct.use_tc ? launch_scan_t<true, true>(a, ct, tm, grid, smem, s)
+                                   : launch_scan_t<true, false>(a, ct, tm, grid, smem, s);
+    return ct.use_tc ? launch_scan_t<false, true>(a, ct, tm, grid, smem, s)
+                     : launch_scan_t<false, false>(a, ct, tm, grid, smem, s);
 }
 
 cudaError_t launch_merge_segments(const uint64_t* seg_keys, const uint32_t* seg_count, uint32_t nq,
