@@ -173,6 +173,44 @@ __device__ inline uint32_t warp_merge(uint64_t* A, uint32_t* cA_ptr, uint32_t K,
     return nc;
 }
 
+// Same contract as warp_merge for a top-K list A in GLOBAL memory, with the
+// list staged once into the warp's shared scratch (K <= kStageMaxK): one
+// coalesced load instead of a chain of dependent global reads, all rank
+// searches in shared memory, and only the elements that move are written back.
+constexpr int kStageMaxK = 128;
+__device__ inline uint32_t warp_merge_staged(uint64_t* A, uint32_t* cA_ptr, uint32_t K, const uint64_t* B,
+                                             uint32_t m, uint64_t* scratch) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t cA = *reinterpret_cast<volatile uint32_t*>(cA_ptr);
+    if (m == 0) return cA;
+    for (uint32_t i = lane; i < cA; i += 32) scratch[i] = A[i];
+    __syncwarp();
+    uint64_t minb = kEmptyKey;
+    for (uint32_t b = lane; b < m; b += 32) minb = B[b] < minb ? B[b] : minb;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const uint64_t o = __shfl_xor_sync(0xffffffffu, minb, off);
+        minb = o < minb ? o : minb;
+    }
+    // A elements >= min(B) shift right by the number of smaller B elements
+    const uint32_t first = lower_bound_u64(scratch, cA, minb);
+    for (uint32_t i = first + lane; i < cA; i += 32) {
+        const uint64_t a = scratch[i];
+        const uint32_t pos = i + count_less(B, m, a);
+        if (pos < K) A[pos] = a;
+    }
+    for (uint32_t b = lane; b < m; b += 32) {
+        const uint64_t kb = B[b];
+        const uint32_t pos = count_less(B, m, kb) + lower_bound_u64(scratch, cA, kb);
+        if (pos < K) A[pos] = kb;
+    }
+    const uint32_t nc = min(K, cA + m);
+    __syncwarp();
+    if (lane == 0) *cA_ptr = nc;
+    __syncwarp();
+    return nc;
+}
+
 // ---- error plumbing ----------------------------------------------------------
 #define DADE_CUDA_TRY(expr)                                                      \
     do {                                                                         \

@@ -35,19 +35,20 @@ namespace dade_gpu {
 
 namespace {
 
-constexpr int kWarpList = 256;  // survivor-list entries per warp per round
+constexpr int kWarpList = 128;  // survivor-list entries per warp per round
 
 // Relative error budget of the TF32 filter: |p~ - acc| <= kTcDelta * (|o|^2 + |q|^2)
-// over the first slice. Derivation: TF32 inputs (cvt.rna,
-// 2^-11 relative each) give a dot-product error <= (2^-10 + 2^-22) sum|o_k q_k|
-// <= 5e-4 (|o|^2 + |q|^2); tensor-core fp32 accumulation of 8-term steps and
-// the fp32 norms / combination add < 1e-5; the exact sequential fp32 partial
-// differs from the real distance by < 32 * 3 * 2^-24 relative (< 1e-5 of
-// (|o| + |q|)^2). 2e-3 leaves a > 3x margin.
-constexpr float kTcDelta = 2e-3f;
+// over the first slice. Derivation: fp32 operands read as TF32
+// (truncated, < 2^-10 relative each) give a dot-product error
+// < (2^-9 + 2^-20) sum|o_k q_k| <= 9.8e-4 (|o|^2 + |q|^2); tensor-core fp32
+// accumulation of 8-term steps and the fp32 norms / combination add < 1e-5;
+// the exact sequential fp32 partial differs from the real distance by
+// < 32 * 3 * 2^-24 relative (< 1e-5 of (|o| + |q|)^2). So
+// |p~ - acc| < 2 * 9.8e-4 + 3e-5 < 2.1e-3 of (|o|^2 + |q|^2); 4e-3 leaves ~2x.
+constexpr float kTcDelta = 4e-3f;
 
 struct SmemLayout {
-    size_t slots, q_res, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, keys, bars, total;
+    size_t slots, q_res, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, keys, mscratch, bars, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -73,6 +74,7 @@ __host__ __device__ inline SmemLayout smem_layout(int n_ckpt, int d_res, int n_b
     L.wl_meta = off; off = align16(off + sizeof(uint32_t) * kWarps * kWarpList);
     L.wl_acc = off; off = align16(off + sizeof(float) * kWarps * kWarpList);
     L.keys = off; off = align16(off + sizeof(uint64_t) * kWarps * kRT);
+    L.mscratch = off; off = align16(off + sizeof(uint64_t) * kWarps * kStageMaxK);
     L.bars = off; off = align16(off + sizeof(uint64_t) * 2 * n_buf);
     L.total = off + 1024;  // slack for aligning the dynamic smem base
     return L;
@@ -145,10 +147,12 @@ __device__ __forceinline__ void refresh_thr(float* thr_s, const float* r_s, cons
 // then tighten r_s[j] / thr_s / the global radius from the new K-th key.
 __device__ __forceinline__ void merge_query(const ScanArgs& a, uint64_t* kb, uint32_t m, uint32_t j,
                                             const uint32_t* qidx_s, const uint32_t* slot_s, float* r_s,
-                                            float* thr_s, int n_ckpt, int lane, bool tighten = true) {
+                                            float* thr_s, int n_ckpt, int lane, uint64_t* scratch,
+                                            bool tighten = true) {
     const size_t seg = (size_t)qidx_s[j] * a.n_slots + slot_s[j];
     uint64_t* A = a.seg_keys + seg * a.K;
-    const uint32_t nc = warp_merge(A, a.seg_count + seg, a.K, kb, m, false);
+    const uint32_t nc = a.K <= (uint32_t)kStageMaxK ? warp_merge_staged(A, a.seg_count + seg, a.K, kb, m, scratch)
+                                                    : warp_merge(A, a.seg_count + seg, a.K, kb, m, false);
     if (tighten && nc == a.K) {
         const float rn = hi_f(A[a.K - 1]);
         if (rn < r_s[j]) {
@@ -170,7 +174,7 @@ __device__ __forceinline__ void merge_list_candidates(const ScanArgs& a, const u
                                                       uint32_t row_base, int warp, int lane,
                                                       const uint32_t* qidx_s, const uint32_t* slot_s,
                                                       float* r_s, float* thr_s, int n_ckpt,
-                                                      unsigned long long& st_bytes) {
+                                                      unsigned long long& st_bytes, uint64_t* scratch) {
     for (int jj = 0; jj < 8; ++jj) {
         uint32_t m = 0;
         for (uint32_t e0 = 0; e0 < n; e0 += 32) {
@@ -192,7 +196,7 @@ __device__ __forceinline__ void merge_list_candidates(const ScanArgs& a, const u
         __syncwarp();
         if (m) {
             if (a.row_ids && lane == 0) st_bytes += 4ull * m;
-            merge_query(a, kb, m, warp * 8 + jj, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane, false);
+            merge_query(a, kb, m, warp * 8 + jj, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane, scratch, false);
         }
     }
 }
@@ -265,7 +269,9 @@ template <bool kSqrtKey, bool kTC>
 __global__ void __launch_bounds__(kThreadsTotal, 2)
 dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned base derived by pointer arithmetic (keeps the shared
+    // address space visible to the compiler -> LDS, not generic loads)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int n_ckpt = ct.n_ckpt;
     const int d_res = ct.d_res;  // resident query dims (0 -> staged per box by the producer)
     const int n_buf = ct.n_buf;
@@ -323,7 +329,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
     __syncthreads();
     // resident queries, k-major [d_res][kQS]
     for (uint32_t idx = tid; idx < (uint32_t)d_res * kQC; idx += kThreadsTotal) {
-        const uint32_t j = idx / d_res, k = idx - j * d_res;
+        const uint32_t k = idx / kQC, j = idx - k * kQC;  // j fastest: conflict-free stores
         q_res[k * kQS + j] = j < qcount ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k) : 0.f;
     }
     __syncthreads();
@@ -376,6 +382,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
     uint32_t* wl_meta = reinterpret_cast<uint32_t*>(smem + L.wl_meta) + warp * kWarpList;
     float* wl_acc = reinterpret_cast<float*>(smem + L.wl_acc) + warp * kWarpList;
     uint64_t* kb = reinterpret_cast<uint64_t*>(smem + L.keys) + warp * kRT;
+    uint64_t* ms = reinterpret_cast<uint64_t*>(smem + L.mscratch) + warp * kStageMaxK;
     const uint32_t my_q = (uint32_t)max(0, min(8, (int)qcount - warp * 8));
     if (kTC && lane < (int)my_q) {  // first-slice query norms for the filter bound
         const int j = warp * 8 + lane;
@@ -393,7 +400,6 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
     const int g = lane >> 2, tq = lane & 3;  // MMA fragment coordinates
 
     uint64_t acc[4][4];      // SIMT dense accumulators (kTC == false)
-    float tcd[8][4];         // MMA accumulators: 8 m-tiles of 16 rows x this warp's 8 queries
     uint32_t alive = 0;
     for (uint32_t s = 0; s < n_steps; ++s) {
         const uint32_t t = s / c_dense;
@@ -415,12 +421,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
             }
             __syncwarp();
             if (lane == 0) st_dco += (unsigned long long)nrows * my_q;
-            if constexpr (kTC) {
-#pragma unroll
-                for (int mt = 0; mt < 8; ++mt)
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) tcd[mt][v] = 0.f;
-            } else {
+            if constexpr (!kTC) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -442,19 +443,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
         const float* qk = d_res > 0 ? q_res + k0 * kQS : slot_q(sl);
 
         if constexpr (kTC) {
-            // ---- tensor-core dot products o . q over this chunk ----------------
-            if (my_q > 0) {
-                for (uint32_t ks = 0; ks < w; ks += 8) {
-                    const uint32_t b0 = to_tf32(qk[(ks + tq) * kQS + warp * 8 + g]);
-                    const uint32_t b1 = to_tf32(qk[(ks + tq + 4) * kQS + warp * 8 + g]);
-#pragma unroll
-                    for (int mt = 0; mt < 8; ++mt) {
-                        const int r0 = mt * 16 + g;
-                        mma_tf32(tcd[mt], to_tf32(ob[swz(r0, ks + tq)]), to_tf32(ob[swz(r0 + 8, ks + tq)]),
-                                 to_tf32(ob[swz(r0, ks + tq + 4)]), to_tf32(ob[swz(r0 + 8, ks + tq + 4)]), b0, b1);
-                    }
-                }
-            }
+            // the filter runs once per tile over all dense boxes (below)
         } else {
             // ---- dense register-tiled exact update ----------------------------
             if (__any_sync(0xffffffffu, alive != 0)) {
@@ -506,10 +495,31 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                     }
                 }
             }
-            // filter: prune for sure iff p~ - delta > thr; everything else is decided exactly
+            // Tensor-core dot products o . q over the dense dims, one 16-row
+            // m-tile at a time (4 live accumulators), then the filter: prune for
+            // sure iff p~ - delta > thr; everything else is decided exactly.
+            // Operands are fed as raw fp32 bits: the tensor core reads them as
+            // TF32 (low mantissa bits ignored), which kTcDelta accounts for.
             uint32_t valid = 0;
-#pragma unroll
+            const float* qkd = q_res;
+#pragma unroll 1
             for (int mt = 0; mt < 8; ++mt) {
+                float d4[4] = {0.f, 0.f, 0.f, 0.f};
+                if (my_q > 0 && (uint32_t)(mt * 16) < nrows) {
+                    for (int cc = 0; cc < c_dense; ++cc) {
+                        const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
+                        const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], wc = ct.end[cc] - lo;
+                        const int r0 = mt * 16 + g;
+#pragma unroll 4
+                        for (uint32_t ks = 0; ks < wc; ks += 8) {
+                            const uint32_t b0 = __float_as_uint(qkd[(lo + ks + tq) * kQS + warp * 8 + g]);
+                            const uint32_t b1 = __float_as_uint(qkd[(lo + ks + tq + 4) * kQS + warp * 8 + g]);
+                            mma_tf32(d4, __float_as_uint(bc[swz(r0, ks + tq)]), __float_as_uint(bc[swz(r0 + 8, ks + tq)]),
+                                     __float_as_uint(bc[swz(r0, ks + tq + 4)]),
+                                     __float_as_uint(bc[swz(r0 + 8, ks + tq + 4)]), b0, b1);
+                        }
+                    }
+                }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int rb = mt * 16 + 8 * h;
@@ -521,7 +531,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                         if (row < nrows && jj < my_q) {
                             const int j = warp * 8 + jj;
                             const float nq = n_q[j];
-                            const float pt = no + nq - 2.f * tcd[mt][2 * h + cq];
+                            const float pt = no + nq - 2.f * d4[2 * h + cq];
                             const float delta = kTcDelta * (no + nq);
                             const uint32_t bit = 1u << (mt * 4 + h * 2 + cq);
                             valid |= bit;
@@ -593,7 +603,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                     __syncwarp();
                     if (m) {
                         if (a.row_ids && lane == 0) st_bytes += 4ull * m;
-                        merge_query(a, kb, m, j, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane);
+                        merge_query(a, kb, m, j, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane, ms);
                     }
                 }
             }
@@ -704,7 +714,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
             PH_MARK(t_r1);
             PH_ADD(3, t_r0, t_r1);
             merge_list_candidates(a, wl_meta, wl_acc, n, kb, row_base, warp, lane, qidx_s, slot_s, r_s, thr_s,
-                                  n_ckpt, st_bytes);
+                                  n_ckpt, st_bytes, ms);
             PH_MARK(t_r2);
             PH_ADD(4, t_r1, t_r2);
         }

@@ -29,6 +29,8 @@ for it in range(3):
     buf = np.zeros(16, np.uint64)
     _capi.check(_capi.lib.dade_gpu_debug_counters(dev.h, _capi.ptr(buf)))
     ph = buf[8:13].astype(np.float64)
+    if os.environ.get("DADE_GPU_DEBUG") == "1":
+        print("  filter violations:", int(buf[3]))
     names = ["wait+barrier", "dense", "epilogue", "survivors", "merges"]
     tot = ph.sum()
     print(f"scan {scan_ms:.3f} ms total {total_ms:.3f} ms dco {st.total_dco} dims {st.dims_accumulated} "
