@@ -48,7 +48,7 @@ constexpr int kWarpList = 128;  // survivor-list entries per warp per round
 constexpr float kTcDelta = 4e-3f;
 
 struct SmemLayout {
-    size_t slots, q_res, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, keys, mscratch, bars, total;
+    size_t slots, q_res, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, s2_meta, s2_acc, keys, mscratch, bars, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -73,6 +73,8 @@ __host__ __device__ inline SmemLayout smem_layout(int n_ckpt, int d_res, int n_b
     L.slot = off; off = align16(off + sizeof(uint32_t) * kQC);
     L.wl_meta = off; off = align16(off + sizeof(uint32_t) * kWarps * kWarpList);
     L.wl_acc = off; off = align16(off + sizeof(float) * kWarps * kWarpList);
+    L.s2_meta = off; off = align16(off + sizeof(uint32_t) * kWarps * kWarpList);
+    L.s2_acc = off; off = align16(off + sizeof(float) * kWarps * kWarpList);
     L.keys = off; off = align16(off + sizeof(uint64_t) * kWarps * kRT);
     L.mscratch = off; off = align16(off + sizeof(uint64_t) * kWarps * kStageMaxK);
     L.bars = off; off = align16(off + sizeof(uint64_t) * 2 * n_buf);
@@ -383,6 +385,8 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
     float* wl_acc = reinterpret_cast<float*>(smem + L.wl_acc) + warp * kWarpList;
     uint64_t* kb = reinterpret_cast<uint64_t*>(smem + L.keys) + warp * kRT;
     uint64_t* ms = reinterpret_cast<uint64_t*>(smem + L.mscratch) + warp * kStageMaxK;
+    uint32_t* s2_meta = reinterpret_cast<uint32_t*>(smem + L.s2_meta) + warp * kWarpList;
+    float* s2_acc = reinterpret_cast<float*>(smem + L.s2_acc) + warp * kWarpList;
     const uint32_t my_q = (uint32_t)max(0, min(8, (int)qcount - warp * 8));
     if (kTC && lane < (int)my_q) {  // first-slice query norms for the filter bound
         const int j = warp * 8 + lane;
@@ -478,7 +482,6 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
         const int ck = ct.ckpt[c];
         const uint32_t row_base = row_start + tb;
         uint32_t pending = 0;  // pairs needing the exact / sparse path
-        bool from_prefix = false;
         if constexpr (kTC) {
             // first-slice squared norms of this lane's rows l + 32i
             float no_reg[4];
@@ -501,57 +504,65 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
             // Operands are fed as raw fp32 bits: the tensor core reads them as
             // TF32 (low mantissa bits ignored), which kTcDelta accounts for.
             uint32_t valid = 0;
-            const float* qkd = q_res;
 #pragma unroll 1
-            for (int mt = 0; mt < 8; ++mt) {
-                float d4[4] = {0.f, 0.f, 0.f, 0.f};
-                if (my_q > 0 && (uint32_t)(mt * 16) < nrows) {
+            for (int mp = 0; mp < 8; mp += 2) {
+                float d4[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+                if (my_q > 0 && (uint32_t)(mp * 16) < nrows) {
                     for (int cc = 0; cc < c_dense; ++cc) {
                         const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
                         const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], wc = ct.end[cc] - lo;
-                        const int r0 = mt * 16 + g;
+                        // rows mp*16 + g (+8, +16, +24) all have row % 8 == g
+                        const float* rowp = bc + (mp * 16 + g) * kBox + tq;
+                        const float* qcol = q_res + (lo + tq) * kQS + warp * 8 + g;
 #pragma unroll 4
                         for (uint32_t ks = 0; ks < wc; ks += 8) {
-                            const uint32_t b0 = __float_as_uint(qkd[(lo + ks + tq) * kQS + warp * 8 + g]);
-                            const uint32_t b1 = __float_as_uint(qkd[(lo + ks + tq + 4) * kQS + warp * 8 + g]);
-                            mma_tf32(d4, __float_as_uint(bc[swz(r0, ks + tq)]), __float_as_uint(bc[swz(r0 + 8, ks + tq)]),
-                                     __float_as_uint(bc[swz(r0, ks + tq + 4)]),
-                                     __float_as_uint(bc[swz(r0 + 8, ks + tq + 4)]), b0, b1);
+                            const int c0 = (int)(((ks >> 2) ^ g) << 2), c1 = (int)((((ks >> 2) + 1) ^ g) << 2);
+                            const uint32_t b0 = __float_as_uint(qcol[ks * kQS]);
+                            const uint32_t b1 = __float_as_uint(qcol[(ks + 4) * kQS]);
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                const float* rp = rowp + u * 16 * kBox;
+                                mma_tf32(d4[u], __float_as_uint(rp[c0]), __float_as_uint(rp[8 * kBox + c0]),
+                                         __float_as_uint(rp[c1]), __float_as_uint(rp[8 * kBox + c1]), b0, b1);
+                            }
                         }
                     }
                 }
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int rb = mt * 16 + 8 * h;
-                    const float no = __shfl_sync(0xffffffffu, no_reg[rb >> 5], (rb + g) & 31);
-                    const uint32_t row = rb + g;
+                for (int u = 0; u < 2; ++u) {
+                    const int mt = mp + u;
 #pragma unroll
-                    for (int cq = 0; cq < 2; ++cq) {
-                        const uint32_t jj = 2 * tq + cq;
-                        if (row < nrows && jj < my_q) {
-                            const int j = warp * 8 + jj;
-                            const float nq = n_q[j];
-                            const float pt = no + nq - 2.f * d4[2 * h + cq];
-                            const float delta = kTcDelta * (no + nq);
-                            const uint32_t bit = 1u << (mt * 4 + h * 2 + cq);
-                            valid |= bit;
-                            if (!(pt - delta > thr_s[j * n_ckpt + ck])) pending |= bit;
-                            else if (ct.debug) {
-                                // debug: the filter's prune must agree with the exact prefix
-                                float xx = 0.f;
-                                for (int cc = 0; cc < c_dense; ++cc) {
-                                    const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
-                                    const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
-                                    for (uint32_t k = lo; k < hi; ++k) xx = sq_step(xx, bc[swz(row, k - lo)], q_res[k * kQS + j]);
+                    for (int h = 0; h < 2; ++h) {
+                        const int rb = mt * 16 + 8 * h;
+                        const float no = __shfl_sync(0xffffffffu, no_reg[rb >> 5], (rb + g) & 31);
+                        const uint32_t row = rb + g;
+#pragma unroll
+                        for (int cq = 0; cq < 2; ++cq) {
+                            const uint32_t jj = 2 * tq + cq;
+                            if (row < nrows && jj < my_q) {
+                                const int j = warp * 8 + jj;
+                                const float nq = n_q[j];
+                                const float pt = no + nq - 2.f * d4[u][2 * h + cq];
+                                const float delta = kTcDelta * (no + nq);
+                                const uint32_t bit = 1u << (mt * 4 + h * 2 + cq);
+                                valid |= bit;
+                                if (!(pt - delta > thr_s[j * n_ckpt + ck])) pending |= bit;
+                                else if (ct.debug) {
+                                    // debug: the filter's prune must agree with the exact prefix
+                                    float xx = 0.f;
+                                    for (int cc = 0; cc < c_dense; ++cc) {
+                                        const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
+                                        const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
+                                        for (uint32_t k = lo; k < hi; ++k) xx = sq_step(xx, bc[swz(row, k - lo)], q_res[k * kQS + j]);
+                                    }
+                                    if (!(xx > thr_s[j * n_ckpt + ck])) atomicAdd(a.counters + 3, 1ull);
                                 }
-                                if (!(xx > thr_s[j * n_ckpt + ck])) atomicAdd(a.counters + 3, 1ull);
                             }
                         }
                     }
                 }
             }
             st_dims += (unsigned long long)__popc(valid & ~pending) * d0;
-            from_prefix = true;
         } else if (has_sparse) {
             uint32_t dead = 0;
 #pragma unroll
@@ -612,92 +623,51 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
 
         PH_MARK(t_e1);
         PH_ADD(2, t_d1, t_e1);
-        // ---- sparse rounds: compact, advance exactly, merge --------------------
-        while (__any_sync(0xffffffffu, pending != 0)) {
-            PH_MARK(t_r0);
-            uint32_t n;
-            if constexpr (kTC) {
-                n = compact_round(
-                    pending, wl_meta, wl_acc, lane,
-                    [&](int b, uint32_t& row, uint32_t& jj) {
-                        row = (b >> 2) * 16 + ((b >> 1) & 1) * 8 + g;
-                        jj = 2 * tq + (b & 1);
-                    },
-                    [&](int) { return 0.f; });
-            } else {
-                n = compact_round(
-                    pending, wl_meta, wl_acc, lane,
-                    [&](int b, uint32_t& row, uint32_t& jj) {
-                        row = lane + 32 * (b >> 3);
-                        jj = b & 7;
-                    },
-                    [&](int b) {
-                        const uint64_t v = acc[b >> 3][(b & 7) >> 1];
-                        return (b & 1) ? hi_f(v) : lo_f(v);
-                    });
-            }
-            // one pair per lane: [exact dense prefix from smem] + remaining chunks from L2
+        // ---- survivors of the first checkpoint -----------------------------------
+        // advance(list, n): one pair per lane from chunk c_dense on, straight
+        // from L2 (each chunk one round trip), marking final candidates.
+        auto advance = [&](uint32_t* lm, float* la, uint32_t n) {
             for (uint32_t e = lane; e < n; e += 32) {
-                const uint32_t meta = wl_meta[e];
-                float x = wl_acc[e];
+                const uint32_t meta = lm[e];
+                float x = la[e];
                 const uint32_t row = meta & 0xffu, jj = (meta >> 8) & 0xffu, j = warp * 8 + jj;
                 bool live = true;
-                if (from_prefix) {
-                    for (int cc = 0; cc < c_dense; ++cc) {
-                        const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
-                        const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
-                        for (uint32_t k = lo; k < hi; k += 4) {
-                            const float4 o4 = *reinterpret_cast<const float4*>(bc + swz(row, k - lo));
-                            x = sq_step(x, o4.x, q_res[(k + 0) * kQS + j]);
-                            x = sq_step(x, o4.y, q_res[(k + 1) * kQS + j]);
-                            x = sq_step(x, o4.z, q_res[(k + 2) * kQS + j]);
-                            x = sq_step(x, o4.w, q_res[(k + 3) * kQS + j]);
+                const float* orow = a.storage + (size_t)(row_base + row) * dim;
+                const float* qrow = a.queries + (size_t)qidx_s[j] * dim;
+                for (int cc = c_dense; cc < ct.n_chunks; ++cc) {
+                    const uint32_t lo = ct.end[cc - 1], hi = ct.end[cc];
+                    if (vec && hi - lo == (uint32_t)kCH) {
+                        float4 o8[kCH / 4], q8[kCH / 4];
+#pragma unroll
+                        for (int v = 0; v < kCH / 4; ++v) {
+                            o8[v] = __ldg(reinterpret_cast<const float4*>(orow + lo) + v);
+                            q8[v] = __ldg(reinterpret_cast<const float4*>(qrow + lo) + v);
                         }
+#pragma unroll
+                        for (int v = 0; v < kCH / 4; ++v) {
+                            x = sq_step(x, o8[v].x, q8[v].x);
+                            x = sq_step(x, o8[v].y, q8[v].y);
+                            x = sq_step(x, o8[v].z, q8[v].z);
+                            x = sq_step(x, o8[v].w, q8[v].w);
+                        }
+                    } else if (vec) {
+                        for (uint32_t kk = lo; kk < hi; kk += 4) {
+                            const float4 o4 = __ldg(reinterpret_cast<const float4*>(orow + kk));
+                            const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + kk));
+                            x = sq_step(x, o4.x, q4.x);
+                            x = sq_step(x, o4.y, q4.y);
+                            x = sq_step(x, o4.z, q4.z);
+                            x = sq_step(x, o4.w, q4.w);
+                        }
+                    } else {
+                        for (uint32_t kk = lo; kk < hi; ++kk) x = sq_step(x, __ldg(orow + kk), __ldg(qrow + kk));
                     }
-                    if (x > thr_s[j * n_ckpt + ck]) {
-                        st_dims += d0;
+                    st_bytes += 8ull * (hi - lo);
+                    const int k2 = ct.ckpt[cc];
+                    if (k2 >= 0 && x > thr_s[j * n_ckpt + k2]) {
+                        st_dims += hi;
                         live = false;
-                    }
-                }
-                if (live) {
-                    const float* orow = a.storage + (size_t)(row_base + row) * dim;
-                    const float* qrow = a.queries + (size_t)qidx_s[j] * dim;
-                    for (int cc = c_dense; cc < ct.n_chunks; ++cc) {
-                        const uint32_t lo = ct.end[cc - 1], hi = ct.end[cc];
-                        if (vec && hi - lo == (uint32_t)kCH) {
-                            // whole chunk in flight at once: one L2 round trip
-                            float4 o8[kCH / 4], q8[kCH / 4];
-#pragma unroll
-                            for (int v = 0; v < kCH / 4; ++v) {
-                                o8[v] = __ldg(reinterpret_cast<const float4*>(orow + lo) + v);
-                                q8[v] = __ldg(reinterpret_cast<const float4*>(qrow + lo) + v);
-                            }
-#pragma unroll
-                            for (int v = 0; v < kCH / 4; ++v) {
-                                x = sq_step(x, o8[v].x, q8[v].x);
-                                x = sq_step(x, o8[v].y, q8[v].y);
-                                x = sq_step(x, o8[v].z, q8[v].z);
-                                x = sq_step(x, o8[v].w, q8[v].w);
-                            }
-                        } else if (vec) {
-                            for (uint32_t kk = lo; kk < hi; kk += 4) {
-                                const float4 o4 = __ldg(reinterpret_cast<const float4*>(orow + kk));
-                                const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + kk));
-                                x = sq_step(x, o4.x, q4.x);
-                                x = sq_step(x, o4.y, q4.y);
-                                x = sq_step(x, o4.z, q4.z);
-                                x = sq_step(x, o4.w, q4.w);
-                            }
-                        } else {
-                            for (uint32_t kk = lo; kk < hi; ++kk) x = sq_step(x, __ldg(orow + kk), __ldg(qrow + kk));
-                        }
-                        st_bytes += 8ull * (hi - lo);
-                        const int k2 = ct.ckpt[cc];
-                        if (k2 >= 0 && x > thr_s[j * n_ckpt + k2]) {
-                            st_dims += hi;
-                            live = false;
-                            break;
-                        }
+                        break;
                     }
                 }
                 bool is_cand = false;
@@ -707,24 +677,90 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                     is_cand = !(key > r_s[j]);
                     x = key;
                 }
-                wl_meta[e] = meta | (is_cand ? 0x80000000u : 0u);
-                wl_acc[e] = x;
+                lm[e] = meta | (is_cand ? 0x80000000u : 0u);
+                la[e] = x;
             }
             __syncwarp();
-            PH_MARK(t_r1);
-            PH_ADD(3, t_r0, t_r1);
-            merge_list_candidates(a, wl_meta, wl_acc, n, kb, row_base, warp, lane, qidx_s, slot_s, r_s, thr_s,
-                                  n_ckpt, st_bytes, ms);
-            PH_MARK(t_r2);
-            PH_ADD(4, t_r1, t_r2);
-        }
-        tighten_warp_radii(a, warp, lane, my_q, qidx_s, slot_s, r_s, thr_s, n_ckpt);
+            merge_list_candidates(a, lm, la, n, kb, row_base, warp, lane, qidx_s, slot_s, r_s, thr_s, n_ckpt,
+                                  st_bytes, ms);
+        };
+
         if constexpr (kTC) {
-            // the tile's boxes were read by the exact prefix: release them now
+            // stage 1: exact dense prefix of every pair the filter kept (from the
+            // resident boxes), survivors of the checkpoint into the s2 list ...
+            uint32_t n2 = 0;
+            while (__any_sync(0xffffffffu, pending != 0)) {
+                PH_MARK(t_r0);
+                const uint32_t n = compact_round(
+                    pending, wl_meta, wl_acc, lane,
+                    [&](int b, uint32_t& row, uint32_t& jj) {
+                        row = (b >> 2) * 16 + ((b >> 1) & 1) * 8 + g;
+                        jj = 2 * tq + (b & 1);
+                    },
+                    [&](int) { return 0.f; });
+                for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+                    const uint32_t e = e0 + lane;
+                    bool keep = false;
+                    uint32_t meta = 0;
+                    float x = 0.f;
+                    if (e < n) {
+                        meta = wl_meta[e];
+                        const uint32_t row = meta & 0xffu, j = warp * 8 + ((meta >> 8) & 0xffu);
+                        for (int cc = 0; cc < c_dense; ++cc) {
+                            const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
+                            const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
+                            for (uint32_t k = lo; k < hi; k += 4) {
+                                const float4 o4 = *reinterpret_cast<const float4*>(bc + swz(row, k - lo));
+                                x = sq_step(x, o4.x, q_res[(k + 0) * kQS + j]);
+                                x = sq_step(x, o4.y, q_res[(k + 1) * kQS + j]);
+                                x = sq_step(x, o4.z, q_res[(k + 2) * kQS + j]);
+                                x = sq_step(x, o4.w, q_res[(k + 3) * kQS + j]);
+                            }
+                        }
+                        keep = !(x > thr_s[j * n_ckpt + ck]);
+                        if (!keep) st_dims += d0;
+                    }
+                    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                    if (n2 + __popc(bal) > (uint32_t)kWarpList) {  // s2 full: drain it now
+                        advance(s2_meta, s2_acc, n2);
+                        n2 = 0;
+                    }
+                    if (keep) {
+                        const uint32_t pos = n2 + __popc(bal & ((1u << lane) - 1u));
+                        s2_meta[pos] = meta;
+                        s2_acc[pos] = x;
+                    }
+                    n2 += __popc(bal);
+                    __syncwarp();
+                }
+                PH_MARK(t_r1);
+                PH_ADD(3, t_r0, t_r1);
+            }
+            // ... release the tile's boxes (the producer can refill them while
+            // this warp waits on L2), then stage 2
             __syncwarp();
             if (lane == 0)
                 for (int cc = 0; cc < c_dense; ++cc) mbar_arrive(empty_bar + (s - (c_dense - 1) + cc) % n_buf);
+            PH_MARK(t_r2);
+            if (n2) advance(s2_meta, s2_acc, n2);
+            PH_MARK(t_r3);
+            PH_ADD(4, t_r2, t_r3);
+        } else {
+            while (__any_sync(0xffffffffu, pending != 0)) {
+                const uint32_t n = compact_round(
+                    pending, wl_meta, wl_acc, lane,
+                    [&](int b, uint32_t& row, uint32_t& jj) {
+                        row = lane + 32 * (b >> 3);
+                        jj = b & 7;
+                    },
+                    [&](int b) {
+                        const uint64_t v = acc[b >> 3][(b & 7) >> 1];
+                        return (b & 1) ? hi_f(v) : lo_f(v);
+                    });
+                advance(wl_meta, wl_acc, n);
+            }
         }
+        tighten_warp_radii(a, warp, lane, my_q, qidx_s, slot_s, r_s, thr_s, n_ckpt);
     }  // steps
 
     // ---- counters -------------------------------------------------------------
