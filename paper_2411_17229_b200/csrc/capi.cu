@@ -134,7 +134,7 @@ ChunkTable make_chunks(uint32_t dim, const std::vector<uint32_t>& cps) {
     ct.n_buf = tc ? std::max(4, 2 * ct.n_dense + 2) : 4;
     ct.use_tma = 0;  // decided per launch (needs a tensor map of the rows)
     const char* dbg = std::getenv("DADE_GPU_DEBUG");
-    ct.debug = (dbg && dbg[0] == '1') ? 1 : 0;
+    ct.debug = dbg ? std::atoi(dbg) : 0;
     return ct;
 }
 
@@ -159,6 +159,47 @@ bool make_row_tmap(CUtensorMap* m, const float* base, uint64_t rows, uint32_t di
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+
+bool make_1d_tmap(CUtensorMap* m, const float* base, uint64_t n) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                    &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            encode = nullptr;
+        if (!encode) return false;
+    }
+    if (n == 0 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    cuuint64_t gdim[1] = {n};
+    cuuint32_t box[1] = {(cuuint32_t)kRT};
+    cuuint32_t estride[1] = {1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<float*>(base), gdim, nullptr, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// First-slice row norms of a row set (the tensor-core filter's |o|^2), cached
+// per (rows, d0), plus their 1-D tensor map.
+struct RowNorms {
+    DevBuf buf;
+    const float* rows = nullptr;
+    uint32_t n = 0, dim = 0, d0 = 0;
+    bool tm_ok = false;
+    CUtensorMap map{};
+    const float* get(const float* r, uint32_t nn, uint32_t d, uint32_t dd0, cudaStream_t s) {
+        if (r != rows || nn != n || d != dim || dd0 != d0) {
+            buf.ensure((size_t)std::max<uint32_t>(nn, 1) * 4);
+            cuda_check(launch_row_norms(r, nn, d, dd0, buf.as<float>(), s), "row norms");
+            rows = r;
+            n = nn;
+            dim = d;
+            d0 = dd0;
+            tm_ok = make_1d_tmap(&map, buf.as<float>(), std::max<uint32_t>(nn, 1));
+        }
+        return buf.as<float>();
+    }
+};
 
 struct TmapCache {
     const float* base = nullptr;
@@ -214,9 +255,11 @@ struct dade_gpu_ctx {
     // workspaces
     DevBuf q_in, q_rot, probes, probe_count, c_seg_keys, c_seg_count, c_r;
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
-    DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts;
+    DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
     DevBuf counters, phase;
     TmapCache tm_centroids, tm_storage, tm_base;
+    RowNorms norms_storage, norms_base;
+    CUtensorMap tm_none{};
 
     // profiling
     bool profiling = false;
@@ -300,11 +343,16 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
     bool tma = false;
     const CUtensorMap& tm = c->tm_centroids.get(a.storage, c->n_clusters, c->dim, tma);
     ct.use_tma = (tma && ct.vec_ok) ? 1 : 0;
-    cuda_check(launch_scan(a, ct, tm, nb * qchunks, /*sqrt_key=*/false, s), "coarse scan");
+    cuda_check(launch_scan(a, ct, tm, c->tm_none, nb * qchunks, /*sqrt_key=*/false, s), "coarse scan");
     cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, nb, n_probe, c->probes.as<uint64_t>(),
                                      c->probe_count.as<uint32_t>(), s),
                "coarse merge");
     c->launches += 3;
+}
+
+bool seed_disabled() {
+    const char* e = std::getenv("DADE_GPU_NO_SEED");
+    return e && e[0] == '1';
 }
 
 unsigned long long* phase_ptr(dade_gpu_ctx* c) {
@@ -363,7 +411,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     c->bucket_q.ensure((size_t)nq * n_probe * 4);
     c->bucket_slot.ensure((size_t)nq * n_probe * 4);
     c->items.ensure(max_items * sizeof(WorkItem));
-    c->n_items.ensure(4);
+    c->n_items.ensure(8);
     g.counts = c->g_counts.as<uint32_t>();
     g.cursor = c->g_cursor.as<uint32_t>();
     g.bucket_off = c->g_boff.as<uint32_t>();
@@ -404,8 +452,41 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     bool tma = false;
     const CUtensorMap& tm = c->tm_storage.get(a.storage, std::max<uint32_t>(c->count, 1), c->dim, tma);
     ct.use_tma = (tma && ct.vec_ok && c->count > 0) ? 1 : 0;
-    record(c, c->e1);
-    cuda_check(launch_scan(a, ct, tm, (uint32_t)max_items, true, s), "dco scan");
+    // Radius seeding: an exact (FD) pass over the first rows of every query's
+    // nearest list gives each query a K-th distance before the main scan, so
+    // no tile starts at r = +inf. Its top-K is discarded (the main scan
+    // re-reads those rows); only the atomicMin'd radius is kept. Any K-th
+    // distance of a subset of the probed candidates bounds the final radius.
+    if (n_probe > 1 && !seed_disabled()) {
+        const uint32_t seed_rows = std::max<uint32_t>(kRT, (2 * k + kRT - 1) / kRT * kRT);
+        c->seed_keys.ensure((size_t)nq * k * 8);
+        c->seed_count.ensure((size_t)nq * 4);
+        cuda_check(cudaMemsetAsync(c->seed_count.p, 0, (size_t)nq * 4, s), "memset");
+        ScanArgs sa = a;
+        sa.n_items = g.n_items + 1;
+        sa.seg_keys = c->seed_keys.as<uint64_t>();
+        sa.seg_count = c->seed_count.as<uint32_t>();
+        sa.n_slots = 1;
+        sa.seed = 1;
+        sa.max_rows = seed_rows;
+        sa.counters = nullptr;
+        sa.phase = nullptr;
+        ChunkTable sct = make_chunks(c->dim, {});
+        sct.use_tma = ct.use_tma;
+        const size_t max_rb0 = (nq + kQC - 1) / kQC + c->n_clusters;
+        record(c, c->e1);
+        cuda_check(launch_scan(sa, sct, tm, c->tm_none, (uint32_t)max_rb0, true, s), "seed scan");
+        ++c->launches;
+    } else {
+        record(c, c->e1);
+    }
+    const CUtensorMap* tn = &c->tm_none;
+    if (ct.use_tc) {
+        a.row_norms = c->norms_storage.get(a.storage, c->count, c->dim, ct.end[ct.n_dense - 1], s);
+        if (c->norms_storage.tm_ok) tn = &c->norms_storage.map;
+        else ct.use_tma = 0;
+    }
+    cuda_check(launch_scan(a, ct, tm, *tn, (uint32_t)max_items, true, s), "dco scan");
     record(c, c->e2);
     cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, n_probe, k, out_keys, out_count, s),
                "merge");
@@ -456,7 +537,13 @@ void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t
     const CUtensorMap& tm = c->tm_base.get(a.storage, std::max<uint32_t>(c->b_count, 1), c->b_dim, tma);
     ct.use_tma = (tma && ct.vec_ok && c->b_count > 0) ? 1 : 0;
     record(c, c->e1);
-    cuda_check(launch_scan(a, ct, tm, nb * qchunks, true, s), "flat scan");
+    const CUtensorMap* tn = &c->tm_none;
+    if (ct.use_tc) {
+        a.row_norms = c->norms_base.get(a.storage, c->b_count, c->b_dim, ct.end[ct.n_dense - 1], s);
+        if (c->norms_base.tm_ok) tn = &c->norms_base.map;
+        else ct.use_tma = 0;
+    }
+    cuda_check(launch_scan(a, ct, tm, *tn, nb * qchunks, true, s), "flat scan");
     record(c, c->e2);
     cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, nb, k, out_keys, out_count, s), "merge");
     c->launches += 3;
@@ -565,6 +652,8 @@ int dade_gpu_destroy(dade_gpu_ctx* c) {
         if (!c) return;
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
+        c->norms_storage.buf.release();
+        c->norms_base.buf.release();
         DevBuf* bufs[] = {&c->W, &c->centroids, &c->storage, &c->ids, &c->offsets, &c->base,
                           &c->d_cps, &c->d_coeff, &c->d_scale, &c->q_in, &c->q_rot, &c->probes,
                           &c->probe_count, &c->c_seg_keys, &c->c_seg_count, &c->c_r, &c->g_counts,
@@ -656,6 +745,7 @@ int dade_gpu_set_ivf(dade_gpu_ctx* c, uint32_t dim, uint32_t count, uint32_t n_c
         c->dim = dim;
         c->count = count;
         c->n_clusters = n_clusters;
+        c->norms_storage.rows = nullptr;
         c->h_offsets.assign(offsets, offsets + n_clusters + 1);
         c->dev_offsets = c->h_offsets;
         c->has_ivf = true;
@@ -703,6 +793,7 @@ int dade_gpu_set_ivf_shard(dade_gpu_ctx* c, const uint8_t* mask) {
         cuda_check(cudaStreamSynchronize(c->stream), "shard");
         c->dev_offsets = dev;
         c->count = (uint32_t)rows;
+        c->norms_storage.rows = nullptr;
     });
 }
 
@@ -713,6 +804,7 @@ int dade_gpu_set_base(dade_gpu_ctx* c, uint32_t dim, uint32_t count, const float
         c->use_device();
         upload(c->base, data, (size_t)count * dim * 4, c->stream);
         cuda_check(cudaStreamSynchronize(c->stream), "base upload");
+        c->norms_base.rows = nullptr;
         c->b_dim = dim;
         c->b_count = count;
         c->b_id_base = id_base;

@@ -31,11 +31,15 @@ struct ScanArgs {
     uint64_t neg_zero2;      // 0x8000000080000000 (opaque to ptxas)
     unsigned long long* counters;  // [3] total_dco, dims_accumulated, bytes
     unsigned long long* phase;     // nullable: per-phase clocks (debug)
+    uint32_t max_rows;             // nonzero: scan only the first max_rows rows of each item
+    int seed;                      // radius-seeding pass: every query writes slot 0
+    const float* row_norms;        // [rows] first-slice |o|^2 (tensor-core filter only)
 };
 
 size_t scan_smem_bytes(int n_ckpt, int d_res, int n_buf);
-cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tmap, uint32_t grid,
-                        bool sqrt_key, cudaStream_t s);
+cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tmap,
+                        const CUtensorMap& tmap_norms, uint32_t grid, bool sqrt_key, cudaStream_t s);
+cudaError_t launch_row_norms(const float* rows, uint32_t n, uint32_t dim, uint32_t d0, float* out, cudaStream_t s);
 cudaError_t launch_merge_segments(const uint64_t* seg_keys, const uint32_t* seg_count, uint32_t nq,
                                   uint32_t n_slots, uint32_t K, uint64_t* out_keys,
                                   uint32_t* out_count, cudaStream_t s);
@@ -65,7 +69,7 @@ struct GroupArgs {
     uint32_t* bucket_q;             // [nq * n_probe]
     uint32_t* bucket_slot;          // [nq * n_probe]
     WorkItem* items;                // [max_items]
-    uint32_t* n_items;              // [1]
+    uint32_t* n_items;              // [2]: all items, rank-bucket-0 items
 };
 cudaError_t launch_group(const GroupArgs& g, cudaStream_t s);
 

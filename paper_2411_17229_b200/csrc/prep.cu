@@ -100,7 +100,10 @@ __global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
         rb += c;
         ri += (c + kQC - 1) / kQC;
     }
-    if (threadIdx.x == 1023) *g.n_items = s_i[1023];
+    if (threadIdx.x == 1023) g.n_items[0] = s_i[1023];
+    __syncthreads();
+    // items of rank bucket 0 (every query's nearest list) come first
+    if (threadIdx.x == 0) g.n_items[1] = g.n_rb > 1 ? g.item_off[g.n_lists] : s_i[1023];
 }
 
 __global__ void group_scatter_kernel(const GroupArgs g) {

@@ -48,7 +48,7 @@ constexpr int kWarpList = 128;  // survivor-list entries per warp per round
 constexpr float kTcDelta = 4e-3f;
 
 struct SmemLayout {
-    size_t slots, q_res, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, s2_meta, s2_acc, keys, mscratch, bars, total;
+    size_t slots, norms, q_res, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, s2_meta, s2_acc, keys, mscratch, bars, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -65,6 +65,7 @@ __host__ __device__ inline SmemLayout smem_layout(int n_ckpt, int d_res, int n_b
     size_t off = 0;
     L.slots = off; off = align16(off + slot_bytes(d_res) * n_buf);
     off = (off + 1023) & ~size_t(1023);
+    L.norms = off; off = align16(off + sizeof(float) * kRT * n_buf);
     L.q_res = off; off = align16(off + sizeof(float) * (size_t)d_res * kQS);
     L.n_q = off; off = align16(off + sizeof(float) * kQC);
     L.r_s = off; off = align16(off + sizeof(float) * kQC);
@@ -104,10 +105,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(0x10000)  // suspend-time hint (ns): sleep instead of spinning
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, int x, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
@@ -126,6 +134,15 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return r;
+}
+
+// A fragment of m16n8k8.tf32 straight from a 128B-swizzled box: ldmatrix.x4
+// treats each 8 x 16-byte sub-tile as 8 rows x 4 fp32 (thread t gets row t/4,
+// word t%4), which is exactly a0..a3 = A[g][tq], A[g+8][tq], A[g][tq+4], A[g+8][tq+4].
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr));
 }
 
 // D += A(16x8, row) * B(8x8, col), TF32 in, FP32 accumulate.
@@ -269,7 +286,8 @@ __device__ __forceinline__ uint32_t compact_round(uint32_t& pending, uint32_t* w
 // CTA barrier every step.
 template <bool kSqrtKey, bool kTC>
 __global__ void __launch_bounds__(kThreadsTotal, 2)
-dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const __grid_constant__ CUtensorMap tmap) {
+dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const __grid_constant__ CUtensorMap tmap,
+                const __grid_constant__ CUtensorMap tmap_n) {
     extern __shared__ unsigned char smem_raw[];
     // 1024-byte aligned base derived by pointer arithmetic (keeps the shared
     // address space visible to the compiler -> LDS, not generic loads)
@@ -288,6 +306,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* empty_bar = full_bar + n_buf;
     auto slot_o = [&](uint32_t sl) { return reinterpret_cast<float*>(smem + L.slots + sl * sbytes); };
+    float* norms_s = reinterpret_cast<float*>(smem + L.norms);
     auto slot_q = [&](uint32_t sl) { return reinterpret_cast<float*>(smem + L.slots + sl * sbytes + (size_t)kRT * kBox * 4); };
 
     const int tid = threadIdx.x;
@@ -319,6 +338,8 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
         }
     }
     if (tid < kQC && tid >= (int)qcount) { qidx_s[tid] = 0; slot_s[tid] = 0; }
+    if (a.seed && tid < kQC) slot_s[tid] = 0;
+    if (a.max_rows) row_count = min(row_count, a.max_rows);
     if (tid < kQC) r_s[tid] = __int_as_float(0x7f800000);
     if (tid == 0) {
         for (int i = 0; i < n_buf; ++i) {
@@ -360,13 +381,18 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                 st_bytes += 4ull * w * qcount;
             }
             float* ob = slot_o(sl);
+            const bool want_norms = kTC && c == 0;  // first-slice row norms ride with chunk 0
             if (ct.use_tma) {
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(full_bar + sl, kRT * kBox * 4);
+                    mbar_arrive_expect_tx(full_bar + sl, kRT * kBox * 4 + (want_norms ? kRT * 4 : 0));
                     tma_load_2d(ob, &tmap, (int)k0, (int)(row_start + tb), full_bar + sl);
+                    if (want_norms) tma_load_1d(norms_s + sl * kRT, &tmap_n, (int)(row_start + tb), full_bar + sl);
                 }
             } else {
+                if (want_norms)
+                    for (uint32_t r = lane; r < (uint32_t)kRT; r += 32)
+                        norms_s[sl * kRT + r] = r < nrows ? __ldg(a.row_norms + row_start + tb + r) : 0.f;
                 for (uint32_t idx = lane; idx < (uint32_t)kRT * kBox; idx += 32) {
                     const uint32_t r = idx / kBox, cc = idx - r * kBox;
                     ob[swz(r, cc)] = (r < nrows && cc < w) ? __ldg(a.storage + (size_t)(row_start + tb + r) * dim + k0 + cc) : 0.f;
@@ -483,47 +509,54 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
         const uint32_t row_base = row_start + tb;
         uint32_t pending = 0;  // pairs needing the exact / sparse path
         if constexpr (kTC) {
-            // first-slice squared norms of this lane's rows l + 32i
-            float no_reg[4];
+            // Tensor-core dot products o . q over the dense dims (ldmatrix A
+            // fragments from the swizzled boxes, B from the resident queries),
+            // then the filter per pair:
+            //   prune for sure  iff  (1 - delta)(|o|^2 + |q|^2) - 2 o.q > thr
+            // (|o|^2 precomputed per row, |q|^2 per query); everything else is
+            // decided exactly below. Operands are fed as raw fp32 bits: the
+            // tensor core reads them as TF32, which kTcDelta accounts for.
+            const float* nrm = norms_s + ((s - (c_dense - 1)) % n_buf) * kRT;
+            float nqp[2], thq[2];
+            uint32_t qmask = 0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) no_reg[i] = 0.f;
-            for (int cc = 0; cc < c_dense; ++cc) {
-                const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
-                const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], wc = ct.end[cc] - lo;
-                for (uint32_t k4 = 0; k4 < wc; k4 += 4) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float4 v = *reinterpret_cast<const float4*>(bc + swz(lane + 32 * i, k4));
-                        no_reg[i] = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, no_reg[i]))));
-                    }
-                }
+            for (int cq = 0; cq < 2; ++cq) {
+                const uint32_t jj = 2 * tq + cq;
+                const int j = warp * 8 + jj;
+                const bool ok = jj < my_q;
+                nqp[cq] = ok ? (1.f - kTcDelta) * n_q[j] : 0.f;
+                thq[cq] = ok ? thr_s[j * n_ckpt + ck] : -__int_as_float(0x7f800000);
+                if (ok) qmask |= 0x33333333u & (0x11111111u << cq);
             }
-            // Tensor-core dot products o . q over the dense dims, one 16-row
-            // m-tile at a time (4 live accumulators), then the filter: prune for
-            // sure iff p~ - delta > thr; everything else is decided exactly.
-            // Operands are fed as raw fp32 bits: the tensor core reads them as
-            // TF32 (low mantissa bits ignored), which kTcDelta accounts for.
-            uint32_t valid = 0;
+            uint32_t valid = qmask;
+            if (nrows < (uint32_t)kRT) {
+#pragma unroll
+                for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if ((uint32_t)(mt * 16 + 8 * h + g) >= nrows) valid &= ~(3u << (mt * 4 + h * 2));
+            }
+            const int sm = lane >> 3, rr = lane & 7;  // ldmatrix: sub-matrix and row this lane addresses
 #pragma unroll 1
             for (int mp = 0; mp < 8; mp += 2) {
                 float d4[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
                 if (my_q > 0 && (uint32_t)(mp * 16) < nrows) {
                     for (int cc = 0; cc < c_dense; ++cc) {
-                        const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
+                        const uint32_t sb = smem_u32(slot_o((s - (c_dense - 1) + cc) % n_buf));
                         const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], wc = ct.end[cc] - lo;
-                        // rows mp*16 + g (+8, +16, +24) all have row % 8 == g
-                        const float* rowp = bc + (mp * 16 + g) * kBox + tq;
                         const float* qcol = q_res + (lo + tq) * kQS + warp * 8 + g;
+                        const uint32_t rowa = (uint32_t)(mp * 16 + (sm & 1) * 8 + rr);
 #pragma unroll 4
                         for (uint32_t ks = 0; ks < wc; ks += 8) {
-                            const int c0 = (int)(((ks >> 2) ^ g) << 2), c1 = (int)((((ks >> 2) + 1) ^ g) << 2);
                             const uint32_t b0 = __float_as_uint(qcol[ks * kQS]);
                             const uint32_t b1 = __float_as_uint(qcol[(ks + 4) * kQS]);
+                            const uint32_t chunk = (ks >> 2) + (sm >> 1);
 #pragma unroll
                             for (int u = 0; u < 2; ++u) {
-                                const float* rp = rowp + u * 16 * kBox;
-                                mma_tf32(d4[u], __float_as_uint(rp[c0]), __float_as_uint(rp[8 * kBox + c0]),
-                                         __float_as_uint(rp[c1]), __float_as_uint(rp[8 * kBox + c1]), b0, b1);
+                                const uint32_t row = rowa + 16 * u;
+                                uint32_t a0, a1, a2, a3;
+                                ldsm_x4(sb + row * (kBox * 4) + ((chunk ^ (row & 7)) << 4), a0, a1, a2, a3);
+                                mma_tf32(d4[u], a0, a1, a2, a3, b0, b1);
                             }
                         }
                     }
@@ -533,35 +566,34 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                     const int mt = mp + u;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const int rb = mt * 16 + 8 * h;
-                        const float no = __shfl_sync(0xffffffffu, no_reg[rb >> 5], (rb + g) & 31);
-                        const uint32_t row = rb + g;
+                        const float nop = (1.f - kTcDelta) * nrm[mt * 16 + 8 * h + g];
 #pragma unroll
                         for (int cq = 0; cq < 2; ++cq) {
-                            const uint32_t jj = 2 * tq + cq;
-                            if (row < nrows && jj < my_q) {
-                                const int j = warp * 8 + jj;
-                                const float nq = n_q[j];
-                                const float pt = no + nq - 2.f * d4[u][2 * h + cq];
-                                const float delta = kTcDelta * (no + nq);
-                                const uint32_t bit = 1u << (mt * 4 + h * 2 + cq);
-                                valid |= bit;
-                                if (!(pt - delta > thr_s[j * n_ckpt + ck])) pending |= bit;
-                                else if (ct.debug) {
-                                    // debug: the filter's prune must agree with the exact prefix
-                                    float xx = 0.f;
-                                    for (int cc = 0; cc < c_dense; ++cc) {
-                                        const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
-                                        const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
-                                        for (uint32_t k = lo; k < hi; ++k) xx = sq_step(xx, bc[swz(row, k - lo)], q_res[k * kQS + j]);
-                                    }
-                                    if (!(xx > thr_s[j * n_ckpt + ck])) atomicAdd(a.counters + 3, 1ull);
-                                }
-                            }
+                            const float lhs = fmaf(-2.f, d4[u][2 * h + cq], nop + nqp[cq]);
+                            if (!(lhs > thq[cq])) pending |= 1u << (mt * 4 + h * 2 + cq);
                         }
                     }
                 }
             }
+            pending &= valid;
+            if (ct.debug == 1) {
+                // debug: every filter prune must agree with the exact prefix
+                uint32_t pruned = valid & ~pending;
+                while (pruned) {
+                    const int b = __ffs(pruned) - 1;
+                    pruned &= pruned - 1;
+                    const uint32_t row = (b >> 2) * 16 + ((b >> 1) & 1) * 8 + g;
+                    const int j = warp * 8 + 2 * tq + (b & 1);
+                    float xx = 0.f;
+                    for (int cc = 0; cc < c_dense; ++cc) {
+                        const float* bc = slot_o((s - (c_dense - 1) + cc) % n_buf);
+                        const uint32_t lo = cc == 0 ? 0u : ct.end[cc - 1], hi = ct.end[cc];
+                        for (uint32_t k = lo; k < hi; ++k) xx = sq_step(xx, bc[swz(row, k - lo)], q_res[k * kQS + j]);
+                    }
+                    if (!(xx > thr_s[j * n_ckpt + ck])) atomicAdd(a.counters + 3, 1ull);
+                }
+            }
+            if (ct.debug == 2) pending = 0;  // experiment: filter only
             st_dims += (unsigned long long)__popc(valid & ~pending) * d0;
         } else if (has_sparse) {
             uint32_t dead = 0;
@@ -869,22 +901,40 @@ __global__ void keys_to_results_kernel(const uint64_t* __restrict__ keys, const 
 size_t scan_smem_bytes(int n_ckpt, int d_res, int n_buf) { return smem_layout(n_ckpt, d_res, n_buf).total; }
 
 template <bool kSqrtKey, bool kTC>
-static cudaError_t launch_scan_t(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tm, uint32_t grid,
-                                 size_t smem, cudaStream_t s) {
+static cudaError_t launch_scan_t(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tm,
+                                 const CUtensorMap& tn, uint32_t grid, size_t smem, cudaStream_t s) {
     DADE_CUDA_TRY(cudaFuncSetAttribute(dco_scan_kernel<kSqrtKey, kTC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-    dco_scan_kernel<kSqrtKey, kTC><<<grid, kThreadsTotal, smem, s>>>(a, ct, tm);
+    dco_scan_kernel<kSqrtKey, kTC><<<grid, kThreadsTotal, smem, s>>>(a, ct, tm, tn);
     return cudaGetLastError();
 }
 
-cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tm, uint32_t grid,
-                        bool sqrt_key, cudaStream_t s) {
+cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tm, const CUtensorMap& tn,
+                        uint32_t grid, bool sqrt_key, cudaStream_t s) {
     if (grid == 0) return cudaSuccess;
     const size_t smem = scan_smem_bytes(ct.n_ckpt, ct.d_res, ct.n_buf);
-    if (sqrt_key) return ct.use_tc ? launch_scan_t<true, true>(a, ct, tm, grid, smem, s)
-                                   : launch_scan_t<true, false>(a, ct, tm, grid, smem, s);
-    return ct.use_tc ? launch_scan_t<false, true>(a, ct, tm, grid, smem, s)
-                     : launch_scan_t<false, false>(a, ct, tm, grid, smem, s);
+    if (sqrt_key) return ct.use_tc ? launch_scan_t<true, true>(a, ct, tm, tn, grid, smem, s)
+                                   : launch_scan_t<true, false>(a, ct, tm, tn, grid, smem, s);
+    return ct.use_tc ? launch_scan_t<false, true>(a, ct, tm, tn, grid, smem, s)
+                     : launch_scan_t<false, false>(a, ct, tm, tn, grid, smem, s);
+}
+
+// First-slice squared norms |o[0:d0]|^2 of every row (fp32 fma; any rounding
+// is covered by the filter's error budget).
+__global__ void row_norms_kernel(const float* __restrict__ rows, uint32_t n, uint32_t dim, uint32_t d0,
+                                 float* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* r = rows + (size_t)i * dim;
+    float acc = 0.f;
+    for (uint32_t k = 0; k < d0; ++k) acc = fmaf(r[k], r[k], acc);
+    out[i] = acc;
+}
+
+cudaError_t launch_row_norms(const float* rows, uint32_t n, uint32_t dim, uint32_t d0, float* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    row_norms_kernel<<<(n + 255) / 256, 256, 0, s>>>(rows, n, dim, d0, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_merge_segments(const uint64_t* seg_keys, const uint32_t* seg_count, uint32_t nq,
