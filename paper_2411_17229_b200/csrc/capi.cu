@@ -172,11 +172,14 @@ bool make_1d_tmap(CUtensorMap* m, const float* base, uint64_t n) {
     }
     if (n == 0 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
     cuuint64_t gdim[1] = {n};
+    cuuint64_t gstride[1] = {n * 4};  // unused for rank 1, but must be a valid array
     cuuint32_t box[1] = {(cuuint32_t)kRT};
     cuuint32_t estride[1] = {1};
-    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<float*>(base), gdim, nullptr, box, estride,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<float*>(base), gdim, gstride, box,
+                              estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS && std::getenv("DADE_GPU_VERBOSE")) std::fprintf(stderr, "[dade_gpu] 1d tmap error %d\n", (int)r);
+    return r == CUDA_SUCCESS;
 }
 
 // First-slice row norms of a row set (the tensor-core filter's |o|^2), cached
@@ -189,13 +192,16 @@ struct RowNorms {
     CUtensorMap map{};
     const float* get(const float* r, uint32_t nn, uint32_t d, uint32_t dd0, cudaStream_t s) {
         if (r != rows || nn != n || d != dim || dd0 != d0) {
-            buf.ensure((size_t)std::max<uint32_t>(nn, 1) * 4);
+            // padded by 8 floats: the kernel reads 16-byte aligned windows
+            buf.ensure(((size_t)nn + 8) * 4);
+            cuda_check(cudaMemsetAsync(buf.p, 0, ((size_t)nn + 8) * 4, s), "memset");
             cuda_check(launch_row_norms(r, nn, d, dd0, buf.as<float>(), s), "row norms");
             rows = r;
             n = nn;
             dim = d;
             d0 = dd0;
-            tm_ok = make_1d_tmap(&map, buf.as<float>(), std::max<uint32_t>(nn, 1));
+            tm_ok = true;  // windows are fetched with a plain bulk copy
+            if (std::getenv("DADE_GPU_VERBOSE")) std::fprintf(stderr, "[dade_gpu] row norms n=%u d0=%u tmap=%d\n", nn, dd0, (int)tm_ok);
         }
         return buf.as<float>();
     }
@@ -213,6 +219,7 @@ struct TmapCache {
             rows = r;
             dim = d;
             ok = make_row_tmap(&map, b, r, d);
+            if (std::getenv("DADE_GPU_VERBOSE")) std::fprintf(stderr, "[dade_gpu] row tmap rows=%llu dim=%u ok=%d\n", (unsigned long long)r, d, (int)ok);
         }
         const char* env = std::getenv("DADE_GPU_NO_TMA");
         usable = ok && !(env && env[0] == '1');
@@ -256,6 +263,7 @@ struct dade_gpu_ctx {
     DevBuf q_in, q_rot, probes, probe_count, c_seg_keys, c_seg_count, c_r;
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
+    DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket;
     DevBuf counters, phase;
     TmapCache tm_centroids, tm_storage, tm_base;
     RowNorms norms_storage, norms_base;
@@ -348,6 +356,11 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
                                      c->probe_count.as<uint32_t>(), s),
                "coarse merge");
     c->launches += 3;
+}
+
+bool env_flag(const char* name) {
+    const char* e = std::getenv(name);
+    return e && e[0] == '1';
 }
 
 bool seed_disabled() {
@@ -448,6 +461,8 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
     a.phase = phase_ptr(c);
+    if (const char* dbg = std::getenv("DADE_GPU_DEBUG"))
+        if (std::atoi(dbg) == 3) a.census = c->counters.as<unsigned long long>() + 3;
     ChunkTable ct = make_chunks(c->dim, c->cps);
     bool tma = false;
     const CUtensorMap& tm = c->tm_storage.get(a.storage, std::max<uint32_t>(c->count, 1), c->dim, tma);
@@ -486,11 +501,69 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
         if (c->norms_storage.tm_ok) tn = &c->norms_storage.map;
         else ct.use_tma = 0;
     }
+    // Streaming mode (tensor-core filter): the scan hands first-checkpoint
+    // survivors to advance_survivors_kernel instead of chasing them itself.
+    const bool streaming = ct.use_tc && ct.n_ckpt <= 63 && !env_flag("DADE_GPU_NO_STREAM");
+    uint32_t cap = 0;
+    if (streaming) {
+        cap = (uint32_t)std::min<uint64_t>(64ull << 20, std::max<uint64_t>(1u << 20, (uint64_t)nq * 1024));
+        c->surv.ensure((size_t)cap * sizeof(Survivor));
+        c->surv_count.ensure(4);
+        cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
+        a.surv = c->surv.as<Survivor>();
+        a.surv_count = c->surv_count.as<uint32_t>();
+        a.surv_cap = cap;
+    }
     cuda_check(launch_scan(a, ct, tm, *tn, (uint32_t)max_items, true, s), "dco scan");
+    if (streaming) {
+        c->cand_q.ensure((size_t)cap * 4);
+        c->cand_key.ensure((size_t)cap * 8);
+        c->cand_count.ensure(4);
+        c->q_count.ensure((size_t)nq * 4);
+        c->q_off.ensure((size_t)nq * 4);
+        c->q_cursor.ensure((size_t)nq * 4);
+        c->bucket.ensure((size_t)cap * 8);
+        cuda_check(cudaMemsetAsync(c->cand_count.p, 0, 4, s), "memset");
+        cuda_check(cudaMemsetAsync(c->q_count.p, 0, (size_t)nq * 4, s), "memset");
+        SurvArgs sv{};
+        sv.surv = a.surv;
+        sv.surv_count = a.surv_count;
+        sv.surv_cap = cap;
+        sv.storage = a.storage;
+        sv.row_ids = a.row_ids;
+        sv.id_base = a.id_base;
+        sv.dim = c->dim;
+        sv.queries = d_q;
+        sv.r_global = a.r_global;
+        sv.coeff = a.coeff;
+        sv.n_dense_dims = ct.end[ct.n_dense - 1];
+        sv.n_ckpt = ct.n_ckpt;
+        for (int i = 0; i < ct.n_ckpt; ++i) sv.cps[i] = (uint16_t)c->cps[i];
+        sv.first_ckpt = 1;
+        sv.cand_q = c->cand_q.as<uint32_t>();
+        sv.cand_key = c->cand_key.as<uint64_t>();
+        sv.cand_count = c->cand_count.as<uint32_t>();
+        sv.cand_cap = cap;
+        sv.q_count = c->q_count.as<uint32_t>();
+        sv.counters = a.counters;
+        cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
+        c->launches += 1;
+    }
     record(c, c->e2);
     cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, n_probe, k, out_keys, out_count, s),
                "merge");
     c->launches += 3;
+    if (streaming) {
+        cuda_check(launch_bucket_candidates(c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
+                                            c->cand_count.as<uint32_t>(), cap, c->q_count.as<uint32_t>(),
+                                            c->q_off.as<uint32_t>(), c->q_cursor.as<uint32_t>(),
+                                            c->bucket.as<uint64_t>(), nq, cap, s),
+                   "bucket candidates");
+        cuda_check(launch_merge_buckets(c->bucket.as<uint64_t>(), c->q_off.as<uint32_t>(), c->q_count.as<uint32_t>(),
+                                        nq, k, out_keys, out_count, s),
+                   "merge buckets");
+        c->launches += 3;
+    }
 }
 
 void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint64_t* out_keys,

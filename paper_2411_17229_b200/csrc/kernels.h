@@ -9,6 +9,15 @@
 
 namespace dade_gpu {
 
+// A pair that passed the first checkpoint exactly, handed from the streaming
+// filter to the survivor kernel: storage row, query, slot and its partial sum.
+struct Survivor {
+    uint32_t q;    // query index (UINT32_MAX = empty entry)
+    uint32_t row;  // device storage row
+    float acc;     // exact partial over the dense dims
+    uint32_t slot;
+};
+
 struct ScanArgs {
     const float* storage;    // device rows [*, dim], contiguous
     const uint32_t* row_ids; // nullable: ids = id_base + row
@@ -34,9 +43,43 @@ struct ScanArgs {
     uint32_t max_rows;             // nonzero: scan only the first max_rows rows of each item
     int seed;                      // radius-seeding pass: every query writes slot 0
     const float* row_norms;        // [rows] first-slice |o|^2 (tensor-core filter only)
+    unsigned long long* census;    // nullable debug: [0] merges, [1] merged candidates
+    Survivor* surv;                // nullable: hand first-checkpoint survivors to advance_survivors
+    uint32_t* surv_count;
+    uint32_t surv_cap;
 };
 
 size_t scan_smem_bytes(int n_ckpt, int d_res, int n_buf);
+
+// Survivor kernel (stage 2 of the streaming scan) and candidate bucketing.
+struct SurvArgs {
+    const Survivor* surv;
+    const uint32_t* surv_count;
+    uint32_t surv_cap;
+    const float* storage;
+    const uint32_t* row_ids;
+    uint32_t id_base;
+    uint32_t dim;
+    const float* queries;
+    const uint32_t* r_global;
+    const double* coeff;
+    uint32_t n_dense_dims;        // d0
+    uint32_t n_ckpt;
+    uint16_t cps[64];             // checkpoint dims (those > d0 are tested here)
+    uint32_t first_ckpt;          // index of the first checkpoint after d0
+    uint32_t* cand_q;             // candidates: query ...
+    uint64_t* cand_key;           // ... and (dist, id) key
+    uint32_t* cand_count;
+    uint32_t cand_cap;
+    uint32_t* q_count;            // per-query candidate counts
+    unsigned long long* counters; // [1] dims
+};
+cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cudaStream_t s);
+cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
+                                     uint32_t cand_cap, uint32_t* q_count, uint32_t* q_off, uint32_t* q_cursor,
+                                     uint64_t* bucket, uint32_t nq, uint32_t max_cands, cudaStream_t s);
+cudaError_t launch_merge_buckets(const uint64_t* bucket, const uint32_t* q_off, const uint32_t* q_count, uint32_t nq,
+                                 uint32_t K, uint64_t* out_keys, uint32_t* out_count, cudaStream_t s);
 cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tmap,
                         const CUtensorMap& tmap_norms, uint32_t grid, bool sqrt_key, cudaStream_t s);
 cudaError_t launch_row_norms(const float* rows, uint32_t n, uint32_t dim, uint32_t d0, float* out, cudaStream_t s);

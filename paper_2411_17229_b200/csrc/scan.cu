@@ -25,6 +25,7 @@
 // Warp w owns queries [8w, 8w+8) of the chunk for the whole item, so after
 // the per-step __syncthreads that guards the o-tile double buffer, all
 // survivor / candidate / merge work is warp-local.
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 
@@ -36,6 +37,7 @@ namespace dade_gpu {
 namespace {
 
 constexpr int kWarpList = 128;  // survivor-list entries per warp per round
+constexpr int kNormWin = kRT + 4;  // 16-byte aligned window of row norms per box
 
 // Relative error budget of the TF32 filter: |p~ - acc| <= kTcDelta * (|o|^2 + |q|^2)
 // over the first slice. Derivation: fp32 operands read as TF32
@@ -65,7 +67,7 @@ __host__ __device__ inline SmemLayout smem_layout(int n_ckpt, int d_res, int n_b
     size_t off = 0;
     L.slots = off; off = align16(off + slot_bytes(d_res) * n_buf);
     off = (off + 1023) & ~size_t(1023);
-    L.norms = off; off = align16(off + sizeof(float) * kRT * n_buf);
+    L.norms = off; off = align16(off + sizeof(float) * kNormWin * n_buf);
     L.q_res = off; off = align16(off + sizeof(float) * (size_t)d_res * kQS);
     L.n_q = off; off = align16(off + sizeof(float) * kQC);
     L.r_s = off; off = align16(off + sizeof(float) * kQC);
@@ -111,12 +113,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity), "r"(0x10000)  // suspend-time hint (ns): sleep instead of spinning
         : "memory");
 }
-__device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, int x, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];\n" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(smem_u32(bar))
-        : "memory");
+// Plain (non-tensor) bulk copy global -> shared, completing on an mbarrier.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
     asm volatile(
@@ -215,6 +217,10 @@ __device__ __forceinline__ void merge_list_candidates(const ScanArgs& a, const u
         __syncwarp();
         if (m) {
             if (a.row_ids && lane == 0) st_bytes += 4ull * m;
+            if (a.census && lane == 0) {
+                atomicAdd(a.census + 0, 1ull);
+                atomicAdd(a.census + 1, (unsigned long long)m);
+            }
             merge_query(a, kb, m, warp * 8 + jj, qidx_s, slot_s, r_s, thr_s, n_ckpt, lane, scratch, false);
         }
     }
@@ -385,14 +391,18 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
             if (ct.use_tma) {
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(full_bar + sl, kRT * kBox * 4 + (want_norms ? kRT * 4 : 0));
+                    mbar_arrive_expect_tx(full_bar + sl, kRT * kBox * 4 + (want_norms ? kNormWin * 4 : 0));
                     tma_load_2d(ob, &tmap, (int)k0, (int)(row_start + tb), full_bar + sl);
-                    if (want_norms) tma_load_1d(norms_s + sl * kRT, &tmap_n, (int)(row_start + tb), full_bar + sl);
+                    if (want_norms)  // 16B-aligned window [start & ~3, +kNormWin) of the padded norms array
+                        bulk_load(norms_s + sl * kNormWin, a.row_norms + ((row_start + tb) & ~3u), kNormWin * 4,
+                                  full_bar + sl);
                 }
             } else {
-                if (want_norms)
-                    for (uint32_t r = lane; r < (uint32_t)kRT; r += 32)
-                        norms_s[sl * kRT + r] = r < nrows ? __ldg(a.row_norms + row_start + tb + r) : 0.f;
+                if (want_norms) {
+                    const uint32_t al = (row_start + tb) & ~3u;
+                    for (uint32_t r = lane; r < (uint32_t)kNormWin; r += 32)
+                        norms_s[sl * kNormWin + r] = __ldg(a.row_norms + al + r);
+                }
                 for (uint32_t idx = lane; idx < (uint32_t)kRT * kBox; idx += 32) {
                     const uint32_t r = idx / kBox, cc = idx - r * kBox;
                     ob[swz(r, cc)] = (r < nrows && cc < w) ? __ldg(a.storage + (size_t)(row_start + tb + r) * dim + k0 + cc) : 0.f;
@@ -516,7 +526,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
             // (|o|^2 precomputed per row, |q|^2 per query); everything else is
             // decided exactly below. Operands are fed as raw fp32 bits: the
             // tensor core reads them as TF32, which kTcDelta accounts for.
-            const float* nrm = norms_s + ((s - (c_dense - 1)) % n_buf) * kRT;
+            const float* nrm = norms_s + ((s - (c_dense - 1)) % n_buf) * kNormWin + ((row_start + tb) & 3u);
             float nqp[2], thq[2];
             uint32_t qmask = 0;
 #pragma unroll
@@ -526,7 +536,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                 const bool ok = jj < my_q;
                 nqp[cq] = ok ? (1.f - kTcDelta) * n_q[j] : 0.f;
                 thq[cq] = ok ? thr_s[j * n_ckpt + ck] : -__int_as_float(0x7f800000);
-                if (ok) qmask |= 0x33333333u & (0x11111111u << cq);
+                if (ok) qmask |= cq == 0 ? 0x55555555u : 0xAAAAAAAAu;  // bit = mt*4 + h*2 + cq
             }
             uint32_t valid = qmask;
             if (nrows < (uint32_t)kRT) {
@@ -594,6 +604,10 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                 }
             }
             if (ct.debug == 2) pending = 0;  // experiment: filter only
+            if (ct.debug == 3) {             // census: pairs kept by the filter
+                const uint32_t v = __reduce_add_sync(0xffffffffu, __popc(pending));
+                if (lane == 0) atomicAdd(a.counters + 5, (unsigned long long)v);
+            }
             st_dims += (unsigned long long)__popc(valid & ~pending) * d0;
         } else if (has_sparse) {
             uint32_t dead = 0;
@@ -658,7 +672,9 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
         // ---- survivors of the first checkpoint -----------------------------------
         // advance(list, n): one pair per lane from chunk c_dense on, straight
         // from L2 (each chunk one round trip), marking final candidates.
+        bool merged = false;  // did this warp merge candidates in this tile?
         auto advance = [&](uint32_t* lm, float* la, uint32_t n) {
+            merged = true;
             for (uint32_t e = lane; e < n; e += 32) {
                 const uint32_t meta = lm[e];
                 float x = la[e];
@@ -717,6 +733,32 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                                   st_bytes, ms);
         };
 
+        // Streaming mode: append the s2 list to the global survivor worklist for
+        // advance_survivors_kernel (no L2 chains or merges inside this kernel);
+        // when the worklist is full, advance the pairs here instead.
+        auto emit_or_advance = [&](uint32_t n2) {
+            bool ok = false;
+            if (a.surv) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(a.surv_count, n2);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                ok = base + n2 <= a.surv_cap;
+                for (uint32_t e = lane; e < n2; e += 32) {
+                    if (base + e >= a.surv_cap) continue;
+                    Survivor v;
+                    const uint32_t meta = s2_meta[e];
+                    const uint32_t j = warp * 8 + ((meta >> 8) & 0xffu);
+                    v.q = ok ? qidx_s[j] : 0xffffffffu;  // a partial append is voided
+                    v.row = row_base + (meta & 0xffu);
+                    v.acc = s2_acc[e];
+                    v.slot = slot_s[j];
+                    a.surv[base + e] = v;
+                }
+                if (ok) st_bytes += 16ull * n2;
+            }
+            if (!ok) advance(s2_meta, s2_acc, n2);
+        };
+
         if constexpr (kTC) {
             // stage 1: exact dense prefix of every pair the filter kept (from the
             // resident boxes), survivors of the checkpoint into the s2 list ...
@@ -754,7 +796,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                     }
                     const uint32_t bal = __ballot_sync(0xffffffffu, keep);
                     if (n2 + __popc(bal) > (uint32_t)kWarpList) {  // s2 full: drain it now
-                        advance(s2_meta, s2_acc, n2);
+                        emit_or_advance(n2);
                         n2 = 0;
                     }
                     if (keep) {
@@ -774,7 +816,8 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
             if (lane == 0)
                 for (int cc = 0; cc < c_dense; ++cc) mbar_arrive(empty_bar + (s - (c_dense - 1) + cc) % n_buf);
             PH_MARK(t_r2);
-            if (n2) advance(s2_meta, s2_acc, n2);
+            if (ct.debug == 3 && lane == 0) atomicAdd(a.counters + 6, (unsigned long long)n2);
+            if (n2) emit_or_advance(n2);
             PH_MARK(t_r3);
             PH_ADD(4, t_r2, t_r3);
         } else {
@@ -792,7 +835,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                 advance(wl_meta, wl_acc, n);
             }
         }
-        tighten_warp_radii(a, warp, lane, my_q, qidx_s, slot_s, r_s, thr_s, n_ckpt);
+        if (merged) tighten_warp_radii(a, warp, lane, my_q, qidx_s, slot_s, r_s, thr_s, n_ckpt);
     }  // steps
 
     // ---- counters -------------------------------------------------------------
@@ -808,6 +851,157 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
         atomicAdd(a.counters + 1, v1);
         atomicAdd(a.counters + 2, v2);
     }
+}
+
+// ---- stage 2 of the streaming scan: first-checkpoint survivors ------------------
+// One thread per survivor: continue the exact accumulation from d0 through the
+// remaining checkpoints straight from L2/HBM (checkpointed_scan,
+// proj/src/estimator.cpp:39-70) against the query's radius; exact full-D
+// distances <= r become (query, key) candidates.
+__global__ void __launch_bounds__(256) advance_survivors_kernel(const SurvArgs a) {
+    const uint32_t n = min(*a.surv_count, a.surv_cap);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += stride) {  // warp-uniform grid-stride loop
+    const uint32_t i = i0 + threadIdx.x;
+    bool is_cand = false;
+    uint32_t q = 0;
+    uint64_t key = 0;
+    unsigned long long dims = 0;
+    if (i < n) {
+        const Survivor v = a.surv[i];
+        if (v.q != 0xffffffffu) {
+            q = v.q;
+            const float r = __uint_as_float(a.r_global[q]);
+            const float* orow = a.storage + (size_t)v.row * a.dim;
+            const float* qrow = a.queries + (size_t)q * a.dim;
+            float x = v.acc;
+            uint32_t lo = a.n_dense_dims;
+            bool live = true;
+            const bool vec = ((a.dim | lo) & 3u) == 0;
+            for (uint32_t ci = a.first_ckpt; ci <= a.n_ckpt; ++ci) {
+                const uint32_t hi = ci < a.n_ckpt ? a.cps[ci] : a.dim;
+                if (vec && ((hi - lo) & 3u) == 0) {
+                    uint32_t k = lo;
+                    for (; k + 32 <= hi; k += 32) {  // 8 float4 pairs in flight per round trip
+                        float4 o8[8], q8[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            o8[u] = __ldg(reinterpret_cast<const float4*>(orow + k) + u);
+                            q8[u] = __ldg(reinterpret_cast<const float4*>(qrow + k) + u);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            x = sq_step(x, o8[u].x, q8[u].x);
+                            x = sq_step(x, o8[u].y, q8[u].y);
+                            x = sq_step(x, o8[u].z, q8[u].z);
+                            x = sq_step(x, o8[u].w, q8[u].w);
+                        }
+                    }
+                    for (; k < hi; k += 4) {
+                        const float4 o4 = __ldg(reinterpret_cast<const float4*>(orow + k));
+                        const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + k));
+                        x = sq_step(x, o4.x, q4.x);
+                        x = sq_step(x, o4.y, q4.y);
+                        x = sq_step(x, o4.z, q4.z);
+                        x = sq_step(x, o4.w, q4.w);
+                    }
+                } else {
+                    for (uint32_t k = lo; k < hi; ++k) x = sq_step(x, __ldg(orow + k), __ldg(qrow + k));
+                }
+                lo = hi;
+                if (ci < a.n_ckpt && x > prune_threshold(a.coeff[ci], r)) {
+                    dims += hi;
+                    live = false;
+                    break;
+                }
+            }
+            if (live) {
+                dims += a.dim;
+                const float key_d = __fsqrt_rn(x);
+                if (!(key_d > r)) {
+                    is_cand = true;
+                    const uint32_t id = a.row_ids ? __ldg(a.row_ids + v.row) : a.id_base + v.row;
+                    key = make_key(key_d, id);
+                }
+            }
+        }
+    }
+    // warp-aggregated candidate append
+    const uint32_t bal = __ballot_sync(0xffffffffu, is_cand);
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (bal) {
+        if (lane == 0) base = atomicAdd(a.cand_count, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (is_cand) {
+            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
+            if (pos < a.cand_cap) {
+                a.cand_q[pos] = q;
+                a.cand_key[pos] = key;
+                atomicAdd(a.q_count + q, 1u);
+            }
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) dims += __shfl_xor_sync(0xffffffffu, dims, off);
+    if (lane == 0 && a.counters && dims) atomicAdd(a.counters + 1, dims);
+    }
+}
+
+// Exclusive scan of per-query candidate counts (single CTA).
+__global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* cnt, uint32_t n, uint32_t* off) {
+    __shared__ uint32_t s_v[1024];
+    const uint32_t per = (n + 1023) / 1024;
+    const uint32_t lo = threadIdx.x * per, hi = min(n, lo + per);
+    uint32_t sum = 0;
+    for (uint32_t e = lo; e < hi; ++e) sum += cnt[e];
+    s_v[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const uint32_t v = threadIdx.x >= (unsigned)o ? s_v[threadIdx.x - o] : 0;
+        __syncthreads();
+        s_v[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = s_v[threadIdx.x] - sum;
+    for (uint32_t e = lo; e < hi; ++e) {
+        off[e] = run;
+        run += cnt[e];
+    }
+}
+
+__global__ void scatter_candidates_kernel(const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
+                                          uint32_t cand_cap, const uint32_t* q_off, uint32_t* q_cursor, uint64_t* bucket) {
+    const uint32_t n = min(*cand_count, cand_cap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t q = cand_q[i];
+        bucket[q_off[q] + atomicAdd(q_cursor + q, 1u)] = cand_key[i];
+    }
+}
+
+// Merge each query's candidate bucket into its top-K (out_keys already holds
+// the slot-segment merge); unsorted 256-key batches, warp per query.
+__global__ void __launch_bounds__(128)
+merge_buckets_kernel(const uint64_t* __restrict__ bucket, const uint32_t* __restrict__ q_off,
+                     const uint32_t* __restrict__ q_count, uint32_t nq, uint32_t K, uint64_t* out_keys,
+                     uint32_t* out_count) {
+    __shared__ uint64_t bbuf[4][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t q = blockIdx.x * 4 + warp;
+    if (q >= nq) return;
+    uint64_t* A = out_keys + (size_t)q * K;
+    uint32_t* cA = out_count + q;
+    const uint32_t cnt = q_count[q];
+    const uint64_t* src = bucket + q_off[q];
+    uint64_t* B = bbuf[warp];
+    for (uint32_t b0 = 0; b0 < cnt; b0 += 256) {
+        const uint32_t m = min(256u, cnt - b0);
+        for (uint32_t e = lane; e < m; e += 32) B[e] = src[b0 + e];
+        __syncwarp();
+        warp_merge(A, cA, K, B, m, false);
+        __syncwarp();
+    }
+    const uint32_t c = *reinterpret_cast<volatile uint32_t*>(cA);
+    for (uint32_t i = c + lane; i < K; i += 32) A[i] = kEmptyKey;
 }
 
 // Final per-query merge of n_slots segments into out_keys [nq x K] (K5).
@@ -917,6 +1111,30 @@ cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorM
                                    : launch_scan_t<true, false>(a, ct, tm, tn, grid, smem, s);
     return ct.use_tc ? launch_scan_t<false, true>(a, ct, tm, tn, grid, smem, s)
                      : launch_scan_t<false, false>(a, ct, tm, tn, grid, smem, s);
+}
+
+cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cudaStream_t s) {
+    if (max_entries == 0) return cudaSuccess;
+    advance_survivors_kernel<<<std::min<uint32_t>((max_entries + 255) / 256, 148 * 16), 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
+                                     uint32_t cand_cap, uint32_t* q_count, uint32_t* q_off, uint32_t* q_cursor,
+                                     uint64_t* bucket, uint32_t nq, uint32_t max_cands, cudaStream_t s) {
+    scan_counts_kernel<<<1, 1024, 0, s>>>(q_count, nq, q_off);
+    DADE_CUDA_TRY(cudaMemsetAsync(q_cursor, 0, (size_t)nq * 4, s));
+    if (max_cands)
+        scatter_candidates_kernel<<<std::min<uint32_t>((max_cands + 255) / 256, 148 * 8), 256, 0, s>>>(cand_q, cand_key, cand_count, cand_cap,
+                                                                          q_off, q_cursor, bucket);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_buckets(const uint64_t* bucket, const uint32_t* q_off, const uint32_t* q_count, uint32_t nq,
+                                 uint32_t K, uint64_t* out_keys, uint32_t* out_count, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    merge_buckets_kernel<<<(nq + 3) / 4, 128, 0, s>>>(bucket, q_off, q_count, nq, K, out_keys, out_count);
+    return cudaGetLastError();
 }
 
 // First-slice squared norms |o[0:d0]|^2 of every row (fp32 fma; any rounding
