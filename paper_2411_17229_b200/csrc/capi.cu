@@ -140,7 +140,7 @@ ChunkTable make_chunks(uint32_t dim, const std::vector<uint32_t>& cps) {
 
 // 2D tensor map over row-major fp32 rows [rows][dim]: box [kRT rows][kBox
 // dims], 128-byte swizzle (matches swz() in scan.cu), OOB -> zeros.
-bool make_row_tmap(CUtensorMap* m, const float* base, uint64_t rows, uint32_t dim) {
+bool make_row_tmap(CUtensorMap* m, const float* base, uint64_t rows, uint32_t dim, uint32_t box_rows = kRT) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -153,7 +153,7 @@ bool make_row_tmap(CUtensorMap* m, const float* base, uint64_t rows, uint32_t di
     if (dim % 4 != 0 || dim < (uint32_t)kBox || rows == 0 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
     cuuint64_t gdim[2] = {dim, rows};
     cuuint64_t gstride[1] = {(cuuint64_t)dim * 4};
-    cuuint32_t box[2] = {(cuuint32_t)kBox, (cuuint32_t)kRT};
+    cuuint32_t box[2] = {(cuuint32_t)kBox, (cuuint32_t)box_rows};
     cuuint32_t estride[2] = {1, 1};
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box, estride,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -211,14 +211,16 @@ struct TmapCache {
     const float* base = nullptr;
     uint64_t rows = 0;
     uint32_t dim = 0;
+    uint32_t box_rows = kRT;
     bool ok = false;
     CUtensorMap map{};
+    explicit TmapCache(uint32_t br = kRT) : box_rows(br) {}
     const CUtensorMap& get(const float* b, uint64_t r, uint32_t d, bool& usable) {
         if (b != base || r != rows || d != dim) {
             base = b;
             rows = r;
             dim = d;
-            ok = make_row_tmap(&map, b, r, d);
+            ok = make_row_tmap(&map, b, r, d, box_rows);
             if (std::getenv("DADE_GPU_VERBOSE")) std::fprintf(stderr, "[dade_gpu] row tmap rows=%llu dim=%u ok=%d\n", (unsigned long long)r, d, (int)ok);
         }
         const char* env = std::getenv("DADE_GPU_NO_TMA");
@@ -263,9 +265,11 @@ struct dade_gpu_ctx {
     DevBuf q_in, q_rot, probes, probe_count, c_seg_keys, c_seg_count, c_r;
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
-    DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket;
+    DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max;
+    uint32_t surv_cap_hint = 0;
     DevBuf counters, phase;
     TmapCache tm_centroids, tm_storage, tm_base;
+    TmapCache tm32_storage{32}, tm32_base{32};
     RowNorms norms_storage, norms_base;
     CUtensorMap tm_none{};
 
@@ -393,6 +397,133 @@ void finish_profile(dade_gpu_ctx* c) {
     c->last_bytes = (double)h[2];
 }
 
+__global__ void tighten_from_topk_kernel(const uint64_t* keys, const uint32_t* count, uint32_t nq, uint32_t K,
+                                         uint32_t* r_global) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq || count[q] < K) return;
+    atomicMin(r_global + q, (uint32_t)(keys[(size_t)q * K + K - 1] >> 32));
+}
+
+// The streaming tensor-core path applies when the first checkpoint is a
+// multiple of 8 dims (MMA k) within two 32-dim TMA boxes.
+bool filter_ok(dade_gpu_ctx* c, const ChunkTable& ct, uint32_t dim) {
+    if (!ct.use_tc || !ct.use_tma || ct.n_ckpt > 63 || env_flag("DADE_GPU_NO_STREAM")) return false;
+    const uint32_t d0 = ct.end[ct.n_dense - 1];
+    return d0 % 8 == 0 && d0 <= 2 * kBox && dim % 4 == 0 && dim >= (uint32_t)kBox;
+}
+
+// Streaming passes: [nearest lists], [the rest] (or one flat pass). Each pass =
+// tensor-core filter -> survivor kernel -> candidate buckets -> merge into the
+// running top-K; between passes every query's radius is tightened from it.
+void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, const float* d_q, uint32_t nq,
+                   uint32_t k, bool two_pass, uint32_t max_items, const GroupArgs* g, const float* rows,
+                   uint32_t n_rows, TmapCache& tm32, uint64_t* out_keys, uint32_t* out_count) {
+    cudaStream_t s = c->stream;
+    bool tma = false;
+    const CUtensorMap& tm = tm32.get(rows, std::max<uint32_t>(n_rows, 1), a.dim, tma);
+    if (!tma) fail(DADE_GPU_CUDA_ERROR, "tensor map for the streaming filter failed");
+    const uint32_t d0 = ct.end[ct.n_dense - 1];
+    uint32_t cap = std::max<uint32_t>(c->surv_cap_hint, (uint32_t)std::min<uint64_t>(64ull << 20, std::max<uint64_t>(1u << 20, (uint64_t)nq * 1024)));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        c->surv.ensure((size_t)cap * sizeof(Survivor));
+        c->surv_count.ensure(8);
+        c->cand_q.ensure((size_t)cap * 4);
+        c->cand_key.ensure((size_t)cap * 8);
+        c->cand_count.ensure(4);
+        c->q_count.ensure((size_t)nq * 4);
+        c->q_off.ensure((size_t)nq * 4);
+        c->q_cursor.ensure((size_t)nq * 4);
+        c->bucket.ensure((size_t)cap * 8);
+        c->surv_max.ensure(4);
+        cuda_check(cudaMemsetAsync(c->surv_max.p, 0, 4, s), "memset");
+        cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
+        const int n_pass = two_pass ? 2 : 1;
+        for (int pass = 0; pass < n_pass; ++pass) {
+            cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
+            FilterArgs f{};
+            f.queries = d_q;
+            f.dim = a.dim;
+            f.d0 = d0;
+            f.c_dense = (int)((d0 + kBox - 1) / kBox);
+            f.coeff0 = c->coeff[0];
+            f.r_global = a.r_global;
+            f.items = a.items;
+            f.n_items = a.n_items;
+            f.bucket_q = a.bucket_q;
+            f.bucket_slot = a.bucket_slot;
+            f.flat_rows = a.flat_rows;
+            f.flat_block = a.flat_block;
+            f.flat_nq = a.flat_nq;
+            f.flat_qchunks = a.flat_qchunks;
+            f.surv = c->surv.as<Survivor>();
+            f.surv_count = c->surv_count.as<uint32_t>();
+            f.surv_cap = cap;
+            f.counters = a.counters;
+            uint32_t grid = a.items ? max_items : a.flat_qchunks * ((a.flat_rows + a.flat_block - 1) / a.flat_block);
+            if (two_pass) {
+                if (pass == 0) {
+                    f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
+                    grid = (uint32_t)((nq + kQC - 1) / kQC + c->n_clusters);
+                } else {
+                    f.item_base = g->n_items + 1;  // the rest
+                }
+            }
+            cuda_check(launch_filter(f, tm, grid, s), "filter");
+            cuda_check(cudaMemsetAsync(c->cand_count.p, 0, 4, s), "memset");
+            cuda_check(cudaMemsetAsync(c->q_count.p, 0, (size_t)nq * 4, s), "memset");
+            SurvArgs sv{};
+            sv.surv = f.surv;
+            sv.surv_count = f.surv_count;
+            sv.surv_cap = cap;
+            sv.storage = rows;
+            sv.row_ids = a.row_ids;
+            sv.id_base = a.id_base;
+            sv.dim = a.dim;
+            sv.queries = d_q;
+            sv.r_global = a.r_global;
+            sv.coeff = a.coeff;
+            sv.n_dense_dims = d0;
+            sv.n_ckpt = ct.n_ckpt;
+            for (int i = 0; i < ct.n_ckpt; ++i) sv.cps[i] = (uint16_t)c->cps[i];
+            sv.first_ckpt = 1;
+            sv.cand_q = c->cand_q.as<uint32_t>();
+            sv.cand_key = c->cand_key.as<uint64_t>();
+            sv.cand_count = c->cand_count.as<uint32_t>();
+            sv.cand_cap = cap;
+            sv.q_count = c->q_count.as<uint32_t>();
+            sv.counters = a.counters;
+            sv.surv_max = c->surv_max.as<uint32_t>();
+            cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
+            cuda_check(launch_bucket_candidates(c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
+                                                c->cand_count.as<uint32_t>(), cap, c->q_count.as<uint32_t>(),
+                                                c->q_off.as<uint32_t>(), c->q_cursor.as<uint32_t>(),
+                                                c->bucket.as<uint64_t>(), nq, cap, s),
+                       "bucket candidates");
+            cuda_check(launch_merge_buckets(c->bucket.as<uint64_t>(), c->q_off.as<uint32_t>(),
+                                            c->q_count.as<uint32_t>(), nq, k, out_keys, out_count, s),
+                       "merge buckets");
+            c->launches += 5;
+            if (pass + 1 < n_pass) {
+                tighten_from_topk_kernel<<<(nq + 255) / 256, 256, 0, s>>>(out_keys, out_count, nq, k, a.r_global);
+                cuda_check(cudaGetLastError(), "tighten");
+                ++c->launches;
+            }
+        }
+        // the worklists must not have overflowed: otherwise grow them and redo
+        uint32_t mx = 0;
+        cuda_check(cudaMemcpyAsync(&mx, c->surv_max.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        if (mx <= cap) {
+            c->surv_cap_hint = std::max(c->surv_cap_hint, mx);
+            return;
+        }
+        cap = (uint32_t)std::min<uint64_t>(0xffffffffull, (uint64_t)mx * 2);
+        cuda_check(launch_fill_u32(a.r_global, 0x7f800000u, nq, s), "fill");
+        cuda_check(cudaMemsetAsync(a.counters, 0, 64, s), "memset");
+    }
+    fail(DADE_GPU_RUNTIME_ERROR, "survivor worklist overflow");
+}
+
 // Rotated device queries -> packed top-K keys [nq x k] + counts in
 // out_keys/out_count (device). Stats counters left in c->counters.
 void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint32_t n_probe,
@@ -501,69 +632,17 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
         if (c->norms_storage.tm_ok) tn = &c->norms_storage.map;
         else ct.use_tma = 0;
     }
-    // Streaming mode (tensor-core filter): the scan hands first-checkpoint
-    // survivors to advance_survivors_kernel instead of chasing them itself.
-    const bool streaming = ct.use_tc && ct.n_ckpt <= 63 && !env_flag("DADE_GPU_NO_STREAM");
-    uint32_t cap = 0;
-    if (streaming) {
-        cap = (uint32_t)std::min<uint64_t>(64ull << 20, std::max<uint64_t>(1u << 20, (uint64_t)nq * 1024));
-        c->surv.ensure((size_t)cap * sizeof(Survivor));
-        c->surv_count.ensure(4);
-        cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
-        a.surv = c->surv.as<Survivor>();
-        a.surv_count = c->surv_count.as<uint32_t>();
-        a.surv_cap = cap;
+    if (filter_ok(c, ct, c->dim)) {
+        stream_passes(c, a, ct, d_q, nq, k, nrb > 1, (uint32_t)max_items, &g, c->storage.as<float>(), c->count,
+                      c->tm32_storage, out_keys, out_count);
+        record(c, c->e2);
+        return;
     }
     cuda_check(launch_scan(a, ct, tm, *tn, (uint32_t)max_items, true, s), "dco scan");
-    if (streaming) {
-        c->cand_q.ensure((size_t)cap * 4);
-        c->cand_key.ensure((size_t)cap * 8);
-        c->cand_count.ensure(4);
-        c->q_count.ensure((size_t)nq * 4);
-        c->q_off.ensure((size_t)nq * 4);
-        c->q_cursor.ensure((size_t)nq * 4);
-        c->bucket.ensure((size_t)cap * 8);
-        cuda_check(cudaMemsetAsync(c->cand_count.p, 0, 4, s), "memset");
-        cuda_check(cudaMemsetAsync(c->q_count.p, 0, (size_t)nq * 4, s), "memset");
-        SurvArgs sv{};
-        sv.surv = a.surv;
-        sv.surv_count = a.surv_count;
-        sv.surv_cap = cap;
-        sv.storage = a.storage;
-        sv.row_ids = a.row_ids;
-        sv.id_base = a.id_base;
-        sv.dim = c->dim;
-        sv.queries = d_q;
-        sv.r_global = a.r_global;
-        sv.coeff = a.coeff;
-        sv.n_dense_dims = ct.end[ct.n_dense - 1];
-        sv.n_ckpt = ct.n_ckpt;
-        for (int i = 0; i < ct.n_ckpt; ++i) sv.cps[i] = (uint16_t)c->cps[i];
-        sv.first_ckpt = 1;
-        sv.cand_q = c->cand_q.as<uint32_t>();
-        sv.cand_key = c->cand_key.as<uint64_t>();
-        sv.cand_count = c->cand_count.as<uint32_t>();
-        sv.cand_cap = cap;
-        sv.q_count = c->q_count.as<uint32_t>();
-        sv.counters = a.counters;
-        cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
-        c->launches += 1;
-    }
     record(c, c->e2);
     cuda_check(launch_merge_segments(a.seg_keys, a.seg_count, nq, n_probe, k, out_keys, out_count, s),
                "merge");
     c->launches += 3;
-    if (streaming) {
-        cuda_check(launch_bucket_candidates(c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
-                                            c->cand_count.as<uint32_t>(), cap, c->q_count.as<uint32_t>(),
-                                            c->q_off.as<uint32_t>(), c->q_cursor.as<uint32_t>(),
-                                            c->bucket.as<uint64_t>(), nq, cap, s),
-                   "bucket candidates");
-        cuda_check(launch_merge_buckets(c->bucket.as<uint64_t>(), c->q_off.as<uint32_t>(), c->q_count.as<uint32_t>(),
-                                        nq, k, out_keys, out_count, s),
-                   "merge buckets");
-        c->launches += 3;
-    }
 }
 
 void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint64_t* out_keys,

@@ -44,12 +44,36 @@ struct ScanArgs {
     int seed;                      // radius-seeding pass: every query writes slot 0
     const float* row_norms;        // [rows] first-slice |o|^2 (tensor-core filter only)
     unsigned long long* census;    // nullable debug: [0] merges, [1] merged candidates
+    const uint32_t* item_base;     // nullable: work item index = blockIdx.x + *item_base
     Survivor* surv;                // nullable: hand first-checkpoint survivors to advance_survivors
     uint32_t* surv_count;
     uint32_t surv_cap;
 };
 
 size_t scan_smem_bytes(int n_ckpt, int d_res, int n_buf);
+
+// Streaming tensor-core filter (filter.cu): first-slice test for every pair of
+// the work items, first-checkpoint survivors appended to surv.
+struct FilterArgs {
+    const float* queries;         // rotated [nq, dim]
+    uint32_t dim;
+    uint32_t d0;                  // dense dims = first checkpoint (multiple of 8, <= 64)
+    int c_dense;                  // ceil(d0 / 32) boxes per tile
+    double coeff0;                // reject coefficient of the first checkpoint
+    const uint32_t* r_global;     // radius per query (float bits), fixed for the launch
+    const WorkItem* items;        // IVF items (or nullptr: flat grid below)
+    const uint32_t* n_items;
+    const uint32_t* item_base;    // nullable
+    const uint32_t* bucket_q;
+    const uint32_t* bucket_slot;
+    uint32_t flat_rows, flat_block, flat_nq, flat_qchunks;
+    Survivor* surv;
+    uint32_t* surv_count;
+    uint32_t surv_cap;
+    unsigned long long* counters; // [0] dco, [1] dims, [2] bytes
+};
+size_t filter_smem_bytes(int d0, int c_dense);
+cudaError_t launch_filter(const FilterArgs& a, const CUtensorMap& tmap32, uint32_t grid, cudaStream_t s);
 
 // Survivor kernel (stage 2 of the streaming scan) and candidate bucketing.
 struct SurvArgs {
@@ -73,6 +97,7 @@ struct SurvArgs {
     uint32_t cand_cap;
     uint32_t* q_count;            // per-query candidate counts
     unsigned long long* counters; // [1] dims
+    uint32_t* surv_max;           // running max of the survivor count (overflow check)
 };
 cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cudaStream_t s);
 cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,

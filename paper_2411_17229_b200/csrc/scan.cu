@@ -323,8 +323,9 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
     // ---- decode the work item ------------------------------------------------
     uint32_t row_start, row_count, qcount;
     if (a.items != nullptr) {
-        if (blockIdx.x >= *a.n_items) return;
-        const WorkItem wi = a.items[blockIdx.x];
+        const uint32_t item = blockIdx.x + (a.item_base ? *a.item_base : 0u);
+        if (item >= *a.n_items) return;
+        const WorkItem wi = a.items[item];
         row_start = wi.row_start;
         row_count = wi.row_count;
         qcount = wi.bucket_count;
@@ -859,6 +860,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
 // proj/src/estimator.cpp:39-70) against the query's radius; exact full-D
 // distances <= r become (query, key) candidates.
 __global__ void __launch_bounds__(256) advance_survivors_kernel(const SurvArgs a) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.surv_max) atomicMax(a.surv_max, *a.surv_count);
     const uint32_t n = min(*a.surv_count, a.surv_cap);
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += stride) {  // warp-uniform grid-stride loop
