@@ -265,7 +265,8 @@ struct dade_gpu_ctx {
     DevBuf q_in, q_rot, probes, probe_count, c_seg_keys, c_seg_count, c_r;
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
-    DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max;
+    DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter;
+    int n_sms = 148;
     uint32_t surv_cap_hint = 0;
     DevBuf counters, phase;
     TmapCache tm_centroids, tm_storage, tm_base;
@@ -361,6 +362,9 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
                "coarse merge");
     c->launches += 3;
 }
+
+constexpr uint32_t kFilterItemRows = 1024;  // row piece of a streaming work item
+constexpr uint32_t kSeedRows = 512;         // rows of the nearest list used by the radius seed
 
 bool env_flag(const char* name) {
     const char* e = std::getenv(name);
@@ -461,13 +465,14 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             f.counters = a.counters;
             uint32_t grid = a.items ? max_items : a.flat_qchunks * ((a.flat_rows + a.flat_block - 1) / a.flat_block);
             if (two_pass) {
-                if (pass == 0) {
-                    f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
-                    grid = (uint32_t)((nq + kQC - 1) / kQC + c->n_clusters);
-                } else {
-                    f.item_base = g->n_items + 1;  // the rest
-                }
+                if (pass == 0) f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
+                else f.item_base = g->n_items + 1;          // the rest
             }
+            // persistent CTAs pull items from a counter: two per SM
+            c->item_counter.ensure(4);
+            cuda_check(cudaMemsetAsync(c->item_counter.p, 0, 4, s), "memset");
+            f.item_counter = c->item_counter.as<uint32_t>();
+            grid = std::min<uint32_t>(grid, (uint32_t)c->n_sms * 2);
             cuda_check(launch_filter(f, tm, grid, s), "filter");
             cuda_check(cudaMemsetAsync(c->cand_count.p, 0, 4, s), "memset");
             cuda_check(cudaMemsetAsync(c->q_count.p, 0, (size_t)nq * 4, s), "memset");
@@ -546,8 +551,20 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
         if (nrb == 0 || v > g.rb_end[nrb - 1]) g.rb_end[nrb++] = v;
     }
     g.n_rb = nrb;
+    ChunkTable ct = make_chunks(c->dim, c->cps);
+    bool tma = false;
+    const CUtensorMap& tm = c->tm_storage.get(c->storage.as<float>(), std::max<uint32_t>(c->count, 1), c->dim, tma);
+    ct.use_tma = (tma && ct.vec_ok && c->count > 0) ? 1 : 0;
+    const bool use_filter = filter_ok(c, ct, c->dim);
+    // the streaming filter splits long lists into row pieces (more, shorter items)
+    g.max_item_rows = use_filter ? kFilterItemRows : 0;
     const size_t ne = (size_t)nrb * c->n_clusters;
-    const size_t max_items = ((size_t)nq * n_probe + kQC - 1) / kQC + ne;
+    size_t max_items = ((size_t)nq * n_probe + kQC - 1) / kQC + ne;
+    if (use_filter) {
+        uint32_t max_len = 0;
+        for (uint32_t l = 0; l < c->n_clusters; ++l) max_len = std::max(max_len, c->dev_offsets[l + 1] - c->dev_offsets[l]);
+        max_items *= std::max<uint32_t>(1, (max_len + kFilterItemRows - 1) / kFilterItemRows);
+    }
     c->g_counts.ensure(ne * 4);
     c->g_cursor.ensure(ne * 4);
     c->g_boff.ensure(ne * 4);
@@ -594,49 +611,29 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     a.phase = phase_ptr(c);
     if (const char* dbg = std::getenv("DADE_GPU_DEBUG"))
         if (std::atoi(dbg) == 3) a.census = c->counters.as<unsigned long long>() + 3;
-    ChunkTable ct = make_chunks(c->dim, c->cps);
-    bool tma = false;
-    const CUtensorMap& tm = c->tm_storage.get(a.storage, std::max<uint32_t>(c->count, 1), c->dim, tma);
-    ct.use_tma = (tma && ct.vec_ok && c->count > 0) ? 1 : 0;
     // Radius seeding: an exact (FD) pass over the first rows of every query's
     // nearest list gives each query a K-th distance before the main scan, so
     // no tile starts at r = +inf. Its top-K is discarded (the main scan
     // re-reads those rows); only the atomicMin'd radius is kept. Any K-th
     // distance of a subset of the probed candidates bounds the final radius.
+    record(c, c->e1);
     if (n_probe > 1 && !seed_disabled()) {
-        const uint32_t seed_rows = std::max<uint32_t>(kRT, (2 * k + kRT - 1) / kRT * kRT);
-        c->seed_keys.ensure((size_t)nq * k * 8);
-        c->seed_count.ensure((size_t)nq * 4);
-        cuda_check(cudaMemsetAsync(c->seed_count.p, 0, (size_t)nq * 4, s), "memset");
-        ScanArgs sa = a;
-        sa.n_items = g.n_items + 1;
-        sa.seg_keys = c->seed_keys.as<uint64_t>();
-        sa.seg_count = c->seed_count.as<uint32_t>();
-        sa.n_slots = 1;
-        sa.seed = 1;
-        sa.max_rows = seed_rows;
-        sa.counters = nullptr;
-        sa.phase = nullptr;
-        ChunkTable sct = make_chunks(c->dim, {});
-        sct.use_tma = ct.use_tma;
-        const size_t max_rb0 = (nq + kQC - 1) / kQC + c->n_clusters;
-        record(c, c->e1);
-        cuda_check(launch_scan(sa, sct, tm, c->tm_none, (uint32_t)max_rb0, true, s), "seed scan");
+        cuda_check(launch_seed_radius(c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>(), a.storage, c->dim,
+                                      d_q, nq, k, kSeedRows, a.r_global, s),
+                   "seed radius");
         ++c->launches;
-    } else {
-        record(c, c->e1);
+    }
+    if (use_filter) {
+        stream_passes(c, a, ct, d_q, nq, k, nrb > 1, (uint32_t)max_items, &g, c->storage.as<float>(), c->count,
+                      c->tm32_storage, out_keys, out_count);
+        record(c, c->e2);
+        return;
     }
     const CUtensorMap* tn = &c->tm_none;
     if (ct.use_tc) {
         a.row_norms = c->norms_storage.get(a.storage, c->count, c->dim, ct.end[ct.n_dense - 1], s);
         if (c->norms_storage.tm_ok) tn = &c->norms_storage.map;
         else ct.use_tma = 0;
-    }
-    if (filter_ok(c, ct, c->dim)) {
-        stream_passes(c, a, ct, d_q, nq, k, nrb > 1, (uint32_t)max_items, &g, c->storage.as<float>(), c->count,
-                      c->tm32_storage, out_keys, out_count);
-        record(c, c->e2);
-        return;
     }
     cuda_check(launch_scan(a, ct, tm, *tn, (uint32_t)max_items, true, s), "dco scan");
     record(c, c->e2);
@@ -795,6 +792,7 @@ int dade_gpu_create(int device, dade_gpu_ctx** out) {
         cuda_check(cudaEventCreate(&c->e1), "event");
         cuda_check(cudaEventCreate(&c->e2), "event");
         cuda_check(cudaEventCreate(&c->e3), "event");
+        cuda_check(cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, device), "attr");
         *out = c;
     });
 }

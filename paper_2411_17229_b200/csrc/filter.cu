@@ -116,11 +116,28 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t dim = a.dim;
 
+    __shared__ uint32_t s_item;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
+    if (lane == 0)
+        for (int i = 0; i < kFSlots; ++i) mbar_init_f(bars + warp * kFSlots + i, 1);
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    const int g = lane >> 2, tq = lane & 3;
+    const int smi = lane >> 3, rr = lane & 7;  // ldmatrix addressing
+    unsigned long long st_dco = 0, st_dims = 0, st_bytes = 0, st_surv = 0;
+    uint32_t k_base = 0;  // this warp's running ring position (mbarrier phases persist across items)
+    const uint32_t base = a.items ? (a.item_base ? *a.item_base : 0u) : 0u;
+    const uint32_t end = a.items ? *a.n_items : a.flat_qchunks * ((a.flat_rows + a.flat_block - 1) / a.flat_block);
+
+  for (;;) {  // persistent: CTAs pull work items from a global counter
+    __syncthreads();  // previous item fully consumed (q_res, thr reuse)
+    if (tid == 0) s_item = base + atomicAdd(a.item_counter, 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    if (item >= end) break;
+
     // ---- work item -------------------------------------------------------------
     uint32_t row_start, row_count, qcount;
     if (a.items != nullptr) {
-        const uint32_t item = blockIdx.x + (a.item_base ? *a.item_base : 0u);
-        if (item >= *a.n_items) return;
         const WorkItem wi = a.items[item];
         row_start = wi.row_start;
         row_count = wi.row_count;
@@ -130,7 +147,7 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
             slot_s[tid] = a.bucket_slot[wi.bucket_start + tid];
         }
     } else {
-        const uint32_t rb = blockIdx.x / a.flat_qchunks, qc = blockIdx.x % a.flat_qchunks;
+        const uint32_t rb = item / a.flat_qchunks, qc = item % a.flat_qchunks;
         row_start = rb * a.flat_block;
         row_count = min(a.flat_block, a.flat_rows - row_start);
         qcount = min((uint32_t)kQC, a.flat_nq - qc * kQC);
@@ -140,10 +157,6 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
         }
     }
     if (tid < kQC && tid >= (int)qcount) { qidx_s[tid] = 0; slot_s[tid] = 0; }
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
-    if (lane == 0)
-        for (int i = 0; i < kFSlots; ++i) mbar_init_f(bars + warp * kFSlots + i, 1);
-    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
     for (uint32_t idx = tid; idx < d0 * kQC; idx += kFThreads) {
         const uint32_t k = idx / kQC, j = idx - k * kQC;
@@ -177,14 +190,11 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
         for (int c = 0; c < c_dense; ++c)
             tma2d_f(box(slot, c), &tmap, c * kBox, (int)(row_start + t * kFRows), mybar + slot);
     };
-    const int g = lane >> 2, tq = lane & 3;
-    const int smi = lane >> 3, rr = lane & 7;  // ldmatrix addressing
-    unsigned long long st_dco = 0, st_dims = 0, st_bytes = 0, st_surv = 0;
-    uint32_t k_iter = 0;  // tiles processed by this warp (ring position)
     if (lane == 0) {
-        if ((uint32_t)warp < n_tiles) issue(warp, 0);
-        if ((uint32_t)(warp + kFWarps) < n_tiles) issue(warp + kFWarps, 1);
+        if ((uint32_t)warp < n_tiles) issue(warp, k_base % kFSlots);
+        if ((uint32_t)(warp + kFWarps) < n_tiles) issue(warp + kFWarps, (k_base + 1) % kFSlots);
     }
+    uint32_t k_iter = k_base;
     for (uint32_t t = warp; t < n_tiles; t += kFWarps, ++k_iter) {
         const uint32_t slot = k_iter % kFSlots;
         const uint32_t tb = t * kFRows, nrows = min((uint32_t)kFRows, row_count - tb);
@@ -339,6 +349,8 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
         __syncwarp();
         if (lane == 0 && t + 2 * kFWarps < n_tiles) issue(t + 2 * kFWarps, slot);
     }
+    k_base = k_iter;
+  }  // items
 
     // ---- counters ----------------------------------------------------------------
 #pragma unroll

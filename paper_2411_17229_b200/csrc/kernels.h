@@ -71,6 +71,7 @@ struct FilterArgs {
     uint32_t* surv_count;
     uint32_t surv_cap;
     unsigned long long* counters; // [0] dco, [1] dims, [2] bytes
+    uint32_t* item_counter;       // persistent scheduling (zeroed before the launch)
 };
 size_t filter_smem_bytes(int d0, int c_dense);
 cudaError_t launch_filter(const FilterArgs& a, const CUtensorMap& tmap32, uint32_t grid, cudaStream_t s);
@@ -119,6 +120,9 @@ cudaError_t launch_keys_to_results(const uint64_t* keys, const uint32_t* count, 
 
 // prep.cu
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s);
+cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const uint32_t* list_offsets,
+                               const float* storage, uint32_t dim, const float* queries, uint32_t nq, uint32_t K,
+                               uint32_t S, uint32_t* r_global, cudaStream_t s);
 cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
                           cudaStream_t s);
 // Probe grouping (K3): probe keys [nq x nprobe] (low 32 bits = list id) ->
@@ -138,6 +142,7 @@ struct GroupArgs {
     uint32_t* bucket_slot;          // [nq * n_probe]
     WorkItem* items;                // [max_items]
     uint32_t* n_items;              // [2]: all items, rank-bucket-0 items
+    uint32_t max_item_rows;         // 0: one item per (list, query chunk); else split rows
 };
 cudaError_t launch_group(const GroupArgs& g, cudaStream_t s);
 

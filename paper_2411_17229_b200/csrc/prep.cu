@@ -1,5 +1,6 @@
 // Query rotation (K1), probe grouping (K3) and the per-pair DCO kernels that
 // mirror DcoStrategy::evaluate / partial_sqdist / calibration's ratio walk.
+#include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
@@ -70,6 +71,18 @@ __global__ void group_count_kernel(const GroupArgs g) {
 }
 
 // Single-CTA exclusive scans of the bucket sizes and item counts.
+// work items of one (rank bucket, list) entry: query chunks x row pieces
+__device__ __forceinline__ uint32_t entry_items(const GroupArgs& g, uint32_t e, uint32_t c) {
+    if (c == 0) return 0;
+    uint32_t pieces = 1;
+    if (g.max_item_rows) {
+        const uint32_t list = e % g.n_lists;
+        const uint32_t len = g.list_offsets[list + 1] - g.list_offsets[list];
+        pieces = max(1u, (len + g.max_item_rows - 1) / g.max_item_rows);
+    }
+    return (c + kQC - 1) / kQC * pieces;
+}
+
 __global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
     __shared__ uint32_t s_b[1024], s_i[1024];
     const uint32_t n = g.n_rb * g.n_lists;
@@ -79,7 +92,7 @@ __global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
     for (uint32_t e = lo; e < hi; ++e) {
         const uint32_t c = g.counts[e];
         sb += c;
-        si += (c + kQC - 1) / kQC;
+        si += entry_items(g, e, c);
     }
     s_b[threadIdx.x] = sb;
     s_i[threadIdx.x] = si;
@@ -98,7 +111,7 @@ __global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
         g.bucket_off[e] = rb;
         g.item_off[e] = ri;
         rb += c;
-        ri += (c + kQC - 1) / kQC;
+        ri += entry_items(g, e, c);
     }
     if (threadIdx.x == 1023) g.n_items[0] = s_i[1023];
     __syncthreads();
@@ -127,14 +140,18 @@ __global__ void group_items_kernel(const GroupArgs g) {
     const uint32_t list = e % g.n_lists;
     const uint32_t start = g.list_offsets[list], len = g.list_offsets[list + 1] - start;
     const uint32_t ni = (c + kQC - 1) / kQC;
-    for (uint32_t t = 0; t < ni; ++t) {
-        WorkItem w;
-        w.row_start = start;
-        w.row_count = len;
-        w.bucket_start = g.bucket_off[e] + t * kQC;
-        w.bucket_count = min((uint32_t)kQC, c - t * kQC);
-        g.items[g.item_off[e] + t] = w;
-    }
+    const uint32_t piece = g.max_item_rows ? g.max_item_rows : max(len, 1u);
+    const uint32_t np = max(1u, (len + piece - 1) / piece);
+    uint32_t o = g.item_off[e];
+    for (uint32_t t = 0; t < ni; ++t)
+        for (uint32_t p = 0; p < np; ++p) {
+            WorkItem w;
+            w.row_start = start + p * piece;
+            w.row_count = min(piece, len - p * piece);
+            w.bucket_start = g.bucket_off[e] + t * kQC;
+            w.bucket_count = min((uint32_t)kQC, c - t * kQC);
+            g.items[o++] = w;
+        }
 }
 
 // ---- per-pair DCO: checkpointed_scan (proj/src/estimator.cpp:24-70) ------------
@@ -226,12 +243,84 @@ __global__ void pair_partials_kernel(const float* __restrict__ data, uint32_t di
     }
 }
 
+// ---- radius seed: exact distances to the first rows of each query's nearest list
+// One warp per query: S <= kSeedMax rows of its rank-0 list, exact sequential
+// fp32 distances (sqrtf, the search's key space), bitonic sort in shared
+// memory, K-th smallest -> atomicMin(r_global). Any K exact distances to
+// probed candidates bound the final K-th distance, so the seed is safe.
+constexpr int kSeedMax = 512;
+__global__ void __launch_bounds__(128) seed_radius_kernel(const uint64_t* __restrict__ probes, uint32_t n_probe,
+                                                          const uint32_t* __restrict__ list_offsets,
+                                                          const float* __restrict__ storage, uint32_t dim,
+                                                          const float* __restrict__ queries, uint32_t nq, uint32_t K,
+                                                          uint32_t S, uint32_t* r_global) {
+    __shared__ float dist[4][kSeedMax];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t q = blockIdx.x * 4 + warp;
+    if (q >= nq) return;
+    const uint32_t list = (uint32_t)probes[(size_t)q * n_probe];
+    const uint32_t start = list_offsets[list], len = list_offsets[list + 1] - start;
+    const uint32_t n = min(len, S);
+    if (n < K) return;  // too few rows for a K-th distance
+    const float* qr = queries + (size_t)q * dim;
+    float* d = dist[warp];
+    const bool vec = (dim & 3u) == 0;
+    for (uint32_t r = lane; r < (uint32_t)kSeedMax; r += 32) {
+        float acc = __int_as_float(0x7f800000);
+        if (r < n) {
+            const float* o = storage + (size_t)(start + r) * dim;
+            acc = 0.f;
+            if (vec) {
+                for (uint32_t k = 0; k < dim; k += 4) {
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(o + k));
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(qr + k));
+                    acc = sq_step(acc, a.x, b.x);
+                    acc = sq_step(acc, a.y, b.y);
+                    acc = sq_step(acc, a.z, b.z);
+                    acc = sq_step(acc, a.w, b.w);
+                }
+            } else {
+                for (uint32_t k = 0; k < dim; ++k) acc = sq_step(acc, __ldg(o + k), __ldg(qr + k));
+            }
+            acc = __fsqrt_rn(acc);
+        }
+        d[r] = acc;
+    }
+    __syncwarp();
+    // bitonic sort of kSeedMax keys, ascending
+    for (uint32_t size = 2; size <= (uint32_t)kSeedMax; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = lane; i < (uint32_t)kSeedMax / 2; i += 32) {
+                const uint32_t lo = 2 * i - (i & (stride - 1));
+                const uint32_t hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const float x = d[lo], y = d[hi];
+                if ((x > y) == up) {
+                    d[lo] = y;
+                    d[hi] = x;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (lane == 0) atomicMin(r_global + q, __float_as_uint(d[K - 1]));
+}
+
 __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, size_t n) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
 }
 
 }  // namespace
+
+cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const uint32_t* list_offsets,
+                               const float* storage, uint32_t dim, const float* queries, uint32_t nq, uint32_t K,
+                               uint32_t S, uint32_t* r_global, cudaStream_t s) {
+    if (nq == 0 || K > (uint32_t)kSeedMax) return cudaSuccess;
+    seed_radius_kernel<<<(nq + 3) / 4, 128, 0, s>>>(probes, n_probe, list_offsets, storage, dim, queries, nq, K,
+                                                     std::min<uint32_t>(S, kSeedMax), r_global);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s) {
     if (n == 0) return cudaSuccess;

@@ -381,9 +381,24 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
             if (d_res == 0) {
                 // stage this chunk's query slice (zero beyond w) next to the box
                 float* qs = slot_q(sl);
-                for (uint32_t idx = lane; idx < (uint32_t)kQC * kBox; idx += 32) {
-                    const uint32_t j = idx / kBox, cc = idx - j * kBox;
-                    qs[cc * kQS + j] = (j < qcount && cc < w) ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k0 + cc) : 0.f;
+                if (ct.vec_ok) {  // lane owns queries lane, lane + 32: 16-byte loads, transposed stores
+                    for (uint32_t j = lane; j < (uint32_t)kQC; j += 32) {
+                        const float* src = a.queries + (size_t)qidx_s[j] * dim + k0;
+#pragma unroll
+                        for (uint32_t v = 0; v < kBox / 4; ++v) {
+                            float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (j < qcount && 4 * v < w) f = __ldg(reinterpret_cast<const float4*>(src) + v);
+                            qs[(4 * v + 0) * kQS + j] = f.x;
+                            qs[(4 * v + 1) * kQS + j] = f.y;
+                            qs[(4 * v + 2) * kQS + j] = f.z;
+                            qs[(4 * v + 3) * kQS + j] = f.w;
+                        }
+                    }
+                } else {
+                    for (uint32_t idx = lane; idx < (uint32_t)kQC * kBox; idx += 32) {
+                        const uint32_t j = idx / kBox, cc = idx - j * kBox;
+                        qs[cc * kQS + j] = (j < qcount && cc < w) ? __ldg(a.queries + (size_t)qidx_s[j] * dim + k0 + cc) : 0.f;
+                    }
                 }
                 st_bytes += 4ull * w * qcount;
             }
