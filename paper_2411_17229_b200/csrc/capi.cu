@@ -499,6 +499,12 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             sv.counters = a.counters;
             sv.surv_max = c->surv_max.as<uint32_t>();
             cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
+            if (a.counters && pass < 2)  // survivors / candidates per pass (low words of counters[4 + 2 pass ..])
+                for (int w = 0; w < 2; ++w)
+                    cuda_check(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(a.counters + 4 + 2 * pass + w),
+                                               w == 0 ? c->surv_count.p : c->cand_count.p, 4,
+                                               cudaMemcpyDeviceToDevice, s),
+                               "census");
             cuda_check(launch_bucket_candidates(c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
                                                 c->cand_count.as<uint32_t>(), cap, c->q_count.as<uint32_t>(),
                                                 c->q_off.as<uint32_t>(), c->q_cursor.as<uint32_t>(),

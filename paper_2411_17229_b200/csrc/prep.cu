@@ -244,66 +244,82 @@ __global__ void pair_partials_kernel(const float* __restrict__ data, uint32_t di
 }
 
 // ---- radius seed: exact distances to the first rows of each query's nearest list
-// One warp per query: S <= kSeedMax rows of its rank-0 list, exact sequential
-// fp32 distances (sqrtf, the search's key space), bitonic sort in shared
-// memory, K-th smallest -> atomicMin(r_global). Any K exact distances to
-// probed candidates bound the final K-th distance, so the seed is safe.
+// One CTA (256 threads) per query: S <= kSeedMax rows of its rank-0 list, two
+// rows per thread with interleaved exact sequential fp32 accumulations
+// (sqrtf: the search's key space), bitonic sort in shared memory, K-th
+// smallest -> atomicMin(r_global). Any K exact distances to probed candidates
+// bound the final K-th distance, so the seed is safe.
 constexpr int kSeedMax = 512;
-__global__ void __launch_bounds__(128) seed_radius_kernel(const uint64_t* __restrict__ probes, uint32_t n_probe,
-                                                          const uint32_t* __restrict__ list_offsets,
-                                                          const float* __restrict__ storage, uint32_t dim,
-                                                          const float* __restrict__ queries, uint32_t nq, uint32_t K,
-                                                          uint32_t S, uint32_t* r_global) {
-    __shared__ float dist[4][kSeedMax];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t q = blockIdx.x * 4 + warp;
-    if (q >= nq) return;
+constexpr int kSeedThreads = 256;
+__global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
+    const uint64_t* __restrict__ probes, uint32_t n_probe, const uint32_t* __restrict__ list_offsets,
+    const float* __restrict__ storage, uint32_t dim, const float* __restrict__ queries, uint32_t nq, uint32_t K,
+    uint32_t S, uint32_t* r_global) {
+    __shared__ float d[kSeedMax];
+    const uint32_t q = blockIdx.x;
     const uint32_t list = (uint32_t)probes[(size_t)q * n_probe];
     const uint32_t start = list_offsets[list], len = list_offsets[list + 1] - start;
     const uint32_t n = min(len, S);
-    if (n < K) return;  // too few rows for a K-th distance
+    if (n < K) return;  // too few rows for a K-th distance (uniform per CTA)
     const float* qr = queries + (size_t)q * dim;
-    float* d = dist[warp];
-    const bool vec = (dim & 3u) == 0;
-    for (uint32_t r = lane; r < (uint32_t)kSeedMax; r += 32) {
-        float acc = __int_as_float(0x7f800000);
-        if (r < n) {
-            const float* o = storage + (size_t)(start + r) * dim;
-            acc = 0.f;
-            if (vec) {
-                for (uint32_t k = 0; k < dim; k += 4) {
-                    const float4 a = __ldg(reinterpret_cast<const float4*>(o + k));
-                    const float4 b = __ldg(reinterpret_cast<const float4*>(qr + k));
-                    acc = sq_step(acc, a.x, b.x);
-                    acc = sq_step(acc, a.y, b.y);
-                    acc = sq_step(acc, a.z, b.z);
-                    acc = sq_step(acc, a.w, b.w);
-                }
-            } else {
-                for (uint32_t k = 0; k < dim; ++k) acc = sq_step(acc, __ldg(o + k), __ldg(qr + k));
+    const uint32_t r0 = threadIdx.x, r1 = threadIdx.x + kSeedThreads;
+    const float* o0 = storage + (size_t)(start + min(r0, n - 1)) * dim;
+    const float* o1 = storage + (size_t)(start + min(r1, n - 1)) * dim;
+    float a0 = 0.f, a1 = 0.f;
+    if ((dim & 3u) == 0) {
+        uint32_t k = 0;
+        for (; k + 16 <= dim; k += 16) {
+            float4 x0[4], x1[4], y[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                x0[u] = __ldg(reinterpret_cast<const float4*>(o0 + k) + u);
+                x1[u] = __ldg(reinterpret_cast<const float4*>(o1 + k) + u);
+                y[u] = __ldg(reinterpret_cast<const float4*>(qr + k) + u);
             }
-            acc = __fsqrt_rn(acc);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a0 = sq_step(a0, x0[u].x, y[u].x); a1 = sq_step(a1, x1[u].x, y[u].x);
+                a0 = sq_step(a0, x0[u].y, y[u].y); a1 = sq_step(a1, x1[u].y, y[u].y);
+                a0 = sq_step(a0, x0[u].z, y[u].z); a1 = sq_step(a1, x1[u].z, y[u].z);
+                a0 = sq_step(a0, x0[u].w, y[u].w); a1 = sq_step(a1, x1[u].w, y[u].w);
+            }
         }
-        d[r] = acc;
+        for (; k < dim; k += 4) {
+            const float4 x0 = __ldg(reinterpret_cast<const float4*>(o0 + k));
+            const float4 x1 = __ldg(reinterpret_cast<const float4*>(o1 + k));
+            const float4 y = __ldg(reinterpret_cast<const float4*>(qr + k));
+            a0 = sq_step(a0, x0.x, y.x); a1 = sq_step(a1, x1.x, y.x);
+            a0 = sq_step(a0, x0.y, y.y); a1 = sq_step(a1, x1.y, y.y);
+            a0 = sq_step(a0, x0.z, y.z); a1 = sq_step(a1, x1.z, y.z);
+            a0 = sq_step(a0, x0.w, y.w); a1 = sq_step(a1, x1.w, y.w);
+        }
+    } else {
+        for (uint32_t k = 0; k < dim; ++k) {
+            const float y = __ldg(qr + k);
+            a0 = sq_step(a0, __ldg(o0 + k), y);
+            a1 = sq_step(a1, __ldg(o1 + k), y);
+        }
     }
-    __syncwarp();
-    // bitonic sort of kSeedMax keys, ascending
+    const float inf = __int_as_float(0x7f800000);
+    d[r0] = r0 < n ? __fsqrt_rn(a0) : inf;
+    d[r1] = r1 < n ? __fsqrt_rn(a1) : inf;
+    __syncthreads();
+    // bitonic sort of kSeedMax keys, ascending: one compare-exchange per thread per stage
     for (uint32_t size = 2; size <= (uint32_t)kSeedMax; size <<= 1) {
         for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (uint32_t i = lane; i < (uint32_t)kSeedMax / 2; i += 32) {
-                const uint32_t lo = 2 * i - (i & (stride - 1));
-                const uint32_t hi = lo + stride;
-                const bool up = (lo & size) == 0;
-                const float x = d[lo], y = d[hi];
-                if ((x > y) == up) {
-                    d[lo] = y;
-                    d[hi] = x;
-                }
+            const uint32_t i = threadIdx.x;
+            const uint32_t lo = 2 * i - (i & (stride - 1));
+            const uint32_t hi = lo + stride;
+            const bool up = (lo & size) == 0;
+            const float x = d[lo], y = d[hi];
+            if ((x > y) == up) {
+                d[lo] = y;
+                d[hi] = x;
             }
-            __syncwarp();
+            __syncthreads();
         }
     }
-    if (lane == 0) atomicMin(r_global + q, __float_as_uint(d[K - 1]));
+    if (threadIdx.x == 0) atomicMin(r_global + q, __float_as_uint(d[K - 1]));
 }
 
 __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, size_t n) {
@@ -317,8 +333,8 @@ cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const u
                                const float* storage, uint32_t dim, const float* queries, uint32_t nq, uint32_t K,
                                uint32_t S, uint32_t* r_global, cudaStream_t s) {
     if (nq == 0 || K > (uint32_t)kSeedMax) return cudaSuccess;
-    seed_radius_kernel<<<(nq + 3) / 4, 128, 0, s>>>(probes, n_probe, list_offsets, storage, dim, queries, nq, K,
-                                                     std::min<uint32_t>(S, kSeedMax), r_global);
+    seed_radius_kernel<<<nq, kSeedThreads, 0, s>>>(probes, n_probe, list_offsets, storage, dim, queries, nq, K,
+                                                    std::min<uint32_t>(S, kSeedMax), r_global);
     return cudaGetLastError();
 }
 

@@ -31,6 +31,8 @@ for it in range(3):
     ph = buf[8:13].astype(np.float64)
     if os.environ.get("DADE_GPU_DEBUG") == "1":
         print("  filter violations:", int(buf[3]))
+    print(f"  pass1 survivors {int(buf[4]) & 0xffffffff} cands {int(buf[5]) & 0xffffffff}  "
+          f"pass2 survivors {int(buf[6]) & 0xffffffff} cands {int(buf[7]) & 0xffffffff}")
     if os.environ.get("DADE_GPU_DEBUG") == "3":
         print(f"  merges {int(buf[3])} merged-cands {int(buf[4])} filter-kept {int(buf[5])} ckpt0-survivors {int(buf[6])}")
     names = ["wait+barrier", "dense", "epilogue", "survivors", "merges"]
