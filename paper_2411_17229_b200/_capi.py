@@ -75,6 +75,7 @@ def _load():
         "dade_gpu_calibrate": ([P, P, U32, D, U32, U64, U64, U32, P, P, P], I),
         "dade_gpu_launch_count": ([P], U64),
         "dade_gpu_debug_counters": ([P, P], I),
+        "dade_gpu_debug_radius": ([P, P, U32], I),
         "dade_gpu_set_profiling": ([P, I], I),
         "dade_gpu_last_scan_profile": ([P, P, P, P], I),
     }

@@ -419,9 +419,16 @@ bool filter_ok(dade_gpu_ctx* c, const ChunkTable& ct, uint32_t dim) {
 // Streaming passes: [nearest lists], [the rest] (or one flat pass). Each pass =
 // tensor-core filter -> survivor kernel -> candidate buckets -> merge into the
 // running top-K; between passes every query's radius is tightened from it.
+struct SeedArgs {
+    bool on;
+    const uint64_t* probes;
+    uint32_t n_probe;
+    const uint32_t* offsets;
+};
+
 void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, const float* d_q, uint32_t nq,
                    uint32_t k, bool two_pass, uint32_t max_items, const GroupArgs* g, const float* rows,
-                   uint32_t n_rows, TmapCache& tm32, uint64_t* out_keys, uint32_t* out_count) {
+                   uint32_t n_rows, TmapCache& tm32, uint64_t* out_keys, uint32_t* out_count, const SeedArgs& seed) {
     cudaStream_t s = c->stream;
     bool tma = false;
     const CUtensorMap& tm = tm32.get(rows, std::max<uint32_t>(n_rows, 1), a.dim, tma);
@@ -441,6 +448,12 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         c->surv_max.ensure(4);
         cuda_check(cudaMemsetAsync(c->surv_max.p, 0, 4, s), "memset");
         cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
+        if (seed.on) {
+            cuda_check(launch_seed_radius(seed.probes, seed.n_probe, seed.offsets, rows, a.row_ids, a.dim, d_q, nq, k,
+                                          kSeedRows, a.r_global, out_keys, out_count, s),
+                       "seed radius");
+            ++c->launches;
+        }
         const int n_pass = two_pass ? 2 : 1;
         for (int pass = 0; pass < n_pass; ++pass) {
             cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
@@ -564,6 +577,11 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     const bool use_filter = filter_ok(c, ct, c->dim);
     // the streaming filter splits long lists into row pieces (more, shorter items)
     g.max_item_rows = use_filter ? kFilterItemRows : 0;
+    const bool seeded = n_probe > 1 && !seed_disabled() && k <= 512;
+    if (use_filter && seeded) {  // the seed's rows of every nearest list are final results already
+        g.seed_skip = kSeedRows;
+        g.seed_min = k;
+    }
     const size_t ne = (size_t)nrb * c->n_clusters;
     size_t max_items = ((size_t)nq * n_probe + kQC - 1) / kQC + ne;
     if (use_filter) {
@@ -623,17 +641,18 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     // re-reads those rows); only the atomicMin'd radius is kept. Any K-th
     // distance of a subset of the probed candidates bounds the final radius.
     record(c, c->e1);
-    if (n_probe > 1 && !seed_disabled()) {
-        cuda_check(launch_seed_radius(c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>(), a.storage, c->dim,
-                                      d_q, nq, k, kSeedRows, a.r_global, s),
-                   "seed radius");
-        ++c->launches;
-    }
     if (use_filter) {
+        SeedArgs sd{seeded, c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>()};
         stream_passes(c, a, ct, d_q, nq, k, nrb > 1, (uint32_t)max_items, &g, c->storage.as<float>(), c->count,
-                      c->tm32_storage, out_keys, out_count);
+                      c->tm32_storage, out_keys, out_count, sd);
         record(c, c->e2);
         return;
+    }
+    if (seeded) {
+        cuda_check(launch_seed_radius(c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>(), a.storage,
+                                      a.row_ids, c->dim, d_q, nq, k, kSeedRows, a.r_global, nullptr, nullptr, s),
+                   "seed radius");
+        ++c->launches;
     }
     const CUtensorMap* tn = &c->tm_none;
     if (ct.use_tc) {
@@ -1327,6 +1346,15 @@ int dade_gpu_calibrate(dade_gpu_ctx* c, const float* data, uint32_t n, double p_
 }
 
 uint64_t dade_gpu_launch_count(dade_gpu_ctx* c) { return c ? c->launches : 0; }
+
+// Debug: copy the per-query radius (float bits) left by the last IVF search.
+int dade_gpu_debug_radius(dade_gpu_ctx* c, uint32_t* out, uint32_t nq) {
+    return guarded([&] {
+        c->use_device();
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        cuda_check(cudaMemcpy(out, c->r_global.p, (size_t)nq * 4, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
 
 // Debug: the last scan's counters [0..7] and per-phase clocks [8..15].
 int dade_gpu_debug_counters(dade_gpu_ctx* c, uint64_t* out16) {

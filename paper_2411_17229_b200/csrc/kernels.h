@@ -121,8 +121,9 @@ cudaError_t launch_keys_to_results(const uint64_t* keys, const uint32_t* count, 
 // prep.cu
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s);
 cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const uint32_t* list_offsets,
-                               const float* storage, uint32_t dim, const float* queries, uint32_t nq, uint32_t K,
-                               uint32_t S, uint32_t* r_global, cudaStream_t s);
+                               const float* storage, const uint32_t* row_ids, uint32_t dim, const float* queries,
+                               uint32_t nq, uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,
+                               uint32_t* out_count, cudaStream_t s);
 cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
                           cudaStream_t s);
 // Probe grouping (K3): probe keys [nq x nprobe] (low 32 bits = list id) ->
@@ -143,6 +144,7 @@ struct GroupArgs {
     WorkItem* items;                // [max_items]
     uint32_t* n_items;              // [2]: all items, rank-bucket-0 items
     uint32_t max_item_rows;         // 0: one item per (list, query chunk); else split rows
+    uint32_t seed_skip, seed_min;   // rank-0 lists of >= seed_min rows skip their first seed_skip rows
 };
 cudaError_t launch_group(const GroupArgs& g, cudaStream_t s);
 

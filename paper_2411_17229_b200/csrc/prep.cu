@@ -72,14 +72,20 @@ __global__ void group_count_kernel(const GroupArgs g) {
 
 // Single-CTA exclusive scans of the bucket sizes and item counts.
 // work items of one (rank bucket, list) entry: query chunks x row pieces
+// Rows [skip, len) of an entry's list still to scan: rank-bucket-0 entries skip
+// the rows the seed already scored exactly (when the seed ran: len >= seed_min).
+__device__ __forceinline__ uint32_t entry_skip(const GroupArgs& g, uint32_t e, uint32_t len) {
+    return (g.seed_skip && e < g.n_lists && len >= g.seed_min) ? min(len, g.seed_skip) : 0u;
+}
+
 __device__ __forceinline__ uint32_t entry_items(const GroupArgs& g, uint32_t e, uint32_t c) {
     if (c == 0) return 0;
+    const uint32_t list = e % g.n_lists;
+    const uint32_t len = g.list_offsets[list + 1] - g.list_offsets[list];
+    const uint32_t rem = len - entry_skip(g, e, len);
+    if (rem == 0) return 0;
     uint32_t pieces = 1;
-    if (g.max_item_rows) {
-        const uint32_t list = e % g.n_lists;
-        const uint32_t len = g.list_offsets[list + 1] - g.list_offsets[list];
-        pieces = max(1u, (len + g.max_item_rows - 1) / g.max_item_rows);
-    }
+    if (g.max_item_rows) pieces = max(1u, (rem + g.max_item_rows - 1) / g.max_item_rows);
     return (c + kQC - 1) / kQC * pieces;
 }
 
@@ -138,7 +144,10 @@ __global__ void group_items_kernel(const GroupArgs g) {
     const uint32_t c = g.counts[e];
     if (c == 0) return;
     const uint32_t list = e % g.n_lists;
-    const uint32_t start = g.list_offsets[list], len = g.list_offsets[list + 1] - start;
+    const uint32_t len0 = g.list_offsets[list + 1] - g.list_offsets[list];
+    const uint32_t skip = entry_skip(g, e, len0);
+    const uint32_t start = g.list_offsets[list] + skip, len = len0 - skip;
+    if (len == 0) return;
     const uint32_t ni = (c + kQC - 1) / kQC;
     const uint32_t piece = g.max_item_rows ? g.max_item_rows : max(len, 1u);
     const uint32_t np = max(1u, (len + piece - 1) / piece);
@@ -251,11 +260,16 @@ __global__ void pair_partials_kernel(const float* __restrict__ data, uint32_t di
 // bound the final K-th distance, so the seed is safe.
 constexpr int kSeedMax = 512;
 constexpr int kSeedThreads = 256;
+// With out_keys, the seed also becomes the query's first K results: its keys are
+// exact (dist, id) of rows [0, S) of the nearest list, and the streaming scan
+// skips those rows (GroupArgs::seed_skip), so nothing is evaluated twice and
+// every query holds K results before any pruning, like the reference's heap.
 __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
     const uint64_t* __restrict__ probes, uint32_t n_probe, const uint32_t* __restrict__ list_offsets,
-    const float* __restrict__ storage, uint32_t dim, const float* __restrict__ queries, uint32_t nq, uint32_t K,
-    uint32_t S, uint32_t* r_global) {
-    __shared__ float d[kSeedMax];
+    const float* __restrict__ storage, const uint32_t* __restrict__ row_ids, uint32_t dim,
+    const float* __restrict__ queries, uint32_t nq, uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,
+    uint32_t* out_count) {
+    __shared__ uint64_t d[kSeedMax];
     const uint32_t q = blockIdx.x;
     const uint32_t list = (uint32_t)probes[(size_t)q * n_probe];
     const uint32_t start = list_offsets[list], len = list_offsets[list + 1] - start;
@@ -300,18 +314,22 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
             a1 = sq_step(a1, __ldg(o1 + k), y);
         }
     }
-    const float inf = __int_as_float(0x7f800000);
-    d[r0] = r0 < n ? __fsqrt_rn(a0) : inf;
-    d[r1] = r1 < n ? __fsqrt_rn(a1) : inf;
+    auto key_of = [&](uint32_t r, float acc) -> uint64_t {
+        if (r >= n) return ~0ull;
+        const uint32_t id = row_ids ? __ldg(row_ids + start + r) : start + r;
+        return make_key(__fsqrt_rn(acc), id);
+    };
+    d[r0] = key_of(r0, a0);
+    d[r1] = key_of(r1, a1);
     __syncthreads();
-    // bitonic sort of kSeedMax keys, ascending: one compare-exchange per thread per stage
+    // bitonic sort of kSeedMax (dist, id) keys, ascending: one compare-exchange per thread per stage
     for (uint32_t size = 2; size <= (uint32_t)kSeedMax; size <<= 1) {
         for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
             const uint32_t i = threadIdx.x;
             const uint32_t lo = 2 * i - (i & (stride - 1));
             const uint32_t hi = lo + stride;
             const bool up = (lo & size) == 0;
-            const float x = d[lo], y = d[hi];
+            const uint64_t x = d[lo], y = d[hi];
             if ((x > y) == up) {
                 d[lo] = y;
                 d[hi] = x;
@@ -319,7 +337,11 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
             __syncthreads();
         }
     }
-    if (threadIdx.x == 0) atomicMin(r_global + q, __float_as_uint(d[K - 1]));
+    if (threadIdx.x == 0) atomicMin(r_global + q, (uint32_t)(d[K - 1] >> 32));
+    if (out_keys) {
+        for (uint32_t i = threadIdx.x; i < K; i += kSeedThreads) out_keys[(size_t)q * K + i] = d[i];
+        if (threadIdx.x == 0) out_count[q] = K;
+    }
 }
 
 __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, size_t n) {
@@ -330,11 +352,12 @@ __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, size_t n) {
 }  // namespace
 
 cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const uint32_t* list_offsets,
-                               const float* storage, uint32_t dim, const float* queries, uint32_t nq, uint32_t K,
-                               uint32_t S, uint32_t* r_global, cudaStream_t s) {
+                               const float* storage, const uint32_t* row_ids, uint32_t dim, const float* queries,
+                               uint32_t nq, uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,
+                               uint32_t* out_count, cudaStream_t s) {
     if (nq == 0 || K > (uint32_t)kSeedMax) return cudaSuccess;
-    seed_radius_kernel<<<nq, kSeedThreads, 0, s>>>(probes, n_probe, list_offsets, storage, dim, queries, nq, K,
-                                                    std::min<uint32_t>(S, kSeedMax), r_global);
+    seed_radius_kernel<<<nq, kSeedThreads, 0, s>>>(probes, n_probe, list_offsets, storage, row_ids, dim, queries, nq,
+                                                    K, std::min<uint32_t>(S, kSeedMax), r_global, out_keys, out_count);
     return cudaGetLastError();
 }
 
