@@ -364,7 +364,13 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
 }
 
 constexpr uint32_t kFilterItemRows = 1024;  // row piece of a streaming work item
-constexpr uint32_t kSeedRows = 512;         // rows of the nearest list used by the radius seed
+constexpr uint32_t kSeedRowsDefault = 512;  // rows of the nearest list used by the radius seed
+
+uint32_t seed_rows(uint32_t k) {
+    uint32_t s = kSeedRowsDefault;
+    if (const char* e = std::getenv("DADE_GPU_SEED_ROWS")) s = (uint32_t)std::atoi(e);
+    return std::min<uint32_t>(512, std::max<uint32_t>(s, k));
+}
 
 bool env_flag(const char* name) {
     const char* e = std::getenv(name);
@@ -450,7 +456,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
         if (seed.on) {
             cuda_check(launch_seed_radius(seed.probes, seed.n_probe, seed.offsets, rows, a.row_ids, a.dim, d_q, nq, k,
-                                          kSeedRows, a.r_global, out_keys, out_count, s),
+                                          seed_rows(k), a.r_global, out_keys, out_count, s),
                        "seed radius");
             ++c->launches;
         }
@@ -579,7 +585,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     g.max_item_rows = use_filter ? kFilterItemRows : 0;
     const bool seeded = n_probe > 1 && !seed_disabled() && k <= 512;
     if (use_filter && seeded) {  // the seed's rows of every nearest list are final results already
-        g.seed_skip = kSeedRows;
+        g.seed_skip = seed_rows(k);
         g.seed_min = k;
     }
     const size_t ne = (size_t)nrb * c->n_clusters;
@@ -650,7 +656,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     }
     if (seeded) {
         cuda_check(launch_seed_radius(c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>(), a.storage,
-                                      a.row_ids, c->dim, d_q, nq, k, kSeedRows, a.r_global, nullptr, nullptr, s),
+                                      a.row_ids, c->dim, d_q, nq, k, seed_rows(k), a.r_global, nullptr, nullptr, s),
                    "seed radius");
         ++c->launches;
     }
