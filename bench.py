@@ -52,38 +52,48 @@ class ClockSampler:
 
     def __init__(self, gpu: int, path: Path):
         self.path = path
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.f = open(path, "w")
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
-    def stop(self):
+    def stop(self, window=None):
+        """Summarise the samples taken inside `window` = (t0, t1) (host epoch
+        seconds of the timed region); all samples if None or none fall inside."""
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
         self.p.terminate()
         self.p.wait()
         self.f.close()
-        sm, mx, reasons = [], [], set()
+        rows = []
         for line in self.path.read_text().splitlines():
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-            except ValueError:
+                ts = time.mktime(time.strptime(parts[0].split(".")[0], "%Y/%m/%d %H:%M:%S")) + \
+                    float("0." + parts[0].split(".")[1]) if "." in parts[0] else 0.0
+                rows.append((ts, float(parts[1]), float(parts[2]), parts))
+            except (ValueError, IndexError):
                 continue
+        inside = [r for r in rows if window and window[0] <= r[0] <= window[1]]
+        use = inside or rows
+        sm, mx, reasons = [], [], set()
+        for _, a, b, parts in use:
+            sm.append(a)
+            mx.append(b)
             for name, v in zip(self.REASONS, parts[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "samples_in_timed_region": len(inside), "reasons": sorted(reasons)}
 
 
 def measured_peaks():
@@ -250,17 +260,19 @@ def run_ours(args, cfg):
             return out_ids, out_d, out_c
         return gdist.sharded_ivf_search(dev, None, q_dev, nq, k, cfg.nprobe, raw=True)
 
+    clocks = ClockSampler(local, Path(tempfile.gettempdir()) / f"dade_clocks_{local}.csv")
+    time.sleep(0.3)  # let the sampler start emitting before the timed region
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local, Path(tempfile.gettempdir()) / f"dade_clocks_{local}.csv")
     l0 = dev.launches
     evs = []
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    t_region0 = time.time()
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (outside the events)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -269,9 +281,10 @@ def run_ours(args, cfg):
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize()
+    t_region1 = time.time()
     if world > 1:
         dist.barrier()
-    clk = clocks.stop()
+    clk = clocks.stop((t_region0, t_region1))
     launches = (dev.launches - l0) // max(args.steps, 1)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     mean_ms = float(np.mean(step_ms))
@@ -398,7 +411,7 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="config1")
