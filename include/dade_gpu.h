@@ -165,6 +165,9 @@ int dade_gpu_calibrate(dade_gpu_ctx* ctx, const float* data, uint32_t n, double 
  * and, with DADE_GPU_PHASES=1 in the environment, per-phase clock sums [8..15]. */
 int dade_gpu_debug_counters(dade_gpu_ctx* ctx, uint64_t* out16);
 
+/* Debug: per-query radius (float bits) left by the last IVF search. */
+int dade_gpu_debug_radius(dade_gpu_ctx* ctx, uint32_t* out, uint32_t nq);
+
 /* Number of CUDA kernels this handle launched so far (bench evidence). */
 uint64_t dade_gpu_launch_count(dade_gpu_ctx* ctx);
 
@@ -174,6 +177,9 @@ uint64_t dade_gpu_launch_count(dade_gpu_ctx* ctx);
 int dade_gpu_set_profiling(dade_gpu_ctx* ctx, int on);
 int dade_gpu_last_scan_profile(dade_gpu_ctx* ctx, double* scan_ms, double* scan_bytes,
                                double* total_ms);
+/* Device time (ms) of the streaming tensor-core filter launches of the last
+ * search (the dominant kernel) and how many there were. Requires profiling. */
+int dade_gpu_last_filter_profile(dade_gpu_ctx* ctx, double* filter_ms, int* n_launches);
 
 #ifdef __cplusplus
 }

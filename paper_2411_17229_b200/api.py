@@ -78,6 +78,11 @@ class Device:
     def set_profiling(self, on: bool):
         check(_capi.lib.dade_gpu_set_profiling(self.h, int(on)))
 
+    def last_filter_profile(self):
+        ms, n = C.c_double(), C.c_int()
+        check(_capi.lib.dade_gpu_last_filter_profile(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
     def last_scan_profile(self):
         a, b, c = C.c_double(), C.c_double(), C.c_double()
         check(_capi.lib.dade_gpu_last_scan_profile(self.h, C.byref(a), C.byref(b), C.byref(c)))

@@ -277,7 +277,9 @@ struct dade_gpu_ctx {
     // profiling
     bool profiling = false;
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
-    double last_scan_ms = 0, last_bytes = 0, last_total_ms = 0;
+    cudaEvent_t ef[4] = {nullptr, nullptr, nullptr, nullptr};  // filter launches of the streaming passes
+    int n_filter_passes = 0;
+    double last_scan_ms = 0, last_bytes = 0, last_total_ms = 0, last_filter_ms = 0;
 
     void use_device() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
 };
@@ -405,6 +407,11 @@ void finish_profile(dade_gpu_ctx* c) {
     unsigned long long h[3] = {0, 0, 0};
     cuda_check(cudaMemcpy(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost), "D2H counters");
     c->last_bytes = (double)h[2];
+    c->last_filter_ms = 0;
+    for (int p = 0; p < c->n_filter_passes; ++p) {
+        cuda_check(cudaEventElapsedTime(&ms, c->ef[2 * p], c->ef[2 * p + 1]), "elapsed");
+        c->last_filter_ms += ms;
+    }
 }
 
 __global__ void tighten_from_topk_kernel(const uint64_t* keys, const uint32_t* count, uint32_t nq, uint32_t K,
@@ -492,7 +499,10 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             cuda_check(cudaMemsetAsync(c->item_counter.p, 0, 4, s), "memset");
             f.item_counter = c->item_counter.as<uint32_t>();
             grid = std::min<uint32_t>(grid, (uint32_t)c->n_sms * 2);
+            if (c->profiling) cuda_check(cudaEventRecord(c->ef[2 * pass], s), "event");
             cuda_check(launch_filter(f, tm, grid, s), "filter");
+            if (c->profiling) cuda_check(cudaEventRecord(c->ef[2 * pass + 1], s), "event");
+            c->n_filter_passes = n_pass;
             cuda_check(cudaMemsetAsync(c->cand_count.p, 0, 4, s), "memset");
             cuda_check(cudaMemsetAsync(c->q_count.p, 0, (size_t)nq * 4, s), "memset");
             SurvArgs sv{};
@@ -767,6 +777,7 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     c->counters.ensure(64);
     cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
     record(c, c->e0);
+    c->n_filter_passes = 0;
     if (nq == 0) return;
     const float* d_q = stage_queries(c, queries, nq, dim, flags);
     c->out_keys.ensure((size_t)nq * k * 8);
@@ -823,6 +834,7 @@ int dade_gpu_create(int device, dade_gpu_ctx** out) {
         cuda_check(cudaEventCreate(&c->e1), "event");
         cuda_check(cudaEventCreate(&c->e2), "event");
         cuda_check(cudaEventCreate(&c->e3), "event");
+        for (auto& e : c->ef) cuda_check(cudaEventCreate(&e), "event");
         cuda_check(cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, device), "attr");
         *out = c;
     });
@@ -847,6 +859,7 @@ int dade_gpu_destroy(dade_gpu_ctx* c) {
         cudaEventDestroy(c->e1);
         cudaEventDestroy(c->e2);
         cudaEventDestroy(c->e3);
+        for (auto& e : c->ef) cudaEventDestroy(e);
         cudaStreamDestroy(c->own_stream);
         delete c;
     });
@@ -1378,6 +1391,14 @@ int dade_gpu_set_profiling(dade_gpu_ctx* c, int on) {
     return guarded([&] {
         if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
         c->profiling = on != 0;
+    });
+}
+
+int dade_gpu_last_filter_profile(dade_gpu_ctx* c, double* filter_ms, int* n_launches) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (filter_ms) *filter_ms = c->last_filter_ms;
+        if (n_launches) *n_launches = c->n_filter_passes;
     });
 }
 

@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     nm = subprocess.run(["nm", "-D", "--defined-only", str(_capi.LIB_PATH)], capture_output=True, text=True).stdout
     for s in declared_symbols():
         assert re.search(rf"\bT {s}\b", nm), s
-    assert set(declared_symbols()) <= set(_capi.EXPORTED) | {"dade_gpu_debug_radius"}
+    assert set(declared_symbols()) <= set(_capi.EXPORTED)
 
 
 def test_library_is_sm100a_native():
