@@ -269,7 +269,9 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
     const float* __restrict__ storage, const uint32_t* __restrict__ row_ids, uint32_t dim,
     const float* __restrict__ queries, uint32_t nq, uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,
     uint32_t* out_count) {
-    __shared__ uint64_t d[kSeedMax];
+    extern __shared__ __align__(16) unsigned char seed_smem[];
+    float* seed_tile = reinterpret_cast<float*>(seed_smem);      // [kSeedMax][36] staged slices
+    uint64_t* d = reinterpret_cast<uint64_t*>(seed_smem);        // keys, after the tile is consumed
     const uint32_t q = blockIdx.x;
     const uint32_t list = (uint32_t)probes[(size_t)q * n_probe];
     const uint32_t start = list_offsets[list], len = list_offsets[list + 1] - start;
@@ -277,37 +279,36 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
     if (n < K) return;  // too few rows for a K-th distance (uniform per CTA)
     const float* qr = queries + (size_t)q * dim;
     const uint32_t r0 = threadIdx.x, r1 = threadIdx.x + kSeedThreads;
-    const float* o0 = storage + (size_t)(start + min(r0, n - 1)) * dim;
-    const float* o1 = storage + (size_t)(start + min(r1, n - 1)) * dim;
     float a0 = 0.f, a1 = 0.f;
     if ((dim & 3u) == 0) {
-        uint32_t k = 0;
-        for (; k + 16 <= dim; k += 16) {
-            float4 x0[4], x1[4], y[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                x0[u] = __ldg(reinterpret_cast<const float4*>(o0 + k) + u);
-                x1[u] = __ldg(reinterpret_cast<const float4*>(o1 + k) + u);
-                y[u] = __ldg(reinterpret_cast<const float4*>(qr + k) + u);
+        // Stage 32-dim slices of all S rows in shared memory with coalesced
+        // 16-byte loads (row stride 36 floats: conflict-free LDS.128), then each
+        // thread advances its two rows' exact sequential sums from smem.
+        float* tile = seed_tile;
+        for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
+            const uint32_t w = min(32u, dim - k0), w4 = w >> 2;
+            __syncthreads();
+            for (uint32_t idx = threadIdx.x; idx < (uint32_t)kSeedMax * 8; idx += kSeedThreads) {
+                const uint32_t r = idx >> 3, c4 = idx & 7;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (r < n && c4 < w4) v = __ldg(reinterpret_cast<const float4*>(storage + (size_t)(start + r) * dim + k0) + c4);
+                *reinterpret_cast<float4*>(tile + r * 36 + 4 * c4) = v;
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                a0 = sq_step(a0, x0[u].x, y[u].x); a1 = sq_step(a1, x1[u].x, y[u].x);
-                a0 = sq_step(a0, x0[u].y, y[u].y); a1 = sq_step(a1, x1[u].y, y[u].y);
-                a0 = sq_step(a0, x0[u].z, y[u].z); a1 = sq_step(a1, x1[u].z, y[u].z);
-                a0 = sq_step(a0, x0[u].w, y[u].w); a1 = sq_step(a1, x1[u].w, y[u].w);
+            __syncthreads();
+            for (uint32_t c4 = 0; c4 < w4; ++c4) {
+                const float4 y = __ldg(reinterpret_cast<const float4*>(qr + k0) + c4);
+                const float4 x0 = *reinterpret_cast<const float4*>(tile + r0 * 36 + 4 * c4);
+                const float4 x1 = *reinterpret_cast<const float4*>(tile + r1 * 36 + 4 * c4);
+                a0 = sq_step(a0, x0.x, y.x); a1 = sq_step(a1, x1.x, y.x);
+                a0 = sq_step(a0, x0.y, y.y); a1 = sq_step(a1, x1.y, y.y);
+                a0 = sq_step(a0, x0.z, y.z); a1 = sq_step(a1, x1.z, y.z);
+                a0 = sq_step(a0, x0.w, y.w); a1 = sq_step(a1, x1.w, y.w);
             }
         }
-        for (; k < dim; k += 4) {
-            const float4 x0 = __ldg(reinterpret_cast<const float4*>(o0 + k));
-            const float4 x1 = __ldg(reinterpret_cast<const float4*>(o1 + k));
-            const float4 y = __ldg(reinterpret_cast<const float4*>(qr + k));
-            a0 = sq_step(a0, x0.x, y.x); a1 = sq_step(a1, x1.x, y.x);
-            a0 = sq_step(a0, x0.y, y.y); a1 = sq_step(a1, x1.y, y.y);
-            a0 = sq_step(a0, x0.z, y.z); a1 = sq_step(a1, x1.z, y.z);
-            a0 = sq_step(a0, x0.w, y.w); a1 = sq_step(a1, x1.w, y.w);
-        }
+        __syncthreads();
     } else {
+        const float* o0 = storage + (size_t)(start + min(r0, n - 1)) * dim;
+        const float* o1 = storage + (size_t)(start + min(r1, n - 1)) * dim;
         for (uint32_t k = 0; k < dim; ++k) {
             const float y = __ldg(qr + k);
             a0 = sq_step(a0, __ldg(o0 + k), y);
@@ -356,8 +357,10 @@ cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const u
                                uint32_t nq, uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,
                                uint32_t* out_count, cudaStream_t s) {
     if (nq == 0 || K > (uint32_t)kSeedMax) return cudaSuccess;
-    seed_radius_kernel<<<nq, kSeedThreads, 0, s>>>(probes, n_probe, list_offsets, storage, row_ids, dim, queries, nq,
-                                                    K, std::min<uint32_t>(S, kSeedMax), r_global, out_keys, out_count);
+    const size_t smem = sizeof(float) * kSeedMax * 36;
+    DADE_CUDA_TRY(cudaFuncSetAttribute(seed_radius_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    seed_radius_kernel<<<nq, kSeedThreads, smem, s>>>(probes, n_probe, list_offsets, storage, row_ids, dim, queries, nq,
+                                                       K, std::min<uint32_t>(S, kSeedMax), r_global, out_keys, out_count);
     return cudaGetLastError();
 }
 
