@@ -193,8 +193,8 @@ struct RowNorms {
     const float* get(const float* r, uint32_t nn, uint32_t d, uint32_t dd0, cudaStream_t s) {
         if (r != rows || nn != n || d != dim || dd0 != d0) {
             // padded by 8 floats: the kernel reads 16-byte aligned windows
-            buf.ensure(((size_t)nn + 8) * 4);
-            cuda_check(cudaMemsetAsync(buf.p, 0, ((size_t)nn + 8) * 4, s), "memset");
+            buf.ensure(((size_t)nn + 40) * 4);
+            cuda_check(cudaMemsetAsync(buf.p, 0, ((size_t)nn + 40) * 4, s), "memset");
             cuda_check(launch_row_norms(r, nn, d, dd0, buf.as<float>(), s), "row norms");
             rows = r;
             n = nn;
@@ -441,7 +441,8 @@ struct SeedArgs {
 
 void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, const float* d_q, uint32_t nq,
                    uint32_t k, bool two_pass, uint32_t max_items, const GroupArgs* g, const float* rows,
-                   uint32_t n_rows, TmapCache& tm32, uint64_t* out_keys, uint32_t* out_count, const SeedArgs& seed) {
+                   uint32_t n_rows, TmapCache& tm32, uint64_t* out_keys, uint32_t* out_count, const SeedArgs& seed,
+                   RowNorms* norms) {
     cudaStream_t s = c->stream;
     bool tma = false;
     const CUtensorMap& tm = tm32.get(rows, std::max<uint32_t>(n_rows, 1), a.dim, tma);
@@ -485,6 +486,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             f.flat_block = a.flat_block;
             f.flat_nq = a.flat_nq;
             f.flat_qchunks = a.flat_qchunks;
+            f.row_norms = norms->get(rows, n_rows, a.dim, d0, s);
             f.surv = c->surv.as<Survivor>();
             f.surv_count = c->surv_count.as<uint32_t>();
             f.surv_cap = cap;
@@ -660,7 +662,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     if (use_filter) {
         SeedArgs sd{seeded, c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>()};
         stream_passes(c, a, ct, d_q, nq, k, nrb > 1, (uint32_t)max_items, &g, c->storage.as<float>(), c->count,
-                      c->tm32_storage, out_keys, out_count, sd);
+                      c->tm32_storage, out_keys, out_count, sd, &c->norms_storage);
         record(c, c->e2);
         return;
     }

@@ -202,17 +202,8 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
         st_dco += (uint64_t)nrows * qcount;
         st_bytes += 4ull * d0 * nrows;
 
-        // first-slice row norms from the box (each lane: row `lane`)
-        float no = 0.f;
-        for (int c = 0; c < c_dense; ++c) {
-            const float* b = box(slot, c);
-            const int wc = min(kBox, (int)d0 - c * kBox);
-            for (int k4 = 0; k4 < wc; k4 += 4) {
-                const float4 v = *reinterpret_cast<const float4*>(b + swzf(lane, k4));
-                no = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, no))));
-            }
-        }
-        no *= (1.f - kTcDeltaF);
+        // first-slice row norm of row `lane` (precomputed per row; padded array)
+        const float no = (1.f - kTcDeltaF) * __ldg(a.row_norms + row_start + tb + lane);
 
         // tensor-core filter, queries in halves of 32 (4 n-tiles)
         for (int half = 0; half < 2; ++half) {

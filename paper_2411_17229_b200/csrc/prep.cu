@@ -13,26 +13,32 @@ namespace {
 // ---- K1: out[i][k] = (float) sum_r W[k*D + r] * in[i][r] --------------------
 // f64 accumulation in r order with separately rounded DMUL/DADD, exactly
 // OrthoTransform::transform_vector (proj/src/transform.cpp:221-228).
-constexpr int kRotTile = 32;  // outputs (cols) and rows per CTA
+constexpr int kRotTile = 32;  // output columns per CTA
+constexpr int kRotRows = 64;  // rows per CTA (8 per thread: independent DADD chains)
 constexpr int kRotK = 32;     // r chunk
 
 __global__ void __launch_bounds__(256)
 rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in, uint32_t n,
               float* __restrict__ out) {
     __shared__ double ws[kRotTile][kRotK + 1];
-    __shared__ double xs[kRotTile][kRotK + 1];
+    __shared__ double xs[kRotRows][kRotK + 1];
     const int tx = threadIdx.x & 31;  // output column within tile
-    const int ty = threadIdx.x >> 5;  // 0..7 -> rows ty*4 .. ty*4+3
+    const int ty = threadIdx.x >> 5;  // 0..7 -> rows ty*8 .. ty*8+7
     const uint32_t col0 = blockIdx.x * kRotTile;
-    const uint32_t row0 = blockIdx.y * kRotTile;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const uint32_t row0 = blockIdx.y * kRotRows;
+    double acc[8];
+#pragma unroll
+    for (int ii = 0; ii < 8; ++ii) acc[ii] = 0.0;
     for (uint32_t r0 = 0; r0 < dim; r0 += kRotK) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < kRotTile * kRotK; idx += 256) {
             const int a = idx / kRotK, b = idx % kRotK;
             const uint32_t col = col0 + a, r = r0 + b;
             ws[a][b] = (col < dim && r < dim) ? W[(size_t)col * dim + r] : 0.0;
-            const uint32_t row = row0 + a;
+        }
+        for (int idx = threadIdx.x; idx < kRotRows * kRotK; idx += 256) {
+            const int a = idx / kRotK, b = idx % kRotK;
+            const uint32_t row = row0 + a, r = r0 + b;
             xs[a][b] = (row < n && r < dim) ? (double)in[(size_t)row * dim + r] : 0.0;
         }
         __syncthreads();
@@ -40,14 +46,14 @@ rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restric
         for (int b = 0; b < kmax; ++b) {
             const double w = ws[tx][b];
 #pragma unroll
-            for (int ii = 0; ii < 4; ++ii) acc[ii] = __dadd_rn(acc[ii], __dmul_rn(w, xs[ty * 4 + ii][b]));
+            for (int ii = 0; ii < 8; ++ii) acc[ii] = __dadd_rn(acc[ii], __dmul_rn(w, xs[ty * 8 + ii][b]));
         }
     }
     const uint32_t col = col0 + tx;
     if (col < dim) {
 #pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-            const uint32_t row = row0 + ty * 4 + ii;
+        for (int ii = 0; ii < 8; ++ii) {
+            const uint32_t row = row0 + ty * 8 + ii;
             if (row < n) out[(size_t)row * dim + col] = __double2float_rn(acc[ii]);
         }
     }
@@ -285,15 +291,22 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
         // 16-byte loads (row stride 36 floats: conflict-free LDS.128), then each
         // thread advances its two rows' exact sequential sums from smem.
         float* tile = seed_tile;
+        // this thread stages 16-byte column c4 of rows rb + 32 m (m < 16) of every slice
+        const uint32_t c4 = threadIdx.x & 7, rb = threadIdx.x >> 3;
+        const float* rowp = storage + (size_t)(start + min(rb, n - 1)) * dim + 4 * c4;
+        const size_t rstep = (size_t)32 * dim;
         for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
             const uint32_t w = min(32u, dim - k0), w4 = w >> 2;
             __syncthreads();
-            for (uint32_t idx = threadIdx.x; idx < (uint32_t)kSeedMax * 8; idx += kSeedThreads) {
-                const uint32_t r = idx >> 3, c4 = idx & 7;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (r < n && c4 < w4) v = __ldg(reinterpret_cast<const float4*>(storage + (size_t)(start + r) * dim + k0) + c4);
-                *reinterpret_cast<float4*>(tile + r * 36 + 4 * c4) = v;
+            float4 v[16];
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const uint32_t r = rb + 32 * m;
+                v[m] = (r < n && c4 < w4) ? __ldg(reinterpret_cast<const float4*>(rowp + m * rstep + k0))
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
             }
+#pragma unroll
+            for (int m = 0; m < 16; ++m) *reinterpret_cast<float4*>(tile + (rb + 32 * m) * 36 + 4 * c4) = v[m];
             __syncthreads();
             for (uint32_t c4 = 0; c4 < w4; ++c4) {
                 const float4 y = __ldg(reinterpret_cast<const float4*>(qr + k0) + c4);
@@ -373,7 +386,7 @@ cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s) {
 cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
                           cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    dim3 grid((dim + kRotTile - 1) / kRotTile, (n + kRotTile - 1) / kRotTile);
+    dim3 grid((dim + kRotTile - 1) / kRotTile, (n + kRotRows - 1) / kRotRows);
     rotate_kernel<<<grid, 256, 0, s>>>(W, dim, in, n, out);
     return cudaGetLastError();
 }

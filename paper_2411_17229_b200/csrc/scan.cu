@@ -1002,6 +1002,7 @@ merge_buckets_kernel(const uint64_t* __restrict__ bucket, const uint32_t* __rest
                      const uint32_t* __restrict__ q_count, uint32_t nq, uint32_t K, uint64_t* out_keys,
                      uint32_t* out_count) {
     __shared__ uint64_t bbuf[4][256];
+    __shared__ uint64_t abuf[4][kStageMaxK];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t q = blockIdx.x * 4 + warp;
     if (q >= nq) return;
@@ -1014,7 +1015,8 @@ merge_buckets_kernel(const uint64_t* __restrict__ bucket, const uint32_t* __rest
         const uint32_t m = min(256u, cnt - b0);
         for (uint32_t e = lane; e < m; e += 32) B[e] = src[b0 + e];
         __syncwarp();
-        warp_merge(A, cA, K, B, m, false);
+        if (K <= (uint32_t)kStageMaxK) warp_merge_staged(A, cA, K, B, m, abuf[warp]);
+        else warp_merge(A, cA, K, B, m, false);
         __syncwarp();
     }
     const uint32_t c = *reinterpret_cast<volatile uint32_t*>(cA);
