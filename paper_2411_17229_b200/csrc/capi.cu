@@ -463,9 +463,15 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         cuda_check(cudaMemsetAsync(c->surv_max.p, 0, 4, s), "memset");
         cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
         if (seed.on) {
-            cuda_check(launch_seed_radius(seed.probes, seed.n_probe, seed.offsets, rows, a.row_ids, a.dim, d_q, nq, k,
-                                          seed_rows(k), a.r_global, out_keys, out_count, s),
-                       "seed radius");
+            if (g && g->n_rb >= 1 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
+                cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->n_lists, seed.offsets,
+                                                    rows, a.row_ids, a.dim, d_q, k, seed_rows(k), a.r_global,
+                                                    out_keys, out_count, s),
+                           "seed radius (lists)");
+            else
+                cuda_check(launch_seed_radius(seed.probes, seed.n_probe, seed.offsets, rows, a.row_ids, a.dim, d_q, nq,
+                                              k, seed_rows(k), a.r_global, out_keys, out_count, s),
+                           "seed radius");
             ++c->launches;
         }
         const int n_pass = two_pass ? 2 : 1;

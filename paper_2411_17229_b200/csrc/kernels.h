@@ -121,6 +121,11 @@ cudaError_t launch_keys_to_results(const uint64_t* keys, const uint32_t* count, 
 
 // prep.cu
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s);
+cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* bucket_off, const uint32_t* bucket_q,
+                                     uint32_t n_lists, const uint32_t* list_offsets, const float* storage,
+                                     const uint32_t* row_ids, uint32_t dim, const float* queries, uint32_t K,
+                                     uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
+                                     cudaStream_t s);
 cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const uint32_t* list_offsets,
                                const float* storage, const uint32_t* row_ids, uint32_t dim, const float* queries,
                                uint32_t nq, uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,

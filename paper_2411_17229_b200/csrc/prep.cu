@@ -358,6 +358,111 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
     }
 }
 
+// List-major seed: one CTA per nearest list, for the queries whose nearest
+// list it is (the rank-bucket-0 bucket), 8 queries at a time: the list's first
+// S rows are staged once per 32-dim slice (coalesced, shared by the 8 queries)
+// and every thread advances 2 rows x 8 queries of exact sequential sums; then
+// one warp per query sorts its S keys. Same output as seed_radius_kernel.
+constexpr int kSeedGroup = 8;
+__global__ void __launch_bounds__(kSeedThreads) seed_radius_list_kernel(
+    const uint32_t* __restrict__ counts, const uint32_t* __restrict__ bucket_off, const uint32_t* __restrict__ bucket_q,
+    uint32_t n_lists, const uint32_t* __restrict__ list_offsets, const float* __restrict__ storage,
+    const uint32_t* __restrict__ row_ids, uint32_t dim, const float* __restrict__ queries, uint32_t K, uint32_t S,
+    uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count) {
+    extern __shared__ __align__(16) unsigned char seed_smem[];
+    float* tile = reinterpret_cast<float*>(seed_smem);                 // [kSeedMax][36]
+    float* qt = tile + kSeedMax * 36;                                  // [kSeedGroup][32]
+    float* accs = qt + kSeedGroup * 32;                                // [kSeedGroup][kSeedMax]
+    uint64_t* keys = reinterpret_cast<uint64_t*>(accs + kSeedGroup * kSeedMax);  // [8 warps][kSeedMax]
+    const uint32_t list = blockIdx.x;
+    const uint32_t cnt = counts[list];  // entry e = list of rank bucket 0
+    if (cnt == 0) return;
+    const uint32_t start = list_offsets[list], len = list_offsets[list + 1] - start;
+    const uint32_t n = min(len, S);
+    if (n < K) return;
+    const uint32_t* qs = bucket_q + bucket_off[list];
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t c4 = tid & 7, rb = tid >> 3;
+    const float* rowp = storage + (size_t)(start + min(rb, n - 1)) * dim + 4 * c4;
+    const size_t rstep = (size_t)32 * dim;
+    const uint32_t r0 = tid, r1 = tid + kSeedThreads;
+    for (uint32_t g0 = 0; g0 < cnt; g0 += kSeedGroup) {
+        const uint32_t ng = min((uint32_t)kSeedGroup, cnt - g0);
+        float a0[kSeedGroup], a1[kSeedGroup];
+#pragma unroll
+        for (int u = 0; u < kSeedGroup; ++u) a0[u] = a1[u] = 0.f;
+        for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
+            const uint32_t w = min(32u, dim - k0), w4 = w >> 2;
+            __syncthreads();
+            float4 v[16];
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const uint32_t r = rb + 32 * m;
+                v[m] = (r < n && c4 < w4) ? __ldg(reinterpret_cast<const float4*>(rowp + m * rstep + k0))
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int m = 0; m < 16; ++m) *reinterpret_cast<float4*>(tile + (rb + 32 * m) * 36 + 4 * c4) = v[m];
+            if (tid < kSeedGroup * 32) {
+                const uint32_t u = tid >> 5, k = tid & 31;
+                qt[tid] = (u < ng && k < w) ? __ldg(queries + (size_t)qs[g0 + u] * dim + k0 + k) : 0.f;
+            }
+            __syncthreads();
+            for (uint32_t cc = 0; cc < w4; ++cc) {
+                const float4 x0 = *reinterpret_cast<const float4*>(tile + r0 * 36 + 4 * cc);
+                const float4 x1 = *reinterpret_cast<const float4*>(tile + r1 * 36 + 4 * cc);
+#pragma unroll
+                for (int u = 0; u < kSeedGroup; ++u) {
+                    const float4 y = *reinterpret_cast<const float4*>(qt + u * 32 + 4 * cc);
+                    a0[u] = sq_step(a0[u], x0.x, y.x); a1[u] = sq_step(a1[u], x1.x, y.x);
+                    a0[u] = sq_step(a0[u], x0.y, y.y); a1[u] = sq_step(a1[u], x1.y, y.y);
+                    a0[u] = sq_step(a0[u], x0.z, y.z); a1[u] = sq_step(a1[u], x1.z, y.z);
+                    a0[u] = sq_step(a0[u], x0.w, y.w); a1[u] = sq_step(a1[u], x1.w, y.w);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kSeedGroup; ++u) {
+            accs[u * kSeedMax + r0] = a0[u];
+            accs[u * kSeedMax + r1] = a1[u];
+        }
+        __syncthreads();
+        if (warp < ng) {  // one warp per query: keys, bitonic sort, outputs
+            const uint32_t q = qs[g0 + warp];
+            uint64_t* kk = keys + warp * kSeedMax;
+            for (uint32_t r = lane; r < (uint32_t)kSeedMax; r += 32) {
+                uint64_t key = ~0ull;
+                if (r < n) {
+                    const uint32_t id = row_ids ? __ldg(row_ids + start + r) : start + r;
+                    key = make_key(__fsqrt_rn(accs[warp * kSeedMax + r]), id);
+                }
+                kk[r] = key;
+            }
+            __syncwarp();
+            for (uint32_t size = 2; size <= (uint32_t)kSeedMax; size <<= 1) {
+                for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (uint32_t i = lane; i < (uint32_t)kSeedMax / 2; i += 32) {
+                        const uint32_t lo = 2 * i - (i & (stride - 1));
+                        const uint32_t hi = lo + stride;
+                        const bool up = (lo & size) == 0;
+                        const uint64_t x = kk[lo], y = kk[hi];
+                        if ((x > y) == up) {
+                            kk[lo] = y;
+                            kk[hi] = x;
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            if (lane == 0) atomicMin(r_global + q, (uint32_t)(kk[K - 1] >> 32));
+            if (out_keys) {
+                for (uint32_t i = lane; i < K; i += 32) out_keys[(size_t)q * K + i] = kk[i];
+                if (lane == 0) out_count[q] = K;
+            }
+        }
+    }
+}
+
 __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, size_t n) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -374,6 +479,22 @@ cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const u
     DADE_CUDA_TRY(cudaFuncSetAttribute(seed_radius_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     seed_radius_kernel<<<nq, kSeedThreads, smem, s>>>(probes, n_probe, list_offsets, storage, row_ids, dim, queries, nq,
                                                        K, std::min<uint32_t>(S, kSeedMax), r_global, out_keys, out_count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* bucket_off, const uint32_t* bucket_q,
+                                     uint32_t n_lists, const uint32_t* list_offsets, const float* storage,
+                                     const uint32_t* row_ids, uint32_t dim, const float* queries, uint32_t K,
+                                     uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
+                                     cudaStream_t s) {
+    if (n_lists == 0 || K > (uint32_t)kSeedMax) return cudaSuccess;
+    const size_t smem = sizeof(float) * (kSeedMax * 36 + kSeedGroup * 32 + kSeedGroup * kSeedMax) +
+                        sizeof(uint64_t) * (kSeedThreads / 32) * kSeedMax;
+    DADE_CUDA_TRY(cudaFuncSetAttribute(seed_radius_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    seed_radius_list_kernel<<<n_lists, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, n_lists, list_offsets,
+                                                                 storage, row_ids, dim, queries, K,
+                                                                 std::min<uint32_t>(S, kSeedMax), r_global, out_keys,
+                                                                 out_count);
     return cudaGetLastError();
 }
 
