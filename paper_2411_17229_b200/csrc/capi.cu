@@ -265,7 +265,7 @@ struct dade_gpu_ctx {
     DevBuf q_in, q_rot, probes, probe_count, c_seg_keys, c_seg_count, c_r;
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
-    DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter;
+    DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter, seed_goff;
     int n_sms = 148;
     uint32_t surv_cap_hint = 0;
     DevBuf counters, phase;
@@ -464,9 +464,9 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
         if (seed.on) {
             if (g && g->n_rb >= 1 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
-                cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->n_lists, seed.offsets,
-                                                    rows, a.row_ids, a.dim, d_q, k, seed_rows(k), a.r_global,
-                                                    out_keys, out_count, s),
+                cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->n_lists,
+                                                    nq / 8 + g->n_lists + 1, seed.offsets, rows, a.row_ids, a.dim,
+                                                    d_q, k, seed_rows(k), a.r_global, out_keys, out_count, s),
                            "seed radius (lists)");
             else
                 cuda_check(launch_seed_radius(seed.probes, seed.n_probe, seed.offsets, rows, a.row_ids, a.dim, d_q, nq,
@@ -629,6 +629,8 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     g.bucket_slot = c->bucket_slot.as<uint32_t>();
     g.items = c->items.as<WorkItem>();
     g.n_items = c->n_items.as<uint32_t>();
+    c->seed_goff.ensure(((size_t)c->n_clusters + 1) * 4);
+    g.seed_goff = c->seed_goff.as<uint32_t>();
     cuda_check(launch_group(g, s), "group");
     c->launches += 4;
     // K4 scan

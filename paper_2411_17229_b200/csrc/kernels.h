@@ -122,7 +122,8 @@ cudaError_t launch_keys_to_results(const uint64_t* keys, const uint32_t* count, 
 // prep.cu
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s);
 cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* bucket_off, const uint32_t* bucket_q,
-                                     uint32_t n_lists, const uint32_t* list_offsets, const float* storage,
+                                     const uint32_t* seed_goff, uint32_t n_lists, uint32_t max_groups,
+                                     const uint32_t* list_offsets, const float* storage,
                                      const uint32_t* row_ids, uint32_t dim, const float* queries, uint32_t K,
                                      uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
                                      cudaStream_t s);
@@ -151,6 +152,7 @@ struct GroupArgs {
     uint32_t* n_items;              // [2]: all items, rank-bucket-0 items
     uint32_t max_item_rows;         // 0: one item per (list, query chunk); else split rows
     uint32_t seed_skip, seed_min;   // rank-0 lists of >= seed_min rows skip their first seed_skip rows
+    uint32_t* seed_goff;            // nullable [n_lists + 1]: prefix of ceil(rank-0 count / 8)
 };
 cudaError_t launch_group(const GroupArgs& g, cudaStream_t s);
 

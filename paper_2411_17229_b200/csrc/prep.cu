@@ -96,35 +96,42 @@ __device__ __forceinline__ uint32_t entry_items(const GroupArgs& g, uint32_t e, 
 }
 
 __global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
-    __shared__ uint32_t s_b[1024], s_i[1024];
+    __shared__ uint32_t s_b[1024], s_i[1024], s_g[1024];
     const uint32_t n = g.n_rb * g.n_lists;
     const uint32_t per = (n + 1023) / 1024;
     const uint32_t lo = threadIdx.x * per, hi = min(n, lo + per);
-    uint32_t sb = 0, si = 0;
+    uint32_t sb = 0, si = 0, sg = 0;
     for (uint32_t e = lo; e < hi; ++e) {
         const uint32_t c = g.counts[e];
         sb += c;
         si += entry_items(g, e, c);
+        if (e < g.n_lists) sg += (c + 7) / 8;  // seed groups of the nearest-list bucket
     }
     s_b[threadIdx.x] = sb;
     s_i[threadIdx.x] = si;
+    s_g[threadIdx.x] = sg;
     __syncthreads();
     for (int off = 1; off < 1024; off <<= 1) {
         const uint32_t vb = threadIdx.x >= (unsigned)off ? s_b[threadIdx.x - off] : 0;
         const uint32_t vi = threadIdx.x >= (unsigned)off ? s_i[threadIdx.x - off] : 0;
+        const uint32_t vg = threadIdx.x >= (unsigned)off ? s_g[threadIdx.x - off] : 0;
         __syncthreads();
         s_b[threadIdx.x] += vb;
         s_i[threadIdx.x] += vi;
+        s_g[threadIdx.x] += vg;
         __syncthreads();
     }
-    uint32_t rb = s_b[threadIdx.x] - sb, ri = s_i[threadIdx.x] - si;
+    uint32_t rb = s_b[threadIdx.x] - sb, ri = s_i[threadIdx.x] - si, rg = s_g[threadIdx.x] - sg;
     for (uint32_t e = lo; e < hi; ++e) {
         const uint32_t c = g.counts[e];
         g.bucket_off[e] = rb;
         g.item_off[e] = ri;
+        if (g.seed_goff && e < g.n_lists) g.seed_goff[e] = rg;
         rb += c;
         ri += entry_items(g, e, c);
+        if (e < g.n_lists) rg += (c + 7) / 8;
     }
+    if (g.seed_goff && threadIdx.x == 1023) g.seed_goff[g.n_lists] = s_g[1023];
     if (threadIdx.x == 1023) g.n_items[0] = s_i[1023];
     __syncthreads();
     // items of rank bucket 0 (every query's nearest list) come first
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
 constexpr int kSeedGroup = 8;
 __global__ void __launch_bounds__(kSeedThreads) seed_radius_list_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ bucket_off, const uint32_t* __restrict__ bucket_q,
-    uint32_t n_lists, const uint32_t* __restrict__ list_offsets, const float* __restrict__ storage,
+    const uint32_t* __restrict__ seed_goff, uint32_t n_lists, const uint32_t* __restrict__ list_offsets, const float* __restrict__ storage,
     const uint32_t* __restrict__ row_ids, uint32_t dim, const float* __restrict__ queries, uint32_t K, uint32_t S,
     uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count) {
     extern __shared__ __align__(16) unsigned char seed_smem[];
@@ -374,9 +381,18 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_list_kernel(
     float* qt = tile + kSeedMax * 36;                                  // [kSeedGroup][32]
     float* accs = qt + kSeedGroup * 32;                                // [kSeedGroup][kSeedMax]
     uint64_t* keys = reinterpret_cast<uint64_t*>(accs + kSeedGroup * kSeedMax);  // [8 warps][kSeedMax]
-    const uint32_t list = blockIdx.x;
-    const uint32_t cnt = counts[list];  // entry e = list of rank bucket 0
-    if (cnt == 0) return;
+    // CTA -> (list, group): binary search in the per-list group prefix
+    const uint32_t b = blockIdx.x;
+    if (b >= seed_goff[n_lists]) return;
+    uint32_t lo_l = 0, hi_l = n_lists;
+    while (hi_l - lo_l > 1) {
+        const uint32_t mid = (lo_l + hi_l) >> 1;
+        if (seed_goff[mid] <= b) lo_l = mid; else hi_l = mid;
+    }
+    const uint32_t list = lo_l;
+    const uint32_t cnt_all = counts[list];  // entry e = list of rank bucket 0
+    const uint32_t gfirst = (b - seed_goff[list]) * kSeedGroup;
+    if (gfirst >= cnt_all) return;
     const uint32_t start = list_offsets[list], len = list_offsets[list + 1] - start;
     const uint32_t n = min(len, S);
     if (n < K) return;
@@ -386,7 +402,8 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_list_kernel(
     const float* rowp = storage + (size_t)(start + min(rb, n - 1)) * dim + 4 * c4;
     const size_t rstep = (size_t)32 * dim;
     const uint32_t r0 = tid, r1 = tid + kSeedThreads;
-    for (uint32_t g0 = 0; g0 < cnt; g0 += kSeedGroup) {
+    const uint32_t cnt = min(cnt_all, gfirst + kSeedGroup);
+    for (uint32_t g0 = gfirst; g0 < cnt; g0 += kSeedGroup) {
         const uint32_t ng = min((uint32_t)kSeedGroup, cnt - g0);
         float a0[kSeedGroup], a1[kSeedGroup];
 #pragma unroll
@@ -483,7 +500,8 @@ cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const u
 }
 
 cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* bucket_off, const uint32_t* bucket_q,
-                                     uint32_t n_lists, const uint32_t* list_offsets, const float* storage,
+                                     const uint32_t* seed_goff, uint32_t n_lists, uint32_t max_groups,
+                                     const uint32_t* list_offsets, const float* storage,
                                      const uint32_t* row_ids, uint32_t dim, const float* queries, uint32_t K,
                                      uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
                                      cudaStream_t s) {
@@ -491,7 +509,8 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
     const size_t smem = sizeof(float) * (kSeedMax * 36 + kSeedGroup * 32 + kSeedGroup * kSeedMax) +
                         sizeof(uint64_t) * (kSeedThreads / 32) * kSeedMax;
     DADE_CUDA_TRY(cudaFuncSetAttribute(seed_radius_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    seed_radius_list_kernel<<<n_lists, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, n_lists, list_offsets,
+    seed_radius_list_kernel<<<max_groups, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, seed_goff, n_lists,
+                                                                    list_offsets,
                                                                  storage, row_ids, dim, queries, K,
                                                                  std::min<uint32_t>(S, kSeedMax), r_global, out_keys,
                                                                  out_count);
