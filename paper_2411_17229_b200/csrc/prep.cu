@@ -377,10 +377,11 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_list_kernel(
     const uint32_t* __restrict__ row_ids, uint32_t dim, const float* __restrict__ queries, uint32_t K, uint32_t S,
     uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count) {
     extern __shared__ __align__(16) unsigned char seed_smem[];
-    float* tile = reinterpret_cast<float*>(seed_smem);                 // [kSeedMax][36]
-    float* qt = tile + kSeedMax * 36;                                  // [kSeedGroup][32]
-    float* accs = qt + kSeedGroup * 32;                                // [kSeedGroup][kSeedMax]
-    uint64_t* keys = reinterpret_cast<uint64_t*>(accs + kSeedGroup * kSeedMax);  // [8 warps][kSeedMax]
+    float* qt = reinterpret_cast<float*>(seed_smem);                   // [kSeedGroup][32]
+    float* tile = qt + kSeedGroup * 32;                                // [kSeedMax][36]
+    // after the last slice the tile's space is reused: sums, then sort keys
+    float* accs = tile;                                                // [kSeedGroup][kSeedMax]
+    uint64_t* keys = reinterpret_cast<uint64_t*>(tile + kSeedGroup * kSeedMax);  // [8 warps][kSeedMax]
     // CTA -> (list, group): binary search in the per-list group prefix
     const uint32_t b = blockIdx.x;
     if (b >= seed_goff[n_lists]) return;
@@ -438,6 +439,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_list_kernel(
                 }
             }
         }
+        __syncthreads();  // everyone done reading the last slice
 #pragma unroll
         for (int u = 0; u < kSeedGroup; ++u) {
             accs[u * kSeedMax + r0] = a0[u];
@@ -506,8 +508,7 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
                                      uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
                                      cudaStream_t s) {
     if (n_lists == 0 || K > (uint32_t)kSeedMax) return cudaSuccess;
-    const size_t smem = sizeof(float) * (kSeedMax * 36 + kSeedGroup * 32 + kSeedGroup * kSeedMax) +
-                        sizeof(uint64_t) * (kSeedThreads / 32) * kSeedMax;
+    const size_t smem = sizeof(float) * (kSeedMax * 36 + kSeedGroup * 32);  // sums + keys alias the tile
     DADE_CUDA_TRY(cudaFuncSetAttribute(seed_radius_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     seed_radius_list_kernel<<<max_groups, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, seed_goff, n_lists,
                                                                     list_offsets,
