@@ -941,47 +941,9 @@ int dade_gpu_set_ivf(dade_gpu_ctx* c, uint32_t dim, uint32_t count, uint32_t n_c
             }
             rows = tmp.data();
         }
-        // Device posting order: rows of each list sorted by (distance to the
-        // list's centroid, id). Results do not depend on scan order (FD returns
-        // the K smallest (dist, id) of the probed set; DADE thresholds are
-        // batch-staled anyway), but the radius seed reads the first rows of a
-        // query's nearest list, and the most central rows make the tightest
-        // seed. The ids array travels with the rows.
-        std::vector<float> srt;
-        std::vector<uint32_t> sid;
-        const uint32_t* ids_up = ids;
-        if (!env_flag("DADE_GPU_NO_REORDER") && count > 0) {
-            srt.resize((size_t)count * dim);
-            sid.resize(count);
-            std::vector<std::pair<float, uint32_t>> key;
-            for (uint32_t cl = 0; cl < n_clusters; ++cl) {
-                const uint32_t b = offsets[cl], len = offsets[cl + 1] - b;
-                const float* cen = centroids + (size_t)cl * dim;
-                key.resize(len);
-                for (uint32_t pos = 0; pos < len; ++pos) {
-                    const float* r = rows + (size_t)(b + pos) * dim;
-                    float acc = 0.f;
-                    for (uint32_t k = 0; k < dim; ++k) {
-                        const float d = r[k] - cen[k];
-                        acc += d * d;
-                    }
-                    key[pos] = {acc, pos};
-                }
-                std::sort(key.begin(), key.end(), [&](const auto& x, const auto& y) {
-                    return x.first != y.first ? x.first < y.first : ids[b + x.second] < ids[b + y.second];
-                });
-                for (uint32_t i = 0; i < len; ++i) {
-                    std::memcpy(srt.data() + (size_t)(b + i) * dim, rows + (size_t)(b + key[i].second) * dim,
-                                sizeof(float) * dim);
-                    sid[b + i] = ids[b + key[i].second];
-                }
-            }
-            rows = srt.data();
-            ids_up = sid.data();
-        }
         upload(c->centroids, centroids, (size_t)n_clusters * dim * 4, c->stream);
         upload(c->storage, rows, (size_t)count * dim * 4, c->stream);
-        upload(c->ids, ids_up, (size_t)count * 4, c->stream);
+        upload(c->ids, ids, (size_t)count * 4, c->stream);
         upload(c->offsets, offsets, (size_t)(n_clusters + 1) * 4, c->stream);
         cuda_check(cudaStreamSynchronize(c->stream), "ivf upload");
         c->dim = dim;
