@@ -29,6 +29,11 @@ namespace {
 
 thread_local std::string g_last_error;
 
+bool env_flag(const char* name) {
+    const char* e = std::getenv(name);
+    return e && e[0] == '1';
+}
+
 struct ApiError : std::runtime_error {
     int code;
     ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
@@ -266,6 +271,8 @@ struct dade_gpu_ctx {
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
     DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter, seed_goff;
+    DevBuf cnorm, qnorm, coarse_lo, coarse_hi, coarse_overflow;
+    bool coarse_force_exact = false, coarse_tc_used = false;
     int n_sms = 148;
     uint32_t surv_cap_hint = 0;
     DevBuf counters, phase;
@@ -321,6 +328,33 @@ void set_tables(dade_gpu_ctx* c, uint32_t kind, uint32_t dim, std::vector<uint32
 // squared-distance key space.
 void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_probe) {
     cudaStream_t s = c->stream;
+    c->probes.ensure((size_t)nq * n_probe * 8);
+    c->probe_count.ensure((size_t)nq * 4);
+    if (n_probe <= 256 && !c->coarse_force_exact && !env_flag("DADE_GPU_NO_TC_COARSE")) {
+        // tensor-core p~ for all (query, centroid) pairs + exact l2_sq on the
+        // boundary candidates (coarse.cu); query chunks bound the p~ buffers
+        const uint32_t chunk = (uint32_t)std::max<uint64_t>(
+            64, std::min<uint64_t>(nq, (256ull << 20) / (8ull * c->n_clusters)));
+        c->cnorm.ensure((size_t)c->n_clusters * 4);
+        c->qnorm.ensure((size_t)chunk * 4);
+        c->coarse_lo.ensure((size_t)chunk * c->n_clusters * 4);
+        c->coarse_hi.ensure((size_t)chunk * c->n_clusters * 4);
+        c->coarse_overflow.ensure(4);
+        cuda_check(cudaMemsetAsync(c->coarse_overflow.p, 0, 4, s), "memset");
+        for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
+            const uint32_t m = std::min(chunk, nq - q0);
+            cuda_check(launch_coarse_tc(c->centroids.as<float>(), c->n_clusters, d_q + (size_t)q0 * c->dim, m, c->dim,
+                                        n_probe, c->cnorm.as<float>(), c->qnorm.as<float>(),
+                                        c->coarse_lo.as<float>(), c->coarse_hi.as<float>(),
+                                        c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
+                                        c->coarse_overflow.as<uint32_t>(), s),
+                       "coarse tc");
+            c->launches += 4;
+        }
+        c->coarse_tc_used = true;
+        return;
+    }
+    c->coarse_tc_used = false;
     const uint32_t qchunks = (nq + kQC - 1) / kQC;
     const uint32_t max_blocks = (c->n_clusters + kRT - 1) / kRT;
     uint32_t nb = std::max<uint32_t>(1, std::min<uint32_t>(max_blocks, (1184 + qchunks - 1) / qchunks));
@@ -372,11 +406,6 @@ uint32_t seed_rows(uint32_t k) {
     uint32_t s = kSeedRowsDefault;
     if (const char* e = std::getenv("DADE_GPU_SEED_ROWS")) s = (uint32_t)std::atoi(e);
     return std::min<uint32_t>(512, std::max<uint32_t>(s, k));
-}
-
-bool env_flag(const char* name) {
-    const char* e = std::getenv(name);
-    return e && e[0] == '1';
 }
 
 bool seed_disabled() {
@@ -817,6 +846,24 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     }
     record(c, c->e3);
     if (!dev) cuda_check(cudaStreamSynchronize(s), "search");
+    if (c->coarse_tc_used) {
+        // more boundary candidates than the exact stage holds (pathological
+        // ties): redo the search with the all-exact coarse ranking
+        uint32_t ov = 0;
+        cuda_check(cudaMemcpyAsync(&ov, c->coarse_overflow.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        if (ov) {
+            c->coarse_force_exact = true;
+            try {
+                search_common(c, queries, nq, dim, k, flags, out_ids, out_dists, out_counts, stats, run);
+            } catch (...) {
+                c->coarse_force_exact = false;
+                throw;
+            }
+            c->coarse_force_exact = false;
+            return;
+        }
+    }
     collect_stats(c, stats);
     finish_profile(c);
 }

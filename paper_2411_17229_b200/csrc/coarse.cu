@@ -1,0 +1,260 @@
+// Coarse ranking (K2, proj/src/ivf.cpp:215-219) on tensor cores with an exact
+// boundary: the n_probe nearest centroids by exact fp32 l2_sq, ties by id.
+//
+//   1. coarse_tc_kernel: p~(q, c) = |q|^2 + |c|^2 - 2 q.c over all D dims with
+//      mma.sync TF32 (fp32 bits read as TF32); writes lo = p~ - delta and
+//      hi = p~ + delta, delta = kCoarseDelta (|q|^2 + |c|^2) bounding |p~ - acc|
+//      for the reference's exact sequential fp32 l2_sq `acc` (same derivation
+//      as the scan filter, with D-term accumulation < 1e-4).
+//   2. coarse_select_kernel (warp per query): B = n_probe-th smallest hi (radix
+//      select on float bits) bounds the n_probe-th smallest exact acc, so every
+//      exact top-n_probe centroid has lo <= B; those candidates get the exact
+//      sequential l2_sq and are sorted by (acc, id); the first n_probe are the
+//      probes, bit-identical to the reference ranking.
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dade_gpu {
+
+namespace {
+
+constexpr float kCoarseDelta = 4e-3f;
+constexpr int kCQ = 64;     // queries per CTA tile
+constexpr int kCC = 128;    // centroids per CTA tile
+constexpr int kCK = 32;     // dims per staged slice
+constexpr int kCS = kCK + 4;  // padded smem row (floats)
+
+__device__ __forceinline__ void mma_tf32_c(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                           uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// CTA: 128 centroids (M) x 64 queries (N); 8 warps = 4 (M: 32 rows each) x 2 (N: 32 cols each).
+__global__ void __launch_bounds__(256) coarse_tc_kernel(const float* __restrict__ cen, uint32_t n_cen,
+                                                        const float* __restrict__ q, uint32_t nq, uint32_t dim,
+                                                        const float* __restrict__ cnorm, const float* __restrict__ qnorm,
+                                                        float* __restrict__ lo_out, float* __restrict__ hi_out) {
+    __shared__ __align__(16) float cs[kCC * kCS];
+    __shared__ __align__(16) float qs[kCQ * kCS];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, tq = lane & 3;
+    const int wm = warp & 3, wn = warp >> 2;
+    const uint32_t c0 = blockIdx.x * kCC, q0 = blockIdx.y * kCQ;
+    float d[2][4][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) d[a][b][v] = 0.f;
+    const bool vec = (dim & 3u) == 0;
+    for (uint32_t k0 = 0; k0 < dim; k0 += kCK) {
+        const uint32_t w = min((uint32_t)kCK, dim - k0);
+        __syncthreads();
+        for (uint32_t idx = tid; idx < (uint32_t)kCC * (kCK / 4); idx += 256) {
+            const uint32_t r = idx >> 3, c4 = idx & 7;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c0 + r < n_cen) {
+                const float* src = cen + (size_t)(c0 + r) * dim + k0 + 4 * c4;
+                if (vec && 4 * c4 + 4 <= w) v = __ldg(reinterpret_cast<const float4*>(src));
+                else {
+                    float t[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (int e = 0; e < 4; ++e) if (4 * c4 + e < w) t[e] = __ldg(src + e);
+                    v = make_float4(t[0], t[1], t[2], t[3]);
+                }
+            }
+            *reinterpret_cast<float4*>(cs + r * kCS + 4 * c4) = v;
+        }
+        for (uint32_t idx = tid; idx < (uint32_t)kCQ * (kCK / 4); idx += 256) {
+            const uint32_t r = idx >> 3, c4 = idx & 7;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (q0 + r < nq) {
+                const float* src = q + (size_t)(q0 + r) * dim + k0 + 4 * c4;
+                if (vec && 4 * c4 + 4 <= w) v = __ldg(reinterpret_cast<const float4*>(src));
+                else {
+                    float t[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (int e = 0; e < 4; ++e) if (4 * c4 + e < w) t[e] = __ldg(src + e);
+                    v = make_float4(t[0], t[1], t[2], t[3]);
+                }
+            }
+            *reinterpret_cast<float4*>(qs + r * kCS + 4 * c4) = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < kCK; ks += 8) {
+            uint32_t A[2][4];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const float* r0 = cs + (wm * 32 + mt * 16 + g) * kCS + ks + tq;
+                A[mt][0] = __float_as_uint(r0[0]);
+                A[mt][1] = __float_as_uint(r0[8 * kCS]);
+                A[mt][2] = __float_as_uint(r0[4]);
+                A[mt][3] = __float_as_uint(r0[8 * kCS + 4]);
+            }
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                const float* qb = qs + (wn * 32 + nt * 8 + g) * kCS + ks + tq;
+                const uint32_t b0 = __float_as_uint(qb[0]), b1 = __float_as_uint(qb[4]);
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) mma_tf32_c(d[mt][nt], A[mt][0], A[mt][1], A[mt][2], A[mt][3], b0, b1);
+            }
+        }
+    }
+    // epilogue: row = centroid, col = query
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t c = c0 + wm * 32 + mt * 16 + h * 8 + g;
+            if (c >= n_cen) continue;
+            const float cn = cnorm[c];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int cq = 0; cq < 2; ++cq) {
+                    const uint32_t qq = q0 + wn * 32 + nt * 8 + 2 * tq + cq;
+                    if (qq >= nq) continue;
+                    const float s = cn + qnorm[qq];
+                    const float p = fmaf(-2.f, d[mt][nt][h * 2 + cq], s);
+                    const float dl = kCoarseDelta * s;
+                    lo_out[(size_t)qq * n_cen + c] = p - dl;
+                    hi_out[(size_t)qq * n_cen + c] = p + dl;
+                }
+        }
+}
+
+__global__ void sq_norms_kernel(const float* __restrict__ rows, uint32_t n, uint32_t dim, float* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* r = rows + (size_t)i * dim;
+    float a = 0.f;
+    for (uint32_t k = 0; k < dim; ++k) a = fmaf(r[k], r[k], a);
+    out[i] = a;
+}
+
+// order-preserving key of a float (any sign)
+__device__ __forceinline__ uint32_t fkey(float x) {
+    const uint32_t u = __float_as_uint(x);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+constexpr int kSelCap = 512;  // exact-candidate list per query
+
+// Warp per query (4 warps per CTA).
+__global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restrict__ lo, const float* __restrict__ hi,
+                                                            const float* __restrict__ cen, uint32_t n_cen,
+                                                            const float* __restrict__ q, uint32_t nq, uint32_t dim,
+                                                            uint32_t n_probe, uint64_t* __restrict__ probes,
+                                                            uint32_t* __restrict__ overflow) {
+    __shared__ uint32_t hist[4][256];
+    __shared__ uint64_t cand[4][kSelCap];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t qi = blockIdx.x * 4 + warp;
+    if (qi >= nq) return;
+    const float* hrow = hi + (size_t)qi * n_cen;
+    const float* lrow = lo + (size_t)qi * n_cen;
+    uint32_t* h = hist[warp];
+    // radix select: key of the n_probe-th smallest hi (4 passes of 8 bits)
+    uint32_t prefix = 0, rank = n_probe;  // rank: 1-based within the current prefix class
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        for (int b = lane; b < 256; b += 32) h[b] = 0;
+        __syncwarp();
+        const uint32_t mask_hi = pass == 0 ? 0u : (0xffffffffu << (32 - 8 * pass));
+        for (uint32_t c = lane; c < n_cen; c += 32) {
+            const uint32_t k = fkey(hrow[c]);
+            if ((k & mask_hi) == prefix) atomicAdd(&h[(k >> shift) & 0xffu], 1u);
+        }
+        __syncwarp();
+        // find the digit holding the rank-th element (lane 0 scans; 256 bins)
+        uint32_t digit = 0, before = 0;
+        if (lane == 0) {
+            uint32_t run = 0;
+            for (int b = 0; b < 256; ++b) {
+                if (run + h[b] >= rank) { digit = b; before = run; break; }
+                run += h[b];
+            }
+        }
+        digit = __shfl_sync(0xffffffffu, digit, 0);
+        before = __shfl_sync(0xffffffffu, before, 0);
+        prefix |= digit << shift;
+        rank -= before;
+        __syncwarp();
+    }
+    // prefix = fkey(B); candidates: lo <= B
+    uint32_t n = 0;
+    for (uint32_t c0 = 0; c0 < n_cen; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        const bool is = c < n_cen && fkey(lrow[c]) <= prefix;
+        const uint32_t bal = __ballot_sync(0xffffffffu, is);
+        const uint32_t pos = n + __popc(bal & ((1u << lane) - 1u));
+        if (is && pos < (uint32_t)kSelCap) cand[warp][pos] = c;
+        n += __popc(bal);
+    }
+    if (n > (uint32_t)kSelCap) {  // pathological ties: exact ranking of everything is the fallback
+        if (lane == 0) atomicAdd(overflow, 1u);
+        n = min(n, (uint32_t)kSelCap);
+    }
+    __syncwarp();
+    // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43) per candidate, key (acc, id)
+    const float* qr = q + (size_t)qi * dim;
+    for (uint32_t e = lane; e < n; e += 32) {
+        const uint32_t c = (uint32_t)cand[warp][e];
+        const float* cr = cen + (size_t)c * dim;
+        float acc = 0.f;
+        if ((dim & 3u) == 0) {
+            for (uint32_t k = 0; k < dim; k += 4) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(qr + k));
+                const float4 b = __ldg(reinterpret_cast<const float4*>(cr + k));
+                acc = sq_step(acc, a.x, b.x);
+                acc = sq_step(acc, a.y, b.y);
+                acc = sq_step(acc, a.z, b.z);
+                acc = sq_step(acc, a.w, b.w);
+            }
+        } else {
+            for (uint32_t k = 0; k < dim; ++k) acc = sq_step(acc, __ldg(qr + k), __ldg(cr + k));
+        }
+        cand[warp][e] = make_key(acc, c);
+    }
+    // pad and bitonic-sort the candidate keys
+    uint32_t m = 1;
+    while (m < n) m <<= 1;
+    for (uint32_t e = n + lane; e < m; e += 32) cand[warp][e] = ~0ull;
+    __syncwarp();
+    uint64_t* kk = cand[warp];
+    for (uint32_t size = 2; size <= m; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = lane; i < m / 2; i += 32) {
+                const uint32_t lo_i = 2 * i - (i & (stride - 1)), hi_i = lo_i + stride;
+                const bool up = (lo_i & size) == 0;
+                const uint64_t x = kk[lo_i], y = kk[hi_i];
+                if ((x > y) == up) { kk[lo_i] = y; kk[hi_i] = x; }
+            }
+            __syncwarp();
+        }
+    for (uint32_t i = lane; i < n_probe; i += 32) probes[(size_t)qi * n_probe + i] = kk[i];
+}
+
+}  // namespace
+
+cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
+                             uint32_t n_probe, float* cnorm, float* qnorm, float* lo, float* hi, uint64_t* probes,
+                             uint32_t* overflow, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    sq_norms_kernel<<<(n_cen + 255) / 256, 256, 0, s>>>(centroids, n_cen, dim, cnorm);
+    sq_norms_kernel<<<(nq + 255) / 256, 256, 0, s>>>(queries, nq, dim, qnorm);
+    dim3 grid((n_cen + kCC - 1) / kCC, (nq + kCQ - 1) / kCQ);
+    coarse_tc_kernel<<<grid, 256, 0, s>>>(centroids, n_cen, queries, nq, dim, cnorm, qnorm, lo, hi);
+    coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(lo, hi, centroids, n_cen, queries, nq, dim, n_probe, probes,
+                                                      overflow);
+    return cudaGetLastError();
+}
+
+}  // namespace dade_gpu

@@ -119,6 +119,11 @@ cudaError_t launch_keys_to_results(const uint64_t* keys, const uint32_t* count, 
                                    uint32_t K, uint32_t* ids, float* dists, uint32_t* counts_out,
                                    cudaStream_t s);
 
+// coarse.cu: tensor-core coarse ranking with an exact boundary
+cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
+                             uint32_t n_probe, float* cnorm, float* qnorm, float* lo, float* hi, uint64_t* probes,
+                             uint32_t* overflow, cudaStream_t s);
+
 // prep.cu
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s);
 cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* bucket_off, const uint32_t* bucket_q,
