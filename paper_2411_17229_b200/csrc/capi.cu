@@ -284,7 +284,7 @@ struct dade_gpu_ctx {
     // profiling
     bool profiling = false;
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
-    cudaEvent_t ef[4] = {nullptr, nullptr, nullptr, nullptr};  // filter launches of the streaming passes
+    cudaEvent_t ef[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // filter launches per pass
     int n_filter_passes = 0;
     double last_scan_ms = 0, last_bytes = 0, last_total_ms = 0, last_filter_ms = 0;
 
@@ -503,7 +503,9 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                            "seed radius");
             ++c->launches;
         }
-        const int n_pass = two_pass ? 2 : 1;
+        // passes: nearest lists' first row piece, their remaining pieces, all other
+        // lists (IVF); or one flat pass. The radius is tightened after each.
+        const int n_pass = two_pass ? 3 : 1;
         for (int pass = 0; pass < n_pass; ++pass) {
             cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
             FilterArgs f{};
@@ -527,9 +529,16 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             f.surv_cap = cap;
             f.counters = a.counters;
             uint32_t grid = a.items ? max_items : a.flat_qchunks * ((a.flat_rows + a.flat_block - 1) / a.flat_block);
+            f.piece_lo = 0;
+            f.piece_hi = 0xffffffffu;
             if (two_pass) {
-                if (pass == 0) f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
-                else f.item_base = g->n_items + 1;          // the rest
+                if (pass < 2) {
+                    f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
+                    f.piece_lo = pass == 0 ? 0u : 1u;
+                    f.piece_hi = pass == 0 ? 1u : 0xffffffffu;
+                } else {
+                    f.item_base = g->n_items + 1;  // the rest
+                }
             }
             // persistent CTAs pull items from a counter: two per SM
             c->item_counter.ensure(4);
@@ -565,7 +574,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             sv.counters = a.counters;
             sv.surv_max = c->surv_max.as<uint32_t>();
             cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
-            if (a.counters && pass < 2)  // survivors / candidates per pass (low words of counters[4 + 2 pass ..])
+            if (a.counters && pass < 2)  // survivors / candidates of passes 0, 1 (low words of counters[4 + 2 pass ..])
                 for (int w = 0; w < 2; ++w)
                     cuda_check(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(a.counters + 4 + 2 * pass + w),
                                                w == 0 ? c->surv_count.p : c->cand_count.p, 4,

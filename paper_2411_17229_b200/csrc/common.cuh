@@ -29,7 +29,7 @@ struct WorkItem {
     uint32_t row_start;
     uint32_t row_count;
     uint32_t bucket_start;
-    uint32_t bucket_count;
+    uint32_t bucket_count;  // low 16 bits: queries; high 16 bits: row-piece index within the list
 };
 
 // Chunk table: chunk c covers dims [c_begin, end[c]); ckpt[c] = checkpoint

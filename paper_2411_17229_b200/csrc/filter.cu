@@ -139,9 +139,11 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
     uint32_t row_start, row_count, qcount;
     if (a.items != nullptr) {
         const WorkItem wi = a.items[item];
+        const uint32_t piece = wi.bucket_count >> 16;
+        if (piece < a.piece_lo || piece >= a.piece_hi) continue;  // another sub-pass's rows
         row_start = wi.row_start;
         row_count = wi.row_count;
-        qcount = wi.bucket_count;
+        qcount = wi.bucket_count & 0xffffu;
         if (tid < (int)qcount) {
             qidx_s[tid] = a.bucket_q[wi.bucket_start + tid];
             slot_s[tid] = a.bucket_slot[wi.bucket_start + tid];

@@ -73,6 +73,7 @@ struct FilterArgs {
     unsigned long long* counters; // [0] dco, [1] dims, [2] bytes
     uint32_t* item_counter;       // persistent scheduling (zeroed before the launch)
     const float* row_norms;       // [rows + 32] first-slice |o|^2 per storage row
+    uint32_t piece_lo, piece_hi;  // only items whose row piece is in [piece_lo, piece_hi)
 };
 size_t filter_smem_bytes(int d0, int c_dense);
 cudaError_t launch_filter(const FilterArgs& a, const CUtensorMap& tmap32, uint32_t grid, cudaStream_t s);

@@ -171,7 +171,7 @@ __global__ void group_items_kernel(const GroupArgs g) {
             w.row_start = start + p * piece;
             w.row_count = min(piece, len - p * piece);
             w.bucket_start = g.bucket_off[e] + t * kQC;
-            w.bucket_count = min((uint32_t)kQC, c - t * kQC);
+            w.bucket_count = min((uint32_t)kQC, c - t * kQC) | (min(p, 0xffffu) << 16);
             g.items[o++] = w;
         }
 }

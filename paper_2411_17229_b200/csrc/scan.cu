@@ -328,7 +328,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
         const WorkItem wi = a.items[item];
         row_start = wi.row_start;
         row_count = wi.row_count;
-        qcount = wi.bucket_count;
+        qcount = wi.bucket_count & 0xffffu;
         if (tid < (int)qcount) {
             qidx_s[tid] = a.bucket_q[wi.bucket_start + tid];
             slot_s[tid] = a.bucket_slot[wi.bucket_start + tid];
