@@ -271,7 +271,7 @@ struct dade_gpu_ctx {
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
     DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter, seed_goff;
-    DevBuf cnorm, qnorm, coarse_lo, coarse_hi, coarse_overflow;
+    DevBuf cnorm, qnorm, coarse_lo, coarse_overflow;  // coarse_lo: p~ per (query, centroid)
     bool coarse_force_exact = false, coarse_tc_used = false;
     int n_sms = 148;
     uint32_t surv_cap_hint = 0;
@@ -338,14 +338,13 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
         c->cnorm.ensure((size_t)c->n_clusters * 4);
         c->qnorm.ensure((size_t)chunk * 4);
         c->coarse_lo.ensure((size_t)chunk * c->n_clusters * 4);
-        c->coarse_hi.ensure((size_t)chunk * c->n_clusters * 4);
         c->coarse_overflow.ensure(4);
         cuda_check(cudaMemsetAsync(c->coarse_overflow.p, 0, 4, s), "memset");
         for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
             const uint32_t m = std::min(chunk, nq - q0);
             cuda_check(launch_coarse_tc(c->centroids.as<float>(), c->n_clusters, d_q + (size_t)q0 * c->dim, m, c->dim,
                                         n_probe, c->cnorm.as<float>(), c->qnorm.as<float>(),
-                                        c->coarse_lo.as<float>(), c->coarse_hi.as<float>(),
+                                        c->coarse_lo.as<float>(),
                                         c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
                                         c->coarse_overflow.as<uint32_t>(), s),
                        "coarse tc");
@@ -400,6 +399,15 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
 }
 
 constexpr uint32_t kFilterItemRows = 1024;  // row piece of a streaming work item
+// Nearest-list items use shorter pieces: those rows keep most pairs (they hold
+// the query's neighbours), and short items spread that work over every SM.
+// Pass 0 takes the pieces covering the first kFilterItemRows rows.
+uint32_t rank0_item_rows() {
+    uint32_t r = 256;
+    if (const char* e = std::getenv("DADE_GPU_R0_ROWS")) r = (uint32_t)std::atoi(e);
+    r = std::max<uint32_t>(32, std::min<uint32_t>(r, kFilterItemRows));
+    return r;
+}
 constexpr uint32_t kSeedRowsDefault = 512;  // rows of the nearest list used by the radius seed
 
 uint32_t seed_rows(uint32_t k) {
@@ -494,7 +502,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         if (seed.on) {
             if (g && g->n_rb >= 1 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->n_lists,
-                                                    nq / 8 + g->n_lists + 1, seed.offsets, rows, a.row_ids, a.dim,
+                                                    nq / kSeedGroup + g->n_lists + 1, seed.offsets, rows, a.row_ids, a.dim,
                                                     d_q, k, seed_rows(k), a.r_global, out_keys, out_count, s),
                            "seed radius (lists)");
             else
@@ -531,11 +539,13 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             uint32_t grid = a.items ? max_items : a.flat_qchunks * ((a.flat_rows + a.flat_block - 1) / a.flat_block);
             f.piece_lo = 0;
             f.piece_hi = 0xffffffffu;
+            if (const char* ts = std::getenv("DADE_GPU_TRACE_SLOW_NS")) f.trace_slow_ns = (uint32_t)std::atoi(ts);
             if (two_pass) {
                 if (pass < 2) {
                     f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
-                    f.piece_lo = pass == 0 ? 0u : 1u;
-                    f.piece_hi = pass == 0 ? 1u : 0xffffffffu;
+                    const uint32_t p0 = std::max<uint32_t>(1, kFilterItemRows / rank0_item_rows());
+                    f.piece_lo = pass == 0 ? 0u : p0;
+                    f.piece_hi = pass == 0 ? p0 : 0xffffffffu;
                 } else {
                     f.item_base = g->n_items + 1;  // the rest
                 }
@@ -566,6 +576,9 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             sv.n_ckpt = ct.n_ckpt;
             for (int i = 0; i < ct.n_ckpt; ++i) sv.cps[i] = (uint16_t)c->cps[i];
             sv.first_ckpt = 1;
+            sv.vec4 = (a.dim % 4 == 0 && d0 % 4 == 0) ? 1u : 0u;
+            for (int i = 0; i < ct.n_ckpt; ++i)
+                if (c->cps[i] % 4 != 0) sv.vec4 = 0;
             sv.cand_q = c->cand_q.as<uint32_t>();
             sv.cand_key = c->cand_key.as<uint64_t>();
             sv.cand_count = c->cand_count.as<uint32_t>();
@@ -639,6 +652,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     const bool use_filter = filter_ok(c, ct, c->dim);
     // the streaming filter splits long lists into row pieces (more, shorter items)
     g.max_item_rows = use_filter ? kFilterItemRows : 0;
+    g.rank0_item_rows = use_filter && nrb > 1 ? rank0_item_rows() : 0;
     const bool seeded = n_probe > 1 && !seed_disabled() && k <= 512;
     if (use_filter && seeded) {  // the seed's rows of every nearest list are final results already
         g.seed_skip = seed_rows(k);
@@ -649,7 +663,8 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     if (use_filter) {
         uint32_t max_len = 0;
         for (uint32_t l = 0; l < c->n_clusters; ++l) max_len = std::max(max_len, c->dev_offsets[l + 1] - c->dev_offsets[l]);
-        max_items *= std::max<uint32_t>(1, (max_len + kFilterItemRows - 1) / kFilterItemRows);
+        const uint32_t piece = g.rank0_item_rows ? g.rank0_item_rows : kFilterItemRows;
+        max_items *= std::max<uint32_t>(1, (max_len + piece - 1) / piece);
     }
     c->g_counts.ensure(ne * 4);
     c->g_cursor.ensure(ne * 4);
@@ -666,6 +681,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     g.bucket_q = c->bucket_q.as<uint32_t>();
     g.bucket_slot = c->bucket_slot.as<uint32_t>();
     g.items = c->items.as<WorkItem>();
+    g.max_items = max_items;
     g.n_items = c->n_items.as<uint32_t>();
     c->seed_goff.ensure(((size_t)c->n_clusters + 1) * 4);
     g.seed_goff = c->seed_goff.as<uint32_t>();

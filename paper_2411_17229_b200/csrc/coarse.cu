@@ -2,8 +2,9 @@
 // boundary: the n_probe nearest centroids by exact fp32 l2_sq, ties by id.
 //
 //   1. coarse_tc_kernel: p~(q, c) = |q|^2 + |c|^2 - 2 q.c over all D dims with
-//      mma.sync TF32 (fp32 bits read as TF32); writes lo = p~ - delta and
-//      hi = p~ + delta, delta = kCoarseDelta (|q|^2 + |c|^2) bounding |p~ - acc|
+//      mma.sync TF32 (fp32 bits read as TF32); writes p~; the select kernel
+//      forms lo = p~ - delta and hi = p~ + delta, delta = kCoarseDelta
+//      (|q|^2 + |c|^2) bounding |p~ - acc|
 //      for the reference's exact sequential fp32 l2_sq `acc` (same derivation
 //      as the scan filter, with D-term accumulation < 1e-4).
 //   2. coarse_select_kernel (warp per query): B = n_probe-th smallest hi (radix
@@ -40,7 +41,7 @@ __device__ __forceinline__ void mma_tf32_c(float (&d)[4], uint32_t a0, uint32_t 
 __global__ void __launch_bounds__(256) coarse_tc_kernel(const float* __restrict__ cen, uint32_t n_cen,
                                                         const float* __restrict__ q, uint32_t nq, uint32_t dim,
                                                         const float* __restrict__ cnorm, const float* __restrict__ qnorm,
-                                                        float* __restrict__ lo_out, float* __restrict__ hi_out) {
+                                                        float* __restrict__ p_out) {
     __shared__ __align__(16) float cs[kCC * kCS];
     __shared__ __align__(16) float qs[kCQ * kCS];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -122,21 +123,26 @@ __global__ void __launch_bounds__(256) coarse_tc_kernel(const float* __restrict_
                     const uint32_t qq = q0 + wn * 32 + nt * 8 + 2 * tq + cq;
                     if (qq >= nq) continue;
                     const float s = cn + qnorm[qq];
-                    const float p = fmaf(-2.f, d[mt][nt][h * 2 + cq], s);
-                    const float dl = kCoarseDelta * s;
-                    lo_out[(size_t)qq * n_cen + c] = p - dl;
-                    hi_out[(size_t)qq * n_cen + c] = p + dl;
+                    p_out[(size_t)qq * n_cen + c] = fmaf(-2.f, d[mt][nt][h * 2 + cq], s);
                 }
         }
 }
 
-__global__ void sq_norms_kernel(const float* __restrict__ rows, uint32_t n, uint32_t dim, float* __restrict__ out) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const float* r = rows + (size_t)i * dim;
-    float a = 0.f;
-    for (uint32_t k = 0; k < dim; ++k) a = fmaf(r[k], r[k], a);
-    out[i] = a;
+// |row|^2 of the centroids then the queries, warp per row (only bounds use them)
+__global__ void __launch_bounds__(256) sq_norms_kernel(const float* __restrict__ a, uint32_t na,
+                                                       const float* __restrict__ b, uint32_t nb, uint32_t dim,
+                                                       float* __restrict__ out_a, float* __restrict__ out_b) {
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= na + nb) return;
+    const float* r = w < na ? a + (size_t)w * dim : b + (size_t)(w - na) * dim;
+    float acc = 0.f;
+    for (uint32_t k = lane; k < dim; k += 32) acc = fmaf(r[k], r[k], acc);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) {
+        if (w < na) out_a[w] = acc;
+        else out_b[w - na] = acc;
+    }
 }
 
 // order-preserving key of a float (any sign)
@@ -148,7 +154,9 @@ __device__ __forceinline__ uint32_t fkey(float x) {
 constexpr int kSelCap = 512;  // exact-candidate list per query
 
 // Warp per query (4 warps per CTA).
-__global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restrict__ lo, const float* __restrict__ hi,
+__global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restrict__ pt,
+                                                            const float* __restrict__ cnorm,
+                                                            const float* __restrict__ qnorm,
                                                             const float* __restrict__ cen, uint32_t n_cen,
                                                             const float* __restrict__ q, uint32_t nq, uint32_t dim,
                                                             uint32_t n_probe, uint64_t* __restrict__ probes,
@@ -158,8 +166,11 @@ __global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restr
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t qi = blockIdx.x * 4 + warp;
     if (qi >= nq) return;
-    const float* hrow = hi + (size_t)qi * n_cen;
-    const float* lrow = lo + (size_t)qi * n_cen;
+    const float* prow = pt + (size_t)qi * n_cen;
+    const float qn = qnorm[qi];
+    // bounds of the exact l2_sq: p~ -/+ kCoarseDelta (|q|^2 + |c|^2)
+    auto hi_of = [&](uint32_t c) { return prow[c] + kCoarseDelta * (cnorm[c] + qn); };
+    auto lo_of = [&](uint32_t c) { return prow[c] - kCoarseDelta * (cnorm[c] + qn); };
     uint32_t* h = hist[warp];
     // radix select: key of the n_probe-th smallest hi (4 passes of 8 bits)
     uint32_t prefix = 0, rank = n_probe;  // rank: 1-based within the current prefix class
@@ -169,21 +180,12 @@ __global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restr
         __syncwarp();
         const uint32_t mask_hi = pass == 0 ? 0u : (0xffffffffu << (32 - 8 * pass));
         for (uint32_t c = lane; c < n_cen; c += 32) {
-            const uint32_t k = fkey(hrow[c]);
+            const uint32_t k = fkey(hi_of(c));
             if ((k & mask_hi) == prefix) atomicAdd(&h[(k >> shift) & 0xffu], 1u);
         }
         __syncwarp();
-        // find the digit holding the rank-th element (lane 0 scans; 256 bins)
-        uint32_t digit = 0, before = 0;
-        if (lane == 0) {
-            uint32_t run = 0;
-            for (int b = 0; b < 256; ++b) {
-                if (run + h[b] >= rank) { digit = b; before = run; break; }
-                run += h[b];
-            }
-        }
-        digit = __shfl_sync(0xffffffffu, digit, 0);
-        before = __shfl_sync(0xffffffffu, before, 0);
+        uint32_t digit, before;
+        warp_hist_find(h, rank, lane, digit, before);
         prefix |= digit << shift;
         rank -= before;
         __syncwarp();
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restr
     uint32_t n = 0;
     for (uint32_t c0 = 0; c0 < n_cen; c0 += 32) {
         const uint32_t c = c0 + lane;
-        const bool is = c < n_cen && fkey(lrow[c]) <= prefix;
+        const bool is = c < n_cen && fkey(lo_of(c)) <= prefix;
         const uint32_t bal = __ballot_sync(0xffffffffu, is);
         const uint32_t pos = n + __popc(bal & ((1u << lane) - 1u));
         if (is && pos < (uint32_t)kSelCap) cand[warp][pos] = c;
@@ -245,15 +247,15 @@ __global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restr
 }  // namespace
 
 cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
-                             uint32_t n_probe, float* cnorm, float* qnorm, float* lo, float* hi, uint64_t* probes,
+                             uint32_t n_probe, float* cnorm, float* qnorm, float* pt, uint64_t* probes,
                              uint32_t* overflow, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
-    sq_norms_kernel<<<(n_cen + 255) / 256, 256, 0, s>>>(centroids, n_cen, dim, cnorm);
-    sq_norms_kernel<<<(nq + 255) / 256, 256, 0, s>>>(queries, nq, dim, qnorm);
+    sq_norms_kernel<<<(unsigned)(((size_t)n_cen + nq + 7) / 8), 256, 0, s>>>(centroids, n_cen, queries, nq, dim,
+                                                                             cnorm, qnorm);
     dim3 grid((n_cen + kCC - 1) / kCC, (nq + kCQ - 1) / kCQ);
-    coarse_tc_kernel<<<grid, 256, 0, s>>>(centroids, n_cen, queries, nq, dim, cnorm, qnorm, lo, hi);
-    coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(lo, hi, centroids, n_cen, queries, nq, dim, n_probe, probes,
-                                                      overflow);
+    coarse_tc_kernel<<<grid, 256, 0, s>>>(centroids, n_cen, queries, nq, dim, cnorm, qnorm, pt);
+    coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe,
+                                                      probes, overflow);
     return cudaGetLastError();
 }
 

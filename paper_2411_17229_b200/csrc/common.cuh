@@ -25,6 +25,9 @@ constexpr uint64_t kEmptyKey = ~0ull;
 // One CTA work item: a contiguous row range of the device storage (one IVF
 // posting list, or one row block of a flat base) against up to kQC queries
 // taken from bucket arrays (query index, output slot).
+// queries per radius-seed CTA (seed_radius_list_kernel; group prefix in group_scan_kernel)
+constexpr int kSeedGroup = 16;
+
 struct WorkItem {
     uint32_t row_start;
     uint32_t row_count;
@@ -87,6 +90,44 @@ __device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float(stati
 __device__ __forceinline__ float prune_threshold(double coeff, float r) {
     const double r2 = __dmul_rn(static_cast<double>(r), static_cast<double>(r));
     return __double2float_rd(__dmul_rn(coeff, r2));
+}
+
+// Radix-select digit search by one warp: hist[256] (shared) counts the
+// elements of the current prefix class by digit; returns the digit holding the
+// rank-th (1-based) element and the count of elements in lower digits.
+__device__ __forceinline__ void warp_hist_find(const uint32_t* hist, uint32_t rank, uint32_t lane, uint32_t& digit,
+                                               uint32_t& before) {
+    uint32_t bins[8], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        bins[j] = hist[lane * 8 + j];
+        sum += bins[j];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= (uint32_t)off) incl += y;
+    }
+    const uint32_t excl = incl - sum;
+    const bool mine = excl < rank && rank <= incl;
+    uint32_t d = 0, b = 0;
+    if (mine) {
+        uint32_t cum = excl;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (cum + bins[j] >= rank) {
+                d = lane * 8 + j;
+                b = cum;
+                break;
+            }
+            cum += bins[j];
+        }
+    }
+    const uint32_t who = __ballot_sync(0xffffffffu, mine);
+    const int src = who ? __ffs(who) - 1 : 0;
+    digit = __shfl_sync(0xffffffffu, d, src);
+    before = __shfl_sync(0xffffffffu, b, src);
 }
 
 __device__ __forceinline__ uint64_t make_key(float dist, uint32_t id) {

@@ -77,6 +77,40 @@ __device__ __forceinline__ void mma_tf32_f(float (&d)[4], uint32_t a0, uint32_t 
 // element (row, k) of a 128B-swizzled [rows][32] fp32 box
 __device__ __forceinline__ int swzf(int row, int k) { return row * kBox + ((((k >> 2) ^ (row & 7))) << 2) + (k & 3); }
 
+// Exact sequential fp32 prefix over the dense dims for G kept pairs per lane
+// (meta = row | query << 8), G independent chains interleaved for ILP; each
+// chain is the reference's accumulation order (proj/src/estimator.cpp:36-44).
+template <int G>
+__device__ __forceinline__ void prefix_chains(const float* box0, int c_dense, uint32_t d0, const float* q_res,
+                                              const uint32_t (&meta)[4], float (&x)[4]) {
+    for (int c = 0; c < c_dense; ++c) {
+        const float* b = box0 + (size_t)c * kFRows * kBox;
+        const float* qq = q_res + (size_t)c * kBox * kQS;
+        const int wc = min(kBox, (int)d0 - c * kBox);
+        const float* qb[G];
+        const float* rb[G];
+        int sw[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const uint32_t row = meta[i] & 0xffu;
+            qb[i] = qq + (meta[i] >> 8);
+            rb[i] = b + row * kBox;
+            sw[i] = (int)(row & 7);
+        }
+#pragma unroll 2
+        for (int k = 0; k < wc; k += 4) {
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const float4 o4 = *reinterpret_cast<const float4*>(rb[i] + ((((k >> 2) ^ sw[i])) << 2));
+                x[i] = sq_step(x[i], o4.x, qb[i][(k + 0) * kQS]);
+                x[i] = sq_step(x[i], o4.y, qb[i][(k + 1) * kQS]);
+                x[i] = sq_step(x[i], o4.z, qb[i][(k + 2) * kQS]);
+                x[i] = sq_step(x[i], o4.w, qb[i][(k + 3) * kQS]);
+            }
+        }
+    }
+}
+
 struct FLayout {
     size_t boxes, q_res, n_q, thr, qidx, slot, list_meta, list_acc, bars, total;
 };
@@ -134,6 +168,9 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
     __syncthreads();
     const uint32_t item = s_item;
     if (item >= end) break;
+    uint64_t t_item0 = 0;
+    if (a.trace_slow_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item0));
+    uint32_t kept_item = 0;
 
     // ---- work item -------------------------------------------------------------
     uint32_t row_start, row_count, qcount;
@@ -291,47 +328,44 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
                 __syncwarp();
                 const uint32_t n = min(tot, (uint32_t)kFList);
                 pruned -= n;
-                for (uint32_t e0 = 0; e0 < n; e0 += 32) {
-                    const uint32_t e = e0 + lane;
-                    bool surv = false;
-                    uint32_t meta = 0;
-                    float x = 0.f;
-                    if (e < n) {
-                        meta = lmeta[e];
-                        const uint32_t row = meta & 0xffu, j = meta >> 8;
-                        for (int c = 0; c < c_dense; ++c) {
-                            const float* b = box(slot, c);
-                            const float* qq = q_res + (size_t)c * kBox * kQS + j;
-                            const int wc = min(kBox, (int)d0 - c * kBox);
-                            for (int k = 0; k < wc; k += 4) {
-                                const float4 o4 = *reinterpret_cast<const float4*>(b + swzf(row, k));
-                                x = sq_step(x, o4.x, qq[(k + 0) * kQS]);
-                                x = sq_step(x, o4.y, qq[(k + 1) * kQS]);
-                                x = sq_step(x, o4.z, qq[(k + 2) * kQS]);
-                                x = sq_step(x, o4.w, qq[(k + 3) * kQS]);
-                            }
-                        }
-                        surv = !(x > thr[j]);
-                        if (!surv) st_dims += d0;
-                    }
+                kept_item += n;
+                // up to 4 kept pairs per lane, their sequential chains interleaved
+                const uint32_t ng = (n + 31) >> 5;
+                uint32_t meta[4];
+                float x[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t e = (uint32_t)i * 32 + lane;
+                    meta[i] = e < n ? lmeta[e] : 0u;
+                }
+                const float* sb = box(slot, 0);
+                if (ng > 2) prefix_chains<4>(sb, c_dense, d0, q_res, meta, x);
+                else if (ng > 1) prefix_chains<2>(sb, c_dense, d0, q_res, meta, x);
+                else prefix_chains<1>(sb, c_dense, d0, q_res, meta, x);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if ((uint32_t)i >= ng) break;
+                    const uint32_t e = (uint32_t)i * 32 + lane;
+                    const uint32_t j = meta[i] >> 8;
+                    const bool surv = e < n && !(x[i] > thr[j]);
+                    if (e < n && !surv) st_dims += d0;
                     const uint32_t bal = __ballot_sync(0xffffffffu, surv);
                     if (bal) {
-                        uint32_t base = 0;
-                        if (lane == 0) base = atomicAdd(a.surv_count, __popc(bal));
-                        base = __shfl_sync(0xffffffffu, base, 0);
+                        uint32_t sbase = 0;
+                        if (lane == 0) sbase = atomicAdd(a.surv_count, __popc(bal));
+                        sbase = __shfl_sync(0xffffffffu, sbase, 0);
                         if (surv) {
-                            const uint32_t p = base + __popc(bal & ((1u << lane) - 1u));
+                            const uint32_t p = sbase + __popc(bal & ((1u << lane) - 1u));
                             if (p < a.surv_cap) {
-                                const uint32_t row = meta & 0xffu, j = meta >> 8;
                                 Survivor v;
                                 v.q = qidx_s[j];
-                                v.row = row_start + tb + row;
-                                v.acc = x;
+                                v.row = row_start + tb + (meta[i] & 0xffu);
+                                v.acc = x[i];
                                 v.slot = slot_s[j];
                                 a.surv[p] = v;
                             }
                         }
-                                        st_surv += __popc(bal);  // every lane adds: divided by 32 at the end
+                        st_surv += __popc(bal);  // every lane adds: divided by 32 at the end
                     }
                 }
                 __syncwarp();
@@ -343,6 +377,13 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
         if (lane == 0 && t + 2 * kFWarps < n_tiles) issue(t + 2 * kFWarps, slot);
     }
     k_base = k_iter;
+    if (a.trace_slow_ns && lane == 0) {
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t_item0 > a.trace_slow_ns)
+            printf("slow item %u warp %d: %llu ns rows %u q %u tiles %u kept %u\n", item, warp,
+                   (unsigned long long)(t1 - t_item0), row_count, qcount, n_tiles, kept_item);
+    }
   }  // items
 
     // ---- counters ----------------------------------------------------------------

@@ -74,6 +74,7 @@ struct FilterArgs {
     uint32_t* item_counter;       // persistent scheduling (zeroed before the launch)
     const float* row_norms;       // [rows + 32] first-slice |o|^2 per storage row
     uint32_t piece_lo, piece_hi;  // only items whose row piece is in [piece_lo, piece_hi)
+    uint32_t trace_slow_ns;       // diagnostic: printf items slower than this (0 = off)
 };
 size_t filter_smem_bytes(int d0, int c_dense);
 cudaError_t launch_filter(const FilterArgs& a, const CUtensorMap& tmap32, uint32_t grid, cudaStream_t s);
@@ -101,6 +102,7 @@ struct SurvArgs {
     uint32_t* q_count;            // per-query candidate counts
     unsigned long long* counters; // [1] dims
     uint32_t* surv_max;           // running max of the survivor count (overflow check)
+    uint32_t vec4;                // dim, d0 and every checkpoint are multiples of 4 (16-byte staging)
 };
 cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cudaStream_t s);
 cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
@@ -122,7 +124,7 @@ cudaError_t launch_keys_to_results(const uint64_t* keys, const uint32_t* count, 
 
 // coarse.cu: tensor-core coarse ranking with an exact boundary
 cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
-                             uint32_t n_probe, float* cnorm, float* qnorm, float* lo, float* hi, uint64_t* probes,
+                             uint32_t n_probe, float* cnorm, float* qnorm, float* pt, uint64_t* probes,
                              uint32_t* overflow, cudaStream_t s);
 
 // prep.cu
@@ -155,8 +157,10 @@ struct GroupArgs {
     uint32_t* bucket_q;             // [nq * n_probe]
     uint32_t* bucket_slot;          // [nq * n_probe]
     WorkItem* items;                // [max_items]
+    size_t max_items;               // capacity of items (upper bound of n_items[0])
     uint32_t* n_items;              // [2]: all items, rank-bucket-0 items
     uint32_t max_item_rows;         // 0: one item per (list, query chunk); else split rows
+    uint32_t rank0_item_rows;       // row piece of rank-bucket-0 entries (0: max_item_rows)
     uint32_t seed_skip, seed_min;   // rank-0 lists of >= seed_min rows skip their first seed_skip rows
     uint32_t* seed_goff;            // nullable [n_lists + 1]: prefix of ceil(rank-0 count / 8)
 };

@@ -76,12 +76,79 @@ __global__ void group_count_kernel(const GroupArgs g) {
     atomicAdd(&g.counts[rank_bucket(g, p) * g.n_lists + list], 1u);
 }
 
+// Shared-memory variants (n_rb * n_lists <= kGroupSmemEntries): a CTA counts a
+// contiguous range of (query, probe) pairs in shared memory and flushes one
+// global atomic per touched entry, so a list probed by most queries costs one
+// atomic per CTA instead of one per query.
+constexpr uint32_t kGroupSmemEntries = 12288;
+constexpr uint32_t kGroupPerThread = 16;  // pairs per thread
+
+__device__ __forceinline__ uint32_t pair_entry(const GroupArgs& g, size_t i) {
+    const uint32_t p = (uint32_t)(i % g.n_probe);
+    const uint32_t list = (uint32_t)g.probes[i];
+    if (list >= g.n_lists || g.list_offsets[list + 1] == g.list_offsets[list]) return 0xffffffffu;
+    return rank_bucket(g, p) * g.n_lists + list;
+}
+
+__global__ void __launch_bounds__(256) group_count_smem_kernel(const GroupArgs g) {
+    extern __shared__ uint32_t gsh[];
+    const uint32_t ne = g.n_rb * g.n_lists;
+    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) gsh[e] = 0;
+    __syncthreads();
+    const size_t n = (size_t)g.nq * g.n_probe;
+    const size_t base = (size_t)blockIdx.x * blockDim.x * kGroupPerThread;
+#pragma unroll 4
+    for (uint32_t j = 0; j < kGroupPerThread; ++j) {
+        const size_t i = base + (size_t)j * blockDim.x + threadIdx.x;
+        if (i < n) {
+            const uint32_t e = pair_entry(g, i);
+            if (e != 0xffffffffu) atomicAdd(&gsh[e], 1u);
+        }
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x)
+        if (gsh[e]) atomicAdd(&g.counts[e], gsh[e]);
+}
+
+__global__ void __launch_bounds__(256) group_scatter_smem_kernel(const GroupArgs g) {
+    extern __shared__ uint32_t gsh[];
+    const uint32_t ne = g.n_rb * g.n_lists;
+    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) gsh[e] = 0;
+    __syncthreads();
+    const size_t n = (size_t)g.nq * g.n_probe;
+    const size_t base = (size_t)blockIdx.x * blockDim.x * kGroupPerThread;
+    uint32_t ent[kGroupPerThread], loc[kGroupPerThread];
+#pragma unroll
+    for (uint32_t j = 0; j < kGroupPerThread; ++j) {
+        const size_t i = base + (size_t)j * blockDim.x + threadIdx.x;
+        ent[j] = i < n ? pair_entry(g, i) : 0xffffffffu;
+        loc[j] = ent[j] != 0xffffffffu ? atomicAdd(&gsh[ent[j]], 1u) : 0u;
+    }
+    __syncthreads();
+    // this CTA's range inside every touched entry
+    for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x)
+        if (gsh[e]) gsh[e] = g.bucket_off[e] + atomicAdd(&g.cursor[e], gsh[e]);
+    __syncthreads();
+#pragma unroll
+    for (uint32_t j = 0; j < kGroupPerThread; ++j) {
+        if (ent[j] == 0xffffffffu) continue;
+        const size_t i = base + (size_t)j * blockDim.x + threadIdx.x;
+        const uint32_t pos = gsh[ent[j]] + loc[j];
+        g.bucket_q[pos] = (uint32_t)(i / g.n_probe);
+        g.bucket_slot[pos] = (uint32_t)(i % g.n_probe);
+    }
+}
+
 // Single-CTA exclusive scans of the bucket sizes and item counts.
 // work items of one (rank bucket, list) entry: query chunks x row pieces
 // Rows [skip, len) of an entry's list still to scan: rank-bucket-0 entries skip
 // the rows the seed already scored exactly (when the seed ran: len >= seed_min).
 __device__ __forceinline__ uint32_t entry_skip(const GroupArgs& g, uint32_t e, uint32_t len) {
     return (g.seed_skip && e < g.n_lists && len >= g.seed_min) ? min(len, g.seed_skip) : 0u;
+}
+
+__device__ __forceinline__ uint32_t entry_piece(const GroupArgs& g, uint32_t e) {
+    return (e < g.n_lists && g.rank0_item_rows) ? g.rank0_item_rows : g.max_item_rows;
 }
 
 __device__ __forceinline__ uint32_t entry_items(const GroupArgs& g, uint32_t e, uint32_t c) {
@@ -91,7 +158,8 @@ __device__ __forceinline__ uint32_t entry_items(const GroupArgs& g, uint32_t e, 
     const uint32_t rem = len - entry_skip(g, e, len);
     if (rem == 0) return 0;
     uint32_t pieces = 1;
-    if (g.max_item_rows) pieces = max(1u, (rem + g.max_item_rows - 1) / g.max_item_rows);
+    const uint32_t pr = entry_piece(g, e);
+    if (pr) pieces = max(1u, (rem + pr - 1) / pr);
     return (c + kQC - 1) / kQC * pieces;
 }
 
@@ -105,7 +173,7 @@ __global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
         const uint32_t c = g.counts[e];
         sb += c;
         si += entry_items(g, e, c);
-        if (e < g.n_lists) sg += (c + 7) / 8;  // seed groups of the nearest-list bucket
+        if (e < g.n_lists) sg += (c + kSeedGroup - 1) / kSeedGroup;  // seed groups of the nearest-list bucket
     }
     s_b[threadIdx.x] = sb;
     s_i[threadIdx.x] = si;
@@ -129,7 +197,7 @@ __global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
         if (g.seed_goff && e < g.n_lists) g.seed_goff[e] = rg;
         rb += c;
         ri += entry_items(g, e, c);
-        if (e < g.n_lists) rg += (c + 7) / 8;
+        if (e < g.n_lists) rg += (c + kSeedGroup - 1) / kSeedGroup;
     }
     if (g.seed_goff && threadIdx.x == 1023) g.seed_goff[g.n_lists] = s_g[1023];
     if (threadIdx.x == 1023) g.n_items[0] = s_i[1023];
@@ -151,29 +219,33 @@ __global__ void group_scatter_kernel(const GroupArgs g) {
     g.bucket_slot[pos] = p;
 }
 
-__global__ void group_items_kernel(const GroupArgs g) {
-    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= g.n_rb * g.n_lists) return;
+// One thread per work item: its entry is the last one whose item offset is <= t.
+__global__ void __launch_bounds__(256) group_items_kernel(const GroupArgs g) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.n_items[0]) return;
+    const uint32_t ne = g.n_rb * g.n_lists;
+    uint32_t lo = 0, hi = ne;  // item_off[lo] <= t < item_off[hi] (item_off[ne] := inf)
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (g.item_off[mid] <= t) lo = mid; else hi = mid;
+    }
+    const uint32_t e = lo;
     const uint32_t c = g.counts[e];
-    if (c == 0) return;
     const uint32_t list = e % g.n_lists;
     const uint32_t len0 = g.list_offsets[list + 1] - g.list_offsets[list];
     const uint32_t skip = entry_skip(g, e, len0);
     const uint32_t start = g.list_offsets[list] + skip, len = len0 - skip;
-    if (len == 0) return;
-    const uint32_t ni = (c + kQC - 1) / kQC;
-    const uint32_t piece = g.max_item_rows ? g.max_item_rows : max(len, 1u);
+    const uint32_t pr = entry_piece(g, e);
+    const uint32_t piece = pr ? pr : max(len, 1u);
     const uint32_t np = max(1u, (len + piece - 1) / piece);
-    uint32_t o = g.item_off[e];
-    for (uint32_t t = 0; t < ni; ++t)
-        for (uint32_t p = 0; p < np; ++p) {
-            WorkItem w;
-            w.row_start = start + p * piece;
-            w.row_count = min(piece, len - p * piece);
-            w.bucket_start = g.bucket_off[e] + t * kQC;
-            w.bucket_count = min((uint32_t)kQC, c - t * kQC) | (min(p, 0xffffu) << 16);
-            g.items[o++] = w;
-        }
+    const uint32_t li = t - g.item_off[e];
+    const uint32_t tq = li / np, p = li - tq * np;  // query chunk major, row piece minor
+    WorkItem w;
+    w.row_start = start + p * piece;
+    w.row_count = min(piece, len - p * piece);
+    w.bucket_start = g.bucket_off[e] + tq * kQC;
+    w.bucket_count = min((uint32_t)kQC, c - tq * kQC) | (min(p, 0xffffu) << 16);
+    g.items[t] = w;
 }
 
 // ---- per-pair DCO: checkpointed_scan (proj/src/estimator.cpp:24-70) ------------
@@ -365,23 +437,165 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
     }
 }
 
-// List-major seed: one CTA per nearest list, for the queries whose nearest
-// list it is (the rank-bucket-0 bucket), 8 queries at a time: the list's first
-// S rows are staged once per 32-dim slice (coalesced, shared by the 8 queries)
-// and every thread advances 2 rows x 8 queries of exact sequential sums; then
-// one warp per query sorts its S keys. Same output as seed_radius_kernel.
-constexpr int kSeedGroup = 8;
-__global__ void __launch_bounds__(kSeedThreads) seed_radius_list_kernel(
+// List-major seed: one CTA per (nearest list, group of up to 8 of the queries
+// whose nearest list it is). The list's first S rows stream through shared
+// memory in 16-dim slices (cp.async, double-buffered, shared by the group);
+// every thread advances rows (t, t + 256) x G queries of exact sequential fp32
+// sums with packed f32x2 arithmetic (two queries per instruction, same
+// rounding as sq_step); then one warp per query sorts its S keys. Same output
+// as seed_radius_kernel. Requires dim % 4 == 0 (the streaming path's rule).
+constexpr int kSeedSlice = 16;                 // dims per staged slice
+constexpr int kSeedRS = kSeedSlice + 4;        // padded row stride (floats): conflict-free LDS.128
+constexpr int kSeedTileF = kSeedMax * kSeedRS; // floats per tile buffer
+
+__device__ __forceinline__ void cp_async16_s(void* dst, const void* src, bool pred) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(pred ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4_s(void* dst, const void* src, bool pred) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(pred ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// exact sums of rows (tid, tid + 256) x G queries over all dims -> accs[u][row]
+template <int G, bool kTwo>
+__device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* accs, const float* storage,
+                                                uint32_t start, uint32_t n, uint32_t dim, const float* queries,
+                                                const uint32_t* qs, uint32_t ng, uint64_t nz2) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t r0 = tid, r1 = tid + kSeedThreads;
+    const uint32_t n_slices = (dim + kSeedSlice - 1) / kSeedSlice;
+    auto issue = [&](uint32_t sl, uint32_t buf) {
+        const uint32_t k0 = sl * kSeedSlice;
+        float* tb = tile + buf * kSeedTileF;
+#pragma unroll
+        for (int i = 0; i < (kSeedMax * kSeedSlice / 4) / kSeedThreads; ++i) {
+            const uint32_t idx = tid + i * kSeedThreads, row = idx >> 2, c4 = idx & 3;
+            if (!kTwo && row >= (uint32_t)kSeedThreads) break;  // rows (t + 256) unused
+            const bool ok = row < n && k0 + 4 * c4 < dim;
+            const float* src = storage + (size_t)(start + (ok ? row : 0)) * dim + (ok ? k0 + 4 * c4 : 0);
+            cp_async16_s(tb + row * kSeedRS + 4 * c4, src, ok);
+        }
+        static_assert(kSeedSlice * kSeedGroup <= kSeedThreads, "one query element per thread");
+        if (tid < (uint32_t)(kSeedSlice * kSeedGroup)) {  // qt[buf][k][u]
+            const uint32_t k = tid / kSeedGroup, u = tid % kSeedGroup;
+            const bool ok = u < ng && k0 + k < dim;
+            const float* src = queries + (ok ? (size_t)qs[u] * dim + k0 + k : 0);
+            cp_async4_s(qt + buf * kSeedSlice * kSeedGroup + k * kSeedGroup + u, src, ok);
+        }
+        cp_async_commit();
+    };
+    uint64_t acc0[G / 2], acc1[G / 2];
+#pragma unroll
+    for (int p = 0; p < G / 2; ++p) acc0[p] = acc1[p] = 0ull;
+    issue(0, 0);
+    for (uint32_t sl = 0; sl < n_slices; ++sl) {
+        const uint32_t buf = sl & 1;
+        if (sl + 1 < n_slices) {
+            issue(sl + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float* tb = tile + buf * kSeedTileF;
+        const float* qb = qt + buf * kSeedSlice * kSeedGroup;
+#pragma unroll
+        for (int c = 0; c < kSeedSlice / 4; ++c) {
+            const float4 x0 = *reinterpret_cast<const float4*>(tb + r0 * kSeedRS + 4 * c);
+            const float4 x1 = kTwo ? *reinterpret_cast<const float4*>(tb + r1 * kSeedRS + 4 * c)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float o0[4] = {x0.x, x0.y, x0.z, x0.w};
+            const float o1[4] = {x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint64_t* q2 = reinterpret_cast<const uint64_t*>(qb + (4 * c + e) * kSeedGroup);
+#pragma unroll
+                for (int p = 0; p < G / 2; ++p) {
+                    const uint64_t qq = q2[p];
+                    acc0[p] = sq_step2(acc0[p], o0[e], qq, nz2);
+                    if (kTwo) acc1[p] = sq_step2(acc1[p], o1[e], qq, nz2);
+                }
+            }
+        }
+        __syncthreads();  // buffer free for the slice after next
+    }
+#pragma unroll
+    for (int p = 0; p < G / 2; ++p) {
+        accs[(2 * p) * kSeedMax + r0] = lo_f(acc0[p]);
+        accs[(2 * p + 1) * kSeedMax + r0] = hi_f(acc0[p]);
+        accs[(2 * p) * kSeedMax + r1] = lo_f(acc1[p]);
+        accs[(2 * p + 1) * kSeedMax + r1] = hi_f(acc1[p]);
+    }
+    __syncthreads();
+}
+
+// ascending bitonic sort of m (power of two) keys in shared memory by one warp
+__device__ __forceinline__ void warp_bitonic_sort(uint64_t* kk, uint32_t m, uint32_t lane) {
+    for (uint32_t size = 2; size <= m; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = lane; i < m / 2; i += 32) {
+                const uint32_t lo = 2 * i - (i & (stride - 1));
+                const uint32_t hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t x = kk[lo], y = kk[hi];
+                if ((x > y) == up) {
+                    kk[lo] = y;
+                    kk[hi] = x;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+constexpr int kSeedSmall = 128;  // sorted slots when the K-th distance has few ties
+
+// K-th smallest (1-based) of the first n sqrt(acc) values as float bits
+// (positive floats order like their bits): warp radix select, 8 bits per
+// pass, histogram in shared memory. Requires K <= n <= kSeedMax.
+__device__ __forceinline__ uint32_t seed_select(const float* acc, uint32_t n, uint32_t K, uint32_t* hist,
+                                                uint32_t lane) {
+    uint32_t v[kSeedMax / 32];
+#pragma unroll
+    for (int i = 0; i < kSeedMax / 32; ++i) {
+        const uint32_t r = lane + 32u * i;
+        v[i] = r < n ? __float_as_uint(__fsqrt_rn(acc[r])) : 0xffffffffu;
+    }
+    uint32_t prefix = 0, mask = 0, rem = K;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (uint32_t j = lane; j < 256; j += 32) hist[j] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < kSeedMax / 32; ++i)
+            if ((v[i] & mask) == prefix) atomicAdd(&hist[(v[i] >> shift) & 0xffu], 1u);
+        __syncwarp();
+        uint32_t d, before;
+        warp_hist_find(hist, rem, lane, d, before);
+        rem -= before;
+        prefix |= d << shift;
+        mask |= 0xffu << shift;
+        __syncwarp();
+    }
+    return prefix;
+}
+
+__global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ bucket_off, const uint32_t* __restrict__ bucket_q,
     const uint32_t* __restrict__ seed_goff, uint32_t n_lists, const uint32_t* __restrict__ list_offsets, const float* __restrict__ storage,
     const uint32_t* __restrict__ row_ids, uint32_t dim, const float* __restrict__ queries, uint32_t K, uint32_t S,
-    uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count) {
+    uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count, uint64_t nz2) {
     extern __shared__ __align__(16) unsigned char seed_smem[];
-    float* qt = reinterpret_cast<float*>(seed_smem);                   // [kSeedGroup][32]
-    float* tile = qt + kSeedGroup * 32;                                // [kSeedMax][36]
+    float* tile = reinterpret_cast<float*>(seed_smem);                  // [2][kSeedMax][kSeedRS]
+    float* qt = tile + 2 * kSeedTileF;                                  // [2][kSeedSlice][kSeedGroup]
     // after the last slice the tile's space is reused: sums, then sort keys
-    float* accs = tile;                                                // [kSeedGroup][kSeedMax]
-    uint64_t* keys = reinterpret_cast<uint64_t*>(tile + kSeedGroup * kSeedMax);  // [8 warps][kSeedMax]
+    float* accs = tile;                                                 // [kSeedGroup][kSeedMax]
+    uint64_t* keys = reinterpret_cast<uint64_t*>(tile + kSeedGroup * kSeedMax);  // [8 warps][kSeedMax], then hist [8][256]
     // CTA -> (list, group): binary search in the per-list group prefix
     const uint32_t b = blockIdx.x;
     if (b >= seed_goff[n_lists]) return;
@@ -392,93 +606,61 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_list_kernel(
     }
     const uint32_t list = lo_l;
     const uint32_t cnt_all = counts[list];  // entry e = list of rank bucket 0
-    const uint32_t gfirst = (b - seed_goff[list]) * kSeedGroup;
-    if (gfirst >= cnt_all) return;
+    const uint32_t g0 = (b - seed_goff[list]) * kSeedGroup;
+    if (g0 >= cnt_all) return;
     const uint32_t start = list_offsets[list], len = list_offsets[list + 1] - start;
     const uint32_t n = min(len, S);
     if (n < K) return;
-    const uint32_t* qs = bucket_q + bucket_off[list];
+    const uint32_t* qs = bucket_q + bucket_off[list] + g0;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t c4 = tid & 7, rb = tid >> 3;
-    const float* rowp = storage + (size_t)(start + min(rb, n - 1)) * dim + 4 * c4;
-    const size_t rstep = (size_t)32 * dim;
-    const uint32_t r0 = tid, r1 = tid + kSeedThreads;
-    const uint32_t cnt = min(cnt_all, gfirst + kSeedGroup);
-    for (uint32_t g0 = gfirst; g0 < cnt; g0 += kSeedGroup) {
-        const uint32_t ng = min((uint32_t)kSeedGroup, cnt - g0);
-        float a0[kSeedGroup], a1[kSeedGroup];
+    const uint32_t ng = min((uint32_t)kSeedGroup, cnt_all - g0);
+    switch ((ng + 1) >> 1) {  // G = ng rounded up to even: no padded query pairs beyond one
+#define SEED_G(P)                                                                                      \
+    case P:                                                                                            \
+        if (n > (uint32_t)kSeedThreads)                                                                \
+            seed_group_sums<2 * P, true>(tile, qt, accs, storage, start, n, dim, queries, qs, ng, nz2); \
+        else                                                                                           \
+            seed_group_sums<2 * P, false>(tile, qt, accs, storage, start, n, dim, queries, qs, ng, nz2); \
+        break;
+        SEED_G(1) SEED_G(2) SEED_G(3) SEED_G(4) SEED_G(5) SEED_G(6) SEED_G(7) default: SEED_G(8)
+#undef SEED_G
+    }
+    for (uint32_t u = warp; u < ng; u += kSeedThreads / 32) {  // one warp per query: K-th distance, sorted top-K keys
+        const uint32_t q = qs[u];
+        uint64_t* kk = keys + warp * kSeedMax;
+        uint32_t* hist = reinterpret_cast<uint32_t*>(keys + (kSeedThreads / 32) * kSeedMax) + warp * 256;
+        const float* acc = accs + u * kSeedMax;
+        const uint32_t T = seed_select(acc, n, K, hist, lane);
+        // keys of the rows with dist <= T (>= K of them): usually few, sorted
+        // in a 128-slot bitonic; a tie-heavy list falls back to all S rows
+        uint32_t c = 0;
 #pragma unroll
-        for (int u = 0; u < kSeedGroup; ++u) a0[u] = a1[u] = 0.f;
-        for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
-            const uint32_t w = min(32u, dim - k0), w4 = w >> 2;
-            __syncthreads();
-            float4 v[16];
-#pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                const uint32_t r = rb + 32 * m;
-                v[m] = (r < n && c4 < w4) ? __ldg(reinterpret_cast<const float4*>(rowp + m * rstep + k0))
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int m = 0; m < 16; ++m) *reinterpret_cast<float4*>(tile + (rb + 32 * m) * 36 + 4 * c4) = v[m];
-            if (tid < kSeedGroup * 32) {
-                const uint32_t u = tid >> 5, k = tid & 31;
-                qt[tid] = (u < ng && k < w) ? __ldg(queries + (size_t)qs[g0 + u] * dim + k0 + k) : 0.f;
-            }
-            __syncthreads();
-            for (uint32_t cc = 0; cc < w4; ++cc) {
-                const float4 x0 = *reinterpret_cast<const float4*>(tile + r0 * 36 + 4 * cc);
-                const float4 x1 = *reinterpret_cast<const float4*>(tile + r1 * 36 + 4 * cc);
-#pragma unroll
-                for (int u = 0; u < kSeedGroup; ++u) {
-                    const float4 y = *reinterpret_cast<const float4*>(qt + u * 32 + 4 * cc);
-                    a0[u] = sq_step(a0[u], x0.x, y.x); a1[u] = sq_step(a1[u], x1.x, y.x);
-                    a0[u] = sq_step(a0[u], x0.y, y.y); a1[u] = sq_step(a1[u], x1.y, y.y);
-                    a0[u] = sq_step(a0[u], x0.z, y.z); a1[u] = sq_step(a1[u], x1.z, y.z);
-                    a0[u] = sq_step(a0[u], x0.w, y.w); a1[u] = sq_step(a1[u], x1.w, y.w);
-                }
-            }
+        for (int i = 0; i < kSeedMax / 32; ++i) {
+            const uint32_t r = lane + 32u * i;
+            const float dv = r < n ? __fsqrt_rn(acc[r]) : 0.f;
+            const bool take = r < n && __float_as_uint(dv) <= T;
+            const uint32_t bal = __ballot_sync(0xffffffffu, take);
+            const uint32_t pos = c + __popc(bal & ((1u << lane) - 1u));
+            if (take && pos < (uint32_t)kSeedSmall)
+                kk[pos] = make_key(dv, row_ids ? __ldg(row_ids + start + r) : start + r);
+            c += __popc(bal);
         }
-        __syncthreads();  // everyone done reading the last slice
-#pragma unroll
-        for (int u = 0; u < kSeedGroup; ++u) {
-            accs[u * kSeedMax + r0] = a0[u];
-            accs[u * kSeedMax + r1] = a1[u];
+        uint32_t m = kSeedSmall;
+        if (c > (uint32_t)kSeedSmall) {
+            m = kSeedMax;
+            for (uint32_t r = lane; r < (uint32_t)kSeedMax; r += 32)
+                kk[r] = r < n ? make_key(__fsqrt_rn(acc[r]), row_ids ? __ldg(row_ids + start + r) : start + r) : ~0ull;
+        } else {
+            for (uint32_t r = c + lane; r < (uint32_t)kSeedSmall; r += 32) kk[r] = ~0ull;
         }
-        __syncthreads();
-        if (warp < ng) {  // one warp per query: keys, bitonic sort, outputs
-            const uint32_t q = qs[g0 + warp];
-            uint64_t* kk = keys + warp * kSeedMax;
-            for (uint32_t r = lane; r < (uint32_t)kSeedMax; r += 32) {
-                uint64_t key = ~0ull;
-                if (r < n) {
-                    const uint32_t id = row_ids ? __ldg(row_ids + start + r) : start + r;
-                    key = make_key(__fsqrt_rn(accs[warp * kSeedMax + r]), id);
-                }
-                kk[r] = key;
-            }
-            __syncwarp();
-            for (uint32_t size = 2; size <= (uint32_t)kSeedMax; size <<= 1) {
-                for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (uint32_t i = lane; i < (uint32_t)kSeedMax / 2; i += 32) {
-                        const uint32_t lo = 2 * i - (i & (stride - 1));
-                        const uint32_t hi = lo + stride;
-                        const bool up = (lo & size) == 0;
-                        const uint64_t x = kk[lo], y = kk[hi];
-                        if ((x > y) == up) {
-                            kk[lo] = y;
-                            kk[hi] = x;
-                        }
-                    }
-                    __syncwarp();
-                }
-            }
-            if (lane == 0) atomicMin(r_global + q, (uint32_t)(kk[K - 1] >> 32));
-            if (out_keys) {
-                for (uint32_t i = lane; i < K; i += 32) out_keys[(size_t)q * K + i] = kk[i];
-                if (lane == 0) out_count[q] = K;
-            }
+        __syncwarp();
+        warp_bitonic_sort(kk, m, lane);
+        if (lane == 0) atomicMin(r_global + q, (uint32_t)(kk[K - 1] >> 32));
+        if (out_keys) {
+            for (uint32_t i = lane; i < K; i += 32) out_keys[(size_t)q * K + i] = kk[i];
+            if (lane == 0) out_count[q] = K;
         }
+        __syncwarp();  // kk / hist reused by this warp's next query
     }
 }
 
@@ -508,13 +690,17 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
                                      uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
                                      cudaStream_t s) {
     if (n_lists == 0 || K > (uint32_t)kSeedMax) return cudaSuccess;
-    const size_t smem = sizeof(float) * (kSeedMax * 36 + kSeedGroup * 32);  // sums + keys alias the tile
+    // double-buffered tile + query slices; sums [8][S] and keys [8][S] alias the tile
+    const size_t smem = sizeof(float) * (2 * kSeedTileF + 2 * kSeedSlice * kSeedGroup);
+    static_assert(sizeof(float) * 2 * kSeedTileF >=
+                      sizeof(float) * kSeedGroup * kSeedMax + (sizeof(uint64_t) * kSeedMax + sizeof(uint32_t) * 256) * (kSeedThreads / 32),
+                  "seed sums + keys + histograms must fit in the tile");
     DADE_CUDA_TRY(cudaFuncSetAttribute(seed_radius_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     seed_radius_list_kernel<<<max_groups, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, seed_goff, n_lists,
                                                                     list_offsets,
                                                                  storage, row_ids, dim, queries, K,
                                                                  std::min<uint32_t>(S, kSeedMax), r_global, out_keys,
-                                                                 out_count);
+                                                                 out_count, 0x8000000080000000ull);
     return cudaGetLastError();
 }
 
@@ -538,10 +724,23 @@ cudaError_t launch_group(const GroupArgs& g, cudaStream_t s) {
     DADE_CUDA_TRY(cudaMemsetAsync(g.counts, 0, sizeof(uint32_t) * ne, s));
     DADE_CUDA_TRY(cudaMemsetAsync(g.cursor, 0, sizeof(uint32_t) * ne, s));
     const unsigned gp = (unsigned)((pairs + 255) / 256);
-    if (pairs) group_count_kernel<<<gp, 256, 0, s>>>(g);
+    const bool smem = ne <= kGroupSmemEntries;
+    const unsigned gs = (unsigned)((pairs + 256 * kGroupPerThread - 1) / (256 * kGroupPerThread));
+    const size_t sh = sizeof(uint32_t) * ne;
+    if (smem && sh > 48 * 1024) {
+        DADE_CUDA_TRY(cudaFuncSetAttribute(group_count_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        DADE_CUDA_TRY(cudaFuncSetAttribute(group_scatter_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+    }
+    if (pairs) {
+        if (smem) group_count_smem_kernel<<<gs, 256, sh, s>>>(g);
+        else group_count_kernel<<<gp, 256, 0, s>>>(g);
+    }
     group_scan_kernel<<<1, 1024, 0, s>>>(g);
-    if (pairs) group_scatter_kernel<<<gp, 256, 0, s>>>(g);
-    group_items_kernel<<<(ne + 255) / 256, 256, 0, s>>>(g);
+    if (pairs) {
+        if (smem) group_scatter_smem_kernel<<<gs, 256, sh, s>>>(g);
+        else group_scatter_kernel<<<gp, 256, 0, s>>>(g);
+    }
+    if (g.max_items) group_items_kernel<<<(unsigned)((g.max_items + 255) / 256), 256, 0, s>>>(g);
     return cudaGetLastError();
 }
 

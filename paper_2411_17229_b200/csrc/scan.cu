@@ -870,97 +870,139 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
 }
 
 // ---- stage 2 of the streaming scan: first-checkpoint survivors ------------------
-// One thread per survivor: continue the exact accumulation from d0 through the
-// remaining checkpoints straight from L2/HBM (checkpointed_scan,
-// proj/src/estimator.cpp:39-70) against the query's radius; exact full-D
-// distances <= r become (query, key) candidates.
-__global__ void __launch_bounds__(256) advance_survivors_kernel(const SurvArgs a) {
+// Continue each survivor's exact accumulation from d0 through the remaining
+// checkpoints (checkpointed_scan, proj/src/estimator.cpp:39-70) against its
+// query's radius; exact full-D distances <= r become (query, key) candidates.
+// A warp takes 32 survivors (lane = survivor) and walks the dims in chunks of
+// <= 32: the live survivors' row and query chunks are staged in shared memory
+// with coalesced loads (8 lanes per 128-byte row chunk), then every lane
+// advances its own sequential sum from shared memory. (A thread reading its
+// own row from global would touch 32 lines per warp load.)
+constexpr int kSvStride = 36;  // floats per staged row: 16-byte aligned, conflict-free LDS.128
+constexpr int kSvWarps = 8;
+
+__global__ void __launch_bounds__(kSvWarps * 32, 2) advance_survivors_kernel(const SurvArgs a) {
+    extern __shared__ __align__(16) float sv_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* o_s = sv_smem + (size_t)warp * 2 * 32 * kSvStride;
+    float* q_s = o_s + 32 * kSvStride;
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.surv_max) atomicMax(a.surv_max, *a.surv_count);
     const uint32_t n = min(*a.surv_count, a.surv_cap);
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += stride) {  // warp-uniform grid-stride loop
-    const uint32_t i = i0 + threadIdx.x;
-    bool is_cand = false;
-    uint32_t q = 0;
-    uint64_t key = 0;
-    unsigned long long dims = 0;
-    if (i < n) {
-        const Survivor v = a.surv[i];
-        if (v.q != 0xffffffffu) {
-            q = v.q;
-            const float r = __uint_as_float(a.r_global[q]);
-            const float* orow = a.storage + (size_t)v.row * a.dim;
-            const float* qrow = a.queries + (size_t)q * a.dim;
-            float x = v.acc;
-            uint32_t lo = a.n_dense_dims;
-            bool live = true;
-            const bool vec = ((a.dim | lo) & 3u) == 0;
-            for (uint32_t ci = a.first_ckpt; ci <= a.n_ckpt; ++ci) {
-                const uint32_t hi = ci < a.n_ckpt ? a.cps[ci] : a.dim;
-                if (vec && ((hi - lo) & 3u) == 0) {
-                    uint32_t k = lo;
-                    for (; k + 32 <= hi; k += 32) {  // 8 float4 pairs in flight per round trip
-                        float4 o8[8], q8[8];
+    const uint32_t n_groups = (n + 31) / 32;
+    const uint32_t dim = a.dim;
+    for (uint32_t grp = blockIdx.x * kSvWarps + warp; grp < n_groups; grp += gridDim.x * kSvWarps) {
+        const uint32_t i = grp * 32 + lane;
+        bool live = false;
+        uint32_t q = 0, row = 0;
+        float x = 0.f, r = 0.f;
+        if (i < n) {
+            const Survivor v = a.surv[i];
+            if (v.q != 0xffffffffu) {
+                live = true;
+                q = v.q;
+                row = v.row;
+                x = v.acc;
+                r = __uint_as_float(a.r_global[q]);
+            }
+        }
+        unsigned long long dims = 0;
+        uint32_t lo = a.n_dense_dims;
+        for (uint32_t ci = a.first_ckpt; ci <= a.n_ckpt; ++ci) {
+            const uint32_t act0 = __ballot_sync(0xffffffffu, live);
+            if (!act0) break;
+            const uint32_t hi = ci < a.n_ckpt ? a.cps[ci] : dim;
+            for (uint32_t k0 = lo; k0 < hi; k0 += 32) {
+                const uint32_t w = min(32u, hi - k0);
+                if (a.vec4 && (w & 3u) == 0) {
+                    // 4 survivors per pass: lane = (survivor sub 0..3, 16-byte column 0..7)
+                    const uint32_t sub = lane >> 3, c4 = lane & 7;
+                    // all loads in flight before the first store: one memory latency per chunk
+                    float4 ov[8], qv[8];
+                    bool okv[8];
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            o8[u] = __ldg(reinterpret_cast<const float4*>(orow + k) + u);
-                            q8[u] = __ldg(reinterpret_cast<const float4*>(qrow + k) + u);
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            x = sq_step(x, o8[u].x, q8[u].x);
-                            x = sq_step(x, o8[u].y, q8[u].y);
-                            x = sq_step(x, o8[u].z, q8[u].z);
-                            x = sq_step(x, o8[u].w, q8[u].w);
+                    for (uint32_t sg = 0; sg < 8; ++sg) {
+                        const uint32_t sidx = 4 * sg + sub;
+                        const uint32_t srow = __shfl_sync(0xffffffffu, row, sidx);
+                        const uint32_t sq = __shfl_sync(0xffffffffu, q, sidx);
+                        okv[sg] = ((act0 >> sidx) & 1u) && 4 * c4 < w;
+                        if (okv[sg]) {
+                            ov[sg] = __ldg(reinterpret_cast<const float4*>(a.storage + (size_t)srow * dim + k0) + c4);
+                            qv[sg] = __ldg(reinterpret_cast<const float4*>(a.queries + (size_t)sq * dim + k0) + c4);
                         }
                     }
-                    for (; k < hi; k += 4) {
-                        const float4 o4 = __ldg(reinterpret_cast<const float4*>(orow + k));
-                        const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + k));
-                        x = sq_step(x, o4.x, q4.x);
-                        x = sq_step(x, o4.y, q4.y);
-                        x = sq_step(x, o4.z, q4.z);
-                        x = sq_step(x, o4.w, q4.w);
+#pragma unroll
+                    for (uint32_t sg = 0; sg < 8; ++sg) {
+                        const uint32_t sidx = 4 * sg + sub;
+                        if (okv[sg]) {
+                            *reinterpret_cast<float4*>(o_s + sidx * kSvStride + 4 * c4) = ov[sg];
+                            *reinterpret_cast<float4*>(q_s + sidx * kSvStride + 4 * c4) = qv[sg];
+                        }
+                    }
+                    __syncwarp();
+                    if (live) {
+                        const float* os = o_s + lane * kSvStride;
+                        const float* qs = q_s + lane * kSvStride;
+                        for (uint32_t k = 0; k < w; k += 4) {
+                            const float4 o4 = *reinterpret_cast<const float4*>(os + k);
+                            const float4 q4 = *reinterpret_cast<const float4*>(qs + k);
+                            x = sq_step(x, o4.x, q4.x);
+                            x = sq_step(x, o4.y, q4.y);
+                            x = sq_step(x, o4.z, q4.z);
+                            x = sq_step(x, o4.w, q4.w);
+                        }
                     }
                 } else {
-                    for (uint32_t k = lo; k < hi; ++k) x = sq_step(x, __ldg(orow + k), __ldg(qrow + k));
+                    // any alignment: one survivor per pass, lane = dim
+                    for (uint32_t m = act0; m; m &= m - 1) {
+                        const uint32_t sidx = __ffs(m) - 1;
+                        const uint32_t srow = __shfl_sync(0xffffffffu, row, sidx);
+                        const uint32_t sq = __shfl_sync(0xffffffffu, q, sidx);
+                        if ((uint32_t)lane < w) {
+                            o_s[sidx * kSvStride + lane] = __ldg(a.storage + (size_t)srow * dim + k0 + lane);
+                            q_s[sidx * kSvStride + lane] = __ldg(a.queries + (size_t)sq * dim + k0 + lane);
+                        }
+                    }
+                    __syncwarp();
+                    if (live)
+                        for (uint32_t k = 0; k < w; ++k)
+                            x = sq_step(x, o_s[lane * kSvStride + k], q_s[lane * kSvStride + k]);
                 }
-                lo = hi;
-                if (ci < a.n_ckpt && x > prune_threshold(a.coeff[ci], r)) {
-                    dims += hi;
-                    live = false;
-                    break;
-                }
+                __syncwarp();  // staging buffers free for the next chunk
             }
-            if (live) {
-                dims += a.dim;
-                const float key_d = __fsqrt_rn(x);
-                if (!(key_d > r)) {
-                    is_cand = true;
-                    const uint32_t id = a.row_ids ? __ldg(a.row_ids + v.row) : a.id_base + v.row;
-                    key = make_key(key_d, id);
+            lo = hi;
+            if (live && ci < a.n_ckpt && x > prune_threshold(a.coeff[ci], r)) {
+                dims += hi;
+                live = false;
+            }
+        }
+        bool is_cand = false;
+        uint64_t key = 0;
+        if (live) {
+            dims += dim;
+            const float key_d = __fsqrt_rn(x);
+            if (!(key_d > r)) {
+                is_cand = true;
+                const uint32_t id = a.row_ids ? __ldg(a.row_ids + row) : a.id_base + row;
+                key = make_key(key_d, id);
+            }
+        }
+        // warp-aggregated candidate append
+        const uint32_t bal = __ballot_sync(0xffffffffu, is_cand);
+        if (bal) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(a.cand_count, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (is_cand) {
+                const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
+                if (pos < a.cand_cap) {
+                    a.cand_q[pos] = q;
+                    a.cand_key[pos] = key;
+                    atomicAdd(a.q_count + q, 1u);
                 }
             }
         }
-    }
-    // warp-aggregated candidate append
-    const uint32_t bal = __ballot_sync(0xffffffffu, is_cand);
-    const int lane = threadIdx.x & 31;
-    uint32_t base = 0;
-    if (bal) {
-        if (lane == 0) base = atomicAdd(a.cand_count, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (is_cand) {
-            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
-            if (pos < a.cand_cap) {
-                a.cand_q[pos] = q;
-                a.cand_key[pos] = key;
-                atomicAdd(a.q_count + q, 1u);
-            }
-        }
-    }
-    for (int off = 16; off > 0; off >>= 1) dims += __shfl_xor_sync(0xffffffffu, dims, off);
-    if (lane == 0 && a.counters && dims) atomicAdd(a.counters + 1, dims);
+        for (int off = 16; off > 0; off >>= 1) dims += __shfl_xor_sync(0xffffffffu, dims, off);
+        if (lane == 0 && a.counters && dims) atomicAdd(a.counters + 1, dims);
     }
 }
 
@@ -1134,7 +1176,14 @@ cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorM
 
 cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cudaStream_t s) {
     if (max_entries == 0) return cudaSuccess;
-    advance_survivors_kernel<<<std::min<uint32_t>((max_entries + 255) / 256, 148 * 16), 256, 0, s>>>(a);
+    const size_t smem = sizeof(float) * kSvWarps * 2 * 32 * kSvStride;
+    DADE_CUDA_TRY(cudaFuncSetAttribute(advance_survivors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t groups = (max_entries + 31) / 32;
+    const uint32_t grid = std::min<uint32_t>((groups + kSvWarps - 1) / kSvWarps, (uint32_t)sms * 3);
+    advance_survivors_kernel<<<grid, kSvWarps * 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 

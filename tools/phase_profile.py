@@ -26,6 +26,7 @@ for it in range(3):
                                               _capi.QUERIES_RAW | _capi.DEVICE_PTRS, _capi.ptr(oi), _capi.ptr(od),
                                               _capi.ptr(oc), ctypes.byref(st)))
     scan_ms, scan_bytes, total_ms = dev.last_scan_profile()
+    filt_ms, n_filt = dev.last_filter_profile()
     buf = np.zeros(16, np.uint64)
     _capi.check(_capi.lib.dade_gpu_debug_counters(dev.h, _capi.ptr(buf)))
     ph = buf[8:13].astype(np.float64)
@@ -38,6 +39,7 @@ for it in range(3):
     names = ["wait+barrier", "dense", "epilogue", "survivors", "merges"]
     tot = ph.sum()
     print(f"scan {scan_ms:.3f} ms total {total_ms:.3f} ms dco {st.total_dco} dims {st.dims_accumulated} "
-          f"frac {st.dims_accumulated / max(1, st.total_dco) / cfg.dim:.4f}")
+          f"frac {st.dims_accumulated / max(1, st.total_dco) / cfg.dim:.4f} "
+          f"filter {filt_ms:.3f} ms / {n_filt}")
     if tot:
         print("  " + "  ".join(f"{n} {100 * v / tot:.1f}%" for n, v in zip(names, ph)))
