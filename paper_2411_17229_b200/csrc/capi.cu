@@ -399,11 +399,12 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
 }
 
 constexpr uint32_t kFilterItemRows = 1024;  // row piece of a streaming work item
+constexpr uint32_t kFilterQ = 32;           // queries per streaming work item (one warp's MMA N)
 // Nearest-list items use shorter pieces: those rows keep most pairs (they hold
 // the query's neighbours), and short items spread that work over every SM.
 // Pass 0 takes the pieces covering the first kFilterItemRows rows.
 uint32_t rank0_item_rows() {
-    uint32_t r = 256;
+    uint32_t r = 32;  // one tile: a nearest list's heavy rows spread over every warp
     if (const char* e = std::getenv("DADE_GPU_R0_ROWS")) r = (uint32_t)std::atoi(e);
     r = std::max<uint32_t>(32, std::min<uint32_t>(r, kFilterItemRows));
     return r;
@@ -419,6 +420,13 @@ uint32_t seed_rows(uint32_t k) {
 bool seed_disabled() {
     const char* e = std::getenv("DADE_GPU_NO_SEED");
     return e && e[0] == '1';
+}
+
+// the phase buffer without resetting it (nullptr unless DADE_GPU_PHASES=1)
+unsigned long long* phase_ptr_keep(dade_gpu_ctx* c) {
+    const char* e = std::getenv("DADE_GPU_PHASES");
+    if (!(e && e[0] == '1') || !c->phase.p) return nullptr;
+    return c->phase.as<unsigned long long>();
 }
 
 unsigned long long* phase_ptr(dade_gpu_ctx* c) {
@@ -539,7 +547,8 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             uint32_t grid = a.items ? max_items : a.flat_qchunks * ((a.flat_rows + a.flat_block - 1) / a.flat_block);
             f.piece_lo = 0;
             f.piece_hi = 0xffffffffu;
-            if (const char* ts = std::getenv("DADE_GPU_TRACE_SLOW_NS")) f.trace_slow_ns = (uint32_t)std::atoi(ts);
+            f.debug = ct.debug;
+            if (unsigned long long* ph = phase_ptr_keep(c)) f.census = ph + 2 * pass;  // DADE_GPU_PHASES=1
             if (two_pass) {
                 if (pass < 2) {
                     f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
@@ -653,13 +662,14 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     // the streaming filter splits long lists into row pieces (more, shorter items)
     g.max_item_rows = use_filter ? kFilterItemRows : 0;
     g.rank0_item_rows = use_filter && nrb > 1 ? rank0_item_rows() : 0;
+    g.q_chunk = use_filter ? kFilterQ : (uint32_t)kQC;
     const bool seeded = n_probe > 1 && !seed_disabled() && k <= 512;
     if (use_filter && seeded) {  // the seed's rows of every nearest list are final results already
         g.seed_skip = seed_rows(k);
         g.seed_min = k;
     }
     const size_t ne = (size_t)nrb * c->n_clusters;
-    size_t max_items = ((size_t)nq * n_probe + kQC - 1) / kQC + ne;
+    size_t max_items = ((size_t)nq * n_probe + g.q_chunk - 1) / g.q_chunk + ne;
     if (use_filter) {
         uint32_t max_len = 0;
         for (uint32_t l = 0; l < c->n_clusters; ++l) max_len = std::max(max_len, c->dev_offsets[l + 1] - c->dev_offsets[l]);

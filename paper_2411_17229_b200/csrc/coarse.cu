@@ -212,7 +212,23 @@ __global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restr
         const float* cr = cen + (size_t)c * dim;
         float acc = 0.f;
         if ((dim & 3u) == 0) {
-            for (uint32_t k = 0; k < dim; k += 4) {
+            uint32_t k = 0;
+            for (; k + 32 <= dim; k += 32) {  // 8 float4 pairs in flight per round trip
+                float4 a8[8], b8[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    a8[u] = __ldg(reinterpret_cast<const float4*>(qr + k) + u);
+                    b8[u] = __ldg(reinterpret_cast<const float4*>(cr + k) + u);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    acc = sq_step(acc, a8[u].x, b8[u].x);
+                    acc = sq_step(acc, a8[u].y, b8[u].y);
+                    acc = sq_step(acc, a8[u].z, b8[u].z);
+                    acc = sq_step(acc, a8[u].w, b8[u].w);
+                }
+            }
+            for (; k < dim; k += 4) {
                 const float4 a = __ldg(reinterpret_cast<const float4*>(qr + k));
                 const float4 b = __ldg(reinterpret_cast<const float4*>(cr + k));
                 acc = sq_step(acc, a.x, b.x);

@@ -74,7 +74,8 @@ struct FilterArgs {
     uint32_t* item_counter;       // persistent scheduling (zeroed before the launch)
     const float* row_norms;       // [rows + 32] first-slice |o|^2 per storage row
     uint32_t piece_lo, piece_hi;  // only items whose row piece is in [piece_lo, piece_hi)
-    uint32_t trace_slow_ns;       // diagnostic: printf items slower than this (0 = off)
+    int debug;                    // 1: re-check every filter prune exactly (counters[3] = violations)
+    unsigned long long* census;   // nullable: [0] tiles with kept pairs | tiles << 32, [1] kept pairs (diagnostic)
 };
 size_t filter_smem_bytes(int d0, int c_dense);
 cudaError_t launch_filter(const FilterArgs& a, const CUtensorMap& tmap32, uint32_t grid, cudaStream_t s);
@@ -161,6 +162,7 @@ struct GroupArgs {
     uint32_t* n_items;              // [2]: all items, rank-bucket-0 items
     uint32_t max_item_rows;         // 0: one item per (list, query chunk); else split rows
     uint32_t rank0_item_rows;       // row piece of rank-bucket-0 entries (0: max_item_rows)
+    uint32_t q_chunk;               // queries per work item (kQC; 32 for the streaming filter)
     uint32_t seed_skip, seed_min;   // rank-0 lists of >= seed_min rows skip their first seed_skip rows
     uint32_t* seed_goff;            // nullable [n_lists + 1]: prefix of ceil(rank-0 count / 8)
 };

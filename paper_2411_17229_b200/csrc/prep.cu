@@ -160,7 +160,7 @@ __device__ __forceinline__ uint32_t entry_items(const GroupArgs& g, uint32_t e, 
     uint32_t pieces = 1;
     const uint32_t pr = entry_piece(g, e);
     if (pr) pieces = max(1u, (rem + pr - 1) / pr);
-    return (c + kQC - 1) / kQC * pieces;
+    return (c + g.q_chunk - 1) / g.q_chunk * pieces;
 }
 
 __global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(256) group_items_kernel(const GroupArgs g) {
     WorkItem w;
     w.row_start = start + p * piece;
     w.row_count = min(piece, len - p * piece);
-    w.bucket_start = g.bucket_off[e] + tq * kQC;
-    w.bucket_count = min((uint32_t)kQC, c - tq * kQC) | (min(p, 0xffffu) << 16);
+    w.bucket_start = g.bucket_off[e] + tq * g.q_chunk;
+    w.bucket_count = min(g.q_chunk, c - tq * g.q_chunk) | (min(p, 0xffffu) << 16);
     g.items[t] = w;
 }
 

@@ -1,13 +1,15 @@
-"""Top SASS lines by warp-stall samples of one kernel in an .ncu-rep (diagnostic).
-    python tools/ncu_top.py report.ncu-rep [kernel-regex] [n]"""
+"""Top SASS lines by warp-stall samples of one kernel launch in an .ncu-rep (diagnostic).
+    python tools/ncu_top.py report.ncu-rep [kernel-regex] [n] [launch-skip]"""
 import csv, io, subprocess, sys
 
 rep = sys.argv[1]
-kern = sys.argv[2] if len(sys.argv) > 2 else None
+kern = sys.argv[2] if len(sys.argv) > 2 else ""
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--launch-count", "1"]
+skip = sys.argv[4] if len(sys.argv) > 4 else "0"
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--launch-skip", skip,
+       "--launch-count", "1"]
 if kern:
-    cmd += ["-k", "regex:" + kern]
+    cmd += ["--kernel-name", "regex:" + kern]
 out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]

@@ -41,5 +41,9 @@ for it in range(3):
     print(f"scan {scan_ms:.3f} ms total {total_ms:.3f} ms dco {st.total_dco} dims {st.dims_accumulated} "
           f"frac {st.dims_accumulated / max(1, st.total_dco) / cfg.dim:.4f} "
           f"filter {filt_ms:.3f} ms / {n_filt}")
-    if tot:
+    if os.environ.get("DADE_GPU_PHASES") == "1":
+        for p in range(3):
+            a, b = int(buf[8 + 2 * p]), int(buf[9 + 2 * p])
+            print(f"  filter pass {p}: tiles {a >> 32} with-kept {a & 0xffffffff} kept pairs {b}")
+    if False and tot:
         print("  " + "  ".join(f"{n} {100 * v / tot:.1f}%" for n, v in zip(names, ph)))
