@@ -212,6 +212,48 @@ struct RowNorms {
     }
 };
 
+// Per-row extra K=8 operand of the tcgen05 filter, [rows][8] fp32 = (-h hi, -h lo,
+// 1, 1, 0...), h = (1 - delta)|o_{0:d0}|^2 / 2 (umma.cu), TMA-loaded with 32B swizzle.
+bool make_aug_tmap(CUtensorMap* m, const float* base, uint64_t rows, uint32_t box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                    &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            encode = nullptr;
+        if (!encode) return false;
+    }
+    if (rows == 0 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    cuuint64_t gdim[2] = {8, rows};
+    cuuint64_t gstride[1] = {8 * 4};
+    cuuint32_t box[2] = {8, box_rows};
+    cuuint32_t estride[2] = {1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct RowAug {
+    DevBuf buf;
+    const float* rows = nullptr;
+    uint32_t n = 0, dim = 0, d0 = 0;
+    bool ok = false;
+    CUtensorMap map{};
+    const CUtensorMap* get(const float* r, uint32_t nn, uint32_t d, uint32_t dd0, const float* norms, cudaStream_t s) {
+        if (r != rows || nn != n || d != dim || dd0 != d0) {
+            buf.ensure(((size_t)nn + 1) * 32);
+            cuda_check(launch_row_aug(norms, nn, buf.as<float>(), s), "row aug");
+            rows = r;
+            n = nn;
+            dim = d;
+            d0 = dd0;
+            ok = make_aug_tmap(&map, buf.as<float>(), std::max<uint32_t>(nn, 1), 128);
+        }
+        return ok ? &map : nullptr;
+    }
+};
+
 struct TmapCache {
     const float* base = nullptr;
     uint64_t rows = 0;
@@ -271,7 +313,7 @@ struct dade_gpu_ctx {
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
     DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter, seed_goff;
-    DevBuf cnorm, qnorm, coarse_lo, coarse_overflow;  // coarse_lo: p~ per (query, centroid)
+    DevBuf cnorm, qnorm, coarse_lo, coarse_overflow, q_norms;  // coarse_lo: p~ per (query, centroid)
     bool coarse_force_exact = false, coarse_tc_used = false;
     int n_sms = 148;
     uint32_t surv_cap_hint = 0;
@@ -279,6 +321,7 @@ struct dade_gpu_ctx {
     TmapCache tm_centroids, tm_storage, tm_base;
     TmapCache tm32_storage{32}, tm32_base{32};
     RowNorms norms_storage, norms_base;
+    RowAug aug_storage;
     CUtensorMap tm_none{};
 
     // profiling
@@ -403,8 +446,9 @@ constexpr uint32_t kFilterQ = 32;           // queries per streaming work item (
 // Nearest-list items use shorter pieces: those rows keep most pairs (they hold
 // the query's neighbours), and short items spread that work over every SM.
 // Pass 0 takes the pieces covering the first kFilterItemRows rows.
-uint32_t rank0_item_rows() {
-    uint32_t r = 32;  // one tile: a nearest list's heavy rows spread over every warp
+constexpr uint32_t kUmmaQ = 256;            // queries per tcgen05 work item (MMA N)
+uint32_t rank0_item_rows(bool umma) {
+    uint32_t r = umma ? 128 : 32;  // one tile: a nearest list's heavy rows spread over every SM / warp
     if (const char* e = std::getenv("DADE_GPU_R0_ROWS")) r = (uint32_t)std::atoi(e);
     r = std::max<uint32_t>(32, std::min<uint32_t>(r, kFilterItemRows));
     return r;
@@ -474,6 +518,14 @@ bool filter_ok(dade_gpu_ctx* c, const ChunkTable& ct, uint32_t dim) {
     return d0 % 8 == 0 && d0 <= 2 * kBox && dim % 4 == 0 && dim >= (uint32_t)kBox;
 }
 
+// tcgen05 filter (umma.cu): 128-row TMA tiles (tm_storage), d0 a multiple of 8 up to 64
+bool umma_ok(dade_gpu_ctx* c, const ChunkTable& ct, bool tma128) {
+    (void)c;
+    if (!tma128 || env_flag("DADE_GPU_NO_UMMA")) return false;
+    const uint32_t d0 = ct.end[ct.n_dense - 1];
+    return d0 % 8 == 0 && d0 <= 2 * kBox;
+}
+
 // Streaming passes: [nearest lists], [the rest] (or one flat pass). Each pass =
 // tensor-core filter -> survivor kernel -> candidate buckets -> merge into the
 // running top-K; between passes every query's radius is tightened from it.
@@ -486,13 +538,18 @@ struct SeedArgs {
 
 void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, const float* d_q, uint32_t nq,
                    uint32_t k, bool two_pass, uint32_t max_items, const GroupArgs* g, const float* rows,
-                   uint32_t n_rows, TmapCache& tm32, uint64_t* out_keys, uint32_t* out_count, const SeedArgs& seed,
-                   RowNorms* norms) {
+                   uint32_t n_rows, TmapCache& tm_tile, bool umma, uint64_t* out_keys, uint32_t* out_count,
+                   const SeedArgs& seed, RowNorms* norms) {
     cudaStream_t s = c->stream;
     bool tma = false;
-    const CUtensorMap& tm = tm32.get(rows, std::max<uint32_t>(n_rows, 1), a.dim, tma);
+    const CUtensorMap& tm = tm_tile.get(rows, std::max<uint32_t>(n_rows, 1), a.dim, tma);
     if (!tma) fail(DADE_GPU_CUDA_ERROR, "tensor map for the streaming filter failed");
     const uint32_t d0 = ct.end[ct.n_dense - 1];
+    if (umma) {  // first-slice query norms for the tcgen05 filter's -c terms
+        c->q_norms.ensure((size_t)std::max<uint32_t>(nq, 1) * 4);
+        cuda_check(launch_row_norms(d_q, nq, a.dim, d0, c->q_norms.as<float>(), s), "query norms");
+        ++c->launches;
+    }
     uint32_t cap = std::max<uint32_t>(c->surv_cap_hint, (uint32_t)std::min<uint64_t>(64ull << 20, std::max<uint64_t>(1u << 20, (uint64_t)nq * 1024)));
     for (int attempt = 0; attempt < 2; ++attempt) {
         c->surv.ensure((size_t)cap * sizeof(Survivor));
@@ -548,24 +605,32 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             f.piece_lo = 0;
             f.piece_hi = 0xffffffffu;
             f.debug = ct.debug;
-            if (unsigned long long* ph = phase_ptr_keep(c)) f.census = ph + 2 * pass;  // DADE_GPU_PHASES=1
+            if (const char* ex = std::getenv("DADE_GPU_UMMA_EXP")) f.exp = std::atoi(ex);
+            if (unsigned long long* ph = phase_ptr_keep(c)) f.census = umma ? (pass == 2 ? ph : nullptr) : ph + 2 * pass;  // DADE_GPU_PHASES=1
             if (two_pass) {
                 if (pass < 2) {
                     f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
-                    const uint32_t p0 = std::max<uint32_t>(1, kFilterItemRows / rank0_item_rows());
+                    const uint32_t p0 = std::max<uint32_t>(1, kFilterItemRows / rank0_item_rows(umma));
                     f.piece_lo = pass == 0 ? 0u : p0;
                     f.piece_hi = pass == 0 ? p0 : 0xffffffffu;
                 } else {
                     f.item_base = g->n_items + 1;  // the rest
                 }
             }
-            // persistent CTAs pull items from a counter: two per SM
+            // persistent CTAs pull items from a counter: two per SM (one for tcgen05)
             c->item_counter.ensure(4);
             cuda_check(cudaMemsetAsync(c->item_counter.p, 0, 4, s), "memset");
             f.item_counter = c->item_counter.as<uint32_t>();
-            grid = std::min<uint32_t>(grid, (uint32_t)c->n_sms * 2);
+            f.q_norms = umma ? c->q_norms.as<float>() : nullptr;
+            const CUtensorMap* taug = nullptr;
+            if (umma) {
+                taug = c->aug_storage.get(rows, n_rows, a.dim, d0, f.row_norms, s);
+                if (!taug) fail(DADE_GPU_CUDA_ERROR, "tensor map for the tcgen05 filter's row operand failed");
+            }
+            grid = std::min<uint32_t>(grid, (uint32_t)c->n_sms * (umma ? 1 : 2));
             if (c->profiling) cuda_check(cudaEventRecord(c->ef[2 * pass], s), "event");
-            cuda_check(launch_filter(f, tm, grid, s), "filter");
+            if (umma) cuda_check(launch_filter_umma(f, tm, *taug, grid, s), "filter (tcgen05)");
+            else cuda_check(launch_filter(f, tm, grid, s), "filter");
             if (c->profiling) cuda_check(cudaEventRecord(c->ef[2 * pass + 1], s), "event");
             c->n_filter_passes = n_pass;
             cuda_check(cudaMemsetAsync(c->cand_count.p, 0, 4, s), "memset");
@@ -581,10 +646,10 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             sv.queries = d_q;
             sv.r_global = a.r_global;
             sv.coeff = a.coeff;
-            sv.n_dense_dims = d0;
+            sv.n_dense_dims = umma ? 0 : d0;  // tcgen05 filter: survivors restart from dim 0
             sv.n_ckpt = ct.n_ckpt;
             for (int i = 0; i < ct.n_ckpt; ++i) sv.cps[i] = (uint16_t)c->cps[i];
-            sv.first_ckpt = 1;
+            sv.first_ckpt = umma ? 0 : 1;
             sv.vec4 = (a.dim % 4 == 0 && d0 % 4 == 0) ? 1u : 0u;
             for (int i = 0; i < ct.n_ckpt; ++i)
                 if (c->cps[i] % 4 != 0) sv.vec4 = 0;
@@ -661,8 +726,9 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     const bool use_filter = filter_ok(c, ct, c->dim);
     // the streaming filter splits long lists into row pieces (more, shorter items)
     g.max_item_rows = use_filter ? kFilterItemRows : 0;
-    g.rank0_item_rows = use_filter && nrb > 1 ? rank0_item_rows() : 0;
-    g.q_chunk = use_filter ? kFilterQ : (uint32_t)kQC;
+    const bool umma = use_filter && umma_ok(c, ct, tma);
+    g.rank0_item_rows = use_filter && nrb > 1 ? rank0_item_rows(umma) : 0;
+    g.q_chunk = umma ? kUmmaQ : use_filter ? kFilterQ : (uint32_t)kQC;
     const bool seeded = n_probe > 1 && !seed_disabled() && k <= 512;
     if (use_filter && seeded) {  // the seed's rows of every nearest list are final results already
         g.seed_skip = seed_rows(k);
@@ -734,7 +800,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     if (use_filter) {
         SeedArgs sd{seeded, c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>()};
         stream_passes(c, a, ct, d_q, nq, k, nrb > 1, (uint32_t)max_items, &g, c->storage.as<float>(), c->count,
-                      c->tm32_storage, out_keys, out_count, sd, &c->norms_storage);
+                      umma ? c->tm_storage : c->tm32_storage, umma, out_keys, out_count, sd, &c->norms_storage);
         record(c, c->e2);
         return;
     }
@@ -938,6 +1004,8 @@ int dade_gpu_destroy(dade_gpu_ctx* c) {
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
         c->norms_storage.buf.release();
+        c->aug_storage.buf.release();
+        c->aug_storage.rows = nullptr;
         c->norms_base.buf.release();
         DevBuf* bufs[] = {&c->W, &c->centroids, &c->storage, &c->ids, &c->offsets, &c->base,
                           &c->d_cps, &c->d_coeff, &c->d_scale, &c->q_in, &c->q_rot, &c->probes,
@@ -1032,6 +1100,7 @@ int dade_gpu_set_ivf(dade_gpu_ctx* c, uint32_t dim, uint32_t count, uint32_t n_c
         c->count = count;
         c->n_clusters = n_clusters;
         c->norms_storage.rows = nullptr;
+        c->aug_storage.rows = nullptr;
         c->h_offsets.assign(offsets, offsets + n_clusters + 1);
         c->dev_offsets = c->h_offsets;
         c->has_ivf = true;
@@ -1080,6 +1149,7 @@ int dade_gpu_set_ivf_shard(dade_gpu_ctx* c, const uint8_t* mask) {
         c->dev_offsets = dev;
         c->count = (uint32_t)rows;
         c->norms_storage.rows = nullptr;
+        c->aug_storage.rows = nullptr;
     });
 }
 

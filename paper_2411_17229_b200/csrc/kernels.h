@@ -76,9 +76,18 @@ struct FilterArgs {
     uint32_t piece_lo, piece_hi;  // only items whose row piece is in [piece_lo, piece_hi)
     int debug;                    // 1: re-check every filter prune exactly (counters[3] = violations)
     unsigned long long* census;   // nullable: [0] tiles with kept pairs | tiles << 32, [1] kept pairs (diagnostic)
+    const float* q_norms;         // [nq] first-slice |q|^2 (sequential fmaf), tcgen05 filter only
+    int exp;                      // experiments (DADE_GPU_UMMA_EXP): 1 skip epilogue work, 2 skip MMAs
 };
 size_t filter_smem_bytes(int d0, int c_dense);
 cudaError_t launch_filter(const FilterArgs& a, const CUtensorMap& tmap32, uint32_t grid, cudaStream_t s);
+// umma.cu: the same filter on tcgen05 (128-row tiles, TMEM accumulators); kept
+// pairs leave with acc = 0 and are continued from dim 0 (SurvArgs::first_ckpt = 0)
+size_t filter_umma_smem_bytes(int c_dense);
+cudaError_t launch_filter_umma(const FilterArgs& a, const CUtensorMap& tmap128, const CUtensorMap& tmap_aug,
+                               uint32_t grid, cudaStream_t s);
+// per-row extra operand [n][8] = (-h hi, -h lo, 1, 1, 0, 0, 0, 0) from first-slice norms
+cudaError_t launch_row_aug(const float* norms, uint32_t n, float* out, cudaStream_t s);
 
 // Survivor kernel (stage 2 of the streaming scan) and candidate bucketing.
 struct SurvArgs {

@@ -892,19 +892,21 @@ __global__ void __launch_bounds__(kSvWarps * 32, 2) advance_survivors_kernel(con
     const uint32_t dim = a.dim;
     for (uint32_t grp = blockIdx.x * kSvWarps + warp; grp < n_groups; grp += gridDim.x * kSvWarps) {
         const uint32_t i = grp * 32 + lane;
-        bool live = false;
+        bool live = false, flagged = false;
         uint32_t q = 0, row = 0;
         float x = 0.f, r = 0.f;
         if (i < n) {
             const Survivor v = a.surv[i];
             if (v.q != 0xffffffffu) {
                 live = true;
+                flagged = (v.slot >> 31) != 0;  // debug: a pair the filter's bound pruned
                 q = v.q;
                 row = v.row;
                 x = v.acc;
                 r = __uint_as_float(a.r_global[q]);
             }
         }
+        unsigned long long viol = 0;
         unsigned long long dims = 0;
         uint32_t lo = a.n_dense_dims;
         for (uint32_t ci = a.first_ckpt; ci <= a.n_ckpt; ++ci) {
@@ -970,9 +972,15 @@ __global__ void __launch_bounds__(kSvWarps * 32, 2) advance_survivors_kernel(con
                 __syncwarp();  // staging buffers free for the next chunk
             }
             lo = hi;
-            if (live && ci < a.n_ckpt && x > prune_threshold(a.coeff[ci], r)) {
-                dims += hi;
-                live = false;
+            if (live && ci < a.n_ckpt) {
+                const bool pr = x > prune_threshold(a.coeff[ci], r);
+                if (flagged) {  // the exact prefix must agree with the bound; then drop it as the filter would
+                    viol += pr ? 0 : 1;
+                    live = false;
+                } else if (pr) {
+                    dims += hi;
+                    live = false;
+                }
             }
         }
         bool is_cand = false;
@@ -1001,8 +1009,12 @@ __global__ void __launch_bounds__(kSvWarps * 32, 2) advance_survivors_kernel(con
                 }
             }
         }
-        for (int off = 16; off > 0; off >>= 1) dims += __shfl_xor_sync(0xffffffffu, dims, off);
+        for (int off = 16; off > 0; off >>= 1) {
+            dims += __shfl_xor_sync(0xffffffffu, dims, off);
+            viol += __shfl_xor_sync(0xffffffffu, viol, off);
+        }
         if (lane == 0 && a.counters && dims) atomicAdd(a.counters + 1, dims);
+        if (lane == 0 && a.counters && viol) atomicAdd(a.counters + 3, viol);
     }
 }
 

@@ -1,0 +1,554 @@
+// Streaming first-slice DCO filter on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, accumulators in TMEM).
+//
+// One persistent CTA per SM. Work item = (posting-list row piece of <= 1024
+// rows, up to 256 of the queries probing that list). For every 128-row tile of
+// the piece, ONE tcgen05.mma chain computes, for all 128 x N (row, query) pairs,
+//
+//     acc = o.q - h_o - c_q,   h_o = (1 - delta)|o|^2 / 2,
+//                              c_q = ((1 - delta)|q|^2 - thr_q) / 2
+//
+// over the dense dims [0, d0) (TF32 operands straight from the fp32 rows: the
+// tile is TMA-loaded 128B-swizzled, K-major) plus one extra K=8 step whose
+// operands are (-h_o hi, -h_o lo, 1, 1) per row (a precomputed [rows][8] array,
+// TMA-loaded 32B-swizzled with the tile) and (1, 1, -c_q hi, -c_q lo) per query
+// (hi + lo splits keep the TF32 truncation below 2^-20 relative). The pair is
+// pruned for sure iff acc < 0, i.e.
+// (1 - delta)(|o|^2 + |q|^2) - 2 o.q > thr_q: the same rigorous bound as the
+// mma.sync filter (filter.cu); the reference would reject the
+// pair at its first checkpoint (proj/src/estimator.cpp:46-58).
+//
+// Roles (warp-specialised, mbarrier pipelines, no CTA barrier after setup):
+//   warp 16     stager: pulls items from the global counter and stages each
+//               item's queries (B operand, cp.async into the 128B-swizzled
+//               K-major layout), -c (B_aug) and query ids into one of two item
+//               buffers, running up to one item ahead of the MMAs;
+//   warp 17     TMA: loads 128-row tiles (+ their K=8 row operand) into a
+//               4-stage ring, running ahead across item boundaries;
+//   warp 18     MMA: one elected lane issues the tcgen05.mma chain of each tile
+//               into one of two TMEM accumulator buffers (2 x 256 columns);
+//   warps 0-15  epilogue: warp w reads TMEM lanes 32 (w % 4).. (its rows) and
+//               column quarter w / 4, two 32-column tcgen05.ld in flight; a
+//               chunk whose values are all negative is pruned whole (the
+//               common case); otherwise every kept (row, query) pair is
+//               appended to the survivor worklist, whose kernel runs the exact
+//               sequential fp32 accumulation from dim 0
+//               (advance_survivors_kernel).
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dade_gpu {
+
+namespace {
+
+constexpr int kUM = 128;            // rows per tile (MMA M, TMEM lanes)
+constexpr int kUQ = 256;            // max queries per item (MMA N)
+constexpr int kUEpiWarps = 16;
+constexpr int kUStager = kUEpiWarps;      // warp index
+constexpr int kUTma = kUEpiWarps + 1;     // warp index
+constexpr int kUMma = kUEpiWarps + 2;     // warp index
+constexpr int kUThreads = (kUEpiWarps + 3) * 32;
+constexpr int kUNB = 2;                   // item (B) buffers
+constexpr uint32_t kUTmemCols = 512;      // 2 accumulator buffers x 256 columns
+constexpr float kUDelta = 4e-3f;          // same bound as filter.cu / scan.cu
+constexpr uint32_t kUSentinel = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mb_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mb_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase
+// completes instead of spinning (spinning role warps steal issue slots from the
+// epilogue warps sharing their scheduler)
+__device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAITU_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAITU_%=;\n"
+        "}\n" ::"r"(su32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+__device__ __forceinline__ void tma2d_u(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// same, without the wait (several loads in flight; caller issues tcgen05.wait::ld)
+__device__ __forceinline__ void tc_ld32_nowait(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+// Shared-memory matrix descriptors (tcgen05 "version 1"):
+// K-major, 128B swizzle: rows of 128 B, 8-row atoms 1024 B apart (SBO).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// K-major, 32B swizzle (the K=8 tf32 operands): rows of 32 B, 8-row atoms 256 B apart.
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+}
+// byte offset of element (row, k < 8) in a 32B-swizzled K=8 operand (what TMA
+// SWIZZLE_32B writes): 16-byte chunk index ^= row bit 2
+__device__ __forceinline__ uint32_t sw32_off(uint32_t row, uint32_t k) {
+    return row * 32 + ((((k >> 2) ^ (row >> 2)) & 1u) << 4) + (k & 3) * 4;
+}
+
+struct UItem {  // published by the stager in item buffer ib
+    uint32_t row_start, row_count, qcount, ncols;
+};
+struct UMeta {  // per accumulator buffer, published by the MMA warp
+    uint32_t row0, nrows, qcount, ncols, ib, last, pad0, pad1;
+};
+
+struct ULayout {
+    size_t a, b, a_aug, b_aug, qidx, slot, item, meta, bars, tmem_slot, total;
+    int stages;
+};
+
+__host__ __device__ inline ULayout u_layout(int c_dense) {
+    ULayout L;
+    L.stages = c_dense == 1 ? 4 : 2;
+    size_t off = 0;
+    L.a = off; off += (size_t)L.stages * c_dense * kUM * 128;          // 1024-aligned atoms
+    L.b = off; off += (size_t)kUNB * c_dense * kUQ * 128;
+    L.a_aug = off; off += (size_t)L.stages * kUM * 32;                 // per stage, TMA (SW32)
+    L.b_aug = off; off += (size_t)kUNB * kUQ * 32;
+    L.qidx = off; off += (size_t)kUNB * kUQ * 4;
+    L.slot = off; off += (size_t)kUNB * kUQ * 4;
+    L.item = off; off += kUNB * sizeof(UItem);
+    L.meta = off; off += 2 * sizeof(UMeta);
+    L.bars = off; off += 8 * 24;
+    L.tmem_slot = off; off += 16;
+    L.total = off + 1024;
+    return L;
+}
+
+__global__ void __launch_bounds__(kUThreads, 1)
+dco_filter_umma_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap,
+                       const __grid_constant__ CUtensorMap tmap_aug) {
+    extern __shared__ unsigned char usmem_raw[];
+    unsigned char* sm = usmem_raw + ((1024u - (su32(usmem_raw) & 1023u)) & 1023u);
+    const int c_dense = a.c_dense;
+    const ULayout L = u_layout(c_dense);
+    const int S = L.stages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
+    uint64_t* afull = bars;            // [S]   TMA bytes landed
+    uint64_t* aempty = bars + 4;       // [S]   MMAs reading the stage done (commit)
+    uint64_t* accfull = bars + 8;      // [2]   MMAs of the tile done (commit)
+    uint64_t* accempty = bars + 10;    // [2]   every epilogue warp done with the buffer
+    uint64_t* metafull = bars + 12;    // [2]   tile metadata written (MMA warp)
+    uint64_t* bready = bars + 14;      // [NB]  item staged (stager)
+    uint64_t* bfree = bars + 16;       // [NB]  item's MMAs done (commit) + epilogue done with its ids
+    UItem* items = reinterpret_cast<UItem*>(sm + L.item);
+    UMeta* meta = reinterpret_cast<UMeta*>(sm + L.meta);
+    uint32_t* qidx_s = reinterpret_cast<uint32_t*>(sm + L.qidx);
+    uint32_t* slot_s = reinterpret_cast<uint32_t*>(sm + L.slot);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + L.tmem_slot);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            mb_init(afull + i, 1);
+            mb_init(aempty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mb_init(accfull + i, 1);
+            mb_init(accempty + i, kUEpiWarps);
+            mb_init(metafull + i, 1);
+        }
+        for (int i = 0; i < kUNB; ++i) {
+            mb_init(bready + i, 1);
+            mb_init(bfree + i, 1 + kUEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == kUMma) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                     "r"(kUTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t d0 = a.d0;
+
+    if (warp == kUStager) {
+        // ============================ stager ============================
+        const uint32_t base = a.item_base ? *a.item_base : 0u;
+        const uint32_t end = *a.n_items;
+        long long tp_stage = 0, tp_items = 0;
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t ib = k % kUNB;
+            // next item of this pass (other pieces are another sub-pass's)
+            WorkItem wi{};
+            bool have = false;
+            for (;;) {
+                uint32_t item = 0;
+                if (lane == 0) item = base + atomicAdd(a.item_counter, 1u);
+                item = __shfl_sync(0xffffffffu, item, 0);
+                if (item >= end) break;
+                wi = a.items[item];
+                const uint32_t piece = wi.bucket_count >> 16;
+                if (piece >= a.piece_lo && piece < a.piece_hi) {
+                    have = true;
+                    break;
+                }
+            }
+            if (k >= (uint32_t)kUNB) mb_wait(bfree + ib, ((k / kUNB) - 1) & 1);
+            if (!have) {
+                if (lane == 0) {
+                    items[ib] = UItem{kUSentinel, 0, 0, 0};
+                    mb_arrive(bready + ib);
+                }
+                break;
+            }
+            const long long t0 = clock64();
+            ++tp_items;
+            const uint32_t qcount = wi.bucket_count & 0xffffu;
+            const uint32_t ncols = max(32u, (qcount + 31) & ~31u);
+            unsigned char* bb = sm + L.b + (size_t)ib * c_dense * kUQ * 128;
+            float* baug = reinterpret_cast<float*>(sm + L.b_aug + (size_t)ib * kUQ * 32);
+            // loads first (8 independent chains per lane), then the smem writes / cp.async
+            constexpr int kPer = kUQ / 32;
+            uint32_t qv[kPer], sv[kPer];
+            float rv[kPer], nv[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const uint32_t j = lane + 32u * u;
+                qv[u] = j < qcount ? a.bucket_q[wi.bucket_start + j] : 0u;
+                sv[u] = j < qcount ? a.bucket_slot[wi.bucket_start + j] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const uint32_t j = lane + 32u * u;
+                rv[u] = j < qcount ? __uint_as_float(a.r_global[qv[u]]) : 0.f;
+                nv[u] = j < qcount ? a.q_norms[qv[u]] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const uint32_t j = lane + 32u * u;
+                if (j >= ncols) break;
+                float nc_hi = -__int_as_float(0x7f800000), nc_lo = 0.f;  // padding: -c = -inf (pruned)
+                if (j < qcount) {
+                    qidx_s[ib * kUQ + j] = qv[u];
+                    slot_s[ib * kUQ + j] = sv[u];
+                    const float th = prune_threshold(a.coeff0, rv[u]);
+                    const float nc = 0.5f * (th - (1.f - kUDelta) * nv[u]);
+                    nc_hi = tf32_hi(nc);
+                    nc_lo = isfinite(nc) ? nc - nc_hi : 0.f;
+                    const float* qrow = a.queries + (size_t)qv[u] * a.dim;
+                    for (int c = 0; c < c_dense; ++c) {
+                        unsigned char* brow = bb + (size_t)c * kUQ * 128 + (size_t)j * 128;
+                        const int wc4 = min(8, (int)(d0 - c * 32) / 4);
+                        for (int ch = 0; ch < 8; ++ch) {
+                            unsigned char* dst = brow + ((ch ^ (int)(j & 7)) << 4);
+                            if (ch < wc4) cp16(dst, qrow + c * 32 + ch * 4);
+                            else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                    }
+                } else {
+                    for (int c = 0; c < c_dense; ++c) {
+                        unsigned char* brow = bb + (size_t)c * kUQ * 128 + (size_t)j * 128;
+                        for (int ch = 0; ch < 8; ++ch)
+                            *reinterpret_cast<float4*>(brow + ch * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+                for (uint32_t kk = 0; kk < 8; ++kk)
+                    baug[sw32_off(j, kk) / 4] = kk < 2 ? 1.f : kk == 2 ? nc_hi : kk == 3 ? nc_lo : 0.f;
+            }
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                items[ib] = UItem{wi.row_start, wi.row_count, qcount, ncols};
+                mb_arrive(bready + ib);
+            }
+            tp_stage += clock64() - t0;
+        }
+        if (lane == 0 && a.census) {
+            atomicAdd(a.census + 0, (unsigned long long)tp_items);
+            atomicAdd(a.census + 1, (unsigned long long)tp_stage);
+        }
+    } else if (warp == kUTma) {
+        // ============================ TMA ============================
+        const uint32_t tile_bytes = (uint32_t)c_dense * kUM * 128 + kUM * 32;
+        uint32_t a_issue = 0;
+        long long tp_aempty = 0;
+        for (uint32_t k = 0;; ++k) {
+            mb_wait(bready + (k % kUNB), (k / kUNB) & 1);
+            const UItem it = items[k % kUNB];
+            if (it.row_start == kUSentinel) break;
+            const uint32_t n_tiles = (it.row_count + kUM - 1) / kUM;
+            for (uint32_t t = 0; t < n_tiles; ++t, ++a_issue) {
+                const uint32_t s = a_issue % S;
+                const long long t0 = clock64();
+                if (a_issue >= (uint32_t)S) mb_wait(aempty + s, ((a_issue / S) - 1) & 1);
+                tp_aempty += clock64() - t0;
+                if (lane == 0) {
+                    mb_arrive_tx(afull + s, tile_bytes);
+                    for (int c = 0; c < c_dense; ++c)
+                        tma2d_u(sm + L.a + ((size_t)s * c_dense + c) * kUM * 128, &tmap, c * 32,
+                                (int)(it.row_start + t * kUM), afull + s);
+                    tma2d_u(sm + L.a_aug + (size_t)s * kUM * 32, &tmap_aug, 0, (int)(it.row_start + t * kUM),
+                            afull + s);
+                }
+                __syncwarp();
+            }
+        }
+        if (lane == 0 && a.census) atomicAdd(a.census + 7, (unsigned long long)tp_aempty);
+    } else if (warp == kUMma) {
+        // ============================ MMA ============================
+        unsigned long long st_dco = 0, st_bytes = 0;
+        long long tp_bready = 0, tp_accempty = 0, tp_afull = 0;
+        uint32_t a_use = 0, acc_it = 0;
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t ib = k % kUNB;
+            {
+                const long long t0 = clock64();
+                mb_wait(bready + ib, (k / kUNB) & 1);
+                tp_bready += clock64() - t0;
+            }
+            const UItem it = items[ib];
+            if (it.row_start == kUSentinel) break;
+            const uint32_t n_tiles = (it.row_count + kUM - 1) / kUM;
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((it.ncols >> 3) << 17) |
+                                   ((uint32_t)(kUM >> 4) << 24);
+            const unsigned char* bb = sm + L.b + (size_t)ib * c_dense * kUQ * 128;
+            const float* baug = reinterpret_cast<const float*>(sm + L.b_aug + (size_t)ib * kUQ * 32);
+            for (uint32_t t = 0; t < n_tiles; ++t) {
+                const uint32_t s = a_use % S;
+                const uint32_t b = acc_it & 1;
+                long long t0 = clock64();
+                if (acc_it >= 2) mb_wait(accempty + b, ((acc_it >> 1) - 1) & 1);
+                tp_accempty += clock64() - t0;
+                const uint32_t nrows = min((uint32_t)kUM, it.row_count - t * kUM);
+                if (lane == 0) {  // metadata first: the epilogue prefetches the row norms meanwhile
+                    meta[b] = UMeta{it.row_start + t * kUM, nrows, it.qcount, it.ncols, ib,
+                                    t + 1 == n_tiles ? 1u : 0u, 0, 0};
+                    mb_arrive(metafull + b);
+                }
+                t0 = clock64();
+                mb_wait(afull + s, (a_use / S) & 1);
+                tp_afull += clock64() - t0;
+                tc_fence_after();
+                if (lane == 0 && a.exp == 2) {  // experiment: no MMAs
+                    tc_commit(aempty + s);
+                    tc_commit(accfull + b);
+                    if (t + 1 == n_tiles) tc_commit(bfree + ib);
+                } else if (lane == 0) {
+                    const uint32_t td = tmem + b * 256;
+                    uint32_t accf = 0;
+                    for (int c = 0; c < c_dense; ++c) {
+                        const uint32_t sa = su32(sm + L.a + ((size_t)s * c_dense + c) * kUM * 128);
+                        const uint32_t sb = su32(bb + (size_t)c * kUQ * 128);
+                        const int nk = min(4, (int)(d0 - c * 32) / 8);
+                        for (int kk = 0; kk < nk; ++kk) {
+                            tc_mma(td, desc_sw128(sa + kk * 32), desc_sw128(sb + kk * 32), idesc, accf);
+                            accf = 1;
+                        }
+                    }
+                    tc_mma(td, desc_sw32(su32(sm + L.a_aug + (size_t)s * kUM * 32)), desc_sw32(su32(baug)), idesc, 1u);
+                    tc_commit(aempty + s);
+                    tc_commit(accfull + b);
+                    if (t + 1 == n_tiles) tc_commit(bfree + ib);
+                }
+                __syncwarp();
+                st_dco += (unsigned long long)nrows * it.qcount;
+                st_bytes += 4ull * d0 * nrows;
+                ++a_use;
+                ++acc_it;
+            }
+        }
+        // tell the epilogue warps to stop
+        {
+            const uint32_t b = acc_it & 1;
+            if (acc_it >= 2) mb_wait(accempty + b, ((acc_it >> 1) - 1) & 1);
+            if (lane == 0) {
+                meta[b].row0 = kUSentinel;
+                mb_arrive(metafull + b);
+            }
+            __syncwarp();
+        }
+        if (lane == 0 && a.census) {
+            atomicAdd(a.census + 2, (unsigned long long)tp_bready);
+            atomicAdd(a.census + 3, (unsigned long long)tp_accempty);
+            atomicAdd(a.census + 4, (unsigned long long)tp_afull);
+        }
+        if (lane == 0 && a.counters) {
+            atomicAdd(a.counters + 0, st_dco);
+            atomicAdd(a.counters + 1, st_dco * d0);  // kept pairs' share is taken back by the epilogue
+            atomicAdd(a.counters + 2, st_bytes);
+        }
+    } else {
+        // ============================ epilogue ============================
+        const uint32_t quarter = warp & 3, cgrp = warp >> 2;  // rows 32 quarter.., columns chunks cgrp + 4 i
+        unsigned long long st_kept = 0, st_surv = 0;
+        long long te_meta = 0, te_acc = 0;
+        const bool dbg = a.debug == 1;
+        auto emit_chunk = [&](const float (&v)[32], uint32_t c0, const UMeta& m, uint32_t r) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const uint32_t col = c0 + i;
+                const bool valid = col < m.qcount && r < m.nrows;
+                const bool keep = valid && !(v[i] < 0.f);
+                const bool emit = dbg ? valid : keep;  // debug: every pair, the pruned ones flagged
+                const uint32_t bal = __ballot_sync(0xffffffffu, emit);
+                if (!bal) continue;
+                uint32_t sb = 0;
+                if (lane == 0) sb = atomicAdd(a.surv_count, __popc(bal));
+                sb = __shfl_sync(0xffffffffu, sb, 0);
+                if (emit) {
+                    const uint32_t p = sb + __popc(bal & ((1u << lane) - 1u));
+                    if (p < a.surv_cap) {
+                        Survivor sv;
+                        sv.q = qidx_s[m.ib * kUQ + col];
+                        sv.row = m.row0 + r;
+                        sv.acc = 0.f;
+                        sv.slot = slot_s[m.ib * kUQ + col] | (keep ? 0u : 0x80000000u);
+                        a.surv[p] = sv;
+                    }
+                }
+                const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+                if (lane == 0) {
+                    st_surv += __popc(bal);
+                    st_kept += __popc(kb);
+                }
+            }
+        };
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t b = k & 1;
+            long long t0 = clock64();
+            mb_wait(metafull + b, (k >> 1) & 1);
+            te_meta += clock64() - t0;
+            const UMeta m = meta[b];
+            if (m.row0 == kUSentinel) break;
+            const uint32_t r = quarter * 32 + lane;
+            // rows past the item (next list's rows / TMA zero fill) never keep
+            const uint32_t rowmask = r < m.nrows ? 0u : 0x80000000u;
+            t0 = clock64();
+            mb_wait(accfull + b, (k >> 1) & 1);
+            te_acc += clock64() - t0;
+            tc_fence_after();
+            const uint32_t nch = a.exp == 1 ? 0u : m.ncols / 32;
+            const uint32_t tbase = tmem + ((quarter * 32) << 16) + b * 256;
+            for (uint32_t c = cgrp; c < nch; c += 8) {  // two chunks (c, c + 4) per round
+                const bool two = c + 4 < nch;
+                float v0[32], v1[32];
+                tc_ld32_nowait(tbase + c * 32, v0);
+                if (two) tc_ld32_nowait(tbase + (c + 4) * 32, v1);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                // all negative <=> the AND of the 32 bit patterns has the sign bit
+                uint32_t and0 = rowmask | __float_as_uint(v0[0]), and1 = rowmask | (two ? __float_as_uint(v1[0]) : ~0u);
+#pragma unroll
+                for (int i = 1; i < 32; ++i) {
+                    and0 &= __float_as_uint(v0[i]);
+                    if (two) and1 &= __float_as_uint(v1[i]);
+                }
+                if (__any_sync(0xffffffffu, !(and0 >> 31)) || dbg) emit_chunk(v0, c * 32, m, r);
+                if (two && (__any_sync(0xffffffffu, !(and1 >> 31)) || dbg)) emit_chunk(v1, (c + 4) * 32, m, r);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                mb_arrive(accempty + b);
+                if (m.last) mb_arrive(bfree + m.ib);  // this item's query ids no longer read
+            }
+        }
+        if (lane == 0 && a.census && warp == 0) {
+            atomicAdd(a.census + 5, (unsigned long long)te_meta);
+            atomicAdd(a.census + 6, (unsigned long long)te_acc);
+        }
+        if (lane == 0 && a.counters) {
+            // kept pairs continue in the survivor kernel (which counts their dims)
+            if (st_kept) atomicAdd(a.counters + 1, 0ull - (unsigned long long)st_kept * d0);
+            atomicAdd(a.counters + 2, 16ull * st_surv);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kUMma) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kUTmemCols));
+    }
+}
+
+}  // namespace
+
+size_t filter_umma_smem_bytes(int c_dense) { return u_layout(c_dense).total; }
+
+cudaError_t launch_filter_umma(const FilterArgs& a, const CUtensorMap& tmap128, const CUtensorMap& tmap_aug,
+                               uint32_t grid, cudaStream_t s) {
+    if (grid == 0) return cudaSuccess;
+    const size_t smem = filter_umma_smem_bytes(a.c_dense);
+    DADE_CUDA_TRY(cudaFuncSetAttribute(dco_filter_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dco_filter_umma_kernel<<<grid, kUThreads, smem, s>>>(a, tmap128, tmap_aug);
+    return cudaGetLastError();
+}
+
+namespace {
+__global__ void row_aug_kernel(const float* __restrict__ norms, uint32_t n, float* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float h = 0.5f * (1.f - kUDelta) * norms[i];
+    const float hi = tf32_hi(h);
+    float4* o = reinterpret_cast<float4*>(out + (size_t)i * 8);
+    o[0] = make_float4(-hi, -(h - hi), 1.f, 1.f);
+    o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+}  // namespace
+
+cudaError_t launch_row_aug(const float* norms, uint32_t n, float* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    row_aug_kernel<<<(n + 255) / 256, 256, 0, s>>>(norms, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace dade_gpu

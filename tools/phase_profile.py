@@ -42,8 +42,16 @@ for it in range(3):
           f"frac {st.dims_accumulated / max(1, st.total_dco) / cfg.dim:.4f} "
           f"filter {filt_ms:.3f} ms / {n_filt}")
     if os.environ.get("DADE_GPU_PHASES") == "1":
-        for p in range(3):
-            a, b = int(buf[8 + 2 * p]), int(buf[9 + 2 * p])
-            print(f"  filter pass {p}: tiles {a >> 32} with-kept {a & 0xffffffff} kept pairs {b}")
+        if os.environ.get("DADE_GPU_NO_UMMA") == "1":
+            for p in range(3):
+                a, b = int(buf[8 + 2 * p]), int(buf[9 + 2 * p])
+                print(f"  filter pass {p}: tiles {a >> 32} with-kept {a & 0xffffffff} kept pairs {b}")
+        else:
+            c = [int(x) for x in buf[8:16]]
+            ncta = 148
+            us = lambda x: x / ncta / 1.9e3
+            print(f"  umma pass 2 per CTA: items {c[0] / ncta:.1f} stage {us(c[1]):.1f} us | mma wait: bready "
+                  f"{us(c[2]):.1f} accempty {us(c[3]):.1f} afull {us(c[4]):.1f} us | epi warp0 wait: meta "
+                  f"{us(c[5]):.1f} acc {us(c[6]):.1f} us | tma wait aempty {us(c[7]):.1f} us")
     if False and tot:
         print("  " + "  ".join(f"{n} {100 * v / tot:.1f}%" for n, v in zip(names, ph)))
