@@ -104,7 +104,14 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel: str = "dco_scan"):
+def measured_bf16():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["bf16_tflops"])
+    return 2250.0  # nominal dense bf16 (B200_PROFILING.md fallback)
+
+
+def ncu_traffic(kernel: str = "dco_filter_umma"):
     """dram bytes per launch of the scan kernel from the committed ncu summary."""
     for p in sorted((ROOT / "profiles").glob("ncu_*summary*.json"), reverse=True):
         try:
@@ -374,6 +381,7 @@ def run_ours(args, cfg):
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
     peak, peak_src = measured_peaks()
+    peak_bf16 = measured_bf16()
     traffic, traffic_src = ncu_traffic()
     roof = None
     if scan_ms:
@@ -383,17 +391,26 @@ def run_ours(args, cfg):
         d0 = cfg.delta_d
         pairs = stats.total_dco
         tc_tflops = 2.0 * pairs * d0 / (kern_ms / 1e3) / 1e12
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "dco_filter_kernel" if filter_ms else "dco_scan_kernel",
+        # dominant kernel: dco_filter_umma_kernel (tcgen05 TF32, TMEM accumulators). Algorithmic
+        # work = the first-slice dot products o.q over d0 dims of every DCO pair.
+        tf32_peak = 0.5 * peak_bf16  # TF32 dense = half the measured dense bf16 rate
+        roof = {"bound": "tensor", "achieved": tc_tflops, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": tc_tflops / tf32_peak, "traffic": traffic,
+                "kernel": "dco_filter_umma_kernel" if filter_ms else "dco_scan_kernel",
                 "kernel_launches_per_step": n_filter, "kernel_ms_per_step": kern_ms,
-                "algorithmic_bytes_per_step": scan_bytes, "scan_ms_seed_to_merge": scan_ms,
-                "peak_source": peak_src, "traffic_source": traffic_src,
-                "bytes_definition": "first-slice box bytes staged per (row tile, query chunk) + resident query "
-                                    "slices + work-item metadata + 16 B per survivor handed on (kernel-counted)",
-                "tensor": {"tf32_tflops": tc_tflops, "flops_definition": "2 * DCO pairs * d0 (first-slice o.q)",
-                           "peak_tf32_dense_tflops": 0.5 * 1632.7,
-                           "frac": tc_tflops / (0.5 * 1632.7)},
-                "note": "the filter is issue/latency bound (see DESIGN.md §5), not HBM or tensor bound"}
+                "flops_definition": "2 * DCO pairs * d0 per step (first-slice o.q of every (row, query) pair)",
+                "algorithmic_flops_per_step": 2.0 * pairs * d0, "scan_ms_seed_to_merge": scan_ms,
+                "peak_source": f"MEASURED_PEAKS.json bf16_tflops {peak_bf16} / 2 (TF32 dense)",
+                "traffic_source": traffic_src,
+                "tmem": {"bytes_per_pair": 4, "achieved_gbs": 4.0 * pairs / (kern_ms / 1e3) / 1e9,
+                         "peak_gbs": 64 * 148 * 1.965,
+                         "frac": 4.0 * pairs / (kern_ms / 1e3) / 1e9 / (64 * 148 * 1.965),
+                         "note": "fp32 accumulators read back with tcgen05.ld at 64 B/cycle/SM "
+                                 "(B300_MICROARCH.md TMEM table): the binding limit of this design"},
+                "hbm": {"achieved_gbs": achieved, "peak_gbs": peak, "frac": achieved / peak,
+                        "bytes_per_step": scan_bytes,
+                        "bytes_definition": "first-slice row-tile bytes per (tile, query item) + 16 B per "
+                                            "survivor handed on (kernel-counted)"}}
         el = stats.dims_accumulated
         roof["alu"] = {"reference_element_ops_per_s": el / (scan_ms / 1e3), "dims_accumulated": el,
                        "note": "DcoStats dims a sequential CPU scan would accumulate, per second of GPU scan"}
