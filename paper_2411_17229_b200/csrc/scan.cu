@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -1018,6 +1019,162 @@ __global__ void __launch_bounds__(kSvWarps * 32, 2) advance_survivors_kernel(con
     }
 }
 
+// Pipelined variant for dim, d0 and every checkpoint multiples of 4 (the
+// streaming path's rule): row chunks go global -> shared with cp.async (no
+// register staging, so three CTAs fit per SM) and the next chunk of the live
+// survivors is in flight while the current one is accumulated. Survivors come
+// out of the filters grouped by query, so when a warp's 32 survivors share one
+// query its chunk is staged once (else each lane reads its own from L1/L2).
+constexpr int kSpWarps = 8;
+constexpr int kSpRS = 36;                              // floats per staged row chunk
+constexpr int kSpWarpFloats = 2 * 32 * kSpRS + 2 * 32;  // rows[2][32][36] + q[2][32]
+
+__device__ __forceinline__ void sp_cp16(float* dst, const float* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kernel(const SurvArgs a) {
+    extern __shared__ __align__(16) float sp_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* rbuf = sp_smem + (size_t)warp * kSpWarpFloats;  // [2][32][kSpRS]
+    float* qbuf = rbuf + 2 * 32 * kSpRS;                   // [2][32]
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.surv_max) atomicMax(a.surv_max, *a.surv_count);
+    const uint32_t n = min(*a.surv_count, a.surv_cap);
+    const uint32_t n_groups = (n + 31) / 32;
+    const uint32_t dim = a.dim, n_ckpt = a.n_ckpt;
+    auto hi_of = [&](uint32_t ci) -> uint32_t { return ci < n_ckpt ? (uint32_t)a.cps[ci] : dim; };
+    for (uint32_t grp = blockIdx.x * kSpWarps + warp; grp < n_groups; grp += gridDim.x * kSpWarps) {
+        const uint32_t i = grp * 32 + lane;
+        bool live = false, flagged = false;
+        uint32_t q = 0, row = 0;
+        float x = 0.f, r = 0.f;
+        if (i < n) {
+            const Survivor v = a.surv[i];
+            if (v.q != 0xffffffffu) {
+                live = true;
+                flagged = (v.slot >> 31) != 0;  // debug: a pair the filter's bound pruned
+                q = v.q;
+                row = v.row;
+                x = v.acc;
+                r = __uint_as_float(a.r_global[q]);
+            }
+        }
+        uint32_t act = __ballot_sync(0xffffffffu, live);
+        unsigned long long dims = 0, viol = 0;
+        if (act) {
+            const uint32_t q0 = __shfl_sync(0xffffffffu, q, __ffs(act) - 1);
+            const bool qsame = __all_sync(0xffffffffu, !live || q == q0);
+            const float* qrow = a.queries + (size_t)q * dim;
+            auto issue = [&](uint32_t ci, uint32_t k0, uint32_t buf, uint32_t mask) {
+                const uint32_t w = min(32u, hi_of(ci) - k0);
+                const uint32_t sub = lane >> 3, c4 = lane & 7;
+                float* rb = rbuf + buf * 32 * kSpRS;
+#pragma unroll
+                for (uint32_t sg = 0; sg < 8; ++sg) {
+                    const uint32_t sidx = 4 * sg + sub;
+                    const uint32_t srow = __shfl_sync(0xffffffffu, row, sidx);
+                    if (((mask >> sidx) & 1u) && 4 * c4 < w)
+                        sp_cp16(rb + sidx * kSpRS + 4 * c4, a.storage + (size_t)srow * dim + k0 + 4 * c4);
+                }
+                if (qsame && lane < 8 && 4u * lane < w)
+                    sp_cp16(qbuf + buf * 32 + 4 * lane, a.queries + (size_t)q0 * dim + k0 + 4 * lane);
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+            };
+            uint32_t ci = a.first_ckpt, k0 = a.n_dense_dims, buf = 0;
+            issue(ci, k0, 0, act);
+            for (;;) {
+                const uint32_t hi = hi_of(ci);
+                const uint32_t w = min(32u, hi - k0);
+                uint32_t nci = ci, nk0 = k0 + 32;
+                if (nk0 >= hi) {
+                    nci = ci + 1;
+                    nk0 = hi;
+                }
+                const bool has_next = nci <= n_ckpt && nk0 < dim;
+                if (has_next) issue(nci, nk0, buf ^ 1, act);  // speculative: the live set of now
+                if (has_next) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+                else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                __syncwarp();
+                if (live) {
+                    const float* os = rbuf + buf * 32 * kSpRS + lane * kSpRS;
+                    if (qsame) {
+                        const float* qs = qbuf + buf * 32;
+                        for (uint32_t k = 0; k < w; k += 4) {
+                            const float4 o4 = *reinterpret_cast<const float4*>(os + k);
+                            const float4 q4 = *reinterpret_cast<const float4*>(qs + k);
+                            x = sq_step(x, o4.x, q4.x);
+                            x = sq_step(x, o4.y, q4.y);
+                            x = sq_step(x, o4.z, q4.z);
+                            x = sq_step(x, o4.w, q4.w);
+                        }
+                    } else {
+                        for (uint32_t k = 0; k < w; k += 4) {
+                            const float4 o4 = *reinterpret_cast<const float4*>(os + k);
+                            const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + k0 + k));
+                            x = sq_step(x, o4.x, q4.x);
+                            x = sq_step(x, o4.y, q4.y);
+                            x = sq_step(x, o4.z, q4.z);
+                            x = sq_step(x, o4.w, q4.w);
+                        }
+                    }
+                }
+                __syncwarp();  // buffer `buf` free for the chunk after next
+                if (k0 + w == hi && ci < n_ckpt && live) {
+                    const bool pr = x > prune_threshold(a.coeff[ci], r);
+                    if (flagged) {  // the exact prefix must agree with the bound; then drop it as the filter would
+                        viol += pr ? 0 : 1;
+                        live = false;
+                    } else if (pr) {
+                        dims += hi;
+                        live = false;
+                    }
+                }
+                act = __ballot_sync(0xffffffffu, live);
+                if (!has_next || !act) {
+                    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                    break;
+                }
+                ci = nci;
+                k0 = nk0;
+                buf ^= 1;
+            }
+        }
+        bool is_cand = false;
+        uint64_t key = 0;
+        if (live) {
+            dims += dim;
+            const float key_d = __fsqrt_rn(x);
+            if (!(key_d > r)) {
+                is_cand = true;
+                const uint32_t id = a.row_ids ? __ldg(a.row_ids + row) : a.id_base + row;
+                key = make_key(key_d, id);
+            }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, is_cand);
+        if (bal) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(a.cand_count, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (is_cand) {
+                const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
+                if (pos < a.cand_cap) {
+                    a.cand_q[pos] = q;
+                    a.cand_key[pos] = key;
+                    atomicAdd(a.q_count + q, 1u);
+                }
+            }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            dims += __shfl_xor_sync(0xffffffffu, dims, off);
+            viol += __shfl_xor_sync(0xffffffffu, viol, off);
+        }
+        if (lane == 0 && a.counters && dims) atomicAdd(a.counters + 1, dims);
+        if (lane == 0 && a.counters && viol) atomicAdd(a.counters + 3, viol);
+    }
+}
+
 // Exclusive scan of per-query candidate counts (single CTA).
 __global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* cnt, uint32_t n, uint32_t* off) {
     __shared__ uint32_t s_v[1024];
@@ -1188,11 +1345,19 @@ cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorM
 
 cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cudaStream_t s) {
     if (max_entries == 0) return cudaSuccess;
-    const size_t smem = sizeof(float) * kSvWarps * 2 * 32 * kSvStride;
-    DADE_CUDA_TRY(cudaFuncSetAttribute(advance_survivors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (a.vec4 && !std::getenv("DADE_GPU_SURV_V1")) {
+        const size_t smem = sizeof(float) * kSpWarps * kSpWarpFloats;
+        DADE_CUDA_TRY(cudaFuncSetAttribute(advance_survivors_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const uint32_t groups = (max_entries + 31) / 32;
+        const uint32_t grid = std::min<uint32_t>((groups + kSpWarps - 1) / kSpWarps, (uint32_t)sms * 3);
+        advance_survivors_pipe_kernel<<<grid, kSpWarps * 32, smem, s>>>(a);
+        return cudaGetLastError();
+    }
+    const size_t smem = sizeof(float) * kSvWarps * 2 * 32 * kSvStride;
+    DADE_CUDA_TRY(cudaFuncSetAttribute(advance_survivors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint32_t groups = (max_entries + 31) / 32;
     const uint32_t grid = std::min<uint32_t>((groups + kSvWarps - 1) / kSvWarps, (uint32_t)sms * 3);
     advance_survivors_kernel<<<grid, kSvWarps * 32, smem, s>>>(a);
