@@ -433,20 +433,33 @@ dco_filter_umma_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap t
         unsigned long long st_kept = 0, st_surv = 0;
         long long te_meta = 0, te_acc = 0;
         const bool dbg = a.debug == 1;
+        // kept pairs of a 32-column chunk -> worklist, column (query) major so the
+        // survivor kernel's warps mostly see one query; one atomic per chunk
         auto emit_chunk = [&](const float (&v)[32], uint32_t c0, const UMeta& m, uint32_t r) {
+            // pass 1: count (one atomic per chunk); pass 2: recompute the ballots and write
+            uint32_t total = 0, kept = 0;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 const uint32_t col = c0 + i;
                 const bool valid = col < m.qcount && r < m.nrows;
                 const bool keep = valid && !(v[i] < 0.f);
-                const bool emit = dbg ? valid : keep;  // debug: every pair, the pruned ones flagged
-                const uint32_t bal = __ballot_sync(0xffffffffu, emit);
-                if (!bal) continue;
-                uint32_t sb = 0;
-                if (lane == 0) sb = atomicAdd(a.surv_count, __popc(bal));
-                sb = __shfl_sync(0xffffffffu, sb, 0);
+                total += __popc(__ballot_sync(0xffffffffu, dbg ? valid : keep));  // debug: every pair, pruned ones flagged
+                kept += __popc(__ballot_sync(0xffffffffu, keep));
+            }
+            if (!total) return;
+            uint32_t sb = 0;
+            if (lane == 0) sb = atomicAdd(a.surv_count, total);
+            sb = __shfl_sync(0xffffffffu, sb, 0);
+            const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const uint32_t col = c0 + i;
+                const bool valid = col < m.qcount && r < m.nrows;
+                const bool keep = valid && !(v[i] < 0.f);
+                const bool emit = dbg ? valid : keep;
+                const uint32_t bl = __ballot_sync(0xffffffffu, emit);
                 if (emit) {
-                    const uint32_t p = sb + __popc(bal & ((1u << lane) - 1u));
+                    const uint32_t p = sb + __popc(bl & lt);
                     if (p < a.surv_cap) {
                         Survivor sv;
                         sv.q = qidx_s[m.ib * kUQ + col];
@@ -456,11 +469,11 @@ dco_filter_umma_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap t
                         a.surv[p] = sv;
                     }
                 }
-                const uint32_t kb = __ballot_sync(0xffffffffu, keep);
-                if (lane == 0) {
-                    st_surv += __popc(bal);
-                    st_kept += __popc(kb);
-                }
+                sb += __popc(bl);
+            }
+            if (lane == 0) {
+                st_surv += total;
+                st_kept += kept;
             }
         };
         for (uint32_t k = 0;; ++k) {
