@@ -317,6 +317,8 @@ struct dade_gpu_ctx {
     bool coarse_force_exact = false, coarse_tc_used = false;
     int n_sms = 148;
     uint32_t surv_cap_hint = 0;
+    uint32_t surv_cap_used = 0;     // worklist capacity of the last streaming search (0: none)
+    uint32_t* h_flags = nullptr;    // pinned [2]: surv_max, coarse overflow of the last search
     DevBuf counters, phase;
     TmapCache tm_centroids, tm_storage, tm_base;
     TmapCache tm32_storage{32}, tm32_base{32};
@@ -550,8 +552,14 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         cuda_check(launch_row_norms(d_q, nq, a.dim, d0, c->q_norms.as<float>(), s), "query norms");
         ++c->launches;
     }
-    uint32_t cap = std::max<uint32_t>(c->surv_cap_hint, (uint32_t)std::min<uint64_t>(64ull << 20, std::max<uint64_t>(1u << 20, (uint64_t)nq * 1024)));
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    // Worklist capacity: a hint learnt from earlier searches; overflow is detected
+    // after the search (search_overflowed) and the search is redone larger, so
+    // no host sync sits in the middle of the pipeline.
+    uint32_t base_cap = (uint32_t)std::min<uint64_t>(64ull << 20, std::max<uint64_t>(1u << 20, (uint64_t)nq * 1024));
+    if (const char* e = std::getenv("DADE_GPU_SURV_CAP")) base_cap = (uint32_t)std::max(64, std::atoi(e));  // test hook
+    const uint32_t cap = std::max<uint32_t>(c->surv_cap_hint, base_cap);
+    c->surv_cap_used = cap;
+    {
         c->surv.ensure((size_t)cap * sizeof(Survivor));
         c->surv_count.ensure(8);
         c->cand_q.ensure((size_t)cap * 4);
@@ -682,19 +690,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 ++c->launches;
             }
         }
-        // the worklists must not have overflowed: otherwise grow them and redo
-        uint32_t mx = 0;
-        cuda_check(cudaMemcpyAsync(&mx, c->surv_max.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
-        cuda_check(cudaStreamSynchronize(s), "sync");
-        if (mx <= cap) {
-            c->surv_cap_hint = std::max(c->surv_cap_hint, mx);
-            return;
-        }
-        cap = (uint32_t)std::min<uint64_t>(0xffffffffull, (uint64_t)mx * 2);
-        cuda_check(launch_fill_u32(a.r_global, 0x7f800000u, nq, s), "fill");
-        cuda_check(cudaMemsetAsync(a.counters, 0, 64, s), "memset");
     }
-    fail(DADE_GPU_RUNTIME_ERROR, "survivor worklist overflow");
 }
 
 // Rotated device queries -> packed top-K keys [nq x k] + counts in
@@ -908,6 +904,29 @@ void collect_stats(dade_gpu_ctx* c, dade_gpu_stats* stats) {
     stats->dims_accumulated += h[1];
 }
 
+// Overflow flags of the search just enqueued (worklist, coarse candidate list):
+// read back with the results in one pinned copy; check after the sync.
+void enqueue_flags(dade_gpu_ctx* c) {
+    if (!c->h_flags) cuda_check(cudaMallocHost(reinterpret_cast<void**>(&c->h_flags), 8), "cudaMallocHost");
+    c->h_flags[0] = c->h_flags[1] = 0;
+    if (c->surv_cap_used)
+        cuda_check(cudaMemcpyAsync(c->h_flags, c->surv_max.p, 4, cudaMemcpyDeviceToHost, c->stream), "D2H flags");
+    if (c->coarse_tc_used)
+        cuda_check(cudaMemcpyAsync(c->h_flags + 1, c->coarse_overflow.p, 4, cudaMemcpyDeviceToHost, c->stream),
+                   "D2H flags");
+}
+
+// after the sync: true if the search must be redone (and the redo is configured)
+bool search_overflowed(dade_gpu_ctx* c) {
+    if (c->surv_cap_used && c->h_flags[0] > c->surv_cap_used) {
+        c->surv_cap_hint = (uint32_t)std::min<uint64_t>(0xffffffffull, (uint64_t)c->h_flags[0] * 2);
+        c->surv_cap_used = 0;
+        return true;
+    }
+    if (c->surv_cap_used) c->surv_cap_hint = std::max(c->surv_cap_hint, c->h_flags[0]);
+    return false;
+}
+
 // Common driver: results as ids/dists/counts (host or device).
 void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t dim, uint32_t k,
                    uint32_t flags, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
@@ -918,6 +937,7 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
     record(c, c->e0);
     c->n_filter_passes = 0;
+    c->surv_cap_used = 0;
     if (nq == 0) return;
     const float* d_q = stage_queries(c, queries, nq, dim, flags);
     c->out_keys.ensure((size_t)nq * k * 8);
@@ -946,13 +966,16 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
             cuda_check(cudaMemcpyAsync(out_counts, cnts, (size_t)nq * 4, cudaMemcpyDeviceToHost, s), "D2H counts");
     }
     record(c, c->e3);
-    if (!dev) cuda_check(cudaStreamSynchronize(s), "search");
+    enqueue_flags(c);
+    cuda_check(cudaStreamSynchronize(s), "search");
+    if (search_overflowed(c)) {  // survivor worklist too small: redo with the observed size x2
+        search_common(c, queries, nq, dim, k, flags, out_ids, out_dists, out_counts, stats, run);
+        return;
+    }
     if (c->coarse_tc_used) {
         // more boundary candidates than the exact stage holds (pathological
         // ties): redo the search with the all-exact coarse ranking
-        uint32_t ov = 0;
-        cuda_check(cudaMemcpyAsync(&ov, c->coarse_overflow.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
-        cuda_check(cudaStreamSynchronize(s), "sync");
+        const uint32_t ov = c->h_flags[1];
         if (ov) {
             c->coarse_force_exact = true;
             try {
@@ -1003,6 +1026,8 @@ int dade_gpu_destroy(dade_gpu_ctx* c) {
         if (!c) return;
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
+        if (c->h_flags) cudaFreeHost(c->h_flags);
+        c->h_flags = nullptr;
         c->norms_storage.buf.release();
         c->aug_storage.buf.release();
         c->aug_storage.rows = nullptr;
@@ -1315,7 +1340,21 @@ int dade_gpu_ivf_search_keys(dade_gpu_ctx* c, const float* d_queries, uint32_t n
         if (nq == 0) return;
         const float* d_q = stage_queries(c, d_queries, nq, c->dim, flags | DADE_GPU_DEVICE_PTRS);
         c->out_count.ensure((size_t)nq * 4);
-        ivf_search_device(c, d_q, nq, k, n_probe, d_out_keys, c->out_count.as<uint32_t>());
+        for (int attempt = 0;; ++attempt) {
+            c->surv_cap_used = 0;
+            ivf_search_device(c, d_q, nq, k, n_probe, d_out_keys, c->out_count.as<uint32_t>());
+            enqueue_flags(c);
+            cuda_check(cudaStreamSynchronize(c->stream), "search");
+            if (!search_overflowed(c)) break;
+            if (attempt >= 2) fail(DADE_GPU_RUNTIME_ERROR, "survivor worklist overflow");
+            cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+        }
+        if (c->coarse_tc_used && c->h_flags[1]) {  // pathological coarse ties: all-exact ranking
+            c->coarse_force_exact = true;
+            cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+            ivf_search_device(c, d_q, nq, k, n_probe, d_out_keys, c->out_count.as<uint32_t>());
+            c->coarse_force_exact = false;
+        }
         collect_stats(c, stats);
     });
 }
