@@ -13,48 +13,84 @@ namespace {
 // ---- K1: out[i][k] = (float) sum_r W[k*D + r] * in[i][r] --------------------
 // f64 accumulation in r order with separately rounded DMUL/DADD, exactly
 // OrthoTransform::transform_vector (proj/src/transform.cpp:221-228).
-constexpr int kRotTile = 32;  // output columns per CTA
-constexpr int kRotRows = 64;  // rows per CTA (8 per thread: independent DADD chains)
-constexpr int kRotK = 32;     // r chunk
+
+// 32 output columns x 64 rows per CTA, a 4-row x 2-column register block per
+// thread; W and x chunks staged transposed ([r][col], [r][row]) so each
+// thread's weights and inputs of one r are 16-byte loads. Every output element
+// is the reference's sequential fp64 sum over r = 0..D-1 (DMUL + DADD, no FMA).
+constexpr int kRotC = 32;   // columns per CTA
+constexpr int kRotR = 64;   // rows per CTA
+constexpr int kRotK = 32;   // r chunk
 
 __global__ void __launch_bounds__(256)
 rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in, uint32_t n,
               float* __restrict__ out) {
-    __shared__ double ws[kRotTile][kRotK + 1];
-    __shared__ double xs[kRotRows][kRotK + 1];
-    const int tx = threadIdx.x & 31;  // output column within tile
-    const int ty = threadIdx.x >> 5;  // 0..7 -> rows ty*8 .. ty*8+7
-    const uint32_t col0 = blockIdx.x * kRotTile;
-    const uint32_t row0 = blockIdx.y * kRotRows;
-    double acc[8];
+    __shared__ __align__(16) double ws[kRotK][kRotC + 2];
+    __shared__ __align__(16) double xs[kRotK][kRotR + 2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tc = lane & 15;                    // columns 2 tc, 2 tc + 1
+    const int tr = warp * 2 + (lane >> 4);       // rows 4 tr .. 4 tr + 3
+    const uint32_t col0 = blockIdx.x * kRotC;
+    const uint32_t row0 = blockIdx.y * kRotR;
+    double acc[4][2];
 #pragma unroll
-    for (int ii = 0; ii < 8; ++ii) acc[ii] = 0.0;
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+    // chunk r0's W / x values: this thread's 4 + 8 staging elements, loaded one
+    // chunk ahead into registers while the previous chunk is accumulated
+    constexpr int kWPer = kRotC * kRotK / 256, kXPer = kRotR * kRotK / 256;
+    double wreg[kWPer];
+    float xreg[kXPer];
+    auto load_chunk = [&](uint32_t r0) {
+#pragma unroll
+        for (int u = 0; u < kWPer; ++u) {
+            const int idx = threadIdx.x + 256 * u, a = idx / kRotK, b = idx % kRotK;
+            const uint32_t col = col0 + a, r = r0 + b;
+            wreg[u] = (col < dim && r < dim) ? __ldg(W + (size_t)col * dim + r) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kXPer; ++u) {
+            const int idx = threadIdx.x + 256 * u, a = idx / kRotK, b = idx % kRotK;
+            const uint32_t row = row0 + a, r = r0 + b;
+            xreg[u] = (row < n && r < dim) ? __ldg(in + (size_t)row * dim + r) : 0.f;
+        }
+    };
+    load_chunk(0);
     for (uint32_t r0 = 0; r0 < dim; r0 += kRotK) {
         __syncthreads();
-        for (int idx = threadIdx.x; idx < kRotTile * kRotK; idx += 256) {
-            const int a = idx / kRotK, b = idx % kRotK;
-            const uint32_t col = col0 + a, r = r0 + b;
-            ws[a][b] = (col < dim && r < dim) ? W[(size_t)col * dim + r] : 0.0;
+#pragma unroll
+        for (int u = 0; u < kWPer; ++u) {
+            const int idx = threadIdx.x + 256 * u;
+            ws[idx % kRotK][idx / kRotK] = wreg[u];
         }
-        for (int idx = threadIdx.x; idx < kRotRows * kRotK; idx += 256) {
-            const int a = idx / kRotK, b = idx % kRotK;
-            const uint32_t row = row0 + a, r = r0 + b;
-            xs[a][b] = (row < n && r < dim) ? (double)in[(size_t)row * dim + r] : 0.0;
+#pragma unroll
+        for (int u = 0; u < kXPer; ++u) {
+            const int idx = threadIdx.x + 256 * u;
+            xs[idx % kRotK][idx / kRotK] = (double)xreg[u];
         }
         __syncthreads();
+        if (r0 + kRotK < dim) load_chunk(r0 + kRotK);
         const int kmax = (int)min((uint32_t)kRotK, dim - r0);
+#pragma unroll 4
         for (int b = 0; b < kmax; ++b) {
-            const double w = ws[tx][b];
+            const double2 w = *reinterpret_cast<const double2*>(&ws[b][2 * tc]);
+            const double2 x01 = *reinterpret_cast<const double2*>(&xs[b][4 * tr]);
+            const double2 x23 = *reinterpret_cast<const double2*>(&xs[b][4 * tr + 2]);
+            const double x[4] = {x01.x, x01.y, x23.x, x23.y};
 #pragma unroll
-            for (int ii = 0; ii < 8; ++ii) acc[ii] = __dadd_rn(acc[ii], __dmul_rn(w, xs[ty * 8 + ii][b]));
+            for (int i = 0; i < 4; ++i) {
+                acc[i][0] = __dadd_rn(acc[i][0], __dmul_rn(w.x, x[i]));
+                acc[i][1] = __dadd_rn(acc[i][1], __dmul_rn(w.y, x[i]));
+            }
         }
     }
-    const uint32_t col = col0 + tx;
-    if (col < dim) {
 #pragma unroll
-        for (int ii = 0; ii < 8; ++ii) {
-            const uint32_t row = row0 + ty * 8 + ii;
-            if (row < n) out[(size_t)row * dim + col] = __double2float_rn(acc[ii]);
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t row = row0 + 4 * tr + i;
+        if (row >= n) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const uint32_t col = col0 + 2 * tc + j;
+            if (col < dim) out[(size_t)row * dim + col] = __double2float_rn(acc[i][j]);
         }
     }
 }
@@ -713,7 +749,7 @@ cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s) {
 cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
                           cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    dim3 grid((dim + kRotTile - 1) / kRotTile, (n + kRotRows - 1) / kRotRows);
+    dim3 grid((dim + kRotC - 1) / kRotC, (n + kRotR - 1) / kRotR);
     rotate_kernel<<<grid, 256, 0, s>>>(W, dim, in, n, out);
     return cudaGetLastError();
 }
