@@ -260,6 +260,148 @@ __global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restr
     for (uint32_t i = lane; i < n_probe; i += 32) probes[(size_t)qi * n_probe + i] = kk[i];
 }
 
+// Fast path (n_cen <= 1024, dim % 4 == 0), warp per query:
+//   * the query's p~ row and the bounds live in registers (32 per lane);
+//   * B = n_probe-th smallest upper bound by bitwise descent (warp-reduced counts);
+//   * candidates (lower bound <= B) compacted by ballots;
+//   * exact l2_sq of 32 candidates at a time: their rows staged 32 dims at a time
+//     through shared memory with coalesced 16-byte loads (8 lanes per 128-byte
+//     row chunk), each lane then advancing its candidate's sequential fp32 sum;
+//   * (acc, id) bitonic sort of the candidates, first n_probe -> probes.
+constexpr int kFsWarps = 4;
+__device__ __forceinline__ void cs_cp16(float* dst, const float* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+constexpr int kFsRS = 36;  // floats per staged row chunk (16-byte aligned, conflict-free LDS.128)
+
+__global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
+    const float* __restrict__ pt, const float* __restrict__ cnorm, const float* __restrict__ qnorm,
+    const float* __restrict__ cen, uint32_t n_cen, const float* __restrict__ q, uint32_t nq, uint32_t dim,
+    uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow) {
+    __shared__ uint64_t cand[kFsWarps][kSelCap];
+    __shared__ __align__(16) float rows[kFsWarps][32 * kFsRS];
+    __shared__ __align__(16) float qch[kFsWarps][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t qi = blockIdx.x * kFsWarps + warp;
+    if (qi >= nq) return;
+    const float* prow = pt + (size_t)qi * n_cen;
+    const float qn = qnorm[qi];
+    uint32_t hk[32], lk[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t c = lane + 32u * j;
+        if (c < n_cen) {
+            const float p = prow[c], d = kCoarseDelta * (cnorm[c] + qn);
+            hk[j] = fkey(p + d);
+            lk[j] = fkey(p - d);
+        } else {
+            hk[j] = 0xffffffffu;
+            lk[j] = 0xffffffffu;
+        }
+    }
+    // B = the n_probe-th smallest hk: largest prefix with count(hk < prefix) < n_probe.
+    // Bits above the highest one where the warp's min and max key differ are common
+    // to every key, B included: start the descent below them.
+    uint32_t kmin = 0xffffffffu, kmax = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        kmin = min(kmin, hk[j]);
+        if (lane + 32u * j < n_cen) kmax = max(kmax, hk[j]);
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    const int top = kmin == kmax ? -1 : 31 - __clz(kmin ^ kmax);
+    uint32_t pre = top >= 31 ? 0u : (kmin & ~((2u << top) - 1u));
+    if (kmin == kmax) pre = kmin;
+    for (int bit = top; bit >= 0; --bit) {
+        const uint32_t trial = pre | (1u << bit);
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) cnt += hk[j] < trial ? 1u : 0u;
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (cnt < n_probe) pre = trial;
+    }
+    const uint32_t B = pre;  // exactly the n_probe-th smallest key
+    // candidates: every centroid whose lower bound is <= B
+    uint32_t n = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const bool is = lk[j] <= B && (lane + 32u * j) < n_cen;
+        const uint32_t bal = __ballot_sync(0xffffffffu, is);
+        const uint32_t pos = n + __popc(bal & ((1u << lane) - 1u));
+        if (is && pos < (uint32_t)kSelCap) cand[warp][pos] = lane + 32u * j;
+        n += __popc(bal);
+    }
+    if (n > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
+        if (lane == 0) atomicAdd(overflow, 1u);
+        n = kSelCap;
+    }
+    __syncwarp();
+    // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43) of the candidates
+    const float* qr = q + (size_t)qi * dim;
+    float* rs = rows[warp];
+    float* qs = qch[warp];
+    for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const uint32_t my_c = e < n ? (uint32_t)cand[warp][e] : 0u;
+        const uint32_t nv = min(32u, n - e0);
+        float acc = 0.f;
+        for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
+            const uint32_t w = min(32u, dim - k0);
+            const uint32_t sub = lane >> 3, c4 = lane & 7;
+            float4 v[8];
+#pragma unroll
+            for (int sg = 0; sg < 8; ++sg) {
+                const uint32_t sidx = 4 * sg + sub;
+                const uint32_t cc = __shfl_sync(0xffffffffu, my_c, sidx);
+                v[sg] = (sidx < nv && 4 * c4 < w) ? __ldg(reinterpret_cast<const float4*>(cen + (size_t)cc * dim + k0) + c4)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const float4 qv = (lane < 8 && 4u * lane < w) ? __ldg(reinterpret_cast<const float4*>(qr + k0) + lane)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            __syncwarp();  // previous chunk's readers done
+#pragma unroll
+            for (int sg = 0; sg < 8; ++sg)
+                *reinterpret_cast<float4*>(rs + (4 * sg + sub) * kFsRS + 4 * c4) = v[sg];
+            if (lane < 8) *reinterpret_cast<float4*>(qs + 4 * lane) = qv;
+            __syncwarp();
+            if (e < n) {
+                const float* os = rs + lane * kFsRS;
+                for (uint32_t k = 0; k < w; k += 4) {
+                    const float4 o4 = *reinterpret_cast<const float4*>(os + k);
+                    const float4 q4 = *reinterpret_cast<const float4*>(qs + k);
+                    acc = sq_step(acc, q4.x, o4.x);
+                    acc = sq_step(acc, q4.y, o4.y);
+                    acc = sq_step(acc, q4.z, o4.z);
+                    acc = sq_step(acc, q4.w, o4.w);
+                }
+            }
+        }
+        __syncwarp();
+        if (e < n) cand[warp][e] = make_key(acc, my_c);
+    }
+    __syncwarp();
+    // pad and bitonic-sort the candidate keys
+    uint32_t m = 1;
+    while (m < n) m <<= 1;
+    for (uint32_t e = n + lane; e < m; e += 32) cand[warp][e] = ~0ull;
+    __syncwarp();
+    uint64_t* kk = cand[warp];
+    for (uint32_t size = 2; size <= m; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = lane; i < m / 2; i += 32) {
+                const uint32_t lo_i = 2 * i - (i & (stride - 1)), hi_i = lo_i + stride;
+                const bool up = (lo_i & size) == 0;
+                const uint64_t x = kk[lo_i], y = kk[hi_i];
+                if ((x > y) == up) { kk[lo_i] = y; kk[hi_i] = x; }
+            }
+            __syncwarp();
+        }
+    for (uint32_t i = lane; i < n_probe; i += 32) probes[(size_t)qi * n_probe + i] = kk[i];
+}
+
 }  // namespace
 
 cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
@@ -270,8 +412,12 @@ cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float
                                                                              cnorm, qnorm);
     dim3 grid((n_cen + kCC - 1) / kCC, (nq + kCQ - 1) / kCQ);
     coarse_tc_kernel<<<grid, 256, 0, s>>>(centroids, n_cen, queries, nq, dim, cnorm, qnorm, pt);
-    coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe,
-                                                      probes, overflow);
+    if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap)
+        coarse_select_fast_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
+            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow);
+    else
+        coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim,
+                                                          n_probe, probes, overflow);
     return cudaGetLastError();
 }
 
