@@ -319,6 +319,10 @@ struct dade_gpu_ctx {
     uint32_t surv_cap_hint = 0;
     uint32_t surv_cap_used = 0;     // worklist capacity of the last streaming search (0: none)
     uint32_t* h_flags = nullptr;    // pinned [2]: surv_max, coarse overflow of the last search
+    cudaStream_t copy_stream = nullptr;  // H2D of host query chunks (overlapped with rotation / coarse)
+    cudaEvent_t copy_ev[9] = {};
+    uint32_t stage_n_probe = 0;     // > 0: stage_queries may also coarse-rank the chunks (IVF)
+    bool probes_ready = false;      // probes of this search already computed per chunk
     DevBuf counters, phase;
     TmapCache tm_centroids, tm_storage, tm_base;
     TmapCache tm32_storage{32}, tm32_base{32};
@@ -368,6 +372,35 @@ void set_tables(dade_gpu_ctx* c, uint32_t kind, uint32_t dim, std::vector<uint32
     c->has_strategy = true;
 }
 
+bool coarse_tc_ok(dade_gpu_ctx* c, uint32_t n_probe) {
+    return n_probe <= 256 && !c->coarse_force_exact && !env_flag("DADE_GPU_NO_TC_COARSE");
+}
+uint32_t coarse_tc_chunk(dade_gpu_ctx* c, uint32_t nq) {
+    return (uint32_t)std::max<uint64_t>(64, std::min<uint64_t>(std::max<uint32_t>(nq, 1),
+                                                               (256ull << 20) / (8ull * c->n_clusters)));
+}
+// buffers for queries [0, nq) in chunks of coarse_tc_chunk(); overflow flag reset
+void coarse_tc_begin(dade_gpu_ctx* c, uint32_t nq) {
+    const uint32_t chunk = coarse_tc_chunk(c, nq);
+    c->probes.ensure((size_t)std::max<uint32_t>(nq, 1) * 256 * 8);
+    c->probe_count.ensure((size_t)std::max<uint32_t>(nq, 1) * 4);
+    c->cnorm.ensure((size_t)c->n_clusters * 4);
+    c->qnorm.ensure((size_t)chunk * 4);
+    c->coarse_lo.ensure((size_t)chunk * c->n_clusters * 4);
+    c->coarse_overflow.ensure(4);
+    cuda_check(cudaMemsetAsync(c->coarse_overflow.p, 0, 4, c->stream), "memset");
+    c->coarse_tc_used = true;
+}
+// queries [q0, q0 + m) (m <= coarse_tc_chunk) -> probes rows [q0, q0 + m)
+void coarse_tc_range(dade_gpu_ctx* c, const float* d_q, uint32_t q0, uint32_t m, uint32_t n_probe) {
+    cuda_check(launch_coarse_tc(c->centroids.as<float>(), c->n_clusters, d_q + (size_t)q0 * c->dim, m, c->dim, n_probe,
+                                c->cnorm.as<float>(), c->qnorm.as<float>(), c->coarse_lo.as<float>(),
+                                c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
+                                c->coarse_overflow.as<uint32_t>(), c->stream),
+               "coarse tc");
+    c->launches += 4;
+}
+
 // Coarse ranking (K2): exact l2_sq to every centroid, K = n_probe smallest by
 // (dist^2, cluster id) (proj/src/ivf.cpp:215-219), as a flat FD scan in
 // squared-distance key space.
@@ -375,27 +408,13 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
     cudaStream_t s = c->stream;
     c->probes.ensure((size_t)nq * n_probe * 8);
     c->probe_count.ensure((size_t)nq * 4);
-    if (n_probe <= 256 && !c->coarse_force_exact && !env_flag("DADE_GPU_NO_TC_COARSE")) {
+    if (coarse_tc_ok(c, n_probe)) {
         // tensor-core p~ for all (query, centroid) pairs + exact l2_sq on the
         // boundary candidates (coarse.cu); query chunks bound the p~ buffers
-        const uint32_t chunk = (uint32_t)std::max<uint64_t>(
-            64, std::min<uint64_t>(nq, (256ull << 20) / (8ull * c->n_clusters)));
-        c->cnorm.ensure((size_t)c->n_clusters * 4);
-        c->qnorm.ensure((size_t)chunk * 4);
-        c->coarse_lo.ensure((size_t)chunk * c->n_clusters * 4);
-        c->coarse_overflow.ensure(4);
-        cuda_check(cudaMemsetAsync(c->coarse_overflow.p, 0, 4, s), "memset");
-        for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
-            const uint32_t m = std::min(chunk, nq - q0);
-            cuda_check(launch_coarse_tc(c->centroids.as<float>(), c->n_clusters, d_q + (size_t)q0 * c->dim, m, c->dim,
-                                        n_probe, c->cnorm.as<float>(), c->qnorm.as<float>(),
-                                        c->coarse_lo.as<float>(),
-                                        c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
-                                        c->coarse_overflow.as<uint32_t>(), s),
-                       "coarse tc");
-            c->launches += 4;
-        }
-        c->coarse_tc_used = true;
+        coarse_tc_begin(c, nq);
+        const uint32_t chunk = coarse_tc_chunk(c, nq);
+        for (uint32_t q0 = 0; q0 < nq; q0 += chunk)
+            coarse_tc_range(c, d_q, q0, std::min(chunk, nq - q0), n_probe);
         return;
     }
     c->coarse_tc_used = false;
@@ -698,7 +717,8 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
 void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint32_t n_probe,
                        uint64_t* out_keys, uint32_t* out_count) {
     cudaStream_t s = c->stream;
-    coarse_rank(c, d_q, nq, n_probe);
+    if (!c->probes_ready) coarse_rank(c, d_q, nq, n_probe);
+    c->probes_ready = false;
     // K3 grouping
     GroupArgs g{};
     g.probes = c->probes.as<uint64_t>();
@@ -876,9 +896,52 @@ void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t
 }
 
 // Query staging shared by the two searches: H2D (host path) and rotation.
+// Raw host queries: H2D in chunks on the copy stream; each chunk is rotated (and
+// for IVF searches coarse-ranked) on the compute stream as soon as it lands, so
+// the PCIe transfer hides behind those per-query stages.
+const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t dim) {
+    const size_t bytes = (size_t)nq * dim * 4;
+    c->q_in.ensure(bytes);
+    c->q_rot.ensure(bytes);
+    if (!c->copy_stream) {
+        cuda_check(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "stream");
+        for (cudaEvent_t& e : c->copy_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    const uint32_t n_probe = c->stage_n_probe;
+    const bool coarse = n_probe && c->has_ivf && dim == c->dim && coarse_tc_ok(c, n_probe);
+    uint32_t nch = std::min<uint32_t>(4, (nq + 1023) / 1024);
+    uint32_t per = (nq + nch - 1) / nch;
+    if (coarse) per = std::min(per, coarse_tc_chunk(c, nq));
+    nch = (nq + per - 1) / per;
+    if (nch > 8) return nullptr;
+    // the copy stream must not overwrite q_in while earlier work on the stream reads it
+    cuda_check(cudaEventRecord(c->copy_ev[8], c->stream), "event");
+    cuda_check(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[8], 0), "wait");
+    if (coarse) coarse_tc_begin(c, nq);
+    for (uint32_t i = 0; i < nch; ++i) {
+        const uint32_t q0 = i * per, m = std::min(per, nq - q0);
+        cuda_check(cudaMemcpyAsync(c->q_in.as<float>() + (size_t)q0 * dim, queries + (size_t)q0 * dim,
+                                   (size_t)m * dim * 4, cudaMemcpyHostToDevice, c->copy_stream),
+                   "H2D queries");
+        cuda_check(cudaEventRecord(c->copy_ev[i], c->copy_stream), "event");
+        cuda_check(cudaStreamWaitEvent(c->stream, c->copy_ev[i], 0), "wait");
+        cuda_check(launch_rotate(c->W.as<double>(), dim, c->q_in.as<float>() + (size_t)q0 * dim, m,
+                                 c->q_rot.as<float>() + (size_t)q0 * dim, c->stream),
+                   "rotate");
+        ++c->launches;
+        if (coarse) coarse_tc_range(c, c->q_rot.as<float>(), q0, m, n_probe);
+    }
+    c->probes_ready = coarse;
+    return c->q_rot.as<float>();
+}
+
 const float* stage_queries(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t dim,
                            uint32_t flags) {
     const size_t bytes = (size_t)nq * dim * 4;
+    c->probes_ready = false;
+    if (!(flags & DADE_GPU_DEVICE_PTRS) && (flags & DADE_GPU_QUERIES_RAW) && c->t_dim == dim && nq >= 2048 &&
+        !env_flag("DADE_GPU_NO_OVERLAP"))
+        if (const float* d = stage_queries_overlapped(c, queries, nq, dim)) return d;
     const float* d_in = queries;
     if (!(flags & DADE_GPU_DEVICE_PTRS)) {
         c->q_in.ensure(bytes);
@@ -1028,6 +1091,12 @@ int dade_gpu_destroy(dade_gpu_ctx* c) {
         cudaStreamSynchronize(c->stream);
         if (c->h_flags) cudaFreeHost(c->h_flags);
         c->h_flags = nullptr;
+        if (c->copy_stream) {
+            cudaStreamSynchronize(c->copy_stream);
+            for (cudaEvent_t e : c->copy_ev) cudaEventDestroy(e);
+            cudaStreamDestroy(c->copy_stream);
+            c->copy_stream = nullptr;
+        }
         c->norms_storage.buf.release();
         c->aug_storage.buf.release();
         c->aug_storage.rows = nullptr;
@@ -1311,10 +1380,17 @@ int dade_gpu_ivf_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint
     return guarded([&] {
         check_ivf_args(c, k, n_probe);
         if (nq && (!queries || !out_ids || !out_dists)) fail(DADE_GPU_INVALID_INPUT, "ivf_search: null argument");
-        search_common(c, queries, nq, c->dim, k, flags, out_ids, out_dists, out_counts, stats,
-                      [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
-                          ivf_search_device(c, d_q, nq, k, n_probe, ok, oc);
-                      });
+        c->stage_n_probe = n_probe;
+        try {
+            search_common(c, queries, nq, c->dim, k, flags, out_ids, out_dists, out_counts, stats,
+                          [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
+                              ivf_search_device(c, d_q, nq, k, n_probe, ok, oc);
+                          });
+        } catch (...) {
+            c->stage_n_probe = 0;
+            throw;
+        }
+        c->stage_n_probe = 0;
     });
 }
 
