@@ -592,7 +592,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         cuda_check(cudaMemsetAsync(c->surv_max.p, 0, 4, s), "memset");
         cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
         if (seed.on) {
-            if (g && g->n_rb >= 1 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
+            if (g && g->n_rb >= 1 && k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->n_lists,
                                                     nq / kSeedGroup + g->n_lists + 1, seed.offsets, rows, a.row_ids, a.dim,
                                                     d_q, k, seed_rows(k), a.r_global, out_keys, out_count, s),

@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
 // sums with packed f32x2 arithmetic (two queries per instruction, same
 // rounding as sq_step); then one warp per query sorts its S keys. Same output
 // as seed_radius_kernel. Requires dim % 4 == 0 (the streaming path's rule).
-constexpr int kSeedSlice = 16;                 // dims per staged slice
+constexpr int kSeedSlice = 8;                  // dims per staged slice (48 KB double buffer: 4 CTAs / SM)
 constexpr int kSeedRS = kSeedSlice + 4;        // padded row stride (floats): conflict-free LDS.128
 constexpr int kSeedTileF = kSeedMax * kSeedRS; // floats per tile buffer
 
@@ -511,7 +511,8 @@ __device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* a
         float* tb = tile + buf * kSeedTileF;
 #pragma unroll
         for (int i = 0; i < (kSeedMax * kSeedSlice / 4) / kSeedThreads; ++i) {
-            const uint32_t idx = tid + i * kSeedThreads, row = idx >> 2, c4 = idx & 3;
+            constexpr uint32_t kCh = kSeedSlice / 4;  // 16-byte chunks per row slice
+            const uint32_t idx = tid + i * kSeedThreads, row = idx / kCh, c4 = idx % kCh;
             if (!kTwo && row >= (uint32_t)kSeedThreads) break;  // rows (t + 256) unused
             const bool ok = row < n && k0 + 4 * c4 < dim;
             const float* src = storage + (size_t)(start + (ok ? row : 0)) * dim + (ok ? k0 + 4 * c4 : 0);
@@ -550,12 +551,19 @@ __device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* a
             const float o1[4] = {x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const uint64_t* q2 = reinterpret_cast<const uint64_t*>(qb + (4 * c + e) * kSeedGroup);
+                // query pairs of this dim, two per 16-byte load (the queries are broadcast)
+                const ulonglong2* q4 = reinterpret_cast<const ulonglong2*>(qb + (4 * c + e) * kSeedGroup);
+                uint64_t qp[G / 2 + 1];
+#pragma unroll
+                for (int p = 0; p < G / 2; p += 2) {
+                    const ulonglong2 v = q4[p / 2];
+                    qp[p] = v.x;
+                    qp[p + 1] = v.y;
+                }
 #pragma unroll
                 for (int p = 0; p < G / 2; ++p) {
-                    const uint64_t qq = q2[p];
-                    acc0[p] = sq_step2(acc0[p], o0[e], qq, nz2);
-                    if (kTwo) acc1[p] = sq_step2(acc1[p], o1[e], qq, nz2);
+                    acc0[p] = sq_step2(acc0[p], o0[e], qp[p], nz2);
+                    if (kTwo) acc1[p] = sq_step2(acc1[p], o1[e], qp[p], nz2);
                 }
             }
         }
@@ -595,14 +603,8 @@ constexpr int kSeedSmall = 128;  // sorted slots when the K-th distance has few 
 // K-th smallest (1-based) of the first n sqrt(acc) values as float bits
 // (positive floats order like their bits): warp radix select, 8 bits per
 // pass, histogram in shared memory. Requires K <= n <= kSeedMax.
-__device__ __forceinline__ uint32_t seed_select(const float* acc, uint32_t n, uint32_t K, uint32_t* hist,
-                                                uint32_t lane) {
-    uint32_t v[kSeedMax / 32];
-#pragma unroll
-    for (int i = 0; i < kSeedMax / 32; ++i) {
-        const uint32_t r = lane + 32u * i;
-        v[i] = r < n ? __float_as_uint(__fsqrt_rn(acc[r])) : 0xffffffffu;
-    }
+__device__ __forceinline__ uint32_t warp_select16(const uint32_t (&v)[kSeedMax / 32], uint32_t K, uint32_t* hist,
+                                                  uint32_t lane) {
     uint32_t prefix = 0, mask = 0, rem = K;
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (uint32_t j = lane; j < 256; j += 32) hist[j] = 0;
@@ -621,7 +623,7 @@ __device__ __forceinline__ uint32_t seed_select(const float* acc, uint32_t n, ui
     return prefix;
 }
 
-__global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
+__global__ void __launch_bounds__(kSeedThreads, 4) seed_radius_list_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ bucket_off, const uint32_t* __restrict__ bucket_q,
     const uint32_t* __restrict__ seed_goff, uint32_t n_lists, const uint32_t* __restrict__ list_offsets, const float* __restrict__ storage,
     const uint32_t* __restrict__ row_ids, uint32_t dim, const float* __restrict__ queries, uint32_t K, uint32_t S,
@@ -631,7 +633,7 @@ __global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
     float* qt = tile + 2 * kSeedTileF;                                  // [2][kSeedSlice][kSeedGroup]
     // after the last slice the tile's space is reused: sums, then sort keys
     float* accs = tile;                                                 // [kSeedGroup][kSeedMax]
-    uint64_t* keys = reinterpret_cast<uint64_t*>(tile + kSeedGroup * kSeedMax);  // [8 warps][kSeedMax], then hist [8][256]
+    uint64_t* keys = reinterpret_cast<uint64_t*>(tile + kSeedGroup * kSeedMax);  // [8 warps][kSeedSmall], then hist [8][256]
     // CTA -> (list, group): binary search in the per-list group prefix
     const uint32_t b = blockIdx.x;
     if (b >= seed_goff[n_lists]) return;
@@ -663,34 +665,53 @@ __global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
     }
     for (uint32_t u = warp; u < ng; u += kSeedThreads / 32) {  // one warp per query: K-th distance, sorted top-K keys
         const uint32_t q = qs[u];
-        uint64_t* kk = keys + warp * kSeedMax;
-        uint32_t* hist = reinterpret_cast<uint32_t*>(keys + (kSeedThreads / 32) * kSeedMax) + warp * 256;
+        uint64_t* kk = keys + warp * kSeedSmall;
+        uint32_t* hist = reinterpret_cast<uint32_t*>(keys + (kSeedThreads / 32) * kSeedSmall) + warp * 256;
         const float* acc = accs + u * kSeedMax;
-        const uint32_t T = seed_select(acc, n, K, hist, lane);
-        // keys of the rows with dist <= T (>= K of them): usually few, sorted
-        // in a 128-slot bitonic; a tie-heavy list falls back to all S rows
+        // dist bits of this lane's rows (positive floats order like their bits)
+        uint32_t dv[kSeedMax / 32];
+#pragma unroll
+        for (int i = 0; i < kSeedMax / 32; ++i) {
+            const uint32_t r = lane + 32u * i;
+            dv[i] = r < n ? __float_as_uint(__fsqrt_rn(acc[r])) : 0xffffffffu;
+        }
+        const uint32_t T = warp_select16(dv, K, hist, lane);  // K-th smallest distance
+        // the K best keys: every dist < T, then ties at T by ascending id (the
+        // (K - #lt)-th smallest id among them, by the same select) -> exactly K <= 128
+        uint32_t c_lt = 0, c_eq = 0;
+#pragma unroll
+        for (int i = 0; i < kSeedMax / 32; ++i) {
+            c_lt += __popc(__ballot_sync(0xffffffffu, dv[i] < T));
+            c_eq += __popc(__ballot_sync(0xffffffffu, dv[i] == T));
+        }
+        uint32_t tid_max = 0xffffffffu;  // ids at distance T taken: <= tid_max
+        if (c_lt + c_eq > (uint32_t)kSeedSmall) {
+            uint32_t iv[kSeedMax / 32];
+#pragma unroll
+            for (int i = 0; i < kSeedMax / 32; ++i) {
+                const uint32_t r = lane + 32u * i;
+                iv[i] = dv[i] == T ? (row_ids ? __ldg(row_ids + start + r) : start + r) : 0xffffffffu;
+            }
+            tid_max = warp_select16(iv, K - c_lt, hist, lane);
+        }
         uint32_t c = 0;
 #pragma unroll
         for (int i = 0; i < kSeedMax / 32; ++i) {
             const uint32_t r = lane + 32u * i;
-            const float dv = r < n ? __fsqrt_rn(acc[r]) : 0.f;
-            const bool take = r < n && __float_as_uint(dv) <= T;
+            bool take = dv[i] < T;
+            uint32_t id = 0;
+            if (dv[i] <= T) {
+                id = row_ids ? __ldg(row_ids + start + r) : start + r;
+                take = take || (dv[i] == T && id <= tid_max);
+            }
             const uint32_t bal = __ballot_sync(0xffffffffu, take);
             const uint32_t pos = c + __popc(bal & ((1u << lane) - 1u));
-            if (take && pos < (uint32_t)kSeedSmall)
-                kk[pos] = make_key(dv, row_ids ? __ldg(row_ids + start + r) : start + r);
+            if (take && pos < (uint32_t)kSeedSmall) kk[pos] = make_key(__uint_as_float(dv[i]), id);
             c += __popc(bal);
         }
-        uint32_t m = kSeedSmall;
-        if (c > (uint32_t)kSeedSmall) {
-            m = kSeedMax;
-            for (uint32_t r = lane; r < (uint32_t)kSeedMax; r += 32)
-                kk[r] = r < n ? make_key(__fsqrt_rn(acc[r]), row_ids ? __ldg(row_ids + start + r) : start + r) : ~0ull;
-        } else {
-            for (uint32_t r = c + lane; r < (uint32_t)kSeedSmall; r += 32) kk[r] = ~0ull;
-        }
+        for (uint32_t r = c + lane; r < (uint32_t)kSeedSmall; r += 32) kk[r] = ~0ull;
         __syncwarp();
-        warp_bitonic_sort(kk, m, lane);
+        warp_bitonic_sort(kk, kSeedSmall, lane);
         if (lane == 0) atomicMin(r_global + q, (uint32_t)(kk[K - 1] >> 32));
         if (out_keys) {
             for (uint32_t i = lane; i < K; i += 32) out_keys[(size_t)q * K + i] = kk[i];
@@ -725,11 +746,11 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
                                      const uint32_t* row_ids, uint32_t dim, const float* queries, uint32_t K,
                                      uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
                                      cudaStream_t s) {
-    if (n_lists == 0 || K > (uint32_t)kSeedMax) return cudaSuccess;
-    // double-buffered tile + query slices; sums [8][S] and keys [8][S] alias the tile
+    if (n_lists == 0 || K > (uint32_t)kSeedSmall) return cudaErrorInvalidValue;  // caller: K <= kSeedListMaxK
+    // double-buffered tile + query slices; sums [16][S], keys [8][128] and histograms alias the tile
     const size_t smem = sizeof(float) * (2 * kSeedTileF + 2 * kSeedSlice * kSeedGroup);
     static_assert(sizeof(float) * 2 * kSeedTileF >=
-                      sizeof(float) * kSeedGroup * kSeedMax + (sizeof(uint64_t) * kSeedMax + sizeof(uint32_t) * 256) * (kSeedThreads / 32),
+                      sizeof(float) * kSeedGroup * kSeedMax + (sizeof(uint64_t) * kSeedSmall + sizeof(uint32_t) * 256) * (kSeedThreads / 32),
                   "seed sums + keys + histograms must fit in the tile");
     DADE_CUDA_TRY(cudaFuncSetAttribute(seed_radius_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     seed_radius_list_kernel<<<max_groups, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, seed_goff, n_lists,
