@@ -474,12 +474,15 @@ uint32_t rank0_item_rows(bool umma) {
     r = std::max<uint32_t>(32, std::min<uint32_t>(r, kFilterItemRows));
     return r;
 }
-constexpr uint32_t kSeedRowsDefault = 512;  // rows of the nearest list used by the radius seed
+constexpr uint32_t kSeedRowsDefault = 1024;  // rows of the nearest list used by the radius seed
 
+// rows of each nearest list the radius seed scores exactly (and the scan then
+// skips): the list-major kernel (K <= 128) takes up to 1024, the per-query one 512
 uint32_t seed_rows(uint32_t k) {
+    const bool list_kernel = k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY");
     uint32_t s = kSeedRowsDefault;
     if (const char* e = std::getenv("DADE_GPU_SEED_ROWS")) s = (uint32_t)std::atoi(e);
-    return std::min<uint32_t>(512, std::max<uint32_t>(s, k));
+    return std::min<uint32_t>(list_kernel ? 1024 : 512, std::max<uint32_t>(s, k));
 }
 
 bool seed_disabled() {

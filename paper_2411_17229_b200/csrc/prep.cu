@@ -480,9 +480,10 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
 // sums with packed f32x2 arithmetic (two queries per instruction, same
 // rounding as sq_step); then one warp per query sorts its S keys. Same output
 // as seed_radius_kernel. Requires dim % 4 == 0 (the streaming path's rule).
-constexpr int kSeedSlice = 8;                  // dims per staged slice (48 KB double buffer: 4 CTAs / SM)
+constexpr int kSeedListMax = 1024;             // rows per list seed (up to 4 per thread)
+constexpr int kSeedSlice = 8;                  // dims per staged slice
 constexpr int kSeedRS = kSeedSlice + 4;        // padded row stride (floats): conflict-free LDS.128
-constexpr int kSeedTileF = kSeedMax * kSeedRS; // floats per tile buffer
+constexpr int kSeedTileF = kSeedListMax * kSeedRS; // floats per tile buffer
 
 __device__ __forceinline__ void cp_async16_s(void* dst, const void* src, bool pred) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
@@ -498,22 +499,20 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// exact sums of rows (tid, tid + 256) x G queries over all dims -> accs[u][row]
-template <int G, bool kTwo>
+// exact sums of rows (tid + 256 j, j < kR) x G queries over all dims -> accs[u][row]
+template <int G, int kR>
 __device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* accs, const float* storage,
                                                 uint32_t start, uint32_t n, uint32_t dim, const float* queries,
                                                 const uint32_t* qs, uint32_t ng, uint64_t nz2) {
     const uint32_t tid = threadIdx.x;
-    const uint32_t r0 = tid, r1 = tid + kSeedThreads;
     const uint32_t n_slices = (dim + kSeedSlice - 1) / kSeedSlice;
     auto issue = [&](uint32_t sl, uint32_t buf) {
         const uint32_t k0 = sl * kSeedSlice;
         float* tb = tile + buf * kSeedTileF;
+        constexpr uint32_t kCh = kSeedSlice / 4;  // 16-byte chunks per row slice
 #pragma unroll
-        for (int i = 0; i < (kSeedMax * kSeedSlice / 4) / kSeedThreads; ++i) {
-            constexpr uint32_t kCh = kSeedSlice / 4;  // 16-byte chunks per row slice
+        for (int i = 0; i < (kR * kSeedThreads * (int)kCh) / kSeedThreads; ++i) {
             const uint32_t idx = tid + i * kSeedThreads, row = idx / kCh, c4 = idx % kCh;
-            if (!kTwo && row >= (uint32_t)kSeedThreads) break;  // rows (t + 256) unused
             const bool ok = row < n && k0 + 4 * c4 < dim;
             const float* src = storage + (size_t)(start + (ok ? row : 0)) * dim + (ok ? k0 + 4 * c4 : 0);
             cp_async16_s(tb + row * kSeedRS + 4 * c4, src, ok);
@@ -527,9 +526,11 @@ __device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* a
         }
         cp_async_commit();
     };
-    uint64_t acc0[G / 2], acc1[G / 2];
+    uint64_t acc[kR][G / 2];
 #pragma unroll
-    for (int p = 0; p < G / 2; ++p) acc0[p] = acc1[p] = 0ull;
+    for (int j = 0; j < kR; ++j)
+#pragma unroll
+        for (int p = 0; p < G / 2; ++p) acc[j][p] = 0ull;
     issue(0, 0);
     for (uint32_t sl = 0; sl < n_slices; ++sl) {
         const uint32_t buf = sl & 1;
@@ -544,11 +545,15 @@ __device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* a
         const float* qb = qt + buf * kSeedSlice * kSeedGroup;
 #pragma unroll
         for (int c = 0; c < kSeedSlice / 4; ++c) {
-            const float4 x0 = *reinterpret_cast<const float4*>(tb + r0 * kSeedRS + 4 * c);
-            const float4 x1 = kTwo ? *reinterpret_cast<const float4*>(tb + r1 * kSeedRS + 4 * c)
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-            const float o0[4] = {x0.x, x0.y, x0.z, x0.w};
-            const float o1[4] = {x1.x, x1.y, x1.z, x1.w};
+            float o[kR][4];
+#pragma unroll
+            for (int j = 0; j < kR; ++j) {
+                const float4 x = *reinterpret_cast<const float4*>(tb + (tid + j * kSeedThreads) * kSeedRS + 4 * c);
+                o[j][0] = x.x;
+                o[j][1] = x.y;
+                o[j][2] = x.z;
+                o[j][3] = x.w;
+            }
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 // query pairs of this dim, two per 16-byte load (the queries are broadcast)
@@ -561,21 +566,21 @@ __device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* a
                     qp[p + 1] = v.y;
                 }
 #pragma unroll
-                for (int p = 0; p < G / 2; ++p) {
-                    acc0[p] = sq_step2(acc0[p], o0[e], qp[p], nz2);
-                    if (kTwo) acc1[p] = sq_step2(acc1[p], o1[e], qp[p], nz2);
-                }
+                for (int j = 0; j < kR; ++j)
+#pragma unroll
+                    for (int p = 0; p < G / 2; ++p) acc[j][p] = sq_step2(acc[j][p], o[j][e], qp[p], nz2);
             }
         }
         __syncthreads();  // buffer free for the slice after next
     }
 #pragma unroll
-    for (int p = 0; p < G / 2; ++p) {
-        accs[(2 * p) * kSeedMax + r0] = lo_f(acc0[p]);
-        accs[(2 * p + 1) * kSeedMax + r0] = hi_f(acc0[p]);
-        accs[(2 * p) * kSeedMax + r1] = lo_f(acc1[p]);
-        accs[(2 * p + 1) * kSeedMax + r1] = hi_f(acc1[p]);
-    }
+    for (int j = 0; j < kR; ++j)
+#pragma unroll
+        for (int p = 0; p < G / 2; ++p) {
+            const uint32_t r = tid + j * kSeedThreads;
+            accs[(2 * p) * kSeedListMax + r] = lo_f(acc[j][p]);
+            accs[(2 * p + 1) * kSeedListMax + r] = hi_f(acc[j][p]);
+        }
     __syncthreads();
 }
 
@@ -603,14 +608,15 @@ constexpr int kSeedSmall = 128;  // sorted slots when the K-th distance has few 
 // K-th smallest (1-based) of the first n sqrt(acc) values as float bits
 // (positive floats order like their bits): warp radix select, 8 bits per
 // pass, histogram in shared memory. Requires K <= n <= kSeedMax.
-__device__ __forceinline__ uint32_t warp_select16(const uint32_t (&v)[kSeedMax / 32], uint32_t K, uint32_t* hist,
-                                                  uint32_t lane) {
+template <int NV>
+__device__ __forceinline__ uint32_t warp_select_regs(const uint32_t (&v)[NV], uint32_t K, uint32_t* hist,
+                                                     uint32_t lane) {
     uint32_t prefix = 0, mask = 0, rem = K;
     for (int shift = 24; shift >= 0; shift -= 8) {
         for (uint32_t j = lane; j < 256; j += 32) hist[j] = 0;
         __syncwarp();
 #pragma unroll
-        for (int i = 0; i < kSeedMax / 32; ++i)
+        for (int i = 0; i < NV; ++i)
             if ((v[i] & mask) == prefix) atomicAdd(&hist[(v[i] >> shift) & 0xffu], 1u);
         __syncwarp();
         uint32_t d, before;
@@ -623,7 +629,7 @@ __device__ __forceinline__ uint32_t warp_select16(const uint32_t (&v)[kSeedMax /
     return prefix;
 }
 
-__global__ void __launch_bounds__(kSeedThreads, 4) seed_radius_list_kernel(
+__global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ bucket_off, const uint32_t* __restrict__ bucket_q,
     const uint32_t* __restrict__ seed_goff, uint32_t n_lists, const uint32_t* __restrict__ list_offsets, const float* __restrict__ storage,
     const uint32_t* __restrict__ row_ids, uint32_t dim, const float* __restrict__ queries, uint32_t K, uint32_t S,
@@ -632,8 +638,8 @@ __global__ void __launch_bounds__(kSeedThreads, 4) seed_radius_list_kernel(
     float* tile = reinterpret_cast<float*>(seed_smem);                  // [2][kSeedMax][kSeedRS]
     float* qt = tile + 2 * kSeedTileF;                                  // [2][kSeedSlice][kSeedGroup]
     // after the last slice the tile's space is reused: sums, then sort keys
-    float* accs = tile;                                                 // [kSeedGroup][kSeedMax]
-    uint64_t* keys = reinterpret_cast<uint64_t*>(tile + kSeedGroup * kSeedMax);  // [8 warps][kSeedSmall], then hist [8][256]
+    float* accs = tile;                                                 // [kSeedGroup][kSeedListMax]
+    uint64_t* keys = reinterpret_cast<uint64_t*>(tile + kSeedGroup * kSeedListMax);  // [8 warps][kSeedSmall], then hist [8][256]
     // CTA -> (list, group): binary search in the per-list group prefix
     const uint32_t b = blockIdx.x;
     if (b >= seed_goff[n_lists]) return;
@@ -652,13 +658,16 @@ __global__ void __launch_bounds__(kSeedThreads, 4) seed_radius_list_kernel(
     const uint32_t* qs = bucket_q + bucket_off[list] + g0;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t ng = min((uint32_t)kSeedGroup, cnt_all - g0);
+    const int rsel = n > 2u * kSeedThreads ? 4 : n > (uint32_t)kSeedThreads ? 2 : 1;
     switch ((ng + 1) >> 1) {  // G = ng rounded up to even: no padded query pairs beyond one
 #define SEED_G(P)                                                                                      \
     case P:                                                                                            \
-        if (n > (uint32_t)kSeedThreads)                                                                \
-            seed_group_sums<2 * P, true>(tile, qt, accs, storage, start, n, dim, queries, qs, ng, nz2); \
+        if (rsel == 4)                                                                                 \
+            seed_group_sums<2 * P, 4>(tile, qt, accs, storage, start, n, dim, queries, qs, ng, nz2);   \
+        else if (rsel == 2)                                                                            \
+            seed_group_sums<2 * P, 2>(tile, qt, accs, storage, start, n, dim, queries, qs, ng, nz2);   \
         else                                                                                           \
-            seed_group_sums<2 * P, false>(tile, qt, accs, storage, start, n, dim, queries, qs, ng, nz2); \
+            seed_group_sums<2 * P, 1>(tile, qt, accs, storage, start, n, dim, queries, qs, ng, nz2);   \
         break;
         SEED_G(1) SEED_G(2) SEED_G(3) SEED_G(4) SEED_G(5) SEED_G(6) SEED_G(7) default: SEED_G(8)
 #undef SEED_G
@@ -667,36 +676,37 @@ __global__ void __launch_bounds__(kSeedThreads, 4) seed_radius_list_kernel(
         const uint32_t q = qs[u];
         uint64_t* kk = keys + warp * kSeedSmall;
         uint32_t* hist = reinterpret_cast<uint32_t*>(keys + (kSeedThreads / 32) * kSeedSmall) + warp * 256;
-        const float* acc = accs + u * kSeedMax;
+        const float* acc = accs + u * kSeedListMax;
         // dist bits of this lane's rows (positive floats order like their bits)
-        uint32_t dv[kSeedMax / 32];
+        constexpr int kNV = kSeedListMax / 32;
+        uint32_t dv[kNV];
 #pragma unroll
-        for (int i = 0; i < kSeedMax / 32; ++i) {
+        for (int i = 0; i < kNV; ++i) {
             const uint32_t r = lane + 32u * i;
             dv[i] = r < n ? __float_as_uint(__fsqrt_rn(acc[r])) : 0xffffffffu;
         }
-        const uint32_t T = warp_select16(dv, K, hist, lane);  // K-th smallest distance
+        const uint32_t T = warp_select_regs(dv, K, hist, lane);  // K-th smallest distance
         // the K best keys: every dist < T, then ties at T by ascending id (the
         // (K - #lt)-th smallest id among them, by the same select) -> exactly K <= 128
         uint32_t c_lt = 0, c_eq = 0;
 #pragma unroll
-        for (int i = 0; i < kSeedMax / 32; ++i) {
+        for (int i = 0; i < kNV; ++i) {
             c_lt += __popc(__ballot_sync(0xffffffffu, dv[i] < T));
             c_eq += __popc(__ballot_sync(0xffffffffu, dv[i] == T));
         }
         uint32_t tid_max = 0xffffffffu;  // ids at distance T taken: <= tid_max
         if (c_lt + c_eq > (uint32_t)kSeedSmall) {
-            uint32_t iv[kSeedMax / 32];
+            uint32_t iv[kNV];
 #pragma unroll
-            for (int i = 0; i < kSeedMax / 32; ++i) {
+            for (int i = 0; i < kNV; ++i) {
                 const uint32_t r = lane + 32u * i;
                 iv[i] = dv[i] == T ? (row_ids ? __ldg(row_ids + start + r) : start + r) : 0xffffffffu;
             }
-            tid_max = warp_select16(iv, K - c_lt, hist, lane);
+            tid_max = warp_select_regs(iv, K - c_lt, hist, lane);
         }
         uint32_t c = 0;
 #pragma unroll
-        for (int i = 0; i < kSeedMax / 32; ++i) {
+        for (int i = 0; i < kNV; ++i) {
             const uint32_t r = lane + 32u * i;
             bool take = dv[i] < T;
             uint32_t id = 0;
@@ -750,13 +760,13 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
     // double-buffered tile + query slices; sums [16][S], keys [8][128] and histograms alias the tile
     const size_t smem = sizeof(float) * (2 * kSeedTileF + 2 * kSeedSlice * kSeedGroup);
     static_assert(sizeof(float) * 2 * kSeedTileF >=
-                      sizeof(float) * kSeedGroup * kSeedMax + (sizeof(uint64_t) * kSeedSmall + sizeof(uint32_t) * 256) * (kSeedThreads / 32),
+                      sizeof(float) * kSeedGroup * kSeedListMax + (sizeof(uint64_t) * kSeedSmall + sizeof(uint32_t) * 256) * (kSeedThreads / 32),
                   "seed sums + keys + histograms must fit in the tile");
     DADE_CUDA_TRY(cudaFuncSetAttribute(seed_radius_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     seed_radius_list_kernel<<<max_groups, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, seed_goff, n_lists,
                                                                     list_offsets,
                                                                  storage, row_ids, dim, queries, K,
-                                                                 std::min<uint32_t>(S, kSeedMax), r_global, out_keys,
+                                                                 std::min<uint32_t>(S, kSeedListMax), r_global, out_keys,
                                                                  out_count, 0x8000000080000000ull);
     return cudaGetLastError();
 }
