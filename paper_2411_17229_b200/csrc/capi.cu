@@ -312,7 +312,7 @@ struct dade_gpu_ctx {
     DevBuf q_in, q_rot, probes, probe_count, c_seg_keys, c_seg_count, c_r;
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
-    DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter, seed_goff;
+    DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter, seed_goff, seed_glist;
     DevBuf cnorm, qnorm, coarse_lo, coarse_overflow, q_norms;  // coarse_lo: p~ per (query, centroid)
     bool coarse_force_exact = false, coarse_tc_used = false;
     int n_sms = 148;
@@ -596,7 +596,8 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
         if (seed.on) {
             if (g && g->n_rb >= 1 && k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
-                cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->n_lists,
+                cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->seed_glist,
+                                                    g->n_lists,
                                                     nq / kSeedGroup + g->n_lists + 1, seed.offsets, rows, a.row_ids, a.dim,
                                                     d_q, k, seed_rows(k), a.r_global, out_keys, out_count, s),
                            "seed radius (lists)");
@@ -780,6 +781,8 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     g.n_items = c->n_items.as<uint32_t>();
     c->seed_goff.ensure(((size_t)c->n_clusters + 1) * 4);
     g.seed_goff = c->seed_goff.as<uint32_t>();
+    c->seed_glist.ensure(((size_t)nq / kSeedGroup + c->n_clusters + 1) * 4);
+    g.seed_glist = c->seed_glist.as<uint32_t>();
     cuda_check(launch_group(g, s), "group");
     c->launches += 4;
     // K4 scan

@@ -140,7 +140,8 @@ cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float
 // prep.cu
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s);
 cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* bucket_off, const uint32_t* bucket_q,
-                                     const uint32_t* seed_goff, uint32_t n_lists, uint32_t max_groups,
+                                     const uint32_t* seed_goff, const uint32_t* seed_glist, uint32_t n_lists,
+                                     uint32_t max_groups,
                                      const uint32_t* list_offsets, const float* storage,
                                      const uint32_t* row_ids, uint32_t dim, const float* queries, uint32_t K,
                                      uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
@@ -173,7 +174,8 @@ struct GroupArgs {
     uint32_t rank0_item_rows;       // row piece of rank-bucket-0 entries (0: max_item_rows)
     uint32_t q_chunk;               // queries per work item (kQC; 32 for the streaming filter)
     uint32_t seed_skip, seed_min;   // rank-0 lists of >= seed_min rows skip their first seed_skip rows
-    uint32_t* seed_goff;            // nullable [n_lists + 1]: prefix of ceil(rank-0 count / 8)
+    uint32_t* seed_goff;            // nullable [n_lists + 1]: prefix of ceil(rank-0 count / kSeedGroup)
+    uint32_t* seed_glist;           // nullable [seed groups]: the list of each seed group
 };
 cudaError_t launch_group(const GroupArgs& g, cudaStream_t s);
 

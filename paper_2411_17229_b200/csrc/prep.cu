@@ -230,7 +230,11 @@ __global__ void __launch_bounds__(1024) group_scan_kernel(const GroupArgs g) {
         const uint32_t c = g.counts[e];
         g.bucket_off[e] = rb;
         g.item_off[e] = ri;
-        if (g.seed_goff && e < g.n_lists) g.seed_goff[e] = rg;
+        if (g.seed_goff && e < g.n_lists) {
+            g.seed_goff[e] = rg;
+            if (g.seed_glist)
+                for (uint32_t j = 0; j < (c + kSeedGroup - 1) / kSeedGroup; ++j) g.seed_glist[rg + j] = e;
+        }
         rb += c;
         ri += entry_items(g, e, c);
         if (e < g.n_lists) rg += (c + kSeedGroup - 1) / kSeedGroup;
@@ -631,7 +635,8 @@ __device__ __forceinline__ uint32_t warp_select_regs(const uint32_t (&v)[NV], ui
 
 __global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ bucket_off, const uint32_t* __restrict__ bucket_q,
-    const uint32_t* __restrict__ seed_goff, uint32_t n_lists, const uint32_t* __restrict__ list_offsets, const float* __restrict__ storage,
+    const uint32_t* __restrict__ seed_goff, const uint32_t* __restrict__ seed_glist, uint32_t n_lists,
+    const uint32_t* __restrict__ list_offsets, const float* __restrict__ storage,
     const uint32_t* __restrict__ row_ids, uint32_t dim, const float* __restrict__ queries, uint32_t K, uint32_t S,
     uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count, uint64_t nz2) {
     extern __shared__ __align__(16) unsigned char seed_smem[];
@@ -643,12 +648,7 @@ __global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
     // CTA -> (list, group): binary search in the per-list group prefix
     const uint32_t b = blockIdx.x;
     if (b >= seed_goff[n_lists]) return;
-    uint32_t lo_l = 0, hi_l = n_lists;
-    while (hi_l - lo_l > 1) {
-        const uint32_t mid = (lo_l + hi_l) >> 1;
-        if (seed_goff[mid] <= b) lo_l = mid; else hi_l = mid;
-    }
-    const uint32_t list = lo_l;
+    const uint32_t list = seed_glist[b];
     const uint32_t cnt_all = counts[list];  // entry e = list of rank bucket 0
     const uint32_t g0 = (b - seed_goff[list]) * kSeedGroup;
     if (g0 >= cnt_all) return;
@@ -751,7 +751,8 @@ cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const u
 }
 
 cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* bucket_off, const uint32_t* bucket_q,
-                                     const uint32_t* seed_goff, uint32_t n_lists, uint32_t max_groups,
+                                     const uint32_t* seed_goff, const uint32_t* seed_glist, uint32_t n_lists,
+                                     uint32_t max_groups,
                                      const uint32_t* list_offsets, const float* storage,
                                      const uint32_t* row_ids, uint32_t dim, const float* queries, uint32_t K,
                                      uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
@@ -763,7 +764,8 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
                       sizeof(float) * kSeedGroup * kSeedListMax + (sizeof(uint64_t) * kSeedSmall + sizeof(uint32_t) * 256) * (kSeedThreads / 32),
                   "seed sums + keys + histograms must fit in the tile");
     DADE_CUDA_TRY(cudaFuncSetAttribute(seed_radius_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    seed_radius_list_kernel<<<max_groups, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, seed_goff, n_lists,
+    seed_radius_list_kernel<<<max_groups, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, seed_goff, seed_glist,
+                                                                    n_lists,
                                                                     list_offsets,
                                                                  storage, row_ids, dim, queries, K,
                                                                  std::min<uint32_t>(S, kSeedListMax), r_global, out_keys,
