@@ -8,6 +8,7 @@
 // so it is capturable in a CUDA graph; the host only synchronises when it has
 // to copy results or counters back.
 #include <algorithm>
+#include <utility>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -82,6 +83,20 @@ struct DevBuf {
         p = nullptr;
         cap = 0;
     }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf& operator=(DevBuf&& o) noexcept {  // takes o's allocation
+        if (this != &o) {
+            release();
+            p = o.p;
+            cap = o.cap;
+            o.p = nullptr;
+            o.cap = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }  // (dade_gpu_destroy frees while the device context is current)
 };
 
 // Checkpoint grid rule of CalibrationTable::expected_checkpoints
@@ -1240,8 +1255,8 @@ int dade_gpu_set_ivf_shard(dade_gpu_ctx* c, const uint8_t* mask) {
         cuda_check(cudaStreamSynchronize(c->stream), "shard");
         c->storage.release();
         c->ids.release();
-        c->storage = ns;
-        c->ids = ni;
+        c->storage = std::move(ns);
+        c->ids = std::move(ni);
         ns.p = nullptr;
         ni.p = nullptr;
         upload(c->offsets, dev.data(), (size_t)(nl + 1) * 4, c->stream);
