@@ -249,6 +249,44 @@ bool make_aug_tmap(CUtensorMap* m, const float* base, uint64_t rows, uint32_t bo
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Rows as {8 dims, 256 rows} 32B-swizzled TMA boxes (the radius seed's slices).
+bool make_slice_tmap(CUtensorMap* m, const float* base, uint64_t rows, uint32_t dim) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                    &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            encode = nullptr;
+        if (!encode) return false;
+    }
+    if (dim % 4 != 0 || rows == 0 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+    cuuint64_t gdim[2] = {dim, rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)dim * 4};
+    cuuint32_t box[2] = {8, 256};
+    cuuint32_t estride[2] = {1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct SliceTmap {
+    const float* base = nullptr;
+    uint64_t rows = 0;
+    uint32_t dim = 0;
+    bool ok = false;
+    CUtensorMap map{};
+    const CUtensorMap* get(const float* b, uint64_t r, uint32_t d) {
+        if (b != base || r != rows || d != dim) {
+            base = b;
+            rows = r;
+            dim = d;
+            ok = make_slice_tmap(&map, b, std::max<uint64_t>(r, 1), d);
+        }
+        return ok && !env_flag("DADE_GPU_NO_TMA") ? &map : nullptr;
+    }
+};
+
 struct RowAug {
     DevBuf buf;
     const float* rows = nullptr;
@@ -343,6 +381,7 @@ struct dade_gpu_ctx {
     TmapCache tm32_storage{32}, tm32_base{32};
     RowNorms norms_storage, norms_base;
     RowAug aug_storage;
+    SliceTmap seed_tm;
     CUtensorMap tm_none{};
 
     // profiling
@@ -610,7 +649,30 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         cuda_check(cudaMemsetAsync(c->surv_max.p, 0, 4, s), "memset");
         cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
         if (seed.on) {
-            if (g && g->n_rb >= 1 && k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
+            const CUtensorMap* stm = (g && k <= 128 && seed_tma_ok(a.dim, k) && !env_flag("DADE_GPU_SEED_V1") &&
+                                      !env_flag("DADE_GPU_SEED_PER_QUERY"))
+                                         ? c->seed_tm.get(rows, n_rows, a.dim)
+                                         : nullptr;
+            if (stm) {
+                SeedListArgs sa{};
+                sa.counts = g->counts;
+                sa.bucket_off = g->bucket_off;
+                sa.bucket_q = g->bucket_q;
+                sa.seed_goff = g->seed_goff;
+                sa.seed_glist = g->seed_glist;
+                sa.n_lists = g->n_lists;
+                sa.list_offsets = seed.offsets;
+                sa.row_ids = a.row_ids;
+                sa.dim = a.dim;
+                sa.K = k;
+                sa.S = std::min<uint32_t>(seed_rows(k), 1024);
+                sa.queries = d_q;
+                sa.r_global = a.r_global;
+                sa.out_keys = out_keys;
+                sa.out_count = out_count;
+                sa.nz2 = 0x8000000080000000ull;
+                cuda_check(launch_seed_tma(sa, *stm, nq / kSeedGroup + g->n_lists + 1, s), "seed radius (tma)");
+            } else if (g && g->n_rb >= 1 && k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->seed_glist,
                                                     g->n_lists,
                                                     nq / kSeedGroup + g->n_lists + 1, seed.offsets, rows, a.row_ids, a.dim,

@@ -139,6 +139,26 @@ cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float
 
 // prep.cu
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s);
+// seed.cu: the list-major radius seed with a TMA/mbarrier pipeline (dim <= 256, K <= 128)
+struct SeedListArgs {
+    const uint32_t* counts;         // rank-bucket-0 query count per list (GroupArgs::counts)
+    const uint32_t* bucket_off;
+    const uint32_t* bucket_q;
+    const uint32_t* seed_goff;      // [n_lists + 1] seed-group prefix
+    const uint32_t* seed_glist;     // [groups] list of each seed group
+    uint32_t n_lists;
+    const uint32_t* list_offsets;
+    const uint32_t* row_ids;
+    uint32_t dim, K, S;
+    const float* queries;
+    uint32_t* r_global;
+    uint64_t* out_keys;
+    uint32_t* out_count;
+    uint64_t nz2;                   // 0x8000000080000000 (sq_step2's opaque -0.0 pair)
+};
+bool seed_tma_ok(uint32_t dim, uint32_t K);
+cudaError_t launch_seed_tma(const SeedListArgs& a, const CUtensorMap& tmap, uint32_t max_groups, cudaStream_t s);
+
 cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* bucket_off, const uint32_t* bucket_q,
                                      const uint32_t* seed_goff, const uint32_t* seed_glist, uint32_t n_lists,
                                      uint32_t max_groups,
