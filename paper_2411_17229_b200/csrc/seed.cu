@@ -42,15 +42,16 @@ __device__ __forceinline__ void sd_mb_arrive(uint64_t* bar) {
 __device__ __forceinline__ void sd_mb_arrive_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sd_u32(bar)), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps instead of spinning
 __device__ __forceinline__ void sd_mb_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAITS_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@!P1 bra WAITS_%=;\n"
         "}\n" ::"r"(sd_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)
         : "memory");
 }
 __device__ __forceinline__ void sd_tma2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
