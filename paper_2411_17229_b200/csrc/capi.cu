@@ -8,6 +8,7 @@
 // so it is capturable in a CUDA graph; the host only synchronises when it has
 // to copy results or counters back.
 #include <algorithm>
+#include <chrono>
 #include <utility>
 #include <cmath>
 #include <cstdio>
@@ -1050,6 +1051,19 @@ void collect_stats(dade_gpu_ctx* c, dade_gpu_stats* stats) {
     stats->dims_accumulated += h[1];
 }
 
+// Wait for a search's results (DADE_GPU_SPIN_WAIT=1: poll the stream instead).
+void wait_stream(cudaStream_t s) {
+    if (!env_flag("DADE_GPU_SPIN_WAIT")) {
+        cuda_check(cudaStreamSynchronize(s), "search");
+        return;
+    }
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) return;
+        if (e != cudaErrorNotReady) cuda_check(e, "search");
+    }
+}
+
 // Overflow flags of the search just enqueued (worklist, coarse candidate list):
 // read back with the results in one pinned copy; check after the sync.
 void enqueue_flags(dade_gpu_ctx* c) {
@@ -1078,6 +1092,7 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
                    uint32_t flags, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
                    dade_gpu_stats* stats, const std::function<void(const float*, uint64_t*, uint32_t*)>& run) {
     c->use_device();
+    const auto t_host0 = std::chrono::steady_clock::now();
     cudaStream_t s = c->stream;
     c->counters.ensure(64);
     cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
@@ -1113,7 +1128,12 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     }
     record(c, c->e3);
     enqueue_flags(c);
-    cuda_check(cudaStreamSynchronize(s), "search");
+    const auto t_host1 = std::chrono::steady_clock::now();
+    wait_stream(s);
+    if (env_flag("DADE_GPU_HOST_TIMING"))
+        std::fprintf(stderr, "[dade_gpu] host enqueue %.3f ms, wait %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(t_host1 - t_host0).count(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host1).count());
     if (search_overflowed(c)) {  // survivor worklist too small: redo with the observed size x2
         search_common(c, queries, nq, dim, k, flags, out_ids, out_dists, out_counts, stats, run);
         return;

@@ -60,3 +60,14 @@ print(f"device-buffer search {timeit(device):.3f} ms (wall, incl. final sync)")
 qd2 = torch.empty_like(qd)
 print(f"H2D queries alone    {timeit(lambda: (qd2.copy_(qh, non_blocking=True), torch.cuda.synchronize())):.3f} ms")
 print(f"D2H results alone    {timeit(lambda: (ih.copy_(idd, non_blocking=True), dh.copy_(ddd, non_blocking=True), ch.copy_(cdd, non_blocking=True), torch.cuda.synchronize())):.3f} ms")
+# device-side spans of one host-buffer search (events e0 -> e3 include the H2D and D2H)
+dev.set_profiling(True)
+for name, f in (("host-buffer", host), ("device-buffer", device)):
+    for _ in range(3):
+        if FLUSH:
+            flush.zero_()
+        torch.cuda.synchronize()
+        f()
+    scan_ms, _, total_ms = dev.last_scan_profile()
+    print(f"{name}: device span start->end {total_ms:.3f} ms (scan {scan_ms:.3f} ms)")
+dev.set_profiling(False)
