@@ -383,6 +383,7 @@ struct dade_gpu_ctx {
     RowNorms norms_storage, norms_base;
     RowAug aug_storage;
     SliceTmap seed_tm;
+    DevBuf flat_offsets;  // {0, b_count}: the flat base as one list
     CUtensorMap tm_none{};
 
     // profiling
@@ -618,7 +619,7 @@ struct SeedArgs {
 void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, const float* d_q, uint32_t nq,
                    uint32_t k, bool two_pass, uint32_t max_items, const GroupArgs* g, const float* rows,
                    uint32_t n_rows, TmapCache& tm_tile, bool umma, uint64_t* out_keys, uint32_t* out_count,
-                   const SeedArgs& seed, RowNorms* norms) {
+                   const SeedArgs& seed, RowNorms* norms, bool flat = false) {
     cudaStream_t s = c->stream;
     bool tma = false;
     const CUtensorMap& tm = tm_tile.get(rows, std::max<uint32_t>(n_rows, 1), a.dim, tma);
@@ -664,6 +665,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 sa.n_lists = g->n_lists;
                 sa.list_offsets = seed.offsets;
                 sa.row_ids = a.row_ids;
+                sa.id_base = a.id_base;
                 sa.dim = a.dim;
                 sa.K = k;
                 sa.S = std::min<uint32_t>(seed_rows(k), 1024);
@@ -676,8 +678,9 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             } else if (g && g->n_rb >= 1 && k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->seed_glist,
                                                     g->n_lists,
-                                                    nq / kSeedGroup + g->n_lists + 1, seed.offsets, rows, a.row_ids, a.dim,
-                                                    d_q, k, seed_rows(k), a.r_global, out_keys, out_count, s),
+                                                    nq / kSeedGroup + g->n_lists + 1, seed.offsets, rows, a.row_ids,
+                                                    a.id_base, a.dim, d_q, k, seed_rows(k), a.r_global, out_keys,
+                                                    out_count, s),
                            "seed radius (lists)");
             else
                 cuda_check(launch_seed_radius(seed.probes, seed.n_probe, seed.offsets, rows, a.row_ids, a.dim, d_q, nq,
@@ -687,7 +690,10 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         }
         // passes: nearest lists' first row piece, their remaining pieces, all other
         // lists (IVF); or one flat pass. The radius is tightened after each.
-        const int n_pass = two_pass ? 3 : 1;
+        // IVF: nearest lists' first pieces, their other pieces, the other lists.
+        // Flat (one list holding the whole base, every query on it): growing row
+        // ranges [0, 4), [4, 32), [32, inf) of 1024-row pieces, tightened between.
+        const int n_pass = (two_pass || flat) ? 3 : 1;
         for (int pass = 0; pass < n_pass; ++pass) {
             cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
             FilterArgs f{};
@@ -716,10 +722,17 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             f.debug = ct.debug;
             if (const char* ex = std::getenv("DADE_GPU_UMMA_EXP")) f.exp = std::atoi(ex);
             if (unsigned long long* ph = phase_ptr_keep(c)) f.census = umma ? (pass == 2 ? ph : nullptr) : ph + 2 * pass;  // DADE_GPU_PHASES=1
-            if (two_pass) {
+            if (flat) {
+                static const uint32_t lo[3] = {0, 4, 32}, hi[3] = {4, 32, 0xffffffffu};
+                f.n_items = g->n_items + 1;
+                f.piece_lo = lo[pass];
+                f.piece_hi = hi[pass];
+            } else if (two_pass) {
                 if (pass < 2) {
                     f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
-                    const uint32_t p0 = std::max<uint32_t>(1, kFilterItemRows / rank0_item_rows(umma));
+                    uint32_t p0_rows = kFilterItemRows;  // rows of each nearest list (past the seed) in pass 0
+                    if (const char* e = std::getenv("DADE_GPU_P0_ROWS")) p0_rows = (uint32_t)std::atoi(e);
+                    const uint32_t p0 = std::max<uint32_t>(1, p0_rows / rank0_item_rows(umma));
                     f.piece_lo = pass == 0 ? 0u : p0;
                     f.piece_hi = pass == 0 ? p0 : 0xffffffffu;
                 } else {
@@ -923,9 +936,90 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     c->launches += 3;
 }
 
+// Flat exhaustive DADE scan on the streaming path: the base is one posting list
+// probed by every query (n_probe = 1), so grouping, the radius seed (its first
+// rows), the tcgen05 filter, survivors and merges are the IVF ones.
+bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint64_t* out_keys,
+                 uint32_t* out_count) {
+    cudaStream_t s = c->stream;
+    if (env_flag("DADE_GPU_FLAT_V1") || std::getenv("DADE_GPU_FLAT_BLOCKS") || k > 128 || c->b_count == 0) return false;
+    ChunkTable ct = make_chunks(c->b_dim, c->cps);
+    bool tma = false;
+    c->tm_base.get(c->base.as<float>(), std::max<uint32_t>(c->b_count, 1), c->b_dim, tma);
+    ct.use_tma = (tma && ct.vec_ok) ? 1 : 0;
+    if (!filter_ok(c, ct, c->b_dim) || !umma_ok(c, ct, tma)) return false;
+    // one list [0, b_count); every query's probe 0 is it
+    c->flat_offsets.ensure(8);
+    const uint32_t h_off[2] = {0, c->b_count};
+    cuda_check(cudaMemcpyAsync(c->flat_offsets.p, h_off, 8, cudaMemcpyHostToDevice, s), "H2D offsets");
+    c->probes.ensure((size_t)nq * 8);
+    cuda_check(cudaMemsetAsync(c->probes.p, 0, (size_t)nq * 8, s), "memset");
+    GroupArgs g{};
+    g.probes = c->probes.as<uint64_t>();
+    g.nq = nq;
+    g.n_probe = 1;
+    g.n_lists = 1;
+    g.list_offsets = c->flat_offsets.as<uint32_t>();
+    g.n_rb = 1;
+    g.rb_end[0] = 1;
+    g.max_item_rows = kFilterItemRows;
+    g.rank0_item_rows = 0;
+    g.q_chunk = kUmmaQ;
+    g.seed_skip = std::min<uint32_t>(seed_rows(k), c->b_count);
+    g.seed_min = k;
+    const size_t max_items = ((size_t)nq + kUmmaQ - 1) / kUmmaQ * ((c->b_count + kFilterItemRows - 1) / kFilterItemRows) + 1;
+    c->g_counts.ensure(8);
+    c->g_cursor.ensure(8);
+    c->g_boff.ensure(8);
+    c->g_ioff.ensure(8);
+    c->bucket_q.ensure((size_t)nq * 4);
+    c->bucket_slot.ensure((size_t)nq * 4);
+    c->items.ensure(max_items * sizeof(WorkItem));
+    c->n_items.ensure(8);
+    g.counts = c->g_counts.as<uint32_t>();
+    g.cursor = c->g_cursor.as<uint32_t>();
+    g.bucket_off = c->g_boff.as<uint32_t>();
+    g.item_off = c->g_ioff.as<uint32_t>();
+    g.bucket_q = c->bucket_q.as<uint32_t>();
+    g.bucket_slot = c->bucket_slot.as<uint32_t>();
+    g.items = c->items.as<WorkItem>();
+    g.max_items = max_items;
+    g.n_items = c->n_items.as<uint32_t>();
+    c->seed_goff.ensure(8);
+    g.seed_goff = c->seed_goff.as<uint32_t>();
+    c->seed_glist.ensure(((size_t)nq / kSeedGroup + 2) * 4);
+    g.seed_glist = c->seed_glist.as<uint32_t>();
+    cuda_check(launch_group(g, s), "group");
+    c->launches += 4;
+    c->r_global.ensure((size_t)nq * 4);
+    cuda_check(launch_fill_u32(c->r_global.as<uint32_t>(), 0x7f800000u, nq, s), "fill");
+    ScanArgs a{};
+    a.storage = c->base.as<float>();
+    a.row_ids = nullptr;
+    a.id_base = c->b_id_base;
+    a.dim = c->b_dim;
+    a.queries = d_q;
+    a.items = g.items;
+    a.n_items = g.n_items;
+    a.bucket_q = g.bucket_q;
+    a.bucket_slot = g.bucket_slot;
+    a.r_global = c->r_global.as<uint32_t>();
+    a.K = k;
+    a.coeff = c->d_coeff.as<double>();
+    a.neg_zero2 = 0x8000000080000000ull;
+    a.counters = c->counters.as<unsigned long long>();
+    record(c, c->e1);
+    SeedArgs sd{true, c->probes.as<uint64_t>(), 1, c->flat_offsets.as<uint32_t>()};
+    stream_passes(c, a, ct, d_q, nq, k, false, (uint32_t)max_items, &g, c->base.as<float>(), c->b_count, c->tm_base,
+                  true, out_keys, out_count, sd, &c->norms_base, true);
+    record(c, c->e2);
+    return true;
+}
+
 void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint64_t* out_keys,
                         uint32_t* out_count) {
     cudaStream_t s = c->stream;
+    if (flat_stream(c, d_q, nq, k, out_keys, out_count)) return;
     const uint32_t qchunks = (nq + kQC - 1) / kQC;
     const uint32_t max_blocks = (c->b_count + kRT - 1) / kRT;
     uint32_t nb = std::max<uint32_t>(1, std::min<uint32_t>(max_blocks, (1184 + qchunks - 1) / qchunks));

@@ -148,7 +148,8 @@ struct SeedListArgs {
     const uint32_t* seed_glist;     // [groups] list of each seed group
     uint32_t n_lists;
     const uint32_t* list_offsets;
-    const uint32_t* row_ids;
+    const uint32_t* row_ids;        // nullable: ids = id_base + row
+    uint32_t id_base;
     uint32_t dim, K, S;
     const float* queries;
     uint32_t* r_global;
@@ -163,9 +164,9 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
                                      const uint32_t* seed_goff, const uint32_t* seed_glist, uint32_t n_lists,
                                      uint32_t max_groups,
                                      const uint32_t* list_offsets, const float* storage,
-                                     const uint32_t* row_ids, uint32_t dim, const float* queries, uint32_t K,
-                                     uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
-                                     cudaStream_t s);
+                                     const uint32_t* row_ids, uint32_t id_base, uint32_t dim, const float* queries,
+                                     uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,
+                                     uint32_t* out_count, cudaStream_t s);
 cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const uint32_t* list_offsets,
                                const float* storage, const uint32_t* row_ids, uint32_t dim, const float* queries,
                                uint32_t nq, uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,

@@ -637,8 +637,8 @@ __global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
     const uint32_t* __restrict__ counts, const uint32_t* __restrict__ bucket_off, const uint32_t* __restrict__ bucket_q,
     const uint32_t* __restrict__ seed_goff, const uint32_t* __restrict__ seed_glist, uint32_t n_lists,
     const uint32_t* __restrict__ list_offsets, const float* __restrict__ storage,
-    const uint32_t* __restrict__ row_ids, uint32_t dim, const float* __restrict__ queries, uint32_t K, uint32_t S,
-    uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count, uint64_t nz2) {
+    const uint32_t* __restrict__ row_ids, uint32_t id_base, uint32_t dim, const float* __restrict__ queries, uint32_t K,
+    uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count, uint64_t nz2) {
     extern __shared__ __align__(16) unsigned char seed_smem[];
     float* tile = reinterpret_cast<float*>(seed_smem);                  // [2][kSeedMax][kSeedRS]
     float* qt = tile + 2 * kSeedTileF;                                  // [2][kSeedSlice][kSeedGroup]
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
 #pragma unroll
             for (int i = 0; i < kNV; ++i) {
                 const uint32_t r = lane + 32u * i;
-                iv[i] = dv[i] == T ? (row_ids ? __ldg(row_ids + start + r) : start + r) : 0xffffffffu;
+                iv[i] = dv[i] == T ? (row_ids ? __ldg(row_ids + start + r) : id_base + start + r) : 0xffffffffu;
             }
             tid_max = warp_select_regs(iv, K - c_lt, hist, lane);
         }
@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
             bool take = dv[i] < T;
             uint32_t id = 0;
             if (dv[i] <= T) {
-                id = row_ids ? __ldg(row_ids + start + r) : start + r;
+                id = row_ids ? __ldg(row_ids + start + r) : id_base + start + r;
                 take = take || (dv[i] == T && id <= tid_max);
             }
             const uint32_t bal = __ballot_sync(0xffffffffu, take);
@@ -754,9 +754,9 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
                                      const uint32_t* seed_goff, const uint32_t* seed_glist, uint32_t n_lists,
                                      uint32_t max_groups,
                                      const uint32_t* list_offsets, const float* storage,
-                                     const uint32_t* row_ids, uint32_t dim, const float* queries, uint32_t K,
-                                     uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count,
-                                     cudaStream_t s) {
+                                     const uint32_t* row_ids, uint32_t id_base, uint32_t dim, const float* queries,
+                                     uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,
+                                     uint32_t* out_count, cudaStream_t s) {
     if (n_lists == 0 || K > (uint32_t)kSeedSmall) return cudaErrorInvalidValue;  // caller: K <= kSeedListMaxK
     // double-buffered tile + query slices; sums [16][S], keys [8][128] and histograms alias the tile
     const size_t smem = sizeof(float) * (2 * kSeedTileF + 2 * kSeedSlice * kSeedGroup);
@@ -767,7 +767,7 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
     seed_radius_list_kernel<<<max_groups, kSeedThreads, smem, s>>>(counts, bucket_off, bucket_q, seed_goff, seed_glist,
                                                                     n_lists,
                                                                     list_offsets,
-                                                                 storage, row_ids, dim, queries, K,
+                                                                 storage, row_ids, id_base, dim, queries, K,
                                                                  std::min<uint32_t>(S, kSeedListMax), r_global, out_keys,
                                                                  out_count, 0x8000000080000000ull);
     return cudaGetLastError();

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kSdThreads, 2) seed_tma_kernel(const SeedListA
 #pragma unroll
                 for (int i = 0; i < kNV; ++i) {
                     const uint32_t r = lane + 32u * i;
-                    iv[i] = dv[i] == T ? (row_ids ? __ldg(row_ids + start + r) : start + r) : 0xffffffffu;
+                    iv[i] = dv[i] == T ? (row_ids ? __ldg(row_ids + start + r) : a.id_base + start + r) : 0xffffffffu;
                 }
                 tid_max = sd_select(iv, K - c_lt, hist, lane);
             }
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kSdThreads, 2) seed_tma_kernel(const SeedListA
                 bool take = dv[i] < T;
                 uint32_t id = 0;
                 if (dv[i] <= T) {
-                    id = row_ids ? __ldg(row_ids + start + r) : start + r;
+                    id = row_ids ? __ldg(row_ids + start + r) : a.id_base + start + r;
                     take = take || (dv[i] == T && id <= tid_max);
                 }
                 const uint32_t bal = __ballot_sync(0xffffffffu, take);
