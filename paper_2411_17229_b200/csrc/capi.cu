@@ -691,9 +691,11 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         // passes: nearest lists' first row piece, their remaining pieces, all other
         // lists (IVF); or one flat pass. The radius is tightened after each.
         // IVF: nearest lists' first pieces, their other pieces, the other lists.
-        // Flat (one list holding the whole base, every query on it): growing row
-        // ranges [0, 4), [4, 32), [32, inf) of 1024-row pieces, tightened between.
-        const int n_pass = (two_pass || flat) ? 3 : 1;
+        // Flat (one list holding the whole base, every query on it): row ranges
+        // of 1024-row pieces growing 4x per pass, the radius tightened between.
+        static const uint32_t flat_lo[6] = {0, 2, 8, 32, 128, 512};
+        static const uint32_t flat_hi[6] = {2, 8, 32, 128, 512, 0xffffffffu};
+        const int n_pass = flat ? 6 : two_pass ? 3 : 1;
         for (int pass = 0; pass < n_pass; ++pass) {
             cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
             FilterArgs f{};
@@ -723,10 +725,9 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             if (const char* ex = std::getenv("DADE_GPU_UMMA_EXP")) f.exp = std::atoi(ex);
             if (unsigned long long* ph = phase_ptr_keep(c)) f.census = umma ? (pass == 2 ? ph : nullptr) : ph + 2 * pass;  // DADE_GPU_PHASES=1
             if (flat) {
-                static const uint32_t lo[3] = {0, 4, 32}, hi[3] = {4, 32, 0xffffffffu};
                 f.n_items = g->n_items + 1;
-                f.piece_lo = lo[pass];
-                f.piece_hi = hi[pass];
+                f.piece_lo = flat_lo[pass];
+                f.piece_hi = flat_hi[pass];
             } else if (two_pass) {
                 if (pass < 2) {
                     f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
