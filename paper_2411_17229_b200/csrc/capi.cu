@@ -723,7 +723,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             f.piece_hi = 0xffffffffu;
             f.debug = ct.debug;
             if (const char* ex = std::getenv("DADE_GPU_UMMA_EXP")) f.exp = std::atoi(ex);
-            if (unsigned long long* ph = phase_ptr_keep(c)) f.census = umma ? (pass == 2 ? ph : nullptr) : ph + 2 * pass;  // DADE_GPU_PHASES=1
+            if (unsigned long long* ph = phase_ptr_keep(c)) f.census = umma ? (pass == n_pass - 1 ? ph : nullptr) : ph + 2 * pass;  // DADE_GPU_PHASES=1
             if (flat) {
                 f.n_items = g->n_items + 1;
                 f.piece_lo = flat_lo[pass];
@@ -1009,6 +1009,7 @@ bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uin
     a.coeff = c->d_coeff.as<double>();
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
+    a.phase = phase_ptr(c);
     record(c, c->e1);
     SeedArgs sd{true, c->probes.as<uint64_t>(), 1, c->flat_offsets.as<uint32_t>()};
     stream_passes(c, a, ct, d_q, nq, k, false, (uint32_t)max_items, &g, c->base.as<float>(), c->b_count, c->tm_base,

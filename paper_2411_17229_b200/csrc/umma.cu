@@ -435,37 +435,47 @@ dco_filter_umma_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap t
         const bool dbg = a.debug == 1;
         // kept pairs of a 32-column chunk -> worklist, column (query) major so the
         // survivor kernel's warps mostly see one query; one atomic per chunk
-        auto emit_chunk = [&](const float (&v)[32], uint32_t c0, const UMeta& m, uint32_t r) {
-            // pass 1: count (one atomic per chunk); pass 2: recompute the ballots and write
-            uint32_t total = 0, kept = 0;
+        // kept pairs of a 32-column chunk -> worklist, column (query) major so the
+        // survivor kernel's warps mostly see one query; one atomic per chunk, and
+        // only the columns holding a kept pair are walked
+        // keep mask of a 32-column chunk for this lane's row: bit i <=> !(v[i] < 0)
+        // (sign bit clear), restricted to real rows and queries
+        auto keep_mask = [&](const float (&v)[32], uint32_t c0, const UMeta& m, uint32_t r) -> uint32_t {
+            uint32_t km = 0;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const uint32_t col = c0 + i;
-                const bool valid = col < m.qcount && r < m.nrows;
-                const bool keep = valid && !(v[i] < 0.f);
-                total += __popc(__ballot_sync(0xffffffffu, dbg ? valid : keep));  // debug: every pair, pruned ones flagged
-                kept += __popc(__ballot_sync(0xffffffffu, keep));
-            }
+            for (int i = 0; i < 32; ++i) km |= (~__float_as_uint(v[i]) >> 31) << i;
+            const uint32_t ncol = m.qcount > c0 ? min(32u, m.qcount - c0) : 0u;
+            const uint32_t vmask = r < m.nrows ? (ncol == 32 ? 0xffffffffu : ((1u << ncol) - 1u)) : 0u;
+            return km & vmask;
+        };
+        auto valid_mask = [&](uint32_t c0, const UMeta& m, uint32_t r) -> uint32_t {
+            const uint32_t ncol = m.qcount > c0 ? min(32u, m.qcount - c0) : 0u;
+            return r < m.nrows ? (ncol == 32 ? 0xffffffffu : ((1u << ncol) - 1u)) : 0u;
+        };
+        // kept pairs of a chunk -> worklist, column (query) major so the survivor
+        // kernel's warps mostly see one query; one atomic per chunk, and only the
+        // columns holding a pair to emit are walked
+        auto emit_chunk = [&](uint32_t km, uint32_t em, uint32_t c0, const UMeta& m, uint32_t r) {
+            const uint32_t total = __reduce_add_sync(0xffffffffu, __popc(em));
             if (!total) return;
+            const uint32_t kept = __reduce_add_sync(0xffffffffu, __popc(km));
             uint32_t sb = 0;
             if (lane == 0) sb = atomicAdd(a.surv_count, total);
             sb = __shfl_sync(0xffffffffu, sb, 0);
             const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const uint32_t col = c0 + i;
-                const bool valid = col < m.qcount && r < m.nrows;
-                const bool keep = valid && !(v[i] < 0.f);
-                const bool emit = dbg ? valid : keep;
+            for (uint32_t cols = __reduce_or_sync(0xffffffffu, em); cols; cols &= cols - 1) {
+                const int i = __ffs(cols) - 1;
+                const bool emit = (em >> i) & 1u;
                 const uint32_t bl = __ballot_sync(0xffffffffu, emit);
                 if (emit) {
                     const uint32_t p = sb + __popc(bl & lt);
                     if (p < a.surv_cap) {
+                        const uint32_t col = c0 + i;
                         Survivor sv;
                         sv.q = qidx_s[m.ib * kUQ + col];
                         sv.row = m.row0 + r;
                         sv.acc = 0.f;
-                        sv.slot = slot_s[m.ib * kUQ + col] | (keep ? 0u : 0x80000000u);
+                        sv.slot = slot_s[m.ib * kUQ + col] | (((km >> i) & 1u) ? 0u : 0x80000000u);
                         a.surv[p] = sv;
                     }
                 }
@@ -483,30 +493,26 @@ dco_filter_umma_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap t
             te_meta += clock64() - t0;
             const UMeta m = meta[b];
             if (m.row0 == kUSentinel) break;
-            const uint32_t r = quarter * 32 + lane;
-            // rows past the item (next list's rows / TMA zero fill) never keep
-            const uint32_t rowmask = r < m.nrows ? 0u : 0x80000000u;
+            const uint32_t r = quarter * 32 + lane;  // rows past the item are masked in keep_mask
             t0 = clock64();
             mb_wait(accfull + b, (k >> 1) & 1);
             te_acc += clock64() - t0;
             tc_fence_after();
             const uint32_t nch = a.exp == 1 ? 0u : m.ncols / 32;
             const uint32_t tbase = tmem + ((quarter * 32) << 16) + b * 256;
-            for (uint32_t c = cgrp; c < nch; c += 8) {  // two chunks (c, c + 4) per round
-                const bool two = c + 4 < nch;
-                float v0[32], v1[32];
-                tc_ld32_nowait(tbase + c * 32, v0);
-                if (two) tc_ld32_nowait(tbase + (c + 4) * 32, v1);
+            for (uint32_t c = cgrp; c < nch; c += 4) {  // one 32-column chunk per round
+                float v[32];
+                tc_ld32_nowait(tbase + c * 32, v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                // all negative <=> the AND of the 32 bit patterns has the sign bit
-                uint32_t and0 = rowmask | __float_as_uint(v0[0]), and1 = rowmask | (two ? __float_as_uint(v1[0]) : ~0u);
+                // all negative <=> the AND of the bit patterns has the sign bit (rows
+                // past the item are forced negative); only then the keep mask
+                uint32_t andv = (r < m.nrows ? 0u : 0x80000000u) | __float_as_uint(v[0]);
 #pragma unroll
-                for (int i = 1; i < 32; ++i) {
-                    and0 &= __float_as_uint(v0[i]);
-                    if (two) and1 &= __float_as_uint(v1[i]);
-                }
-                if (__any_sync(0xffffffffu, !(and0 >> 31)) || dbg) emit_chunk(v0, c * 32, m, r);
-                if (two && (__any_sync(0xffffffffu, !(and1 >> 31)) || dbg)) emit_chunk(v1, (c + 4) * 32, m, r);
+                for (int i = 1; i < 32; ++i) andv &= __float_as_uint(v[i]);
+                if (!__any_sync(0xffffffffu, !(andv >> 31)) && !dbg) continue;
+                const uint32_t km = keep_mask(v, c * 32, m, r);
+                const uint32_t em = dbg ? valid_mask(c * 32, m, r) : km;
+                emit_chunk(km, em, c * 32, m, r);
             }
             tc_fence_before();
             __syncwarp();

@@ -32,3 +32,13 @@ dt = time.perf_counter() - t0
 gt = art.gt
 rec = np.mean([len(set(ids[i, :cnt[i]].tolist()) & set(gt[i].tolist())) / cfg.k for i in range(len(gt))])
 print(f"{name}: {len(q)} queries in {dt * 1e3:.2f} ms (host buffers, incl. copies) -> {len(q) / dt:.0f} q/s, recall@{cfg.k} {rec:.4f}")
+
+if os.environ.get("DADE_GPU_PHASES") == "1":
+    from paper_2411_17229_b200 import _capi
+    buf = np.zeros(16, np.uint64)
+    _capi.check(_capi.lib.dade_gpu_debug_counters(dev.h, _capi.ptr(buf)))
+    c = [int(x) for x in buf[8:16]]
+    us = lambda x: x / 148 / 1.9e3
+    print(f"last pass per CTA: items {c[0] / 148:.1f} stage {us(c[1]):.1f} us | mma wait: bready {us(c[2]):.1f} "
+          f"accempty {us(c[3]):.1f} afull {us(c[4]):.1f} us | epi warp0 wait: meta {us(c[5]):.1f} acc {us(c[6]):.1f} us "
+          f"| tma wait aempty {us(c[7]):.1f} us")
