@@ -379,6 +379,7 @@ struct dade_gpu_ctx {
     bool probes_ready = false;      // probes of this search already computed per chunk
     DevBuf counters, phase;
     TmapCache tm_centroids, tm_storage, tm_base;
+    TmapCache tm_queries{256};  // rotated queries, {32 dims, 256 rows} boxes (tcgen05 coarse GEMM)
     TmapCache tm32_storage{32}, tm32_base{32};
     RowNorms norms_storage, norms_base;
     RowAug aug_storage;
@@ -449,10 +450,35 @@ void coarse_tc_begin(dade_gpu_ctx* c, uint32_t nq) {
 }
 // queries [q0, q0 + m) (m <= coarse_tc_chunk) -> probes rows [q0, q0 + m)
 void coarse_tc_range(dade_gpu_ctx* c, const float* d_q, uint32_t q0, uint32_t m, uint32_t n_probe) {
+    cudaStream_t s = c->stream;
+    // tcgen05 GEMM for p~ when both operands can be TMA-tiled; mma.sync otherwise
+    bool tma_c = false, tma_q = false;
+    const CUtensorMap* tmc = nullptr;
+    const CUtensorMap* tmq = nullptr;
+    if (!env_flag("DADE_GPU_NO_UMMA") && c->dim % 4 == 0 && c->dim >= (uint32_t)kBox) {
+        tmc = &c->tm_centroids.get(c->centroids.as<float>(), c->n_clusters, c->dim, tma_c);
+        tmq = &c->tm_queries.get(d_q, q0 + m, c->dim, tma_q);
+    }
+    if (tma_c && tma_q) {
+        const float* qc = d_q + (size_t)q0 * c->dim;
+        cuda_check(launch_coarse_norms(c->centroids.as<float>(), c->n_clusters, qc, m, c->dim, c->cnorm.as<float>(),
+                                       c->qnorm.as<float>(), s),
+                   "coarse norms");
+        cuda_check(launch_coarse_umma(*tmc, *tmq, q0, c->n_clusters, m, c->dim, c->cnorm.as<float>(),
+                                      c->qnorm.as<float>(), c->coarse_lo.as<float>(), s),
+                   "coarse gemm (tcgen05)");
+        cuda_check(launch_coarse_select(c->centroids.as<float>(), c->n_clusters, qc, m, c->dim, n_probe,
+                                        c->cnorm.as<float>(), c->qnorm.as<float>(), c->coarse_lo.as<float>(),
+                                        c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
+                                        c->coarse_overflow.as<uint32_t>(), s),
+                   "coarse select");
+        c->launches += 3;
+        return;
+    }
     cuda_check(launch_coarse_tc(c->centroids.as<float>(), c->n_clusters, d_q + (size_t)q0 * c->dim, m, c->dim, n_probe,
                                 c->cnorm.as<float>(), c->qnorm.as<float>(), c->coarse_lo.as<float>(),
                                 c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
-                                c->coarse_overflow.as<uint32_t>(), c->stream),
+                                c->coarse_overflow.as<uint32_t>(), s),
                "coarse tc");
     c->launches += 4;
 }

@@ -421,4 +421,25 @@ cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float
     return cudaGetLastError();
 }
 
+cudaError_t launch_coarse_norms(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
+                                float* cnorm, float* qnorm, cudaStream_t s) {
+    if (nq + n_cen == 0) return cudaSuccess;
+    sq_norms_kernel<<<(unsigned)(((size_t)n_cen + nq + 7) / 8), 256, 0, s>>>(centroids, n_cen, queries, nq, dim,
+                                                                             cnorm, qnorm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq,
+                                 uint32_t dim, uint32_t n_probe, const float* cnorm, const float* qnorm,
+                                 const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap)
+        coarse_select_fast_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
+            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow);
+    else
+        coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim,
+                                                          n_probe, probes, overflow);
+    return cudaGetLastError();
+}
+
 }  // namespace dade_gpu

@@ -564,6 +564,120 @@ __global__ void row_aug_kernel(const float* __restrict__ norms, uint32_t n, floa
 }
 }  // namespace
 
+// ---- coarse ranking GEMM on tcgen05 ----------------------------------------------
+// p~(q, c) = |c|^2 + |q|^2 - 2 c.q for a 128-centroid x 256-query tile per CTA:
+// lane 0 of warp 4 TMA-loads 32-dim atoms of both operands (SW128) into a
+// 3-stage ring and issues the TF32 MMAs into a 256-column TMEM accumulator;
+// warps 0-3 read it back (TMEM lane = centroid) and store p~ per (query, centroid)
+// for coarse_select (same values and bound as coarse_tc_kernel, coarse.cu).
+namespace {
+constexpr int kCgM = 128, kCgN = 256, kCgStages = 3;
+constexpr int kCgThreads = 160;
+
+__global__ void __launch_bounds__(kCgThreads, 1)
+coarse_umma_kernel(const __grid_constant__ CUtensorMap tm_cen, const __grid_constant__ CUtensorMap tm_q, uint32_t q0,
+                   uint32_t n_cen, uint32_t nq, uint32_t dim, const float* __restrict__ cnorm,
+                   const float* __restrict__ qnorm, float* __restrict__ p_out) {
+    extern __shared__ unsigned char cg_raw[];
+    unsigned char* sm = cg_raw + ((1024u - (su32(cg_raw) & 1023u)) & 1023u);
+    constexpr uint32_t kABytes = kCgM * 128, kBBytes = kCgN * 128;
+    unsigned char* ring = sm;  // [stage][A 16 KB | B 32 KB]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kCgStages * (kABytes + kBBytes));
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kCgStages;
+    uint64_t* accf = bars + 2 * kCgStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kCgStages + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t c0 = blockIdx.x * kCgM, qt = blockIdx.y * kCgN;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kCgStages; ++i) {
+            mb_init(full + i, 1);
+            mb_init(empty + i, 1);
+        }
+        mb_init(accf, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 4) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                     "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t n_atoms = (dim + 31) / 32;
+    if (warp == 4) {
+        if (lane == 0) {
+            auto issue = [&](uint32_t k) {
+                const uint32_t s = k % kCgStages;
+                if (k >= (uint32_t)kCgStages) mb_wait(empty + s, ((k / kCgStages) - 1) & 1);
+                unsigned char* st = ring + (size_t)s * (kABytes + kBBytes);
+                mb_arrive_tx(full + s, kABytes + kBBytes);
+                tma2d_u(st, &tm_cen, (int)(k * 32), (int)c0, full + s);
+                tma2d_u(st + kABytes, &tm_q, (int)(k * 32), (int)(q0 + qt), full + s);
+            };
+            uint32_t k_issue = 0;
+            while (k_issue < n_atoms && k_issue < (uint32_t)kCgStages) issue(k_issue++);
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kCgN >> 3) << 17) |
+                                   ((uint32_t)(kCgM >> 4) << 24);
+            for (uint32_t k = 0; k < n_atoms; ++k) {
+                const uint32_t s = k % kCgStages;
+                mb_wait(full + s, (k / kCgStages) & 1);
+                tc_fence_after();
+                const unsigned char* st = ring + (size_t)s * (kABytes + kBBytes);
+                const uint32_t sa = su32(st), sb = su32(st + kABytes);
+                const int nk = min(4, (int)(dim - k * 32 + 7) / 8);
+                for (int kk = 0; kk < nk; ++kk)
+                    tc_mma(tmem, desc_sw128(sa + kk * 32), desc_sw128(sb + kk * 32), idesc, (k | kk) ? 1u : 0u);
+                tc_commit(empty + s);
+                if (k_issue < n_atoms) issue(k_issue++);
+            }
+            tc_commit(accf);
+        }
+        __syncwarp();
+    } else {
+        // epilogue: TMEM lane = centroid c0 + 32 warp + lane; columns = queries
+        mb_wait(accf, 0);
+        tc_fence_after();
+        const uint32_t c = c0 + warp * 32 + lane;
+        const float cn = c < n_cen ? cnorm[c] : 0.f;
+        for (uint32_t j = 0; j < (uint32_t)kCgN / 32; ++j) {
+            if (qt + j * 32 >= nq) break;
+            float v[32];
+            tc_ld32_nowait(tmem + ((warp * 32) << 16) + j * 32, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            if (c >= n_cen) continue;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const uint32_t qq = qt + j * 32 + i;
+                if (qq < nq) p_out[(size_t)qq * n_cen + c] = fmaf(-2.f, v[i], cn + qnorm[qq]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+    }
+}
+
+}  // namespace
+
+size_t coarse_umma_smem_bytes() { return (size_t)kCgStages * (kCgM * 128 + kCgN * 128) + 8 * 8 + 1024; }
+
+cudaError_t launch_coarse_umma(const CUtensorMap& tm_cen, const CUtensorMap& tm_q, uint32_t q0, uint32_t n_cen,
+                               uint32_t nq, uint32_t dim, const float* cnorm, const float* qnorm, float* p_out,
+                               cudaStream_t s) {
+    if (nq == 0 || n_cen == 0) return cudaSuccess;
+    const size_t smem = coarse_umma_smem_bytes();
+    DADE_CUDA_TRY(cudaFuncSetAttribute(coarse_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((n_cen + kCgM - 1) / kCgM, (nq + kCgN - 1) / kCgN);
+    coarse_umma_kernel<<<grid, kCgThreads, smem, s>>>(tm_cen, tm_q, q0, n_cen, nq, dim, cnorm, qnorm, p_out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_row_aug(const float* norms, uint32_t n, float* out, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     row_aug_kernel<<<(n + 255) / 256, 256, 0, s>>>(norms, n, out);
