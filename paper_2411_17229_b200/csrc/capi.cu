@@ -392,6 +392,10 @@ struct dade_gpu_ctx {
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
     cudaEvent_t ef[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // filter launches per pass
     int n_filter_passes = 0;
+    // DADE_GPU_TIMELINE=1: labelled events on both streams, printed per search (diagnostic)
+    std::vector<std::pair<const char*, cudaEvent_t>> tl;
+    size_t tl_used = 0;
+    bool tl_on = false;
     double last_scan_ms = 0, last_bytes = 0, last_total_ms = 0, last_filter_ms = 0;
 
     void use_device() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
@@ -587,6 +591,31 @@ unsigned long long* phase_ptr(dade_gpu_ctx* c) {
     return c->phase.as<unsigned long long>();
 }
 
+void tl_mark(dade_gpu_ctx* c, const char* name, cudaStream_t s) {
+    if (!c->tl_on) return;
+    if (c->tl_used == c->tl.size()) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreate(&e), "event");
+        c->tl.push_back({name, e});
+    }
+    c->tl[c->tl_used].first = name;
+    cuda_check(cudaEventRecord(c->tl[c->tl_used++].second, s), "event");
+}
+
+void tl_print(dade_gpu_ctx* c) {
+    if (!c->tl_on || !c->tl_used) return;
+    cuda_check(cudaEventSynchronize(c->tl[c->tl_used - 1].second), "event sync");
+    std::string line = "[dade_gpu] timeline (ms):";
+    for (size_t i = 1; i < c->tl_used; ++i) {
+        float ms = 0;
+        cuda_check(cudaEventElapsedTime(&ms, c->tl[0].second, c->tl[i].second), "elapsed");
+        char buf[96];
+        std::snprintf(buf, sizeof buf, " %s %.3f", c->tl[i].first, ms);
+        line += buf;
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());
+}
+
 void record(dade_gpu_ctx* c, cudaEvent_t e) {
     if (c->profiling) cuda_check(cudaEventRecord(e, c->stream), "event");
 }
@@ -714,6 +743,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                            "seed radius");
             ++c->launches;
         }
+        tl_mark(c, "seeded", s);
         // passes: nearest lists' first row piece, their remaining pieces, all other
         // lists (IVF); or one flat pass. The radius is tightened after each.
         // IVF: nearest lists' first pieces, their other pieces, the other lists.
@@ -830,6 +860,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 cuda_check(cudaGetLastError(), "tighten");
                 ++c->launches;
             }
+            tl_mark(c, "pass", s);
         }
     }
 }
@@ -841,6 +872,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     cudaStream_t s = c->stream;
     if (!c->probes_ready) coarse_rank(c, d_q, nq, n_probe);
     c->probes_ready = false;
+    tl_mark(c, "ranked", s);
     // K3 grouping
     GroupArgs g{};
     g.probes = c->probes.as<uint64_t>();
@@ -1130,12 +1162,14 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
                                    (size_t)m * dim * 4, cudaMemcpyHostToDevice, c->copy_stream),
                    "H2D queries");
         cuda_check(cudaEventRecord(c->copy_ev[i], c->copy_stream), "event");
+        tl_mark(c, "h2d_chunk", c->copy_stream);
         cuda_check(cudaStreamWaitEvent(c->stream, c->copy_ev[i], 0), "wait");
         cuda_check(launch_rotate(c->W.as<double>(), dim, c->q_in.as<float>() + (size_t)q0 * dim, m,
                                  c->q_rot.as<float>() + (size_t)q0 * dim, c->stream),
                    "rotate");
         ++c->launches;
         if (coarse) coarse_tc_range(c, c->q_rot.as<float>(), q0, m, n_probe);
+        tl_mark(c, "chunk_ranked", c->stream);
     }
     c->probes_ready = coarse;
     return c->q_rot.as<float>();
@@ -1219,13 +1253,18 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     c->counters.ensure(64);
     cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
     record(c, c->e0);
+    c->tl_on = env_flag("DADE_GPU_TIMELINE");
+    c->tl_used = 0;
+    tl_mark(c, "start", s);
     c->n_filter_passes = 0;
     c->surv_cap_used = 0;
     if (nq == 0) return;
     const float* d_q = stage_queries(c, queries, nq, dim, flags);
+    tl_mark(c, "staged", s);
     c->out_keys.ensure((size_t)nq * k * 8);
     c->out_count.ensure((size_t)nq * 4);
     run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
+    tl_mark(c, "searched", s);
     const bool dev = flags & DADE_GPU_DEVICE_PTRS;
     uint32_t* ids = out_ids;
     float* dists = out_dists;
@@ -1248,6 +1287,7 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
         if (out_counts)
             cuda_check(cudaMemcpyAsync(out_counts, cnts, (size_t)nq * 4, cudaMemcpyDeviceToHost, s), "D2H counts");
     }
+    tl_mark(c, "results_d2h", s);
     record(c, c->e3);
     enqueue_flags(c);
     const auto t_host1 = std::chrono::steady_clock::now();
@@ -1278,6 +1318,7 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     }
     collect_stats(c, stats);
     finish_profile(c);
+    tl_print(c);
 }
 
 }  // namespace

@@ -13,7 +13,7 @@ if kern:
 out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]
-data = rows[2:]
+data = [r for r in rows[2:] if len(r) == len(h)]
 i_s = h.index("Warp Stall Sampling (All Samples)")
 ie = h.index("Instructions Executed")
 stall = [j for j, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
