@@ -1147,22 +1147,42 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
     }
     const uint32_t n_probe = c->stage_n_probe;
     const bool coarse = n_probe && c->has_ivf && dim == c->dim && coarse_tc_ok(c, n_probe);
-    uint32_t nch = std::min<uint32_t>(4, (nq + 1023) / 1024);
-    uint32_t per = (nq + nch - 1) / nch;
-    if (coarse) per = std::min(per, coarse_tc_chunk(c, nq));
-    nch = (nq + per - 1) / per;
-    if (nch > 8) return nullptr;
+    // Two chunks (~30% / ~70%) unless the coarse buffers cap them: the second
+    // copy runs under the first chunk's rotate + coarse ranking. Per-chunk fixed
+    // costs (~55 us: the coarse GEMM's and selection's latency) make finer
+    // chunking a net loss (tools/chunk_sweep.sh). Every copy is enqueued before
+    // any compute, so the copy engine never waits on the host's launches.
+    const uint32_t cap = coarse ? coarse_tc_chunk(c, nq) : nq;
+    uint32_t sizes[8], nch = 0, rem = nq;
+    uint32_t want = std::max<uint32_t>(512, (uint32_t)((uint64_t)nq * 3 / 10 + 63) / 64 * 64);
+    if (const char* e = std::getenv("DADE_GPU_CHUNK0")) want = std::max(64, std::atoi(e));  // tuning hook
+    while (rem && nch < 8) {
+        uint32_t m = std::min<uint32_t>({rem, cap, nch == 0 ? want : rem});
+        if (nch == 7) m = rem;
+        if (m > cap) return nullptr;
+        sizes[nch++] = m;
+        rem -= m;
+    }
+    if (rem) return nullptr;
+    if (std::getenv("DADE_GPU_VERBOSE")) {
+        cudaPointerAttributes pa{};
+        const cudaError_t e = cudaPointerGetAttributes(&pa, queries);
+        std::fprintf(stderr, "[dade_gpu] host queries %p: attr rc %d type %d, %u chunks, first %u\n", (const void*)queries,
+                     (int)e, (int)pa.type, nch, sizes[0]);
+    }
     // the copy stream must not overwrite q_in while earlier work on the stream reads it
     cuda_check(cudaEventRecord(c->copy_ev[8], c->stream), "event");
     cuda_check(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[8], 0), "wait");
-    if (coarse) coarse_tc_begin(c, nq);
-    for (uint32_t i = 0; i < nch; ++i) {
-        const uint32_t q0 = i * per, m = std::min(per, nq - q0);
+    for (uint32_t i = 0, q0 = 0; i < nch; q0 += sizes[i], ++i) {
         cuda_check(cudaMemcpyAsync(c->q_in.as<float>() + (size_t)q0 * dim, queries + (size_t)q0 * dim,
-                                   (size_t)m * dim * 4, cudaMemcpyHostToDevice, c->copy_stream),
+                                   (size_t)sizes[i] * dim * 4, cudaMemcpyHostToDevice, c->copy_stream),
                    "H2D queries");
         cuda_check(cudaEventRecord(c->copy_ev[i], c->copy_stream), "event");
         tl_mark(c, "h2d_chunk", c->copy_stream);
+    }
+    if (coarse) coarse_tc_begin(c, nq);
+    for (uint32_t i = 0, q0 = 0; i < nch; q0 += sizes[i], ++i) {
+        const uint32_t m = sizes[i];
         cuda_check(cudaStreamWaitEvent(c->stream, c->copy_ev[i], 0), "wait");
         cuda_check(launch_rotate(c->W.as<double>(), dim, c->q_in.as<float>() + (size_t)q0 * dim, m,
                                  c->q_rot.as<float>() + (size_t)q0 * dim, c->stream),

@@ -138,23 +138,47 @@ __device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* 
     asm volatile("bar.sync 1, %0;\n" ::"r"(kSdT));
 }
 
+// K-th smallest (1-based) of the warp's values v (0xffffffff = absent; at least
+// K present) by 8-bit radix digits, starting below the bits every present value
+// shares (min ^ max) so that no round piles the whole warp onto one histogram
+// bin. Also returns how many values are < and == the result.
 template <int NV>
-__device__ __forceinline__ uint32_t sd_select(const uint32_t (&v)[NV], uint32_t K, uint32_t* hist, uint32_t lane) {
-    uint32_t prefix = 0, mask = 0, rem = K;
-    for (int shift = 24; shift >= 0; shift -= 8) {
+__device__ __forceinline__ uint32_t sd_select(const uint32_t (&v)[NV], uint32_t K, uint32_t* hist, uint32_t lane,
+                                              uint32_t& c_lt, uint32_t& c_eq) {
+    uint32_t lo = 0xffffffffu, hi = 0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        lo = min(lo, v[i]);
+        hi = max(hi, v[i] == 0xffffffffu ? 0u : v[i]);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (hi <= lo) {  // every present value equal
+        c_lt = 0;
+        c_eq = 0;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) c_eq += __popc(__ballot_sync(0xffffffffu, v[i] == lo));
+        return lo;
+    }
+    const int top = (31 - __clz(lo ^ hi)) & ~7;  // lowest byte boundary above which all present values agree
+    uint32_t mask = top >= 24 ? 0u : ~0u << (top + 8);
+    uint32_t prefix = lo & mask, rem = K, d = 0;
+    for (int shift = top; shift >= 0; shift -= 8) {
         for (uint32_t j = lane; j < 256; j += 32) hist[j] = 0;
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < NV; ++i)
             if ((v[i] & mask) == prefix) atomicAdd(&hist[(v[i] >> shift) & 0xffu], 1u);
         __syncwarp();
-        uint32_t d, before;
+        uint32_t before;
         warp_hist_find(hist, rem, lane, d, before);
         rem -= before;
         prefix |= d << shift;
         mask |= 0xffu << shift;
+        if (shift == 0) c_eq = hist[d];
         __syncwarp();
     }
+    c_lt = K - rem;
     return prefix;
 }
 
@@ -263,13 +287,8 @@ __global__ void __launch_bounds__(kSdThreads, 2) seed_tma_kernel(const SeedListA
                 const uint32_t r = lane + 32u * i;
                 dv[i] = r < n ? __float_as_uint(__fsqrt_rn(acc[r])) : 0xffffffffu;
             }
-            const uint32_t T = sd_select(dv, K, hist, lane);  // K-th smallest distance
-            uint32_t c_lt = 0, c_eq = 0;
-#pragma unroll
-            for (int i = 0; i < kNV; ++i) {
-                c_lt += __popc(__ballot_sync(0xffffffffu, dv[i] < T));
-                c_eq += __popc(__ballot_sync(0xffffffffu, dv[i] == T));
-            }
+            uint32_t c_lt, c_eq;
+            const uint32_t T = sd_select(dv, K, hist, lane, c_lt, c_eq);  // K-th smallest distance
             uint32_t tid_max = 0xffffffffu;  // ties at T taken by ascending id
             if (c_lt + c_eq > (uint32_t)kSdSmall) {
                 uint32_t iv[kNV];
@@ -278,18 +297,21 @@ __global__ void __launch_bounds__(kSdThreads, 2) seed_tma_kernel(const SeedListA
                     const uint32_t r = lane + 32u * i;
                     iv[i] = dv[i] == T ? (row_ids ? __ldg(row_ids + start + r) : a.id_base + start + r) : 0xffffffffu;
                 }
-                tid_max = sd_select(iv, K - c_lt, hist, lane);
+                uint32_t t_lt, t_eq;
+                tid_max = sd_select(iv, K - c_lt, hist, lane, t_lt, t_eq);
+            }
+            // ids of the values <= T, loaded together ahead of the (ballot-serialised) compaction
+            uint32_t idv[kNV];
+#pragma unroll
+            for (int i = 0; i < kNV; ++i) {
+                const uint32_t r = lane + 32u * i;
+                idv[i] = dv[i] <= T ? (row_ids ? __ldg(row_ids + start + r) : a.id_base + start + r) : 0u;
             }
             uint32_t c = 0;
 #pragma unroll
             for (int i = 0; i < kNV; ++i) {
-                const uint32_t r = lane + 32u * i;
-                bool take = dv[i] < T;
-                uint32_t id = 0;
-                if (dv[i] <= T) {
-                    id = row_ids ? __ldg(row_ids + start + r) : a.id_base + start + r;
-                    take = take || (dv[i] == T && id <= tid_max);
-                }
+                const uint32_t id = idv[i];
+                const bool take = dv[i] < T || (dv[i] == T && id <= tid_max);
                 const uint32_t bal = __ballot_sync(0xffffffffu, take);
                 const uint32_t pos = c + __popc(bal & ((1u << lane) - 1u));
                 if (take && pos < (uint32_t)kSdSmall) kk[pos] = make_key(__uint_as_float(dv[i]), id);

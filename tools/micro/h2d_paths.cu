@@ -25,6 +25,17 @@ __global__ void pull_kernel_u(const float4* __restrict__ src, float4* __restrict
     for (; i < n; i += stride) dst[i] = src[i];
 }
 
+__global__ void spin_kernel(float* out, int iters) {
+    float a = threadIdx.x, b = 1.0001f;
+    for (int i = 0; i < iters; ++i) a = fmaf(a, b, 0.5f);
+    if (a == 12345.f) out[0] = a;
+}
+__global__ void stream_kernel(const float4* __restrict__ src, float4* __restrict__ dst, size_t n, int reps) {
+    for (int r = 0; r < reps; ++r)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+            dst[i] = src[i];
+}
+
 int main() {
     const size_t bytes = 10u << 20, n4 = bytes / 16;
     float *h, *d, *d2;
@@ -66,6 +77,30 @@ int main() {
     run("D2H memcpy x1", [&] { cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st[0]); });
     run("D2H memcpy split x4", [&] { fork(); for (int k = 0; k < 4; ++k) cudaMemcpyAsync((char*)h + bytes / 4 * k, (char*)d + bytes / 4 * k, bytes / 4, cudaMemcpyDeviceToHost, st[k]); });
     run("D2H zero-copy 592 blk", [&] { pull_kernel<<<592, 256, 0, st[0]>>>((const float4*)d, (float4*)h, n4); });
+    // H2D while the SMs are busy: FMA-only kernel, and an HBM-streaming kernel
+    {
+        float* big_a; float* big_b;
+        const size_t nb = 256u << 20;
+        CK(cudaMalloc(&big_a, nb)); CK(cudaMalloc(&big_b, nb));
+        cudaStream_t cs; CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (int mode = 0; mode < 2; ++mode) {
+            std::vector<float> ts;
+            for (int it = 0; it < 12; ++it) {
+                cudaDeviceSynchronize();
+                if (mode == 0) spin_kernel<<<148 * 8, 256, 0, cs>>>(d2, 200000);
+                else stream_kernel<<<148 * 4, 512, 0, cs>>>((const float4*)big_a, (float4*)big_b, nb / 16, 20);
+                cudaEventRecord(a, st[0]);
+                cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st[0]);
+                cudaEventRecord(b, st[0]);
+                cudaEventSynchronize(b);
+                float ms; cudaEventElapsedTime(&ms, a, b);
+                if (it >= 2) ts.push_back(ms);
+                cudaDeviceSynchronize();
+            }
+            std::sort(ts.begin(), ts.end());
+            printf("H2D memcpy during %-12s med %.3f ms -> %.1f GB/s\n", mode ? "HBM stream" : "FMA spin", ts[ts.size() / 2], bytes / (ts[ts.size() / 2] * 1e6));
+        }
+    }
     // check the zero-copy result
     pull_kernel_u<<<592, 256>>>((const float4*)h, (float4*)d2, n4);
     CK(cudaDeviceSynchronize());
