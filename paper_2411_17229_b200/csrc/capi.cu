@@ -384,6 +384,7 @@ struct dade_gpu_ctx {
     RowNorms norms_storage, norms_base;
     RowAug aug_storage;
     SliceTmap seed_tm;
+    DevBuf seed_work;  // persistent seed's group counter
     DevBuf flat_offsets;  // {0, b_count}: the flat base as one list
     CUtensorMap tm_none{};
 
@@ -729,7 +730,9 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 sa.out_keys = out_keys;
                 sa.out_count = out_count;
                 sa.nz2 = 0x8000000080000000ull;
-                cuda_check(launch_seed_tma(sa, *stm, nq / kSeedGroup + g->n_lists + 1, s), "seed radius (tma)");
+                c->seed_work.ensure(4);
+                cuda_check(launch_seed_tma(sa, *stm, nq / kSeedGroup + g->n_lists + 1, s, c->seed_work.as<uint32_t>()),
+                           "seed radius (tma)");
             } else if (g && g->n_rb >= 1 && k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->seed_glist,
                                                     g->n_lists,

@@ -168,7 +168,9 @@ struct SeedListArgs {
     uint64_t nz2;                   // 0x8000000080000000 (sq_step2's opaque -0.0 pair)
 };
 bool seed_tma_ok(uint32_t dim, uint32_t K);
-cudaError_t launch_seed_tma(const SeedListArgs& a, const CUtensorMap& tmap, uint32_t max_groups, cudaStream_t s);
+// work: one zeroed-per-launch counter word (persistent variant); nullptr: one CTA per group
+cudaError_t launch_seed_tma(const SeedListArgs& a, const CUtensorMap& tmap, uint32_t max_groups, cudaStream_t s,
+                            uint32_t* work = nullptr);
 
 cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* bucket_off, const uint32_t* bucket_q,
                                      const uint32_t* seed_goff, const uint32_t* seed_glist, uint32_t n_lists,

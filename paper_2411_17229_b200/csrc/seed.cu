@@ -14,6 +14,7 @@
 //                id, 128-slot bitonic sort -> out_keys, atomicMin(r_global).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -78,21 +79,28 @@ __host__ __device__ inline SdLayout sd_layout() {
     return L;
 }
 
-// exact sums of rows (tid + 256 j, j < kR) x G queries -> accs[u][row]
-template <int G, int kR>
+// exact sums of rows (tid + 256 j, j < kR) x G queries -> accs[u][row].
+// Slices sl_base .. sl_base + n_slices - 1 of a kStages-deep ring (global slice
+// numbering: the persistent kernel's ring runs across groups). kPersist: the
+// sums go to a separate buffer once afree (if wait_free) completes, and every
+// thread arrives on aready; otherwise they overwrite the ring.
+template <int G, int kR, int kStages, bool kPersist>
 __device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* qres, uint64_t* full, uint64_t* empty,
-                                        uint32_t n_slices, float* accs, uint64_t nz2) {
+                                        uint32_t sl_base, uint32_t n_slices, float* accs, uint64_t nz2,
+                                        uint64_t* afree = nullptr, bool wait_free = false, uint32_t free_parity = 0,
+                                        uint64_t* aready = nullptr) {
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     uint64_t acc[kR][G / 2];
 #pragma unroll
     for (int j = 0; j < kR; ++j)
 #pragma unroll
         for (int p = 0; p < G / 2; ++p) acc[j][p] = 0ull;
-    for (uint32_t sl = 0; sl < n_slices; ++sl) {
-        const uint32_t s = sl % kSdStages;
-        sd_mb_wait(full + s, (sl / kSdStages) & 1);
+    for (uint32_t k = 0; k < n_slices; ++k) {
+        const uint32_t sl = sl_base + k;
+        const uint32_t s = sl % kStages;
+        sd_mb_wait(full + s, (sl / kStages) & 1);
         const unsigned char* slot = ring + (size_t)s * kSdRows * kSdSlice * 4;
-        const float* qb = qres + (size_t)sl * kSdSlice * kSdG;
+        const float* qb = qres + (size_t)k * kSdSlice * kSdG;
 #pragma unroll
         for (int c = 0; c < kSdSlice / 4; ++c) {
             float o[kR][4];
@@ -125,8 +133,12 @@ __device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* 
         __syncwarp();
         if (lane == 0) sd_mb_arrive(empty + s);  // this warp is done with the slot
     }
-    // the ring is reused for the sums: every warp must be past its last slot
-    asm volatile("bar.sync 1, %0;\n" ::"r"(kSdT));
+    if (kPersist) {
+        if (wait_free) sd_mb_wait(afree, free_parity);
+    } else {
+        // the ring is reused for the sums: every warp must be past its last slot
+        asm volatile("bar.sync 1, %0;\n" ::"r"(kSdT));
+    }
 #pragma unroll
     for (int j = 0; j < kR; ++j)
 #pragma unroll
@@ -135,13 +147,10 @@ __device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* 
             accs[(2 * p) * kSdRows + r] = lo_f(acc[j][p]);
             accs[(2 * p + 1) * kSdRows + r] = hi_f(acc[j][p]);
         }
-    asm volatile("bar.sync 1, %0;\n" ::"r"(kSdT));
+    if (kPersist) sd_mb_arrive(aready);
+    else asm volatile("bar.sync 1, %0;\n" ::"r"(kSdT));
 }
 
-// K-th smallest (1-based) of the warp's values v (0xffffffff = absent; at least
-// K present) by 8-bit radix digits, starting below the bits every present value
-// shares (min ^ max) so that no round piles the whole warp onto one histogram
-// bin. Also returns how many values are < and == the result.
 template <int NV>
 __device__ __forceinline__ uint32_t sd_select(const uint32_t (&v)[NV], uint32_t K, uint32_t* hist, uint32_t lane,
                                               uint32_t& c_lt, uint32_t& c_eq) {
@@ -197,6 +206,62 @@ __device__ __forceinline__ void sd_bitonic(uint64_t* kk, uint32_t m, uint32_t la
             }
             __syncwarp();
         }
+    }
+}
+
+// One warp: the K smallest exact sums of query q over rows [0, n) of the list at
+// start (acc[r]) by (sqrt distance, id) -> sorted keys out_keys[q], radius
+// atomicMin(r_global[q]). kk: 128 keys, hist: 256 words (per warp, shared).
+__device__ __forceinline__ void sd_finish_query(const SeedListArgs& a, uint32_t q, const float* accs, uint32_t u,
+                                             uint32_t n, uint32_t start, uint64_t* kk, uint32_t* hist) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t* row_ids = a.row_ids;
+    const uint32_t K = a.K;
+    const float* acc = accs + u * kSdRows;
+    constexpr int kNV = kSdRows / 32;
+    uint32_t dv[kNV];
+#pragma unroll
+    for (int i = 0; i < kNV; ++i) {
+        const uint32_t r = lane + 32u * i;
+        dv[i] = r < n ? __float_as_uint(__fsqrt_rn(acc[r])) : 0xffffffffu;
+    }
+    uint32_t c_lt, c_eq;
+    const uint32_t T = sd_select(dv, K, hist, lane, c_lt, c_eq);  // K-th smallest distance
+    uint32_t tid_max = 0xffffffffu;  // ties at T taken by ascending id
+    if (c_lt + c_eq > (uint32_t)kSdSmall) {
+        uint32_t iv[kNV];
+#pragma unroll
+        for (int i = 0; i < kNV; ++i) {
+            const uint32_t r = lane + 32u * i;
+            iv[i] = dv[i] == T ? (row_ids ? __ldg(row_ids + start + r) : a.id_base + start + r) : 0xffffffffu;
+        }
+        uint32_t t_lt, t_eq;
+        tid_max = sd_select(iv, K - c_lt, hist, lane, t_lt, t_eq);
+    }
+    // ids of the values <= T, loaded together ahead of the (ballot-serialised) compaction
+    uint32_t idv[kNV];
+#pragma unroll
+    for (int i = 0; i < kNV; ++i) {
+        const uint32_t r = lane + 32u * i;
+        idv[i] = dv[i] <= T ? (row_ids ? __ldg(row_ids + start + r) : a.id_base + start + r) : 0u;
+    }
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < kNV; ++i) {
+        const uint32_t id = idv[i];
+        const bool take = dv[i] < T || (dv[i] == T && id <= tid_max);
+        const uint32_t bal = __ballot_sync(0xffffffffu, take);
+        const uint32_t pos = c + __popc(bal & ((1u << lane) - 1u));
+        if (take && pos < (uint32_t)kSdSmall) kk[pos] = make_key(__uint_as_float(dv[i]), id);
+        c += __popc(bal);
+    }
+    for (uint32_t r = c + lane; r < (uint32_t)kSdSmall; r += 32) kk[r] = ~0ull;
+    __syncwarp();
+    sd_bitonic(kk, kSdSmall, lane);
+    if (lane == 0) atomicMin(a.r_global + q, (uint32_t)(kk[K - 1] >> 32));
+    if (a.out_keys) {
+        for (uint32_t i = lane; i < K; i += 32) a.out_keys[(size_t)q * K + i] = kk[i];
+        if (lane == 0) a.out_count[q] = K;
     }
 }
 
@@ -263,9 +328,9 @@ __global__ void __launch_bounds__(kSdThreads, 2) seed_tma_kernel(const SeedListA
         switch ((ng + 1) >> 1) {
 #define SD_G(P)                                                                                 \
     case P:                                                                                     \
-        if (rsel == 4) sd_sums<2 * P, 4>(ring, qres, full, empty, n_slices, accs, a.nz2);       \
-        else if (rsel == 2) sd_sums<2 * P, 2>(ring, qres, full, empty, n_slices, accs, a.nz2);  \
-        else sd_sums<2 * P, 1>(ring, qres, full, empty, n_slices, accs, a.nz2);                 \
+        if (rsel == 4) sd_sums<2 * P, 4, kSdStages, false>(ring, qres, full, empty, 0, n_slices, accs, a.nz2);       \
+        else if (rsel == 2) sd_sums<2 * P, 2, kSdStages, false>(ring, qres, full, empty, 0, n_slices, accs, a.nz2);  \
+        else sd_sums<2 * P, 1, kSdStages, false>(ring, qres, full, empty, 0, n_slices, accs, a.nz2);                 \
         break;
             SD_G(1) SD_G(2) SD_G(3) SD_G(4) SD_G(5) SD_G(6) SD_G(7) default: SD_G(8)
 #undef SD_G
@@ -273,59 +338,197 @@ __global__ void __launch_bounds__(kSdThreads, 2) seed_tma_kernel(const SeedListA
         // ---- selection: one warp per query ----
         uint64_t* keys = reinterpret_cast<uint64_t*>(accs + kSdG * kSdRows);           // [8 warps][128]
         uint32_t* hists = reinterpret_cast<uint32_t*>(keys + (kSdT / 32) * kSdSmall);  // [8 warps][256]
-        const uint32_t* row_ids = a.row_ids;
-        const uint32_t K = a.K;
         for (uint32_t u = warp; u < ng; u += kSdT / 32) {
             const uint32_t q = qs[u];
-            uint64_t* kk = keys + warp * kSdSmall;
-            uint32_t* hist = hists + warp * 256;
-            const float* acc = accs + u * kSdRows;
-            constexpr int kNV = kSdRows / 32;
-            uint32_t dv[kNV];
-#pragma unroll
-            for (int i = 0; i < kNV; ++i) {
-                const uint32_t r = lane + 32u * i;
-                dv[i] = r < n ? __float_as_uint(__fsqrt_rn(acc[r])) : 0xffffffffu;
-            }
-            uint32_t c_lt, c_eq;
-            const uint32_t T = sd_select(dv, K, hist, lane, c_lt, c_eq);  // K-th smallest distance
-            uint32_t tid_max = 0xffffffffu;  // ties at T taken by ascending id
-            if (c_lt + c_eq > (uint32_t)kSdSmall) {
-                uint32_t iv[kNV];
-#pragma unroll
-                for (int i = 0; i < kNV; ++i) {
-                    const uint32_t r = lane + 32u * i;
-                    iv[i] = dv[i] == T ? (row_ids ? __ldg(row_ids + start + r) : a.id_base + start + r) : 0xffffffffu;
-                }
-                uint32_t t_lt, t_eq;
-                tid_max = sd_select(iv, K - c_lt, hist, lane, t_lt, t_eq);
-            }
-            // ids of the values <= T, loaded together ahead of the (ballot-serialised) compaction
-            uint32_t idv[kNV];
-#pragma unroll
-            for (int i = 0; i < kNV; ++i) {
-                const uint32_t r = lane + 32u * i;
-                idv[i] = dv[i] <= T ? (row_ids ? __ldg(row_ids + start + r) : a.id_base + start + r) : 0u;
-            }
-            uint32_t c = 0;
-#pragma unroll
-            for (int i = 0; i < kNV; ++i) {
-                const uint32_t id = idv[i];
-                const bool take = dv[i] < T || (dv[i] == T && id <= tid_max);
-                const uint32_t bal = __ballot_sync(0xffffffffu, take);
-                const uint32_t pos = c + __popc(bal & ((1u << lane) - 1u));
-                if (take && pos < (uint32_t)kSdSmall) kk[pos] = make_key(__uint_as_float(dv[i]), id);
-                c += __popc(bal);
-            }
-            for (uint32_t r = c + lane; r < (uint32_t)kSdSmall; r += 32) kk[r] = ~0ull;
+            sd_finish_query(a, q, accs, u, n, start, keys + warp * kSdSmall, hists + warp * 256);
             __syncwarp();
-            sd_bitonic(kk, kSdSmall, lane);
-            if (lane == 0) atomicMin(a.r_global + q, (uint32_t)(kk[K - 1] >> 32));
-            if (a.out_keys) {
-                for (uint32_t i = lane; i < K; i += 32) a.out_keys[(size_t)q * K + i] = kk[i];
-                if (lane == 0) a.out_count[q] = K;
+        }
+    }
+}
+
+
+// ---- persistent, warp-specialised seed ------------------------------------------
+// One CTA per SM walks the seed groups in the order a global counter hands them
+// out (largest-first is not needed: a group is ~1/7 of a CTA's share):
+//   warp 15       producer: next group id -> gid slot (4 slots, gfull/gempty),
+//                 then its 8-dim slices by TMA into a 2-stage ring (full/empty,
+//                 slice numbering continues across groups);
+//   warps 0-7     sums (sd_sums, as seed_tma_kernel) into accs[i & 1] once the
+//                 selection warps freed it (afree), then aready;
+//   warps 8-14    selection (sd_finish_query) of group i while the sum warps
+//                 already run group i + 1, so the FMA pipe never idles on it.
+constexpr int kSpS = 8;                            // sum warps
+constexpr int kSpL = 7;                            // selection warps (16 warps in all: 4 per SM sub-partition)
+constexpr int kSpThreads = (kSpS + kSpL + 1) * 32;  // 512
+constexpr int kSpStages = 2;
+constexpr int kSpSlots = 4;
+constexpr uint32_t kSpEnd = 0xffffffffu;
+
+struct SpLayout {
+    size_t ring, accs, qres, keys, hist, gid, bars, total;
+};
+__host__ __device__ inline SpLayout sp_layout() {
+    SpLayout L;
+    size_t off = 0;
+    L.ring = off; off += (size_t)kSpStages * kSdRows * kSdSlice * 4;  // 64 KB
+    L.accs = off; off += 2ull * kSdG * kSdRows * 4;                   // 128 KB
+    L.qres = off; off += (size_t)kSdMaxDim * kSdG * 4;                // 16 KB
+    L.keys = off; off += (size_t)kSpL * kSdSmall * 8;
+    L.hist = off; off += (size_t)kSpL * 256 * 4;
+    L.gid = off; off += 64;
+    L.bars = off; off += 8 * (2 * kSpStages + 2 * kSpSlots + 4);
+    L.total = off + 256;
+    return L;
+}
+
+struct SpGroup {
+    uint32_t start, n, ng;
+    const uint32_t* qs;
+};
+__device__ __forceinline__ bool sp_group(const SeedListArgs& a, uint32_t b, SpGroup& G) {
+    const uint32_t list = a.seed_glist[b];
+    const uint32_t cnt_all = a.counts[list];
+    const uint32_t g0 = (b - a.seed_goff[list]) * kSdG;
+    if (g0 >= cnt_all) return false;
+    G.start = a.list_offsets[list];
+    G.n = min(a.list_offsets[list + 1] - G.start, a.S);
+    if (G.n < a.K) return false;
+    G.qs = a.bucket_q + a.bucket_off[list] + g0;
+    G.ng = min((uint32_t)kSdG, cnt_all - g0);
+    return true;
+}
+__device__ __forceinline__ int sp_rsel(uint32_t n) { return n > 2u * kSdT ? 4 : n > (uint32_t)kSdT ? 2 : 1; }
+
+__global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedListArgs a,
+                                                                      const __grid_constant__ CUtensorMap tmap,
+                                                                      uint32_t* work) {
+    extern __shared__ unsigned char sd_raw[];
+    unsigned char* sm = sd_raw + ((256u - (sd_u32(sd_raw) & 255u)) & 255u);
+    const SpLayout L = sp_layout();
+    unsigned char* ring = sm + L.ring;
+    float* accs = reinterpret_cast<float*>(sm + L.accs);  // [2][16][1024]
+    float* qres = reinterpret_cast<float*>(sm + L.qres);  // [dim][16]
+    uint64_t* keys = reinterpret_cast<uint64_t*>(sm + L.keys);
+    uint32_t* hists = reinterpret_cast<uint32_t*>(sm + L.hist);
+    volatile uint32_t* gid = reinterpret_cast<volatile uint32_t*>(sm + L.gid);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.bars);
+    uint64_t* empty = full + kSpStages;
+    uint64_t* gfull = empty + kSpStages;
+    uint64_t* gempty = gfull + kSpSlots;
+    uint64_t* aready = gempty + kSpSlots;
+    uint64_t* afree = aready + 2;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t n_groups = a.seed_goff[a.n_lists];
+    const uint32_t dim = a.dim;
+    const uint32_t n_slices = (dim + kSdSlice - 1) / kSdSlice;
+    if (tid == 0) {
+        for (int i = 0; i < kSpStages; ++i) {
+            sd_mb_init(full + i, 1);
+            sd_mb_init(empty + i, kSpS);
+        }
+        for (int j = 0; j < kSpSlots; ++j) {
+            sd_mb_init(gfull + j, 1);
+            sd_mb_init(gempty + j, kSpL);
+        }
+        for (int b = 0; b < 2; ++b) {
+            sd_mb_init(aready + b, kSpS * 32);
+            sd_mb_init(afree + b, kSpL);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kSpS + kSpL) {
+        // ---- producer ----
+        if (lane != 0) return;
+        uint32_t sl = 0;
+        for (uint32_t i = 0;; ++i) {
+            const uint32_t j = i % kSpSlots;
+            if (i >= (uint32_t)kSpSlots) sd_mb_wait(gempty + j, ((i / kSpSlots) - 1) & 1);
+            uint32_t b;
+            SpGroup G;
+            for (;;) {
+                b = atomicAdd(work, 1u);
+                if (b >= n_groups || sp_group(a, b, G)) break;
             }
-            __syncwarp();
+            gid[j] = b < n_groups ? b : kSpEnd;
+            sd_mb_arrive(gfull + j);
+            if (b >= n_groups) return;
+            const uint32_t n_boxes = (uint32_t)sp_rsel(G.n);
+            const uint32_t bytes = n_boxes * kSdBox * kSdSlice * 4;
+            for (uint32_t k = 0; k < n_slices; ++k, ++sl) {
+                const uint32_t s = sl % kSpStages;
+                if (sl >= (uint32_t)kSpStages) sd_mb_wait(empty + s, ((sl / kSpStages) - 1) & 1);
+                sd_mb_arrive_tx(full + s, bytes);
+                unsigned char* slot = ring + (size_t)s * kSdRows * kSdSlice * 4;
+                for (uint32_t bx = 0; bx < n_boxes; ++bx)
+                    sd_tma2d(slot + (size_t)bx * kSdBox * kSdSlice * 4, &tmap, (int)(k * kSdSlice),
+                             (int)(G.start + bx * kSdBox), full + s);
+            }
+        }
+    }
+    if (warp < kSpS) {
+        // ---- sums ----
+        uint32_t sl = 0;
+        for (uint32_t i = 0;; ++i) {
+            const uint32_t j = i % kSpSlots;
+            sd_mb_wait(gfull + j, (i / kSpSlots) & 1);
+            const uint32_t b = gid[j];
+            if (b == kSpEnd) return;
+            SpGroup G;
+            sp_group(a, b, G);
+            // every sum warp is past the previous group's queries
+            asm volatile("bar.sync 1, %0;\n" ::"r"(kSpS * 32) : "memory");
+            for (uint32_t e = tid; e < dim * kSdG; e += kSpS * 32) {
+                const uint32_t k = e / kSdG, u = e % kSdG;
+                if (u < G.ng) sd_cp4(qres + e, a.queries + (size_t)G.qs[u] * dim + k);
+                else qres[e] = 0.f;
+            }
+            for (uint32_t e = dim * kSdG + tid; e < n_slices * kSdSlice * kSdG; e += kSpS * 32) qres[e] = 0.f;
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            asm volatile("bar.sync 1, %0;\n" ::"r"(kSpS * 32) : "memory");
+            const uint32_t buf = i & 1;
+            float* acc = accs + (size_t)buf * kSdG * kSdRows;
+            const bool wf = i >= 2;
+            const uint32_t fp = ((i >> 1) - 1) & 1;
+            const int rsel = sp_rsel(G.n);
+            switch ((G.ng + 1) >> 1) {
+#define SP_G(P)                                                                                             \
+    case P:                                                                                                 \
+        if (rsel == 4)                                                                                      \
+            sd_sums<2 * P, 4, kSpStages, true>(ring, qres, full, empty, sl, n_slices, acc, a.nz2, afree + buf, \
+                                               wf, fp, aready + buf);                                      \
+        else if (rsel == 2)                                                                                 \
+            sd_sums<2 * P, 2, kSpStages, true>(ring, qres, full, empty, sl, n_slices, acc, a.nz2, afree + buf, \
+                                               wf, fp, aready + buf);                                      \
+        else                                                                                                \
+            sd_sums<2 * P, 1, kSpStages, true>(ring, qres, full, empty, sl, n_slices, acc, a.nz2, afree + buf, \
+                                               wf, fp, aready + buf);                                      \
+        break;
+                SP_G(1) SP_G(2) SP_G(3) SP_G(4) SP_G(5) SP_G(6) SP_G(7) default: SP_G(8)
+#undef SP_G
+            }
+            sl += n_slices;
+        }
+    }
+    // ---- selection ----
+    const uint32_t lw = warp - kSpS;
+    for (uint32_t i = 0;; ++i) {
+        const uint32_t j = i % kSpSlots;
+        sd_mb_wait(gfull + j, (i / kSpSlots) & 1);
+        const uint32_t b = gid[j];
+        if (b == kSpEnd) return;
+        SpGroup G;
+        sp_group(a, b, G);
+        const uint32_t buf = i & 1;
+        sd_mb_wait(aready + buf, (i >> 1) & 1);
+        const float* acc = accs + (size_t)buf * kSdG * kSdRows;
+        for (uint32_t u = lw; u < G.ng; u += kSpL)
+            sd_finish_query(a, G.qs[u], acc, u, G.n, G.start, keys + lw * kSdSmall, hists + lw * 256);
+        __syncwarp();
+        if (lane == 0) {
+            sd_mb_arrive(afree + buf);
+            sd_mb_arrive(gempty + j);
         }
     }
 }
@@ -334,13 +537,32 @@ __global__ void __launch_bounds__(kSdThreads, 2) seed_tma_kernel(const SeedListA
 
 bool seed_tma_ok(uint32_t dim, uint32_t K) { return dim <= (uint32_t)kSdMaxDim && dim % 4 == 0 && K <= (uint32_t)kSdSmall; }
 
-cudaError_t launch_seed_tma(const SeedListArgs& a, const CUtensorMap& tmap, uint32_t max_groups, cudaStream_t s) {
+cudaError_t launch_seed_tma(const SeedListArgs& a, const CUtensorMap& tmap, uint32_t max_groups, cudaStream_t s,
+                            uint32_t* work) {
     if (a.n_lists == 0 || max_groups == 0) return cudaSuccess;
     const size_t smem = sd_layout().total;
     static_assert((size_t)kSdStages * kSdRows * kSdSlice * 4 >=
                       (size_t)kSdG * kSdRows * 4 + (kSdT / 32) * (kSdSmall * 8 + 256 * 4),
                   "sums + keys + histograms must fit in the ring");
     DADE_CUDA_TRY(cudaFuncSetAttribute(seed_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static const bool np = std::getenv("DADE_GPU_SEED_NP") != nullptr;  // one CTA per group (previous kernel)
+    if (!np && work) {
+        const size_t sp = sp_layout().total;
+        int dev = 0, n_sm = 0;
+        DADE_CUDA_TRY(cudaGetDevice(&dev));
+        DADE_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+        DADE_CUDA_TRY(cudaFuncSetAttribute(seed_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp));
+        DADE_CUDA_TRY(cudaMemsetAsync(work, 0, 4, s));
+        seed_persist_kernel<<<std::min<uint32_t>(max_groups, (uint32_t)n_sm), kSpThreads, sp, s>>>(a, tmap, work);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess && std::getenv("DADE_GPU_VERBOSE")) {
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, seed_persist_kernel);
+            std::fprintf(stderr, "[dade_gpu] seed_persist: regs %d max threads %d static smem %zu max dyn %d (asked %zu)\n",
+                         fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, sp);
+        }
+        return e;
+    }
     seed_tma_kernel<<<max_groups, kSdThreads, smem, s>>>(a, tmap);
     return cudaGetLastError();
 }
