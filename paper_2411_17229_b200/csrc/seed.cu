@@ -84,7 +84,7 @@ __host__ __device__ inline SdLayout sd_layout() {
 // numbering: the persistent kernel's ring runs across groups). kPersist: the
 // sums go to a separate buffer once afree (if wait_free) completes, and every
 // thread arrives on aready; otherwise they overwrite the ring.
-template <int G, int kR, int kStages, bool kPersist>
+template <int G, int kR, int kStages, bool kPersist, int kT = kSdT>
 __device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* qres, uint64_t* full, uint64_t* empty,
                                         uint32_t sl_base, uint32_t n_slices, float* accs, uint64_t nz2,
                                         uint64_t* afree = nullptr, bool wait_free = false, uint32_t free_parity = 0,
@@ -106,7 +106,7 @@ __device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* 
             float o[kR][4];
 #pragma unroll
             for (int j = 0; j < kR; ++j) {
-                const uint32_t r = tid + j * kSdT;
+                const uint32_t r = min(tid + j * kT, (uint32_t)kSdRows - 1);  // rows >= 1024 (kT = 384): never stored
                 // 32B-swizzled row segment: 16-byte chunk c ^ row bit 2
                 const float4 x = *reinterpret_cast<const float4*>(slot + r * 32 + (((uint32_t)c ^ (r >> 2)) & 1u) * 16);
                 o[j][0] = x.x;
@@ -143,9 +143,11 @@ __device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* 
     for (int j = 0; j < kR; ++j)
 #pragma unroll
         for (int p = 0; p < G / 2; ++p) {
-            const uint32_t r = tid + j * kSdT;
-            accs[(2 * p) * kSdRows + r] = lo_f(acc[j][p]);
-            accs[(2 * p + 1) * kSdRows + r] = hi_f(acc[j][p]);
+            const uint32_t r = tid + j * kT;
+            if (kT * kR <= kSdRows || r < (uint32_t)kSdRows) {
+                accs[(2 * p) * kSdRows + r] = lo_f(acc[j][p]);
+                accs[(2 * p + 1) * kSdRows + r] = hi_f(acc[j][p]);
+            }
         }
     if (kPersist) sd_mb_arrive(aready);
     else asm volatile("bar.sync 1, %0;\n" ::"r"(kSdT));
@@ -357,8 +359,12 @@ __global__ void __launch_bounds__(kSdThreads, 2) seed_tma_kernel(const SeedListA
 //                 selection warps freed it (afree), then aready;
 //   warps 8-14    selection (sd_finish_query) of group i while the sum warps
 //                 already run group i + 1, so the FMA pipe never idles on it.
-constexpr int kSpS = 8;                            // sum warps
-constexpr int kSpL = 7;                            // selection warps (16 warps in all: 4 per SM sub-partition)
+#ifndef DADE_SP_SUM_WARPS
+#define DADE_SP_SUM_WARPS 8
+#endif
+constexpr int kSpS = DADE_SP_SUM_WARPS;            // sum warps
+constexpr int kSpL = 15 - kSpS;                    // selection warps (16 warps in all: 4 per SM sub-partition)
+constexpr int kSpT = kSpS * 32;                    // sum threads: rows t + kSpT j
 constexpr int kSpThreads = (kSpS + kSpL + 1) * 32;  // 512
 constexpr int kSpStages = 2;
 constexpr int kSpSlots = 4;
@@ -398,6 +404,7 @@ __device__ __forceinline__ bool sp_group(const SeedListArgs& a, uint32_t b, SpGr
     return true;
 }
 __device__ __forceinline__ int sp_rsel(uint32_t n) { return n > 2u * kSdT ? 4 : n > (uint32_t)kSdT ? 2 : 1; }
+__device__ __forceinline__ int sp_rows_per_thread(uint32_t n) { return (int)((n + kSpT - 1) / kSpT); }
 
 __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedListArgs a,
                                                                       const __grid_constant__ CUtensorMap tmap,
@@ -431,7 +438,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
             sd_mb_init(gempty + j, kSpL);
         }
         for (int b = 0; b < 2; ++b) {
-            sd_mb_init(aready + b, kSpS * 32);
+            sd_mb_init(aready + b, kSpT);
             sd_mb_init(afree + b, kSpL);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -491,21 +498,20 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
             float* acc = accs + (size_t)buf * kSdG * kSdRows;
             const bool wf = i >= 2;
             const uint32_t fp = ((i >> 1) - 1) & 1;
-            const int rsel = sp_rsel(G.n);
+            const int rsel = sp_rows_per_thread(G.n);
             switch ((G.ng + 1) >> 1) {
-#define SP_G(P)                                                                                             \
-    case P:                                                                                                 \
-        if (rsel == 4)                                                                                      \
-            sd_sums<2 * P, 4, kSpStages, true>(ring, qres, full, empty, sl, n_slices, acc, a.nz2, afree + buf, \
-                                               wf, fp, aready + buf);                                      \
-        else if (rsel == 2)                                                                                 \
-            sd_sums<2 * P, 2, kSpStages, true>(ring, qres, full, empty, sl, n_slices, acc, a.nz2, afree + buf, \
-                                               wf, fp, aready + buf);                                      \
-        else                                                                                                \
-            sd_sums<2 * P, 1, kSpStages, true>(ring, qres, full, empty, sl, n_slices, acc, a.nz2, afree + buf, \
-                                               wf, fp, aready + buf);                                      \
+#define SP_R(P, R)                                                                                            \
+    sd_sums<2 * P, R, kSpStages, true, kSpT>(ring, qres, full, empty, sl, n_slices, acc, a.nz2, afree + buf, wf, fp, \
+                                             aready + buf)
+#define SP_G(P)                                                 \
+    case P:                                                     \
+        if (rsel >= 4) SP_R(P, 4);                              \
+        else if (rsel == 3) SP_R(P, 3);                         \
+        else if (rsel == 2) SP_R(P, 2);                         \
+        else SP_R(P, 1);                                        \
         break;
                 SP_G(1) SP_G(2) SP_G(3) SP_G(4) SP_G(5) SP_G(6) SP_G(7) default: SP_G(8)
+#undef SP_R
 #undef SP_G
             }
             sl += n_slices;
