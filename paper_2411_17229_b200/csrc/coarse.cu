@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restr
 
 // Fast path (n_cen <= 1024, dim % 4 == 0), warp per query:
 //   * the query's p~ row and the bounds live in registers (32 per lane);
-//   * B = n_probe-th smallest upper bound by bitwise descent (warp-reduced counts);
+//   * B = n_probe-th smallest upper bound by 8-bit radix select;
 //   * candidates (lower bound <= B) compacted by ballots;
 //   * exact l2_sq of 32 candidates at a time: their rows staged 32 dims at a time
 //     through shared memory with coalesced 16-byte loads (8 lanes per 128-byte
@@ -301,9 +301,8 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
             lk[j] = 0xffffffffu;
         }
     }
-    // B = the n_probe-th smallest hk: largest prefix with count(hk < prefix) < n_probe.
-    // Bits above the highest one where the warp's min and max key differ are common
-    // to every key, B included: start the descent below them.
+    // B = the n_probe-th smallest hk: 8-bit radix digits (shared histogram),
+    // starting below the bits every present key shares (min ^ max)
     uint32_t kmin = 0xffffffffu, kmax = 0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
@@ -312,16 +311,26 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
     }
     kmin = __reduce_min_sync(0xffffffffu, kmin);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
-    const int top = kmin == kmax ? -1 : 31 - __clz(kmin ^ kmax);
-    uint32_t pre = top >= 31 ? 0u : (kmin & ~((2u << top) - 1u));
-    if (kmin == kmax) pre = kmin;
-    for (int bit = top; bit >= 0; --bit) {
-        const uint32_t trial = pre | (1u << bit);
-        uint32_t cnt = 0;
+    uint32_t pre = kmin;
+    if (kmax > kmin) {
+        uint32_t* hist = reinterpret_cast<uint32_t*>(rows[warp]);  // free until the exact stage
+        const int top = (31 - __clz(kmin ^ kmax)) & ~7;
+        uint32_t mask = top >= 24 ? 0u : ~0u << (top + 8), rem = n_probe;
+        pre = kmin & mask;
+        for (int shift = top; shift >= 0; shift -= 8) {
+            for (uint32_t j = lane; j < 256; j += 32) hist[j] = 0;
+            __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) cnt += hk[j] < trial ? 1u : 0u;
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (cnt < n_probe) pre = trial;
+            for (int j = 0; j < 32; ++j)
+                if ((hk[j] & mask) == pre) atomicAdd(&hist[(hk[j] >> shift) & 0xffu], 1u);
+            __syncwarp();
+            uint32_t d, before;
+            warp_hist_find(hist, rem, lane, d, before);
+            rem -= before;
+            pre |= d << shift;
+            mask |= 0xffu << shift;
+            __syncwarp();
+        }
     }
     const uint32_t B = pre;  // exactly the n_probe-th smallest key
     // candidates: every centroid whose lower bound is <= B
