@@ -385,6 +385,8 @@ struct dade_gpu_ctx {
     RowAug aug_storage;
     SliceTmap seed_tm;
     DevBuf seed_work;  // persistent seed's group counter
+    DevBuf qslots;     // per-query candidate slots [nq][kQSlots] of a streaming pass
+    DevBuf cand_total; // candidates of a pass (census, qslots mode)
     DevBuf flat_offsets;  // {0, b_count}: the flat base as one list
     CUtensorMap tm_none{};
 
@@ -555,6 +557,7 @@ constexpr uint32_t kFilterQ = 32;           // queries per streaming work item (
 // the query's neighbours), and short items spread that work over every SM.
 // Pass 0 takes the pieces covering the first kFilterItemRows rows.
 constexpr uint32_t kUmmaQ = 256;            // queries per tcgen05 work item (MMA N)
+constexpr uint32_t kQSlots = 256;           // per-query candidate slots of a streaming pass
 uint32_t rank0_item_rows(bool umma) {
     uint32_t r = umma ? 128 : 32;  // one tile: a nearest list's heavy rows spread over every SM / warp
     if (const char* e = std::getenv("DADE_GPU_R0_ROWS")) r = (uint32_t)std::atoi(e);
@@ -840,23 +843,41 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             sv.cand_count = c->cand_count.as<uint32_t>();
             sv.cand_cap = cap;
             sv.q_count = c->q_count.as<uint32_t>();
+            if (!env_flag("DADE_GPU_NO_QSLOTS")) {
+                c->qslots.ensure((size_t)nq * kQSlots * 8);
+                sv.qslots = c->qslots.as<uint64_t>();
+                sv.qslot_cap = kQSlots;
+                if (a.counters && pass < 2) {
+                    c->cand_total.ensure(4);
+                    cuda_check(cudaMemsetAsync(c->cand_total.p, 0, 4, s), "memset");
+                    sv.cand_total = c->cand_total.as<uint32_t>();
+                }
+            }
             sv.counters = a.counters;
             sv.surv_max = c->surv_max.as<uint32_t>();
             cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
             if (a.counters && pass < 2)  // survivors / candidates of passes 0, 1 (low words of counters[4 + 2 pass ..])
                 for (int w = 0; w < 2; ++w)
                     cuda_check(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(a.counters + 4 + 2 * pass + w),
-                                               w == 0 ? c->surv_count.p : c->cand_count.p, 4,
+                                               w == 0 ? c->surv_count.p : sv.cand_total ? c->cand_total.p : c->cand_count.p, 4,
                                                cudaMemcpyDeviceToDevice, s),
                                "census");
-            cuda_check(launch_bucket_candidates(c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
-                                                c->cand_count.as<uint32_t>(), cap, c->q_count.as<uint32_t>(),
-                                                c->q_off.as<uint32_t>(), c->q_cursor.as<uint32_t>(),
-                                                c->bucket.as<uint64_t>(), nq, cap, s),
-                       "bucket candidates");
-            cuda_check(launch_merge_buckets(c->bucket.as<uint64_t>(), c->q_off.as<uint32_t>(),
-                                            c->q_count.as<uint32_t>(), nq, k, out_keys, out_count, s),
-                       "merge buckets");
+            if (sv.qslots) {
+                cuda_check(launch_merge_slots(sv.qslots, sv.qslot_cap, c->q_count.as<uint32_t>(),
+                                              c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
+                                              c->cand_count.as<uint32_t>(), cap, nq, k, out_keys, out_count, s),
+                           "merge slots");
+                c->launches -= 2;
+            } else {
+                cuda_check(launch_bucket_candidates(c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
+                                                    c->cand_count.as<uint32_t>(), cap, c->q_count.as<uint32_t>(),
+                                                    c->q_off.as<uint32_t>(), c->q_cursor.as<uint32_t>(),
+                                                    c->bucket.as<uint64_t>(), nq, cap, s),
+                           "bucket candidates");
+                cuda_check(launch_merge_buckets(c->bucket.as<uint64_t>(), c->q_off.as<uint32_t>(),
+                                                c->q_count.as<uint32_t>(), nq, k, out_keys, out_count, s),
+                           "merge buckets");
+            }
             c->launches += 5;
             if (pass + 1 < n_pass) {
                 tighten_from_topk_kernel<<<(nq + 255) / 256, 256, 0, s>>>(out_keys, out_count, nq, k, a.r_global);

@@ -120,6 +120,9 @@ struct SurvArgs {
     uint32_t* cand_count;
     uint32_t cand_cap;
     uint32_t* q_count;            // per-query candidate counts
+    uint64_t* qslots;             // nullable: per-query candidate slots [nq][qslot_cap]; the overflow
+    uint32_t qslot_cap;           //   past qslot_cap goes to cand_q / cand_key
+    uint32_t* cand_total;         // nullable: candidates of the launch (qslots mode census)
     unsigned long long* counters; // [1] dims
     uint32_t* surv_max;           // running max of the survivor count (overflow check)
     uint32_t vec4;                // dim, d0 and every checkpoint are multiples of 4 (16-byte staging)
@@ -130,6 +133,11 @@ cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* can
                                      uint64_t* bucket, uint32_t nq, uint32_t max_cands, cudaStream_t s);
 cudaError_t launch_merge_buckets(const uint64_t* bucket, const uint32_t* q_off, const uint32_t* q_count, uint32_t nq,
                                  uint32_t K, uint64_t* out_keys, uint32_t* out_count, cudaStream_t s);
+// Merge each query's slot candidates (+ its entries of the overflow list) into its top-K.
+cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const uint32_t* q_count,
+                               const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
+                               uint32_t cand_cap, uint32_t nq, uint32_t K, uint64_t* out_keys, uint32_t* out_count,
+                               cudaStream_t s);
 cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tmap,
                         const CUtensorMap& tmap_norms, uint32_t grid, bool sqrt_key, cudaStream_t s);
 cudaError_t launch_row_norms(const float* rows, uint32_t n, uint32_t dim, uint32_t d0, float* out, cudaStream_t s);

@@ -995,9 +995,24 @@ __global__ void __launch_bounds__(kSvWarps * 32, 2) advance_survivors_kernel(con
                 key = make_key(key_d, id);
             }
         }
-        // warp-aggregated candidate append
-        const uint32_t bal = __ballot_sync(0xffffffffu, is_cand);
-        if (bal) {
+        if (a.qslots) {  // per-query slots; the rare overflow to the shared list
+            if (a.cand_total) {
+                const uint32_t nb = __popc(__ballot_sync(0xffffffffu, is_cand));
+                if (lane == 0 && nb) atomicAdd(a.cand_total, nb);
+            }
+            if (is_cand) {
+                const uint32_t slot = atomicAdd(a.q_count + q, 1u);
+                if (slot < a.qslot_cap) {
+                    a.qslots[(size_t)q * a.qslot_cap + slot] = key;
+                } else {
+                    const uint32_t pos = atomicAdd(a.cand_count, 1u);
+                    if (pos < a.cand_cap) {
+                        a.cand_q[pos] = q;
+                        a.cand_key[pos] = key;
+                    }
+                }
+            }
+        } else if (const uint32_t bal = __ballot_sync(0xffffffffu, is_cand)) {  // warp-aggregated append
             uint32_t base = 0;
             if (lane == 0) base = atomicAdd(a.cand_count, __popc(bal));
             base = __shfl_sync(0xffffffffu, base, 0);
@@ -1152,8 +1167,24 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
                 key = make_key(key_d, id);
             }
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, is_cand);
-        if (bal) {
+        if (a.qslots) {  // per-query slots; the rare overflow to the shared list
+            if (a.cand_total) {
+                const uint32_t nb = __popc(__ballot_sync(0xffffffffu, is_cand));
+                if (lane == 0 && nb) atomicAdd(a.cand_total, nb);
+            }
+            if (is_cand) {
+                const uint32_t slot = atomicAdd(a.q_count + q, 1u);
+                if (slot < a.qslot_cap) {
+                    a.qslots[(size_t)q * a.qslot_cap + slot] = key;
+                } else {
+                    const uint32_t pos = atomicAdd(a.cand_count, 1u);
+                    if (pos < a.cand_cap) {
+                        a.cand_q[pos] = q;
+                        a.cand_key[pos] = key;
+                    }
+                }
+            }
+        } else if (const uint32_t bal = __ballot_sync(0xffffffffu, is_cand)) {
             uint32_t base = 0;
             if (lane == 0) base = atomicAdd(a.cand_count, __popc(bal));
             base = __shfl_sync(0xffffffffu, base, 0);
@@ -1229,6 +1260,55 @@ merge_buckets_kernel(const uint64_t* __restrict__ bucket, const uint32_t* __rest
         if (K <= (uint32_t)kStageMaxK) warp_merge_staged(A, cA, K, B, m, abuf[warp]);
         else warp_merge(A, cA, K, B, m, false);
         __syncwarp();
+    }
+    const uint32_t c = *reinterpret_cast<volatile uint32_t*>(cA);
+    for (uint32_t i = c + lane; i < K; i += 32) A[i] = kEmptyKey;
+}
+
+// Merge each query's slot candidates into its top-K (out_keys already holds the
+// earlier passes' results); a query whose slots overflowed also picks its entries
+// out of the shared overflow list. Unsorted 256-key batches, warp per query.
+__global__ void __launch_bounds__(128)
+merge_slots_kernel(const uint64_t* __restrict__ qslots, uint32_t cap, const uint32_t* __restrict__ q_count,
+                   const uint32_t* __restrict__ cand_q, const uint64_t* __restrict__ cand_key,
+                   const uint32_t* __restrict__ cand_count, uint32_t cand_cap, uint32_t nq, uint32_t K,
+                   uint64_t* out_keys, uint32_t* out_count) {
+    __shared__ uint64_t bbuf[4][256];
+    __shared__ uint64_t abuf[4][kStageMaxK];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t q = blockIdx.x * 4 + warp;
+    if (q >= nq) return;
+    uint64_t* A = out_keys + (size_t)q * K;
+    uint32_t* cA = out_count + q;
+    const uint32_t cnt = q_count[q];
+    uint64_t* B = bbuf[warp];
+    auto merge = [&](uint32_t m) {
+        __syncwarp();
+        if (K <= (uint32_t)kStageMaxK) warp_merge_staged(A, cA, K, B, m, abuf[warp]);
+        else warp_merge(A, cA, K, B, m, false);
+        __syncwarp();
+    };
+    const uint64_t* src = qslots + (size_t)q * cap;
+    const uint32_t m_slots = min(cnt, cap);
+    for (uint32_t b0 = 0; b0 < m_slots; b0 += 256) {
+        const uint32_t m = min(256u, m_slots - b0);
+        for (uint32_t e = lane; e < m; e += 32) B[e] = src[b0 + e];
+        merge(m);
+    }
+    if (cnt > cap) {
+        const uint32_t n_ovf = min(*cand_count, cand_cap);
+        uint32_t nb = 0;
+        for (uint32_t i0 = 0; i0 < n_ovf; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool mine = i < n_ovf && cand_q[i] == q;
+            const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+            if (mine) B[nb + __popc(bal & ((1u << lane) - 1u))] = cand_key[i];
+            nb += __popc(bal);
+            if (nb > 224 || (i0 + 32 >= n_ovf && nb)) {
+                merge(nb);
+                nb = 0;
+            }
+        }
     }
     const uint32_t c = *reinterpret_cast<volatile uint32_t*>(cA);
     for (uint32_t i = c + lane; i < K; i += 32) A[i] = kEmptyKey;
@@ -1372,6 +1452,16 @@ cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* can
     if (max_cands)
         scatter_candidates_kernel<<<std::min<uint32_t>((max_cands + 255) / 256, 148 * 8), 256, 0, s>>>(cand_q, cand_key, cand_count, cand_cap,
                                                                           q_off, q_cursor, bucket);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const uint32_t* q_count,
+                               const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
+                               uint32_t cand_cap, uint32_t nq, uint32_t K, uint64_t* out_keys, uint32_t* out_count,
+                               cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    merge_slots_kernel<<<(nq + 3) / 4, 128, 0, s>>>(qslots, qslot_cap, q_count, cand_q, cand_key, cand_count, cand_cap,
+                                                    nq, K, out_keys, out_count);
     return cudaGetLastError();
 }
 
