@@ -252,6 +252,50 @@ __device__ inline uint32_t warp_merge_staged(uint64_t* A, uint32_t* cA_ptr, uint
     return nc;
 }
 
+// As warp_merge_staged for larger batches: B (shared, capacity >= the next power
+// of two of m, <= 256) is bitonic-sorted first, so every element's final position
+// is found by binary search instead of a linear count over B.
+__device__ inline uint32_t warp_merge_sortb(uint64_t* A, uint32_t* cA_ptr, uint32_t K, uint64_t* B, uint32_t m,
+                                            uint64_t* scratch) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t cA = *reinterpret_cast<volatile uint32_t*>(cA_ptr);
+    if (m == 0) return cA;
+    uint32_t mp = 1;
+    while (mp < m) mp <<= 1;
+    for (uint32_t i = m + lane; i < mp; i += 32) B[i] = kEmptyKey;
+    for (uint32_t i = lane; i < cA; i += 32) scratch[i] = A[i];
+    __syncwarp();
+    for (uint32_t size = 2; size <= mp; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = lane; i < mp / 2; i += 32) {
+                const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t x = B[lo], y = B[hi];
+                if ((x > y) == up) {
+                    B[lo] = y;
+                    B[hi] = x;
+                }
+            }
+            __syncwarp();
+        }
+    const uint32_t first = lower_bound_u64(scratch, cA, B[0]);
+    for (uint32_t i = first + lane; i < cA; i += 32) {
+        const uint64_t a = scratch[i];
+        const uint32_t pos = i + lower_bound_u64(B, m, a);
+        if (pos < K) A[pos] = a;
+    }
+    for (uint32_t b = lane; b < m && b < K; b += 32) {
+        const uint64_t kb = B[b];
+        const uint32_t pos = b + lower_bound_u64(scratch, cA, kb);
+        if (pos < K) A[pos] = kb;
+    }
+    const uint32_t nc = min(K, cA + m);
+    __syncwarp();
+    if (lane == 0) *cA_ptr = nc;
+    __syncwarp();
+    return nc;
+}
+
 // ---- error plumbing ----------------------------------------------------------
 #define DADE_CUDA_TRY(expr)                                                      \
     do {                                                                         \

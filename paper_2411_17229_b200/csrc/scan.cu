@@ -1284,8 +1284,12 @@ merge_slots_kernel(const uint64_t* __restrict__ qslots, uint32_t cap, const uint
     uint64_t* B = bbuf[warp];
     auto merge = [&](uint32_t m) {
         __syncwarp();
-        if (K <= (uint32_t)kStageMaxK) warp_merge_staged(A, cA, K, B, m, abuf[warp]);
-        else warp_merge(A, cA, K, B, m, false);
+        if (K <= (uint32_t)kStageMaxK) {
+            if (m > 32) warp_merge_sortb(A, cA, K, B, m, abuf[warp]);
+            else warp_merge_staged(A, cA, K, B, m, abuf[warp]);
+        } else {
+            warp_merge(A, cA, K, B, m, false);
+        }
         __syncwarp();
     };
     const uint64_t* src = qslots + (size_t)q * cap;
