@@ -1109,6 +1109,14 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
                 }
                 const bool has_next = nci <= n_ckpt && nk0 < dim;
                 if (has_next) issue(nci, nk0, buf ^ 1, act);  // speculative: the live set of now
+                // this lane's query chunk (when the warp's queries differ): eight 16-byte
+                // loads issued before the wait on the row chunk
+                float4 qv[8];
+                if (live && !qsame) {
+#pragma unroll
+                    for (uint32_t j = 0; j < 8; ++j)
+                        if (4 * j < w) qv[j] = __ldg(reinterpret_cast<const float4*>(qrow + k0) + j);
+                }
                 if (has_next) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
                 else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
                 __syncwarp();
@@ -1125,13 +1133,14 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
                             x = sq_step(x, o4.w, q4.w);
                         }
                     } else {
-                        for (uint32_t k = 0; k < w; k += 4) {
-                            const float4 o4 = *reinterpret_cast<const float4*>(os + k);
-                            const float4 q4 = __ldg(reinterpret_cast<const float4*>(qrow + k0 + k));
-                            x = sq_step(x, o4.x, q4.x);
-                            x = sq_step(x, o4.y, q4.y);
-                            x = sq_step(x, o4.z, q4.z);
-                            x = sq_step(x, o4.w, q4.w);
+#pragma unroll
+                        for (uint32_t j = 0; j < 8; ++j) {
+                            if (4 * j >= w) break;
+                            const float4 o4 = *reinterpret_cast<const float4*>(os + 4 * j);
+                            x = sq_step(x, o4.x, qv[j].x);
+                            x = sq_step(x, o4.y, qv[j].y);
+                            x = sq_step(x, o4.z, qv[j].z);
+                            x = sq_step(x, o4.w, qv[j].w);
                         }
                     }
                 }
