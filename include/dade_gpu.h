@@ -18,6 +18,8 @@
  *   dade_gpu_set_strategy_dade  DadeStrategy ctor incl. its ConfigError checks
  *                                                       proj/src/estimator.cpp:115-152
  *   dade_gpu_ivf_search      IvfIndex::search, batched  proj/src/ivf.cpp:207-231
+ *   dade_gpu_ivf_search_batches  a loop of IvfIndex::search over query batches, pipelined
+ *                                                       proj/src/bench.cpp:48-75
  *   dade_gpu_flat_search     linear_scan, batched       proj/src/knn.cpp:31-41
  *   dade_gpu_dco_evaluate    DcoStrategy::evaluate      proj/include/dade/estimator.hpp:64-74
  *   dade_gpu_partial_sums    partial_sqdist at every checkpoint
@@ -120,6 +122,19 @@ int dade_gpu_rotate(dade_gpu_ctx* ctx, const float* in, uint32_t n, float* out, 
 int dade_gpu_ivf_search(dade_gpu_ctx* ctx, const float* queries, uint32_t nq, uint32_t k,
                         uint32_t n_probe, uint32_t flags, uint32_t* out_ids, float* out_dists,
                         uint32_t* out_counts, dade_gpu_stats* stats);
+
+/* A sequence of n_batches batched IvfIndex::search calls over host buffers
+ * (queries[b] [nq x dim] -> out_ids[b] / out_dists[b] / out_counts[b]),
+ * pipelined: batch b+1's host->device copy and batch b-1's device->host copy
+ * run under batch b's search. Results are those of n_batches calls of
+ * dade_gpu_ivf_search (a batch whose worklist overflowed is redone before
+ * return). Pinned host buffers let the copies overlap; DEVICE_PTRS is refused.
+ * Replaces a loop of IvfIndex::search over query batches (the serving loop of
+ * proj/src/bench.cpp:48-75 measure(), batched). */
+int dade_gpu_ivf_search_batches(dade_gpu_ctx* ctx, uint32_t n_batches, const float* const* queries,
+                                uint32_t nq, uint32_t k, uint32_t n_probe, uint32_t flags,
+                                uint32_t* const* out_ids, float* const* out_dists,
+                                uint32_t* const* out_counts, dade_gpu_stats* stats);
 
 /* Batched linear_scan over the flat base. */
 int dade_gpu_flat_search(dade_gpu_ctx* ctx, const float* queries, uint32_t nq, uint32_t k,

@@ -356,6 +356,35 @@ public:
         return search_batch(query, 1, k, n_probe, dco, stats).front();
     }
 
+    // Pipelined sequence of equal-sized batches (dade_gpu_ivf_search_batches):
+    // batches[b] -> results[b], the same as search_batch per batch.
+    std::vector<std::vector<SearchResult>> search_batches(const std::vector<const float*>& batches, std::uint32_t nq,
+                                                          std::uint32_t k, std::uint32_t n_probe,
+                                                          const DcoStrategy& dco, DcoStats* stats = nullptr,
+                                                          bool raw = false) const {
+        if (dco.dim() != dim_) throw InvalidInput("IvfIndex::search: strategy dim mismatch");
+        dco.use(*dev_);
+        const std::uint32_t kk = k ? k : 1;
+        const std::size_t nb = batches.size();
+        std::vector<std::vector<std::uint32_t>> ids(nb, std::vector<std::uint32_t>(std::size_t(nq) * kk)),
+            cnt(nb, std::vector<std::uint32_t>(nq));
+        std::vector<std::vector<float>> d(nb, std::vector<float>(std::size_t(nq) * kk));
+        std::vector<std::uint32_t*> pi(nb), pc(nb);
+        std::vector<float*> pd(nb);
+        for (std::size_t b = 0; b < nb; ++b) {
+            pi[b] = ids[b].data();
+            pc[b] = cnt[b].data();
+            pd[b] = d[b].data();
+        }
+        dade_gpu_stats st{};
+        check(dade_gpu_ivf_search_batches(dev_->get(), (std::uint32_t)nb, batches.data(), nq, k, n_probe,
+                                          raw ? DADE_GPU_QUERIES_RAW : 0, pi.data(), pd.data(), pc.data(), &st));
+        if (stats) stats->add(st);
+        std::vector<std::vector<SearchResult>> out;
+        for (std::size_t b = 0; b < nb; ++b) out.push_back(detail::to_results(ids[b], d[b], cnt[b], nq, kk));
+        return out;
+    }
+
 private:
     explicit IvfIndex(const Device& d) : dev_(&d) {}
     const Device* dev_;

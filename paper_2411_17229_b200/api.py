@@ -382,6 +382,38 @@ class IvfIndex:
             stats._add(st)
         return ids, dists, counts
 
+    def search_batches(self, batches, k: int, n_probe: int, dco, stats: DcoStats | None = None,
+                       raw: bool = False, outputs=None):
+        """A sequence of equal-sized query batches searched with the copies of
+        one batch under the search of its neighbours (dade_gpu_ivf_search_batches);
+        results identical to search_batch per batch. outputs: optional list of
+        (ids, dists, counts) arrays to fill (pinned host memory overlaps best).
+        Returns the list of (ids, dists, counts)."""
+        qs = [_f32(b) for b in batches]
+        if not qs:
+            return []
+        nq = qs[0].shape[0]
+        for q in qs:
+            if q.ndim != 2 or q.shape != (nq, self._dim):
+                raise InvalidInput("IvfIndex::search: every batch must be [nq, dim]")
+        if dco.dim != self._dim:
+            raise InvalidInput("IvfIndex::search: strategy dim mismatch")
+        self.dev.apply(dco)
+        kk = max(k, 1)
+        if outputs is None:
+            outputs = [(np.zeros((nq, kk), np.uint32), np.zeros((nq, kk), np.float32), np.zeros(nq, np.uint32))
+                       for _ in qs]
+        nb = len(qs)
+        PA = C.c_void_p * nb
+        st = _capi.Stats()
+        check(_capi.lib.dade_gpu_ivf_search_batches(
+            self.dev.h, nb, PA(*[ptr(q) for q in qs]), nq, k, n_probe, _capi.QUERIES_RAW if raw else 0,
+            PA(*[ptr(o[0]) for o in outputs]), PA(*[ptr(o[1]) for o in outputs]),
+            PA(*[ptr(o[2]) for o in outputs]), C.byref(st)))
+        if stats is not None:
+            stats._add(st)
+        return outputs
+
     def search(self, query, k: int, n_probe: int, dco, stats: DcoStats | None = None) -> SearchResult:
         """IvfIndex::search (proj/src/ivf.cpp:207-231) for one rotated query."""
         ids, dists, counts = self.search_batch(query, k, n_probe, dco, stats)

@@ -375,6 +375,13 @@ struct dade_gpu_ctx {
     uint32_t* h_flags = nullptr;    // pinned [2]: surv_max, coarse overflow of the last search
     cudaStream_t copy_stream = nullptr;  // H2D of host query chunks (overlapped with rotation / coarse)
     cudaEvent_t copy_ev[9] = {};
+    bool qin_free_recorded = false; // copy_ev[8] marks q_in's last reader (the staging rotations)
+    // pipelined batches (dade_gpu_ivf_search_batches): result double buffers, D2H stream
+    cudaStream_t d2h_stream = nullptr;
+    cudaEvent_t res_ev[2] = {}, d2h_ev[2] = {};
+    DevBuf res_ids[2], res_dists[2], res_counts[2], batch_slot;
+    unsigned long long* h_batch = nullptr;  // pinned [n][4]: surv_max, coarse overflow, total_dco, dims
+    size_t h_batch_n = 0;
     uint32_t stage_n_probe = 0;     // > 0: stage_queries may also coarse-rank the chunks (IVF)
     bool probes_ready = false;      // probes of this search already computed per chunk
     DevBuf counters, phase;
@@ -1194,8 +1201,11 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
         std::fprintf(stderr, "[dade_gpu] host queries %p: attr rc %d type %d, %u chunks, first %u\n", (const void*)queries,
                      (int)e, (int)pa.type, nch, sizes[0]);
     }
-    // the copy stream must not overwrite q_in while earlier work on the stream reads it
-    cuda_check(cudaEventRecord(c->copy_ev[8], c->stream), "event");
+    // the copy stream must not overwrite q_in while earlier work reads it: when the
+    // previous staging was this one, its rotations were the last readers (their
+    // event lets this H2D run under the previous search); otherwise everything
+    // enqueued so far may read it
+    if (!c->qin_free_recorded) cuda_check(cudaEventRecord(c->copy_ev[8], c->stream), "event");
     cuda_check(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[8], 0), "wait");
     for (uint32_t i = 0, q0 = 0; i < nch; q0 += sizes[i], ++i) {
         cuda_check(cudaMemcpyAsync(c->q_in.as<float>() + (size_t)q0 * dim, queries + (size_t)q0 * dim,
@@ -1215,6 +1225,8 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
         if (coarse) coarse_tc_range(c, c->q_rot.as<float>(), q0, m, n_probe);
         tl_mark(c, "chunk_ranked", c->stream);
     }
+    cuda_check(cudaEventRecord(c->copy_ev[8], c->stream), "event");  // q_in read for the last time
+    c->qin_free_recorded = true;
     c->probes_ready = coarse;
     return c->q_rot.as<float>();
 }
@@ -1227,6 +1239,7 @@ const float* stage_queries(dade_gpu_ctx* c, const float* queries, uint32_t nq, u
         !env_flag("DADE_GPU_NO_OVERLAP"))
         if (const float* d = stage_queries_overlapped(c, queries, nq, dim)) return d;
     const float* d_in = queries;
+    c->qin_free_recorded = false;
     if (!(flags & DADE_GPU_DEVICE_PTRS)) {
         c->q_in.ensure(bytes);
         cuda_check(cudaMemcpyAsync(c->q_in.p, queries, bytes, cudaMemcpyHostToDevice, c->stream), "H2D queries");
@@ -1365,6 +1378,100 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     tl_print(c);
 }
 
+// Pipelined sequence of searches over host batches: batch b+1's H2D (copy
+// stream) runs under batch b's search, batch b's D2H (d2h stream) under batch
+// b+1's. Results land in two device buffer sets used alternately; a set is
+// rewritten only after its previous D2H completed. Overflow flags and DcoStats
+// counters of each batch are snapshotted on the compute stream next to its
+// results and checked after the final sync; an overflowed batch is redone by
+// search_common (same results as a sequence of single searches).
+void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, uint32_t nq, uint32_t dim, uint32_t k,
+                    uint32_t flags, uint32_t* const* out_ids, float* const* out_dists, uint32_t* const* out_counts,
+                    dade_gpu_stats* stats, const std::function<void(const float*, uint64_t*, uint32_t*)>& run) {
+    c->use_device();
+    if (nb == 0 || nq == 0) return;
+    cudaStream_t s = c->stream;
+    if (!c->d2h_stream) {
+        cuda_check(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking), "stream");
+        for (int j = 0; j < 2; ++j) {
+            cuda_check(cudaEventCreateWithFlags(&c->res_ev[j], cudaEventDisableTiming), "event");
+            cuda_check(cudaEventCreateWithFlags(&c->d2h_ev[j], cudaEventDisableTiming), "event");
+        }
+    }
+    if (c->h_batch_n < nb) {
+        if (c->h_batch) cudaFreeHost(c->h_batch);
+        c->h_batch = nullptr;
+        cuda_check(cudaMallocHost(reinterpret_cast<void**>(&c->h_batch), (size_t)nb * 32), "cudaMallocHost");
+        c->h_batch_n = nb;
+    }
+    std::memset(c->h_batch, 0, (size_t)nb * 32);
+    c->counters.ensure(64);
+    c->batch_slot.ensure(2 * 32);
+    c->out_keys.ensure((size_t)nq * k * 8);
+    c->out_count.ensure((size_t)nq * 4);
+    for (int j = 0; j < 2; ++j) {
+        c->res_ids[j].ensure((size_t)nq * k * 4);
+        c->res_dists[j].ensure((size_t)nq * k * 4);
+        c->res_counts[j].ensure((size_t)nq * 4);
+    }
+    const bool prof = c->profiling;
+    c->profiling = false;
+    c->tl_on = false;
+    std::vector<uint32_t> cap_used(nb, 0);
+    std::vector<uint8_t> coarse_used(nb, 0);
+    for (uint32_t b = 0; b < nb; ++b) {
+        const uint32_t j = b & 1;
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
+        c->n_filter_passes = 0;
+        c->surv_cap_used = 0;
+        const float* d_q = stage_queries(c, queries[b], nq, dim, flags);
+        run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
+        cap_used[b] = c->surv_cap_used;
+        coarse_used[b] = c->coarse_tc_used;
+        if (b >= 2) cuda_check(cudaStreamWaitEvent(s, c->d2h_ev[j], 0), "wait");  // set j's D2H done
+        cuda_check(launch_keys_to_results(c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), nq, k,
+                                          c->res_ids[j].as<uint32_t>(), c->res_dists[j].as<float>(),
+                                          c->res_counts[j].as<uint32_t>(), s),
+                   "keys_to_results");
+        ++c->launches;
+        auto* slot = reinterpret_cast<unsigned char*>(c->batch_slot.p) + 32 * j;
+        cuda_check(cudaMemsetAsync(slot, 0, 16, s), "memset");
+        if (cap_used[b]) cuda_check(cudaMemcpyAsync(slot, c->surv_max.p, 4, cudaMemcpyDeviceToDevice, s), "flags");
+        if (coarse_used[b])
+            cuda_check(cudaMemcpyAsync(slot + 8, c->coarse_overflow.p, 4, cudaMemcpyDeviceToDevice, s), "flags");
+        cuda_check(cudaMemcpyAsync(slot + 16, c->counters.p, 16, cudaMemcpyDeviceToDevice, s), "counters");
+        cuda_check(cudaEventRecord(c->res_ev[j], s), "event");
+        cudaStream_t t = c->d2h_stream;
+        cuda_check(cudaStreamWaitEvent(t, c->res_ev[j], 0), "wait");
+        cuda_check(cudaMemcpyAsync(out_ids[b], c->res_ids[j].p, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, t), "D2H ids");
+        cuda_check(cudaMemcpyAsync(out_dists[b], c->res_dists[j].p, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, t),
+                   "D2H dists");
+        if (out_counts && out_counts[b])
+            cuda_check(cudaMemcpyAsync(out_counts[b], c->res_counts[j].p, (size_t)nq * 4, cudaMemcpyDeviceToHost, t),
+                       "D2H counts");
+        cuda_check(cudaMemcpyAsync(c->h_batch + 4 * (size_t)b, slot, 32, cudaMemcpyDeviceToHost, t), "D2H flags");
+        cuda_check(cudaEventRecord(c->d2h_ev[j], t), "event");
+    }
+    wait_stream(s);
+    wait_stream(c->d2h_stream);
+    c->profiling = prof;
+    for (uint32_t b = 0; b < nb; ++b) {
+        const unsigned long long* h = c->h_batch + 4 * (size_t)b;
+        const bool surv_over = cap_used[b] && h[0] > cap_used[b];
+        if (cap_used[b]) c->surv_cap_hint = std::max<uint32_t>(c->surv_cap_hint, (uint32_t)std::min<unsigned long long>(h[0], 0xffffffffull));
+        if (surv_over || (coarse_used[b] && (uint32_t)h[1])) {
+            // the single-search driver redoes it (larger worklist / all-exact coarse ranking)
+            search_common(c, queries[b], nq, dim, k, flags, out_ids[b], out_dists[b],
+                          out_counts ? out_counts[b] : nullptr, stats, run);
+            continue;
+        }
+        if (stats) {
+            stats->total_dco += h[2];
+            stats->dims_accumulated += h[3];
+        }
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1407,6 +1514,17 @@ int dade_gpu_destroy(dade_gpu_ctx* c) {
             cudaStreamDestroy(c->copy_stream);
             c->copy_stream = nullptr;
         }
+        if (c->d2h_stream) {
+            cudaStreamSynchronize(c->d2h_stream);
+            for (int j = 0; j < 2; ++j) {
+                cudaEventDestroy(c->res_ev[j]);
+                cudaEventDestroy(c->d2h_ev[j]);
+            }
+            cudaStreamDestroy(c->d2h_stream);
+            c->d2h_stream = nullptr;
+        }
+        if (c->h_batch) cudaFreeHost(c->h_batch);
+        c->h_batch = nullptr;
         c->norms_storage.buf.release();
         c->aug_storage.buf.release();
         c->aug_storage.rows = nullptr;
@@ -1696,6 +1814,30 @@ int dade_gpu_ivf_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint
                           [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
                               ivf_search_device(c, d_q, nq, k, n_probe, ok, oc);
                           });
+        } catch (...) {
+            c->stage_n_probe = 0;
+            throw;
+        }
+        c->stage_n_probe = 0;
+    });
+}
+
+int dade_gpu_ivf_search_batches(dade_gpu_ctx* c, uint32_t n_batches, const float* const* queries, uint32_t nq,
+                                uint32_t k, uint32_t n_probe, uint32_t flags, uint32_t* const* out_ids,
+                                float* const* out_dists, uint32_t* const* out_counts, dade_gpu_stats* stats) {
+    return guarded([&] {
+        check_ivf_args(c, k, n_probe);
+        if (flags & DADE_GPU_DEVICE_PTRS) fail(DADE_GPU_INVALID_INPUT, "ivf_search_batches: host buffers only");
+        if (n_batches && nq && (!queries || !out_ids || !out_dists))
+            fail(DADE_GPU_INVALID_INPUT, "ivf_search_batches: null argument");
+        for (uint32_t b = 0; b < n_batches && nq; ++b)
+            if (!queries[b] || !out_ids[b] || !out_dists[b]) fail(DADE_GPU_INVALID_INPUT, "ivf_search_batches: null batch");
+        c->stage_n_probe = n_probe;
+        try {
+            search_batches(c, n_batches, queries, nq, c->dim, k, flags, out_ids, out_dists, out_counts, stats,
+                           [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
+                               ivf_search_device(c, d_q, nq, k, n_probe, ok, oc);
+                           });
         } catch (...) {
             c->stage_n_probe = 0;
             throw;

@@ -65,6 +65,19 @@ int main(int argc, char** argv) {
     for (const auto& r : res)
         for (std::size_t i = 1; i < r.neighbors.size(); ++i) sorted = sorted && r.neighbors[i - 1] < r.neighbors[i];
     report(sorted, "results ascending by (distance, id)");
+    {
+        DcoStats sb;
+        const auto rb = idx.search_batches({qs.data(), qs.data()}, nq, 10, 3, fd, &sb);
+        bool same = rb.size() == 2;
+        for (std::size_t b = 0; same && b < 2; ++b)
+            for (std::uint32_t q = 0; same && q < nq; ++q) {
+                same = rb[b][q].neighbors.size() == res[q].neighbors.size();
+                for (std::size_t i = 0; same && i < res[q].neighbors.size(); ++i)
+                    same = rb[b][q].neighbors[i].id == res[q].neighbors[i].id &&
+                           rb[b][q].neighbors[i].distance == res[q].neighbors[i].distance;
+            }
+        report(same && sb.total_dco == 2 * st.total_dco, "pipelined batches == single searches (FD), stats summed");
+    }
 
     const DadeStrategy dade(dev, t, cal, cal.delta_d);
     DcoStats sd;

@@ -33,3 +33,12 @@ for rank_lo, rank_hi, name in [(0, 1, "nearest"), (1, cfg.nprobe, "others")]:
           f"pieces max {pieces[used].max()} lists<K {(sizes[used] < K).sum()}")
 print("list sizes: min/median/mean/max", sizes.min(), np.median(sizes), sizes.mean(), sizes.max())
 print("size percentiles 50/90/99/99.9:", np.percentile(sizes, [50, 90, 99, 99.9]))
+# seed census: groups of <= 16 queries per nearest list, rows min(size, 1024)
+cnt0 = np.zeros(cfg.nlist, np.int64)
+np.add.at(cnt0, near[:, 0], 1)
+g = (cnt0 + 15) // 16
+rows = np.minimum(sizes, 1024)
+print(f"seed: groups {g.sum()} lists {(cnt0 > 0).sum()} q/group mean {cnt0.sum() / max(1, g.sum()):.2f} "
+      f"tile bytes {(g * rows).sum() * cfg.dim * 4 / 1e9:.3f} GB (unique {(rows * (cnt0 > 0)).sum() * cfg.dim * 4 / 1e9:.3f} GB) "
+      f"pair-dims {(cnt0 * rows).sum() * cfg.dim:.3e} padded {(((cnt0 + 1) // 2 * 2) * rows).sum() * cfg.dim:.3e}")
+print("q per nearest list histogram:", np.bincount(np.minimum(cnt0, 40)))
