@@ -375,6 +375,7 @@ struct dade_gpu_ctx {
     uint32_t* h_flags = nullptr;    // pinned [2]: surv_max, coarse overflow of the last search
     cudaStream_t copy_stream = nullptr;  // H2D of host query chunks (overlapped with rotation / coarse)
     cudaEvent_t copy_ev[9] = {};
+    bool stage_one_chunk = false;   // staging: one chunk (the H2D is not on the critical path)
     bool qin_free_recorded = false; // copy_ev[8] marks q_in's last reader (the staging rotations)
     // pipelined batches (dade_gpu_ivf_search_batches): result double buffers, D2H stream
     cudaStream_t d2h_stream = nullptr;
@@ -765,7 +766,14 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         static const uint32_t flat_lo[6] = {0, 2, 8, 32, 128, 512};
         static const uint32_t flat_hi[6] = {2, 8, 32, 128, 512, 0xffffffffu};
         const int n_pass = flat ? 6 : two_pass ? 3 : 1;
+        // The next staging's H2D (pipelined batches) starts with the last pass, not
+        // after this search's rotation: under the seed and the early passes the
+        // copy slowed the search by ~60 us, under the last pass's tcgen05 filter
+        // by nothing measurable (tools/e2e_pipe.py; DADE_GPU_H2D_AT_PASS overrides)
+        static const int h2d_pass = std::getenv("DADE_GPU_H2D_AT_PASS") ? std::atoi(std::getenv("DADE_GPU_H2D_AT_PASS")) : -1;
         for (int pass = 0; pass < n_pass; ++pass) {
+            if (pass == (h2d_pass >= 0 ? h2d_pass : n_pass - 1) && c->qin_free_recorded)
+                cuda_check(cudaEventRecord(c->copy_ev[8], s), "event");
             cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
             FilterArgs f{};
             f.queries = d_q;
@@ -1187,6 +1195,7 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
     uint32_t sizes[8], nch = 0, rem = nq;
     uint32_t want = std::max<uint32_t>(512, (uint32_t)((uint64_t)nq * 3 / 10 + 63) / 64 * 64);
     if (const char* e = std::getenv("DADE_GPU_CHUNK0")) want = std::max(64, std::atoi(e));  // tuning hook
+    if (c->stage_one_chunk) want = nq;  // the copy already ran ahead (pipelined batches)
     while (rem && nch < 8) {
         uint32_t m = std::min<uint32_t>({rem, cap, nch == 0 ? want : rem});
         if (nch == 7) m = rem;
@@ -1205,7 +1214,7 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
     // previous staging was this one, its rotations were the last readers (their
     // event lets this H2D run under the previous search); otherwise everything
     // enqueued so far may read it
-    if (!c->qin_free_recorded) cuda_check(cudaEventRecord(c->copy_ev[8], c->stream), "event");
+    if (!c->qin_free_recorded || env_flag("DADE_GPU_SERIAL_H2D")) cuda_check(cudaEventRecord(c->copy_ev[8], c->stream), "event");
     cuda_check(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[8], 0), "wait");
     for (uint32_t i = 0, q0 = 0; i < nch; q0 += sizes[i], ++i) {
         cuda_check(cudaMemcpyAsync(c->q_in.as<float>() + (size_t)q0 * dim, queries + (size_t)q0 * dim,
@@ -1419,12 +1428,27 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
     c->tl_on = false;
     std::vector<uint32_t> cap_used(nb, 0);
     std::vector<uint8_t> coarse_used(nb, 0);
+    // DADE_GPU_HOST_TIMING=1: per-batch host enqueue time and device span / gap (diagnostic)
+    const bool timing = env_flag("DADE_GPU_HOST_TIMING");
+    std::vector<cudaEvent_t> tev;
+    std::vector<double> t_enq;
     for (uint32_t b = 0; b < nb; ++b) {
         const uint32_t j = b & 1;
+        const auto th0 = std::chrono::steady_clock::now();
+        if (timing) {
+            tev.resize(2 * nb);
+            cuda_check(cudaEventCreate(&tev[2 * b]), "event");
+            cuda_check(cudaEventCreate(&tev[2 * b + 1]), "event");
+            cuda_check(cudaEventRecord(tev[2 * b], s), "event");
+        }
         cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
         c->n_filter_passes = 0;
         c->surv_cap_used = 0;
+        // batch b > 0: its H2D ran under batch b-1's search, so per-chunk staging
+        // would only add the coarse stage's fixed latency per chunk
+        c->stage_one_chunk = b > 0;
         const float* d_q = stage_queries(c, queries[b], nq, dim, flags);
+        c->stage_one_chunk = false;
         run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
         cap_used[b] = c->surv_cap_used;
         coarse_used[b] = c->coarse_tc_used;
@@ -1441,6 +1465,10 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
             cuda_check(cudaMemcpyAsync(slot + 8, c->coarse_overflow.p, 4, cudaMemcpyDeviceToDevice, s), "flags");
         cuda_check(cudaMemcpyAsync(slot + 16, c->counters.p, 16, cudaMemcpyDeviceToDevice, s), "counters");
         cuda_check(cudaEventRecord(c->res_ev[j], s), "event");
+        if (timing) {
+            cuda_check(cudaEventRecord(tev[2 * b + 1], s), "event");
+            t_enq.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
+        }
         cudaStream_t t = c->d2h_stream;
         cuda_check(cudaStreamWaitEvent(t, c->res_ev[j], 0), "wait");
         cuda_check(cudaMemcpyAsync(out_ids[b], c->res_ids[j].p, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, t), "D2H ids");
@@ -1455,6 +1483,16 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
     wait_stream(s);
     wait_stream(c->d2h_stream);
     c->profiling = prof;
+    if (timing) {
+        for (uint32_t b = 0; b < nb; ++b) {
+            float span = 0, gap = 0;
+            cuda_check(cudaEventElapsedTime(&span, tev[2 * b], tev[2 * b + 1]), "elapsed");
+            if (b) cuda_check(cudaEventElapsedTime(&gap, tev[2 * b - 1], tev[2 * b]), "elapsed");
+            std::fprintf(stderr, "[dade_gpu] batch %u: host enqueue %.3f ms, device span %.3f ms, gap before %.3f ms\n", b,
+                         t_enq[b], span, gap);
+        }
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
     for (uint32_t b = 0; b < nb; ++b) {
         const unsigned long long* h = c->h_batch + 4 * (size_t)b;
         const bool surv_over = cap_used[b] && h[0] > cap_used[b];
