@@ -5,11 +5,14 @@
 
 One step = one batch of the workload's queries through the whole hot path:
 rotation -> coarse ranking -> probe grouping -> dimension-progressive DCO scan
--> top-K merge (+ NCCL all-gather and merge for N > 1). N = 1 runs BASELINE
-config 1 (1M x 256, 10k queries, nlist 1024, nprobe 32, K 100, dd 32, alpha .1).
-N > 1 shards the same index by list over N ranks and scales the query batch to
-N x 10k (weak scaling: per-GPU scan work constant), merging per-GPU top-K with
-an NCCL all-gather over NVLink.
+-> top-K merge. N = 1 runs BASELINE config 1 (1M x 256, 10k queries, nlist
+1024, nprobe 32, K 100, dd 32, alpha .1). N > 1 shards the same index by list
+over N ranks and scales the job to N x 10k queries, rank r owning 10k of them
+(weak scaling): each rank rotates and coarse-ranks its own queries, NCCL
+all-gathers the rotated queries and probes, scans its lists in two phases with
+an all-reduce(MIN) of the per-query radius between them (the nearest list's
+owner seeds the radius), and an all-to-all returns each query's per-shard top-K
+to its owner for the merge (paper_2411_17229_b200/dist.py).
 
 value  = queries / device time, inputs resident in HBM, CUDA events on the
          launching stream, L2 flushed (512 MB write) between steps, max over ranks.
@@ -253,6 +256,9 @@ def run_ours(args, cfg):
 
     nq, k = nq_total, cfg.k
     q_dev = art.q_raw.contiguous()
+    # N > 1: rank r owns queries [r * nq_loc, (r + 1) * nq_loc) of the job (query-owner scheme)
+    nq_loc = cfg.nq
+    q_loc = art.q_raw[rank * nq_loc:(rank + 1) * nq_loc].contiguous()
     out_ids = torch.empty((nq, k), dtype=torch.int32, device=device)
     out_d = torch.empty((nq, k), dtype=torch.float32, device=device)
     out_c = torch.empty((nq,), dtype=torch.int32, device=device)
@@ -265,7 +271,7 @@ def run_ours(args, cfg):
                                                       _capi.ptr(out_ids), _capi.ptr(out_d), _capi.ptr(out_c),
                                                       None))
             return out_ids, out_d, out_c
-        return gdist.sharded_ivf_search(dev, None, q_dev, nq, k, cfg.nprobe, raw=True)
+        return gdist.sharded_ivf_search(dev, None, q_loc, nq_loc, k, cfg.nprobe, raw=True)
 
     clocks = ClockSampler(local, Path(tempfile.gettempdir()) / f"dade_clocks_{local}.csv")
     time.sleep(0.3)  # let the sampler start emitting before the timed region
@@ -328,11 +334,48 @@ def run_ours(args, cfg):
         scan_ms, scan_bytes = float(np.median(sm)), float(np.median(sb))
         filter_ms, n_filter = float(np.median(fms)), nf
 
+    # ---- e2e at N > 1: each rank's own query slice from pinned host memory, its own
+    # results back to pinned host memory, host wall clock, max over ranks ----------
+    e2e_multi = None
+    if world > 1:
+        qh = torch.empty((nq_loc, cfg.dim), dtype=torch.float32, pin_memory=True)
+        qh.copy_(q_loc.cpu())
+        ihm = torch.empty((nq_loc, k), dtype=torch.int32, pin_memory=True)
+        dhm = torch.empty((nq_loc, k), dtype=torch.float32, pin_memory=True)
+        chm = torch.empty((nq_loc,), dtype=torch.int32, pin_memory=True)
+
+        def e2e_multi_step():
+            qd = qh.to(device, non_blocking=True)
+            i_, d_, c_ = gdist.sharded_ivf_search(dev, None, qd, nq_loc, k, cfg.nprobe, raw=True)
+            ihm.copy_(i_, non_blocking=True)
+            dhm.copy_(d_, non_blocking=True)
+            chm.copy_(c_, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        for _ in range(args.warmup):
+            e2e_multi_step()
+        ts_m = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            e2e_multi_step()
+            ts_m.append(time.perf_counter() - t0)
+        t = torch.tensor([float(np.mean(ts_m))], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_multi = {"value": nq / float(t.item()), "unit": UNIT, "h2d_bytes_per_step": nq * cfg.dim * 4,
+                     "d2h_bytes_per_step": nq * (k * 8 + 4), "ms_per_step": 1e3 * float(t.item()),
+                     "api": "paper_2411_17229_b200.dist.sharded_ivf_search per step on every rank: H2D of the "
+                            "rank's raw query slice, search, D2H of its ids/dists/counts; host wall clock, max "
+                            "over ranks; bytes are whole-job",
+                     "recall_at_k_rank0": recall(ihm.numpy().astype(np.uint32), chm.numpy().astype(np.uint32),
+                                                 art.gt[:nq_loc]) if rank == 0 else None}
+
     if rank != 0:
         dist.destroy_process_group()
         return 0
 
-    rec = recall(ids_np, cnt_np, art.gt)
+    rec = recall(ids_np, cnt_np, art.gt if world == 1 else art.gt[:nq_loc])
 
     # ---- e2e through the C ABI with pinned host buffers ------------------------------
     e2e = None
@@ -461,7 +504,9 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded Gaussian mixture, BASELINE config shapes; GPU-built PCA/k-means/calibration)",
         "config": {"workload": cfg.describe(), "queries_per_step": nq,
-                   "parallelism": "single GPU" if world == 1 else f"list-sharded x{world}, NCCL all-gather merge",
+                   "parallelism": "single GPU" if world == 1 else
+                   f"list-sharded x{world}; rank r owns {nq_loc} queries: NCCL all-gather of rotated queries and "
+                   f"probes, all-reduce MIN of the radius, all-to-all of top-K keys",
                    "l2": "flushed between steps (512 MB write); base 1 GB > L2",
                    "timed": "rotate+coarse+group+scan+merge on device-resident raw queries"},
         "recall_at_k": rec,
@@ -470,7 +515,7 @@ def run_ours(args, cfg):
         "clocks": clk,
         "roofline": roof,
         "cpu_baseline": cpu,
-        "e2e": e2e,
+        "e2e": e2e if world == 1 else e2e_multi,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

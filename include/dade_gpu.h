@@ -20,6 +20,9 @@
  *   dade_gpu_ivf_search      IvfIndex::search, batched  proj/src/ivf.cpp:207-231
  *   dade_gpu_ivf_search_batches  a loop of IvfIndex::search over query batches, pipelined
  *                                                       proj/src/bench.cpp:48-75
+ *   dade_gpu_ivf_search_keys_begin/_end  the probe loop of IvfIndex::search split at its
+ *                            nearest list, so list shards share one heap threshold
+ *                                                       proj/src/ivf.cpp:221-229
  *   dade_gpu_flat_search     linear_scan, batched       proj/src/knn.cpp:31-41
  *   dade_gpu_dco_evaluate    DcoStrategy::evaluate      proj/include/dade/estimator.hpp:64-74
  *   dade_gpu_partial_sums    partial_sqdist at every checkpoint
@@ -150,6 +153,34 @@ int dade_gpu_ivf_search_keys(dade_gpu_ctx* ctx, const float* d_queries, uint32_t
 int dade_gpu_flat_search_keys(dade_gpu_ctx* ctx, const float* d_queries, uint32_t nq,
                               uint32_t k, uint32_t flags, uint64_t* d_out_keys,
                               dade_gpu_stats* stats);
+
+/* The coarse ranking of IvfIndex::search (proj/src/ivf.cpp:215-219) alone:
+ * rotation when QUERIES_RAW, then per query the n_probe nearest centroids as
+ * packed keys ((float_bits(l2_sq) << 32) | list, ascending) into d_probes
+ * [nq x n_probe] and the rotated queries into d_q_rot [nq x dim] (nullable).
+ * Device pointers (DEVICE_PTRS required). Multi-GPU: each rank ranks its own
+ * query slice; the slices are all-gathered and handed to _begin. */
+int dade_gpu_coarse_probes(dade_gpu_ctx* ctx, const float* d_queries, uint32_t nq,
+                           uint32_t n_probe, uint32_t flags, float* d_q_rot, uint64_t* d_probes);
+
+/* dade_gpu_ivf_search_keys in two phases, for list-sharded multi-GPU search.
+ * _begin scans every query's nearest LOCAL list (its first probe with rows on
+ * this shard) and copies the per-query radius (fp32 bits as u32, +inf =
+ * 0x7f800000) to d_radius [nq] on the context's stream. The caller min-reduces
+ * d_radius across shards (NCCL all-reduce MIN; as int32 the bits order like
+ * the distances), then _end scans the other lists with the reduced radius and
+ * completes d_out_keys. A shard whose nearest local list is far from a query
+ * would otherwise scan its lists with a radius no candidate there can beat.
+ * d_probes (nullable): the queries' probe keys from dade_gpu_coarse_probes
+ * (then d_queries are rotated queries, no QUERIES_RAW); d_queries must stay
+ * valid until _end. Device pointers only; no other search may run on the
+ * context in between. */
+int dade_gpu_ivf_search_keys_begin(dade_gpu_ctx* ctx, const float* d_queries, uint32_t nq,
+                                   uint32_t k, uint32_t n_probe, uint32_t flags,
+                                   const uint64_t* d_probes, uint64_t* d_out_keys,
+                                   uint32_t* d_radius);
+int dade_gpu_ivf_search_keys_end(dade_gpu_ctx* ctx, const uint32_t* d_radius,
+                                 dade_gpu_stats* stats);
 
 /* Merge G gathered key blocks [G x nq x k] (e.g. an NCCL all-gather) into the
  * global top-K: ids/dists/counts as dade_gpu_ivf_search. Device pointers. */

@@ -345,6 +345,16 @@ struct dade_gpu_ctx {
 
     // ivf
     bool has_ivf = false;
+    bool sharded = false;  // set_ivf_shard removed lists with rows
+    // two-phase search (dade_gpu_ivf_search_keys_begin/_end): 1 = stop before the
+    // last pass, 2 = resume at it; the begun search's arguments
+    int split = 0;
+    struct {
+        bool active = false;
+        const float* d_q = nullptr;
+        uint32_t nq = 0, k = 0, n_probe = 0;
+        uint64_t* keys = nullptr;
+    } sp;
     uint32_t dim = 0, count = 0, n_clusters = 0;
     DevBuf centroids, storage, ids, offsets;
     std::vector<uint32_t> h_offsets;  // full index offsets (host)
@@ -657,6 +667,11 @@ __global__ void tighten_from_topk_kernel(const uint64_t* keys, const uint32_t* c
     atomicMin(r_global + q, (uint32_t)(keys[(size_t)q * K + K - 1] >> 32));
 }
 
+__global__ void min_u32_kernel(uint32_t* r, const uint32_t* other, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) r[i] = min(r[i], other[i]);
+}
+
 // The streaming tensor-core path applies when the first checkpoint is a
 // multiple of 8 dims (MMA k) within two 32-dim TMA boxes.
 bool filter_ok(dade_gpu_ctx* c, const ChunkTable& ct, uint32_t dim) {
@@ -692,7 +707,8 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
     const CUtensorMap& tm = tm_tile.get(rows, std::max<uint32_t>(n_rows, 1), a.dim, tma);
     if (!tma) fail(DADE_GPU_CUDA_ERROR, "tensor map for the streaming filter failed");
     const uint32_t d0 = ct.end[ct.n_dense - 1];
-    if (umma) {  // first-slice query norms for the tcgen05 filter's -c terms
+    const bool resume = c->split == 2, stop = c->split == 1;
+    if (umma && !resume) {  // first-slice query norms for the tcgen05 filter's -c terms
         c->q_norms.ensure((size_t)std::max<uint32_t>(nq, 1) * 4);
         cuda_check(launch_row_norms(d_q, nq, a.dim, d0, c->q_norms.as<float>(), s), "query norms");
         ++c->launches;
@@ -715,9 +731,11 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         c->q_cursor.ensure((size_t)nq * 4);
         c->bucket.ensure((size_t)cap * 8);
         c->surv_max.ensure(4);
-        cuda_check(cudaMemsetAsync(c->surv_max.p, 0, 4, s), "memset");
-        cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
-        if (seed.on) {
+        if (!resume) {
+            cuda_check(cudaMemsetAsync(c->surv_max.p, 0, 4, s), "memset");
+            cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
+        }
+        if (seed.on && !resume) {
             const CUtensorMap* stm = (g && k <= 128 && seed_tma_ok(a.dim, k) && !env_flag("DADE_GPU_SEED_V1") &&
                                       !env_flag("DADE_GPU_SEED_PER_QUERY"))
                                          ? c->seed_tm.get(rows, n_rows, a.dim)
@@ -771,7 +789,10 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         // copy slowed the search by ~60 us, under the last pass's tcgen05 filter
         // by nothing measurable (tools/e2e_pipe.py; DADE_GPU_H2D_AT_PASS overrides)
         static const int h2d_pass = std::getenv("DADE_GPU_H2D_AT_PASS") ? std::atoi(std::getenv("DADE_GPU_H2D_AT_PASS")) : -1;
-        for (int pass = 0; pass < n_pass; ++pass) {
+        static const int max_pass = std::getenv("DADE_GPU_MAX_PASS") ? std::atoi(std::getenv("DADE_GPU_MAX_PASS")) : 99;  // diagnostic
+        for (int pass = 0; pass < std::min(n_pass, max_pass); ++pass) {
+            if (resume && pass < n_pass - 1) continue;  // phase 2: the last pass only
+            if (stop && pass == n_pass - 1) break;      // phase 1: everything before it
             if (pass == (h2d_pass >= 0 ? h2d_pass : n_pass - 1) && c->qin_free_recorded)
                 cuda_check(cudaEventRecord(c->copy_ev[8], s), "event");
             cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
@@ -862,7 +883,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 c->qslots.ensure((size_t)nq * kQSlots * 8);
                 sv.qslots = c->qslots.as<uint64_t>();
                 sv.qslot_cap = kQSlots;
-                if (a.counters && pass < 2) {
+                if (a.counters && (pass < 2 || !ct.debug)) {
                     c->cand_total.ensure(4);
                     cuda_check(cudaMemsetAsync(c->cand_total.p, 0, 4, s), "memset");
                     sv.cand_total = c->cand_total.as<uint32_t>();
@@ -871,9 +892,12 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             sv.counters = a.counters;
             sv.surv_max = c->surv_max.as<uint32_t>();
             cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
-            if (a.counters && pass < 2)  // survivors / candidates of passes 0, 1 (low words of counters[4 + 2 pass ..])
+            // survivors / candidates of passes 0, 1 (low words of counters[4 + 2 pass ..]); of pass 2 in
+            // counters[3] (low / high word) unless a debug mode owns that word
+            if (a.counters && (pass < 2 || (pass == 2 && !ct.debug && !std::getenv("DADE_GPU_DEBUG"))))
                 for (int w = 0; w < 2; ++w)
-                    cuda_check(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(a.counters + 4 + 2 * pass + w),
+                    cuda_check(cudaMemcpyAsync(pass < 2 ? reinterpret_cast<uint32_t*>(a.counters + 4 + 2 * pass + w)
+                                                        : reinterpret_cast<uint32_t*>(a.counters + 3) + w,
                                                w == 0 ? c->surv_count.p : sv.cand_total ? c->cand_total.p : c->cand_count.p, 4,
                                                cudaMemcpyDeviceToDevice, s),
                                "census");
@@ -909,8 +933,19 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
 void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint32_t n_probe,
                        uint64_t* out_keys, uint32_t* out_count) {
     cudaStream_t s = c->stream;
-    if (!c->probes_ready) coarse_rank(c, d_q, nq, n_probe);
+    const bool resume = c->split == 2;  // phase 2 of a two-phase search: device state of phase 1 kept
+    if (!c->probes_ready && !resume) coarse_rank(c, d_q, nq, n_probe);
     c->probes_ready = false;
+    // single-phase search of a sharded index: each query's nearest LOCAL list goes
+    // first (seed, first passes), else a shard missing a query's nearest list
+    // would scan with r = +inf. The two-phase search keeps the global order: the
+    // shard owning the nearest list seeds the query, the all-reduced radius serves the others.
+    if (c->sharded && c->split == 0) {
+        cuda_check(launch_local_probes(c->probes.as<uint64_t>(), nq, n_probe, c->offsets.as<uint32_t>(),
+                                       c->n_clusters, s),
+                   "local probes");
+        ++c->launches;
+    }
     tl_mark(c, "ranked", s);
     // K3 grouping
     GroupArgs g{};
@@ -972,15 +1007,19 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     g.seed_goff = c->seed_goff.as<uint32_t>();
     c->seed_glist.ensure(((size_t)nq / kSeedGroup + c->n_clusters + 1) * 4);
     g.seed_glist = c->seed_glist.as<uint32_t>();
-    cuda_check(launch_group(g, s), "group");
-    c->launches += 4;
+    if (!resume) {
+        cuda_check(launch_group(g, s), "group");
+        c->launches += 4;
+    }
     // K4 scan
     const size_t nseg = (size_t)nq * n_probe;
     c->seg_keys.ensure(nseg * k * 8);
     c->seg_count.ensure(nseg * 4);
     c->r_global.ensure((size_t)nq * 4);
-    cuda_check(cudaMemsetAsync(c->seg_count.p, 0, nseg * 4, s), "memset");
-    cuda_check(launch_fill_u32(c->r_global.as<uint32_t>(), 0x7f800000u, nq, s), "fill");
+    if (!resume) {
+        cuda_check(cudaMemsetAsync(c->seg_count.p, 0, nseg * 4, s), "memset");
+        cuda_check(launch_fill_u32(c->r_global.as<uint32_t>(), 0x7f800000u, nq, s), "fill");
+    }
     ScanArgs a{};
     a.storage = c->storage.as<float>();
     a.row_ids = c->ids.as<uint32_t>();
@@ -1015,12 +1054,13 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
         record(c, c->e2);
         return;
     }
-    if (seeded) {
+    if (seeded && !resume) {
         cuda_check(launch_seed_radius(c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>(), a.storage,
                                       a.row_ids, c->dim, d_q, nq, k, seed_rows(k), a.r_global, nullptr, nullptr, s),
                    "seed radius");
         ++c->launches;
     }
+    if (c->split == 1) return;  // phase 1 of the all-SIMT path: the seed's radius only
     const CUtensorMap* tn = &c->tm_none;
     if (ct.use_tc) {
         a.row_norms = c->norms_storage.get(a.storage, c->count, c->dim, ct.end[ct.n_dense - 1], s);
@@ -1664,6 +1704,7 @@ int dade_gpu_set_ivf(dade_gpu_ctx* c, uint32_t dim, uint32_t count, uint32_t n_c
         c->h_offsets.assign(offsets, offsets + n_clusters + 1);
         c->dev_offsets = c->h_offsets;
         c->has_ivf = true;
+        c->sharded = false;
     });
 }
 
@@ -1680,6 +1721,7 @@ int dade_gpu_set_ivf_shard(dade_gpu_ctx* c, const uint8_t* mask) {
         for (uint32_t l = 0; l < nl; ++l) {
             dev[l] = (uint32_t)rows;
             if (mask[l]) rows += c->dev_offsets[l + 1] - c->dev_offsets[l];
+            else if (c->dev_offsets[l + 1] > c->dev_offsets[l]) c->sharded = true;
         }
         dev[nl] = (uint32_t)rows;
         DevBuf ns, ni;
@@ -1908,7 +1950,11 @@ int dade_gpu_ivf_search_keys(dade_gpu_ctx* c, const float* d_queries, uint32_t n
         c->out_count.ensure((size_t)nq * 4);
         for (int attempt = 0;; ++attempt) {
             c->surv_cap_used = 0;
+            c->tl_on = env_flag("DADE_GPU_TIMELINE");
+            c->tl_used = 0;
+            tl_mark(c, "start", c->stream);
             ivf_search_device(c, d_q, nq, k, n_probe, d_out_keys, c->out_count.as<uint32_t>());
+            tl_print(c);
             enqueue_flags(c);
             cuda_check(cudaStreamSynchronize(c->stream), "search");
             if (!search_overflowed(c)) break;
@@ -1920,6 +1966,127 @@ int dade_gpu_ivf_search_keys(dade_gpu_ctx* c, const float* d_queries, uint32_t n
             cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
             ivf_search_device(c, d_q, nq, k, n_probe, d_out_keys, c->out_count.as<uint32_t>());
             c->coarse_force_exact = false;
+        }
+        collect_stats(c, stats);
+    });
+}
+
+int dade_gpu_coarse_probes(dade_gpu_ctx* c, const float* d_queries, uint32_t nq, uint32_t n_probe, uint32_t flags,
+                           float* d_q_rot, uint64_t* d_probes) {
+    return guarded([&] {
+        check_ivf_args(c, 1, n_probe);
+        if (!(flags & DADE_GPU_DEVICE_PTRS)) fail(DADE_GPU_INVALID_INPUT, "coarse_probes: device pointers only");
+        if (nq && (!d_queries || !d_probes)) fail(DADE_GPU_INVALID_INPUT, "coarse_probes: null argument");
+        c->use_device();
+        if (nq == 0) return;
+        const float* d_q = stage_queries(c, d_queries, nq, c->dim, flags);
+        coarse_rank(c, d_q, nq, n_probe);
+        if (c->coarse_tc_used) {  // boundary-candidate overflow (pathological ties): all-exact ranking
+            enqueue_flags(c);
+            cuda_check(cudaStreamSynchronize(c->stream), "coarse");
+            if (c->h_flags[1]) {
+                c->coarse_force_exact = true;
+                try {
+                    coarse_rank(c, d_q, nq, n_probe);
+                } catch (...) {
+                    c->coarse_force_exact = false;
+                    throw;
+                }
+                c->coarse_force_exact = false;
+            }
+        }
+        cuda_check(cudaMemcpyAsync(d_probes, c->probes.p, (size_t)nq * n_probe * 8, cudaMemcpyDeviceToDevice, c->stream),
+                   "probes");
+        if (d_q_rot && d_q_rot != d_q)
+            cuda_check(cudaMemcpyAsync(d_q_rot, d_q, (size_t)nq * c->dim * 4, cudaMemcpyDeviceToDevice, c->stream),
+                       "rotated queries");
+    });
+}
+
+int dade_gpu_ivf_search_keys_begin(dade_gpu_ctx* c, const float* d_queries, uint32_t nq, uint32_t k,
+                                   uint32_t n_probe, uint32_t flags, const uint64_t* d_probes,
+                                   uint64_t* d_out_keys, uint32_t* d_radius) {
+    return guarded([&] {
+        check_ivf_args(c, k, n_probe);
+        if (nq && (!d_queries || !d_out_keys || !d_radius)) fail(DADE_GPU_INVALID_INPUT, "search_keys_begin: null argument");
+        if (d_probes && (flags & DADE_GPU_QUERIES_RAW))
+            fail(DADE_GPU_INVALID_INPUT, "search_keys_begin: given probes need rotated queries");
+        c->use_device();
+        c->counters.ensure(64);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+        c->sp.active = false;
+        if (nq == 0) return;
+        const float* d_q = stage_queries(c, d_queries, nq, c->dim, flags | DADE_GPU_DEVICE_PTRS);
+        if (d_probes) {  // coarse ranking done elsewhere (dade_gpu_coarse_probes on the queries' owner)
+            c->probes.ensure((size_t)nq * n_probe * 8);
+            cuda_check(cudaMemcpyAsync(c->probes.p, d_probes, (size_t)nq * n_probe * 8, cudaMemcpyDeviceToDevice,
+                                       c->stream),
+                       "probes");
+            c->probes_ready = true;
+            c->coarse_tc_used = false;
+        }
+        c->out_count.ensure((size_t)nq * 4);
+        c->surv_cap_used = 0;
+        c->split = 1;
+        try {
+            ivf_search_device(c, d_q, nq, k, n_probe, d_out_keys, c->out_count.as<uint32_t>());
+        } catch (...) {
+            c->split = 0;
+            throw;
+        }
+        c->split = 0;
+        cuda_check(cudaMemcpyAsync(d_radius, c->r_global.p, (size_t)nq * 4, cudaMemcpyDeviceToDevice, c->stream),
+                   "radius");
+        c->sp.active = true;
+        c->sp.d_q = d_q;
+        c->sp.nq = nq;
+        c->sp.k = k;
+        c->sp.n_probe = n_probe;
+        c->sp.keys = d_out_keys;
+    });
+}
+
+int dade_gpu_ivf_search_keys_end(dade_gpu_ctx* c, const uint32_t* d_radius, dade_gpu_stats* stats) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        c->use_device();
+        if (!c->sp.active) {
+            collect_stats(c, stats);  // nq == 0 (or nothing begun): nothing to scan
+            return;
+        }
+        c->sp.active = false;
+        const uint32_t nq = c->sp.nq, k = c->sp.k, n_probe = c->sp.n_probe;
+        if (d_radius) {
+            min_u32_kernel<<<(nq + 255) / 256, 256, 0, c->stream>>>(c->r_global.as<uint32_t>(), d_radius, nq);
+            cuda_check(cudaGetLastError(), "radius");
+        }
+        c->split = 2;
+        try {
+            ivf_search_device(c, c->sp.d_q, nq, k, n_probe, c->sp.keys, c->out_count.as<uint32_t>());
+        } catch (...) {
+            c->split = 0;
+            throw;
+        }
+        c->split = 0;
+        enqueue_flags(c);
+        cuda_check(cudaStreamSynchronize(c->stream), "search");
+        // worklist overflow / coarse ties: this shard's search is redone whole and
+        // locally (its answer is still this shard's exact top-K; only the shared
+        // radius is not used again)
+        for (int attempt = 0; search_overflowed(c) || (c->coarse_tc_used && c->h_flags[1]); ++attempt) {
+            if (attempt >= 3) fail(DADE_GPU_RUNTIME_ERROR, "survivor worklist overflow");
+            c->coarse_force_exact = c->coarse_tc_used && c->h_flags[1];
+            cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+            c->surv_cap_used = 0;
+            try {
+                ivf_search_device(c, c->sp.d_q, nq, k, n_probe, c->sp.keys, c->out_count.as<uint32_t>());
+            } catch (...) {
+                c->coarse_force_exact = false;
+                throw;
+            }
+            c->coarse_force_exact = false;
+            enqueue_flags(c);
+            cuda_check(cudaStreamSynchronize(c->stream), "search");
         }
         collect_stats(c, stats);
     });

@@ -219,6 +219,8 @@ struct GroupArgs {
     uint32_t* seed_glist;           // nullable [seed groups]: the list of each seed group
 };
 cudaError_t launch_group(const GroupArgs& g, cudaStream_t s);
+cudaError_t launch_local_probes(uint64_t* probes, uint32_t nq, uint32_t n_probe, const uint32_t* list_offsets,
+                                uint32_t n_lists, cudaStream_t s);
 
 cudaError_t launch_evaluate(const float* o, const float* q, const float* r, uint32_t n, uint32_t dim,
                             const uint32_t* cps, const double* coeff, const double* scale,

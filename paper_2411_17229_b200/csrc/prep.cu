@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
     uint64_t* d = reinterpret_cast<uint64_t*>(seed_smem);        // keys, after the tile is consumed
     const uint32_t q = blockIdx.x;
     const uint32_t list = (uint32_t)probes[(size_t)q * n_probe];
+    if (list == 0xffffffffu) return;  // no probed list on this shard (local_probes_kernel)
     const uint32_t start = list_offsets[list], len = list_offsets[list + 1] - start;
     const uint32_t n = min(len, S);
     if (n < K) return;  // too few rows for a K-th distance (uniform per CTA)
@@ -785,6 +786,40 @@ cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32
     if (n == 0) return cudaSuccess;
     dim3 grid((dim + kRotC - 1) / kRotC, (n + kRotR - 1) / kRotR);
     rotate_kernel<<<grid, 256, 0, s>>>(W, dim, in, n, out);
+    return cudaGetLastError();
+}
+
+// Sharded index (dade_gpu_set_ivf_shard): per query, the probes whose list has
+// rows on this device move to the front in probe order and the rest become
+// empty (UINT64_MAX, skipped by the grouping), so rank bucket 0 -- the seed's
+// list and the first streaming passes -- is the nearest LOCAL list. The probe
+// set, hence every FD result, is unchanged. One warp per query, in place
+// (compaction only moves entries left, after their chunk was read).
+__global__ void local_probes_kernel(uint64_t* probes, uint32_t nq, uint32_t n_probe, const uint32_t* list_offsets,
+                                    uint32_t n_lists) {
+    const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (q >= nq) return;
+    uint64_t* p = probes + (size_t)q * n_probe;
+    uint32_t n = 0;
+    for (uint32_t c0 = 0; c0 < n_probe; c0 += 32) {
+        const uint32_t i = c0 + lane;
+        const uint64_t key = i < n_probe ? p[i] : ~0ull;
+        const uint32_t list = (uint32_t)key;
+        const bool keep = i < n_probe && list < n_lists && list_offsets[list + 1] > list_offsets[list];
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) p[n + __popc(bal & ((1u << lane) - 1u))] = key;
+        n += __popc(bal);
+        __syncwarp();
+    }
+    for (uint32_t i = n + lane; i < n_probe; i += 32) p[i] = ~0ull;
+}
+
+cudaError_t launch_local_probes(uint64_t* probes, uint32_t nq, uint32_t n_probe, const uint32_t* list_offsets,
+                                uint32_t n_lists, cudaStream_t s) {
+    if (nq == 0 || n_probe == 0) return cudaSuccess;
+    local_probes_kernel<<<(unsigned)(((size_t)nq * 32 + 255) / 256), 256, 0, s>>>(probes, nq, n_probe, list_offsets,
+                                                                                 n_lists);
     return cudaGetLastError();
 }
 

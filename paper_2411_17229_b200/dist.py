@@ -62,17 +62,69 @@ def ivf_search_keys(dev, d_queries, nq: int, k: int, n_probe: int, out_keys, raw
         stats._add(st)
 
 
+def coarse_probes(dev, d_queries, nq: int, n_probe: int, q_rot_out, probes_out, raw: bool = False) -> None:
+    """Rotation (raw) + coarse ranking of nq queries: rotated rows -> q_rot_out [nq, D],
+    probe keys -> probes_out (int64 [nq, n_probe])."""
+    flags = _capi.DEVICE_PTRS | (_capi.QUERIES_RAW if raw else 0)
+    _capi.check(_capi.lib.dade_gpu_coarse_probes(dev.h, _capi.ptr(d_queries), nq, n_probe, flags,
+                                                 _capi.ptr(q_rot_out), _capi.ptr(probes_out)))
+
+
+def ivf_search_keys_begin(dev, d_queries, nq: int, k: int, n_probe: int, out_keys, radius,
+                          raw: bool = False, probes=None) -> None:
+    """Phase 1 of a shard's search: every query's nearest list if it is local
+    (nearest LOCAL list without given probes); per-query radius -> radius (int32 [nq])."""
+    flags = _capi.DEVICE_PTRS | (_capi.QUERIES_RAW if raw else 0)
+    _capi.check(_capi.lib.dade_gpu_ivf_search_keys_begin(dev.h, _capi.ptr(d_queries), nq, k, n_probe, flags,
+                                                         _capi.ptr(probes), _capi.ptr(out_keys), _capi.ptr(radius)))
+
+
+def ivf_search_keys_end(dev, radius, stats=None) -> None:
+    """Phase 2: the other local lists with the (min-reduced) radius; completes out_keys."""
+    st = _capi.Stats()
+    _capi.check(_capi.lib.dade_gpu_ivf_search_keys_end(dev.h, _capi.ptr(radius),
+                                                       C.byref(st) if stats is not None else None))
+    if stats is not None:
+        stats._add(st)
+
+
 def sharded_ivf_search(dev, group, d_queries, nq: int, k: int, n_probe: int, raw: bool = False):
-    """Local scan + NCCL all-gather + device merge. Returns CUDA (ids, dists, counts)."""
+    """List-sharded IVF-DADE search, query-owner scheme. Every rank owns nq
+    queries (its slice of the job, d_queries on its GPU) and a shard of the
+    lists (dade_gpu_set_ivf_shard):
+      1. rotation + coarse ranking of its own slice (dade_gpu_coarse_probes);
+      2. NCCL all-gather of the rotated slices and their probe keys;
+      3. phase 1 over all queries: the shard owning a query's nearest list
+         seeds it and scans that list; NCCL all-reduce(MIN) of the radius;
+      4. phase 2: every shard scans its other probed lists with that radius;
+      5. NCCL all-to-all of the packed top-K keys (each query's block goes to
+         its owner) and the device merge of the world's blocks.
+    Per-rank work stays that of one GPU on nq queries as the world grows
+    (weak scaling). The context must run on torch's current stream
+    (Device.set_stream), which NCCL uses too. Returns CUDA (ids, dists,
+    counts) for this rank's own queries."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    keys = torch.empty((nq, k), dtype=torch.int64, device=d_queries.device)
-    ivf_search_keys(dev, d_queries, nq, k, n_probe, keys, raw=raw)
-    gathered = torch.empty((world, nq, k), dtype=torch.int64, device=d_queries.device)
-    dist.all_gather_into_tensor(gathered, keys, group=group)
-    ids = torch.empty((nq, k), dtype=torch.int32, device=d_queries.device)
-    dists = torch.empty((nq, k), dtype=torch.float32, device=d_queries.device)
-    counts = torch.empty((nq,), dtype=torch.int32, device=d_queries.device)
-    merge_keys_device(dev, gathered, nq, k, ids, dists, counts)
+    dev_t = d_queries.device
+    dim = d_queries.shape[1]
+    q_rot = torch.empty((nq, dim), dtype=torch.float32, device=dev_t)
+    probes = torch.empty((nq, n_probe), dtype=torch.int64, device=dev_t)
+    coarse_probes(dev, d_queries, nq, n_probe, q_rot, probes, raw=raw)
+    q_all = torch.empty((world * nq, dim), dtype=torch.float32, device=dev_t)
+    p_all = torch.empty((world * nq, n_probe), dtype=torch.int64, device=dev_t)
+    dist.all_gather_into_tensor(q_all, q_rot, group=group)
+    dist.all_gather_into_tensor(p_all, probes, group=group)
+    n_all = world * nq
+    keys = torch.empty((n_all, k), dtype=torch.int64, device=dev_t)
+    radius = torch.empty((n_all,), dtype=torch.int32, device=dev_t)
+    ivf_search_keys_begin(dev, q_all, n_all, k, n_probe, keys, radius, probes=p_all)
+    dist.all_reduce(radius, op=dist.ReduceOp.MIN, group=group)  # fp32 bits >= 0 order as int32
+    ivf_search_keys_end(dev, radius)
+    recv = torch.empty((world, nq, k), dtype=torch.int64, device=dev_t)
+    dist.all_to_all_single(recv, keys, group=group)  # rows [j*nq, (j+1)*nq) -> rank j
+    ids = torch.empty((nq, k), dtype=torch.int32, device=dev_t)
+    dists = torch.empty((nq, k), dtype=torch.float32, device=dev_t)
+    counts = torch.empty((nq,), dtype=torch.int32, device=dev_t)
+    merge_keys_device(dev, recv, nq, k, ids, dists, counts)
     return ids, dists, counts

@@ -2,8 +2,12 @@
 lists sharded by plan_list_shards, every rank scans its own lists for all
 queries (centroids replicated), per-rank top-K packed as (float_bits << 32 | id)
 keys, all-gathered, merged to the global top-K — gives exactly the unsharded
-FD answer. The per-rank scan here is the oracle (checker); on GPUs it is
-libdade_gpu's ivf_search_keys + an NCCL all-gather + dade_gpu_merge_keys."""
+FD answer, also when every rank drops its candidates beyond the per-query
+radius all-reduced (MIN) after its nearest local list, and when the per-shard
+keys go to each query's owner rank by an all-to-all. The per-rank scan here is
+the oracle (checker); on GPUs it is libdade_gpu's coarse_probes, NCCL
+all-gathers, ivf_search_keys_begin, an NCCL all-reduce of the radius,
+ivf_search_keys_end, an NCCL all-to-all and dade_gpu_merge_keys."""
 import os
 import socket
 
@@ -56,12 +60,52 @@ def worker(rank, world, port, result):
     off, ids, sto = shard_index(fx["offsets"], fx["ids"], fx["storage"], dim, owner == rank)
     o = Oracle()
     li, ld, lc, _ = o.ivf_search(fx["centroids"], off, ids, sto, fx["queries"], k, npb)
+    # two-phase scheme (dade_gpu_ivf_search_keys_begin/_end): phase 1 = each query's
+    # nearest LOCAL probed list -> radius; all-reduce MIN of the radius' fp32 bits
+    # as int32; phase 2 keeps only candidates within the reduced radius (FD: prune
+    # iff dist > r), phase-1 results always kept
+    qs = fx["queries"]
+    cen = fx["centroids"].reshape(-1, dim).astype(np.float64)
+    d2c = ((qs.astype(np.float64)[:, None, :] - cen[None]) ** 2).sum(2)
+    probes = np.lexsort((np.tile(np.arange(cen.shape[0]), (qs.shape[0], 1)), d2c), axis=1)[:, :npb]
+    nonempty = np.diff(off.astype(np.int64)) > 0
+    rad = np.full(qs.shape[0], np.inf, np.float32)
+    near = np.full(qs.shape[0], -1)
+    rows = sto.reshape(-1, dim)
+    for q in range(qs.shape[0]):
+        loc = [l for l in probes[q] if nonempty[l]]
+        if not loc:
+            continue
+        near[q] = loc[0]
+        a, b = off[loc[0]], off[loc[0] + 1]
+        dd = np.sqrt(((rows[a:b].astype(np.float64) - qs[q]) ** 2).sum(1))
+        if b - a >= k:
+            rad[q] = np.float32(np.sort(dd)[k - 1] * (1 + 1e-6))
+    r_bits = torch.from_numpy(rad.view(np.int32).copy())
+    dist.all_reduce(r_bits, op=dist.ReduceOp.MIN)
+    r_glob = r_bits.numpy().view(np.float32)
+    assert np.all(r_glob <= rad)
+    for q in range(qs.shape[0]):
+        keep = []
+        for i in range(int(lc[q])):
+            a, b = (off[near[q]], off[near[q] + 1]) if near[q] >= 0 else (0, 0)
+            in_near = np.any(ids[a:b] == li[q, i])
+            if in_near or ld[q, i] <= r_glob[q]:
+                keep.append(i)
+        li[q, :len(keep)], ld[q, :len(keep)] = li[q, keep], ld[q, keep]
+        lc[q] = len(keep)
     keys = torch.from_numpy(pack(li, ld, lc, k).view(np.int64))
-    gathered = [torch.empty_like(keys) for _ in range(world)]
-    dist.all_gather(gathered, keys)
+    # query-owner exchange (dist.sharded_ivf_search): all-to-all sends rows
+    # [j * nq_loc, (j + 1) * nq_loc) of every rank's keys to rank j, which merges
+    # its own queries; the owners' answers are gathered here only to check them
+    nq_loc = qs.shape[0] // world
+    recv = torch.empty((world, nq_loc, k), dtype=torch.int64)
+    dist.all_to_all_single(recv, keys.contiguous())
+    own = torch.from_numpy(merge([b.numpy().view(np.uint64) for b in recv], k).view(np.int64))
+    gathered = [torch.empty_like(own) for _ in range(world)]
+    dist.all_gather(gathered, own)
     if rank == 0:
-        merged = merge([g.numpy().view(np.uint64) for g in gathered], k)
-        result.put(merged)
+        result.put(np.concatenate([g.numpy().view(np.uint64) for g in gathered]))
     dist.barrier()
     dist.destroy_process_group()
 

@@ -1,44 +1,214 @@
-"""Run one search of a BASELINE config end to end on the GPU (IVF or flat), report
-time, recall against exact ground truth and the reference's recall on a sample
-(diagnostic; the bench line itself is config 1).
-    python tools/config_check.py config2 [n_ref_queries]"""
-import os, sys, time, tempfile
+"""One BASELINE config end to end on one B200: device throughput (inputs resident,
+CUDA events, L2 flushed), pipelined host-buffer throughput (dade_gpu_ivf_search_batches),
+recall against exact ground truth, and the reference library on a 1-thread query
+sample of the same artifacts (recall parity). With --shards G..., the sharded
+configs are also run shard by shard on this one GPU (list masks for IVF, row
+blocks for flat): per-shard device time, the on-device G*K -> K key merge, and
+FD-mode bit-identity of the merged answer with the unsharded one. The
+per-shard times are a PROJECTION of a G-GPU run (no NCCL, one GPU), labelled so.
+Prints one JSON line.
+    python tools/config_check.py config2 [--ref-s 10] [--shards 2 4 8] [--nq N]"""
+import argparse, ctypes, json, os, sys, tempfile, time
 from pathlib import Path
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2411_17229_b200 as gp
-from paper_2411_17229_b200 import workloads as W
+from paper_2411_17229_b200 import _capi, workloads as W
+from paper_2411_17229_b200 import dist as gdist
+import bench
 
-name = sys.argv[1] if len(sys.argv) > 1 else "config2"
-n_ref = int(sys.argv[2]) if len(sys.argv) > 2 else 50
-cfg = W.CONFIGS[name]
+ap = argparse.ArgumentParser()
+ap.add_argument("config")
+ap.add_argument("--ref-s", type=float, default=10.0)
+ap.add_argument("--shards", type=int, nargs="*", default=[])
+ap.add_argument("--nq", type=int, default=None)
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--fd-check", type=int, default=2000, help="queries in the FD sharded bit-identity check")
+args = ap.parse_args()
+cfg = W.CONFIGS[args.config]
 dev = gp.Device(0)
-art = W.build(cfg, dev, torch.device("cuda:0"), with_gt=True, log=print)
+device = torch.device("cuda:0")
+t0 = time.time()
+art = W.build(cfg, dev, device, with_gt=True, nq=args.nq, log=lambda *a: print(*a, file=sys.stderr))
+build_s = time.time() - t0
 dco = gp.DadeStrategy(art.transform, art.cal, cfg.delta_d, dev=dev)
-q = art.q_rot.cpu().numpy()
+art.transform.upload(dev)
+nq, k = art.q_raw.shape[0], cfg.k
+q_dev = art.q_raw.contiguous()
+flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
+flags = _capi.QUERIES_RAW | _capi.DEVICE_PTRS
+out_keys = torch.empty((nq, k), dtype=torch.int64, device=device)
+ids_d = torch.empty((nq, k), dtype=torch.int32, device=device)
+dst_d = torch.empty((nq, k), dtype=torch.float32, device=device)
+cnt_d = torch.empty((nq,), dtype=torch.int32, device=device)
+
 if cfg.flat:
     idx = gp.FlatIndex(dev, art.base_rot.cpu().numpy())
-    run = lambda: idx.search_batch(q, cfg.k, dco)
 else:
     idx = gp.IvfIndex(dev, cfg.dim, cfg.n, cfg.nlist, art.centroids, art.offsets, art.ids, art.storage)
-    run = lambda: idx.search_batch(q, cfg.k, cfg.nprobe, dco)
-for _ in range(2):
-    ids, d, cnt = run()
-torch.cuda.synchronize()
-t0 = time.perf_counter()
-ids, d, cnt = run()
-dt = time.perf_counter() - t0
-gt = art.gt
-rec = np.mean([len(set(ids[i, :cnt[i]].tolist()) & set(gt[i].tolist())) / cfg.k for i in range(len(gt))])
-print(f"{name}: {len(q)} queries in {dt * 1e3:.2f} ms (host buffers, incl. copies) -> {len(q) / dt:.0f} q/s, recall@{cfg.k} {rec:.4f}")
 
-if os.environ.get("DADE_GPU_PHASES") == "1":
-    from paper_2411_17229_b200 import _capi
-    buf = np.zeros(16, np.uint64)
-    _capi.check(_capi.lib.dade_gpu_debug_counters(dev.h, _capi.ptr(buf)))
-    c = [int(x) for x in buf[8:16]]
-    us = lambda x: x / 148 / 1.9e3
-    print(f"last pass per CTA: items {c[0] / 148:.1f} stage {us(c[1]):.1f} us | mma wait: bready {us(c[2]):.1f} "
-          f"accempty {us(c[3]):.1f} afull {us(c[4]):.1f} us | epi warp0 wait: meta {us(c[5]):.1f} acc {us(c[6]):.1f} us "
-          f"| tma wait aempty {us(c[7]):.1f} us")
+
+def search_dev(q=q_dev, n=nq, keys=None):
+    if keys is not None:
+        if cfg.flat:
+            _capi.check(_capi.lib.dade_gpu_flat_search_keys(dev.h, _capi.ptr(q), n, k, flags, _capi.ptr(keys), None))
+        else:
+            _capi.check(_capi.lib.dade_gpu_ivf_search_keys(dev.h, _capi.ptr(q), n, k, cfg.nprobe, flags,
+                                                           _capi.ptr(keys), None))
+        return
+    if cfg.flat:
+        _capi.check(_capi.lib.dade_gpu_flat_search(dev.h, _capi.ptr(q), n, k, flags, _capi.ptr(ids_d),
+                                                   _capi.ptr(dst_d), _capi.ptr(cnt_d), None))
+    else:
+        _capi.check(_capi.lib.dade_gpu_ivf_search(dev.h, _capi.ptr(q), n, k, cfg.nprobe, flags, _capi.ptr(ids_d),
+                                                  _capi.ptr(dst_d), _capi.ptr(cnt_d), None))
+
+
+def timed(fn, reps=args.reps):
+    fn()
+    fn()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+dev.apply(dco)
+dev.set_stream(torch.cuda.current_stream().cuda_stream)
+ms = timed(search_dev)
+rec = bench.recall(ids_d.cpu().numpy().astype(np.uint32), cnt_d.cpu().numpy().astype(np.uint32), art.gt)
+line = {"config": cfg.describe(), "n_queries": nq, "build_s": round(build_s, 1),
+        "device": {"ms_per_batch": ms, "queries_per_s": nq / ms * 1e3, "recall_at_k": rec,
+                   "timing": "CUDA events, raw queries resident, L2 flushed, median of %d" % args.reps}}
+
+# pipelined host-buffer path (IVF)
+if not cfg.flat:
+    dev.set_stream(None)
+    qh = torch.empty((nq, cfg.dim), dtype=torch.float32, pin_memory=True)
+    qh.copy_(art.q_raw.cpu())
+    outs = [tuple(torch.empty(s, dtype=t, pin_memory=True) for s, t in
+                  (((nq, k), torch.int32), ((nq, k), torch.float32), ((nq,), torch.int32))) for _ in range(2)]
+    nb = 16
+    idx.search_batches([qh] * 2, k, cfg.nprobe, dco, raw=True, outputs=outs)
+    t1 = time.perf_counter()
+    idx.search_batches([qh] * nb, k, cfg.nprobe, dco, raw=True, outputs=[outs[b % 2] for b in range(nb)])
+    dt = time.perf_counter() - t1
+    line["e2e_pipelined"] = {"batches": nb, "ms_per_batch": 1e3 * dt / nb, "queries_per_s": nb * nq / dt,
+                             "recall_at_k": bench.recall(outs[(nb - 1) % 2][0].numpy().astype(np.uint32),
+                                                         outs[(nb - 1) % 2][2].numpy().astype(np.uint32), art.gt)}
+    dev.set_stream(torch.cuda.current_stream().cuda_stream)
+
+# reference on a 1-thread sample of the same artifacts
+if args.ref_s > 0 and not cfg.flat:
+    tmp = Path(tempfile.mkdtemp(prefix="dade_cc_"))
+    ref, ivf, strat, _keep = bench.reference_setup(art, tmp)
+    q_rot = art.q_rot.cpu().numpy()
+    sidx, rids, rcnt, rst, sec = bench.reference_sample(ivf, strat, q_rot, cfg, 1, args.ref_s)
+    ids_np = ids_d.cpu().numpy().astype(np.uint32)
+    cnt_np = cnt_d.cpu().numpy().astype(np.uint32)
+    line["reference"] = {"queries_per_s_1thread": len(sidx) / sec, "sample": int(len(sidx)),
+                         "recall_at_k": bench.recall(rids, rcnt, art.gt[sidx]),
+                         "ours_recall_at_k_same_sample": bench.recall(ids_np[sidx], cnt_np[sidx], art.gt[sidx])}
+elif cfg.flat:
+    line["reference"] = {"note": "flat linear_scan reference not sampled here (2M x 768 per query); "
+                                 "tests/test_gpu_parity.py checks the flat path against the oracle"}
+
+# sharded projection (one GPU, shard by shard; one context per shard)
+def ev_time(fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+if args.shards and not cfg.flat:
+    from paper_2411_17229_b200.dist import coarse_probes, ivf_search_keys_begin, ivf_search_keys_end
+    fd_check = min(args.fd_check, nq)
+    del idx
+    shard_out = []
+    cur = torch.cuda.current_stream().cuda_stream
+    for G in args.shards:
+        if nq % G:
+            continue
+        nl = nq // G  # strong scaling: rank r owns queries [r nl, (r + 1) nl)
+        owner = gdist.plan_list_shards(art.offsets, G, cfg.dim)
+        ctxs = []
+        for r in range(G):
+            d = gp.Device(0)
+            i = gp.IvfIndex(d, cfg.dim, cfg.n, cfg.nlist, art.centroids, art.offsets, art.ids, art.storage)
+            i.shard((owner == r).astype(np.uint8))
+            art.transform.upload(d)
+            d.set_stream(cur)
+            ctxs.append((d, i, gp.DadeStrategy(art.transform, art.cal, cfg.delta_d, dev=d)))
+
+        def query_owner_search(qsrc, n, strat_of, timing):
+            m = n // G
+            q_rot = torch.empty((n, cfg.dim), dtype=torch.float32, device=device)
+            pr = torch.empty((n, cfg.nprobe), dtype=torch.int64, device=device)
+            keys = torch.empty((G, n, k), dtype=torch.int64, device=device)
+            rads = torch.empty((G, n), dtype=torch.int32, device=device)
+            t = {"coarse": [], "phase1": [], "phase2": [], "merge": []}
+            for r, (d, _, st) in enumerate(ctxs):
+                d.apply(strat_of(d, st))
+                sl = slice(r * m, (r + 1) * m)
+                t["coarse"].append(ev_time(lambda: coarse_probes(d, qsrc[sl].contiguous(), m, cfg.nprobe, q_rot[sl], pr[sl], raw=True)))
+            for r, (d, _, _) in enumerate(ctxs):  # all-gather stands as the shared q_rot / pr
+                t["phase1"].append(ev_time(lambda: ivf_search_keys_begin(d, q_rot, n, k, cfg.nprobe, keys[r], rads[r], probes=pr)))
+            rads.copy_(rads.min(0).values[None].expand(G, n))  # all-reduce MIN
+            for r, (d, _, _) in enumerate(ctxs):
+                t["phase2"].append(ev_time(lambda: ivf_search_keys_end(d, rads[r])))
+            ids_o = torch.empty((n, k), dtype=torch.int32, device=device)
+            dst_o = torch.empty((n, k), dtype=torch.float32, device=device)
+            cnt_o = torch.empty((n,), dtype=torch.int32, device=device)
+            for r, (d, _, _) in enumerate(ctxs):  # all-to-all: rank r merges its queries' G blocks
+                sl = slice(r * m, (r + 1) * m)
+                recv = keys[:, sl].contiguous()
+                t["merge"].append(ev_time(lambda: gdist.merge_keys_device(d, recv, m, k, ids_o[sl], dst_o[sl], cnt_o[sl])))
+            return ids_o, dst_o, cnt_o, t
+
+        runs = []
+        for rep in range(3):
+            flush.zero_()
+            ids_o, dst_o, cnt_o, t = query_owner_search(q_dev, nq, lambda d, st: st, True)
+            runs.append((sum(max(v) for v in t.values()), t))
+        tot, t = min(runs, key=lambda x: x[0])
+        rec_g = bench.recall(ids_o.cpu().numpy().astype(np.uint32), cnt_o.cpu().numpy().astype(np.uint32), art.gt)
+        # FD: merged shards == unsharded, bit for bit (first fd_check queries, rounded to G)
+        m_fd = fd_check // G * G
+        fi, fdst, fc, _ = query_owner_search(q_dev[:m_fd], m_fd, lambda d, st: gp.FdScanningStrategy(cfg.dim), False)
+        del ctxs
+        ref_d = gp.Device(0)
+        ref_i = gp.IvfIndex(ref_d, cfg.dim, cfg.n, cfg.nlist, art.centroids, art.offsets, art.ids, art.storage)
+        art.transform.upload(ref_d)
+        ref_d.apply(gp.FdScanningStrategy(cfg.dim))
+        rkeys = torch.empty((1, m_fd, k), dtype=torch.int64, device=device)
+        _capi.check(_capi.lib.dade_gpu_ivf_search_keys(ref_d.h, _capi.ptr(q_dev), m_fd, k, cfg.nprobe, flags,
+                                                       _capi.ptr(rkeys), None))
+        out2 = [torch.empty_like(x) for x in (fi, fdst, fc)]
+        gdist.merge_keys_device(dev, rkeys, m_fd, k, *out2)
+        same = all(torch.equal(a.view(torch.int32), b.view(torch.int32)) for a, b in zip((fi, fdst, fc), out2))
+        del ref_i, ref_d
+        shard_out.append({"G": G, "queries_per_rank": nl, **{k_ + "_ms": [round(x, 3) for x in v] for k_, v in t.items()},
+                          "projected_ms": tot, "recall_at_k": rec_g,
+                          "fd_merged_equals_unsharded": bool(same), "fd_check_queries": m_fd,
+                          "projected_queries_per_s": nq / tot * 1e3,
+                          "projected_strong_scaling_eff": (ms / tot) / G})
+    line["sharded_projection"] = {
+        "note": "one B200, query-owner scheme of dist.sharded_ivf_search with each shard in its own context: "
+                "coarse ranking of each rank's query slice, phase 1 of every shard over all queries (the owner of "
+                "a query's nearest list seeds it), MIN of the radii, phase 2 of every shard, per-owner key merge; "
+                "projected G-GPU time = sum over stages of the slowest rank (strong scaling: the job's queries "
+                "split over the ranks); the NCCL collectives (all-gather of rotated queries and probes, "
+                "all-reduce of nq*4 B, all-to-all of nq*K*8 B) are not included", "runs": shard_out}
+print(json.dumps(line), flush=True)
