@@ -14,6 +14,7 @@
 //      probes, bit-identical to the reference ranking.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -411,6 +412,238 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
     for (uint32_t i = lane; i < n_probe; i += 32) probes[(size_t)qi * n_probe + i] = kk[i];
 }
 
+// Large-nlist path (1024 < n_cen <= 16384, dim % 4 == 0), CTA (8 warps) per
+// query, every p~ of the query read once into registers (V per thread,
+// centroid c = tid + 256 j):
+//   * T0 = n_probe-th smallest of the 256 per-thread minima of the upper
+//     bounds hi: an upper bound of B (the n_probe smallest minima are n_probe
+//     distinct values <= T0), so the values <= T0 (a few hundred) hold B;
+//   * B = n_probe-th smallest hi among them (warp radix select);
+//   * candidates lo <= B, exact sequential l2_sq (a warp per 32 candidates,
+//     rows staged through shared memory), (acc, id) bitonic sort, first n_probe.
+// Same answer as the warp-per-query kernels, bit for bit.
+__device__ __forceinline__ uint32_t warp_select_smem(const uint32_t* v, uint32_t n, uint32_t rank, uint32_t* hist,
+                                                     uint32_t lane) {
+    uint32_t lo = 0xffffffffu, hi = 0;
+    for (uint32_t i = lane; i < n; i += 32) {
+        lo = min(lo, v[i]);
+        hi = max(hi, v[i]);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (hi <= lo) return lo;
+    const int top = (31 - __clz(lo ^ hi)) & ~7;
+    uint32_t mask = top >= 24 ? 0u : ~0u << (top + 8), prefix = lo & mask;
+    for (int shift = top; shift >= 0; shift -= 8) {
+        for (uint32_t j = lane; j < 256; j += 32) hist[j] = 0;
+        __syncwarp();
+        for (uint32_t i = lane; i < n; i += 32)
+            if ((v[i] & mask) == prefix) atomicAdd(&hist[(v[i] >> shift) & 0xffu], 1u);
+        __syncwarp();
+        uint32_t d, before;
+        warp_hist_find(hist, rank, lane, d, before);
+        rank -= before;
+        prefix |= d << shift;
+        mask |= 0xffu << shift;
+        __syncwarp();
+    }
+    return prefix;
+}
+
+// block-wide exclusive prefix sum of one value per thread; returns the total
+template <int T>
+__device__ __forceinline__ uint32_t block_scan_bs(uint32_t x, uint32_t* wsum, uint32_t& excl) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = x;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= (uint32_t)off) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    uint32_t base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < T / 32; ++w) {
+        if ((uint32_t)w < warp) base += wsum[w];
+        tot += wsum[w];
+    }
+    excl = base + incl - x;
+    __syncthreads();
+    return tot;
+}
+
+// a load the compiler may not keep in registers across passes (cnorm is re-read
+// from L1 per pass instead of occupying V more registers)
+__device__ __forceinline__ float ld_reload(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+constexpr int kBsX = 8;  // warps of the exact stage
+template <int T, int V>
+__global__ void __launch_bounds__(T, 512 / T) coarse_select_big_kernel(
+    const float* __restrict__ pt, const float* __restrict__ cnorm, const float* __restrict__ qnorm,
+    const float* __restrict__ cen, uint32_t n_cen, const float* __restrict__ q, uint32_t nq, uint32_t dim,
+    uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow) {
+    __shared__ uint32_t s_v[kSelCap];        // thread minima, then candidate hi keys
+    __shared__ uint64_t cand[kSelCap];
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t wsum[T / 32];
+    __shared__ uint32_t s_T;
+    __shared__ __align__(16) float rows[kBsX][32 * kFsRS];
+    __shared__ __align__(16) float qch[kBsX][32];
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t qi = blockIdx.x;
+    const float* prow = pt + (size_t)qi * n_cen;
+    const float qn = qnorm[qi];
+    float p[V];
+    uint32_t tmin = 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const uint32_t c = tid + T * j;
+        p[j] = c < n_cen ? prow[c] : 0.f;
+        if (c < n_cen) tmin = min(tmin, fkey(p[j] + kCoarseDelta * (ld_reload(cnorm + c) + qn)));
+    }
+    s_v[tid] = tmin;
+    __syncthreads();
+    // T0: the n_probe-th smallest thread minimum (>= B)
+    if (warp == 0) {
+        const uint32_t t0 = n_probe <= (uint32_t)T ? warp_select_smem(s_v, T, n_probe, hist, lane) : 0xffffffffu;
+        if (lane == 0) s_T = t0;
+    }
+    __syncthreads();
+    const uint32_t T0 = s_T;
+    // the hi keys <= T0
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const uint32_t c = tid + T * j;
+        cnt += (c < n_cen && fkey(p[j] + kCoarseDelta * (ld_reload(cnorm + c) + qn)) <= T0) ? 1u : 0u;
+    }
+    uint32_t pos;
+    const uint32_t M = block_scan_bs<T>(cnt, wsum, pos);
+    if (M > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
+        if (tid == 0) atomicAdd(overflow, 1u);
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const uint32_t c = tid + T * j;
+        if (c < n_cen) {
+            const uint32_t h = fkey(p[j] + kCoarseDelta * (ld_reload(cnorm + c) + qn));
+            if (h <= T0) s_v[pos++] = h;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t b = warp_select_smem(s_v, M, n_probe, hist, lane);
+        if (lane == 0) s_T = b;
+    }
+    __syncthreads();
+    const uint32_t B = s_T;
+    // exact candidates: lo <= B
+    cnt = 0;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const uint32_t c = tid + T * j;
+        cnt += (c < n_cen && fkey(p[j] - kCoarseDelta * (ld_reload(cnorm + c) + qn)) <= B) ? 1u : 0u;
+    }
+    const uint32_t n = block_scan_bs<T>(cnt, wsum, pos);
+    if (n > (uint32_t)kSelCap) {
+        if (tid == 0) atomicAdd(overflow, 1u);
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        const uint32_t c = tid + T * j;
+        if (c < n_cen && fkey(p[j] - kCoarseDelta * (ld_reload(cnorm + c) + qn)) <= B) cand[pos++] = c;
+    }
+    __syncthreads();
+    // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43), warp per 32 candidates
+    const float* qr = q + (size_t)qi * dim;
+    float* rs = rows[warp % kBsX];
+    float* qs = qch[warp % kBsX];
+    for (uint32_t e0 = 32 * warp; e0 < n && warp < (uint32_t)kBsX; e0 += 32 * kBsX) {
+        const uint32_t e = e0 + lane;
+        const uint32_t my_c = e < n ? (uint32_t)cand[e] : 0u;
+        const uint32_t nv = min(32u, n - e0);
+        float acc = 0.f;
+        for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
+            const uint32_t w = min(32u, dim - k0);
+            const uint32_t sub = lane >> 3, c4 = lane & 7;
+            float4 v[8];
+#pragma unroll
+            for (int sg = 0; sg < 8; ++sg) {
+                const uint32_t sidx = 4 * sg + sub;
+                const uint32_t cc = __shfl_sync(0xffffffffu, my_c, sidx);
+                v[sg] = (sidx < nv && 4 * c4 < w) ? __ldg(reinterpret_cast<const float4*>(cen + (size_t)cc * dim + k0) + c4)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const float4 qv = (lane < 8 && 4u * lane < w) ? __ldg(reinterpret_cast<const float4*>(qr + k0) + lane)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            __syncwarp();
+#pragma unroll
+            for (int sg = 0; sg < 8; ++sg)
+                *reinterpret_cast<float4*>(rs + (4 * sg + sub) * kFsRS + 4 * c4) = v[sg];
+            if (lane < 8) *reinterpret_cast<float4*>(qs + 4 * lane) = qv;
+            __syncwarp();
+            if (e < n) {
+                const float* os = rs + lane * kFsRS;
+                for (uint32_t kk = 0; kk < w; kk += 4) {
+                    const float4 o4 = *reinterpret_cast<const float4*>(os + kk);
+                    const float4 q4 = *reinterpret_cast<const float4*>(qs + kk);
+                    acc = sq_step(acc, q4.x, o4.x);
+                    acc = sq_step(acc, q4.y, o4.y);
+                    acc = sq_step(acc, q4.z, o4.z);
+                    acc = sq_step(acc, q4.w, o4.w);
+                }
+            }
+        }
+        __syncwarp();
+        if (e < n) cand[e] = make_key(acc, my_c);
+    }
+    // pad and bitonic-sort the candidate keys (whole CTA)
+    uint32_t m = 1;
+    while (m < n) m <<= 1;
+    for (uint32_t e = n + tid; e < m; e += T) cand[e] = ~0ull;
+    __syncthreads();
+    for (uint32_t size = 2; size <= m; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = tid; i < m / 2; i += T) {
+                const uint32_t lo_i = 2 * i - (i & (stride - 1)), hi_i = lo_i + stride;
+                const bool up = (lo_i & size) == 0;
+                const uint64_t x = cand[lo_i], y = cand[hi_i];
+                if ((x > y) == up) { cand[lo_i] = y; cand[hi_i] = x; }
+            }
+            __syncthreads();
+        }
+    for (uint32_t i = tid; i < n_probe; i += T) probes[(size_t)qi * n_probe + i] = cand[i];
+}
+
+// the select kernel for n_cen centroids
+void launch_select_any(const float* pt, const float* cnorm, const float* qnorm, const float* centroids, uint32_t n_cen,
+                       const float* queries, uint32_t nq, uint32_t dim, uint32_t n_probe, uint64_t* probes,
+                       uint32_t* overflow, cudaStream_t s) {
+    if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap) {
+        coarse_select_fast_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
+            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow);
+        return;
+    }
+    if (n_cen <= 32u * 512 && dim % 4 == 0 && n_probe <= 256 && !std::getenv("DADE_GPU_SELECT_WARP")) {
+#define BS_LAUNCH(TT, VV) coarse_select_big_kernel<TT, VV><<<nq, TT, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, \
+                                                                              queries, nq, dim, n_probe, probes, overflow)
+        if (n_cen <= 16u * 256) BS_LAUNCH(256, 16);
+        else if (n_cen <= 32u * 256) BS_LAUNCH(256, 32);
+        else BS_LAUNCH(512, 32);
+#undef BS_LAUNCH
+        return;
+    }
+    coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe,
+                                                      probes, overflow);
+}
+
 }  // namespace
 
 cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
@@ -421,12 +654,7 @@ cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float
                                                                              cnorm, qnorm);
     dim3 grid((n_cen + kCC - 1) / kCC, (nq + kCQ - 1) / kCQ);
     coarse_tc_kernel<<<grid, 256, 0, s>>>(centroids, n_cen, queries, nq, dim, cnorm, qnorm, pt);
-    if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap)
-        coarse_select_fast_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
-            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow);
-    else
-        coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim,
-                                                          n_probe, probes, overflow);
+    launch_select_any(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, s);
     return cudaGetLastError();
 }
 
@@ -442,12 +670,7 @@ cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const f
                                  uint32_t dim, uint32_t n_probe, const float* cnorm, const float* qnorm,
                                  const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
-    if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap)
-        coarse_select_fast_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
-            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow);
-    else
-        coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim,
-                                                          n_probe, probes, overflow);
+    launch_select_any(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, s);
     return cudaGetLastError();
 }
 
