@@ -412,16 +412,18 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
     for (uint32_t i = lane; i < n_probe; i += 32) probes[(size_t)qi * n_probe + i] = kk[i];
 }
 
-// Large-nlist path (1024 < n_cen <= 16384, dim % 4 == 0), CTA (8 warps) per
-// query, every p~ of the query read once into registers (V per thread,
-// centroid c = tid + 256 j):
-//   * T0 = n_probe-th smallest of the 256 per-thread minima of the upper
-//     bounds hi: an upper bound of B (the n_probe smallest minima are n_probe
-//     distinct values <= T0), so the values <= T0 (a few hundred) hold B;
-//   * B = n_probe-th smallest hi among them (warp radix select);
-//   * candidates lo <= B, exact sequential l2_sq (a warp per 32 candidates,
-//     rows staged through shared memory), (acc, id) bitonic sort, first n_probe.
-// Same answer as the warp-per-query kernels, bit for bit.
+// Large-nlist path (1024 < n_cen <= 16384, dim % 4 == 0), warp per query:
+//   * one pass over the query's p~ row keeps, per lane and 512-centroid chunk,
+//     the minimum upper bound hi of its 16 centroids (<= 32 chunk minima per
+//     lane, <= 1024 per query);
+//   * T0 = n_probe-th smallest of those minima bounds B from above (the
+//     n_probe smallest minima are n_probe distinct hi values <= T0);
+//   * a second pass (the row is L2-hot) keeps the centroids with lo <= T0
+//     (~n_probe of them): every hi <= B is among them (lo <= hi), so B is
+//     their n_probe-th smallest hi; candidates lo <= B get the exact
+//     sequential l2_sq, (acc, id) sort, first n_probe -> probes.
+// Same answer as coarse_select_kernel, bit for bit.
+constexpr int kWdChunk = 512;  // centroids per chunk (16 per lane)
 __device__ __forceinline__ uint32_t warp_select_smem(const uint32_t* v, uint32_t n, uint32_t rank, uint32_t* hist,
                                                      uint32_t lane) {
     uint32_t lo = 0xffffffffu, hi = 0;
@@ -450,124 +452,116 @@ __device__ __forceinline__ uint32_t warp_select_smem(const uint32_t* v, uint32_t
     return prefix;
 }
 
-// block-wide exclusive prefix sum of one value per thread; returns the total
-template <int T>
-__device__ __forceinline__ uint32_t block_scan_bs(uint32_t x, uint32_t* wsum, uint32_t& excl) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t incl = x;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= (uint32_t)off) incl += y;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    uint32_t base = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < T / 32; ++w) {
-        if ((uint32_t)w < warp) base += wsum[w];
-        tot += wsum[w];
-    }
-    excl = base + incl - x;
-    __syncthreads();
-    return tot;
-}
-
-// a load the compiler may not keep in registers across passes (cnorm is re-read
-// from L1 per pass instead of occupying V more registers)
-__device__ __forceinline__ float ld_reload(const float* p) {
-    float v;
-    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-
-constexpr int kBsX = 8;  // warps of the exact stage
-template <int T, int V>
-__global__ void __launch_bounds__(T, 512 / T) coarse_select_big_kernel(
+__global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
     const float* __restrict__ pt, const float* __restrict__ cnorm, const float* __restrict__ qnorm,
     const float* __restrict__ cen, uint32_t n_cen, const float* __restrict__ q, uint32_t nq, uint32_t dim,
     uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow) {
-    __shared__ uint32_t s_v[kSelCap];        // thread minima, then candidate hi keys
-    __shared__ uint64_t cand[kSelCap];
-    __shared__ uint32_t hist[256];
-    __shared__ uint32_t wsum[T / 32];
-    __shared__ uint32_t s_T;
-    __shared__ __align__(16) float rows[kBsX][32 * kFsRS];
-    __shared__ __align__(16) float qch[kBsX][32];
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t qi = blockIdx.x;
+    __shared__ uint64_t cand[kFsWarps][kSelCap];
+    __shared__ __align__(16) float rows[kFsWarps][32 * kFsRS];
+    __shared__ __align__(16) float qch[kFsWarps][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t qi = blockIdx.x * kFsWarps + warp;
+    if (qi >= nq) return;
     const float* prow = pt + (size_t)qi * n_cen;
     const float qn = qnorm[qi];
-    float p[V];
-    uint32_t tmin = 0xffffffffu;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(rows[warp]);    // 256 words
+    uint32_t* hv = hist + 256;                                   // <= 512 hi keys (fits: 768 <= 32 * kFsRS)
+    // pass 1: chunk minima of hi
+    uint32_t gm[32];
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-        const uint32_t c = tid + T * j;
-        p[j] = c < n_cen ? prow[c] : 0.f;
-        if (c < n_cen) tmin = min(tmin, fkey(p[j] + kCoarseDelta * (ld_reload(cnorm + c) + qn)));
-    }
-    s_v[tid] = tmin;
-    __syncthreads();
-    // T0: the n_probe-th smallest thread minimum (>= B)
-    if (warp == 0) {
-        const uint32_t t0 = n_probe <= (uint32_t)T ? warp_select_smem(s_v, T, n_probe, hist, lane) : 0xffffffffu;
-        if (lane == 0) s_T = t0;
-    }
-    __syncthreads();
-    const uint32_t T0 = s_T;
-    // the hi keys <= T0
-    uint32_t cnt = 0;
+    for (int j = 0; j < 32; ++j) {
+        uint32_t m = 0xffffffffu;
+        if ((uint32_t)j * kWdChunk < n_cen) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-        const uint32_t c = tid + T * j;
-        cnt += (c < n_cen && fkey(p[j] + kCoarseDelta * (ld_reload(cnorm + c) + qn)) <= T0) ? 1u : 0u;
+            for (int i = 0; i < kWdChunk / 32; ++i) {
+                const uint32_t c = j * kWdChunk + i * 32 + lane;
+                if (c < n_cen) m = min(m, fkey(prow[c] + kCoarseDelta * (cnorm[c] + qn)));
+            }
+        }
+        gm[j] = m;
     }
-    uint32_t pos;
-    const uint32_t M = block_scan_bs<T>(cnt, wsum, pos);
-    if (M > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
-        if (tid == 0) atomicAdd(overflow, 1u);
-        return;
-    }
+    // T0 = n_probe-th smallest chunk minimum (radix select over registers)
+    uint32_t kmin = 0xffffffffu, kmax = 0;
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-        const uint32_t c = tid + T * j;
-        if (c < n_cen) {
-            const uint32_t h = fkey(p[j] + kCoarseDelta * (ld_reload(cnorm + c) + qn));
-            if (h <= T0) s_v[pos++] = h;
+    for (int j = 0; j < 32; ++j) {
+        kmin = min(kmin, gm[j]);
+        if (gm[j] != 0xffffffffu) kmax = max(kmax, gm[j]);
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    uint32_t T0 = kmin;
+    if (kmax > kmin) {
+        const int top = (31 - __clz(kmin ^ kmax)) & ~7;
+        uint32_t mask = top >= 24 ? 0u : ~0u << (top + 8), rem = n_probe;
+        T0 = kmin & mask;
+        for (int shift = top; shift >= 0; shift -= 8) {
+            for (uint32_t j = lane; j < 256; j += 32) hist[j] = 0;
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if ((gm[j] & mask) == T0) atomicAdd(&hist[(gm[j] >> shift) & 0xffu], 1u);
+            __syncwarp();
+            uint32_t d, before;
+            warp_hist_find(hist, rem, lane, d, before);
+            rem -= before;
+            T0 |= d << shift;
+            mask |= 0xffu << shift;
+            __syncwarp();
         }
     }
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t b = warp_select_smem(s_v, M, n_probe, hist, lane);
-        if (lane == 0) s_T = b;
+    // pass 2: centroids with lo <= T0 -> (p~ bits, id)
+    uint32_t n = 0;
+    for (uint32_t c0 = 0; c0 < n_cen; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        float pv = 0.f;
+        bool is = false;
+        if (c < n_cen) {
+            pv = prow[c];
+            is = fkey(pv - kCoarseDelta * (cnorm[c] + qn)) <= T0;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, is);
+        const uint32_t pos = n + __popc(bal & ((1u << lane) - 1u));
+        if (is && pos < (uint32_t)kSelCap) cand[warp][pos] = (static_cast<uint64_t>(__float_as_uint(pv)) << 32) | c;
+        n += __popc(bal);
     }
-    __syncthreads();
-    const uint32_t B = s_T;
-    // exact candidates: lo <= B
-    cnt = 0;
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-        const uint32_t c = tid + T * j;
-        cnt += (c < n_cen && fkey(p[j] - kCoarseDelta * (ld_reload(cnorm + c) + qn)) <= B) ? 1u : 0u;
-    }
-    const uint32_t n = block_scan_bs<T>(cnt, wsum, pos);
-    if (n > (uint32_t)kSelCap) {
-        if (tid == 0) atomicAdd(overflow, 1u);
+    if (n > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
+        if (lane == 0) atomicAdd(overflow, 1u);
         return;
     }
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-        const uint32_t c = tid + T * j;
-        if (c < n_cen && fkey(p[j] - kCoarseDelta * (ld_reload(cnorm + c) + qn)) <= B) cand[pos++] = c;
+    __syncwarp();
+    for (uint32_t e = lane; e < n; e += 32) {
+        const uint64_t v = cand[warp][e];
+        const uint32_t c = (uint32_t)v;
+        hv[e] = fkey(__uint_as_float((uint32_t)(v >> 32)) + kCoarseDelta * (cnorm[c] + qn));
     }
-    __syncthreads();
-    // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43), warp per 32 candidates
-    const float* qr = q + (size_t)qi * dim;
-    float* rs = rows[warp % kBsX];
-    float* qs = qch[warp % kBsX];
-    for (uint32_t e0 = 32 * warp; e0 < n && warp < (uint32_t)kBsX; e0 += 32 * kBsX) {
+    __syncwarp();
+    const uint32_t B = warp_select_smem(hv, n, n_probe, hist, lane);
+    // candidates lo <= B, compacted in place (ids)
+    uint32_t m2 = 0;
+    for (uint32_t e0 = 0; e0 < n; e0 += 32) {
         const uint32_t e = e0 + lane;
-        const uint32_t my_c = e < n ? (uint32_t)cand[e] : 0u;
+        uint32_t c = 0;
+        bool is = false;
+        if (e < n) {
+            const uint64_t v = cand[warp][e];
+            c = (uint32_t)v;
+            is = fkey(__uint_as_float((uint32_t)(v >> 32)) - kCoarseDelta * (cnorm[c] + qn)) <= B;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, is);
+        __syncwarp();
+        if (is) cand[warp][m2 + __popc(bal & ((1u << lane) - 1u))] = c;
+        m2 += __popc(bal);
+        __syncwarp();
+    }
+    n = m2;
+    __syncwarp();
+    // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43) of the candidates
+    const float* qr = q + (size_t)qi * dim;
+    float* rs = rows[warp];
+    float* qs = qch[warp];
+    for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const uint32_t my_c = e < n ? (uint32_t)cand[warp][e] : 0u;
         const uint32_t nv = min(32u, n - e0);
         float acc = 0.f;
         for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
@@ -602,24 +596,25 @@ __global__ void __launch_bounds__(T, 512 / T) coarse_select_big_kernel(
             }
         }
         __syncwarp();
-        if (e < n) cand[e] = make_key(acc, my_c);
+        if (e < n) cand[warp][e] = make_key(acc, my_c);
     }
-    // pad and bitonic-sort the candidate keys (whole CTA)
+    __syncwarp();
     uint32_t m = 1;
     while (m < n) m <<= 1;
-    for (uint32_t e = n + tid; e < m; e += T) cand[e] = ~0ull;
-    __syncthreads();
+    for (uint32_t e = n + lane; e < m; e += 32) cand[warp][e] = ~0ull;
+    __syncwarp();
+    uint64_t* kk = cand[warp];
     for (uint32_t size = 2; size <= m; size <<= 1)
         for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (uint32_t i = tid; i < m / 2; i += T) {
+            for (uint32_t i = lane; i < m / 2; i += 32) {
                 const uint32_t lo_i = 2 * i - (i & (stride - 1)), hi_i = lo_i + stride;
                 const bool up = (lo_i & size) == 0;
-                const uint64_t x = cand[lo_i], y = cand[hi_i];
-                if ((x > y) == up) { cand[lo_i] = y; cand[hi_i] = x; }
+                const uint64_t x = kk[lo_i], y = kk[hi_i];
+                if ((x > y) == up) { kk[lo_i] = y; kk[hi_i] = x; }
             }
-            __syncthreads();
+            __syncwarp();
         }
-    for (uint32_t i = tid; i < n_probe; i += T) probes[(size_t)qi * n_probe + i] = cand[i];
+    for (uint32_t i = lane; i < n_probe; i += 32) probes[(size_t)qi * n_probe + i] = kk[i];
 }
 
 // the select kernel for n_cen centroids
@@ -631,13 +626,9 @@ void launch_select_any(const float* pt, const float* cnorm, const float* qnorm, 
             pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow);
         return;
     }
-    if (n_cen <= 32u * 512 && dim % 4 == 0 && n_probe <= 256 && !std::getenv("DADE_GPU_SELECT_WARP")) {
-#define BS_LAUNCH(TT, VV) coarse_select_big_kernel<TT, VV><<<nq, TT, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, \
-                                                                              queries, nq, dim, n_probe, probes, overflow)
-        if (n_cen <= 16u * 256) BS_LAUNCH(256, 16);
-        else if (n_cen <= 32u * 256) BS_LAUNCH(256, 32);
-        else BS_LAUNCH(512, 32);
-#undef BS_LAUNCH
+    if (n_cen <= 32u * kWdChunk && dim % 4 == 0 && n_probe <= kSelCap && !std::getenv("DADE_GPU_SELECT_WARP")) {
+        coarse_select_wide_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
+            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow);
         return;
     }
     coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe,
