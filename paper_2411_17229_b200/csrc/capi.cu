@@ -403,6 +403,7 @@ struct dade_gpu_ctx {
     RowAug aug_storage;
     SliceTmap seed_tm;
     DevBuf seed_work;  // persistent seed's group counter
+    DevBuf seed_order; // persistent seed's costliest-first group order
     DevBuf qslots;     // per-query candidate slots [nq][kQSlots] of a streaming pass
     DevBuf cand_total; // candidates of a pass (census, qslots mode)
     DevBuf flat_offsets;  // {0, b_count}: the flat base as one list
@@ -763,6 +764,10 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 sa.out_count = out_count;
                 sa.nz2 = 0x8000000080000000ull;
                 c->seed_work.ensure(4);
+                if (!env_flag("DADE_GPU_SEED_LIST_ORDER")) {  // tuning hook: groups in list order
+                    c->seed_order.ensure(((size_t)nq / kSeedGroup + g->n_lists + 1) * 4);
+                    sa.order = c->seed_order.as<uint32_t>();
+                }
                 cuda_check(launch_seed_tma(sa, *stm, nq / kSeedGroup + g->n_lists + 1, s, c->seed_work.as<uint32_t>()),
                            "seed radius (tma)");
             } else if (g && g->n_rb >= 1 && k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY"))

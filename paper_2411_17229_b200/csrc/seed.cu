@@ -456,6 +456,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
             SpGroup G;
             for (;;) {
                 b = atomicAdd(work, 1u);
+                if (b < n_groups && a.order) b = a.order[b];  // costliest groups first (shorter tail)
                 if (b >= n_groups || sp_group(a, b, G)) break;
             }
             gid[j] = b < n_groups ? b : kSpEnd;
@@ -539,6 +540,36 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
     }
 }
 
+// Costliest-first order of the seed groups for the persistent kernel's work
+// counter (LPT: the last groups handed out are the cheapest, so SMs finish
+// together). Cost = seeded rows x query pairs, counting-sorted into 64 buckets
+// by one CTA; the order inside a bucket does not matter (groups are independent).
+constexpr int kSoBins = 64;
+__global__ void __launch_bounds__(1024) seed_order_kernel(const SeedListArgs a, uint32_t* order) {
+    __shared__ uint32_t hist[kSoBins];
+    const uint32_t n_groups = a.seed_goff[a.n_lists];
+    if (threadIdx.x < kSoBins) hist[threadIdx.x] = 0;
+    __syncthreads();
+    auto bucket = [&](uint32_t b) -> uint32_t {
+        SpGroup G;
+        if (!sp_group(a, b, G)) return 0;
+        const uint32_t cost = G.n * ((G.ng + 1) >> 1);  // <= 1024 x 8
+        return min((uint32_t)kSoBins - 1, cost >> 7);
+    };
+    for (uint32_t b = threadIdx.x; b < n_groups; b += blockDim.x) atomicAdd(&hist[bucket(b)], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {  // descending buckets: exclusive prefix from the top
+        uint32_t run = 0;
+        for (int i = kSoBins - 1; i >= 0; --i) {
+            const uint32_t h = hist[i];
+            hist[i] = run;
+            run += h;
+        }
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < n_groups; b += blockDim.x) order[atomicAdd(&hist[bucket(b)], 1u)] = b;
+}
+
 }  // namespace
 
 bool seed_tma_ok(uint32_t dim, uint32_t K) { return dim <= (uint32_t)kSdMaxDim && dim % 4 == 0 && K <= (uint32_t)kSdSmall; }
@@ -559,6 +590,7 @@ cudaError_t launch_seed_tma(const SeedListArgs& a, const CUtensorMap& tmap, uint
         DADE_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
         DADE_CUDA_TRY(cudaFuncSetAttribute(seed_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp));
         DADE_CUDA_TRY(cudaMemsetAsync(work, 0, 4, s));
+        if (a.order) seed_order_kernel<<<1, 1024, 0, s>>>(a, a.order);
         seed_persist_kernel<<<std::min<uint32_t>(max_groups, (uint32_t)n_sm), kSpThreads, sp, s>>>(a, tmap, work);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess && std::getenv("DADE_GPU_VERBOSE")) {
