@@ -473,8 +473,8 @@ void coarse_tc_begin(dade_gpu_ctx* c, uint32_t nq) {
     c->cnorm.ensure((size_t)c->n_clusters * 4);
     c->qnorm.ensure((size_t)chunk * 4);
     c->coarse_lo.ensure((size_t)chunk * c->n_clusters * 4);
-    c->coarse_overflow.ensure(4);
-    cuda_check(cudaMemsetAsync(c->coarse_overflow.p, 0, 4, c->stream), "memset");
+    c->coarse_overflow.ensure(8);  // [0] overflow flag, [1] candidate census (DADE_GPU_COARSE_CENSUS)
+    cuda_check(cudaMemsetAsync(c->coarse_overflow.p, 0, 8, c->stream), "memset");
     c->coarse_tc_used = true;
 }
 // queries [q0, q0 + m) (m <= coarse_tc_chunk) -> probes rows [q0, q0 + m)
@@ -1433,6 +1433,11 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     collect_stats(c, stats);
     finish_profile(c);
     tl_print(c);
+    if (std::getenv("DADE_GPU_COARSE_CENSUS") && c->coarse_tc_used) {
+        uint32_t h[2] = {0, 0};
+        cuda_check(cudaMemcpy(h, c->coarse_overflow.p, 8, cudaMemcpyDeviceToHost), "census");
+        std::fprintf(stderr, "[dade_gpu] coarse: %.1f exact candidates per query\n", (double)h[1] / std::max(1u, nq));
+    }
 }
 
 // Pipelined sequence of searches over host batches: batch b+1's H2D (copy

@@ -280,7 +280,7 @@ constexpr int kFsRS = 36;  // floats per staged row chunk (16-byte aligned, conf
 __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
     const float* __restrict__ pt, const float* __restrict__ cnorm, const float* __restrict__ qnorm,
     const float* __restrict__ cen, uint32_t n_cen, const float* __restrict__ q, uint32_t nq, uint32_t dim,
-    uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow) {
+    uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow, uint32_t* census = nullptr) {
     __shared__ uint64_t cand[kFsWarps][kSelCap];
     __shared__ __align__(16) float rows[kFsWarps][32 * kFsRS];
     __shared__ __align__(16) float qch[kFsWarps][32];
@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
         if (is && pos < (uint32_t)kSelCap) cand[warp][pos] = lane + 32u * j;
         n += __popc(bal);
     }
+    if (census && lane == 0) atomicAdd(census, n);  // DADE_GPU_COARSE_CENSUS: exact candidates
     if (n > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
         if (lane == 0) atomicAdd(overflow, 1u);
         n = kSelCap;
@@ -623,7 +624,8 @@ void launch_select_any(const float* pt, const float* cnorm, const float* qnorm, 
                        uint32_t* overflow, cudaStream_t s) {
     if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap) {
         coarse_select_fast_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
-            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow);
+            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow,
+            std::getenv("DADE_GPU_COARSE_CENSUS") ? overflow + 1 : nullptr);
         return;
     }
     if (n_cen <= 32u * kWdChunk && dim % 4 == 0 && n_probe <= kSelCap && !std::getenv("DADE_GPU_SELECT_WARP")) {
