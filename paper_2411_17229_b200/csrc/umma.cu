@@ -571,10 +571,10 @@ __global__ void row_aug_kernel(const float* __restrict__ norms, uint32_t n, floa
 // warps 0-3 read it back (TMEM lane = centroid) and store p~ per (query, centroid)
 // for coarse_select (same values and bound as coarse_tc_kernel, coarse.cu).
 namespace {
-constexpr int kCgM = 128, kCgN = 256, kCgStages = 3;
+constexpr int kCgM = 128, kCgN = 256, kCgStages = 2;  // 2 stages: 2 CTAs per SM, one in its epilogue while the other loads
 constexpr int kCgThreads = 160;
 
-__global__ void __launch_bounds__(kCgThreads, 1)
+__global__ void __launch_bounds__(kCgThreads, 2)
 coarse_umma_kernel(const __grid_constant__ CUtensorMap tm_cen, const __grid_constant__ CUtensorMap tm_q, uint32_t q0,
                    uint32_t n_cen, uint32_t nq, uint32_t dim, const float* __restrict__ cnorm,
                    const float* __restrict__ qnorm, float* __restrict__ p_out) {
