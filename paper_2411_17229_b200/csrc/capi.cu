@@ -377,7 +377,7 @@ struct dade_gpu_ctx {
     DevBuf g_counts, g_cursor, g_boff, g_ioff, bucket_q, bucket_slot, items, n_items;
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
     DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter, seed_goff, seed_glist;
-    DevBuf cnorm, qnorm, coarse_lo, coarse_overflow, q_norms;  // coarse_lo: p~ per (query, centroid)
+    DevBuf cnorm, qnorm, coarse_lo, coarse_overflow, q_norms, coarse_gmin;  // coarse_lo: p~ per (query, centroid)
     bool coarse_force_exact = false, coarse_tc_used = false;
     int n_sms = 148;
     uint32_t surv_cap_hint = 0;
@@ -493,13 +493,20 @@ void coarse_tc_range(dade_gpu_ctx* c, const float* d_q, uint32_t q0, uint32_t m,
         cuda_check(launch_coarse_norms(c->centroids.as<float>(), c->n_clusters, qc, m, c->dim, c->cnorm.as<float>(),
                                        c->qnorm.as<float>(), s),
                    "coarse norms");
+        // nlist > 1024: the GEMM epilogue also leaves the per-32-centroid minima of the
+        // upper bounds, the selection's first pass (DADE_GPU_NO_GMIN: the selection reads p~ for them)
+        uint32_t* gmin = nullptr;
+        if (c->n_clusters > 1024 && c->n_clusters <= 16384 && !env_flag("DADE_GPU_NO_GMIN")) {
+            c->coarse_gmin.ensure((size_t)coarse_tc_chunk(c, m) * ((c->n_clusters + 31) / 32) * 4);
+            gmin = c->coarse_gmin.as<uint32_t>();
+        }
         cuda_check(launch_coarse_umma(*tmc, *tmq, q0, c->n_clusters, m, c->dim, c->cnorm.as<float>(),
-                                      c->qnorm.as<float>(), c->coarse_lo.as<float>(), s),
+                                      c->qnorm.as<float>(), c->coarse_lo.as<float>(), s, gmin),
                    "coarse gemm (tcgen05)");
         cuda_check(launch_coarse_select(c->centroids.as<float>(), c->n_clusters, qc, m, c->dim, n_probe,
                                         c->cnorm.as<float>(), c->qnorm.as<float>(), c->coarse_lo.as<float>(),
                                         c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
-                                        c->coarse_overflow.as<uint32_t>(), s),
+                                        c->coarse_overflow.as<uint32_t>(), s, gmin),
                    "coarse select");
         c->launches += 3;
         return;

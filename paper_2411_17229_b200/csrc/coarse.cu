@@ -23,7 +23,6 @@ namespace dade_gpu {
 
 namespace {
 
-constexpr float kCoarseDelta = 4e-3f;
 constexpr int kCQ = 64;     // queries per CTA tile
 constexpr int kCC = 128;    // centroids per CTA tile
 constexpr int kCK = 32;     // dims per staged slice
@@ -146,11 +145,6 @@ __global__ void __launch_bounds__(256) sq_norms_kernel(const float* __restrict__
     }
 }
 
-// order-preserving key of a float (any sign)
-__device__ __forceinline__ uint32_t fkey(float x) {
-    const uint32_t u = __float_as_uint(x);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
 constexpr int kSelCap = 512;  // exact-candidate list per query
 
@@ -170,8 +164,8 @@ __global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restr
     const float* prow = pt + (size_t)qi * n_cen;
     const float qn = qnorm[qi];
     // bounds of the exact l2_sq: p~ -/+ kCoarseDelta (|q|^2 + |c|^2)
-    auto hi_of = [&](uint32_t c) { return prow[c] + kCoarseDelta * (cnorm[c] + qn); };
-    auto lo_of = [&](uint32_t c) { return prow[c] - kCoarseDelta * (cnorm[c] + qn); };
+    auto hi_of = [&](uint32_t c) { return __fadd_rn(prow[c], coarse_delta(cnorm[c], qn)); };
+    auto lo_of = [&](uint32_t c) { return __fsub_rn(prow[c], coarse_delta(cnorm[c], qn)); };
     uint32_t* h = hist[warp];
     // radix select: key of the n_probe-th smallest hi (4 passes of 8 bits)
     uint32_t prefix = 0, rank = n_probe;  // rank: 1-based within the current prefix class
@@ -294,9 +288,9 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
     for (int j = 0; j < 32; ++j) {
         const uint32_t c = lane + 32u * j;
         if (c < n_cen) {
-            const float p = prow[c], d = kCoarseDelta * (cnorm[c] + qn);
-            hk[j] = fkey(p + d);
-            lk[j] = fkey(p - d);
+            const float p = prow[c], d = coarse_delta(cnorm[c], qn);
+            hk[j] = fkey(__fadd_rn(p, d));
+            lk[j] = fkey(__fsub_rn(p, d));
         } else {
             hk[j] = 0xffffffffu;
             lk[j] = 0xffffffffu;
@@ -456,7 +450,8 @@ __device__ __forceinline__ uint32_t warp_select_smem(const uint32_t* v, uint32_t
 __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
     const float* __restrict__ pt, const float* __restrict__ cnorm, const float* __restrict__ qnorm,
     const float* __restrict__ cen, uint32_t n_cen, const float* __restrict__ q, uint32_t nq, uint32_t dim,
-    uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow) {
+    uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow,
+    const uint32_t* __restrict__ gmin) {
     __shared__ uint64_t cand[kFsWarps][kSelCap];
     __shared__ __align__(16) float rows[kFsWarps][32 * kFsRS];
     __shared__ __align__(16) float qch[kFsWarps][32];
@@ -467,19 +462,30 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
     const float qn = qnorm[qi];
     uint32_t* hist = reinterpret_cast<uint32_t*>(rows[warp]);    // 256 words
     uint32_t* hv = hist + 256;                                   // <= 512 hi keys (fits: 768 <= 32 * kFsRS)
-    // pass 1: chunk minima of hi
+    // pass 1: minima of hi over disjoint centroid groups: from the GEMM epilogue
+    // (gmin: per query, one per 32 consecutive centroids) or 512-centroid chunks here
     uint32_t gm[32];
+    if (gmin) {
+        const uint32_t ng = (n_cen + 31) / 32;
+        const uint32_t* gr = gmin + (size_t)qi * ng;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        uint32_t m = 0xffffffffu;
-        if ((uint32_t)j * kWdChunk < n_cen) {
-#pragma unroll
-            for (int i = 0; i < kWdChunk / 32; ++i) {
-                const uint32_t c = j * kWdChunk + i * 32 + lane;
-                if (c < n_cen) m = min(m, fkey(prow[c] + kCoarseDelta * (cnorm[c] + qn)));
-            }
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t i = lane + 32u * j;
+            gm[j] = i < ng ? gr[i] : 0xffffffffu;
         }
-        gm[j] = m;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            uint32_t m = 0xffffffffu;
+            if ((uint32_t)j * kWdChunk < n_cen) {
+#pragma unroll
+                for (int i = 0; i < kWdChunk / 32; ++i) {
+                    const uint32_t c = j * kWdChunk + i * 32 + lane;
+                    if (c < n_cen) m = min(m, fkey(__fadd_rn(prow[c], coarse_delta(cnorm[c], qn))));
+                }
+            }
+            gm[j] = m;
+        }
     }
     // T0 = n_probe-th smallest chunk minimum (radix select over registers)
     uint32_t kmin = 0xffffffffu, kmax = 0;
@@ -518,7 +524,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
         bool is = false;
         if (c < n_cen) {
             pv = prow[c];
-            is = fkey(pv - kCoarseDelta * (cnorm[c] + qn)) <= T0;
+            is = fkey(__fsub_rn(pv, coarse_delta(cnorm[c], qn))) <= T0;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, is);
         const uint32_t pos = n + __popc(bal & ((1u << lane) - 1u));
@@ -533,7 +539,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
     for (uint32_t e = lane; e < n; e += 32) {
         const uint64_t v = cand[warp][e];
         const uint32_t c = (uint32_t)v;
-        hv[e] = fkey(__uint_as_float((uint32_t)(v >> 32)) + kCoarseDelta * (cnorm[c] + qn));
+        hv[e] = fkey(__fadd_rn(__uint_as_float((uint32_t)(v >> 32)), coarse_delta(cnorm[c], qn)));
     }
     __syncwarp();
     const uint32_t B = warp_select_smem(hv, n, n_probe, hist, lane);
@@ -546,7 +552,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
         if (e < n) {
             const uint64_t v = cand[warp][e];
             c = (uint32_t)v;
-            is = fkey(__uint_as_float((uint32_t)(v >> 32)) - kCoarseDelta * (cnorm[c] + qn)) <= B;
+            is = fkey(__fsub_rn(__uint_as_float((uint32_t)(v >> 32)), coarse_delta(cnorm[c], qn))) <= B;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, is);
         __syncwarp();
@@ -621,7 +627,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
 // the select kernel for n_cen centroids
 void launch_select_any(const float* pt, const float* cnorm, const float* qnorm, const float* centroids, uint32_t n_cen,
                        const float* queries, uint32_t nq, uint32_t dim, uint32_t n_probe, uint64_t* probes,
-                       uint32_t* overflow, cudaStream_t s) {
+                       uint32_t* overflow, cudaStream_t s, const uint32_t* gmin = nullptr) {
     if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap) {
         coarse_select_fast_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
             pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow,
@@ -630,7 +636,7 @@ void launch_select_any(const float* pt, const float* cnorm, const float* qnorm, 
     }
     if (n_cen <= 32u * kWdChunk && dim % 4 == 0 && n_probe <= kSelCap && !std::getenv("DADE_GPU_SELECT_WARP")) {
         coarse_select_wide_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
-            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow);
+            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, gmin);
         return;
     }
     coarse_select_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe,
@@ -661,9 +667,10 @@ cudaError_t launch_coarse_norms(const float* centroids, uint32_t n_cen, const fl
 
 cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq,
                                  uint32_t dim, uint32_t n_probe, const float* cnorm, const float* qnorm,
-                                 const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s) {
+                                 const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s,
+                                 const uint32_t* gmin) {
     if (nq == 0) return cudaSuccess;
-    launch_select_any(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, s);
+    launch_select_any(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, s, gmin);
     return cudaGetLastError();
 }
 

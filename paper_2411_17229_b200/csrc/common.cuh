@@ -130,6 +130,17 @@ __device__ __forceinline__ void warp_hist_find(const uint32_t* hist, uint32_t ra
     before = __shfl_sync(0xffffffffu, b, src);
 }
 
+// Coarse ranking bound (coarse.cu): |p~ - l2_sq| <= kCoarseDelta (|q|^2 + |c|^2)
+constexpr float kCoarseDelta = 4e-3f;
+// the bound's half-width and the upper / lower keys, with explicit roundings so every
+// kernel that forms them (GEMM epilogue, selections) gets the same bits
+__device__ __forceinline__ float coarse_delta(float cn, float qn) { return __fmul_rn(kCoarseDelta, __fadd_rn(cn, qn)); }
+// order-preserving key of a float (any sign)
+__device__ __forceinline__ uint32_t fkey(float x) {
+    const uint32_t u = __float_as_uint(x);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 __device__ __forceinline__ uint64_t make_key(float dist, uint32_t id) {
     return (static_cast<uint64_t>(__float_as_uint(dist)) << 32) | id;
 }

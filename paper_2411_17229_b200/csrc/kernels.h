@@ -87,15 +87,18 @@ size_t filter_umma_smem_bytes(int c_dense);
 cudaError_t launch_filter_umma(const FilterArgs& a, const CUtensorMap& tmap128, const CUtensorMap& tmap_aug,
                                uint32_t grid, cudaStream_t s);
 // tcgen05 coarse GEMM: p~ [nq][n_cen] for queries [q0, q0 + nq) of the tm_q map (box {32, 256})
+// gmin (nullable) [nq][ceil(n_cen / 32)]: per query, the minimum coarse upper-bound key (fkey(p~ + delta))
+// of every 32 consecutive centroids (coarse_select_wide_kernel's group minima)
 cudaError_t launch_coarse_umma(const CUtensorMap& tm_cen, const CUtensorMap& tm_q, uint32_t q0, uint32_t n_cen,
                                uint32_t nq, uint32_t dim, const float* cnorm, const float* qnorm, float* p_out,
-                               cudaStream_t s);
+                               cudaStream_t s, uint32_t* gmin = nullptr);
 // coarse.cu pieces around it
 cudaError_t launch_coarse_norms(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
                                 float* cnorm, float* qnorm, cudaStream_t s);
 cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq,
                                  uint32_t dim, uint32_t n_probe, const float* cnorm, const float* qnorm,
-                                 const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s);
+                                 const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s,
+                                 const uint32_t* gmin = nullptr);
 // per-row extra operand [n][8] = (-h hi, -h lo, 1, 1, 0, 0, 0, 0) from first-slice norms
 cudaError_t launch_row_aug(const float* norms, uint32_t n, float* out, cudaStream_t s);
 

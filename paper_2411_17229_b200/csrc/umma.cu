@@ -577,7 +577,7 @@ constexpr int kCgThreads = 160;
 __global__ void __launch_bounds__(kCgThreads, 2)
 coarse_umma_kernel(const __grid_constant__ CUtensorMap tm_cen, const __grid_constant__ CUtensorMap tm_q, uint32_t q0,
                    uint32_t n_cen, uint32_t nq, uint32_t dim, const float* __restrict__ cnorm,
-                   const float* __restrict__ qnorm, float* __restrict__ p_out) {
+                   const float* __restrict__ qnorm, float* __restrict__ p_out, uint32_t* __restrict__ gmin) {
     extern __shared__ unsigned char cg_raw[];
     unsigned char* sm = cg_raw + ((1024u - (su32(cg_raw) & 1023u)) & 1023u);
     constexpr uint32_t kABytes = kCgM * 128, kBBytes = kCgN * 128;
@@ -647,11 +647,23 @@ coarse_umma_kernel(const __grid_constant__ CUtensorMap tm_cen, const __grid_cons
             float v[32];
             tc_ld32_nowait(tmem + ((warp * 32) << 16) + j * 32, v);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-            if (c >= n_cen) continue;
+            const uint32_t ng = (n_cen + 31) / 32, grp = (c0 + warp * 32) / 32;
+            uint32_t mine = 0xffffffffu;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 const uint32_t qq = qt + j * 32 + i;
-                if (qq < nq) p_out[(size_t)qq * n_cen + c] = fmaf(-2.f, v[i], cn + qnorm[qq]);
+                const float qn = qq < nq ? qnorm[qq] : 0.f;
+                const float p = fmaf(-2.f, v[i], cn + qn);
+                if (c < n_cen && qq < nq) p_out[(size_t)qq * n_cen + c] = p;
+                if (gmin) {  // min upper-bound key of this warp's 32 centroids, per query column
+                    const uint32_t m = __reduce_min_sync(
+                        0xffffffffu, c < n_cen ? fkey(__fadd_rn(p, coarse_delta(cn, qn))) : 0xffffffffu);
+                    if (lane == i) mine = m;
+                }
+            }
+            if (gmin) {
+                const uint32_t qq = qt + j * 32 + lane;
+                if (qq < nq && grp < ng) gmin[(size_t)qq * ng + grp] = mine;
             }
         }
     }
@@ -669,12 +681,12 @@ size_t coarse_umma_smem_bytes() { return (size_t)kCgStages * (kCgM * 128 + kCgN 
 
 cudaError_t launch_coarse_umma(const CUtensorMap& tm_cen, const CUtensorMap& tm_q, uint32_t q0, uint32_t n_cen,
                                uint32_t nq, uint32_t dim, const float* cnorm, const float* qnorm, float* p_out,
-                               cudaStream_t s) {
+                               cudaStream_t s, uint32_t* gmin) {
     if (nq == 0 || n_cen == 0) return cudaSuccess;
     const size_t smem = coarse_umma_smem_bytes();
     DADE_CUDA_TRY(cudaFuncSetAttribute(coarse_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((n_cen + kCgM - 1) / kCgM, (nq + kCgN - 1) / kCgN);
-    coarse_umma_kernel<<<grid, kCgThreads, smem, s>>>(tm_cen, tm_q, q0, n_cen, nq, dim, cnorm, qnorm, p_out);
+    coarse_umma_kernel<<<grid, kCgThreads, smem, s>>>(tm_cen, tm_q, q0, n_cen, nq, dim, cnorm, qnorm, p_out, gmin);
     return cudaGetLastError();
 }
 
