@@ -597,9 +597,14 @@ constexpr uint32_t kSeedRowsDefault = 1024;  // rows of the nearest list used by
 
 // rows of each nearest list the radius seed scores exactly (and the scan then
 // skips): the list-major kernel (K <= 128) takes up to 1024, the per-query one 512
-uint32_t seed_rows(uint32_t k) {
+// Rows of each nearest list the seed scores exactly: 1024 up to dim 256, then
+// ~1 MB of rows (256 at dim 960: an IVF group there holds ~1 query, so long rows
+// cost bytes per query -- config 2 1.47 -> 1.21 ms per batch at recall 0.982 vs
+// 0.987). The flat scan's groups are full (every query probes the base): 1024.
+uint32_t seed_rows(uint32_t k, uint32_t dim, bool flat = false) {
     const bool list_kernel = k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY");
     uint32_t s = kSeedRowsDefault;
+    if (dim > 256 && !flat) s = std::min<uint32_t>(s, std::max<uint32_t>(128, (262144u / dim) & ~127u));
     if (const char* e = std::getenv("DADE_GPU_SEED_ROWS")) s = (uint32_t)std::atoi(e);
     return std::min<uint32_t>(list_kernel ? 1024 : 512, std::max<uint32_t>(s, k));
 }
@@ -764,7 +769,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 sa.id_base = a.id_base;
                 sa.dim = a.dim;
                 sa.K = k;
-                sa.S = std::min<uint32_t>(seed_rows(k), 1024);
+                sa.S = std::min<uint32_t>(seed_rows(k, a.dim, flat), 1024);
                 sa.queries = d_q;
                 sa.r_global = a.r_global;
                 sa.out_keys = out_keys;
@@ -781,12 +786,12 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->seed_glist,
                                                     g->n_lists,
                                                     nq / kSeedGroup + g->n_lists + 1, seed.offsets, rows, a.row_ids,
-                                                    a.id_base, a.dim, d_q, k, seed_rows(k), a.r_global, out_keys,
+                                                    a.id_base, a.dim, d_q, k, seed_rows(k, a.dim, flat), a.r_global, out_keys,
                                                     out_count, s),
                            "seed radius (lists)");
             else
                 cuda_check(launch_seed_radius(seed.probes, seed.n_probe, seed.offsets, rows, a.row_ids, a.dim, d_q, nq,
-                                              k, seed_rows(k), a.r_global, out_keys, out_count, s),
+                                              k, seed_rows(k, a.dim, flat), a.r_global, out_keys, out_count, s),
                            "seed radius");
             ++c->launches;
         }
@@ -990,7 +995,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     g.q_chunk = umma ? kUmmaQ : use_filter ? kFilterQ : (uint32_t)kQC;
     const bool seeded = n_probe > 1 && !seed_disabled() && k <= 512;
     if (use_filter && seeded) {  // the seed's rows of every nearest list are final results already
-        g.seed_skip = seed_rows(k);
+        g.seed_skip = seed_rows(k, c->dim);
         g.seed_min = k;
     }
     const size_t ne = (size_t)nrb * c->n_clusters;
@@ -1071,7 +1076,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     }
     if (seeded && !resume) {
         cuda_check(launch_seed_radius(c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>(), a.storage,
-                                      a.row_ids, c->dim, d_q, nq, k, seed_rows(k), a.r_global, nullptr, nullptr, s),
+                                      a.row_ids, c->dim, d_q, nq, k, seed_rows(k, c->dim), a.r_global, nullptr, nullptr, s),
                    "seed radius");
         ++c->launches;
     }
@@ -1118,7 +1123,7 @@ bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uin
     g.max_item_rows = kFilterItemRows;
     g.rank0_item_rows = 0;
     g.q_chunk = kUmmaQ;
-    g.seed_skip = std::min<uint32_t>(seed_rows(k), c->b_count);
+    g.seed_skip = std::min<uint32_t>(seed_rows(k, c->b_dim, true), c->b_count);
     g.seed_min = k;
     const size_t max_items = ((size_t)nq + kUmmaQ - 1) / kUmmaQ * ((c->b_count + kFilterItemRows - 1) / kFilterItemRows) + 1;
     c->g_counts.ensure(8);
