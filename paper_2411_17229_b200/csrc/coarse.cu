@@ -271,6 +271,11 @@ __device__ __forceinline__ void cs_cp16(float* dst, const float* src) {
 }
 constexpr int kFsRS = 36;  // floats per staged row chunk (16-byte aligned, conflict-free LDS.128)
 
+// WPQ = 4 (small batches, where a warp per query leaves the GPU idle): the four
+// warps of a CTA select the same candidates redundantly (no synchronisation),
+// warp w runs the exact rounds w, w + 4, ... and writes its keys into warp 0's
+// list, which warp 0 sorts after the CTA barrier.
+template <int WPQ>
 __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
     const float* __restrict__ pt, const float* __restrict__ cnorm, const float* __restrict__ qnorm,
     const float* __restrict__ cen, uint32_t n_cen, const float* __restrict__ q, uint32_t nq, uint32_t dim,
@@ -279,8 +284,8 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
     __shared__ __align__(16) float rows[kFsWarps][32 * kFsRS];
     __shared__ __align__(16) float qch[kFsWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t qi = blockIdx.x * kFsWarps + warp;
-    if (qi >= nq) return;
+    const uint32_t qi = WPQ == 1 ? blockIdx.x * kFsWarps + warp : blockIdx.x;
+    if (qi >= nq) return;  // uniform per CTA when WPQ > 1
     const float* prow = pt + (size_t)qi * n_cen;
     const float qn = qnorm[qi];
     uint32_t hk[32], lk[32];
@@ -338,17 +343,18 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
         if (is && pos < (uint32_t)kSelCap) cand[warp][pos] = lane + 32u * j;
         n += __popc(bal);
     }
-    if (census && lane == 0) atomicAdd(census, n);  // DADE_GPU_COARSE_CENSUS: exact candidates
+    if (census && lane == 0 && (WPQ == 1 || warp == 0)) atomicAdd(census, n);  // DADE_GPU_COARSE_CENSUS
     if (n > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
         if (lane == 0) atomicAdd(overflow, 1u);
         n = kSelCap;
     }
     __syncwarp();
+    if (WPQ > 1) __syncthreads();  // every warp's id list is written before keys land in warp 0's
     // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43) of the candidates
     const float* qr = q + (size_t)qi * dim;
     float* rs = rows[warp];
     float* qs = qch[warp];
-    for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+    for (uint32_t e0 = 32 * (warp % WPQ); e0 < n; e0 += 32 * WPQ) {
         const uint32_t e = e0 + lane;
         const uint32_t my_c = e < n ? (uint32_t)cand[warp][e] : 0u;
         const uint32_t nv = min(32u, n - e0);
@@ -385,9 +391,14 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
             }
         }
         __syncwarp();
-        if (e < n) cand[warp][e] = make_key(acc, my_c);
+        if (e < n) cand[WPQ == 1 ? warp : 0][e] = make_key(acc, my_c);
     }
-    __syncwarp();
+    if (WPQ == 1) {
+        __syncwarp();
+    } else {
+        __syncthreads();
+        if (warp != 0) return;
+    }
     // pad and bitonic-sort the candidate keys
     uint32_t m = 1;
     while (m < n) m <<= 1;
@@ -629,9 +640,13 @@ void launch_select_any(const float* pt, const float* cnorm, const float* qnorm, 
                        const float* queries, uint32_t nq, uint32_t dim, uint32_t n_probe, uint64_t* probes,
                        uint32_t* overflow, cudaStream_t s, const uint32_t* gmin = nullptr) {
     if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap) {
-        coarse_select_fast_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
-            pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow,
-            std::getenv("DADE_GPU_COARSE_CENSUS") ? overflow + 1 : nullptr);
+        uint32_t* census = std::getenv("DADE_GPU_COARSE_CENSUS") ? overflow + 1 : nullptr;
+        if (nq <= 4096 && n_probe > 32 && !std::getenv("DADE_GPU_SELECT_WPQ1"))  // > 1 exact round
+            coarse_select_fast_kernel<kFsWarps><<<nq, kFsWarps * 32, 0, s>>>(
+                pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, census);
+        else
+            coarse_select_fast_kernel<1><<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
+                pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, census);
         return;
     }
     if (n_cen <= 32u * kWdChunk && dim % 4 == 0 && n_probe <= kSelCap && !std::getenv("DADE_GPU_SELECT_WARP")) {
