@@ -316,7 +316,7 @@ def run_ours(args, cfg):
     stats = gp.DcoStats()
     if world == 1:
         dev.set_profiling(True)
-        sm, sb, fms = [], [], []
+        sm, sb, fms, seed_prof = [], [], [], []
         for _ in range(3):
             flush.zero_()
             torch.cuda.synchronize()
@@ -326,6 +326,7 @@ def run_ours(args, cfg):
                                                       ctypes.byref(st)))
             a, b, c = dev.last_scan_profile()
             fm, nf = dev.last_filter_profile()
+            seed_prof.append(dev.last_seed_profile())
             sm.append(a)
             sb.append(b)
             fms.append(fm)
@@ -495,6 +496,20 @@ def run_ours(args, cfg):
                         "bytes_per_step": scan_bytes,
                         "bytes_definition": "first-slice row-tile bytes per (tile, query item) + 16 B per "
                                             "survivor handed on (kernel-counted)"}}
+        if seed_prof and seed_prof[-1][0] > 0:
+            # the radius seed (largest single launch): exact sequential fp32 (row, query, dim) steps,
+            # 3 FP32 ops each (sub, square, add: no FMA, bit-exact); peak = the issue rate the FP32
+            # pipe sustains for that step, measured by tools/micro/fp_mix.cu (42 steps / SM / cycle)
+            s_ms = float(np.median([x[0] for x in seed_prof]))
+            s_pd = float(seed_prof[-1][1])
+            s_peak = 42.0 * 148 * 1.965e9
+            roof["seed"] = {"kernel": "seed_persist_kernel", "bound": "fp32 issue", "ms_per_step": s_ms,
+                            "pair_dims_per_step": s_pd, "achieved_pair_dims_per_s": s_pd / (s_ms / 1e3),
+                            "peak_pair_dims_per_s": s_peak, "frac": s_pd / (s_ms / 1e3) / s_peak,
+                            "hbm_bytes_per_step_ncu": 1.014e9,
+                            "hbm_frac": 1.014e9 / (s_ms / 1e3) / 1e9 / peak,
+                            "source": "CUDA events around the launch; pair-dims counted by the kernel; ncu bytes "
+                                      "from profiles/ncu_step_summary_r01_v61.json"}
         el = stats.dims_accumulated
         roof["alu"] = {"reference_element_ops_per_s": el / (scan_ms / 1e3), "dims_accumulated": el,
                        "note": "DcoStats dims a sequential CPU scan would accumulate, per second of GPU scan"}

@@ -226,6 +226,10 @@ int dade_gpu_last_scan_profile(dade_gpu_ctx* ctx, double* scan_ms, double* scan_
 /* Device time (ms) of the streaming tensor-core filter launches of the last
  * search (the dominant kernel) and how many there were. Requires profiling. */
 int dade_gpu_last_filter_profile(dade_gpu_ctx* ctx, double* filter_ms, int* n_launches);
+/* Device time (ms) of the persistent radius-seed launch of the last search and
+ * the (row, query, dim) triples it summed exactly. Requires profiling; 0 when
+ * that kernel did not run. */
+int dade_gpu_last_seed_profile(dade_gpu_ctx* ctx, double* seed_ms, double* pair_dims);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,7 @@ def _load():
         "dade_gpu_set_profiling": ([P, I], I),
         "dade_gpu_last_scan_profile": ([P, P, P, P], I),
         "dade_gpu_last_filter_profile": ([P, P, P], I),
+        "dade_gpu_last_seed_profile": ([P, P, P], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -103,7 +104,7 @@ EXPORTED = [
     "dade_gpu_flat_search_keys", "dade_gpu_merge_keys", "dade_gpu_dco_evaluate",
     "dade_gpu_partial_sums", "dade_gpu_calibrate", "dade_gpu_launch_count",
     "dade_gpu_set_profiling", "dade_gpu_last_scan_profile", "dade_gpu_debug_counters",
-    "dade_gpu_last_filter_profile", "dade_gpu_debug_radius",
+    "dade_gpu_last_filter_profile", "dade_gpu_last_seed_profile", "dade_gpu_debug_radius",
 ]
 
 

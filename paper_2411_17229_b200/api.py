@@ -83,6 +83,11 @@ class Device:
         check(_capi.lib.dade_gpu_last_filter_profile(self.h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def last_seed_profile(self):
+        ms, pd = C.c_double(), C.c_double()
+        check(_capi.lib.dade_gpu_last_seed_profile(self.h, C.byref(ms), C.byref(pd)))
+        return ms.value, pd.value
+
     def last_scan_profile(self):
         a, b, c = C.c_double(), C.c_double(), C.c_double()
         check(_capi.lib.dade_gpu_last_scan_profile(self.h, C.byref(a), C.byref(b), C.byref(c)))

@@ -413,6 +413,10 @@ struct dade_gpu_ctx {
     bool profiling = false;
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
     cudaEvent_t ef[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // filter launches per pass
+    cudaEvent_t es[2] = {nullptr, nullptr};  // the persistent seed launch
+    bool seed_profiled = false;
+    double last_seed_ms = 0, last_seed_pair_dims = 0;
+    DevBuf seed_census;  // pair-dims the seed scored (profiling)
     int n_filter_passes = 0;
     // DADE_GPU_TIMELINE=1: labelled events on both streams, printed per search (diagnostic)
     std::vector<std::pair<const char*, cudaEvent_t>> tl;
@@ -674,6 +678,14 @@ void finish_profile(dade_gpu_ctx* c) {
         cuda_check(cudaEventElapsedTime(&ms, c->ef[2 * p], c->ef[2 * p + 1]), "elapsed");
         c->last_filter_ms += ms;
     }
+    c->last_seed_ms = c->last_seed_pair_dims = 0;
+    if (c->seed_profiled) {
+        cuda_check(cudaEventElapsedTime(&ms, c->es[0], c->es[1]), "elapsed");
+        c->last_seed_ms = ms;
+        unsigned long long pd = 0;
+        cuda_check(cudaMemcpy(&pd, c->seed_census.p, 8, cudaMemcpyDeviceToHost), "D2H census");
+        c->last_seed_pair_dims = (double)pd;
+    }
 }
 
 __global__ void tighten_from_topk_kernel(const uint64_t* keys, const uint32_t* count, uint32_t nq, uint32_t K,
@@ -780,8 +792,16 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                     c->seed_order.ensure(((size_t)nq / kSeedGroup + g->n_lists + 1) * 4);
                     sa.order = c->seed_order.as<uint32_t>();
                 }
+                c->seed_profiled = c->profiling;
+                if (c->profiling) {  // device time and pair-dims of the seed (dade_gpu_last_seed_profile)
+                    c->seed_census.ensure(8);
+                    cuda_check(cudaMemsetAsync(c->seed_census.p, 0, 8, s), "memset");
+                    sa.census = c->seed_census.as<unsigned long long>();
+                    cuda_check(cudaEventRecord(c->es[0], s), "event");
+                }
                 cuda_check(launch_seed_tma(sa, *stm, nq / kSeedGroup + g->n_lists + 1, s, c->seed_work.as<uint32_t>()),
                            "seed radius (tma)");
+                if (c->profiling) cuda_check(cudaEventRecord(c->es[1], s), "event");
             } else if (g && g->n_rb >= 1 && k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->seed_glist,
                                                     g->n_lists,
@@ -1599,6 +1619,7 @@ int dade_gpu_create(int device, dade_gpu_ctx** out) {
         cuda_check(cudaEventCreate(&c->e2), "event");
         cuda_check(cudaEventCreate(&c->e3), "event");
         for (auto& e : c->ef) cuda_check(cudaEventCreate(&e), "event");
+        for (auto& e : c->es) cuda_check(cudaEventCreate(&e), "event");
         cuda_check(cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, device), "attr");
         *out = c;
     });
@@ -2358,6 +2379,14 @@ int dade_gpu_last_filter_profile(dade_gpu_ctx* c, double* filter_ms, int* n_laun
         if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
         if (filter_ms) *filter_ms = c->last_filter_ms;
         if (n_launches) *n_launches = c->n_filter_passes;
+    });
+}
+
+int dade_gpu_last_seed_profile(dade_gpu_ctx* c, double* seed_ms, double* pair_dims) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (seed_ms) *seed_ms = c->last_seed_ms;
+        if (pair_dims) *pair_dims = c->last_seed_pair_dims;
     });
 }
 

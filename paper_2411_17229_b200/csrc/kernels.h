@@ -178,6 +178,7 @@ struct SeedListArgs {
     uint32_t* out_count;
     uint64_t nz2;                   // 0x8000000080000000 (sq_step2's opaque -0.0 pair)
     uint32_t* order;                // nullable scratch [groups]: persistent kernel's costliest-first group order
+    unsigned long long* census;     // nullable: += rows x queries x dim of every group scored (profiling)
 };
 bool seed_tma_ok(uint32_t dim, uint32_t K);
 // work: one zeroed-per-launch counter word (persistent variant); nullptr: one CTA per group
