@@ -487,8 +487,8 @@ __global__ void __launch_bounds__(kSeedThreads) seed_radius_kernel(
 // rounding as sq_step); then one warp per query sorts its S keys. Same output
 // as seed_radius_kernel. Requires dim % 4 == 0 (the streaming path's rule).
 constexpr int kSeedListMax = 1024;             // rows per list seed (up to 4 per thread)
-constexpr int kSeedSlice = 8;                  // dims per staged slice
-constexpr int kSeedRS = kSeedSlice + 4;        // padded row stride (floats): conflict-free LDS.128
+constexpr int kSeedSlice8 = 8;                  // dims per staged slice
+constexpr int kSeedRS = kSeedSlice8 + 4;        // padded row stride (floats): conflict-free LDS.128
 constexpr int kSeedTileF = kSeedListMax * kSeedRS; // floats per tile buffer
 
 __device__ __forceinline__ void cp_async16_s(void* dst, const void* src, bool pred) {
@@ -511,11 +511,11 @@ __device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* a
                                                 uint32_t start, uint32_t n, uint32_t dim, const float* queries,
                                                 const uint32_t* qs, uint32_t ng, uint64_t nz2) {
     const uint32_t tid = threadIdx.x;
-    const uint32_t n_slices = (dim + kSeedSlice - 1) / kSeedSlice;
+    const uint32_t n_slices = (dim + kSeedSlice8 - 1) / kSeedSlice8;
     auto issue = [&](uint32_t sl, uint32_t buf) {
-        const uint32_t k0 = sl * kSeedSlice;
+        const uint32_t k0 = sl * kSeedSlice8;
         float* tb = tile + buf * kSeedTileF;
-        constexpr uint32_t kCh = kSeedSlice / 4;  // 16-byte chunks per row slice
+        constexpr uint32_t kCh = kSeedSlice8 / 4;  // 16-byte chunks per row slice
 #pragma unroll
         for (int i = 0; i < (kR * kSeedThreads * (int)kCh) / kSeedThreads; ++i) {
             const uint32_t idx = tid + i * kSeedThreads, row = idx / kCh, c4 = idx % kCh;
@@ -523,12 +523,12 @@ __device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* a
             const float* src = storage + (size_t)(start + (ok ? row : 0)) * dim + (ok ? k0 + 4 * c4 : 0);
             cp_async16_s(tb + row * kSeedRS + 4 * c4, src, ok);
         }
-        static_assert(kSeedSlice * kSeedGroup <= kSeedThreads, "one query element per thread");
-        if (tid < (uint32_t)(kSeedSlice * kSeedGroup)) {  // qt[buf][k][u]
+        static_assert(kSeedSlice8 * kSeedGroup <= kSeedThreads, "one query element per thread");
+        if (tid < (uint32_t)(kSeedSlice8 * kSeedGroup)) {  // qt[buf][k][u]
             const uint32_t k = tid / kSeedGroup, u = tid % kSeedGroup;
             const bool ok = u < ng && k0 + k < dim;
             const float* src = queries + (ok ? (size_t)qs[u] * dim + k0 + k : 0);
-            cp_async4_s(qt + buf * kSeedSlice * kSeedGroup + k * kSeedGroup + u, src, ok);
+            cp_async4_s(qt + buf * kSeedSlice8 * kSeedGroup + k * kSeedGroup + u, src, ok);
         }
         cp_async_commit();
     };
@@ -548,9 +548,9 @@ __device__ __forceinline__ void seed_group_sums(float* tile, float* qt, float* a
         }
         __syncthreads();
         const float* tb = tile + buf * kSeedTileF;
-        const float* qb = qt + buf * kSeedSlice * kSeedGroup;
+        const float* qb = qt + buf * kSeedSlice8 * kSeedGroup;
 #pragma unroll
-        for (int c = 0; c < kSeedSlice / 4; ++c) {
+        for (int c = 0; c < kSeedSlice8 / 4; ++c) {
             float o[kR][4];
 #pragma unroll
             for (int j = 0; j < kR; ++j) {
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(kSeedThreads, 2) seed_radius_list_kernel(
     uint32_t S, uint32_t* r_global, uint64_t* out_keys, uint32_t* out_count, uint64_t nz2) {
     extern __shared__ __align__(16) unsigned char seed_smem[];
     float* tile = reinterpret_cast<float*>(seed_smem);                  // [2][kSeedMax][kSeedRS]
-    float* qt = tile + 2 * kSeedTileF;                                  // [2][kSeedSlice][kSeedGroup]
+    float* qt = tile + 2 * kSeedTileF;                                  // [2][kSeedSlice8][kSeedGroup]
     // after the last slice the tile's space is reused: sums, then sort keys
     float* accs = tile;                                                 // [kSeedGroup][kSeedListMax]
     uint64_t* keys = reinterpret_cast<uint64_t*>(tile + kSeedGroup * kSeedListMax);  // [8 warps][kSeedSmall], then hist [8][256]
@@ -761,7 +761,7 @@ cudaError_t launch_seed_radius_lists(const uint32_t* counts, const uint32_t* buc
                                      uint32_t* out_count, cudaStream_t s) {
     if (n_lists == 0 || K > (uint32_t)kSeedSmall) return cudaErrorInvalidValue;  // caller: K <= kSeedListMaxK
     // double-buffered tile + query slices; sums [16][S], keys [8][128] and histograms alias the tile
-    const size_t smem = sizeof(float) * (2 * kSeedTileF + 2 * kSeedSlice * kSeedGroup);
+    const size_t smem = sizeof(float) * (2 * kSeedTileF + 2 * kSeedSlice8 * kSeedGroup);
     static_assert(sizeof(float) * 2 * kSeedTileF >=
                       sizeof(float) * kSeedGroup * kSeedListMax + (sizeof(uint64_t) * kSeedSmall + sizeof(uint32_t) * 256) * (kSeedThreads / 32),
                   "seed sums + keys + histograms must fit in the tile");

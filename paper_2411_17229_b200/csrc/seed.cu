@@ -27,8 +27,8 @@ constexpr int kSdRows = 1024;         // max seeded rows
 constexpr int kSdT = 256;             // compute threads (8 warps)
 constexpr int kSdThreads = kSdT + 32; // + producer warp
 constexpr int kSdG = kSeedGroup;      // queries per CTA (16)
-constexpr int kSdSlice = 8;           // dims per ring slot (one 32-byte row segment)
-constexpr int kSdStages = 3;
+constexpr int kSdSlice = kSeedSlice;  // dims per ring slot (one 16- or 32-byte row segment)
+constexpr int kSdStages = 24 / kSdSlice;  // 96 KB ring
 constexpr int kSdBox = 256;           // rows per TMA box
 constexpr int kSdSmall = 128;         // sorted slots (K <= 128)
 constexpr int kSdMaxDim = 256;        // resident queries: [dim][16] fp32
@@ -107,8 +107,10 @@ __device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* 
 #pragma unroll
             for (int j = 0; j < kR; ++j) {
                 const uint32_t r = min(tid + j * kT, (uint32_t)kSdRows - 1);  // rows >= 1024 (kT = 384): never stored
-                // 32B-swizzled row segment: 16-byte chunk c ^ row bit 2
-                const float4 x = *reinterpret_cast<const float4*>(slot + r * 32 + (((uint32_t)c ^ (r >> 2)) & 1u) * 16);
+                // 4-dim slices: 16-byte rows, unswizzled; 8-dim: 32B-swizzled, 16-byte chunk c ^ row bit 2
+                const float4 x = kSdSlice == 4
+                                     ? *reinterpret_cast<const float4*>(slot + r * 16)
+                                     : *reinterpret_cast<const float4*>(slot + r * 32 + (((uint32_t)c ^ (r >> 2)) & 1u) * 16);
                 o[j][0] = x.x;
                 o[j][1] = x.y;
                 o[j][2] = x.z;
@@ -366,7 +368,7 @@ constexpr int kSpS = DADE_SP_SUM_WARPS;            // sum warps
 constexpr int kSpL = 15 - kSpS;                    // selection warps (16 warps in all: 4 per SM sub-partition)
 constexpr int kSpT = kSpS * 32;                    // sum threads: rows t + kSpT j
 constexpr int kSpThreads = (kSpS + kSpL + 1) * 32;  // 512
-constexpr int kSpStages = 2;
+constexpr int kSpStages = 16 / kSdSlice;  // 64 KB ring
 constexpr int kSpSlots = 4;
 constexpr uint32_t kSpEnd = 0xffffffffu;
 
