@@ -62,6 +62,36 @@ def ivf_search_keys(dev, d_queries, nq: int, k: int, n_probe: int, out_keys, raw
         stats._add(st)
 
 
+def flat_search_keys(dev, d_queries, nq: int, k: int, out_keys, raw: bool = False, stats=None) -> None:
+    """linear_scan over this device's rows (FlatIndex, ids offset by its id_base) -> packed keys."""
+    flags = _capi.DEVICE_PTRS | (_capi.QUERIES_RAW if raw else 0)
+    st = _capi.Stats()
+    _capi.check(_capi.lib.dade_gpu_flat_search_keys(dev.h, _capi.ptr(d_queries), nq, k, flags, _capi.ptr(out_keys),
+                                                    C.byref(st) if stats is not None else None))
+    if stats is not None:
+        stats._add(st)
+
+
+def sharded_flat_search(dev, group, d_queries, nq: int, k: int, raw: bool = False):
+    """Row-sharded flat exhaustive scan (config 4): rank r holds the contiguous
+    rows plan_row_shards(n, world)[r] as a FlatIndex with id_base = its first
+    row, scans them for all nq queries (replicated), NCCL all-gathers the
+    packed top-K keys ([world, nq, k], 8 B each) and merges them on device.
+    Every rank returns the global (ids, dists, counts)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    keys = torch.empty((nq, k), dtype=torch.int64, device=d_queries.device)
+    flat_search_keys(dev, d_queries, nq, k, keys, raw=raw)
+    gathered = torch.empty((world, nq, k), dtype=torch.int64, device=d_queries.device)
+    dist.all_gather_into_tensor(gathered, keys, group=group)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=d_queries.device)
+    dists = torch.empty((nq, k), dtype=torch.float32, device=d_queries.device)
+    counts = torch.empty((nq,), dtype=torch.int32, device=d_queries.device)
+    merge_keys_device(dev, gathered, nq, k, ids, dists, counts)
+    return ids, dists, counts
+
+
 def coarse_probes(dev, d_queries, nq: int, n_probe: int, q_rot_out, probes_out, raw: bool = False) -> None:
     """Rotation (raw) + coarse ranking of nq queries: rotated rows -> q_rot_out [nq, D],
     probe keys -> probes_out (int64 [nq, n_probe])."""

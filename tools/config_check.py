@@ -132,6 +132,63 @@ def ev_time(fn):
     return e0.elapsed_time(e1)
 
 
+if args.shards and cfg.flat:
+    from paper_2411_17229_b200.dist import flat_search_keys
+    del idx
+    shard_out = []
+    cur = torch.cuda.current_stream().cuda_stream
+    base_np = art.base_rot.cpu().numpy()
+    m_fd = min(args.fd_check, nq, 32)
+    for G in args.shards:
+        plan = gdist.plan_row_shards(cfg.n, G)
+        ctxs = []
+        for r in range(G):
+            d = gp.Device(0)
+            s0, s1 = plan[r]
+            fi_ = gp.FlatIndex(d, base_np[s0:s1], id_base=s0)
+            art.transform.upload(d)
+            d.set_stream(cur)
+            ctxs.append((d, fi_, gp.DadeStrategy(art.transform, art.cal, cfg.delta_d, dev=d)))
+        keys = torch.empty((G, nq, k), dtype=torch.int64, device=device)
+        runs = []
+        for rep in range(3):
+            ts_ = []
+            for r, (d, _, st) in enumerate(ctxs):
+                d.apply(st)
+                flush.zero_()
+                ts_.append(ev_time(lambda: flat_search_keys(d, q_dev, nq, k, keys[r], raw=True)))
+            tm = ev_time(lambda: gdist.merge_keys_device(ctxs[0][0], keys, nq, k, ids_d, dst_d, cnt_d))
+            runs.append((max(ts_) + tm, ts_, tm))
+        tot, ts_, tm = min(runs, key=lambda x: x[0])
+        rec_g = bench.recall(ids_d.cpu().numpy().astype(np.uint32), cnt_d.cpu().numpy().astype(np.uint32), art.gt)
+        fkeys = torch.empty((G, m_fd, k), dtype=torch.int64, device=device)
+        for r, (d, _, _) in enumerate(ctxs):
+            d.apply(gp.FdScanningStrategy(cfg.dim))
+            flat_search_keys(d, q_dev[:m_fd].contiguous(), m_fd, k, fkeys[r], raw=True)
+        del ctxs
+        ref_d = gp.Device(0)
+        ref_i = gp.FlatIndex(ref_d, base_np)
+        art.transform.upload(ref_d)
+        ref_d.apply(gp.FdScanningStrategy(cfg.dim))
+        rkeys = torch.empty((1, m_fd, k), dtype=torch.int64, device=device)
+        flat_search_keys(ref_d, q_dev[:m_fd].contiguous(), m_fd, k, rkeys[0], raw=True)
+        o1 = [torch.empty((m_fd, k), dtype=torch.int32, device=device), torch.empty((m_fd, k), dtype=torch.float32, device=device),
+              torch.empty((m_fd,), dtype=torch.int32, device=device)]
+        o2 = [torch.empty_like(x) for x in o1]
+        gdist.merge_keys_device(ref_d, fkeys, m_fd, k, *o1)
+        gdist.merge_keys_device(ref_d, rkeys, m_fd, k, *o2)
+        same = all(torch.equal(a.view(torch.int32), b.view(torch.int32)) for a, b in zip(o1, o2))
+        del ref_i, ref_d
+        shard_out.append({"G": G, "rows_per_rank": plan[0][1] - plan[0][0], "scan_ms": [round(x, 3) for x in ts_],
+                          "merge_ms": round(tm, 4), "projected_ms": tot, "recall_at_k": rec_g,
+                          "fd_merged_equals_unsharded": bool(same), "fd_check_queries": m_fd,
+                          "projected_queries_per_s": nq / tot * 1e3,
+                          "projected_strong_scaling_eff": (ms / tot) / G})
+    line["sharded_projection"] = {
+        "note": "one B200: the flat base split into G contiguous row shards (FlatIndex with id_base), each "
+                "in its own context scanning all queries; projected G-GPU time = slowest shard + key merge "
+                "(the NCCL all-gather of nq*K*8 B per rank not included)", "runs": shard_out}
+
 if args.shards and not cfg.flat:
     from paper_2411_17229_b200.dist import coarse_probes, ivf_search_keys_begin, ivf_search_keys_end
     fd_check = min(args.fd_check, nq)
