@@ -181,6 +181,12 @@ int dade_gpu_ivf_search_keys_begin(dade_gpu_ctx* ctx, const float* d_queries, ui
                                    uint32_t* d_radius);
 int dade_gpu_ivf_search_keys_end(dade_gpu_ctx* ctx, const uint32_t* d_radius,
                                  dade_gpu_stats* stats);
+/* The flat scan in the same two phases (row-sharded linear_scan): _begin runs the
+ * radius seed over this device's first rows, dade_gpu_ivf_search_keys_end (shared)
+ * runs the streaming passes with the min-reduced radius. */
+int dade_gpu_flat_search_keys_begin(dade_gpu_ctx* ctx, const float* d_queries, uint32_t nq,
+                                    uint32_t k, uint32_t flags, uint64_t* d_out_keys,
+                                    uint32_t* d_radius);
 
 /* Merge G gathered key blocks [G x nq x k] (e.g. an NCCL all-gather) into the
  * global top-K: ids/dists/counts as dade_gpu_ivf_search. Device pointers. */
@@ -216,6 +222,11 @@ int dade_gpu_debug_radius(dade_gpu_ctx* ctx, uint32_t* out, uint32_t nq);
 
 /* Number of CUDA kernels this handle launched so far (bench evidence). */
 uint64_t dade_gpu_launch_count(dade_gpu_ctx* ctx);
+
+/* Rows of each probed list's head (the flat base's first rows) the radius seed
+ * scores exactly; 0 restores the default (1024, ~1 MB of rows per IVF list above
+ * dim 256). A tuning knob: fewer seeded rows give a looser first radius. */
+int dade_gpu_set_seed_rows(dade_gpu_ctx* ctx, uint32_t rows);
 
 /* Measured device time (ms) of the DCO scan kernel(s) in the last search
  * call, via CUDA events on the launching stream, and its algorithmic bytes

@@ -347,6 +347,7 @@ struct dade_gpu_ctx {
     // ivf
     bool has_ivf = false;
     bool sharded = false;  // set_ivf_shard removed lists with rows
+    uint32_t seed_rows_set = 0;  // dade_gpu_set_seed_rows (0: the default rule)
     // two-phase search (dade_gpu_ivf_search_keys_begin/_end): 1 = stop before the
     // last pass, 2 = resume at it; the begun search's arguments
     int split = 0;
@@ -355,6 +356,7 @@ struct dade_gpu_ctx {
         const float* d_q = nullptr;
         uint32_t nq = 0, k = 0, n_probe = 0;
         uint64_t* keys = nullptr;
+        bool flat = false;
     } sp;
     uint32_t dim = 0, count = 0, n_clusters = 0;
     DevBuf centroids, storage, ids, offsets;
@@ -606,9 +608,10 @@ constexpr uint32_t kSeedRowsDefault = 1024;  // rows of the nearest list used by
 // ~1 MB of rows (256 at dim 960: an IVF group there holds ~1 query, so long rows
 // cost bytes per query -- config 2 1.47 -> 1.21 ms per batch at recall 0.982 vs
 // 0.987). The flat scan's groups are full (every query probes the base): 1024.
-uint32_t seed_rows(uint32_t k, uint32_t dim, bool flat = false) {
+uint32_t seed_rows(const dade_gpu_ctx* c, uint32_t k, uint32_t dim, bool flat = false) {
     const bool list_kernel = k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY");
     uint32_t s = kSeedRowsDefault;
+    if (c->seed_rows_set) return std::min<uint32_t>(list_kernel ? 1024 : 512, std::max<uint32_t>(c->seed_rows_set, k));
     if (dim > 256 && !flat) s = std::min<uint32_t>(s, std::max<uint32_t>(128, (262144u / dim) & ~127u));
     if (const char* e = std::getenv("DADE_GPU_SEED_ROWS")) s = (uint32_t)std::atoi(e);
     return std::min<uint32_t>(list_kernel ? 1024 : 512, std::max<uint32_t>(s, k));
@@ -782,7 +785,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 sa.id_base = a.id_base;
                 sa.dim = a.dim;
                 sa.K = k;
-                sa.S = std::min<uint32_t>(seed_rows(k, a.dim, flat), 1024);
+                sa.S = std::min<uint32_t>(seed_rows(c, k, a.dim, flat), 1024);
                 sa.queries = d_q;
                 sa.r_global = a.r_global;
                 sa.out_keys = out_keys;
@@ -807,12 +810,12 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->seed_glist,
                                                     g->n_lists,
                                                     nq / kSeedGroup + g->n_lists + 1, seed.offsets, rows, a.row_ids,
-                                                    a.id_base, a.dim, d_q, k, seed_rows(k, a.dim, flat), a.r_global, out_keys,
+                                                    a.id_base, a.dim, d_q, k, seed_rows(c, k, a.dim, flat), a.r_global, out_keys,
                                                     out_count, s),
                            "seed radius (lists)");
             else
                 cuda_check(launch_seed_radius(seed.probes, seed.n_probe, seed.offsets, rows, a.row_ids, a.dim, d_q, nq,
-                                              k, seed_rows(k, a.dim, flat), a.r_global, out_keys, out_count, s),
+                                              k, seed_rows(c, k, a.dim, flat), a.r_global, out_keys, out_count, s),
                            "seed radius");
             ++c->launches;
         }
@@ -831,9 +834,11 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         // by nothing measurable (tools/e2e_pipe.py; DADE_GPU_H2D_AT_PASS overrides)
         static const int h2d_pass = std::getenv("DADE_GPU_H2D_AT_PASS") ? std::atoi(std::getenv("DADE_GPU_H2D_AT_PASS")) : -1;
         static const int max_pass = std::getenv("DADE_GPU_MAX_PASS") ? std::atoi(std::getenv("DADE_GPU_MAX_PASS")) : 99;  // diagnostic
+        // two-phase split: IVF before its last pass (nearest lists done), flat right after the seed
+        const int split_pass = flat ? 0 : n_pass - 1;
         for (int pass = 0; pass < std::min(n_pass, max_pass); ++pass) {
-            if (resume && pass < n_pass - 1) continue;  // phase 2: the last pass only
-            if (stop && pass == n_pass - 1) break;      // phase 1: everything before it
+            if (resume && pass < split_pass) continue;  // phase 2: from the split pass on
+            if (stop && pass == split_pass) break;      // phase 1: everything before it
             if (pass == (h2d_pass >= 0 ? h2d_pass : n_pass - 1) && c->qin_free_recorded)
                 cuda_check(cudaEventRecord(c->copy_ev[8], s), "event");
             cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
@@ -1016,7 +1021,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     g.q_chunk = umma ? kUmmaQ : use_filter ? kFilterQ : (uint32_t)kQC;
     const bool seeded = n_probe > 1 && !seed_disabled() && k <= 512;
     if (use_filter && seeded) {  // the seed's rows of every nearest list are final results already
-        g.seed_skip = seed_rows(k, c->dim);
+        g.seed_skip = seed_rows(c, k, c->dim);
         g.seed_min = k;
     }
     const size_t ne = (size_t)nrb * c->n_clusters;
@@ -1097,7 +1102,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     }
     if (seeded && !resume) {
         cuda_check(launch_seed_radius(c->probes.as<uint64_t>(), n_probe, c->offsets.as<uint32_t>(), a.storage,
-                                      a.row_ids, c->dim, d_q, nq, k, seed_rows(k, c->dim), a.r_global, nullptr, nullptr, s),
+                                      a.row_ids, c->dim, d_q, nq, k, seed_rows(c, k, c->dim), a.r_global, nullptr, nullptr, s),
                    "seed radius");
         ++c->launches;
     }
@@ -1127,12 +1132,15 @@ bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uin
     c->tm_base.get(c->base.as<float>(), std::max<uint32_t>(c->b_count, 1), c->b_dim, tma);
     ct.use_tma = (tma && ct.vec_ok) ? 1 : 0;
     if (!filter_ok(c, ct, c->b_dim) || !umma_ok(c, ct, tma)) return false;
+    const bool resume = c->split == 2;  // phase 2 of a two-phase search: grouping and seed kept
     // one list [0, b_count); every query's probe 0 is it
     c->flat_offsets.ensure(8);
-    const uint32_t h_off[2] = {0, c->b_count};
-    cuda_check(cudaMemcpyAsync(c->flat_offsets.p, h_off, 8, cudaMemcpyHostToDevice, s), "H2D offsets");
     c->probes.ensure((size_t)nq * 8);
-    cuda_check(cudaMemsetAsync(c->probes.p, 0, (size_t)nq * 8, s), "memset");
+    if (!resume) {
+        const uint32_t h_off[2] = {0, c->b_count};
+        cuda_check(cudaMemcpyAsync(c->flat_offsets.p, h_off, 8, cudaMemcpyHostToDevice, s), "H2D offsets");
+        cuda_check(cudaMemsetAsync(c->probes.p, 0, (size_t)nq * 8, s), "memset");
+    }
     GroupArgs g{};
     g.probes = c->probes.as<uint64_t>();
     g.nq = nq;
@@ -1144,7 +1152,7 @@ bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uin
     g.max_item_rows = kFilterItemRows;
     g.rank0_item_rows = 0;
     g.q_chunk = kUmmaQ;
-    g.seed_skip = std::min<uint32_t>(seed_rows(k, c->b_dim, true), c->b_count);
+    g.seed_skip = std::min<uint32_t>(seed_rows(c, k, c->b_dim, true), c->b_count);
     g.seed_min = k;
     const size_t max_items = ((size_t)nq + kUmmaQ - 1) / kUmmaQ * ((c->b_count + kFilterItemRows - 1) / kFilterItemRows) + 1;
     c->g_counts.ensure(8);
@@ -1168,10 +1176,12 @@ bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uin
     g.seed_goff = c->seed_goff.as<uint32_t>();
     c->seed_glist.ensure(((size_t)nq / kSeedGroup + 2) * 4);
     g.seed_glist = c->seed_glist.as<uint32_t>();
-    cuda_check(launch_group(g, s), "group");
-    c->launches += 4;
     c->r_global.ensure((size_t)nq * 4);
-    cuda_check(launch_fill_u32(c->r_global.as<uint32_t>(), 0x7f800000u, nq, s), "fill");
+    if (!resume) {
+        cuda_check(launch_group(g, s), "group");
+        c->launches += 4;
+        cuda_check(launch_fill_u32(c->r_global.as<uint32_t>(), 0x7f800000u, nq, s), "fill");
+    }
     ScanArgs a{};
     a.storage = c->base.as<float>();
     a.row_ids = nullptr;
@@ -1200,6 +1210,7 @@ void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t
                         uint32_t* out_count) {
     cudaStream_t s = c->stream;
     if (flat_stream(c, d_q, nq, k, out_keys, out_count)) return;
+    if (c->split == 2) return;  // the row-block path is not split: phase 1 ran it whole
     const uint32_t qchunks = (nq + kQC - 1) / kQC;
     const uint32_t max_blocks = (c->b_count + kRT - 1) / kRT;
     uint32_t nb = std::max<uint32_t>(1, std::min<uint32_t>(max_blocks, (1184 + qchunks - 1) / qchunks));
@@ -2085,10 +2096,45 @@ int dade_gpu_ivf_search_keys_begin(dade_gpu_ctx* c, const float* d_queries, uint
         cuda_check(cudaMemcpyAsync(d_radius, c->r_global.p, (size_t)nq * 4, cudaMemcpyDeviceToDevice, c->stream),
                    "radius");
         c->sp.active = true;
+        c->sp.flat = false;
         c->sp.d_q = d_q;
         c->sp.nq = nq;
         c->sp.k = k;
         c->sp.n_probe = n_probe;
+        c->sp.keys = d_out_keys;
+    });
+}
+
+int dade_gpu_flat_search_keys_begin(dade_gpu_ctx* c, const float* d_queries, uint32_t nq, uint32_t k, uint32_t flags,
+                                    uint64_t* d_out_keys, uint32_t* d_radius) {
+    return guarded([&] {
+        check_flat_args(c, k);
+        if (nq && (!d_queries || !d_out_keys || !d_radius)) fail(DADE_GPU_INVALID_INPUT, "search_keys_begin: null argument");
+        c->use_device();
+        c->counters.ensure(64);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+        c->sp.active = false;
+        if (nq == 0) return;
+        const float* d_q = stage_queries(c, d_queries, nq, c->b_dim, flags | DADE_GPU_DEVICE_PTRS);
+        c->out_count.ensure((size_t)nq * 4);
+        c->surv_cap_used = 0;
+        c->split = 1;
+        try {
+            flat_search_device(c, d_q, nq, k, d_out_keys, c->out_count.as<uint32_t>());
+        } catch (...) {
+            c->split = 0;
+            throw;
+        }
+        c->split = 0;
+        c->r_global.ensure((size_t)nq * 4);
+        cuda_check(cudaMemcpyAsync(d_radius, c->r_global.p, (size_t)nq * 4, cudaMemcpyDeviceToDevice, c->stream),
+                   "radius");
+        c->sp.active = true;
+        c->sp.flat = true;
+        c->sp.d_q = d_q;
+        c->sp.nq = nq;
+        c->sp.k = k;
+        c->sp.n_probe = 1;
         c->sp.keys = d_out_keys;
     });
 }
@@ -2107,9 +2153,14 @@ int dade_gpu_ivf_search_keys_end(dade_gpu_ctx* c, const uint32_t* d_radius, dade
             min_u32_kernel<<<(nq + 255) / 256, 256, 0, c->stream>>>(c->r_global.as<uint32_t>(), d_radius, nq);
             cuda_check(cudaGetLastError(), "radius");
         }
+        const bool flat = c->sp.flat;
+        auto run = [&] {
+            if (flat) flat_search_device(c, c->sp.d_q, nq, k, c->sp.keys, c->out_count.as<uint32_t>());
+            else ivf_search_device(c, c->sp.d_q, nq, k, n_probe, c->sp.keys, c->out_count.as<uint32_t>());
+        };
         c->split = 2;
         try {
-            ivf_search_device(c, c->sp.d_q, nq, k, n_probe, c->sp.keys, c->out_count.as<uint32_t>());
+            run();
         } catch (...) {
             c->split = 0;
             throw;
@@ -2126,7 +2177,7 @@ int dade_gpu_ivf_search_keys_end(dade_gpu_ctx* c, const uint32_t* d_radius, dade
             cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
             c->surv_cap_used = 0;
             try {
-                ivf_search_device(c, c->sp.d_q, nq, k, n_probe, c->sp.keys, c->out_count.as<uint32_t>());
+                run();
             } catch (...) {
                 c->coarse_force_exact = false;
                 throw;
@@ -2365,6 +2416,13 @@ int dade_gpu_debug_counters(dade_gpu_ctx* c, uint64_t* out16) {
         std::memset(out16, 0, 16 * sizeof(uint64_t));
         if (c->counters.p) cuda_check(cudaMemcpy(out16, c->counters.p, 64, cudaMemcpyDeviceToHost), "D2H");
         if (c->phase.p) cuda_check(cudaMemcpy(out16 + 8, c->phase.p, 64, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+int dade_gpu_set_seed_rows(dade_gpu_ctx* c, uint32_t rows) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        c->seed_rows_set = rows;
     });
 }
 
