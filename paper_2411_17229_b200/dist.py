@@ -75,14 +75,21 @@ def flat_search_keys(dev, d_queries, nq: int, k: int, out_keys, raw: bool = Fals
 def sharded_flat_search(dev, group, d_queries, nq: int, k: int, raw: bool = False):
     """Row-sharded flat exhaustive scan (config 4): rank r holds the contiguous
     rows plan_row_shards(n, world)[r] as a FlatIndex with id_base = its first
-    row, scans them for all nq queries (replicated), NCCL all-gathers the
-    packed top-K keys ([world, nq, k], 8 B each) and merges them on device.
-    Every rank returns the global (ids, dists, counts)."""
+    row and scans them for all nq queries (replicated) in two phases: the
+    radius seed over its first rows, an NCCL all-reduce(MIN) of the per-query
+    radius, the streaming passes; then an NCCL all-gather of the packed top-K
+    keys ([world, nq, k], 8 B each) and the device merge. Every rank returns
+    the global (ids, dists, counts)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     keys = torch.empty((nq, k), dtype=torch.int64, device=d_queries.device)
-    flat_search_keys(dev, d_queries, nq, k, keys, raw=raw)
+    radius = torch.empty((nq,), dtype=torch.int32, device=d_queries.device)
+    flags = _capi.DEVICE_PTRS | (_capi.QUERIES_RAW if raw else 0)
+    _capi.check(_capi.lib.dade_gpu_flat_search_keys_begin(dev.h, _capi.ptr(d_queries), nq, k, flags,
+                                                          _capi.ptr(keys), _capi.ptr(radius)))
+    dist.all_reduce(radius, op=dist.ReduceOp.MIN, group=group)  # every shard's seed bounds every query
+    ivf_search_keys_end(dev, radius)
     gathered = torch.empty((world, nq, k), dtype=torch.int64, device=d_queries.device)
     dist.all_gather_into_tensor(gathered, keys, group=group)
     ids = torch.empty((nq, k), dtype=torch.int32, device=d_queries.device)
