@@ -1520,7 +1520,15 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
         c->res_dists[j].ensure((size_t)nq * k * 4);
         c->res_counts[j].ensure((size_t)nq * 4);
     }
-    const bool prof = c->profiling;
+    // profiling / one-chunk staging are restored however the loop exits
+    struct Restore {
+        dade_gpu_ctx* c;
+        bool prof;
+        ~Restore() {
+            c->profiling = prof;
+            c->stage_one_chunk = false;
+        }
+    } restore{c, c->profiling};
     c->profiling = false;
     c->tl_on = false;
     std::vector<uint32_t> cap_used(nb, 0);
@@ -1579,7 +1587,7 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
     }
     wait_stream(s);
     wait_stream(c->d2h_stream);
-    c->profiling = prof;
+    c->profiling = restore.prof;
     if (timing) {
         for (uint32_t b = 0; b < nb; ++b) {
             float span = 0, gap = 0;
