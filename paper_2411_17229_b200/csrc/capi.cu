@@ -827,7 +827,11 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         // of 1024-row pieces growing 4x per pass, the radius tightened between.
         static const uint32_t flat_lo[6] = {0, 2, 8, 32, 128, 512};
         static const uint32_t flat_hi[6] = {2, 8, 32, 128, 512, 0xffffffffu};
-        const int n_pass = flat ? 6 : two_pass ? 3 : 1;
+        // IVF: pass 0 = the nearest lists' next rows, then (tcgen05 filter) one pass over
+        // everything else incl. the nearest lists' tails -- a separate middle pass for
+        // those tails (DADE_GPU_THREE_PASS) costs its own filter/survivor/merge launches
+        const bool fold = umma && two_pass && !flat && !env_flag("DADE_GPU_THREE_PASS");
+        const int n_pass = flat ? 6 : two_pass ? (fold ? 2 : 3) : 1;
         // The next staging's H2D (pipelined batches) starts with the last pass, not
         // after this search's rotation: under the seed and the early passes the
         // copy slowed the search by ~60 us, under the last pass's tcgen05 filter
@@ -873,13 +877,16 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 f.piece_lo = flat_lo[pass];
                 f.piece_hi = flat_hi[pass];
             } else if (two_pass) {
-                if (pass < 2) {
+                uint32_t p0_rows = kFilterItemRows;  // rows of each nearest list (past the seed) in pass 0
+                if (const char* e = std::getenv("DADE_GPU_P0_ROWS")) p0_rows = (uint32_t)std::atoi(e);
+                const uint32_t p0 = std::max<uint32_t>(1, p0_rows / rank0_item_rows(umma));
+                if (pass == 0 || (pass == 1 && !fold)) {
                     f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
-                    uint32_t p0_rows = kFilterItemRows;  // rows of each nearest list (past the seed) in pass 0
-                    if (const char* e = std::getenv("DADE_GPU_P0_ROWS")) p0_rows = (uint32_t)std::atoi(e);
-                    const uint32_t p0 = std::max<uint32_t>(1, p0_rows / rank0_item_rows(umma));
                     f.piece_lo = pass == 0 ? 0u : p0;
                     f.piece_hi = pass == 0 ? p0 : 0xffffffffu;
+                } else if (fold) {  // every item: bucket 0 from piece p0 on, the rest whole
+                    f.b0_items = g->n_items + 1;
+                    f.b0_piece_lo = p0;
                 } else {
                     f.item_base = g->n_items + 1;  // the rest
                 }

@@ -74,6 +74,8 @@ struct FilterArgs {
     uint32_t* item_counter;       // persistent scheduling (zeroed before the launch)
     const float* row_norms;       // [rows + 32] first-slice |o|^2 per storage row
     uint32_t piece_lo, piece_hi;  // only items whose row piece is in [piece_lo, piece_hi)
+    const uint32_t* b0_items;     // nullable: items below *b0_items (rank bucket 0) need piece >= b0_piece_lo
+    uint32_t b0_piece_lo;         //   instead (the last IVF pass also takes the nearest lists' tails)
     int debug;                    // 1: re-check every filter prune exactly (counters[3] = violations)
     unsigned long long* census;   // nullable: [0] tiles with kept pairs | tiles << 32, [1] kept pairs (diagnostic)
     const float* q_norms;         // [nq] first-slice |q|^2 (sequential fmaf), tcgen05 filter only

@@ -237,7 +237,9 @@ dco_filter_umma_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap t
                 if (item >= end) break;
                 wi = a.items[item];
                 const uint32_t piece = wi.bucket_count >> 16;
-                if (piece >= a.piece_lo && piece < a.piece_hi) {
+                const bool ok = (a.b0_items && item < *a.b0_items) ? piece >= a.b0_piece_lo
+                                                                   : (piece >= a.piece_lo && piece < a.piece_hi);
+                if (ok) {
                     have = true;
                     break;
                 }
