@@ -115,7 +115,20 @@ def measured_bf16():
 
 
 def ncu_traffic(kernel: str = "dco_filter_umma"):
-    """dram bytes per launch of the scan kernel from the committed ncu summary."""
+    """dram bytes per launch of the scan kernel from the committed ncu summary
+    (the newest per-step summary's launches of that kernel, one search's worth)."""
+    steps = sorted((ROOT / "profiles").glob("ncu_step_summary_*.json"))
+    if steps:
+        try:
+            d = json.loads(steps[-1].read_text())
+            ls = [x for x in d["launches"] if x["kernel"].startswith(kernel)]
+            # the first launch of the capture may belong to the previous search: one search = the last
+            # launches up to the step's launch count (2 filter passes)
+            ls = ls[-2:] if len(ls) >= 2 else ls
+            if ls:
+                return float(np.mean([(x["dram_read_MB"] + x["dram_write_MB"]) * 1e6 for x in ls])), steps[-1].name
+        except Exception:
+            pass
     for p in sorted((ROOT / "profiles").glob("ncu_*summary*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
