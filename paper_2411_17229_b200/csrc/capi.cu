@@ -1343,7 +1343,7 @@ const float* stage_queries(dade_gpu_ctx* c, const float* queries, uint32_t nq, u
                            uint32_t flags) {
     const size_t bytes = (size_t)nq * dim * 4;
     c->probes_ready = false;
-    if (!(flags & DADE_GPU_DEVICE_PTRS) && (flags & DADE_GPU_QUERIES_RAW) && c->t_dim == dim && nq >= 2048 &&
+    if (!(flags & DADE_GPU_DEVICE_PTRS) && (flags & DADE_GPU_QUERIES_RAW) && c->t_dim == dim && (nq >= 2048 || c->stage_one_chunk) &&
         !env_flag("DADE_GPU_NO_OVERLAP"))
         if (const float* d = stage_queries_overlapped(c, queries, nq, dim)) return d;
     const float* d_in = queries;
