@@ -1024,6 +1024,12 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     // the streaming filter splits long lists into row pieces (more, shorter items)
     g.max_item_rows = use_filter ? kFilterItemRows : 0;
     const bool umma = use_filter && umma_ok(c, ct, tma);
+    if (umma && nrb == 3 && !env_flag("DADE_GPU_THREE_PASS") && !env_flag("DADE_GPU_RB3")) {
+        // the tcgen05 path scans ranks 1-3 and the rest in the same (last) pass: one bucket,
+        // fewer and fuller items (the other paths keep the nearer ranks' items first)
+        g.rb_end[1] = n_probe;
+        g.n_rb = nrb = 2;
+    }
     g.rank0_item_rows = use_filter && nrb > 1 ? rank0_item_rows(umma) : 0;
     g.q_chunk = umma ? kUmmaQ : use_filter ? kFilterQ : (uint32_t)kQC;
     const bool seeded = n_probe > 1 && !seed_disabled() && k <= 512;
