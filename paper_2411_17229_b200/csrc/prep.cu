@@ -118,7 +118,7 @@ __global__ void group_count_kernel(const GroupArgs g) {
 // global atomic per touched entry, so a list probed by most queries costs one
 // atomic per CTA instead of one per query.
 constexpr uint32_t kGroupSmemEntries = 12288;
-constexpr uint32_t kGroupPerThread = 16;  // pairs per thread
+constexpr uint32_t kGroupPerThread = 4;   // pairs per thread (more CTAs: count 18 -> 8 us, scatter 27 -> 14 us at config 1)
 
 __device__ __forceinline__ uint32_t pair_entry(const GroupArgs& g, size_t i) {
     const uint32_t p = (uint32_t)(i % g.n_probe);
