@@ -455,6 +455,7 @@ def run_ours(args, cfg):
                "api": "dade_gpu_ivf_search_batches: K steps as one pipelined call over pinned host buffers "
                       "(raw queries H2D, rotation, search, ids/dists/counts D2H every step; host wall clock "
                       "around the call, which returns after the last D2H)",
+               "l2": "not flushed between the pipelined steps: each step streams the 1 GB base (> 126 MB L2)",
                "single_call": {"value": nq / float(np.mean(ts)), "ms_per_call": 1e3 * float(np.mean(ts)),
                                "recall_at_k": e2e_rec,
                                "api": "dade_gpu_ivf_search per step, synchronous, L2 flushed between calls"},
