@@ -957,7 +957,8 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             if (sv.qslots) {
                 cuda_check(launch_merge_slots(sv.qslots, sv.qslot_cap, c->q_count.as<uint32_t>(),
                                               c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
-                                              c->cand_count.as<uint32_t>(), cap, nq, k, out_keys, out_count, s),
+                                              c->cand_count.as<uint32_t>(), cap, nq, k, out_keys, out_count, s,
+                                              pass + 1 < n_pass ? a.r_global : nullptr),
                            "merge slots");
                 c->launches -= 2;
             } else {
@@ -971,7 +972,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                            "merge buckets");
             }
             c->launches += 5;
-            if (pass + 1 < n_pass) {
+            if (pass + 1 < n_pass && !sv.qslots) {  // (the slot merge tightens as it finishes a query)
                 tighten_from_topk_kernel<<<(nq + 255) / 256, 256, 0, s>>>(out_keys, out_count, nq, k, a.r_global);
                 cuda_check(cudaGetLastError(), "tighten");
                 ++c->launches;

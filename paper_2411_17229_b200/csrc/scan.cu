@@ -1281,7 +1281,7 @@ __global__ void __launch_bounds__(128)
 merge_slots_kernel(const uint64_t* __restrict__ qslots, uint32_t cap, const uint32_t* __restrict__ q_count,
                    const uint32_t* __restrict__ cand_q, const uint64_t* __restrict__ cand_key,
                    const uint32_t* __restrict__ cand_count, uint32_t cand_cap, uint32_t nq, uint32_t K,
-                   uint64_t* out_keys, uint32_t* out_count) {
+                   uint64_t* out_keys, uint32_t* out_count, uint32_t* r_global) {
     __shared__ uint64_t bbuf[4][256];
     __shared__ uint64_t abuf[4][kStageMaxK];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1325,6 +1325,8 @@ merge_slots_kernel(const uint64_t* __restrict__ qslots, uint32_t cap, const uint
     }
     const uint32_t c = *reinterpret_cast<volatile uint32_t*>(cA);
     for (uint32_t i = c + lane; i < K; i += 32) A[i] = kEmptyKey;
+    // tighten the radius to the K-th key for the next pass (tighten_from_topk_kernel, fused)
+    if (r_global && lane == 0 && c >= K) atomicMin(r_global + q, (uint32_t)(A[K - 1] >> 32));
 }
 
 // Final per-query merge of n_slots segments into out_keys [nq x K] (K5).
@@ -1471,10 +1473,10 @@ cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* can
 cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const uint32_t* q_count,
                                const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
                                uint32_t cand_cap, uint32_t nq, uint32_t K, uint64_t* out_keys, uint32_t* out_count,
-                               cudaStream_t s) {
+                               cudaStream_t s, uint32_t* r_global) {
     if (nq == 0) return cudaSuccess;
     merge_slots_kernel<<<(nq + 3) / 4, 128, 0, s>>>(qslots, qslot_cap, q_count, cand_q, cand_key, cand_count, cand_cap,
-                                                    nq, K, out_keys, out_count);
+                                                    nq, K, out_keys, out_count, r_global);
     return cudaGetLastError();
 }
 
