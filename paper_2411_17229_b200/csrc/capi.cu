@@ -347,6 +347,12 @@ struct dade_gpu_ctx {
     // ivf
     bool has_ivf = false;
     bool sharded = false;  // set_ivf_shard removed lists with rows
+    struct {  // results of the search in flight, written by its last slot merge when set
+        uint32_t* ids = nullptr;
+        float* dists = nullptr;
+        uint32_t* counts = nullptr;
+        bool done = false;
+    } fo;
     uint32_t seed_rows_set = 0;  // dade_gpu_set_seed_rows (0: the default rule)
     // two-phase search (dade_gpu_ivf_search_keys_begin/_end): 1 = stop before the
     // last pass, 2 = resume at it; the begun search's arguments
@@ -958,8 +964,11 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 cuda_check(launch_merge_slots(sv.qslots, sv.qslot_cap, c->q_count.as<uint32_t>(),
                                               c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
                                               c->cand_count.as<uint32_t>(), cap, nq, k, out_keys, out_count, s,
-                                              pass + 1 < n_pass ? a.r_global : nullptr),
+                                              pass + 1 < n_pass ? a.r_global : nullptr,
+                                              pass + 1 == n_pass && !stop ? c->fo.ids : nullptr, c->fo.dists,
+                                              c->fo.counts),
                            "merge slots");
+                if (pass + 1 == n_pass && !stop && c->fo.ids) c->fo.done = true;
                 c->launches -= 2;
             } else {
                 cuda_check(launch_bucket_candidates(c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
@@ -1435,8 +1444,6 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     tl_mark(c, "staged", s);
     c->out_keys.ensure((size_t)nq * k * 8);
     c->out_count.ensure((size_t)nq * 4);
-    run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
-    tl_mark(c, "searched", s);
     const bool dev = flags & DADE_GPU_DEVICE_PTRS;
     uint32_t* ids = out_ids;
     float* dists = out_dists;
@@ -1449,10 +1456,18 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
         dists = c->out_dists.as<float>();
         cnts = c->out_counts.as<uint32_t>();
     }
-    cuda_check(launch_keys_to_results(c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), nq, k, ids,
-                                      dists, cnts, s),
-               "keys_to_results");
-    ++c->launches;
+    // the streaming path's last slot merge writes ids / dists / counts itself (fo.done)
+    c->fo = {ids, dists, cnts, false};
+    run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
+    const bool fused = c->fo.done;
+    c->fo = {};
+    tl_mark(c, "searched", s);
+    if (!fused) {
+        cuda_check(launch_keys_to_results(c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), nq, k, ids,
+                                          dists, cnts, s),
+                   "keys_to_results");
+        ++c->launches;
+    }
     if (!dev) {
         cuda_check(cudaMemcpyAsync(out_ids, ids, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, s), "D2H ids");
         cuda_check(cudaMemcpyAsync(out_dists, dists, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, s), "D2H dists");

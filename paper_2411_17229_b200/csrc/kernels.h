@@ -142,7 +142,9 @@ cudaError_t launch_merge_buckets(const uint64_t* bucket, const uint32_t* q_off, 
 cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const uint32_t* q_count,
                                const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
                                uint32_t cand_cap, uint32_t nq, uint32_t K, uint64_t* out_keys, uint32_t* out_count,
-                               cudaStream_t s, uint32_t* r_global = nullptr);
+                               cudaStream_t s, uint32_t* r_global = nullptr,
+                               uint32_t* res_ids = nullptr, float* res_dists = nullptr,
+                               uint32_t* res_counts = nullptr);
 cudaError_t launch_scan(const ScanArgs& a, const ChunkTable& ct, const CUtensorMap& tmap,
                         const CUtensorMap& tmap_norms, uint32_t grid, bool sqrt_key, cudaStream_t s);
 cudaError_t launch_row_norms(const float* rows, uint32_t n, uint32_t dim, uint32_t d0, float* out, cudaStream_t s);

@@ -1281,7 +1281,8 @@ __global__ void __launch_bounds__(128)
 merge_slots_kernel(const uint64_t* __restrict__ qslots, uint32_t cap, const uint32_t* __restrict__ q_count,
                    const uint32_t* __restrict__ cand_q, const uint64_t* __restrict__ cand_key,
                    const uint32_t* __restrict__ cand_count, uint32_t cand_cap, uint32_t nq, uint32_t K,
-                   uint64_t* out_keys, uint32_t* out_count, uint32_t* r_global) {
+                   uint64_t* out_keys, uint32_t* out_count, uint32_t* r_global, uint32_t* res_ids,
+                   float* res_dists, uint32_t* res_counts) {
     __shared__ uint64_t bbuf[4][256];
     __shared__ uint64_t abuf[4][kStageMaxK];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1327,6 +1328,15 @@ merge_slots_kernel(const uint64_t* __restrict__ qslots, uint32_t cap, const uint
     for (uint32_t i = c + lane; i < K; i += 32) A[i] = kEmptyKey;
     // tighten the radius to the K-th key for the next pass (tighten_from_topk_kernel, fused)
     if (r_global && lane == 0 && c >= K) atomicMin(r_global + q, (uint32_t)(A[K - 1] >> 32));
+    if (res_ids) {  // the search's last merge: ids / dists / count (keys_to_results_kernel, fused)
+        __syncwarp();
+        for (uint32_t i = lane; i < K; i += 32) {
+            const uint64_t v = A[i];
+            res_ids[(size_t)q * K + i] = i < c ? (uint32_t)v : 0xffffffffu;
+            res_dists[(size_t)q * K + i] = i < c ? __uint_as_float((uint32_t)(v >> 32)) : __int_as_float(0x7f800000);
+        }
+        if (lane == 0 && res_counts) res_counts[q] = c;
+    }
 }
 
 // Final per-query merge of n_slots segments into out_keys [nq x K] (K5).
@@ -1473,10 +1483,12 @@ cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* can
 cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const uint32_t* q_count,
                                const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
                                uint32_t cand_cap, uint32_t nq, uint32_t K, uint64_t* out_keys, uint32_t* out_count,
-                               cudaStream_t s, uint32_t* r_global) {
+                               cudaStream_t s, uint32_t* r_global, uint32_t* res_ids, float* res_dists,
+                               uint32_t* res_counts) {
     if (nq == 0) return cudaSuccess;
     merge_slots_kernel<<<(nq + 3) / 4, 128, 0, s>>>(qslots, qslot_cap, q_count, cand_q, cand_key, cand_count, cand_cap,
-                                                    nq, K, out_keys, out_count, r_global);
+                                                    nq, K, out_keys, out_count, r_global, res_ids, res_dists,
+                                                    res_counts);
     return cudaGetLastError();
 }
 
