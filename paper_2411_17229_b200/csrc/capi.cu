@@ -1583,15 +1583,20 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
         c->stage_one_chunk = b > 0;
         const float* d_q = stage_queries(c, queries[b], nq, dim, flags);
         c->stage_one_chunk = false;
+        if (b >= 2) cuda_check(cudaStreamWaitEvent(s, c->d2h_ev[j], 0), "wait");  // set j's D2H done
+        c->fo = {c->res_ids[j].as<uint32_t>(), c->res_dists[j].as<float>(), c->res_counts[j].as<uint32_t>(), false};
         run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
+        const bool fused = c->fo.done;
+        c->fo = {};
         cap_used[b] = c->surv_cap_used;
         coarse_used[b] = c->coarse_tc_used;
-        if (b >= 2) cuda_check(cudaStreamWaitEvent(s, c->d2h_ev[j], 0), "wait");  // set j's D2H done
-        cuda_check(launch_keys_to_results(c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), nq, k,
-                                          c->res_ids[j].as<uint32_t>(), c->res_dists[j].as<float>(),
-                                          c->res_counts[j].as<uint32_t>(), s),
-                   "keys_to_results");
-        ++c->launches;
+        if (!fused) {
+            cuda_check(launch_keys_to_results(c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), nq, k,
+                                              c->res_ids[j].as<uint32_t>(), c->res_dists[j].as<float>(),
+                                              c->res_counts[j].as<uint32_t>(), s),
+                       "keys_to_results");
+            ++c->launches;
+        }
         auto* slot = reinterpret_cast<unsigned char*>(c->batch_slot.p) + 32 * j;
         cuda_check(cudaMemsetAsync(slot, 0, 16, s), "memset");
         if (cap_used[b]) cuda_check(cudaMemcpyAsync(slot, c->surv_max.p, 4, cudaMemcpyDeviceToDevice, s), "flags");
