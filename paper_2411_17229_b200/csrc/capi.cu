@@ -199,7 +199,6 @@ bool make_1d_tmap(CUtensorMap* m, const float* base, uint64_t n) {
     const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<float*>(base), gdim, gstride, box,
                               estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS && std::getenv("DADE_GPU_VERBOSE")) std::fprintf(stderr, "[dade_gpu] 1d tmap error %d\n", (int)r);
     return r == CUDA_SUCCESS;
 }
 
@@ -222,7 +221,6 @@ struct RowNorms {
             dim = d;
             d0 = dd0;
             tm_ok = true;  // windows are fetched with a plain bulk copy
-            if (std::getenv("DADE_GPU_VERBOSE")) std::fprintf(stderr, "[dade_gpu] row norms n=%u d0=%u tmap=%d\n", nn, dd0, (int)tm_ok);
         }
         return buf.as<float>();
     }
@@ -285,7 +283,7 @@ struct SliceTmap {
             dim = d;
             ok = make_slice_tmap(&map, b, std::max<uint64_t>(r, 1), d);
         }
-        return ok && !env_flag("DADE_GPU_NO_TMA") ? &map : nullptr;
+        return ok ? &map : nullptr;
     }
 };
 
@@ -323,10 +321,8 @@ struct TmapCache {
             rows = r;
             dim = d;
             ok = make_row_tmap(&map, b, r, d, box_rows);
-            if (std::getenv("DADE_GPU_VERBOSE")) std::fprintf(stderr, "[dade_gpu] row tmap rows=%llu dim=%u ok=%d\n", (unsigned long long)r, d, (int)ok);
         }
-        const char* env = std::getenv("DADE_GPU_NO_TMA");
-        usable = ok && !(env && env[0] == '1');
+        usable = ok;
         return map;
     }
 };
@@ -438,6 +434,19 @@ struct dade_gpu_ctx {
 
 namespace {
 
+// The result pointers the last slot merge of the search in flight writes
+// (ctx.fo), cleared however the search exits, so a later keys-only search
+// never writes through a stale pointer.
+struct FusedOutputs {
+    dade_gpu_ctx* c;
+    FusedOutputs(dade_gpu_ctx* cc, uint32_t* ids, float* dists, uint32_t* counts) : c(cc) {
+        c->fo = {ids, dists, counts, false};
+    }
+    ~FusedOutputs() { c->fo = {}; }
+    FusedOutputs(const FusedOutputs&) = delete;
+    FusedOutputs& operator=(const FusedOutputs&) = delete;
+};
+
 void upload(DevBuf& b, const void* src, size_t bytes, cudaStream_t s) {
     b.ensure(bytes);
     if (bytes) cuda_check(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, s), "H2D copy");
@@ -469,7 +478,7 @@ void set_tables(dade_gpu_ctx* c, uint32_t kind, uint32_t dim, std::vector<uint32
 }
 
 bool coarse_tc_ok(dade_gpu_ctx* c, uint32_t n_probe) {
-    return n_probe <= 256 && !c->coarse_force_exact && !env_flag("DADE_GPU_NO_TC_COARSE");
+    return n_probe <= 256 && !c->coarse_force_exact;
 }
 // queries per coarse chunk: the p~ buffer holds chunk x n_clusters fp32 (<= 1 GB).
 // Large chunks keep the selection (a warp per query) at full occupancy: with
@@ -507,9 +516,9 @@ void coarse_tc_range(dade_gpu_ctx* c, const float* d_q, uint32_t q0, uint32_t m,
                                        c->qnorm.as<float>(), s),
                    "coarse norms");
         // nlist > 1024: the GEMM epilogue also leaves the per-32-centroid minima of the
-        // upper bounds, the selection's first pass (DADE_GPU_NO_GMIN: the selection reads p~ for them)
+        // upper bounds, the selection's first pass
         uint32_t* gmin = nullptr;
-        if (c->n_clusters > 1024 && c->n_clusters <= 16384 && !env_flag("DADE_GPU_NO_GMIN")) {
+        if (c->n_clusters > 1024 && c->n_clusters <= 16384) {
             c->coarse_gmin.ensure((size_t)coarse_tc_chunk(c, m) * ((c->n_clusters + 31) / 32) * 4);
             gmin = c->coarse_gmin.as<uint32_t>();
         }
@@ -601,10 +610,7 @@ constexpr uint32_t kFilterQ = 32;           // queries per streaming work item (
 constexpr uint32_t kUmmaQ = 256;            // queries per tcgen05 work item (MMA N)
 constexpr uint32_t kQSlots = 256;           // per-query candidate slots of a streaming pass
 uint32_t rank0_item_rows(bool umma) {
-    uint32_t r = umma ? 128 : 32;  // one tile: a nearest list's heavy rows spread over every SM / warp
-    if (const char* e = std::getenv("DADE_GPU_R0_ROWS")) r = (uint32_t)std::atoi(e);
-    r = std::max<uint32_t>(32, std::min<uint32_t>(r, kFilterItemRows));
-    return r;
+    return umma ? 128 : 32;  // one tile: a nearest list's heavy rows spread over every SM / warp
 }
 constexpr uint32_t kSeedRowsDefault = 1024;  // rows of the nearest list used by the radius seed
 
@@ -615,32 +621,11 @@ constexpr uint32_t kSeedRowsDefault = 1024;  // rows of the nearest list used by
 // cost bytes per query -- config 2 1.47 -> 1.21 ms per batch at recall 0.982 vs
 // 0.987). The flat scan's groups are full (every query probes the base): 1024.
 uint32_t seed_rows(const dade_gpu_ctx* c, uint32_t k, uint32_t dim, bool flat = false) {
-    const bool list_kernel = k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY");
+    const bool list_kernel = k <= 128;
     uint32_t s = kSeedRowsDefault;
     if (c->seed_rows_set) return std::min<uint32_t>(list_kernel ? 1024 : 512, std::max<uint32_t>(c->seed_rows_set, k));
     if (dim > 256 && !flat) s = std::min<uint32_t>(s, std::max<uint32_t>(128, (262144u / dim) & ~127u));
-    if (const char* e = std::getenv("DADE_GPU_SEED_ROWS")) s = (uint32_t)std::atoi(e);
     return std::min<uint32_t>(list_kernel ? 1024 : 512, std::max<uint32_t>(s, k));
-}
-
-bool seed_disabled() {
-    const char* e = std::getenv("DADE_GPU_NO_SEED");
-    return e && e[0] == '1';
-}
-
-// the phase buffer without resetting it (nullptr unless DADE_GPU_PHASES=1)
-unsigned long long* phase_ptr_keep(dade_gpu_ctx* c) {
-    const char* e = std::getenv("DADE_GPU_PHASES");
-    if (!(e && e[0] == '1') || !c->phase.p) return nullptr;
-    return c->phase.as<unsigned long long>();
-}
-
-unsigned long long* phase_ptr(dade_gpu_ctx* c) {
-    const char* e = std::getenv("DADE_GPU_PHASES");
-    if (!(e && e[0] == '1')) return nullptr;
-    c->phase.ensure(64);
-    cuda_check(cudaMemsetAsync(c->phase.p, 0, 64, c->stream), "memset");
-    return c->phase.as<unsigned long long>();
 }
 
 void tl_mark(dade_gpu_ctx* c, const char* name, cudaStream_t s) {
@@ -698,13 +683,6 @@ void finish_profile(dade_gpu_ctx* c) {
     }
 }
 
-__global__ void tighten_from_topk_kernel(const uint64_t* keys, const uint32_t* count, uint32_t nq, uint32_t K,
-                                         uint32_t* r_global) {
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nq || count[q] < K) return;
-    atomicMin(r_global + q, (uint32_t)(keys[(size_t)q * K + K - 1] >> 32));
-}
-
 __global__ void min_u32_kernel(uint32_t* r, const uint32_t* other, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) r[i] = min(r[i], other[i]);
@@ -713,7 +691,7 @@ __global__ void min_u32_kernel(uint32_t* r, const uint32_t* other, uint32_t n) {
 // The streaming tensor-core path applies when the first checkpoint is a
 // multiple of 8 dims (MMA k) within two 32-dim TMA boxes.
 bool filter_ok(dade_gpu_ctx* c, const ChunkTable& ct, uint32_t dim) {
-    if (!ct.use_tc || !ct.use_tma || ct.n_ckpt > 63 || env_flag("DADE_GPU_NO_STREAM")) return false;
+    if (!ct.use_tc || !ct.use_tma || ct.n_ckpt > 63) return false;
     const uint32_t d0 = ct.end[ct.n_dense - 1];
     return d0 % 8 == 0 && d0 <= 2 * kBox && dim % 4 == 0 && dim >= (uint32_t)kBox;
 }
@@ -765,19 +743,14 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         c->cand_key.ensure((size_t)cap * 8);
         c->cand_count.ensure(4);
         c->q_count.ensure((size_t)nq * 4);
-        c->q_off.ensure((size_t)nq * 4);
-        c->q_cursor.ensure((size_t)nq * 4);
-        c->bucket.ensure((size_t)cap * 8);
         c->surv_max.ensure(4);
         if (!resume) {
             cuda_check(cudaMemsetAsync(c->surv_max.p, 0, 4, s), "memset");
             cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
         }
         if (seed.on && !resume) {
-            const CUtensorMap* stm = (g && k <= 128 && seed_tma_ok(a.dim, k) && !env_flag("DADE_GPU_SEED_V1") &&
-                                      !env_flag("DADE_GPU_SEED_PER_QUERY"))
-                                         ? c->seed_tm.get(rows, n_rows, a.dim)
-                                         : nullptr;
+            const CUtensorMap* stm =
+                (g && k <= 128 && seed_tma_ok(a.dim, k)) ? c->seed_tm.get(rows, n_rows, a.dim) : nullptr;
             if (stm) {
                 SeedListArgs sa{};
                 sa.counts = g->counts;
@@ -798,10 +771,8 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 sa.out_count = out_count;
                 sa.nz2 = 0x8000000080000000ull;
                 c->seed_work.ensure(4);
-                if (!env_flag("DADE_GPU_SEED_LIST_ORDER")) {  // tuning hook: groups in list order
-                    c->seed_order.ensure(((size_t)nq / kSeedGroup + g->n_lists + 1) * 4);
-                    sa.order = c->seed_order.as<uint32_t>();
-                }
+                c->seed_order.ensure(((size_t)nq / kSeedGroup + g->n_lists + 1) * 4);
+                sa.order = c->seed_order.as<uint32_t>();
                 c->seed_profiled = c->profiling;
                 if (c->profiling) {  // device time and pair-dims of the seed (dade_gpu_last_seed_profile)
                     c->seed_census.ensure(8);
@@ -812,7 +783,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 cuda_check(launch_seed_tma(sa, *stm, nq / kSeedGroup + g->n_lists + 1, s, c->seed_work.as<uint32_t>()),
                            "seed radius (tma)");
                 if (c->profiling) cuda_check(cudaEventRecord(c->es[1], s), "event");
-            } else if (g && g->n_rb >= 1 && k <= 128 && !env_flag("DADE_GPU_SEED_PER_QUERY"))
+            } else if (g && g->n_rb >= 1 && k <= 128)
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->seed_glist,
                                                     g->n_lists,
                                                     nq / kSeedGroup + g->n_lists + 1, seed.offsets, rows, a.row_ids,
@@ -835,21 +806,19 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         static const uint32_t flat_hi[6] = {2, 8, 32, 128, 512, 0xffffffffu};
         // IVF: pass 0 = the nearest lists' next rows, then (tcgen05 filter) one pass over
         // everything else incl. the nearest lists' tails -- a separate middle pass for
-        // those tails (DADE_GPU_THREE_PASS) costs its own filter/survivor/merge launches
-        const bool fold = umma && two_pass && !flat && !env_flag("DADE_GPU_THREE_PASS");
+        // those tails costs its own filter/survivor/merge launches
+        const bool fold = umma && two_pass && !flat;
         const int n_pass = flat ? 6 : two_pass ? (fold ? 2 : 3) : 1;
         // The next staging's H2D (pipelined batches) starts with the last pass, not
         // after this search's rotation: under the seed and the early passes the
         // copy slowed the search by ~60 us, under the last pass's tcgen05 filter
-        // by nothing measurable (tools/e2e_pipe.py; DADE_GPU_H2D_AT_PASS overrides)
-        static const int h2d_pass = std::getenv("DADE_GPU_H2D_AT_PASS") ? std::atoi(std::getenv("DADE_GPU_H2D_AT_PASS")) : -1;
-        static const int max_pass = std::getenv("DADE_GPU_MAX_PASS") ? std::atoi(std::getenv("DADE_GPU_MAX_PASS")) : 99;  // diagnostic
+        // by nothing measurable
         // two-phase split: IVF before its last pass (nearest lists done), flat right after the seed
         const int split_pass = flat ? 0 : n_pass - 1;
-        for (int pass = 0; pass < std::min(n_pass, max_pass); ++pass) {
+        for (int pass = 0; pass < n_pass; ++pass) {
             if (resume && pass < split_pass) continue;  // phase 2: from the split pass on
             if (stop && pass == split_pass) break;      // phase 1: everything before it
-            if (pass == (h2d_pass >= 0 ? h2d_pass : n_pass - 1) && c->qin_free_recorded)
+            if (pass == n_pass - 1 && c->qin_free_recorded)
                 cuda_check(cudaEventRecord(c->copy_ev[8], s), "event");
             cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
             FilterArgs f{};
@@ -876,16 +845,13 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             f.piece_lo = 0;
             f.piece_hi = 0xffffffffu;
             f.debug = ct.debug;
-            if (const char* ex = std::getenv("DADE_GPU_UMMA_EXP")) f.exp = std::atoi(ex);
-            if (unsigned long long* ph = phase_ptr_keep(c)) f.census = umma ? (pass == n_pass - 1 ? ph : nullptr) : ph + 2 * pass;  // DADE_GPU_PHASES=1
             if (flat) {
                 f.n_items = g->n_items + 1;
                 f.piece_lo = flat_lo[pass];
                 f.piece_hi = flat_hi[pass];
             } else if (two_pass) {
-                uint32_t p0_rows = kFilterItemRows;  // rows of each nearest list (past the seed) in pass 0
-                if (const char* e = std::getenv("DADE_GPU_P0_ROWS")) p0_rows = (uint32_t)std::atoi(e);
-                const uint32_t p0 = std::max<uint32_t>(1, p0_rows / rank0_item_rows(umma));
+                // pass 0: kFilterItemRows rows of each nearest list past the seed
+                const uint32_t p0 = std::max<uint32_t>(1, kFilterItemRows / rank0_item_rows(umma));
                 if (pass == 0 || (pass == 1 && !fold)) {
                     f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
                     f.piece_lo = pass == 0 ? 0u : p0;
@@ -938,54 +904,37 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             sv.cand_count = c->cand_count.as<uint32_t>();
             sv.cand_cap = cap;
             sv.q_count = c->q_count.as<uint32_t>();
-            if (!env_flag("DADE_GPU_NO_QSLOTS")) {
-                c->qslots.ensure((size_t)nq * kQSlots * 8);
-                sv.qslots = c->qslots.as<uint64_t>();
-                sv.qslot_cap = kQSlots;
-                if (a.counters && (pass < 2 || !ct.debug)) {
-                    c->cand_total.ensure(4);
-                    cuda_check(cudaMemsetAsync(c->cand_total.p, 0, 4, s), "memset");
-                    sv.cand_total = c->cand_total.as<uint32_t>();
-                }
+            c->qslots.ensure((size_t)nq * kQSlots * 8);
+            sv.qslots = c->qslots.as<uint64_t>();
+            sv.qslot_cap = kQSlots;
+            if (a.counters && (pass < 2 || !ct.debug)) {
+                c->cand_total.ensure(4);
+                cuda_check(cudaMemsetAsync(c->cand_total.p, 0, 4, s), "memset");
+                sv.cand_total = c->cand_total.as<uint32_t>();
             }
             sv.counters = a.counters;
             sv.surv_max = c->surv_max.as<uint32_t>();
             cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
             // survivors / candidates of passes 0, 1 (low words of counters[4 + 2 pass ..]); of pass 2 in
             // counters[3] (low / high word) unless a debug mode owns that word
-            if (a.counters && (pass < 2 || (pass == 2 && !ct.debug && !std::getenv("DADE_GPU_DEBUG"))))
+            if (a.counters && (pass < 2 || (pass == 2 && !ct.debug)))
                 for (int w = 0; w < 2; ++w)
                     cuda_check(cudaMemcpyAsync(pass < 2 ? reinterpret_cast<uint32_t*>(a.counters + 4 + 2 * pass + w)
                                                         : reinterpret_cast<uint32_t*>(a.counters + 3) + w,
                                                w == 0 ? c->surv_count.p : sv.cand_total ? c->cand_total.p : c->cand_count.p, 4,
                                                cudaMemcpyDeviceToDevice, s),
                                "census");
-            if (sv.qslots) {
-                cuda_check(launch_merge_slots(sv.qslots, sv.qslot_cap, c->q_count.as<uint32_t>(),
-                                              c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
-                                              c->cand_count.as<uint32_t>(), cap, nq, k, out_keys, out_count, s,
-                                              pass + 1 < n_pass ? a.r_global : nullptr,
-                                              pass + 1 == n_pass && !stop ? c->fo.ids : nullptr, c->fo.dists,
-                                              c->fo.counts),
-                           "merge slots");
-                if (pass + 1 == n_pass && !stop && c->fo.ids) c->fo.done = true;
-                c->launches -= 2;
-            } else {
-                cuda_check(launch_bucket_candidates(c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
-                                                    c->cand_count.as<uint32_t>(), cap, c->q_count.as<uint32_t>(),
-                                                    c->q_off.as<uint32_t>(), c->q_cursor.as<uint32_t>(),
-                                                    c->bucket.as<uint64_t>(), nq, cap, s),
-                           "bucket candidates");
-                cuda_check(launch_merge_buckets(c->bucket.as<uint64_t>(), c->q_off.as<uint32_t>(),
-                                                c->q_count.as<uint32_t>(), nq, k, out_keys, out_count, s),
-                           "merge buckets");
-            }
-            c->launches += 5;
-            if (pass + 1 < n_pass && !sv.qslots) {  // (the slot merge tightens as it finishes a query)
-                tighten_from_topk_kernel<<<(nq + 255) / 256, 256, 0, s>>>(out_keys, out_count, nq, k, a.r_global);
-                cuda_check(cudaGetLastError(), "tighten");
-                ++c->launches;
-            }
+            // the slot merge tightens each query's radius as it finishes it; the search's
+            // last merge writes ids / dists / counts when the caller asked for them (fo)
+            cuda_check(launch_merge_slots(sv.qslots, sv.qslot_cap, c->q_count.as<uint32_t>(),
+                                          c->cand_q.as<uint32_t>(), c->cand_key.as<uint64_t>(),
+                                          c->cand_count.as<uint32_t>(), cap, nq, k, out_keys, out_count, s,
+                                          pass + 1 < n_pass ? a.r_global : nullptr,
+                                          pass + 1 == n_pass && !stop ? c->fo.ids : nullptr, c->fo.dists,
+                                          c->fo.counts),
+                       "merge slots");
+            if (pass + 1 == n_pass && !stop && c->fo.ids) c->fo.done = true;
+            c->launches += 3;
             tl_mark(c, "pass", s);
         }
     }
@@ -1034,7 +983,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     // the streaming filter splits long lists into row pieces (more, shorter items)
     g.max_item_rows = use_filter ? kFilterItemRows : 0;
     const bool umma = use_filter && umma_ok(c, ct, tma);
-    if (umma && nrb == 3 && !env_flag("DADE_GPU_THREE_PASS") && !env_flag("DADE_GPU_RB3")) {
+    if (umma && nrb == 3) {
         // the tcgen05 path scans ranks 1-3 and the rest in the same (last) pass: one bucket,
         // fewer and fuller items (the other paths keep the nearer ranks' items first)
         g.rb_end[1] = n_probe;
@@ -1042,7 +991,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     }
     g.rank0_item_rows = use_filter && nrb > 1 ? rank0_item_rows(umma) : 0;
     g.q_chunk = umma ? kUmmaQ : use_filter ? kFilterQ : (uint32_t)kQC;
-    const bool seeded = n_probe > 1 && !seed_disabled() && k <= 512;
+    const bool seeded = n_probe > 1 && k <= 512;
     if (use_filter && seeded) {  // the seed's rows of every nearest list are final results already
         g.seed_skip = seed_rows(c, k, c->dim);
         g.seed_min = k;
@@ -1107,7 +1056,6 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     a.coeff = c->d_coeff.as<double>();
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
-    a.phase = phase_ptr(c);
     if (const char* dbg = std::getenv("DADE_GPU_DEBUG"))
         if (std::atoi(dbg) == 3) a.census = c->counters.as<unsigned long long>() + 3;
     // Radius seeding: an exact (FD) pass over the first rows of every query's
@@ -1149,7 +1097,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
 bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uint64_t* out_keys,
                  uint32_t* out_count) {
     cudaStream_t s = c->stream;
-    if (env_flag("DADE_GPU_FLAT_V1") || std::getenv("DADE_GPU_FLAT_BLOCKS") || k > 128 || c->b_count == 0) return false;
+    if (std::getenv("DADE_GPU_FLAT_BLOCKS") || k > 128 || c->b_count == 0) return false;
     ChunkTable ct = make_chunks(c->b_dim, c->cps);
     bool tma = false;
     c->tm_base.get(c->base.as<float>(), std::max<uint32_t>(c->b_count, 1), c->b_dim, tma);
@@ -1220,7 +1168,6 @@ bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uin
     a.coeff = c->d_coeff.as<double>();
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
-    a.phase = phase_ptr(c);
     record(c, c->e1);
     SeedArgs sd{true, c->probes.as<uint64_t>(), 1, c->flat_offsets.as<uint32_t>()};
     stream_passes(c, a, ct, d_q, nq, k, false, (uint32_t)max_items, &g, c->base.as<float>(), c->b_count, c->tm_base,
@@ -1269,7 +1216,6 @@ void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t
     a.coeff = c->d_coeff.as<double>();
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
-    a.phase = phase_ptr(c);
     ChunkTable ct = make_chunks(c->b_dim, c->cps);
     bool tma = false;
     const CUtensorMap& tm = c->tm_base.get(a.storage, std::max<uint32_t>(c->b_count, 1), c->b_dim, tma);
@@ -1309,7 +1255,6 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
     const uint32_t cap = coarse ? coarse_tc_chunk(c, nq) : nq;
     uint32_t sizes[8], nch = 0, rem = nq;
     uint32_t want = std::max<uint32_t>(512, (uint32_t)((uint64_t)nq * 3 / 10 + 63) / 64 * 64);
-    if (const char* e = std::getenv("DADE_GPU_CHUNK0")) want = std::max(64, std::atoi(e));  // tuning hook
     if (c->stage_one_chunk) want = nq;  // the copy already ran ahead (pipelined batches)
     while (rem && nch < 8) {
         uint32_t m = std::min<uint32_t>({rem, cap, nch == 0 ? want : rem});
@@ -1319,17 +1264,11 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
         rem -= m;
     }
     if (rem) return nullptr;
-    if (std::getenv("DADE_GPU_VERBOSE")) {
-        cudaPointerAttributes pa{};
-        const cudaError_t e = cudaPointerGetAttributes(&pa, queries);
-        std::fprintf(stderr, "[dade_gpu] host queries %p: attr rc %d type %d, %u chunks, first %u\n", (const void*)queries,
-                     (int)e, (int)pa.type, nch, sizes[0]);
-    }
     // the copy stream must not overwrite q_in while earlier work reads it: when the
     // previous staging was this one, its rotations were the last readers (their
     // event lets this H2D run under the previous search); otherwise everything
     // enqueued so far may read it
-    if (!c->qin_free_recorded || env_flag("DADE_GPU_SERIAL_H2D")) cuda_check(cudaEventRecord(c->copy_ev[8], c->stream), "event");
+    if (!c->qin_free_recorded) cuda_check(cudaEventRecord(c->copy_ev[8], c->stream), "event");
     cuda_check(cudaStreamWaitEvent(c->copy_stream, c->copy_ev[8], 0), "wait");
     for (uint32_t i = 0, q0 = 0; i < nch; q0 += sizes[i], ++i) {
         cuda_check(cudaMemcpyAsync(c->q_in.as<float>() + (size_t)q0 * dim, queries + (size_t)q0 * dim,
@@ -1388,18 +1327,7 @@ void collect_stats(dade_gpu_ctx* c, dade_gpu_stats* stats) {
     stats->dims_accumulated += h[1];
 }
 
-// Wait for a search's results (DADE_GPU_SPIN_WAIT=1: poll the stream instead).
-void wait_stream(cudaStream_t s) {
-    if (!env_flag("DADE_GPU_SPIN_WAIT")) {
-        cuda_check(cudaStreamSynchronize(s), "search");
-        return;
-    }
-    for (;;) {
-        const cudaError_t e = cudaStreamQuery(s);
-        if (e == cudaSuccess) return;
-        if (e != cudaErrorNotReady) cuda_check(e, "search");
-    }
-}
+void wait_stream(cudaStream_t s) { cuda_check(cudaStreamSynchronize(s), "search"); }
 
 // Overflow flags of the search just enqueued (worklist, coarse candidate list):
 // read back with the results in one pinned copy; check after the sync.
@@ -1429,7 +1357,6 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
                    uint32_t flags, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
                    dade_gpu_stats* stats, const std::function<void(const float*, uint64_t*, uint32_t*)>& run) {
     c->use_device();
-    const auto t_host0 = std::chrono::steady_clock::now();
     cudaStream_t s = c->stream;
     c->counters.ensure(64);
     cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
@@ -1457,10 +1384,12 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
         cnts = c->out_counts.as<uint32_t>();
     }
     // the streaming path's last slot merge writes ids / dists / counts itself (fo.done)
-    c->fo = {ids, dists, cnts, false};
-    run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
-    const bool fused = c->fo.done;
-    c->fo = {};
+    bool fused = false;
+    {
+        FusedOutputs scope(c, ids, dists, cnts);
+        run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
+        fused = c->fo.done;
+    }
     tl_mark(c, "searched", s);
     if (!fused) {
         cuda_check(launch_keys_to_results(c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), nq, k, ids,
@@ -1477,12 +1406,7 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     tl_mark(c, "results_d2h", s);
     record(c, c->e3);
     enqueue_flags(c);
-    const auto t_host1 = std::chrono::steady_clock::now();
     wait_stream(s);
-    if (env_flag("DADE_GPU_HOST_TIMING"))
-        std::fprintf(stderr, "[dade_gpu] host enqueue %.3f ms, wait %.3f ms\n",
-                     std::chrono::duration<double, std::milli>(t_host1 - t_host0).count(),
-                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host1).count());
     if (search_overflowed(c)) {  // survivor worklist too small: redo with the observed size x2
         search_common(c, queries, nq, dim, k, flags, out_ids, out_dists, out_counts, stats, run);
         return;
@@ -1506,11 +1430,6 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     collect_stats(c, stats);
     finish_profile(c);
     tl_print(c);
-    if (std::getenv("DADE_GPU_COARSE_CENSUS") && c->coarse_tc_used) {
-        uint32_t h[2] = {0, 0};
-        cuda_check(cudaMemcpy(h, c->coarse_overflow.p, 8, cudaMemcpyDeviceToHost), "census");
-        std::fprintf(stderr, "[dade_gpu] coarse: %.1f exact candidates per query\n", (double)h[1] / std::max(1u, nq));
-    }
 }
 
 // Pipelined sequence of searches over host batches: batch b+1's H2D (copy
@@ -1562,19 +1481,8 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
     c->tl_on = false;
     std::vector<uint32_t> cap_used(nb, 0);
     std::vector<uint8_t> coarse_used(nb, 0);
-    // DADE_GPU_HOST_TIMING=1: per-batch host enqueue time and device span / gap (diagnostic)
-    const bool timing = env_flag("DADE_GPU_HOST_TIMING");
-    std::vector<cudaEvent_t> tev;
-    std::vector<double> t_enq;
     for (uint32_t b = 0; b < nb; ++b) {
         const uint32_t j = b & 1;
-        const auto th0 = std::chrono::steady_clock::now();
-        if (timing) {
-            tev.resize(2 * nb);
-            cuda_check(cudaEventCreate(&tev[2 * b]), "event");
-            cuda_check(cudaEventCreate(&tev[2 * b + 1]), "event");
-            cuda_check(cudaEventRecord(tev[2 * b], s), "event");
-        }
         cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
         c->n_filter_passes = 0;
         c->surv_cap_used = 0;
@@ -1584,10 +1492,13 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
         const float* d_q = stage_queries(c, queries[b], nq, dim, flags);
         c->stage_one_chunk = false;
         if (b >= 2) cuda_check(cudaStreamWaitEvent(s, c->d2h_ev[j], 0), "wait");  // set j's D2H done
-        c->fo = {c->res_ids[j].as<uint32_t>(), c->res_dists[j].as<float>(), c->res_counts[j].as<uint32_t>(), false};
-        run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
-        const bool fused = c->fo.done;
-        c->fo = {};
+        bool fused = false;
+        {
+            FusedOutputs scope(c, c->res_ids[j].as<uint32_t>(), c->res_dists[j].as<float>(),
+                               c->res_counts[j].as<uint32_t>());
+            run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
+            fused = c->fo.done;
+        }
         cap_used[b] = c->surv_cap_used;
         coarse_used[b] = c->coarse_tc_used;
         if (!fused) {
@@ -1604,10 +1515,6 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
             cuda_check(cudaMemcpyAsync(slot + 8, c->coarse_overflow.p, 4, cudaMemcpyDeviceToDevice, s), "flags");
         cuda_check(cudaMemcpyAsync(slot + 16, c->counters.p, 16, cudaMemcpyDeviceToDevice, s), "counters");
         cuda_check(cudaEventRecord(c->res_ev[j], s), "event");
-        if (timing) {
-            cuda_check(cudaEventRecord(tev[2 * b + 1], s), "event");
-            t_enq.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
-        }
         cudaStream_t t = c->d2h_stream;
         cuda_check(cudaStreamWaitEvent(t, c->res_ev[j], 0), "wait");
         cuda_check(cudaMemcpyAsync(out_ids[b], c->res_ids[j].p, (size_t)nq * k * 4, cudaMemcpyDeviceToHost, t), "D2H ids");
@@ -1622,16 +1529,6 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
     wait_stream(s);
     wait_stream(c->d2h_stream);
     c->profiling = restore.prof;
-    if (timing) {
-        for (uint32_t b = 0; b < nb; ++b) {
-            float span = 0, gap = 0;
-            cuda_check(cudaEventElapsedTime(&span, tev[2 * b], tev[2 * b + 1]), "elapsed");
-            if (b) cuda_check(cudaEventElapsedTime(&gap, tev[2 * b - 1], tev[2 * b]), "elapsed");
-            std::fprintf(stderr, "[dade_gpu] batch %u: host enqueue %.3f ms, device span %.3f ms, gap before %.3f ms\n", b,
-                         t_enq[b], span, gap);
-        }
-        for (cudaEvent_t e : tev) cudaEventDestroy(e);
-    }
     for (uint32_t b = 0; b < nb; ++b) {
         const unsigned long long* h = c->h_batch + 4 * (size_t)b;
         const bool surv_over = cap_used[b] && h[0] > cap_used[b];

@@ -640,8 +640,8 @@ void launch_select_any(const float* pt, const float* cnorm, const float* qnorm, 
                        const float* queries, uint32_t nq, uint32_t dim, uint32_t n_probe, uint64_t* probes,
                        uint32_t* overflow, cudaStream_t s, const uint32_t* gmin = nullptr) {
     if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap) {
-        uint32_t* census = std::getenv("DADE_GPU_COARSE_CENSUS") ? overflow + 1 : nullptr;
-        if (nq <= 4096 && n_probe > 32 && !std::getenv("DADE_GPU_SELECT_WPQ1"))  // > 1 exact round
+        uint32_t* census = nullptr;
+        if (nq <= 4096 && n_probe > 32)  // > 1 exact round
             coarse_select_fast_kernel<kFsWarps><<<nq, kFsWarps * 32, 0, s>>>(
                 pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, census);
         else

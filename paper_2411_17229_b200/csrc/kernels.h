@@ -133,12 +133,6 @@ struct SurvArgs {
     uint32_t vec4;                // dim, d0 and every checkpoint are multiples of 4 (16-byte staging)
 };
 cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cudaStream_t s);
-cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
-                                     uint32_t cand_cap, uint32_t* q_count, uint32_t* q_off, uint32_t* q_cursor,
-                                     uint64_t* bucket, uint32_t nq, uint32_t max_cands, cudaStream_t s);
-cudaError_t launch_merge_buckets(const uint64_t* bucket, const uint32_t* q_off, const uint32_t* q_count, uint32_t nq,
-                                 uint32_t K, uint64_t* out_keys, uint32_t* out_count, cudaStream_t s);
-// Merge each query's slot candidates (+ its entries of the overflow list) into its top-K.
 cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const uint32_t* q_count,
                                const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
                                uint32_t cand_cap, uint32_t nq, uint32_t K, uint64_t* out_keys, uint32_t* out_count,

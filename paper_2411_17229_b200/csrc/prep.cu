@@ -829,8 +829,7 @@ cudaError_t launch_group(const GroupArgs& g, cudaStream_t s) {
     DADE_CUDA_TRY(cudaMemsetAsync(g.counts, 0, sizeof(uint32_t) * ne, s));
     DADE_CUDA_TRY(cudaMemsetAsync(g.cursor, 0, sizeof(uint32_t) * ne, s));
     const unsigned gp = (unsigned)((pairs + 255) / 256);
-    static const bool global_only = std::getenv("DADE_GPU_GROUP_GLOBAL") != nullptr;  // tuning hook
-    const bool smem = ne <= kGroupSmemEntries && !global_only;
+    const bool smem = ne <= kGroupSmemEntries;
     const unsigned gs = (unsigned)((pairs + 256 * kGroupPerThread - 1) / (256 * kGroupPerThread));
     const size_t sh = sizeof(uint32_t) * ne;
     if (smem && sh > 48 * 1024) {

@@ -1215,65 +1215,6 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
     }
 }
 
-// Exclusive scan of per-query candidate counts (single CTA).
-__global__ void __launch_bounds__(1024) scan_counts_kernel(const uint32_t* cnt, uint32_t n, uint32_t* off) {
-    __shared__ uint32_t s_v[1024];
-    const uint32_t per = (n + 1023) / 1024;
-    const uint32_t lo = threadIdx.x * per, hi = min(n, lo + per);
-    uint32_t sum = 0;
-    for (uint32_t e = lo; e < hi; ++e) sum += cnt[e];
-    s_v[threadIdx.x] = sum;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        const uint32_t v = threadIdx.x >= (unsigned)o ? s_v[threadIdx.x - o] : 0;
-        __syncthreads();
-        s_v[threadIdx.x] += v;
-        __syncthreads();
-    }
-    uint32_t run = s_v[threadIdx.x] - sum;
-    for (uint32_t e = lo; e < hi; ++e) {
-        off[e] = run;
-        run += cnt[e];
-    }
-}
-
-__global__ void scatter_candidates_kernel(const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
-                                          uint32_t cand_cap, const uint32_t* q_off, uint32_t* q_cursor, uint64_t* bucket) {
-    const uint32_t n = min(*cand_count, cand_cap);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t q = cand_q[i];
-        bucket[q_off[q] + atomicAdd(q_cursor + q, 1u)] = cand_key[i];
-    }
-}
-
-// Merge each query's candidate bucket into its top-K (out_keys already holds
-// the slot-segment merge); unsorted 256-key batches, warp per query.
-__global__ void __launch_bounds__(128)
-merge_buckets_kernel(const uint64_t* __restrict__ bucket, const uint32_t* __restrict__ q_off,
-                     const uint32_t* __restrict__ q_count, uint32_t nq, uint32_t K, uint64_t* out_keys,
-                     uint32_t* out_count) {
-    __shared__ uint64_t bbuf[4][256];
-    __shared__ uint64_t abuf[4][kStageMaxK];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t q = blockIdx.x * 4 + warp;
-    if (q >= nq) return;
-    uint64_t* A = out_keys + (size_t)q * K;
-    uint32_t* cA = out_count + q;
-    const uint32_t cnt = q_count[q];
-    const uint64_t* src = bucket + q_off[q];
-    uint64_t* B = bbuf[warp];
-    for (uint32_t b0 = 0; b0 < cnt; b0 += 256) {
-        const uint32_t m = min(256u, cnt - b0);
-        for (uint32_t e = lane; e < m; e += 32) B[e] = src[b0 + e];
-        __syncwarp();
-        if (K <= (uint32_t)kStageMaxK) warp_merge_staged(A, cA, K, B, m, abuf[warp]);
-        else warp_merge(A, cA, K, B, m, false);
-        __syncwarp();
-    }
-    const uint32_t c = *reinterpret_cast<volatile uint32_t*>(cA);
-    for (uint32_t i = c + lane; i < K; i += 32) A[i] = kEmptyKey;
-}
-
 // Merge each query's slot candidates into its top-K (out_keys already holds the
 // earlier passes' results); a query whose slots overflowed also picks its entries
 // out of the shared overflow list. Unsorted 256-key batches, warp per query.
@@ -1453,7 +1394,7 @@ cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cu
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (a.vec4 && !std::getenv("DADE_GPU_SURV_V1")) {
+    if (a.vec4) {
         const size_t smem = sizeof(float) * kSpWarps * kSpWarpFloats;
         DADE_CUDA_TRY(cudaFuncSetAttribute(advance_survivors_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const uint32_t groups = (max_entries + 31) / 32;
@@ -1469,17 +1410,6 @@ cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cu
     return cudaGetLastError();
 }
 
-cudaError_t launch_bucket_candidates(const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
-                                     uint32_t cand_cap, uint32_t* q_count, uint32_t* q_off, uint32_t* q_cursor,
-                                     uint64_t* bucket, uint32_t nq, uint32_t max_cands, cudaStream_t s) {
-    scan_counts_kernel<<<1, 1024, 0, s>>>(q_count, nq, q_off);
-    DADE_CUDA_TRY(cudaMemsetAsync(q_cursor, 0, (size_t)nq * 4, s));
-    if (max_cands)
-        scatter_candidates_kernel<<<std::min<uint32_t>((max_cands + 255) / 256, 148 * 8), 256, 0, s>>>(cand_q, cand_key, cand_count, cand_cap,
-                                                                          q_off, q_cursor, bucket);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const uint32_t* q_count,
                                const uint32_t* cand_q, const uint64_t* cand_key, const uint32_t* cand_count,
                                uint32_t cand_cap, uint32_t nq, uint32_t K, uint64_t* out_keys, uint32_t* out_count,
@@ -1489,13 +1419,6 @@ cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const
     merge_slots_kernel<<<(nq + 3) / 4, 128, 0, s>>>(qslots, qslot_cap, q_count, cand_q, cand_key, cand_count, cand_cap,
                                                     nq, K, out_keys, out_count, r_global, res_ids, res_dists,
                                                     res_counts);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_merge_buckets(const uint64_t* bucket, const uint32_t* q_off, const uint32_t* q_count, uint32_t nq,
-                                 uint32_t K, uint64_t* out_keys, uint32_t* out_count, cudaStream_t s) {
-    if (nq == 0) return cudaSuccess;
-    merge_buckets_kernel<<<(nq + 3) / 4, 128, 0, s>>>(bucket, q_off, q_count, nq, K, out_keys, out_count);
     return cudaGetLastError();
 }
 

@@ -269,86 +269,6 @@ __device__ __forceinline__ void sd_finish_query(const SeedListArgs& a, uint32_t 
     }
 }
 
-__global__ void __launch_bounds__(kSdThreads, 2) seed_tma_kernel(const SeedListArgs a,
-                                                                  const __grid_constant__ CUtensorMap tmap) {
-    extern __shared__ unsigned char sd_raw[];
-    unsigned char* sm = sd_raw + ((256u - (sd_u32(sd_raw) & 255u)) & 255u);
-    const SdLayout L = sd_layout();
-    unsigned char* ring = sm + L.ring;
-    float* qres = reinterpret_cast<float*>(sm + L.qres);  // [dim][16]
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.bars);
-    uint64_t* empty = full + kSdStages;
-    const uint32_t b = blockIdx.x;
-    if (b >= a.seed_goff[a.n_lists]) return;
-    const uint32_t list = a.seed_glist[b];
-    const uint32_t cnt_all = a.counts[list];
-    const uint32_t g0 = (b - a.seed_goff[list]) * kSdG;
-    if (g0 >= cnt_all) return;
-    const uint32_t start = a.list_offsets[list], len = a.list_offsets[list + 1] - start;
-    const uint32_t n = min(len, a.S);
-    if (n < a.K) return;
-    const uint32_t* qs = a.bucket_q + a.bucket_off[list] + g0;
-    const uint32_t ng = min((uint32_t)kSdG, cnt_all - g0);
-    const uint32_t dim = a.dim;
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t n_slices = (dim + kSdSlice - 1) / kSdSlice;
-    const int rsel = n > 2u * kSdT ? 4 : n > (uint32_t)kSdT ? 2 : 1;
-    const uint32_t n_boxes = (uint32_t)rsel;  // 256-row boxes per slice (rows past n are never read)
-
-    if (tid == 0) {
-        for (int i = 0; i < kSdStages; ++i) {
-            sd_mb_init(full + i, 1);
-            sd_mb_init(empty + i, kSdT / 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    // resident queries, transposed [dim][16] (padding queries and dims: 0)
-    for (uint32_t i = tid; i < dim * kSdG; i += kSdThreads) {
-        const uint32_t k = i / kSdG, u = i % kSdG;
-        if (u < ng) sd_cp4(qres + i, a.queries + (size_t)qs[u] * dim + k);
-        else qres[i] = 0.f;
-    }
-    for (uint32_t i = dim * kSdG + tid; i < n_slices * kSdSlice * kSdG; i += kSdThreads) qres[i] = 0.f;
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();
-
-    float* accs = reinterpret_cast<float*>(ring);  // after the dimension loop: [16][1024] sums
-    if (warp == kSdT / 32) {
-        // ---- producer ----
-        if (lane == 0) {
-            const uint32_t bytes = n_boxes * kSdBox * kSdSlice * 4;
-            for (uint32_t sl = 0; sl < n_slices; ++sl) {
-                const uint32_t s = sl % kSdStages;
-                if (sl >= (uint32_t)kSdStages) sd_mb_wait(empty + s, ((sl / kSdStages) - 1) & 1);
-                sd_mb_arrive_tx(full + s, bytes);
-                unsigned char* slot = ring + (size_t)s * kSdRows * kSdSlice * 4;
-                for (uint32_t bx = 0; bx < n_boxes; ++bx)
-                    sd_tma2d(slot + (size_t)bx * kSdBox * kSdSlice * 4, &tmap, (int)(sl * kSdSlice),
-                             (int)(start + bx * kSdBox), full + s);
-            }
-        }
-        __syncwarp();
-    } else {
-        switch ((ng + 1) >> 1) {
-#define SD_G(P)                                                                                 \
-    case P:                                                                                     \
-        if (rsel == 4) sd_sums<2 * P, 4, kSdStages, false>(ring, qres, full, empty, 0, n_slices, accs, a.nz2);       \
-        else if (rsel == 2) sd_sums<2 * P, 2, kSdStages, false>(ring, qres, full, empty, 0, n_slices, accs, a.nz2);  \
-        else sd_sums<2 * P, 1, kSdStages, false>(ring, qres, full, empty, 0, n_slices, accs, a.nz2);                 \
-        break;
-            SD_G(1) SD_G(2) SD_G(3) SD_G(4) SD_G(5) SD_G(6) SD_G(7) default: SD_G(8)
-#undef SD_G
-        }
-        // ---- selection: one warp per query ----
-        uint64_t* keys = reinterpret_cast<uint64_t*>(accs + kSdG * kSdRows);           // [8 warps][128]
-        uint32_t* hists = reinterpret_cast<uint32_t*>(keys + (kSdT / 32) * kSdSmall);  // [8 warps][256]
-        for (uint32_t u = warp; u < ng; u += kSdT / 32) {
-            const uint32_t q = qs[u];
-            sd_finish_query(a, q, accs, u, n, start, keys + warp * kSdSmall, hists + warp * 256);
-            __syncwarp();
-        }
-    }
-}
 
 
 // ---- persistent, warp-specialised seed ------------------------------------------
@@ -580,31 +500,18 @@ bool seed_tma_ok(uint32_t dim, uint32_t K) { return dim <= (uint32_t)kSdMaxDim &
 cudaError_t launch_seed_tma(const SeedListArgs& a, const CUtensorMap& tmap, uint32_t max_groups, cudaStream_t s,
                             uint32_t* work) {
     if (a.n_lists == 0 || max_groups == 0) return cudaSuccess;
-    const size_t smem = sd_layout().total;
+    if (!work) return cudaErrorInvalidValue;  // the persistent kernel's group counter
     static_assert((size_t)kSdStages * kSdRows * kSdSlice * 4 >=
                       (size_t)kSdG * kSdRows * 4 + (kSdT / 32) * (kSdSmall * 8 + 256 * 4),
                   "sums + keys + histograms must fit in the ring");
-    DADE_CUDA_TRY(cudaFuncSetAttribute(seed_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    static const bool np = std::getenv("DADE_GPU_SEED_NP") != nullptr;  // one CTA per group (previous kernel)
-    if (!np && work) {
-        const size_t sp = sp_layout().total;
-        int dev = 0, n_sm = 0;
-        DADE_CUDA_TRY(cudaGetDevice(&dev));
-        DADE_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-        DADE_CUDA_TRY(cudaFuncSetAttribute(seed_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp));
-        DADE_CUDA_TRY(cudaMemsetAsync(work, 0, 4, s));
-        if (a.order) seed_order_kernel<<<1, 1024, 0, s>>>(a, a.order);
-        seed_persist_kernel<<<std::min<uint32_t>(max_groups, (uint32_t)n_sm), kSpThreads, sp, s>>>(a, tmap, work);
-        const cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess && std::getenv("DADE_GPU_VERBOSE")) {
-            cudaFuncAttributes fa{};
-            cudaFuncGetAttributes(&fa, seed_persist_kernel);
-            std::fprintf(stderr, "[dade_gpu] seed_persist: regs %d max threads %d static smem %zu max dyn %d (asked %zu)\n",
-                         fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, sp);
-        }
-        return e;
-    }
-    seed_tma_kernel<<<max_groups, kSdThreads, smem, s>>>(a, tmap);
+    const size_t sp = sp_layout().total;
+    int dev = 0, n_sm = 0;
+    DADE_CUDA_TRY(cudaGetDevice(&dev));
+    DADE_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+    DADE_CUDA_TRY(cudaFuncSetAttribute(seed_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp));
+    DADE_CUDA_TRY(cudaMemsetAsync(work, 0, 4, s));
+    if (a.order) seed_order_kernel<<<1, 1024, 0, s>>>(a, a.order);
+    seed_persist_kernel<<<std::min<uint32_t>(max_groups, (uint32_t)n_sm), kSpThreads, sp, s>>>(a, tmap, work);
     return cudaGetLastError();
 }
 
