@@ -56,8 +56,14 @@ enum { DADE_GPU_FD = 0, DADE_GPU_ADS = 1, DADE_GPU_DADE = 2 };
 /* search flags */
 enum {
     DADE_GPU_QUERIES_RAW = 1u << 0, /* queries are in the raw basis: rotate on device first   */
-    DADE_GPU_DEVICE_PTRS = 1u << 1  /* every array argument is a device pointer; the call is
+    DADE_GPU_DEVICE_PTRS = 1u << 1, /* every array argument is a device pointer; the call is
                                        asynchronous on the handle's stream (no H2D/D2H)      */
+    DADE_GPU_MEASURE_FAILURES = 1u << 2 /* DcoStats::measure_failures: the search also fills
+                                       stats->eligible / failures (estimator.cpp:24-33); every
+                                       pruned pair is carried to the full dim for its exact
+                                       distance, so this is the reference's untimed second
+                                       pass (bench.cpp:65-73), not a serving mode. ivf_search
+                                       and flat_search only.                                   */
 };
 
 typedef struct dade_gpu_ctx dade_gpu_ctx;
@@ -213,9 +219,22 @@ int dade_gpu_calibrate(dade_gpu_ctx* ctx, const float* data, uint32_t n, double 
                        uint32_t delta_d, uint64_t n_pairs, uint64_t seed, uint32_t flags,
                        uint32_t* checkpoints, double* epsilons, uint32_t* n_out);
 
-/* Debug: the last scan's device counters [0..7] (total_dco, dims, bytes, ...)
- * and, with DADE_GPU_PHASES=1 in the environment, per-phase clock sums [8..15]. */
+/* Debug: the last scan's device counters [0..15] (total_dco, dims, bytes, debug,
+ * per-pass census [4..7], eligible, failures). */
 int dade_gpu_debug_counters(dade_gpu_ctx* ctx, uint64_t* out16);
+
+/* Per-(query, candidate, checkpoint) estimator values of the hot path, for
+ * parity with partial_sqdist + dade_estimate (proj/src/estimator.cpp:74-91):
+ * with capacity > 0, every checkpoint partial the survivor kernel of the
+ * following searches evaluates is recorded (the dump is reset at each search's
+ * start; pairs the tensor-core bound prunes are not evaluated exactly and so
+ * are not recorded unless DADE_GPU_DEBUG=1 sends every pair to that kernel).
+ * _get returns min(recorded, capacity, cap) entries: query index, candidate id,
+ * checkpoint dim d, the fp32 partial sum over dims [0, d) and the estimate
+ * est_scale(d) x partial; *n_total = entries recorded (may exceed capacity). */
+int dade_gpu_set_estimate_dump(dade_gpu_ctx* ctx, uint32_t capacity);
+int dade_gpu_get_estimate_dump(dade_gpu_ctx* ctx, uint32_t cap, uint32_t* q, uint32_t* ids, uint32_t* dims,
+                               float* partial, double* estimate, uint64_t* n_total);
 
 /* Debug: per-query radius (float bits) left by the last IVF search. */
 int dade_gpu_debug_radius(dade_gpu_ctx* ctx, uint32_t* out, uint32_t nq);

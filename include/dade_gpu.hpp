@@ -21,6 +21,7 @@
 // proj/docs/FILE_FORMATS.md). Header-only; link libdade_gpu.so.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -161,6 +162,18 @@ struct OrthoTransform {
         for (std::uint32_t k = 0; k + 1 < t.dim; ++k)
             if (t.eigenvalues[k] < t.eigenvalues[k + 1])
                 throw std::runtime_error("transform eigenvalues not nonincreasing");
+        // the loader's corruption check (proj/src/transform.cpp:344-356): columns orthonormal
+        double worst = 0.0;
+        for (std::uint32_t a = 0; a < t.dim; ++a)
+            for (std::uint32_t b = a; b < t.dim; ++b) {
+                double dot = 0.0;
+                const double* ca = t.matrix.data() + std::size_t(a) * t.dim;
+                const double* cb = t.matrix.data() + std::size_t(b) * t.dim;
+                for (std::uint32_t r = 0; r < t.dim; ++r) dot += ca[r] * cb[r];
+                worst = std::max(worst, std::abs(dot - (a == b ? 1.0 : 0.0)));
+            }
+        if (worst > 1e-5)
+            throw std::runtime_error("transform matrix not orthogonal (max deviation " + std::to_string(worst) + ")");
         return t;
     }
     void upload(const Device& d) const {
@@ -346,8 +359,9 @@ public:
         std::vector<std::uint32_t> ids(std::size_t(nq) * kk), cnt(nq);
         std::vector<float> d(std::size_t(nq) * kk);
         dade_gpu_stats st{};
-        check(dade_gpu_ivf_search(dev_->get(), queries, nq, k, n_probe, raw ? DADE_GPU_QUERIES_RAW : 0, ids.data(),
-                                  d.data(), cnt.data(), &st));
+        const std::uint32_t flags = (raw ? DADE_GPU_QUERIES_RAW : 0u) |
+                                    (stats && stats->measure_failures ? DADE_GPU_MEASURE_FAILURES : 0u);
+        check(dade_gpu_ivf_search(dev_->get(), queries, nq, k, n_probe, flags, ids.data(), d.data(), cnt.data(), &st));
         if (stats) stats->add(st);
         return detail::to_results(ids, d, cnt, nq, kk);
     }
@@ -406,7 +420,8 @@ public:
         std::vector<std::uint32_t> ids(std::size_t(nq) * kk), cnt(nq);
         std::vector<float> d(std::size_t(nq) * kk);
         dade_gpu_stats st{};
-        check(dade_gpu_flat_search(dev_->get(), queries, nq, k, 0, ids.data(), d.data(), cnt.data(), &st));
+        const std::uint32_t flags = stats && stats->measure_failures ? DADE_GPU_MEASURE_FAILURES : 0u;
+        check(dade_gpu_flat_search(dev_->get(), queries, nq, k, flags, ids.data(), d.data(), cnt.data(), &st));
         if (stats) stats->add(st);
         return detail::to_results(ids, d, cnt, nq, kk);
     }

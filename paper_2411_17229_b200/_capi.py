@@ -35,6 +35,7 @@ _ERRORS = {1: DadeError, 2: ConfigError, 3: InvalidInput, 4: CudaError}
 # flags
 QUERIES_RAW = 1
 DEVICE_PTRS = 2
+MEASURE_FAILURES = 4
 # strategy kinds
 FD, ADS, DADE = 0, 1, 2
 
@@ -86,6 +87,8 @@ def _load():
         "dade_gpu_last_scan_profile": ([P, P, P, P], I),
         "dade_gpu_last_filter_profile": ([P, P, P], I),
         "dade_gpu_last_seed_profile": ([P, P, P], I),
+        "dade_gpu_set_estimate_dump": ([P, U32], I),
+        "dade_gpu_get_estimate_dump": ([P, U32, P, P, P, P, P, P], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -108,6 +111,7 @@ EXPORTED = [
     "dade_gpu_partial_sums", "dade_gpu_calibrate", "dade_gpu_launch_count",
     "dade_gpu_set_profiling", "dade_gpu_last_scan_profile", "dade_gpu_debug_counters",
     "dade_gpu_last_filter_profile", "dade_gpu_last_seed_profile", "dade_gpu_debug_radius",
+    "dade_gpu_set_estimate_dump", "dade_gpu_get_estimate_dump",
 ]
 
 

@@ -93,6 +93,24 @@ class Device:
         check(_capi.lib.dade_gpu_last_scan_profile(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
+    def set_estimate_dump(self, capacity: int):
+        """Record every checkpoint partial the hot path evaluates (0 disables)."""
+        check(_capi.lib.dade_gpu_set_estimate_dump(self.h, int(capacity)))
+
+    def estimate_dump(self, cap: int):
+        """(query, id, d, partial f32, estimate f64) arrays of the last search's
+        evaluated checkpoints, and the number recorded."""
+        q = np.zeros(cap, np.uint32)
+        ids = np.zeros(cap, np.uint32)
+        dims = np.zeros(cap, np.uint32)
+        part = np.zeros(cap, np.float32)
+        est = np.zeros(cap, np.float64)
+        n = C.c_uint64()
+        check(_capi.lib.dade_gpu_get_estimate_dump(self.h, cap, ptr(q), ptr(ids), ptr(dims), ptr(part), ptr(est),
+                                                   C.byref(n)))
+        m = min(int(n.value), cap)
+        return (q[:m], ids[:m], dims[:m], part[:m], est[:m]), int(n.value)
+
     # -- strategy plumbing ---------------------------------------------------
     def apply(self, dco) -> None:
         if self._strategy_token is dco:
@@ -380,8 +398,8 @@ class IvfIndex:
         dists = np.zeros((nq, kk), np.float32)
         counts = np.zeros(nq, np.uint32)
         st = _capi.Stats()
-        check(_capi.lib.dade_gpu_ivf_search(self.dev.h, ptr(q), nq, k, n_probe,
-                                            _capi.QUERIES_RAW if raw else 0, ptr(ids), ptr(dists),
+        flags = (_capi.QUERIES_RAW if raw else 0) | (_capi.MEASURE_FAILURES if stats and stats.measure_failures else 0)
+        check(_capi.lib.dade_gpu_ivf_search(self.dev.h, ptr(q), nq, k, n_probe, flags, ptr(ids), ptr(dists),
                                             ptr(counts), C.byref(st)))
         if stats is not None:
             stats._add(st)
@@ -408,6 +426,19 @@ class IvfIndex:
         if outputs is None:
             outputs = [(np.zeros((nq, kk), np.uint32), np.zeros((nq, kk), np.float32), np.zeros(nq, np.uint32))
                        for _ in qs]
+        if len(outputs) != len(qs):
+            raise InvalidInput("IvfIndex::search: one (ids, dists, counts) output per batch")
+        want = (((nq, kk), np.uint32), ((nq, kk), np.float32), ((nq,), np.uint32))
+        for out in outputs:  # the C ABI writes nq*k*4 bytes through each pointer
+            if len(out) != 3:
+                raise InvalidInput("IvfIndex::search: outputs are (ids, dists, counts) triples")
+            for a, (shape, dt) in zip(out, want):
+                ok = (isinstance(a, np.ndarray) and a.flags.c_contiguous and a.shape == shape and a.dtype == dt) or \
+                     (hasattr(a, "data_ptr") and a.is_contiguous() and tuple(a.shape) == shape and
+                      a.element_size() == 4 and a.device.type == "cpu")
+                if not ok:
+                    raise InvalidInput(f"IvfIndex::search: output must be a C-contiguous host array of shape "
+                                       f"{shape} and dtype {np.dtype(dt).name}")
         nb = len(qs)
         PA = C.c_void_p * nb
         st = _capi.Stats()
@@ -453,8 +484,9 @@ class FlatIndex:
         dists = np.zeros((nq, kk), np.float32)
         counts = np.zeros(nq, np.uint32)
         st = _capi.Stats()
-        check(_capi.lib.dade_gpu_flat_search(self.dev.h, ptr(q), nq, k, _capi.QUERIES_RAW if raw else 0,
-                                             ptr(ids), ptr(dists), ptr(counts), C.byref(st)))
+        flags = (_capi.QUERIES_RAW if raw else 0) | (_capi.MEASURE_FAILURES if stats and stats.measure_failures else 0)
+        check(_capi.lib.dade_gpu_flat_search(self.dev.h, ptr(q), nq, k, flags, ptr(ids), ptr(dists), ptr(counts),
+                                             C.byref(st)))
         if stats is not None:
             stats._add(st)
         return ids, dists, counts

@@ -31,6 +31,10 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// Device counters of a search: [0] total_dco, [1] dims_accumulated, [2] bytes,
+// [3] debug, [4..7] per-pass census, [8] eligible, [9] failures.
+constexpr size_t kCounterBytes = 128;
+
 bool env_flag(const char* name) {
     const char* e = std::getenv(name);
     return e && e[0] == '1';
@@ -414,6 +418,12 @@ struct dade_gpu_ctx {
     DevBuf flat_offsets;  // {0, b_count}: the flat base as one list
     CUtensorMap tm_none{};
 
+    // failure accounting of the search in flight (DADE_GPU_MEASURE_FAILURES)
+    bool measure = false;
+    // per-(query, candidate, checkpoint) partials of the next searches (dade_gpu_set_estimate_dump)
+    DevBuf dump_entries, dump_count;
+    uint32_t dump_cap = 0;
+
     // profiling
     bool profiling = false;
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
@@ -683,6 +693,25 @@ void finish_profile(dade_gpu_ctx* c) {
     }
 }
 
+// DcoStats of the rows the radius seed scored exactly (the streaming passes skip
+// them, GroupArgs::seed_skip): each is a full-dim DCO with r = +inf, i.e. the
+// reference's accept path; with failure accounting each is also eligible.
+__global__ void seed_stats_kernel(const uint32_t* counts, const uint32_t* list_offsets, uint32_t n_lists,
+                                  uint32_t seed_skip, uint32_t seed_min, uint32_t dim, bool measure,
+                                  unsigned long long* counters) {
+    unsigned long long pairs = 0;
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n_lists; l += gridDim.x * blockDim.x) {
+        const uint32_t len = list_offsets[l + 1] - list_offsets[l];
+        if (len >= seed_min) pairs += (unsigned long long)counts[l] * min(len, seed_skip);
+    }
+    for (int off = 16; off > 0; off >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, off);
+    if ((threadIdx.x & 31) == 0 && pairs) {
+        atomicAdd(counters + 0, pairs);
+        atomicAdd(counters + 1, pairs * dim);
+        if (measure) atomicAdd(counters + 8, pairs);
+    }
+}
+
 __global__ void min_u32_kernel(uint32_t* r, const uint32_t* other, uint32_t n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) r[i] = min(r[i], other[i]);
@@ -795,7 +824,15 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                                               k, seed_rows(c, k, a.dim, flat), a.r_global, out_keys, out_count, s),
                            "seed radius");
             ++c->launches;
+            if (a.counters && g) {
+                seed_stats_kernel<<<1, 256, 0, s>>>(g->counts, seed.offsets, g->n_lists, g->seed_skip, g->seed_min,
+                                                    a.dim, c->measure, a.counters);
+                cuda_check(cudaGetLastError(), "seed stats");
+                ++c->launches;
+            }
         }
+        if (!resume && c->dump_cap)
+            cuda_check(cudaMemsetAsync(c->dump_count.p, 0, 4, s), "memset");
         tl_mark(c, "seeded", s);
         // passes: nearest lists' first row piece, their remaining pieces, all other
         // lists (IVF); or one flat pass. The radius is tightened after each.
@@ -844,7 +881,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             uint32_t grid = a.items ? max_items : a.flat_qchunks * ((a.flat_rows + a.flat_block - 1) / a.flat_block);
             f.piece_lo = 0;
             f.piece_hi = 0xffffffffu;
-            f.debug = ct.debug;
+            f.debug = c->measure ? 1 : ct.debug;  // failure accounting: every pair to the survivors
             if (flat) {
                 f.n_items = g->n_items + 1;
                 f.piece_lo = flat_lo[pass];
@@ -914,6 +951,8 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             }
             sv.counters = a.counters;
             sv.surv_max = c->surv_max.as<uint32_t>();
+            sv.measure = c->measure ? 1u : 0u;
+            if (c->dump_cap) sv.dump = {c->dump_entries.as<uint4>(), c->dump_count.as<uint32_t>(), c->dump_cap};
             cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
             // survivors / candidates of passes 0, 1 (low words of counters[4 + 2 pass ..]); of pass 2 in
             // counters[3] (low / high word) unless a debug mode owns that word
@@ -979,10 +1018,14 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     bool tma = false;
     const CUtensorMap& tm = c->tm_storage.get(c->storage.as<float>(), std::max<uint32_t>(c->count, 1), c->dim, tma);
     ct.use_tma = (tma && ct.vec_ok && c->count > 0) ? 1 : 0;
-    const bool use_filter = filter_ok(c, ct, c->dim);
+    bool use_filter = filter_ok(c, ct, c->dim);
+    bool umma = use_filter && umma_ok(c, ct, tma);
+    if (c->measure && !umma) {  // failure accounting: the tcgen05 streaming path or the all-SIMT scan
+        use_filter = false;
+        ct.use_tc = 0;
+    }
     // the streaming filter splits long lists into row pieces (more, shorter items)
     g.max_item_rows = use_filter ? kFilterItemRows : 0;
-    const bool umma = use_filter && umma_ok(c, ct, tma);
     if (umma && nrb == 3) {
         // the tcgen05 path scans ranks 1-3 and the rest in the same (last) pass: one bucket,
         // fewer and fuller items (the other paths keep the nearer ranks' items first)
@@ -1056,6 +1099,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
     a.coeff = c->d_coeff.as<double>();
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
+    a.measure = c->measure ? 1u : 0u;
     if (const char* dbg = std::getenv("DADE_GPU_DEBUG"))
         if (std::atoi(dbg) == 3) a.census = c->counters.as<unsigned long long>() + 3;
     // Radius seeding: an exact (FD) pass over the first rows of every query's
@@ -1168,6 +1212,7 @@ bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uin
     a.coeff = c->d_coeff.as<double>();
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
+    a.measure = c->measure ? 1u : 0u;
     record(c, c->e1);
     SeedArgs sd{true, c->probes.as<uint64_t>(), 1, c->flat_offsets.as<uint32_t>()};
     stream_passes(c, a, ct, d_q, nq, k, false, (uint32_t)max_items, &g, c->base.as<float>(), c->b_count, c->tm_base,
@@ -1216,7 +1261,9 @@ void flat_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t
     a.coeff = c->d_coeff.as<double>();
     a.neg_zero2 = 0x8000000080000000ull;
     a.counters = c->counters.as<unsigned long long>();
+    a.measure = c->measure ? 1u : 0u;
     ChunkTable ct = make_chunks(c->b_dim, c->cps);
+    if (c->measure) ct.use_tc = 0;  // failure accounting on the all-SIMT scan
     bool tma = false;
     const CUtensorMap& tm = c->tm_base.get(a.storage, std::max<uint32_t>(c->b_count, 1), c->b_dim, tma);
     ct.use_tma = (tma && ct.vec_ok && c->b_count > 0) ? 1 : 0;
@@ -1320,11 +1367,31 @@ const float* stage_queries(dade_gpu_ctx* c, const float* queries, uint32_t nq, u
 
 void collect_stats(dade_gpu_ctx* c, dade_gpu_stats* stats) {
     if (!stats) return;
-    unsigned long long h[3] = {0, 0, 0};
+    unsigned long long h[10] = {};
     cuda_check(cudaMemcpyAsync(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream), "D2H stats");
     cuda_check(cudaStreamSynchronize(c->stream), "sync");
     stats->total_dco += h[0];
     stats->dims_accumulated += h[1];
+    if (c->measure) {  // DcoStats::measure_failures (proj/include/dade/estimator.hpp:31-34)
+        stats->eligible += h[8];
+        stats->failures += h[9];
+    }
+}
+
+// Failure accounting hands every DCO pair to the survivor kernel (16 B each),
+// so a search with DADE_GPU_MEASURE_FAILURES runs in query chunks of at most
+// ~2^27 pairs. The flag is cleared however the search exits.
+struct MeasureScope {
+    dade_gpu_ctx* c;
+    MeasureScope(dade_gpu_ctx* cc, bool on) : c(cc) { c->measure = on; }
+    ~MeasureScope() { c->measure = false; }
+    MeasureScope(const MeasureScope&) = delete;
+    MeasureScope& operator=(const MeasureScope&) = delete;
+};
+uint32_t measure_chunk(uint64_t pairs_per_query, uint32_t nq) {
+    const uint64_t budget = 1ull << 27;
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(std::max<uint32_t>(nq, 1),
+                                                              budget / std::max<uint64_t>(1, pairs_per_query)));
 }
 
 void wait_stream(cudaStream_t s) { cuda_check(cudaStreamSynchronize(s), "search"); }
@@ -1358,8 +1425,8 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
                    dade_gpu_stats* stats, const std::function<void(const float*, uint64_t*, uint32_t*)>& run) {
     c->use_device();
     cudaStream_t s = c->stream;
-    c->counters.ensure(64);
-    cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
+    c->counters.ensure(kCounterBytes);
+    cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, s), "memset");
     record(c, c->e0);
     c->tl_on = env_flag("DADE_GPU_TIMELINE");
     c->tl_used = 0;
@@ -1459,7 +1526,7 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
         c->h_batch_n = nb;
     }
     std::memset(c->h_batch, 0, (size_t)nb * 32);
-    c->counters.ensure(64);
+    c->counters.ensure(kCounterBytes);
     c->batch_slot.ensure(2 * 32);
     c->out_keys.ensure((size_t)nq * k * 8);
     c->out_count.ensure((size_t)nq * 4);
@@ -1483,7 +1550,7 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
     std::vector<uint8_t> coarse_used(nb, 0);
     for (uint32_t b = 0; b < nb; ++b) {
         const uint32_t j = b & 1;
-        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, s), "memset");
         c->n_filter_passes = 0;
         c->surv_cap_used = 0;
         // batch b > 0: its H2D ran under batch b-1's search, so per-chunk staging
@@ -1885,12 +1952,26 @@ int dade_gpu_ivf_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint
     return guarded([&] {
         check_ivf_args(c, k, n_probe);
         if (nq && (!queries || !out_ids || !out_dists)) fail(DADE_GPU_INVALID_INPUT, "ivf_search: null argument");
+        const bool measure = flags & DADE_GPU_MEASURE_FAILURES;
+        MeasureScope ms(c, measure);
+        uint32_t chunk = nq;
+        if (measure) {  // every probed pair goes to the survivor worklist: bound it per chunk
+            uint32_t max_len = 0;
+            for (uint32_t l = 0; l < c->n_clusters; ++l)
+                max_len = std::max(max_len, c->dev_offsets[l + 1] - c->dev_offsets[l]);
+            chunk = measure_chunk((uint64_t)n_probe * max_len, nq);
+        }
         c->stage_n_probe = n_probe;
         try {
-            search_common(c, queries, nq, c->dim, k, flags, out_ids, out_dists, out_counts, stats,
-                          [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
-                              ivf_search_device(c, d_q, nq, k, n_probe, ok, oc);
-                          });
+            for (uint32_t q0 = 0; q0 < nq || q0 == 0; q0 += chunk) {
+                const uint32_t m = std::min(chunk, nq - q0);
+                search_common(c, queries + (size_t)q0 * c->dim, m, c->dim, k, flags, out_ids + (size_t)q0 * k,
+                              out_dists + (size_t)q0 * k, out_counts ? out_counts + q0 : nullptr, stats,
+                              [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
+                                  ivf_search_device(c, d_q, m, k, n_probe, ok, oc);
+                              });
+                if (nq == 0) break;
+            }
         } catch (...) {
             c->stage_n_probe = 0;
             throw;
@@ -1905,6 +1986,8 @@ int dade_gpu_ivf_search_batches(dade_gpu_ctx* c, uint32_t n_batches, const float
     return guarded([&] {
         check_ivf_args(c, k, n_probe);
         if (flags & DADE_GPU_DEVICE_PTRS) fail(DADE_GPU_INVALID_INPUT, "ivf_search_batches: host buffers only");
+        if (flags & DADE_GPU_MEASURE_FAILURES)
+            fail(DADE_GPU_INVALID_INPUT, "ivf_search_batches: failure accounting is a separate dade_gpu_ivf_search pass");
         if (n_batches && nq && (!queries || !out_ids || !out_dists))
             fail(DADE_GPU_INVALID_INPUT, "ivf_search_batches: null argument");
         for (uint32_t b = 0; b < n_batches && nq; ++b)
@@ -1928,10 +2011,18 @@ int dade_gpu_flat_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uin
     return guarded([&] {
         check_flat_args(c, k);
         if (nq && (!queries || !out_ids || !out_dists)) fail(DADE_GPU_INVALID_INPUT, "flat_search: null argument");
-        search_common(c, queries, nq, c->b_dim, k, flags, out_ids, out_dists, out_counts, stats,
-                      [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
-                          flat_search_device(c, d_q, nq, k, ok, oc);
-                      });
+        const bool measure = flags & DADE_GPU_MEASURE_FAILURES;
+        MeasureScope ms(c, measure);
+        const uint32_t chunk = measure ? measure_chunk(c->b_count, nq) : nq;
+        for (uint32_t q0 = 0; q0 < nq || q0 == 0; q0 += chunk) {
+            const uint32_t m = std::min(chunk, nq - q0);
+            search_common(c, queries + (size_t)q0 * c->b_dim, m, c->b_dim, k, flags, out_ids + (size_t)q0 * k,
+                          out_dists + (size_t)q0 * k, out_counts ? out_counts + q0 : nullptr, stats,
+                          [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
+                              flat_search_device(c, d_q, m, k, ok, oc);
+                          });
+            if (nq == 0) break;
+        }
     });
 }
 
@@ -1940,8 +2031,8 @@ int dade_gpu_ivf_search_keys(dade_gpu_ctx* c, const float* d_queries, uint32_t n
     return guarded([&] {
         check_ivf_args(c, k, n_probe);
         c->use_device();
-        c->counters.ensure(64);
-        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+        c->counters.ensure(kCounterBytes);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, c->stream), "memset");
         if (nq == 0) return;
         const float* d_q = stage_queries(c, d_queries, nq, c->dim, flags | DADE_GPU_DEVICE_PTRS);
         c->out_count.ensure((size_t)nq * 4);
@@ -1956,11 +2047,11 @@ int dade_gpu_ivf_search_keys(dade_gpu_ctx* c, const float* d_queries, uint32_t n
             cuda_check(cudaStreamSynchronize(c->stream), "search");
             if (!search_overflowed(c)) break;
             if (attempt >= 2) fail(DADE_GPU_RUNTIME_ERROR, "survivor worklist overflow");
-            cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+            cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, c->stream), "memset");
         }
         if (c->coarse_tc_used && c->h_flags[1]) {  // pathological coarse ties: all-exact ranking
             c->coarse_force_exact = true;
-            cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+            cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, c->stream), "memset");
             ivf_search_device(c, d_q, nq, k, n_probe, d_out_keys, c->out_count.as<uint32_t>());
             c->coarse_force_exact = false;
         }
@@ -2009,8 +2100,8 @@ int dade_gpu_ivf_search_keys_begin(dade_gpu_ctx* c, const float* d_queries, uint
         if (d_probes && (flags & DADE_GPU_QUERIES_RAW))
             fail(DADE_GPU_INVALID_INPUT, "search_keys_begin: given probes need rotated queries");
         c->use_device();
-        c->counters.ensure(64);
-        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+        c->counters.ensure(kCounterBytes);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, c->stream), "memset");
         c->sp.active = false;
         if (nq == 0) return;
         const float* d_q = stage_queries(c, d_queries, nq, c->dim, flags | DADE_GPU_DEVICE_PTRS);
@@ -2050,8 +2141,8 @@ int dade_gpu_flat_search_keys_begin(dade_gpu_ctx* c, const float* d_queries, uin
         check_flat_args(c, k);
         if (nq && (!d_queries || !d_out_keys || !d_radius)) fail(DADE_GPU_INVALID_INPUT, "search_keys_begin: null argument");
         c->use_device();
-        c->counters.ensure(64);
-        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+        c->counters.ensure(kCounterBytes);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, c->stream), "memset");
         c->sp.active = false;
         if (nq == 0) return;
         const float* d_q = stage_queries(c, d_queries, nq, c->b_dim, flags | DADE_GPU_DEVICE_PTRS);
@@ -2113,7 +2204,7 @@ int dade_gpu_ivf_search_keys_end(dade_gpu_ctx* c, const uint32_t* d_radius, dade
         for (int attempt = 0; search_overflowed(c) || (c->coarse_tc_used && c->h_flags[1]); ++attempt) {
             if (attempt >= 3) fail(DADE_GPU_RUNTIME_ERROR, "survivor worklist overflow");
             c->coarse_force_exact = c->coarse_tc_used && c->h_flags[1];
-            cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+            cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, c->stream), "memset");
             c->surv_cap_used = 0;
             try {
                 run();
@@ -2134,8 +2225,8 @@ int dade_gpu_flat_search_keys(dade_gpu_ctx* c, const float* d_queries, uint32_t 
     return guarded([&] {
         check_flat_args(c, k);
         c->use_device();
-        c->counters.ensure(64);
-        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, c->stream), "memset");
+        c->counters.ensure(kCounterBytes);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, c->stream), "memset");
         if (nq == 0) return;
         const float* d_q = stage_queries(c, d_queries, nq, c->b_dim, flags | DADE_GPU_DEVICE_PTRS);
         c->out_count.ensure((size_t)nq * 4);
@@ -2171,8 +2262,8 @@ int dade_gpu_dco_evaluate(dade_gpu_ctx* c, const float* o, const float* q, const
         c->use_device();
         const uint32_t dim = c->s_dim;
         cudaStream_t s = c->stream;
-        c->counters.ensure(64);
-        cuda_check(cudaMemsetAsync(c->counters.p, 0, 64, s), "memset");
+        c->counters.ensure(kCounterBytes);
+        cuda_check(cudaMemsetAsync(c->counters.p, 0, kCounterBytes, s), "memset");
         if (n == 0) return;
         const bool dev = flags & DADE_GPU_DEVICE_PTRS;
         const size_t vb = (size_t)n * dim * 4;
@@ -2353,8 +2444,7 @@ int dade_gpu_debug_counters(dade_gpu_ctx* c, uint64_t* out16) {
         c->use_device();
         cuda_check(cudaStreamSynchronize(c->stream), "sync");
         std::memset(out16, 0, 16 * sizeof(uint64_t));
-        if (c->counters.p) cuda_check(cudaMemcpy(out16, c->counters.p, 64, cudaMemcpyDeviceToHost), "D2H");
-        if (c->phase.p) cuda_check(cudaMemcpy(out16 + 8, c->phase.p, 64, cudaMemcpyDeviceToHost), "D2H");
+        if (c->counters.p) cuda_check(cudaMemcpy(out16, c->counters.p, kCounterBytes, cudaMemcpyDeviceToHost), "D2H");
     });
 }
 
@@ -2362,6 +2452,47 @@ int dade_gpu_set_seed_rows(dade_gpu_ctx* c, uint32_t rows) {
     return guarded([&] {
         if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
         c->seed_rows_set = rows;
+    });
+}
+
+int dade_gpu_set_estimate_dump(dade_gpu_ctx* c, uint32_t capacity) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        c->use_device();
+        c->dump_cap = capacity;
+        if (!capacity) return;
+        c->dump_entries.ensure((size_t)capacity * sizeof(uint4));
+        c->dump_count.ensure(4);
+        cuda_check(cudaMemsetAsync(c->dump_count.p, 0, 4, c->stream), "memset");
+        cuda_check(cudaStreamSynchronize(c->stream), "dump");
+    });
+}
+
+int dade_gpu_get_estimate_dump(dade_gpu_ctx* c, uint32_t cap, uint32_t* q, uint32_t* ids, uint32_t* dims,
+                               float* partial, double* estimate, uint64_t* n_total) {
+    return guarded([&] {
+        if (!c || !n_total) fail(DADE_GPU_INVALID_INPUT, "get_estimate_dump: null argument");
+        if (!c->dump_cap) fail(DADE_GPU_CONFIG_ERROR, "get_estimate_dump: dump not enabled");
+        c->use_device();
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        uint32_t cnt = 0;
+        cuda_check(cudaMemcpy(&cnt, c->dump_count.p, 4, cudaMemcpyDeviceToHost), "D2H");
+        *n_total = cnt;
+        const uint32_t n = std::min({cnt, c->dump_cap, cap});
+        if (!n) return;
+        if (!q || !ids || !dims || !partial || !estimate) fail(DADE_GPU_INVALID_INPUT, "get_estimate_dump: null output");
+        std::vector<uint4> h(n);
+        cuda_check(cudaMemcpy(h.data(), c->dump_entries.p, (size_t)n * sizeof(uint4), cudaMemcpyDeviceToHost), "D2H");
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t ci = h[i].z;
+            if (ci >= c->cps.size()) fail(DADE_GPU_RUNTIME_ERROR, "get_estimate_dump: bad checkpoint index");
+            q[i] = h[i].x;
+            ids[i] = h[i].y;
+            dims[i] = c->cps[ci];
+            std::memcpy(&partial[i], &h[i].w, 4);
+            // dade_estimate / adsampling_estimate (proj/src/estimator.cpp:84-97): est_scale x partial
+            estimate[i] = c->scale[ci] * static_cast<double>(partial[i]);
+        }
     });
 }
 

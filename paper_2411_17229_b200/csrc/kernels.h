@@ -38,8 +38,10 @@ struct ScanArgs {
     uint32_t K;
     const double* coeff;     // [n_ckpt] reject coefficients
     uint64_t neg_zero2;      // 0x8000000080000000 (opaque to ptxas)
-    unsigned long long* counters;  // [3] total_dco, dims_accumulated, bytes
+    unsigned long long* counters;  // [3] total_dco, dims_accumulated, bytes; [8] eligible, [9] failures
     unsigned long long* phase;     // nullable: per-phase clocks (debug)
+    uint32_t measure;              // failure accounting (DcoStats::measure_failures): pruned pairs are
+                                   // carried to the full dim for their exact distance
     uint32_t max_rows;             // nonzero: scan only the first max_rows rows of each item
     int seed;                      // radius-seeding pass: every query writes slot 0
     const float* row_norms;        // [rows] first-slice |o|^2 (tensor-core filter only)
@@ -79,7 +81,6 @@ struct FilterArgs {
     int debug;                    // 1: re-check every filter prune exactly (counters[3] = violations)
     unsigned long long* census;   // nullable: [0] tiles with kept pairs | tiles << 32, [1] kept pairs (diagnostic)
     const float* q_norms;         // [nq] first-slice |q|^2 (sequential fmaf), tcgen05 filter only
-    int exp;                      // experiments (DADE_GPU_UMMA_EXP): 1 skip epilogue work, 2 skip MMAs
 };
 size_t filter_smem_bytes(int d0, int c_dense);
 cudaError_t launch_filter(const FilterArgs& a, const CUtensorMap& tmap32, uint32_t grid, cudaStream_t s);
@@ -103,6 +104,14 @@ cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const f
                                  const uint32_t* gmin = nullptr);
 // per-row extra operand [n][8] = (-h hi, -h lo, 1, 1, 0, 0, 0, 0) from first-slice norms
 cudaError_t launch_row_aug(const float* norms, uint32_t n, float* out, cudaStream_t s);
+
+// Per-(query, candidate, checkpoint) partial sums as the survivor kernel evaluates
+// them (dade_gpu_set_estimate_dump): {query, candidate id, checkpoint index, partial bits}.
+struct EstimateDump {
+    uint4* entries;
+    uint32_t* count;              // running count (may exceed cap: entries past cap are dropped)
+    uint32_t cap;
+};
 
 // Survivor kernel (stage 2 of the streaming scan) and candidate bucketing.
 struct SurvArgs {
@@ -131,6 +140,9 @@ struct SurvArgs {
     unsigned long long* counters; // [1] dims
     uint32_t* surv_max;           // running max of the survivor count (overflow check)
     uint32_t vec4;                // dim, d0 and every checkpoint are multiples of 4 (16-byte staging)
+    uint32_t measure;             // failure accounting: a pruned pair is carried to the full dim, then
+                                  //   counters[8] += exact <= r (eligible), counters[9] += eligible && pruned
+    EstimateDump dump;            // nullable entries: every checkpoint partial the kernel evaluates
 };
 cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cudaStream_t s);
 cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const uint32_t* q_count,

@@ -450,6 +450,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
     __syncwarp();
 
     unsigned long long st_dco = 0, st_dims = 0, st_bytes = 0;
+    unsigned long long st_elig = 0, st_fail = 0;  // failure accounting (a.measure)
     const uint64_t nz2 = a.neg_zero2;
     const uint32_t d0 = ct.end[c_dense - 1];
     const bool has_sparse = c_dense < ct.n_chunks;
@@ -458,6 +459,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
 
     uint64_t acc[4][4];      // SIMT dense accumulators (kTC == false)
     uint32_t alive = 0;
+    uint32_t pre_pruned = 0;  // failure accounting: pairs pruned at the first checkpoint, still scanned
     for (uint32_t s = 0; s < n_steps; ++s) {
         const uint32_t t = s / c_dense;
         const int c = (int)(s - t * c_dense);
@@ -639,13 +641,18 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                 }
             }
             dead &= alive;
-            alive &= ~dead;
             st_dims += (unsigned long long)__popc(dead) * ct.end[c];
+            if (a.measure) {
+                pre_pruned = dead;  // carried to the full dim for their exact distance
+            } else {
+                alive &= ~dead;
+            }
             pending = alive;
         } else {
             // FD: candidates straight from registers, one query at a time
             st_dims += (unsigned long long)__popc(alive) * dim;
             uint32_t cand = 0;
+            // (FD never prunes early: with failure accounting, eligible = the accepted pairs)
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
                 const float r = r_s[warp * 8 + jj];
@@ -657,6 +664,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                     if (((alive >> (i * 8 + jj)) & 1u) && !(key > r)) cand |= 1u << (i * 8 + jj);
                 }
             }
+            if (a.measure) st_elig += __popc(cand);
             if (__any_sync(0xffffffffu, cand != 0)) {
                 for (int jj = 0; jj < 8; ++jj) {
                     const uint32_t j = warp * 8 + jj;
@@ -695,8 +703,9 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
             for (uint32_t e = lane; e < n; e += 32) {
                 const uint32_t meta = lm[e];
                 float x = la[e];
-                const uint32_t row = meta & 0xffu, jj = (meta >> 8) & 0xffu, j = warp * 8 + jj;
+                const uint32_t row = meta & 0x7fu, jj = (meta >> 8) & 0xffu, j = warp * 8 + jj;
                 bool live = true;
+                bool pruned = (meta & 0x80u) != 0;  // failure accounting: pruned at the first checkpoint
                 const float* orow = a.storage + (size_t)(row_base + row) * dim;
                 const float* qrow = a.queries + (size_t)qidx_s[j] * dim;
                 for (int cc = c_dense; cc < ct.n_chunks; ++cc) {
@@ -729,17 +738,27 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                     }
                     st_bytes += 8ull * (hi - lo);
                     const int k2 = ct.ckpt[cc];
-                    if (k2 >= 0 && x > thr_s[j * n_ckpt + k2]) {
+                    if (k2 >= 0 && !pruned && x > thr_s[j * n_ckpt + k2]) {
                         st_dims += hi;
-                        live = false;
-                        break;
+                        if (a.measure) {
+                            pruned = true;
+                        } else {
+                            live = false;
+                            break;
+                        }
                     }
                 }
                 bool is_cand = false;
-                if (live) {
+                if (live && pruned) {  // record_failure_check (proj/src/estimator.cpp:24-33)
+                    if (__fsqrt_rn(x) <= r_s[j]) {
+                        ++st_elig;
+                        ++st_fail;
+                    }
+                } else if (live) {
                     st_dims += dim;
                     const float key = kSqrtKey ? __fsqrt_rn(x) : x;
                     is_cand = !(key > r_s[j]);
+                    if (a.measure && is_cand) ++st_elig;
                     x = key;
                 }
                 lm[e] = meta | (is_cand ? 0x80000000u : 0u);
@@ -842,7 +861,7 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
                 const uint32_t n = compact_round(
                     pending, wl_meta, wl_acc, lane,
                     [&](int b, uint32_t& row, uint32_t& jj) {
-                        row = lane + 32 * (b >> 3);
+                        row = (lane + 32 * (b >> 3)) | (((pre_pruned >> b) & 1u) << 7);
                         jj = b & 7;
                     },
                     [&](int b) {
@@ -862,6 +881,16 @@ dco_scan_kernel(const ScanArgs a, const __grid_constant__ ChunkTable ct, const _
         v0 += __shfl_xor_sync(0xffffffffu, v0, off);
         v1 += __shfl_xor_sync(0xffffffffu, v1, off);
         v2 += __shfl_xor_sync(0xffffffffu, v2, off);
+    }
+    if (a.measure && a.counters) {
+        unsigned long long e = st_elig, f = st_fail;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            e += __shfl_xor_sync(0xffffffffu, e, off);
+            f += __shfl_xor_sync(0xffffffffu, f, off);
+        }
+        if (lane == 0 && e) atomicAdd(a.counters + 8, e);
+        if (lane == 0 && f) atomicAdd(a.counters + 9, f);
     }
     if (lane == 0 && a.counters) {
         atomicAdd(a.counters + 0, v0);
@@ -1050,6 +1079,13 @@ __device__ __forceinline__ void sp_cp16(float* dst, const float* src) {
                  : "memory");
 }
 
+// One evaluated checkpoint partial into the estimate dump (parity tests).
+__device__ __forceinline__ void dump_partial(const SurvArgs& a, uint32_t q, uint32_t row, uint32_t ci, float x) {
+    const uint32_t p = atomicAdd(a.dump.count, 1u);
+    if (p < a.dump.cap)
+        a.dump.entries[p] = make_uint4(q, a.row_ids ? __ldg(a.row_ids + row) : a.id_base + row, ci, __float_as_uint(x));
+}
+
 __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kernel(const SurvArgs a) {
     extern __shared__ __align__(16) float sp_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1063,6 +1099,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
     for (uint32_t grp = blockIdx.x * kSpWarps + warp; grp < n_groups; grp += gridDim.x * kSpWarps) {
         const uint32_t i = grp * 32 + lane;
         bool live = false, flagged = false;
+        bool pruned = false;  // failure accounting: decided, still accumulating to the full dim
         uint32_t q = 0, row = 0;
         float x = 0.f, r = 0.f;
         if (i < n) {
@@ -1077,7 +1114,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
             }
         }
         uint32_t act = __ballot_sync(0xffffffffu, live);
-        unsigned long long dims = 0, viol = 0;
+        unsigned long long dims = 0, viol = 0, elig = 0, fails = 0;
         if (act) {
             const uint32_t q0 = __shfl_sync(0xffffffffu, q, __ffs(act) - 1);
             const bool qsame = __all_sync(0xffffffffu, !live || q == q0);
@@ -1145,14 +1182,18 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
                     }
                 }
                 __syncwarp();  // buffer `buf` free for the chunk after next
-                if (k0 + w == hi && ci < n_ckpt && live) {
+                if (k0 + w == hi && ci < n_ckpt && live && !pruned) {
+                    // checkpointed_scan's test (proj/src/estimator.cpp:46-60) against this pair's radius
                     const bool pr = x > prune_threshold(a.coeff[ci], r);
+                    if (a.dump.entries) dump_partial(a, q, row, ci, x);
                     if (flagged) {  // the exact prefix must agree with the bound; then drop it as the filter would
                         viol += pr ? 0 : 1;
-                        live = false;
+                        if (a.measure) pruned = true;
+                        else live = false;
                     } else if (pr) {
                         dims += hi;
-                        live = false;
+                        if (a.measure) pruned = true;
+                        else live = false;
                     }
                 }
                 act = __ballot_sync(0xffffffffu, live);
@@ -1167,11 +1208,19 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
         }
         bool is_cand = false;
         uint64_t key = 0;
-        if (live) {
+        if (live && pruned) {
+            // record_failure_check (proj/src/estimator.cpp:24-33): x continued the scan's own
+            // accumulator to the full dim, so it is the exact distance a full scan gives
+            if (__fsqrt_rn(x) <= r) {
+                ++elig;
+                ++fails;
+            }
+        } else if (live) {
             dims += dim;
             const float key_d = __fsqrt_rn(x);
             if (!(key_d > r)) {
                 is_cand = true;
+                elig += a.measure ? 1 : 0;
                 const uint32_t id = a.row_ids ? __ldg(a.row_ids + row) : a.id_base + row;
                 key = make_key(key_d, id);
             }
@@ -1212,6 +1261,14 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
         }
         if (lane == 0 && a.counters && dims) atomicAdd(a.counters + 1, dims);
         if (lane == 0 && a.counters && viol) atomicAdd(a.counters + 3, viol);
+        if (a.measure && a.counters) {
+            for (int off = 16; off > 0; off >>= 1) {
+                elig += __shfl_xor_sync(0xffffffffu, elig, off);
+                fails += __shfl_xor_sync(0xffffffffu, fails, off);
+            }
+            if (lane == 0 && elig) atomicAdd(a.counters + 8, elig);
+            if (lane == 0 && fails) atomicAdd(a.counters + 9, fails);
+        }
     }
 }
 

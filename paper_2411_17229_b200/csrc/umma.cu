@@ -381,11 +381,7 @@ dco_filter_umma_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap t
                 mb_wait(afull + s, (a_use / S) & 1);
                 tp_afull += clock64() - t0;
                 tc_fence_after();
-                if (lane == 0 && a.exp == 2) {  // experiment: no MMAs
-                    tc_commit(aempty + s);
-                    tc_commit(accfull + b);
-                    if (t + 1 == n_tiles) tc_commit(bfree + ib);
-                } else if (lane == 0) {
+                if (lane == 0) {
                     const uint32_t td = tmem + b * 256;
                     uint32_t accf = 0;
                     for (int c = 0; c < c_dense; ++c) {
@@ -500,7 +496,7 @@ dco_filter_umma_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap t
             mb_wait(accfull + b, (k >> 1) & 1);
             te_acc += clock64() - t0;
             tc_fence_after();
-            const uint32_t nch = a.exp == 1 ? 0u : m.ncols / 32;
+            const uint32_t nch = m.ncols / 32;
             const uint32_t tbase = tmem + ((quarter * 32) << 16) + b * 256;
             for (uint32_t c = cgrp; c < nch; c += 4) {  // one 32-column chunk per round
                 float v[32];

@@ -88,8 +88,15 @@ def read_transform(path) -> OrthoTransform:
     mean = np.frombuffer(b, "<f8", dim, off).copy(); off += 8 * dim
     ev = np.frombuffer(b, "<f8", dim, off).copy(); off += 8 * dim
     mat = np.frombuffer(b, "<f8", dim * dim, off).copy()
+    if len(b) < off + 8 * dim * dim:
+        raise RuntimeError("truncated file while reading matrix")
     if np.any(ev[:-1] < ev[1:]):
         raise RuntimeError("transform eigenvalues not nonincreasing")
+    # the loader's corruption check (proj/src/transform.cpp:344-356): columns orthonormal
+    cols = mat.reshape(dim, dim)  # row k = column k of the column-major matrix
+    worst = float(np.max(np.abs(cols @ cols.T - np.eye(dim))))
+    if worst > 1e-5:
+        raise RuntimeError(f"transform matrix not orthogonal (max deviation {worst:.6f})")
     return OrthoTransform(dim, kind, mean, ev, mat)
 
 

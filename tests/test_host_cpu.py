@@ -98,3 +98,37 @@ def test_list_shard_plan_balances_and_partitions():
         assert np.array_equal(owner, plan_list_shards(offsets, world, 256))  # deterministic
     shards = plan_row_shards(10, 4)
     assert shards == [(0, 3), (3, 6), (6, 8), (8, 10)]
+
+
+def test_non_orthogonal_transform_rejected_like_reference(tmp_path, ref_lib, ivf_fix):
+    """OrthoTransform::load's corruption check (proj/src/transform.cpp:344-356):
+    the reference, the Python reader and the C++ mirror all refuse a DADE file
+    whose columns are not orthonormal (max deviation > 1e-5), and accept it below."""
+    from paper_2411_17229_b200 import OrthoTransform
+    from paper_2411_17229_b200.io import read_transform, write_transform
+    fx = ivf_fix
+    d = fx["matrix"].size
+    d = int(round(d ** 0.5))
+    good = OrthoTransform(d, 0, np.zeros(d), fx["eig"], fx["matrix"])
+    bad_m = np.array(fx["matrix"], np.float64).copy()
+    bad_m[3] += 1e-3  # one entry of column 0 perturbed
+    bad = OrthoTransform(d, 0, np.zeros(d), fx["eig"], bad_m)
+    write_transform(tmp_path / "good.dade", good)
+    write_transform(tmp_path / "bad.dade", bad)
+    ref_lib.load_transform(tmp_path / "good.dade")
+    read_transform(tmp_path / "good.dade")
+    with pytest.raises(Exception, match="not orthogonal"):
+        ref_lib.load_transform(tmp_path / "bad.dade")
+    with pytest.raises(RuntimeError, match="not orthogonal"):
+        read_transform(tmp_path / "bad.dade")
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "dade_gpu.hpp"\n#include <iostream>\nint main(int, char** v){ try { '
+                   'dade::gpu::OrthoTransform::load(v[1]); } catch (const std::runtime_error& e) { '
+                   'std::cout << e.what(); return 3; } return 0; }\n')
+    exe = tmp_path / "t"
+    subprocess.run(["g++", "-std=c++20", "-I", str(ROOT / "include"), str(src), "-o", str(exe),
+                    f"-L{ROOT / 'paper_2411_17229_b200'}", "-ldade_gpu",
+                    f"-Wl,-rpath,{ROOT / 'paper_2411_17229_b200'}"], check=True)
+    assert subprocess.run([str(exe), str(tmp_path / "good.dade")]).returncode == 0
+    r = subprocess.run([str(exe), str(tmp_path / "bad.dade")], capture_output=True, text=True)
+    assert r.returncode == 3 and "not orthogonal" in r.stdout
