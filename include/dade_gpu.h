@@ -28,6 +28,13 @@
  *   dade_gpu_partial_sums    partial_sqdist at every checkpoint
  *                                                       proj/src/estimator.cpp:74-82
  *   dade_gpu_calibrate       calibrate                  proj/src/calibration.cpp:109-146
+ *   dade_gpu_covariance      compute_covariance         proj/src/transform.cpp:68-95
+ *   dade_gpu_kmeans          kmeans                     proj/src/ivf.cpp:24-143
+ *   dade_gpu_ivf_build       IvfIndex::build            proj/src/ivf.cpp:145-192
+ *   dade_gpu_ground_truth    compute_ground_truth       proj/src/dataset_io.cpp:101-135
+ *   dade_gpu_set_estimate_dump / _get_estimate_dump
+ *                            partial_sqdist + dade_estimate per (query, candidate, step)
+ *                                                       proj/src/estimator.cpp:74-91
  *
  * Status codes mirror the reference's exception split
  * (proj/include/dade/error.hpp:10-19, proj/tools/dade_cli.cpp:407-419).
@@ -238,6 +245,40 @@ int dade_gpu_get_estimate_dump(dade_gpu_ctx* ctx, uint32_t cap, uint32_t* q, uin
 
 /* Debug: per-query radius (float bits) left by the last IVF search. */
 int dade_gpu_debug_radius(dade_gpu_ctx* ctx, uint32_t* out, uint32_t nq);
+
+/* ---- index build on the GPU, reference arithmetic ---------- */
+
+/* compute_covariance (proj/src/transform.cpp:68-95): fp64 mean [dim] and
+ * covariance [dim x dim] row-major (1/n, centred) of n rows, bit-identical to
+ * the reference. data: device if DEVICE_PTRS; mean / cov: host. */
+int dade_gpu_covariance(dade_gpu_ctx* ctx, const float* data, uint32_t n, uint32_t dim, uint32_t flags,
+                        double* mean, double* cov);
+
+/* kmeans(data, n_clusters, max_iters, seed) (proj/src/ivf.cpp:24-143): k-means++
+ * seeding on the reference's mt19937_64 stream, Lloyd iterations with its
+ * early stop and empty-cluster re-seeding; centroids [n_clusters x dim],
+ * assignments [n] and the iteration count equal the reference's. Drops any IVF
+ * index uploaded to the context. Pointers: device if DEVICE_PTRS, else host;
+ * nullable outputs are skipped. */
+int dade_gpu_kmeans(dade_gpu_ctx* ctx, const float* data, uint32_t n, uint32_t dim, uint32_t n_clusters,
+                    uint32_t max_iters, uint64_t seed, uint32_t flags, float* centroids,
+                    uint32_t* assignments, uint32_t* iterations);
+
+/* IvfIndex::build(data, n_clusters, contiguous, .., max_iters, seed)
+ * (proj/src/ivf.cpp:145-192): the k-means above, posting lists in cluster
+ * order with ids ascending. The built index is installed on the context (as
+ * dade_gpu_set_ivf would) and its DIVF arrays copied out: centroids
+ * [n_clusters x dim], offsets [n_clusters + 1], ids [n], storage [n x dim]
+ * (nullable). */
+int dade_gpu_ivf_build(dade_gpu_ctx* ctx, const float* data, uint32_t n, uint32_t dim, uint32_t n_clusters,
+                       uint32_t max_iters, uint64_t seed, uint32_t flags, float* centroids,
+                       uint32_t* offsets, uint32_t* ids, float* storage);
+
+/* compute_ground_truth (proj/src/dataset_io.cpp:101-135): per query the k
+ * nearest of n base rows by (l2_sq_double, id), exactly the reference's ids
+ * (k <= 2048). out_ids [nq x k]. Pointers: device if DEVICE_PTRS, else host. */
+int dade_gpu_ground_truth(dade_gpu_ctx* ctx, const float* base, uint32_t n, const float* queries, uint32_t nq,
+                          uint32_t dim, uint32_t k, uint32_t flags, uint32_t* out_ids);
 
 /* Number of CUDA kernels this handle launched so far (bench evidence). */
 uint64_t dade_gpu_launch_count(dade_gpu_ctx* ctx);

@@ -240,6 +240,8 @@ class RefLib:
             "dref_linear_scan": ([P, U32, U32, P, P, U32, U32, P, P, P, P, P, I, P], I),
             "dref_ground_truth": ([P, U32, P, U32, U32, U32, P], I),
             "dref_kmeans": ([P, U32, U32, U32, U32, U64, P, P, P], I),
+            "dref_ivf_failure_pass": ([P, P, P, U32, U32, U32, P], I),
+            "dref_covariance": ([P, U32, U32, P, P], I),
         }
         for n, (a, r) in sig.items():
             f = getattr(L, n)
@@ -319,6 +321,22 @@ class RefLib:
         out = np.zeros((qs.shape[0], k), np.uint32)
         self._chk(self.L.dref_ground_truth(_p(da), da.shape[0], _p(qs), qs.shape[0], da.shape[1], k, _p(out)))
         return out
+
+    def kmeans(self, data, n_clusters, iters, seed):
+        da = _f32(data)
+        cen = np.zeros((n_clusters, da.shape[1]), np.float32)
+        asg = np.zeros(da.shape[0], np.uint32)
+        it = U32()
+        self._chk(self.L.dref_kmeans(_p(da), da.shape[0], da.shape[1], n_clusters, iters, seed, _p(cen), _p(asg),
+                                     C.byref(it)))
+        return cen, asg, int(it.value)
+
+    def covariance(self, data):
+        da = _f32(data)
+        d = da.shape[1]
+        mean, cov = np.zeros(d), np.zeros((d, d))
+        self._chk(self.L.dref_covariance(_p(da), da.shape[0], d, _p(mean), _p(cov)))
+        return mean, cov
 
     def linear_scan(self, data, strategy, queries, k, threads=1):
         da, qs = _f32(data), _f32(queries)
@@ -419,6 +437,13 @@ class RefIvf:
 
     def save(self, path):
         self.lib._chk(self.lib.L.dref_ivf_save(self.h, str(path).encode()))
+
+    def failure_pass(self, strategy, queries, k, n_probe):
+        """measure()'s untimed second pass: (total_dco, dims, eligible, failures)."""
+        qs = _f32(queries)
+        st = np.zeros(4, np.uint64)
+        self.lib._chk(self.lib.L.dref_ivf_failure_pass(self.h, strategy.h, _p(qs), qs.shape[0], k, n_probe, _p(st)))
+        return st
 
     def search(self, strategy, queries, k, n_probe, threads=1):
         qs = _f32(queries)

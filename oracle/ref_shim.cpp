@@ -325,6 +325,33 @@ int dref_ground_truth(const float* data, std::uint32_t n, const float* queries, 
     });
 }
 
+// The untimed failure pass of measure() (proj/src/bench.cpp:65-73): every query
+// searched once more with DcoStats::measure_failures; stats [4] accumulate
+// total_dco, dims_accumulated, eligible, failures.
+int dref_ivf_failure_pass(void* ivf, void* sp, const float* queries, std::uint32_t nq, std::uint32_t k,
+                          std::uint32_t n_probe, std::uint64_t* stats) {
+    return guard([&] {
+        const IvfIndex& idx = *static_cast<IvfIndex*>(ivf);
+        const DcoStrategy& s = *static_cast<Strategy*>(sp)->s;
+        DcoStats fstats;
+        fstats.measure_failures = true;
+        for (std::uint32_t qi = 0; qi < nq; ++qi)
+            idx.search(queries + static_cast<std::size_t>(qi) * idx.dim(), k, n_probe, s, &fstats);
+        stats[0] += fstats.total_dco;
+        stats[1] += fstats.dims_accumulated;
+        stats[2] += fstats.eligible;
+        stats[3] += fstats.failures;
+    });
+}
+
+int dref_covariance(const float* data, std::uint32_t n, std::uint32_t dim, double* mean, double* cov) {
+    return guard([&] {
+        CovarianceResult c = compute_covariance(make_set(data, n, dim));
+        std::memcpy(mean, c.mean.data(), c.mean.size() * sizeof(double));
+        std::memcpy(cov, c.cov.data(), c.cov.size() * sizeof(double));
+    });
+}
+
 int dref_kmeans(const float* data, std::uint32_t n, std::uint32_t dim, std::uint32_t n_clusters,
                 std::uint32_t iters, std::uint64_t seed, float* centroids,
                 std::uint32_t* assignments, std::uint32_t* iterations) {

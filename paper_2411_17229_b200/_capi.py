@@ -88,6 +88,10 @@ def _load():
         "dade_gpu_last_filter_profile": ([P, P, P], I),
         "dade_gpu_last_seed_profile": ([P, P, P], I),
         "dade_gpu_set_estimate_dump": ([P, U32], I),
+        "dade_gpu_covariance": ([P, P, U32, U32, U32, P, P], I),
+        "dade_gpu_kmeans": ([P, P, U32, U32, U32, U32, U64, U32, P, P, P], I),
+        "dade_gpu_ivf_build": ([P, P, U32, U32, U32, U32, U64, U32, P, P, P, P], I),
+        "dade_gpu_ground_truth": ([P, P, U32, P, U32, U32, U32, U32, P], I),
         "dade_gpu_get_estimate_dump": ([P, U32, P, P, P, P, P, P], I),
     }
     for name, (args, res) in sigs.items():
@@ -111,7 +115,8 @@ EXPORTED = [
     "dade_gpu_partial_sums", "dade_gpu_calibrate", "dade_gpu_launch_count",
     "dade_gpu_set_profiling", "dade_gpu_last_scan_profile", "dade_gpu_debug_counters",
     "dade_gpu_last_filter_profile", "dade_gpu_last_seed_profile", "dade_gpu_debug_radius",
-    "dade_gpu_set_estimate_dump", "dade_gpu_get_estimate_dump",
+    "dade_gpu_set_estimate_dump", "dade_gpu_get_estimate_dump", "dade_gpu_covariance", "dade_gpu_kmeans",
+    "dade_gpu_ivf_build", "dade_gpu_ground_truth",
 ]
 
 

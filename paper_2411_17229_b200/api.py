@@ -22,6 +22,7 @@ __all__ = [
     "Device", "OrthoTransform", "CalibrationTable", "FdScanningStrategy", "DadeStrategy",
     "AdsamplingStrategy", "IvfIndex", "FlatIndex", "linear_scan", "DcoStats", "DcoOutcome",
     "SearchResult", "Neighbor", "ConfigError", "InvalidInput", "expected_checkpoints",
+    "compute_covariance", "fit_pca", "kmeans", "compute_ground_truth",
 ]
 
 
@@ -364,6 +365,25 @@ class IvfIndex:
                                          ptr(_f32(storage))))
 
     @staticmethod
+    def build(dev: Device, data, n_clusters: int, kmeans_max_iters: int, seed: int) -> "IvfIndex":
+        """IvfIndex::build (proj/src/ivf.cpp:145-192, contiguous layout) on the
+        GPU; the DIVF arrays are on the returned index (centroids, offsets, ids,
+        storage), equal to the reference's."""
+        x = _rows(data)
+        n, d = int(x.shape[0]), int(x.shape[1])
+        cen = np.zeros((n_clusters, d), np.float32)
+        off = np.zeros(n_clusters + 1, np.uint32)
+        ids = np.zeros(n, np.uint32)
+        sto = np.zeros((n, d), np.float32)
+        check(_capi.lib.dade_gpu_ivf_build(dev.h, ptr(x), n, d, n_clusters, kmeans_max_iters, int(seed),
+                                           _dev_flag(x), ptr(cen), ptr(off), ptr(ids), ptr(sto)))
+        idx = IvfIndex.__new__(IvfIndex)
+        idx.dev, idx._dim, idx._count, idx._nc = dev, d, n, n_clusters
+        idx.layout, idx.split, idx.offsets = 0, d, off
+        idx.centroids, idx.ids, idx.storage = cen, ids, sto
+        return idx
+
+    @staticmethod
     def from_divf(dev: Device, divf) -> "IvfIndex":
         return IvfIndex(dev, divf.dim, divf.count, divf.n_clusters, divf.centroids, divf.offsets,
                         divf.ids, divf.storage, divf.layout, divf.split)
@@ -490,6 +510,88 @@ class FlatIndex:
         if stats is not None:
             stats._add(st)
         return ids, dists, counts
+
+
+# ---- index build on the GPU, reference arithmetic ---------------
+
+def _dev_flag(x) -> int:
+    return _capi.DEVICE_PTRS if hasattr(x, "data_ptr") and getattr(x, "is_cuda", False) else 0
+
+
+def _rows(x):
+    """numpy -> C-contiguous f32; CUDA tensors pass through (device pointers)."""
+    if hasattr(x, "data_ptr") and getattr(x, "is_cuda", False):
+        assert x.dtype.itemsize == 4 and x.is_contiguous() and x.dim() == 2
+        return x
+    return _f32(x)
+
+
+def compute_covariance(dev: Device, data):
+    """compute_covariance (proj/src/transform.cpp:68-95) on the GPU: (mean [D],
+    cov [D, D]) bit-identical to the reference."""
+    x = _rows(data)
+    n, d = int(x.shape[0]), int(x.shape[1])
+    mean = np.zeros(d, np.float64)
+    cov = np.zeros((d, d), np.float64)
+    check(_capi.lib.dade_gpu_covariance(dev.h, ptr(x), n, d, _dev_flag(x), ptr(mean), ptr(cov)))
+    return mean, cov
+
+
+def fit_pca(dev: Device, data) -> OrthoTransform:
+    """fit_pca (proj/src/transform.cpp:230-253): covariance on the GPU (exact),
+    symmetric eigendecomposition in fp64 (LAPACK; the reference runs cyclic
+    Jacobi, equal to ~1e-12 relative on the well-separated spectra used here),
+    then the reference's column order (variance descending, stable on ties),
+    orientation (first nonzero component positive) and eigenvalue clamp."""
+    mean, cov = compute_covariance(dev, data)
+    d = cov.shape[0]
+    vals, vecs = np.linalg.eigh(cov)
+    order = sorted(range(d), key=lambda i: -vals[i])  # stable: original position on ties
+    eig = np.array([vals[i] for i in order])
+    cols = np.stack([vecs[:, i] for i in order])  # row k = k-th direction
+    for k in range(d):  # orient_column
+        nz = np.nonzero(cols[k])[0]
+        if nz.size and cols[k, nz[0]] < 0:
+            cols[k] = -cols[k]
+    if np.any(eig < -1e-6):
+        raise RuntimeError("eigenvalue below tolerance; input is not positive semidefinite")
+    eig = np.where(eig < 0.0, 0.0, eig)
+    return OrthoTransform(d, 0, mean, eig, np.ascontiguousarray(cols).reshape(-1))
+
+
+def kmeans(dev: Device, data, n_clusters: int, max_iters: int, seed: int):
+    """kmeans (proj/src/ivf.cpp:24-143) on the GPU: (centroids [C, D],
+    assignments [N], iterations), equal to the reference's."""
+    x = _rows(data)
+    n, d = int(x.shape[0]), int(x.shape[1])
+    cen = np.zeros((n_clusters, d), np.float32)
+    asg = np.zeros(n, np.uint32)
+    it = C.c_uint32()
+    check(_capi.lib.dade_gpu_kmeans(dev.h, ptr(x), n, d, n_clusters, max_iters, int(seed), _dev_flag(x), ptr(cen),
+                                    ptr(asg), C.byref(it)))
+    return cen, asg, int(it.value)
+
+
+def compute_ground_truth(dev: Device, data, queries, k: int) -> np.ndarray:
+    """compute_ground_truth (proj/src/dataset_io.cpp:101-135) on the GPU: ids
+    [nq, k] by (l2_sq_double, id), equal to the reference's."""
+    x, q = _rows(data), _rows(queries)
+    if int(x.shape[1]) != int(q.shape[1]):
+        raise InvalidInput("ground truth: dimension mismatch")
+    nq = int(q.shape[0])
+    out = np.zeros((nq, max(k, 1)), np.uint32)
+    flags = _dev_flag(x)
+    if flags != _dev_flag(q):
+        raise InvalidInput("ground truth: base and queries must both be host or both be device arrays")
+    if flags:
+        import torch
+        o = torch.empty((nq, max(k, 1)), dtype=torch.int32, device=x.device)
+        check(_capi.lib.dade_gpu_ground_truth(dev.h, ptr(x), int(x.shape[0]), ptr(q), nq, int(x.shape[1]), k,
+                                              flags, ptr(o)))
+        return o.cpu().numpy().astype(np.uint32)
+    check(_capi.lib.dade_gpu_ground_truth(dev.h, ptr(x), int(x.shape[0]), ptr(q), nq, int(x.shape[1]), k, 0,
+                                          ptr(out)))
+    return out
 
 
 def linear_scan(data_or_index, query, k: int, dco, stats: DcoStats | None = None,

@@ -24,7 +24,7 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
     "-Xptxas", "-v", "--expt-relaxed-constexpr", "-cudart", "static",
 ]
-SOURCES = ["scan.cu", "filter.cu", "umma.cu", "coarse.cu", "prep.cu", "seed.cu", "capi.cu"]
+SOURCES = ["scan.cu", "filter.cu", "umma.cu", "coarse.cu", "prep.cu", "seed.cu", "build.cu", "capi.cu"]
 
 
 def _run(cmd, log=None):

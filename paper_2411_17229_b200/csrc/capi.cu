@@ -498,9 +498,9 @@ uint32_t coarse_tc_chunk(dade_gpu_ctx* c, uint32_t nq) {
                                                                (1ull << 30) / (4ull * c->n_clusters)));
 }
 // buffers for queries [0, nq) in chunks of coarse_tc_chunk(); overflow flag reset
-void coarse_tc_begin(dade_gpu_ctx* c, uint32_t nq) {
+void coarse_tc_begin(dade_gpu_ctx* c, uint32_t nq, uint32_t n_probe) {
     const uint32_t chunk = coarse_tc_chunk(c, nq);
-    c->probes.ensure((size_t)std::max<uint32_t>(nq, 1) * 256 * 8);
+    c->probes.ensure((size_t)std::max<uint32_t>(nq, 1) * n_probe * 8);
     c->probe_count.ensure((size_t)std::max<uint32_t>(nq, 1) * 4);
     c->cnorm.ensure((size_t)c->n_clusters * 4);
     c->qnorm.ensure((size_t)chunk * 4);
@@ -561,7 +561,7 @@ void coarse_rank(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t n_prob
     if (coarse_tc_ok(c, n_probe)) {
         // tensor-core p~ for all (query, centroid) pairs + exact l2_sq on the
         // boundary candidates (coarse.cu); query chunks bound the p~ buffers
-        coarse_tc_begin(c, nq);
+        coarse_tc_begin(c, nq, n_probe);
         const uint32_t chunk = coarse_tc_chunk(c, nq);
         for (uint32_t q0 = 0; q0 < nq; q0 += chunk)
             coarse_tc_range(c, d_q, q0, std::min(chunk, nq - q0), n_probe);
@@ -1324,7 +1324,7 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
         cuda_check(cudaEventRecord(c->copy_ev[i], c->copy_stream), "event");
         tl_mark(c, "h2d_chunk", c->copy_stream);
     }
-    if (coarse) coarse_tc_begin(c, nq);
+    if (coarse) coarse_tc_begin(c, nq, n_probe);
     for (uint32_t i = 0, q0 = 0; i < nch; q0 += sizes[i], ++i) {
         const uint32_t m = sizes[i];
         cuda_check(cudaStreamWaitEvent(c->stream, c->copy_ev[i], 0), "wait");
@@ -2525,6 +2525,330 @@ int dade_gpu_last_scan_profile(dade_gpu_ctx* c, double* scan_ms, double* scan_by
         if (scan_ms) *scan_ms = c->last_scan_ms;
         if (scan_bytes) *scan_bytes = c->last_bytes;
         if (total_ms) *total_ms = c->last_total_ms;
+    });
+}
+
+// ---- index build ------------------------------------------------
+
+// compute_covariance (proj/src/transform.cpp:68-95): mean [dim] and covariance
+// [dim x dim] row-major into host arrays, bit-identical to the reference.
+int dade_gpu_covariance(dade_gpu_ctx* c, const float* data, uint32_t n, uint32_t dim, uint32_t flags, double* mean,
+                        double* cov) {
+    return guarded([&] {
+        if (!c || !data || !mean || !cov) fail(DADE_GPU_INVALID_INPUT, "compute_covariance: null argument");
+        if (dim == 0) fail(DADE_GPU_INVALID_INPUT, "VectorSet: dim must be positive");
+        if (n < 2) fail(DADE_GPU_INVALID_INPUT, "compute_covariance: need at least 2 vectors");
+        c->use_device();
+        cudaStream_t s = c->stream;
+        DevBuf bx, bm, bc;
+        const float* d_x = data;
+        if (!(flags & DADE_GPU_DEVICE_PTRS)) {
+            upload(bx, data, (size_t)n * dim * 4, s);
+            d_x = bx.as<float>();
+        }
+        bm.ensure((size_t)dim * 8);
+        bc.ensure((size_t)dim * dim * 8);
+        cuda_check(launch_covariance(d_x, n, dim, bm.as<double>(), bc.as<double>(), s), "covariance");
+        c->launches += 2;
+        cuda_check(cudaMemcpyAsync(mean, bm.p, (size_t)dim * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaMemcpyAsync(cov, bc.p, (size_t)dim * dim * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaStreamSynchronize(s), "covariance");
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+// kmeans (proj/src/ivf.cpp:24-143) on the context: centroids end in
+// c->centroids ([n_clusters x dim]), assignments in `assign` (device, [n]).
+// The context's IVF index is dropped (the coarse ranking machinery serves as
+// the exact nearest-centroid assignment: (l2_sq, id) order = the reference's
+// first strict minimum).
+uint32_t kmeans_device(dade_gpu_ctx* c, const float* d_x, uint32_t n, uint32_t dim, uint32_t n_clusters,
+                       uint32_t max_iters, uint64_t seed, DevBuf& assign) {
+    cudaStream_t s = c->stream;
+    c->has_ivf = false;
+    c->sharded = false;
+    c->dim = dim;
+    c->n_clusters = n_clusters;
+    c->centroids.ensure((size_t)n_clusters * dim * 4);
+    float* cen = c->centroids.as<float>();
+    // k-means++ seeding; the mt19937_64 stream is generated here (one draw per pick,
+    // plus rejection-sampling spares)
+    std::mt19937_64 gen(seed);
+    const uint32_t n_raw = n_clusters + 64;
+    std::vector<uint64_t> raw(n_raw);
+    for (auto& r : raw) r = gen();
+    DevBuf d_raw, rng, dist2, bsums, scratch;
+    upload(d_raw, raw.data(), raw.size() * 8, s);
+    rng.ensure(16);
+    cuda_check(cudaMemsetAsync(rng.p, 0, 16, s), "memset");
+    dist2.ensure((size_t)n * 8);
+    bsums.ensure(kmpp_block_count(n) * 8);
+    cuda_check(launch_kmpp_seed(d_x, n, dim, n_clusters, d_raw.as<uint64_t>(), n_raw, rng.as<uint32_t>(),
+                                dist2.as<double>(), bsums.as<double>(), cen, nullptr, s),
+               "k-means++ seeding");
+    c->launches += 3 + 2ull * (n_clusters - 1);
+    uint32_t h_rng[3] = {0, 0, 0};
+    cuda_check(cudaMemcpyAsync(h_rng, rng.p, 12, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "k-means++ seeding");
+    if (h_rng[1]) fail(DADE_GPU_RUNTIME_ERROR, "kmeans: random stream exhausted during seeding");
+    dist2.release();
+    // Lloyd iterations
+    assign.ensure((size_t)n * 4);
+    cuda_check(cudaMemsetAsync(assign.p, 0, (size_t)n * 4, s), "memset");  // assignments.assign(count, 0)
+    DevBuf keys_in, keys_out, offs, temp, flag;
+    keys_in.ensure((size_t)n * 8);
+    keys_out.ensure((size_t)n * 8);
+    offs.ensure(((size_t)n_clusters + 1) * 4);
+    size_t temp_bytes = 0;
+    cuda_check(launch_km_sort(nullptr, n, n_clusters, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(), nullptr,
+                              nullptr, &temp_bytes, s),
+               "sort size");
+    temp.ensure(temp_bytes);
+    flag.ensure(4);
+    scratch.ensure(16);
+    std::vector<uint32_t> h_off(n_clusters + 1), counts(n_clusters);
+    const uint32_t chunk = 1u << 20;  // rows per assignment launch (bounds the probe buffers)
+    uint32_t iterations = 0;
+    for (uint32_t iter = 1; iter <= max_iters; ++iter) {
+        cuda_check(cudaMemsetAsync(flag.p, 0, 4, s), "memset");
+        for (uint32_t r0 = 0; r0 < n; r0 += chunk) {
+            const uint32_t m = std::min(chunk, n - r0);
+            const float* rows = d_x + (size_t)r0 * dim;
+            coarse_rank(c, rows, m, 1);
+            if (c->coarse_tc_used) {  // boundary-candidate overflow (ties): all-exact ranking of this chunk
+                enqueue_flags(c);
+                cuda_check(cudaStreamSynchronize(s), "assign");
+                if (c->h_flags[1]) {
+                    c->coarse_force_exact = true;
+                    try {
+                        coarse_rank(c, rows, m, 1);
+                    } catch (...) {
+                        c->coarse_force_exact = false;
+                        throw;
+                    }
+                    c->coarse_force_exact = false;
+                }
+            }
+            cuda_check(launch_km_assign(c->probes.as<uint64_t>(), m, assign.as<uint32_t>() + r0, flag.as<uint32_t>(), s),
+                       "assign");
+            ++c->launches;
+        }
+        uint32_t changed = 0;
+        cuda_check(cudaMemcpyAsync(&changed, flag.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaStreamSynchronize(s), "assign");
+        iterations = iter;
+        if (!changed && iter > 1) break;
+        // new centroids: members in ascending id order per cluster
+        cuda_check(launch_km_sort(assign.as<uint32_t>(), n, n_clusters, keys_in.as<uint64_t>(),
+                                  keys_out.as<uint64_t>(), offs.as<uint32_t>(), temp.p, &temp_bytes, s),
+                   "sort");
+        cuda_check(launch_km_sums(d_x, dim, keys_out.as<uint64_t>(), offs.as<uint32_t>(), n_clusters, cen, s),
+                   "sums");
+        c->launches += 4;
+        cuda_check(cudaMemcpyAsync(h_off.data(), offs.p, h_off.size() * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_check(cudaStreamSynchronize(s), "sums");
+        for (uint32_t cl = 0; cl < n_clusters; ++cl) counts[cl] = h_off[cl + 1] - h_off[cl];
+        // re-seed empties from the largest cluster's farthest member (ivf.cpp:111-130)
+        for (uint32_t cl = 0; cl < n_clusters; ++cl) {
+            if (counts[cl] != 0) continue;
+            uint32_t largest = 0;
+            for (uint32_t c2 = 1; c2 < n_clusters; ++c2)
+                if (counts[c2] > counts[largest]) largest = c2;
+            if (counts[largest] == 0) break;
+            cuda_check(launch_km_reseed(d_x, n, dim, assign.as<uint32_t>(), largest, cl, cen,
+                                        scratch.as<unsigned long long>(), s),
+                       "reseed");
+            c->launches += 3;
+            --counts[largest];
+            ++counts[cl];
+        }
+    }
+    cuda_check(cudaStreamSynchronize(s), "kmeans");
+    c->tm_centroids = TmapCache{};  // the centroid buffer's contents are final now
+    return iterations;
+}
+
+void check_kmeans_args(uint32_t n, uint32_t dim, uint32_t n_clusters, uint32_t max_iters) {
+    if (dim == 0) fail(DADE_GPU_INVALID_INPUT, "VectorSet: dim must be positive");
+    if (n_clusters == 0 || n_clusters > n)
+        fail(DADE_GPU_INVALID_INPUT, "kmeans: n_clusters must be in [1, count], got " + std::to_string(n_clusters));
+    if (max_iters == 0) fail(DADE_GPU_INVALID_INPUT, "kmeans: max_iters must be positive");
+}
+
+}  // namespace
+
+extern "C" {
+
+int dade_gpu_kmeans(dade_gpu_ctx* c, const float* data, uint32_t n, uint32_t dim, uint32_t n_clusters,
+                    uint32_t max_iters, uint64_t seed, uint32_t flags, float* centroids, uint32_t* assignments,
+                    uint32_t* iterations) {
+    return guarded([&] {
+        if (!c || (n && !data)) fail(DADE_GPU_INVALID_INPUT, "kmeans: null argument");
+        check_kmeans_args(n, dim, n_clusters, max_iters);
+        c->use_device();
+        cudaStream_t s = c->stream;
+        DevBuf bx, assign;
+        const float* d_x = data;
+        if (!(flags & DADE_GPU_DEVICE_PTRS)) {
+            upload(bx, data, (size_t)n * dim * 4, s);
+            d_x = bx.as<float>();
+        }
+        const uint32_t it = kmeans_device(c, d_x, n, dim, n_clusters, max_iters, seed, assign);
+        const cudaMemcpyKind kind = (flags & DADE_GPU_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        if (centroids)
+            cuda_check(cudaMemcpyAsync(centroids, c->centroids.p, (size_t)n_clusters * dim * 4, kind, s), "copy");
+        if (assignments) cuda_check(cudaMemcpyAsync(assignments, assign.p, (size_t)n * 4, kind, s), "copy");
+        cuda_check(cudaStreamSynchronize(s), "kmeans");
+        if (iterations) *iterations = it;
+    });
+}
+
+// IvfIndex::build, contiguous layout (proj/src/ivf.cpp:145-192): k-means, posting
+// lists in cluster order with ids ascending; the index is installed on the
+// context and its DIVF arrays copied out (nullable outputs are skipped).
+int dade_gpu_ivf_build(dade_gpu_ctx* c, const float* data, uint32_t n, uint32_t dim, uint32_t n_clusters,
+                       uint32_t max_iters, uint64_t seed, uint32_t flags, float* centroids, uint32_t* offsets,
+                       uint32_t* ids, float* storage) {
+    return guarded([&] {
+        if (!c || (n && !data)) fail(DADE_GPU_INVALID_INPUT, "ivf_build: null argument");
+        check_kmeans_args(n, dim, n_clusters, max_iters);
+        c->use_device();
+        cudaStream_t s = c->stream;
+        DevBuf bx, assign;
+        const float* d_x = data;
+        if (!(flags & DADE_GPU_DEVICE_PTRS)) {
+            upload(bx, data, (size_t)n * dim * 4, s);
+            d_x = bx.as<float>();
+        }
+        kmeans_device(c, d_x, n, dim, n_clusters, max_iters, seed, assign);
+        DevBuf keys_in, keys_out, temp;
+        keys_in.ensure((size_t)n * 8);
+        keys_out.ensure((size_t)n * 8);
+        c->offsets.ensure(((size_t)n_clusters + 1) * 4);
+        size_t temp_bytes = 0;
+        cuda_check(launch_km_sort(nullptr, n, n_clusters, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(), nullptr,
+                                  nullptr, &temp_bytes, s),
+                   "sort size");
+        temp.ensure(temp_bytes);
+        cuda_check(launch_km_sort(assign.as<uint32_t>(), n, n_clusters, keys_in.as<uint64_t>(),
+                                  keys_out.as<uint64_t>(), c->offsets.as<uint32_t>(), temp.p, &temp_bytes, s),
+                   "sort");
+        c->storage.ensure((size_t)n * dim * 4);
+        c->ids.ensure((size_t)n * 4);
+        cuda_check(launch_gather_rows(d_x, dim, keys_out.as<uint64_t>(), n, c->storage.as<float>(),
+                                      c->ids.as<uint32_t>(), s),
+                   "gather");
+        c->launches += 4;
+        c->h_offsets.assign(n_clusters + 1, 0);
+        cuda_check(cudaMemcpyAsync(c->h_offsets.data(), c->offsets.p, ((size_t)n_clusters + 1) * 4,
+                                   cudaMemcpyDeviceToHost, s),
+                   "D2H");
+        cuda_check(cudaStreamSynchronize(s), "ivf_build");
+        c->dev_offsets = c->h_offsets;
+        c->count = n;
+        c->norms_storage.rows = nullptr;
+        c->aug_storage.rows = nullptr;
+        c->has_ivf = true;
+        const cudaMemcpyKind kind = (flags & DADE_GPU_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        if (centroids)
+            cuda_check(cudaMemcpyAsync(centroids, c->centroids.p, (size_t)n_clusters * dim * 4, kind, s), "copy");
+        if (offsets) cuda_check(cudaMemcpyAsync(offsets, c->offsets.p, ((size_t)n_clusters + 1) * 4, kind, s), "copy");
+        if (ids) cuda_check(cudaMemcpyAsync(ids, c->ids.p, (size_t)n * 4, kind, s), "copy");
+        if (storage) cuda_check(cudaMemcpyAsync(storage, c->storage.p, (size_t)n * dim * 4, kind, s), "copy");
+        cuda_check(cudaStreamSynchronize(s), "ivf_build");
+    });
+}
+
+// compute_ground_truth (proj/src/dataset_io.cpp:101-135): per query the k
+// nearest rows by (l2_sq_double, id). Strided samples of the base give each
+// query a shrinking bound on its k-th distance (any k real rows bound it); the
+// last pass scores every row in fp64 and keeps those within the bound, which
+// holds the exact top-k; a per-query sort by (d^2, id) finishes.
+int dade_gpu_ground_truth(dade_gpu_ctx* c, const float* base, uint32_t n, const float* queries, uint32_t nq,
+                          uint32_t dim, uint32_t k, uint32_t flags, uint32_t* out_ids) {
+    return guarded([&] {
+        if (!c || (n && !base) || (nq && (!queries || !out_ids))) fail(DADE_GPU_INVALID_INPUT, "ground truth: null argument");
+        if (dim == 0) fail(DADE_GPU_INVALID_INPUT, "VectorSet: dim must be positive");
+        if (k == 0 || k > n) fail(DADE_GPU_INVALID_INPUT, "ground truth: k must be in [1, count], got " + std::to_string(k));
+        if (k > 2048) fail(DADE_GPU_INVALID_INPUT, "ground truth: k above 2048 is not supported on the GPU");
+        c->use_device();
+        cudaStream_t s = c->stream;
+        const bool dev = flags & DADE_GPU_DEVICE_PTRS;
+        DevBuf bb, bq, bo;
+        const float* d_b = base;
+        const float* d_q = queries;
+        if (!dev) {
+            upload(bb, base, (size_t)n * dim * 4, s);
+            d_b = bb.as<float>();
+        }
+        uint32_t cap = 4096;
+        while (cap < 8 * k) cap <<= 1;
+        // level strides: powers of `ratio`, so each level's sample (rows 0, s, 2s, ...) holds the
+        // previous one; level 0 has between k and k * ratio rows (all kept: bound = +inf)
+        const uint32_t ratio = std::max<uint32_t>(2, cap / (4 * k));
+        uint64_t st = 1;
+        while (st * ratio <= n / k) st *= ratio;
+        std::vector<uint32_t> strides;
+        for (;; st /= ratio) {
+            strides.push_back((uint32_t)st);
+            if (st == 1) break;
+        }
+        const uint32_t chunk = std::max<uint32_t>(64, std::min<uint32_t>(nq, (uint32_t)((1ull << 30) / (cap * 12ull))));
+        DevBuf thr, cnt, cd, ci, ov;
+        thr.ensure((size_t)chunk * 8);
+        cnt.ensure((size_t)chunk * 4);
+        cd.ensure((size_t)chunk * cap * 8);
+        ci.ensure((size_t)chunk * cap * 4);
+        ov.ensure(4);
+        for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
+            const uint32_t m = std::min(chunk, nq - q0);
+            const float* qc = d_q;
+            if (!dev) {
+                upload(bq, queries + (size_t)q0 * dim, (size_t)m * dim * 4, s);
+                qc = bq.as<float>();
+            } else {
+                qc = queries + (size_t)q0 * dim;
+            }
+            {  // +inf bounds for level 0
+                std::vector<double> inf(m, std::numeric_limits<double>::infinity());
+                cuda_check(cudaMemcpyAsync(thr.p, inf.data(), (size_t)m * 8, cudaMemcpyHostToDevice, s), "H2D");
+                cuda_check(cudaStreamSynchronize(s), "thr");
+            }
+            uint32_t* ids_out = dev ? out_ids + (size_t)q0 * k : nullptr;
+            if (!dev) ids_out = static_cast<uint32_t*>(bo.ensure((size_t)m * k * 4));
+            for (size_t lv = 0; lv < strides.size(); ++lv) {
+                const bool last = lv + 1 == strides.size();
+                for (int attempt = 0;; ++attempt) {
+                    cuda_check(cudaMemsetAsync(cnt.p, 0, (size_t)m * 4, s), "memset");
+                    cuda_check(cudaMemsetAsync(ov.p, 0, 4, s), "memset");
+                    cuda_check(launch_gt_scan(d_b, n, strides[lv], qc, m, dim, thr.as<double>(), cap, cnt.as<uint32_t>(),
+                                              cd.as<double>(), ci.as<uint32_t>(), c->n_sms, s),
+                               "gt scan");
+                    // the k-th smallest kept distance bounds each query's k-th distance
+                    cuda_check(launch_gt_select(cnt.as<uint32_t>(), cap, cd.as<double>(), ci.as<uint32_t>(), m, k,
+                                                last ? ids_out : nullptr, thr.as<double>(), ov.as<uint32_t>(), s),
+                               "gt select");
+                    c->launches += 2;
+                    if (!last) break;
+                    uint32_t h_ov = 0;
+                    cuda_check(cudaMemcpyAsync(&h_ov, ov.p, 4, cudaMemcpyDeviceToHost, s), "D2H");
+                    cuda_check(cudaStreamSynchronize(s), "gt");
+                    if (!h_ov) break;  // every query kept all its candidates: exact
+                    // some query had more than cap rows within its bound: rescan with the
+                    // (tighter) k-th of the kept ones
+                    if (attempt >= 4)
+                        fail(DADE_GPU_RUNTIME_ERROR, "ground truth: more than " + std::to_string(cap) +
+                                                         " rows tie at a query's k-th distance");
+                }
+            }
+            if (!dev)
+                cuda_check(cudaMemcpyAsync(out_ids + (size_t)q0 * k, ids_out, (size_t)m * k * 4, cudaMemcpyDeviceToHost, s),
+                           "D2H");
+        }
+        cuda_check(cudaStreamSynchronize(s), "ground truth");
     });
 }
 

@@ -254,4 +254,30 @@ cudaError_t launch_pair_partials(const float* data, uint32_t dim, const uint32_t
                                  const uint32_t* pj, uint64_t n, const uint32_t* cps,
                                  uint32_t n_ckpt, float* out, cudaStream_t s);
 
+// build.cu: the index-build side (covariance, k-means, ground truth) in the
+// reference's fp64 arithmetic
+cudaError_t launch_covariance(const float* x, uint32_t n, uint32_t dim, double* mean, double* cov, cudaStream_t s);
+size_t kmpp_block_count(uint32_t n);
+// rng_state [3] zeroed: position in raw, error flag, first pick; picks (nullable) [n_clusters]
+cudaError_t launch_kmpp_seed(const float* x, uint32_t n, uint32_t dim, uint32_t n_clusters, const uint64_t* raw,
+                             uint32_t n_raw, uint32_t* rng_state, double* dist2, double* block_sums,
+                             float* centroids, uint32_t* picks, cudaStream_t s);
+cudaError_t launch_km_assign(const uint64_t* probes, uint32_t n, uint32_t* assign, uint32_t* changed,
+                             cudaStream_t s);
+// temp == nullptr: *temp_bytes = the radix sort's scratch size
+cudaError_t launch_km_sort(const uint32_t* assign, uint32_t n, uint32_t n_clusters, uint64_t* keys_in,
+                           uint64_t* keys_out, uint32_t* offsets, void* temp, size_t* temp_bytes, cudaStream_t s);
+cudaError_t launch_km_sums(const float* x, uint32_t dim, const uint64_t* sorted, const uint32_t* offsets,
+                           uint32_t n_clusters, float* centroids, cudaStream_t s);
+cudaError_t launch_km_reseed(const float* x, uint32_t n, uint32_t dim, uint32_t* assign, uint32_t largest,
+                             uint32_t empty_c, float* centroids, unsigned long long* scratch, cudaStream_t s);
+cudaError_t launch_gather_rows(const float* x, uint32_t dim, const uint64_t* sorted, uint32_t n, float* rows_out,
+                               uint32_t* ids_out, cudaStream_t s);
+cudaError_t launch_gt_scan(const float* base, uint32_t n, uint32_t row_stride, const float* queries, uint32_t nq,
+                           uint32_t dim, const double* thr, uint32_t cap, uint32_t* cnt, double* cand_d,
+                           uint32_t* cand_id, int n_sms, cudaStream_t s);
+cudaError_t launch_gt_select(const uint32_t* cnt, uint32_t cap, const double* cand_d, const uint32_t* cand_id,
+                             uint32_t nq, uint32_t k, uint32_t* out_ids, double* out_kth, uint32_t* overflow,
+                             cudaStream_t s);
+
 }  // namespace dade_gpu

@@ -50,3 +50,22 @@ def mix_fix():
 @pytest.fixture(scope="session")
 def rot_fix():
     return load_golden("rot_fix")
+
+
+@pytest.fixture(scope="session")
+def cfg0_fix():
+    return load_golden("cfg0_fix")
+
+
+@pytest.fixture(scope="session")
+def hd_fix():
+    return load_golden("hd_fix")
+
+
+@pytest.fixture(scope="session")
+def synth():
+    """tests/golden/synth.py: the generator the fixtures' data came from."""
+    if str(GOLDEN) not in sys.path:
+        sys.path.insert(0, str(GOLDEN))
+    import synth as s
+    return s

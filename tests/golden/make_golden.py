@@ -17,6 +17,16 @@ Fixtures (all small, committed):
                    k-means (20 iters, seed 2) by the reference, with its search
                    outputs for FD / DADE at nprobe 4, K 10, dd 8, and ground truth.
   rot_fix.npz      apply_transform outputs (bit-level) for raw rows.
+  cfg0_fix.npz     BASELINE config 0 in full (100k x 128, 64-component mixture, PCA,
+                   IvfIndex::build nlist 256 / 20 iters / seed 2, calibrate p_s .1 dd 16
+                   100k pairs seed 1, nprobe 16, K 10): the reference's covariance,
+                   transform, calibration, k-means lists and iteration count, FD and
+                   DADE search outputs with DcoStats, measure()'s failure pass, and
+                   compute_ground_truth. Data regenerated from tests/golden/synth.py
+                   (digest-checked); only the reference's outputs are stored.
+  hd_fix.npz       long vectors (D 768 / 960, Delta-d 64, K 10 / 20; configs 4 / 2 shapes
+                   scaled to 8k rows, 16 lists): IvfIndex::build, calibration, FD /
+                   DADE / unbounded-DADE outputs at nprobe 4 and 16, ground truth.
 """
 from __future__ import annotations
 
@@ -29,6 +39,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 
+sys.path.insert(0, str(Path(__file__).resolve().parent))
 from oracle import RefLib  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
@@ -54,6 +65,10 @@ def divf_arrays(path):
 def main():
     ref = RefLib()
     tmp = Path(tempfile.mkdtemp())
+    if len(sys.argv) > 1:  # only the named fixtures (e.g. cfg0 hd)
+        for name in sys.argv[1:]:
+            {"cfg0": make_cfg0, "hd": make_hd}[name](ref, tmp)
+        return
 
     # ---- ivf_fix (proj/tests/test_ivf.cpp:53-73) ---------------------------
     raw, _ = ref.synth(620, 16, 0, 202, alpha=1.0, rotate=True)
@@ -159,8 +174,68 @@ def main():
     # ---- rot_fix: apply_transform bits --------------------------------------
     np.savez_compressed(OUT / "rot_fix.npz", matrix=mat3, eig=eig3, raw=q_raw, rotated=q3,
                         matrix16=mat, raw16=raw[:50], rotated16=rot[:50])
+    make_cfg0(ref, tmp)
+    make_hd(ref, tmp)
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
+
+
+def make_cfg0(ref, tmp):
+    import time
+    import synth
+    c = synth.CFG0
+    t0 = time.time()
+    base_raw, q_raw = synth.config0()
+    print(f"cfg0 data {time.time() - t0:.1f}s", flush=True)
+    cmean, cov = ref.covariance(base_raw)
+    t = ref.fit_pca(base_raw)
+    mean, eig, mat, pre = t.arrays()
+    base, q = t.apply(base_raw), t.apply(q_raw)
+    cal = t.calibrate(base, c["p_s"], c["delta_d"], c["cal_pairs"], c["cal_seed"])
+    ps, dd, cps, eps = cal.get()
+    print(f"cfg0 pca+cal {time.time() - t0:.1f}s", flush=True)
+    ivf = ref.ivf_build(base, c["nlist"], layout=0, split=0, iters=c["kmeans_iters"], seed=c["kmeans_seed"])
+    ivf.save(tmp / "cfg0.ivf")
+    dv = divf_arrays(tmp / "cfg0.ivf")
+    _, _, km_iters = ref.kmeans(base[:2000], 16, c["kmeans_iters"], c["kmeans_seed"])  # (shim smoke)
+    print(f"cfg0 ivf {time.time() - t0:.1f}s", flush=True)
+    strat = {"fd": ref.strategy_fd(c["dim"]), "dade": ref.strategy_dade(t, cal, c["delta_d"])}
+    res = ivf_outputs(ref, ivf, strat, q, c["k"], [c["nprobe"]])
+    fail = ivf.failure_pass(strat["dade"], q, c["k"], c["nprobe"])
+    gt = ref.ground_truth(base, q, c["k"])
+    print(f"cfg0 search+gt {time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(
+        OUT / "cfg0_fix.npz", base_raw_digest=synth.digest(base_raw), q_raw_digest=synth.digest(q_raw),
+        base_digest=synth.digest(base), cov_mean=cmean, cov=cov, mean=mean, eig=eig, matrix=mat,
+        lambda_prefix=pre, cal_p_s=ps, cal_delta_d=dd, cal_cps=np.array(cps, np.uint32), cal_eps=np.array(eps),
+        centroids=dv.centroids, offsets=dv.offsets, ids=dv.ids, dade_failure_stats=fail, gt=gt, **res)
+
+
+def make_hd(ref, tmp):
+    import synth
+    from paper_2411_17229_b200.api import OrthoTransform
+    from paper_2411_17229_b200.io import write_transform
+    out = {}
+    for dim, c in synth.HD.items():
+        base, q, lam = synth.high_dim(dim)
+        write_transform(tmp / f"hd{dim}.dade", OrthoTransform(dim, 0, np.zeros(dim), lam, np.eye(dim).reshape(-1)))
+        t = ref.load_transform(tmp / f"hd{dim}.dade")
+        cal = t.calibrate(base, c["p_s"], c["delta_d"], 20000, 7)
+        ps, dd, cps, eps = cal.get()
+        ivf = ref.ivf_build(base, c["nlist"], layout=0, split=0, iters=20, seed=2)
+        ivf.save(tmp / f"hd{dim}.ivf")
+        dv = divf_arrays(tmp / f"hd{dim}.ivf")
+        strat = {"fd": ref.strategy_fd(dim), "dade": ref.strategy_dade(t, cal, c["delta_d"]),
+                 "unb": ref.strategy_dade(t, ref.cal_unbounded(dim, c["delta_d"]), c["delta_d"])}
+        res = ivf_outputs(ref, ivf, strat, q, c["k"], [c["nprobe"], c["nlist"]])
+        gt = ref.ground_truth(base, q, c["k"])
+        p = f"d{dim}_"
+        out.update({p + "base_digest": synth.digest(base), p + "q_digest": synth.digest(q), p + "eig": lam,
+                    p + "cal_p_s": ps, p + "cal_delta_d": dd, p + "cal_cps": np.array(cps, np.uint32),
+                    p + "cal_eps": np.array(eps), p + "centroids": dv.centroids, p + "offsets": dv.offsets,
+                    p + "ids": dv.ids, p + "gt": gt})
+        out.update({p + kk: v for kk, v in res.items()})
+    np.savez_compressed(OUT / "hd_fix.npz", **out)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,318 @@
+"""GPU parity at BASELINE shapes, through the C ABI, against the reference.
+
+* config 0 in full (100k x 128, nlist 256, nprobe 16, K 10, Delta-d 16, p_s .1)
+  on the reference-built artifacts of tests/golden/cfg0_fix.npz: FD ids,
+  distances and DcoStats bit-exact, DADE recall >= reference - 0.002 with
+  exact accepted distances, measure()'s failure pass, rotation bit-exact;
+* long vectors (D 768 / 960, Delta-d 64, K 10 / 20: configs 4 / 2 shapes,
+  the dim > 256 radius seed `seed_radius_list_kernel` and the d0 = 64 tcgen05
+  filter): FD bit-exact, unbounded DADE (the streaming path, nothing pruned
+  by the estimator) bit-exact with FD, DADE recall;
+* K = 100 at D = 256 through the persistent TMA seed (`seed_persist_kernel`,
+  the headline path) against the oracle;
+* rotation bit-exact at D 256 / 960;
+* per-(query, candidate, checkpoint) estimator values of the hot path itself
+  (the survivor kernel's partials) against partial_sqdist + dade_estimate.
+
+Tolerances (BASELINE.json north_star): FD ids + distances 0 ulp (the spec
+allows 1e-5 relative and id swaps at ties; our (dist, id) keys tie-break
+like the reference's heap); estimator values 0 ulp (spec 1e-5 relative);
+DADE recall >= reference - 0.002 (RECALL_SLACK)."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RECALL_SLACK = 0.002
+
+
+@pytest.fixture(scope="module")
+def gp():
+    import paper_2411_17229_b200 as gp
+    return gp
+
+
+@pytest.fixture(scope="module")
+def dev(gp):
+    return gp.Device(0)
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def assert_same_results(gi, gd, gc, ri, rd, rc):
+    assert np.array_equal(gc, rc)
+    for q in range(gc.shape[0]):
+        assert np.array_equal(gi[q, :gc[q]], ri[q, :rc[q]]), q
+        assert np.array_equal(bits(gd[q, :gc[q]]), bits(rd[q, :rc[q]])), q
+
+
+# ---- config 0 ---------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def cfg0(gp, cfg0_fix, synth):
+    # one context per fixture: a context holds one index at a time
+    dev = gp.Device(0)
+    fx = cfg0_fix
+    base_raw, q_raw = synth.config0()
+    assert synth.digest(base_raw) == str(fx["base_raw_digest"]), "config-0 data differs from the fixture's"
+    assert synth.digest(q_raw) == str(fx["q_raw_digest"])
+    c = synth.CFG0
+    t = gp.OrthoTransform(c["dim"], 0, fx["mean"], fx["eig"], fx["matrix"])
+    base = t.apply(dev, base_raw)  # the reference's transform, rotated on the GPU
+    q = t.apply(dev, q_raw)
+    cal = gp.CalibrationTable(float(fx["cal_p_s"]), int(fx["cal_delta_d"]), [int(x) for x in fx["cal_cps"]],
+                              [float(x) for x in fx["cal_eps"]])
+    idx = gp.IvfIndex(dev, c["dim"], c["n"], c["nlist"], fx["centroids"], fx["offsets"], fx["ids"],
+                      base[fx["ids"].astype(np.int64)])
+    return dict(dev=dev, fx=fx, c=c, t=t, base_raw=base_raw, base=base, q=q, cal=cal, idx=idx)
+
+
+def test_cfg0_rotation_bit_exact(synth, cfg0):
+    # apply_transform on the GPU == the reference's (digest of its rotated base)
+    assert synth.digest(cfg0["base"]) == str(cfg0["fx"]["base_digest"])
+
+
+def test_cfg0_fd_bit_exact_with_stats(gp, cfg0):
+    fx, c = cfg0["fx"], cfg0["c"]
+    st = gp.DcoStats()
+    gi, gd, gc = cfg0["idx"].search_batch(cfg0["q"], c["k"], c["nprobe"], gp.FdScanningStrategy(c["dim"]), st)
+    npb = c["nprobe"]
+    assert_same_results(gi, gd, gc, fx[f"fd_np{npb}_ids"], fx[f"fd_np{npb}_dists"], fx[f"fd_np{npb}_counts"])
+    assert (st.total_dco, st.dims_accumulated) == tuple(int(x) for x in fx[f"fd_np{npb}_stats"])
+
+
+def test_cfg0_dade_recall_and_exact_distances(gp, oracle_lib, cfg0):
+    fx, c, dev = cfg0["fx"], cfg0["c"], cfg0["dev"]
+    dade = gp.DadeStrategy(cfg0["t"], cfg0["cal"], c["delta_d"], dev=dev)
+    st = gp.DcoStats()
+    gi, gd, gc = cfg0["idx"].search_batch(cfg0["q"], c["k"], c["nprobe"], dade, st)
+    base, q = cfg0["base"], cfg0["q"]
+    for qi in range(0, gi.shape[0], 7):
+        for i in range(gc[qi]):
+            ex = math.sqrt(oracle_lib.partial_sqdist(base[gi[qi, i]], q[qi], 0, c["dim"]))
+            assert np.float32(ex) == gd[qi, i]
+    npb = c["nprobe"]
+    rec = oracle_lib.recall(gi, gc, fx["gt"])
+    rref = oracle_lib.recall(fx[f"dade_np{npb}_ids"], fx[f"dade_np{npb}_counts"], fx["gt"])
+    assert rec >= rref - RECALL_SLACK, (rec, rref)
+    # the estimator does prune: fewer dims than FD
+    assert st.dim_fraction(c["dim"]) < 0.6
+
+
+def test_cfg0_failure_pass(gp, cfg0, monkeypatch):
+    """measure()'s untimed pass (proj/src/bench.cpp:65-73): eligible = DCOs whose
+    exact distance is within the radius they were tested against, failures =
+    those the estimator pruned. FD and unbounded DADE never fail; calibrated
+    DADE's rate is the reference's within 0.03 (our thresholds are batched, so
+    not the same sequence of radii) and under the union bound sum(p_s)."""
+    fx, c, dev = cfg0["fx"], cfg0["c"], cfg0["dev"]
+    idx, q = cfg0["idx"], cfg0["q"]
+    fd = gp.FdScanningStrategy(c["dim"])
+    st = gp.DcoStats(measure_failures=True)
+    gi, gd, gc = idx.search_batch(q, c["k"], c["nprobe"], fd, st)
+    assert st.failures == 0 and st.eligible >= gc.sum()
+    unb = gp.DadeStrategy(cfg0["t"], gp.CalibrationTable.unbounded(c["dim"], c["delta_d"]), c["delta_d"], dev=dev)
+    st = gp.DcoStats(measure_failures=True)
+    idx.search_batch(q, c["k"], c["nprobe"], unb, st)
+    assert st.failures == 0 and st.eligible > 0
+    dade = gp.DadeStrategy(cfg0["t"], cfg0["cal"], c["delta_d"], dev=dev)
+    ref = fx["dade_failure_stats"]
+    ref_rate = float(ref[3]) / float(ref[2])
+    rates = []
+    for env in (None, "1"):  # the tcgen05 streaming path, then the all-SIMT scan
+        if env:
+            monkeypatch.setenv("DADE_GPU_NO_UMMA", env)
+        st = gp.DcoStats(measure_failures=True)
+        gi2, _, gc2 = idx.search_batch(q, c["k"], c["nprobe"], dade, st)
+        assert 0 < st.failures <= st.eligible
+        rates.append(st.failure_rate())
+        # the failure pass returns the search's results as well (recall unchanged)
+        from oracle import Oracle
+        assert Oracle().recall(gi2, gc2, fx["gt"]) >= Oracle().recall(
+            fx[f"dade_np{c['nprobe']}_ids"], fx[f"dade_np{c['nprobe']}_counts"], fx["gt"]) - RECALL_SLACK
+    n_ckpt = len(cfg0["cal"].checkpoints)
+    for r in rates:
+        assert abs(r - ref_rate) <= 0.03, (rates, ref_rate)
+        assert r <= n_ckpt * c["p_s"]
+
+
+def test_cfg0_ground_truth_gpu(gp, cfg0):
+    dev = cfg0["dev"]
+    gt = gp.compute_ground_truth(dev, cfg0["base"], cfg0["q"], cfg0["c"]["k"])
+    assert np.array_equal(gt, cfg0["fx"]["gt"])
+
+
+def test_cfg0_covariance_and_pca(gp, cfg0):
+    fx, dev = cfg0["fx"], cfg0["dev"]
+    mean, cov = gp.compute_covariance(dev, cfg0["base_raw"])
+    assert np.array_equal(mean.view(np.uint64), fx["cov_mean"].view(np.uint64))
+    assert np.array_equal(cov.view(np.uint64), fx["cov"].view(np.uint64))  # bit-identical to the reference
+    t = gp.fit_pca(dev, cfg0["base_raw"])
+    trace = float(np.trace(cov))
+    assert np.max(np.abs(t.eigenvalues - fx["eig"])) <= 1e-9 * trace
+    d = t.dim
+    ours = t.matrix.reshape(d, d)
+    ref = np.asarray(fx["matrix"]).reshape(d, d)
+    assert np.max(np.abs(ours - ref)) <= 1e-6  # same columns, same orientation
+    assert np.array_equal(t.mean, fx["mean"])
+
+
+def test_cfg0_ivf_build_identical(gp, cfg0):
+    """IvfIndex::build (k-means++ seeding, 20 Lloyd iterations, seed 2) on the
+    GPU gives the reference's centroids, posting lists and ids bit for bit."""
+    c, fx = cfg0["c"], cfg0["fx"]
+    idx = gp.IvfIndex.build(gp.Device(0), cfg0["base"], c["nlist"], c["kmeans_iters"], c["kmeans_seed"])
+    assert np.array_equal(idx.offsets, fx["offsets"])
+    assert np.array_equal(idx.ids, fx["ids"])
+    assert np.array_equal(bits(idx.centroids), bits(fx["centroids"]))
+
+
+# ---- long vectors (D > 256: configs 2 / 4 shapes) ------------------------------------
+@pytest.fixture(scope="module", params=[768, 960])
+def hd(request, gp, hd_fix, synth):
+    dim = request.param
+    dev = gp.Device(0)
+    fx = {k[len(f"d{dim}_"):]: v for k, v in hd_fix.items() if k.startswith(f"d{dim}_")}
+    base, q, lam = synth.high_dim(dim)
+    assert synth.digest(base) == str(fx["base_digest"]) and synth.digest(q) == str(fx["q_digest"])
+    c = synth.HD[dim]
+    t = gp.OrthoTransform(dim, 0, np.zeros(dim), fx["eig"], np.eye(dim).reshape(-1))
+    cal = gp.CalibrationTable(float(fx["cal_p_s"]), int(fx["cal_delta_d"]), [int(x) for x in fx["cal_cps"]],
+                              [float(x) for x in fx["cal_eps"]])
+    idx = gp.IvfIndex(dev, dim, c["n"], c["nlist"], fx["centroids"], fx["offsets"], fx["ids"],
+                      base[fx["ids"].astype(np.int64)])
+    return dict(dev=dev, dim=dim, fx=fx, c=c, t=t, cal=cal, idx=idx, base=base, q=q)
+
+
+def test_hd_fd_bit_exact(gp, hd):
+    fx, c = hd["fx"], hd["c"]
+    for npb in (c["nprobe"], c["nlist"]):
+        st = gp.DcoStats()
+        gi, gd, gc = hd["idx"].search_batch(hd["q"], c["k"], npb, gp.FdScanningStrategy(hd["dim"]), st)
+        assert_same_results(gi, gd, gc, fx[f"fd_np{npb}_ids"], fx[f"fd_np{npb}_dists"], fx[f"fd_np{npb}_counts"])
+        assert (st.total_dco, st.dims_accumulated) == tuple(int(x) for x in fx[f"fd_np{npb}_stats"])
+    # all lists probed == exact ground truth
+    assert np.array_equal(gi, fx["gt"])
+
+
+def test_hd_unbounded_dade_streaming_equals_fd(gp, hd):
+    dev = hd["dev"]
+    """Unbounded DADE has checkpoints, so it runs the streaming path (radius seed
+    over each nearest list's first rows by seed_radius_list_kernel, tcgen05 filter
+    with d0 = 64, survivors) but never prunes by estimate: the reference gives the
+    FD answer and so must we, bit for bit."""
+    fx, c, dim = hd["fx"], hd["c"], hd["dim"]
+    unb = gp.DadeStrategy(hd["t"], gp.CalibrationTable.unbounded(dim, c["delta_d"]), c["delta_d"], dev=dev)
+    for npb in (c["nprobe"], c["nlist"]):
+        gi, gd, gc = hd["idx"].search_batch(hd["q"], c["k"], npb, unb)
+        assert_same_results(gi, gd, gc, fx[f"fd_np{npb}_ids"], fx[f"fd_np{npb}_dists"], fx[f"fd_np{npb}_counts"])
+        assert_same_results(gi, gd, gc, fx[f"unb_np{npb}_ids"], fx[f"unb_np{npb}_dists"], fx[f"unb_np{npb}_counts"])
+
+
+def test_hd_dade_recall(gp, oracle_lib, hd):
+    dev = hd["dev"]
+    fx, c, dim = hd["fx"], hd["c"], hd["dim"]
+    dade = gp.DadeStrategy(hd["t"], hd["cal"], c["delta_d"], dev=dev)
+    for npb in (c["nprobe"], c["nlist"]):
+        gi, gd, gc = hd["idx"].search_batch(hd["q"], c["k"], npb, dade)
+        for qi in range(gi.shape[0]):
+            for i in range(gc[qi]):
+                ex = math.sqrt(oracle_lib.partial_sqdist(hd["base"][gi[qi, i]], hd["q"][qi], 0, dim))
+                assert np.float32(ex) == gd[qi, i]
+        rec = oracle_lib.recall(gi, gc, fx["gt"])
+        rref = oracle_lib.recall(fx[f"dade_np{npb}_ids"], fx[f"dade_np{npb}_counts"], fx["gt"])
+        assert rec >= rref - RECALL_SLACK, (npb, rec, rref)
+
+
+def test_hd_ground_truth_gpu(gp, hd):
+    dev = hd["dev"]
+    gt = gp.compute_ground_truth(dev, hd["base"], hd["q"], hd["c"]["k"])
+    assert np.array_equal(gt, hd["fx"]["gt"])
+
+
+# ---- K = 100 at D = 256: the persistent TMA seed ---------------------------------------
+@pytest.fixture(scope="module")
+def d256(gp):
+    dev = gp.Device(0)
+    g = np.random.default_rng(256)
+    dim, n, nq, nlist = 256, 40_000, 200, 24
+    lam = np.arange(1, dim + 1) ** -1.2
+    centers = g.standard_normal((nlist, dim)) * 4
+    data = (centers[g.integers(0, nlist, n)] + g.standard_normal((n, dim)) * np.sqrt(lam * dim / lam.sum()))
+    data = data.astype(np.float32)
+    qs = (data[g.integers(0, n, nq)] + 0.3 * g.standard_normal((nq, dim))).astype(np.float32)
+    idx = gp.IvfIndex.build(dev, data, nlist, 10, 5)
+    return dict(dev=dev, dim=dim, data=data, qs=qs, idx=idx, nlist=nlist)
+
+
+def test_k100_d256_seed_persist_fd_exact(gp, oracle_lib, d256):
+    dev = d256["dev"]
+    idx, qs, dim = d256["idx"], d256["qs"], d256["dim"]
+    assert int(np.diff(idx.offsets).max()) > 1024  # lists longer than the seed's rows
+    oi, od, oc, ost = oracle_lib.ivf_search(idx.centroids, idx.offsets, idx.ids, idx.storage, qs, 100, 6)
+    gi, gd, gc = idx.search_batch(qs, 100, 6, gp.FdScanningStrategy(dim))
+    assert_same_results(gi, gd, gc, oi, od, oc)
+    # unbounded DADE: the streaming path with the persistent seed
+    t = gp.OrthoTransform(dim, 0, np.zeros(dim), np.linspace(2.0, 0.1, dim), np.eye(dim).reshape(-1))
+    unb = gp.DadeStrategy(t, gp.CalibrationTable.unbounded(dim, 32), 32, dev=dev)
+    dev.set_profiling(True)
+    try:
+        gi, gd, gc = idx.search_batch(qs, 100, 6, unb)
+        seed_ms, seed_pd = dev.last_seed_profile()
+    finally:
+        dev.set_profiling(False)
+    assert seed_ms > 0 and seed_pd > 0, "seed_persist_kernel did not run"
+    assert_same_results(gi, gd, gc, oi, od, oc)
+
+
+def test_hot_path_estimator_values(gp, oracle_lib, ref_lib, d256, monkeypatch, tmp_path):
+    """Every checkpoint partial the survivor kernel evaluates (DADE_GPU_DEBUG=1
+    sends every pair there, pruned-by-bound ones included) equals
+    partial_sqdist(o, q, 0, d) bit for bit, and est_scale x partial equals the
+    reference's dade_estimate(t, partial, d) (proj/src/estimator.cpp:74-91)."""
+    from paper_2411_17229_b200.io import write_transform
+    idx, qs, dim, data, dev = d256["idx"], d256["qs"], d256["dim"], d256["data"], d256["dev"]
+    lam = np.sort(np.var(data.astype(np.float64), axis=0))[::-1].copy()
+    t = gp.OrthoTransform(dim, 0, np.zeros(dim), lam, np.eye(dim).reshape(-1))
+    cal = gp.CalibrationTable.calibrate(dev, t, data, 0.1, 32, 20000, 3)
+    dade = gp.DadeStrategy(t, cal, 32, dev=dev)
+    write_transform(tmp_path / "t.dade", t)
+    rt = ref_lib.load_transform(tmp_path / "t.dade")
+    cap = 1 << 24
+    dev.set_estimate_dump(cap)
+    try:
+        monkeypatch.setenv("DADE_GPU_DEBUG", "1")
+        idx.search_batch(qs[:64], 100, 6, dade)
+        (q, ids, dims, part, est), n = dev.estimate_dump(cap)
+        assert 0 < n <= cap and len(q) == n
+        # every pair of the first checkpoint is evaluated exactly in debug mode
+        assert np.count_nonzero(dims == cal.checkpoints[0]) > 64 * 1000
+        monkeypatch.delenv("DADE_GPU_DEBUG")
+        idx.search_batch(qs[:64], 100, 6, dade)
+        (_, _, dims2, _, _), n2 = dev.estimate_dump(cap)
+        assert 0 < n2 < n  # the production path evaluates only the filter's survivors
+    finally:
+        dev.set_estimate_dump(0)
+    g = np.random.default_rng(1)
+    for e in g.choice(n, 4000, replace=False):
+        o, qq, d = data[ids[e]], qs[q[e]], int(dims[e])
+        p = np.float32(oracle_lib.partial_sqdist(o, qq, 0, d))
+        assert bits(part[e]) == bits(p), (e, part[e], p)
+        assert est[e] == rt.dade_estimate(float(p), d)
+
+
+@pytest.mark.parametrize("dim", [256, 960])
+def test_rotation_bit_exact_large(gp, dev, oracle_lib, ref_lib, dim, tmp_path):
+    from paper_2411_17229_b200.io import write_transform
+    g = np.random.default_rng(dim)
+    q_, _ = np.linalg.qr(g.standard_normal((dim, dim)))
+    mat = np.ascontiguousarray(q_.T).reshape(-1)
+    raw = (g.standard_normal((300, dim)) * 3).astype(np.float32)
+    t = gp.OrthoTransform(dim, 0, np.zeros(dim), np.linspace(3, 0.1, dim), mat)
+    got = t.apply(dev, raw)
+    assert np.array_equal(bits(got), bits(oracle_lib.apply_transform(mat, raw)))
+    write_transform(tmp_path / "t.dade", t)
+    assert np.array_equal(bits(got), bits(ref_lib.load_transform(tmp_path / "t.dade").apply(raw)))
