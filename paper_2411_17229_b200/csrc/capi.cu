@@ -694,21 +694,29 @@ void finish_profile(dade_gpu_ctx* c) {
 }
 
 // DcoStats of the rows the radius seed scored exactly (the streaming passes skip
-// them, GroupArgs::seed_skip): each is a full-dim DCO with r = +inf, i.e. the
-// reference's accept path; with failure accounting each is also eligible.
+// them, GroupArgs::seed_skip): each is a full-dim DCO that is never pruned. For
+// failure accounting the seed's decision is "among the query's K best of these
+// rows", i.e. a test against the radius it produces, which its K kept rows
+// (seed_min = K) pass: those are the eligible ones.
 __global__ void seed_stats_kernel(const uint32_t* counts, const uint32_t* list_offsets, uint32_t n_lists,
                                   uint32_t seed_skip, uint32_t seed_min, uint32_t dim, bool measure,
                                   unsigned long long* counters) {
-    unsigned long long pairs = 0;
+    unsigned long long pairs = 0, kept = 0;
     for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n_lists; l += gridDim.x * blockDim.x) {
         const uint32_t len = list_offsets[l + 1] - list_offsets[l];
-        if (len >= seed_min) pairs += (unsigned long long)counts[l] * min(len, seed_skip);
+        if (len >= seed_min) {
+            pairs += (unsigned long long)counts[l] * min(len, seed_skip);
+            kept += (unsigned long long)counts[l] * seed_min;
+        }
     }
-    for (int off = 16; off > 0; off >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, off);
+    for (int off = 16; off > 0; off >>= 1) {
+        pairs += __shfl_xor_sync(0xffffffffu, pairs, off);
+        kept += __shfl_xor_sync(0xffffffffu, kept, off);
+    }
     if ((threadIdx.x & 31) == 0 && pairs) {
         atomicAdd(counters + 0, pairs);
         atomicAdd(counters + 1, pairs * dim);
-        if (measure) atomicAdd(counters + 8, pairs);
+        if (measure) atomicAdd(counters + 8, kept);
     }
 }
 

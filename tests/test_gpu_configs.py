@@ -102,41 +102,62 @@ def test_cfg0_dade_recall_and_exact_distances(gp, oracle_lib, cfg0):
     assert st.dim_fraction(c["dim"]) < 0.6
 
 
-def test_cfg0_failure_pass(gp, cfg0, monkeypatch):
+def test_cfg0_failure_pass(gp, cfg0, ref_lib, monkeypatch, tmp_path):
     """measure()'s untimed pass (proj/src/bench.cpp:65-73): eligible = DCOs whose
     exact distance is within the radius they were tested against, failures =
-    those the estimator pruned. FD and unbounded DADE never fail; calibrated
-    DADE's rate is the reference's within 0.03 (our thresholds are batched, so
-    not the same sequence of radii) and under the union bound sum(p_s)."""
+    those the estimator pruned. FD and unbounded DADE never fail; with the
+    calibrated table the reference has no failure at config 0 and ours stays
+    within 0.01 of it; with a deliberately aggressive table (every epsilon
+    -0.03: the reference fails 7.7% of its eligible DCOs) both fail, at rates
+    within 0.10 of each other. The rates are not the reference's exactly
+    because the radii each DCO is tested against differ: the reference's heap
+    threshold shrinks candidate by candidate, ours is set per batch pass (the
+    tcgen05 path: the seed's K-th distance over each nearest list, then the
+    merged top-K; the all-SIMT scan re-scans the seeded rows against the seed
+    radius and fails more, ~14%). Both paths are measured."""
+    from oracle import Oracle
+    from paper_2411_17229_b200.io import Divf, write_divf, write_transform
     fx, c, dev = cfg0["fx"], cfg0["c"], cfg0["dev"]
     idx, q = cfg0["idx"], cfg0["q"]
     fd = gp.FdScanningStrategy(c["dim"])
     st = gp.DcoStats(measure_failures=True)
     gi, gd, gc = idx.search_batch(q, c["k"], c["nprobe"], fd, st)
     assert st.failures == 0 and st.eligible >= gc.sum()
+    assert st.total_dco == int(fx[f"fd_np{c['nprobe']}_stats"][0])
     unb = gp.DadeStrategy(cfg0["t"], gp.CalibrationTable.unbounded(c["dim"], c["delta_d"]), c["delta_d"], dev=dev)
     st = gp.DcoStats(measure_failures=True)
     idx.search_batch(q, c["k"], c["nprobe"], unb, st)
     assert st.failures == 0 and st.eligible > 0
-    dade = gp.DadeStrategy(cfg0["t"], cfg0["cal"], c["delta_d"], dev=dev)
     ref = fx["dade_failure_stats"]
     ref_rate = float(ref[3]) / float(ref[2])
-    rates = []
+    loose = gp.CalibrationTable(cfg0["cal"].p_s, cfg0["cal"].delta_d, cfg0["cal"].checkpoints,
+                                [-0.03] * len(cfg0["cal"].epsilons))
+    # the reference on the same artifacts with the loose table, first 300 queries
+    write_transform(tmp_path / "t.dade", cfg0["t"])
+    write_divf(tmp_path / "i.ivf", Divf(c["dim"], c["n"], c["nlist"], 0, c["dim"], fx["centroids"], fx["offsets"],
+                                        fx["ids"], cfg0["base"][fx["ids"].astype(np.int64)].reshape(-1)))
+    rt = ref_lib.load_transform(tmp_path / "t.dade")
+    rivf = ref_lib.ivf_load(tmp_path / "i.ivf")
+    rloose = ref_lib.strategy_dade(rt, ref_lib.cal_from(loose.p_s, loose.delta_d, loose.checkpoints,
+                                                        loose.epsilons), c["delta_d"])
+    rs = rivf.failure_pass(rloose, q[:300], c["k"], c["nprobe"])
+    ref_loose = float(rs[3]) / float(rs[2])
+    assert rs[3] > 0
     for env in (None, "1"):  # the tcgen05 streaming path, then the all-SIMT scan
         if env:
             monkeypatch.setenv("DADE_GPU_NO_UMMA", env)
+        dade = gp.DadeStrategy(cfg0["t"], cfg0["cal"], c["delta_d"], dev=dev)
         st = gp.DcoStats(measure_failures=True)
         gi2, _, gc2 = idx.search_batch(q, c["k"], c["nprobe"], dade, st)
-        assert 0 < st.failures <= st.eligible
-        rates.append(st.failure_rate())
+        assert st.failures <= st.eligible and st.failure_rate() <= ref_rate + 0.01, (env, st)
         # the failure pass returns the search's results as well (recall unchanged)
-        from oracle import Oracle
         assert Oracle().recall(gi2, gc2, fx["gt"]) >= Oracle().recall(
             fx[f"dade_np{c['nprobe']}_ids"], fx[f"dade_np{c['nprobe']}_counts"], fx["gt"]) - RECALL_SLACK
-    n_ckpt = len(cfg0["cal"].checkpoints)
-    for r in rates:
-        assert abs(r - ref_rate) <= 0.03, (rates, ref_rate)
-        assert r <= n_ckpt * c["p_s"]
+        dl = gp.DadeStrategy(cfg0["t"], loose, c["delta_d"], dev=dev)
+        st = gp.DcoStats(measure_failures=True)
+        idx.search_batch(q[:300], c["k"], c["nprobe"], dl, st)
+        assert st.failures > 0
+        assert abs(st.failure_rate() - ref_loose) <= 0.10, (env, st.failure_rate(), ref_loose)
 
 
 def test_cfg0_ground_truth_gpu(gp, cfg0):
