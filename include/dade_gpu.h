@@ -258,8 +258,8 @@ int dade_gpu_covariance(dade_gpu_ctx* ctx, const float* data, uint32_t n, uint32
  * seeding on the reference's mt19937_64 stream, Lloyd iterations with its
  * early stop and empty-cluster re-seeding; centroids [n_clusters x dim],
  * assignments [n] and the iteration count equal the reference's. Drops any IVF
- * index uploaded to the context. Pointers: device if DEVICE_PTRS, else host;
- * nullable outputs are skipped. */
+ * index uploaded to the context. data: device if DEVICE_PTRS, else host;
+ * outputs: host or device memory (nullable ones are skipped). */
 int dade_gpu_kmeans(dade_gpu_ctx* ctx, const float* data, uint32_t n, uint32_t dim, uint32_t n_clusters,
                     uint32_t max_iters, uint64_t seed, uint32_t flags, float* centroids,
                     uint32_t* assignments, uint32_t* iterations);
@@ -301,6 +301,15 @@ int dade_gpu_last_filter_profile(dade_gpu_ctx* ctx, double* filter_ms, int* n_la
  * the (row, query, dim) triples it summed exactly. Requires profiling; 0 when
  * that kernel did not run. */
 int dade_gpu_last_seed_profile(dade_gpu_ctx* ctx, double* seed_ms, double* pair_dims);
+/* B_union of the last profiled streaming search: the bytes any
+ * scan making the same decisions must read at least -- per base row, 4 x the
+ * most dims any of its (query, row) pairs used (d0 for every row of a probed
+ * list, dim for the seeded rows, the survivors' prune / full dims) -- and the
+ * rows touched. With dade_gpu_last_scan_profile's scan_bytes (B_read: the
+ * slice bytes the kernels loaded, seed rows and survivor chunks included, plus
+ * list metadata) this gives the over-fetch B_read / B_union. 0 unless the
+ * search ran the streaming path with profiling on. */
+int dade_gpu_last_union_profile(dade_gpu_ctx* ctx, double* b_union, double* rows);
 
 #ifdef __cplusplus
 }

@@ -193,6 +193,19 @@ class Oracle:
         return [int(x) for x in cps[:n]], [float(x) for x in eps[:n]]
 
 
+def read_fvecs(path) -> np.ndarray:
+    """fvecs records (proj/docs/FILE_FORMATS.md; read_fvecs, proj/src/dataset_io.cpp)."""
+    raw = np.fromfile(path, "<i4")
+    d = int(raw[0])
+    return raw.reshape(-1, d + 1)[:, 1:].view("<f4").copy()
+
+
+def read_ivecs(path) -> np.ndarray:
+    raw = np.fromfile(path, "<i4")
+    d = int(raw[0])
+    return raw.reshape(-1, d + 1)[:, 1:].copy()
+
+
 class RefError(RuntimeError):
     pass
 
@@ -274,6 +287,11 @@ class RefLib:
         h = P()
         self._chk(self.L.dref_transform_load(str(path).encode(), C.byref(h)))
         return RefTransform(self, h)
+
+    def cal_load(self, path):
+        h = P()
+        self._chk(self.L.dref_cal_load(str(path).encode(), C.byref(h)))
+        return RefCal(self, h)
 
     def cal_from(self, p_s, delta_d, cps, eps):
         c, e = _u32(cps), _f64(eps)

@@ -89,6 +89,12 @@ class Device:
         check(_capi.lib.dade_gpu_last_seed_profile(self.h, C.byref(ms), C.byref(pd)))
         return ms.value, pd.value
 
+    def last_union_profile(self):
+        """(B_union bytes, rows touched) of the last profiled streaming search."""
+        a, b = C.c_double(), C.c_double()
+        check(_capi.lib.dade_gpu_last_union_profile(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def last_scan_profile(self):
         a, b, c = C.c_double(), C.c_double(), C.c_double()
         check(_capi.lib.dade_gpu_last_scan_profile(self.h, C.byref(a), C.byref(b), C.byref(c)))

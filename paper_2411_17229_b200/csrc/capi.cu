@@ -432,6 +432,9 @@ struct dade_gpu_ctx {
     bool seed_profiled = false;
     double last_seed_ms = 0, last_seed_pair_dims = 0;
     DevBuf seed_census;  // pair-dims the seed scored (profiling)
+    DevBuf row_dims, union_out;  // B_union census of the last streaming search (profiling)
+    bool union_valid = false;
+    double last_union_bytes = 0, last_union_rows = 0;
     int n_filter_passes = 0;
     // DADE_GPU_TIMELINE=1: labelled events on both streams, printed per search (diagnostic)
     std::vector<std::pair<const char*, cudaEvent_t>> tl;
@@ -669,6 +672,14 @@ void record(dade_gpu_ctx* c, cudaEvent_t e) {
 
 void finish_profile(dade_gpu_ctx* c) {
     if (!c->profiling) return;
+    c->last_union_bytes = c->last_union_rows = 0;
+    if (c->union_valid) {
+        unsigned long long u[2] = {0, 0};
+        cuda_check(cudaMemcpy(u, c->union_out.p, 16, cudaMemcpyDeviceToHost), "D2H union");
+        c->last_union_bytes = (double)u[0];
+        c->last_union_rows = (double)u[1];
+        c->union_valid = false;
+    }
     cuda_check(cudaEventSynchronize(c->e3), "event sync");
     float ms = 0;
     cuda_check(cudaEventElapsedTime(&ms, c->e1, c->e2), "elapsed");
@@ -698,25 +709,61 @@ void finish_profile(dade_gpu_ctx* c) {
 // failure accounting the seed's decision is "among the query's K best of these
 // rows", i.e. a test against the radius it produces, which its K kept rows
 // (seed_min = K) pass: those are the eligible ones.
+// With group_bytes (the seed kernels other than the TMA one), B_read gets each
+// group's (kSeedGroup queries of one list) rows once.
 __global__ void seed_stats_kernel(const uint32_t* counts, const uint32_t* list_offsets, uint32_t n_lists,
                                   uint32_t seed_skip, uint32_t seed_min, uint32_t dim, bool measure,
-                                  unsigned long long* counters) {
-    unsigned long long pairs = 0, kept = 0;
+                                  bool group_bytes, unsigned long long* counters) {
+    unsigned long long pairs = 0, kept = 0, bytes = 0;
     for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n_lists; l += gridDim.x * blockDim.x) {
         const uint32_t len = list_offsets[l + 1] - list_offsets[l];
         if (len >= seed_min) {
             pairs += (unsigned long long)counts[l] * min(len, seed_skip);
             kept += (unsigned long long)counts[l] * seed_min;
+            bytes += 4ull * dim * min(len, seed_skip) * ((counts[l] + kSeedGroup - 1) / kSeedGroup);
         }
     }
     for (int off = 16; off > 0; off >>= 1) {
         pairs += __shfl_xor_sync(0xffffffffu, pairs, off);
         kept += __shfl_xor_sync(0xffffffffu, kept, off);
+        bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
     }
     if ((threadIdx.x & 31) == 0 && pairs) {
         atomicAdd(counters + 0, pairs);
         atomicAdd(counters + 1, pairs * dim);
+        if (group_bytes) atomicAdd(counters + 2, bytes);
         if (measure) atomicAdd(counters + 8, kept);
+    }
+}
+
+// B_union ("oracle lower bound"): the bytes any scan making this
+// search's decisions must read at least -- per row, the most dims any of its
+// pairs reached: d0 (the first slice) for every row of a probed list, dim for
+// the rows the seed scored exactly, and the survivors' prune / full dims
+// (row_dims). One CTA per list; out[0] += bytes, out[1] += rows touched.
+__global__ void union_census_kernel(const uint32_t* counts, uint32_t n_rb, uint32_t n_lists,
+                                    const uint32_t* list_offsets, uint32_t seed_skip, uint32_t seed_min, uint32_t d0,
+                                    uint32_t dim, const uint32_t* row_dims, unsigned long long* out) {
+    const uint32_t l = blockIdx.x;
+    bool probed = false;
+    for (uint32_t rb = 0; rb < n_rb; ++rb) probed = probed || counts[rb * n_lists + l] > 0;
+    const uint32_t b = list_offsets[l], len = list_offsets[l + 1] - b;
+    const uint32_t seeded = (seed_skip && counts[l] > 0 && len >= seed_min) ? min(len, seed_skip) : 0u;
+    unsigned long long bytes = 0, rows = 0;
+    for (uint32_t r = threadIdx.x; r < len; r += blockDim.x) {
+        uint32_t v = probed ? d0 : 0u;
+        if (r < seeded) v = dim;
+        v = max(v, row_dims[b + r]);
+        bytes += 4ull * v;
+        rows += v ? 1 : 0;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
+        rows += __shfl_xor_sync(0xffffffffu, rows, off);
+    }
+    if ((threadIdx.x & 31) == 0 && bytes) {
+        atomicAdd(out, bytes);
+        atomicAdd(out + 1, rows);
     }
 }
 
@@ -785,9 +832,16 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             cuda_check(cudaMemsetAsync(c->surv_max.p, 0, 4, s), "memset");
             cuda_check(cudaMemsetAsync(out_count, 0, (size_t)nq * 4, s), "memset");
         }
+        const bool census = c->profiling && g;  // B_union census (profiled searches only)
+        bool seed_tma_ran = false;
+        if (census && !resume) {
+            c->row_dims.ensure((size_t)std::max<uint32_t>(n_rows, 1) * 4);
+            cuda_check(cudaMemsetAsync(c->row_dims.p, 0, (size_t)std::max<uint32_t>(n_rows, 1) * 4, s), "memset");
+        }
         if (seed.on && !resume) {
             const CUtensorMap* stm =
                 (g && k <= 128 && seed_tma_ok(a.dim, k)) ? c->seed_tm.get(rows, n_rows, a.dim) : nullptr;
+            seed_tma_ran = stm != nullptr;
             if (stm) {
                 SeedListArgs sa{};
                 sa.counts = g->counts;
@@ -807,6 +861,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 sa.out_keys = out_keys;
                 sa.out_count = out_count;
                 sa.nz2 = 0x8000000080000000ull;
+                sa.counters = a.counters;
                 c->seed_work.ensure(4);
                 c->seed_order.ensure(((size_t)nq / kSeedGroup + g->n_lists + 1) * 4);
                 sa.order = c->seed_order.as<uint32_t>();
@@ -834,7 +889,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             ++c->launches;
             if (a.counters && g) {
                 seed_stats_kernel<<<1, 256, 0, s>>>(g->counts, seed.offsets, g->n_lists, g->seed_skip, g->seed_min,
-                                                    a.dim, c->measure, a.counters);
+                                                    a.dim, c->measure, !seed_tma_ran, a.counters);
                 cuda_check(cudaGetLastError(), "seed stats");
                 ++c->launches;
             }
@@ -960,6 +1015,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             sv.counters = a.counters;
             sv.surv_max = c->surv_max.as<uint32_t>();
             sv.measure = c->measure ? 1u : 0u;
+            if (census) sv.row_dims = c->row_dims.as<uint32_t>();
             if (c->dump_cap) sv.dump = {c->dump_entries.as<uint4>(), c->dump_count.as<uint32_t>(), c->dump_cap};
             cuda_check(launch_advance_survivors(sv, cap, s), "advance survivors");
             // survivors / candidates of passes 0, 1 (low words of counters[4 + 2 pass ..]); of pass 2 in
@@ -982,6 +1038,16 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                        "merge slots");
             if (pass + 1 == n_pass && !stop && c->fo.ids) c->fo.done = true;
             c->launches += 3;
+            if (census && pass + 1 == n_pass && !stop) {
+                c->union_out.ensure(16);
+                cuda_check(cudaMemsetAsync(c->union_out.p, 0, 16, s), "memset");
+                union_census_kernel<<<g->n_lists, 256, 0, s>>>(g->counts, g->n_rb, g->n_lists, seed.offsets,
+                                                               g->seed_skip, g->seed_min, d0, a.dim,
+                                                               c->row_dims.as<uint32_t>(),
+                                                               c->union_out.as<unsigned long long>());
+                cuda_check(cudaGetLastError(), "union census");
+                c->union_valid = true;
+            }
             tl_mark(c, "pass", s);
         }
     }
@@ -2527,6 +2593,14 @@ int dade_gpu_last_seed_profile(dade_gpu_ctx* c, double* seed_ms, double* pair_di
     });
 }
 
+int dade_gpu_last_union_profile(dade_gpu_ctx* c, double* b_union, double* rows) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (b_union) *b_union = c->last_union_bytes;
+        if (rows) *rows = c->last_union_rows;
+    });
+}
+
 int dade_gpu_last_scan_profile(dade_gpu_ctx* c, double* scan_ms, double* scan_bytes, double* total_ms) {
     return guarded([&] {
         if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
@@ -2705,7 +2779,7 @@ int dade_gpu_kmeans(dade_gpu_ctx* c, const float* data, uint32_t n, uint32_t dim
             d_x = bx.as<float>();
         }
         const uint32_t it = kmeans_device(c, d_x, n, dim, n_clusters, max_iters, seed, assign);
-        const cudaMemcpyKind kind = (flags & DADE_GPU_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        const cudaMemcpyKind kind = cudaMemcpyDefault;  // outputs: host or device memory (unified addressing)
         if (centroids)
             cuda_check(cudaMemcpyAsync(centroids, c->centroids.p, (size_t)n_clusters * dim * 4, kind, s), "copy");
         if (assignments) cuda_check(cudaMemcpyAsync(assignments, assign.p, (size_t)n * 4, kind, s), "copy");
@@ -2760,7 +2834,7 @@ int dade_gpu_ivf_build(dade_gpu_ctx* c, const float* data, uint32_t n, uint32_t 
         c->norms_storage.rows = nullptr;
         c->aug_storage.rows = nullptr;
         c->has_ivf = true;
-        const cudaMemcpyKind kind = (flags & DADE_GPU_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        const cudaMemcpyKind kind = cudaMemcpyDefault;  // outputs: host or device memory (unified addressing)
         if (centroids)
             cuda_check(cudaMemcpyAsync(centroids, c->centroids.p, (size_t)n_clusters * dim * 4, kind, s), "copy");
         if (offsets) cuda_check(cudaMemcpyAsync(offsets, c->offsets.p, ((size_t)n_clusters + 1) * 4, kind, s), "copy");

@@ -143,6 +143,7 @@ struct SurvArgs {
     uint32_t measure;             // failure accounting: a pruned pair is carried to the full dim, then
                                   //   counters[8] += exact <= r (eligible), counters[9] += eligible && pruned
     EstimateDump dump;            // nullable entries: every checkpoint partial the kernel evaluates
+    uint32_t* row_dims;           // nullable [rows]: max dims any pair of the row reached (B_union census)
 };
 cudaError_t launch_advance_survivors(const SurvArgs& a, uint32_t max_entries, cudaStream_t s);
 cudaError_t launch_merge_slots(const uint64_t* qslots, uint32_t qslot_cap, const uint32_t* q_count,
@@ -196,6 +197,7 @@ struct SeedListArgs {
     uint64_t nz2;                   // 0x8000000080000000 (sq_step2's opaque -0.0 pair)
     uint32_t* order;                // nullable scratch [groups]: persistent kernel's costliest-first group order
     unsigned long long* census;     // nullable: += rows x queries x dim of every group scored (profiling)
+    unsigned long long* counters;   // nullable: [2] += the rows' bytes each group loads (B_read)
 };
 bool seed_tma_ok(uint32_t dim, uint32_t K);
 // work: one zeroed-per-launch counter word (persistent variant); nullptr: one CTA per group

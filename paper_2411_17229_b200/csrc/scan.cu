@@ -1192,6 +1192,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
                         else live = false;
                     } else if (pr) {
                         dims += hi;
+                        if (a.row_dims) atomicMax(a.row_dims + row, hi);
                         if (a.measure) pruned = true;
                         else live = false;
                     }
@@ -1217,6 +1218,7 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
             }
         } else if (live) {
             dims += dim;
+            if (a.row_dims) atomicMax(a.row_dims + row, dim);
             const float key_d = __fsqrt_rn(x);
             if (!(key_d > r)) {
                 is_cand = true;
@@ -1259,7 +1261,10 @@ __global__ void __launch_bounds__(kSpWarps * 32, 3) advance_survivors_pipe_kerne
             dims += __shfl_xor_sync(0xffffffffu, dims, off);
             viol += __shfl_xor_sync(0xffffffffu, viol, off);
         }
-        if (lane == 0 && a.counters && dims) atomicAdd(a.counters + 1, dims);
+        if (lane == 0 && a.counters && dims) {
+            atomicAdd(a.counters + 1, dims);
+            atomicAdd(a.counters + 2, 4ull * dims);  // each pair's row chunks from dim 0 (B_read)
+        }
         if (lane == 0 && a.counters && viol) atomicAdd(a.counters + 3, viol);
         if (a.measure && a.counters) {
             for (int off = 16; off > 0; off >>= 1) {

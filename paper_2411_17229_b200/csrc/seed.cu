@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
             sd_mb_arrive(gfull + j);
             if (b >= n_groups) return;
             if (a.census) atomicAdd(a.census, (unsigned long long)G.n * G.ng * dim);
+            if (a.counters) atomicAdd(a.counters + 2, 4ull * G.n * dim);  // the group's rows, loaded once
             const uint32_t n_boxes = (uint32_t)sp_rsel(G.n);
             const uint32_t bytes = n_boxes * kSdBox * kSdSlice * 4;
             for (uint32_t k = 0; k < n_slices; ++k, ++sl) {

@@ -8,18 +8,16 @@ This is offline index building, outside every timed region.
 
 Data (BASELINE configs; paper datasets are not available here): each vector =
 center_c + R diag(sqrt(lambda)) z with z ~ N(0, I), component c uniform,
-lambda_i = i^-a normalised to trace D, R Haar-orthogonal, centers ~ N(0, s^2 I).
-Seeded synthetic stand-ins for DEEP/GIST shapes; torch is used only as the
-device-memory / GEMM plumbing of this offline build:
-  * PCA: fp64 covariance (1/N, centred) + eigh, columns by descending variance,
-    sign-oriented like proj/src/transform.cpp:40-56; base rotation with the
-    bit-exact fp64 rotation kernel of libdade_gpu.so.
-  * k-means: random-sample seeding (the reference seeds with k-means++,
-    proj/src/ivf.cpp:38-68 — sequential over N per centroid, too slow at 1M-10M)
-    then Lloyd iterations; posting lists ascending by id (ivf.cpp:163-191).
-  * calibration: dade_gpu_calibrate (the reference algorithm, bit-exact).
-  * ground truth: fp32 GEMM candidates re-ranked exactly in fp64 with
-    (d^2, id) order (compute_ground_truth, proj/src/dataset_io.cpp:101-135).
+lambda_i = i^-a normalised to trace D, R Haar-orthogonal, centers ~ N(0, s^2 I);
+seeded synthetic stand-ins for DEEP/GIST shapes, drawn with torch's device RNG.
+The build runs the reference's algorithms on the GPU (libdade_gpu.so):
+  * PCA: compute_covariance bit-identical (dade_gpu_covariance), fp64 eigh,
+    the reference's column order / orientation / clamp (api.fit_pca);
+    rotation with the bit-exact fp64 kernel (dade_gpu_rotate);
+  * calibration: calibrate, bit-exact (dade_gpu_calibrate);
+  * IVF lists: IvfIndex::build with k-means++ seeding, early stop and
+    empty-cluster re-seeding (dade_gpu_ivf_build): the reference's lists;
+  * ground truth: compute_ground_truth, exact (dade_gpu_ground_truth).
 """
 from __future__ import annotations
 
@@ -29,47 +27,12 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from pathlib import Path
+
 from . import _capi
-from .api import CalibrationTable, Device, OrthoTransform
-
-
-@dataclass(frozen=True)
-class Config:
-    name: str
-    n: int
-    dim: int
-    nq: int
-    n_comp: int
-    alpha: float
-    center_std: float
-    seed: int
-    qseed: int
-    nlist: int
-    nprobe: int
-    k: int
-    delta_d: int
-    p_s: float
-    kmeans_iters: int = 20
-    kmeans_seed: int = 2
-    cal_pairs: int = 100_000
-    cal_seed: int = 1
-    flat: bool = False
-
-    def describe(self) -> str:
-        if self.flat:
-            return (f"{self.name}: flat N={self.n} D={self.dim} nq={self.nq} K={self.k} "
-                    f"dd={self.delta_d} p_s={self.p_s}")
-        return (f"{self.name}: N={self.n} D={self.dim} nq={self.nq} nlist={self.nlist} "
-                f"nprobe={self.nprobe} K={self.k} dd={self.delta_d} p_s={self.p_s}")
-
-
-CONFIGS = {
-    "config0": Config("config0", 100_000, 128, 1_000, 64, 1.0, 4.0, 0, 1, 256, 16, 10, 16, 0.1),
-    "config1": Config("config1", 1_000_000, 256, 10_000, 1024, 1.2, 4.0, 10, 11, 1024, 32, 100, 32, 0.1),
-    "config2": Config("config2", 1_000_000, 960, 1_000, 512, 1.5, 2.0, 20, 21, 1024, 64, 20, 64, 0.05),
-    "config3": Config("config3", 10_000_000, 128, 100_000, 4096, 1.0, 4.0, 30, 31, 16384, 64, 100, 16, 0.1),
-    "config4": Config("config4", 2_000_000, 768, 4_096, 256, 1.3, 4.0, 40, 41, 0, 0, 10, 64, 0.1, flat=True),
-}
+from .api import CalibrationTable, Device, IvfIndex, OrthoTransform, compute_ground_truth
+from .api import fit_pca as api_fit_pca
+from .configs import ART_VERSION, CONFIGS, Config, artifact_dir  # noqa: F401
 
 
 def _spectrum(dim: int, alpha: float) -> torch.Tensor:
@@ -103,30 +66,6 @@ class Mixture:
         return out
 
 
-def fit_pca(x: torch.Tensor, chunk: int = 1 << 18) -> OrthoTransform:
-    n, d = x.shape
-    mean = torch.zeros(d, dtype=torch.float64, device=x.device)
-    for s in range(0, n, chunk):
-        mean += x[s:s + chunk].double().sum(0)
-    mean /= n
-    cov = torch.zeros(d, d, dtype=torch.float64, device=x.device)
-    for s in range(0, n, chunk):
-        c = x[s:s + chunk].double() - mean
-        cov += c.T @ c
-    cov /= n
-    evals, evecs = torch.linalg.eigh(cov.cpu())
-    evals = evals.flip(0).numpy().copy()
-    evecs = evecs.flip(1).numpy().copy()  # columns = directions, descending variance
-    for k in range(d):  # orient_column: first nonzero component positive
-        col = evecs[:, k]
-        nz = np.nonzero(col)[0]
-        if nz.size and col[nz[0]] < 0:
-            evecs[:, k] = -col
-    evals = np.where((evals < 0) & (evals > -1e-6), 0.0, evals)
-    matrix = np.ascontiguousarray(evecs.T).reshape(-1)  # column-major: column k contiguous
-    return OrthoTransform(d, 0, mean.cpu().numpy(), evals, matrix)
-
-
 def rotate_device(dev: Device, t: OrthoTransform, x: torch.Tensor, chunk: int = 1 << 18) -> torch.Tensor:
     """apply_transform on the device with the bit-exact fp64 kernel."""
     t.upload(dev)
@@ -139,86 +78,6 @@ def rotate_device(dev: Device, t: OrthoTransform, x: torch.Tensor, chunk: int = 
                                               _capi.DEVICE_PTRS))
     dev.synchronize()
     dev.set_stream(None)
-    return out
-
-
-@torch.no_grad()
-def kmeans(x: torch.Tensor, c: int, iters: int, seed: int, chunk: int = 1 << 16):
-    n, d = x.shape
-    g = torch.Generator(device="cpu").manual_seed(seed)
-    init = torch.randperm(n, generator=g)[:c].to(x.device)
-    cen = x[init].clone()
-    assign = torch.empty(n, dtype=torch.int64, device=x.device)
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        for it in range(iters + 1):
-            cn = (cen.double() ** 2).sum(1).float()
-            for s in range(0, n, chunk):
-                xs = x[s:s + chunk]
-                dist = cn[None, :] - 2.0 * (xs @ cen.T)
-                assign[s:s + chunk] = dist.argmin(1)
-            if it == iters:
-                break
-            sums = torch.zeros(c, d, dtype=torch.float64, device=x.device)
-            sums.index_add_(0, assign, x.double())
-            cnt = torch.bincount(assign, minlength=c)
-            keep = cnt > 0
-            cen[keep] = (sums[keep] / cnt[keep, None].double()).float()
-            if (~keep).any():  # re-seed empties from random points
-                empt = torch.nonzero(~keep).squeeze(1)
-                pick = torch.randint(0, n, (empt.numel(),), generator=g).to(x.device)
-                cen[empt] = x[pick]
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-    return cen, assign
-
-
-def build_lists(x: torch.Tensor, cen: torch.Tensor, assign: torch.Tensor):
-    n = x.shape[0]
-    key = assign * n + torch.arange(n, device=x.device)
-    order = torch.argsort(key)
-    counts = torch.bincount(assign, minlength=cen.shape[0])
-    offsets = torch.zeros(cen.shape[0] + 1, dtype=torch.int64, device=x.device)
-    offsets[1:] = torch.cumsum(counts, 0)
-    return order, offsets
-
-
-@torch.no_grad()
-def ground_truth(base: torch.Tensor, q: torch.Tensor, k: int, extra: int = 64, qchunk: int = 1024,
-                 bchunk: int = 1 << 18) -> np.ndarray:
-    """Exact top-k by (fp64 d^2, id): fp32 GEMM shortlist, fp64 re-rank."""
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    kk = min(k + extra, base.shape[0])
-    bn = (base.double() ** 2).sum(1).float()
-    out = np.zeros((q.shape[0], k), np.uint32)
-    try:
-        for s in range(0, q.shape[0], qchunk):
-            qs = q[s:s + qchunk]
-            best_d = best_i = None
-            for b in range(0, base.shape[0], bchunk):
-                bs = base[b:b + bchunk]
-                d = bn[None, b:b + bchunk] - 2.0 * (qs @ bs.T)
-                dv, di = torch.topk(d, min(kk, d.shape[1]), dim=1, largest=False)
-                di = di + b
-                if best_d is None:
-                    best_d, best_i = dv, di
-                else:
-                    cd = torch.cat([best_d, dv], 1)
-                    ci = torch.cat([best_i, di], 1)
-                    best_d, sel = torch.topk(cd, kk, dim=1, largest=False)
-                    best_i = torch.gather(ci, 1, sel)
-            cand = base[best_i]  # [m, kk, D]
-            d2 = ((cand.double() - qs.double()[:, None, :]) ** 2).sum(2)
-            # (d2, id) lexicographic
-            ids = best_i
-            order = torch.argsort(ids, dim=1)
-            d2, ids = torch.gather(d2, 1, order), torch.gather(ids, 1, order)
-            order = torch.argsort(d2, dim=1, stable=True)
-            out[s:s + qs.shape[0]] = torch.gather(ids, 1, order)[:, :k].cpu().numpy().astype(np.uint32)
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
     return out
 
 
@@ -238,13 +97,18 @@ class Artifacts:
 
 
 def build(cfg: Config, dev: Device, device: torch.device, with_gt: bool = True, nq: int | None = None,
-          log=print) -> Artifacts:
+          log=print, gt_queries: int | None = None) -> Artifacts:
+    """The workload's artifacts, built on the GPU with the reference's
+    arithmetic (api.fit_pca, CalibrationTable.calibrate, IvfIndex.build,
+    compute_ground_truth), so the reference CPU library given the same files
+    holds the index it would build itself. gt_queries: ground truth for the
+    first queries only (recall sample)."""
     import time
     t0 = time.time()
     mix = Mixture(cfg, device)
     base = mix.draw(cfg.n, cfg.seed + 1000)
     q_raw = mix.draw(nq or cfg.nq, cfg.qseed + 1000)
-    t = fit_pca(base)
+    t = api_fit_pca(dev, base)
     base_rot = rotate_device(dev, t, base)
     q_rot = rotate_device(dev, t, q_raw)
     del base
@@ -254,16 +118,65 @@ def build(cfg: Config, dev: Device, device: torch.device, with_gt: bool = True, 
     log(f"[build] calibration eps={['%.4f' % e for e in cal.epsilons]}")
     art = Artifacts(cfg, t, cal, base_rot, q_raw, q_rot)
     if not cfg.flat:
-        cen, assign = kmeans(base_rot, cfg.nlist, cfg.kmeans_iters, cfg.kmeans_seed)
-        order, offsets = build_lists(base_rot, cen, assign)
-        art.centroids = cen.cpu().numpy()
-        art.offsets = offsets.cpu().numpy().astype(np.uint32)
-        art.ids = order.cpu().numpy().astype(np.uint32)
-        art.storage = base_rot[order].cpu().numpy()
-        sizes = np.diff(art.offsets)
-        log(f"[build] kmeans {time.time() - t0:.1f}s lists min/mean/max {sizes.min()}/{sizes.mean():.0f}/{sizes.max()}")
+        idx = IvfIndex.build(dev, base_rot, cfg.nlist, cfg.kmeans_iters, cfg.kmeans_seed)
+        art.centroids, art.offsets, art.ids, art.storage = idx.centroids, idx.offsets, idx.ids, idx.storage
+        sizes = np.diff(art.offsets.astype(np.int64))
+        log(f"[build] k-means++ / Lloyd {time.time() - t0:.1f}s lists min/mean/max "
+            f"{sizes.min()}/{sizes.mean():.0f}/{sizes.max()}")
     if with_gt:
-        art.gt = ground_truth(base_rot, q_rot, cfg.k)
-        log(f"[build] ground truth {time.time() - t0:.1f}s")
+        m = q_rot.shape[0] if gt_queries is None else min(gt_queries, q_rot.shape[0])
+        art.gt = compute_ground_truth(dev, base_rot, q_rot[:m].contiguous(), cfg.k)
+        log(f"[build] ground truth ({m} queries) {time.time() - t0:.1f}s")
     torch.cuda.synchronize()
     return art
+
+
+# ---- on-disk artifacts in the reference's formats (shared by both bench arms) ------------
+def save(art: Artifacts, out: Path) -> None:
+    """t.dade, c.cal, index.ivf (or base.fvecs for the flat config), queries.fvecs
+    (raw), gt.ivecs: the files the reference's loaders read."""
+    from .io import Divf, write_cal, write_divf, write_fvecs, write_ivecs, write_transform
+    cfg = art.cfg
+    out.mkdir(parents=True, exist_ok=True)
+    tmp = out.with_name(out.name + ".part")
+    tmp.mkdir(parents=True, exist_ok=True)
+    write_transform(tmp / "t.dade", art.transform)
+    write_cal(tmp / "c.cal", art.cal)
+    if cfg.flat:
+        write_fvecs(tmp / "base.fvecs", art.base_rot.cpu().numpy())
+    else:
+        write_divf(tmp / "index.ivf", Divf(cfg.dim, cfg.n, cfg.nlist, 0, cfg.dim, art.centroids, art.offsets,
+                                           art.ids, art.storage.reshape(-1)))
+    write_fvecs(tmp / "queries.fvecs", art.q_raw.cpu().numpy())
+    if art.gt is not None:
+        write_ivecs(tmp / "gt.ivecs", art.gt.astype(np.int32))
+    for f in tmp.iterdir():
+        f.replace(out / f.name)
+    tmp.rmdir()
+    (out / "DONE").write_text(cfg.describe())
+
+
+def ensure_artifacts(cfg: Config, nq: int | None = None, gt_queries: int | None = None, log=print) -> Path:
+    """Build (in this process) and save the workload's artifacts once per box."""
+    out = artifact_dir(cfg, nq=nq)
+    if (out / "DONE").exists():
+        return out
+    dev = Device(0)
+    art = build(cfg, dev, torch.device("cuda:0"), with_gt=True, nq=nq, log=log, gt_queries=gt_queries)
+    save(art, out)
+    return out
+
+
+def main(argv=None):
+    import argparse
+    ap = argparse.ArgumentParser(description="build a BASELINE workload's artifacts in the reference formats")
+    ap.add_argument("--config", default="config1")
+    ap.add_argument("--nq", type=int, default=None)
+    ap.add_argument("--gt-queries", type=int, default=None)
+    a = ap.parse_args(argv)
+    import sys
+    print(ensure_artifacts(CONFIGS[a.config], a.nq, a.gt_queries, log=lambda *x: print(*x, file=sys.stderr)))
+
+
+if __name__ == "__main__":
+    main()

@@ -30,8 +30,27 @@ cfg = W.CONFIGS[args.config]
 dev = gp.Device(0)
 device = torch.device("cuda:0")
 t0 = time.time()
-art = W.build(cfg, dev, device, with_gt=True, nq=args.nq, log=lambda *a: print(*a, file=sys.stderr))
+art_dir = W.ensure_artifacts(cfg, nq=args.nq, gt_queries=bench.GT_SAMPLE, log=lambda *a: print(*a, file=sys.stderr))
 build_s = time.time() - t0
+from types import SimpleNamespace
+from paper_2411_17229_b200.io import read_cal, read_divf, read_fvecs, read_ivecs, read_transform
+art = SimpleNamespace(transform=read_transform(art_dir / "t.dade"), cal=read_cal(art_dir / "c.cal"),
+                      q_raw=torch.from_numpy(read_fvecs(art_dir / "queries.fvecs")).to(device),
+                      gt=read_ivecs(art_dir / "gt.ivecs").astype(np.uint32))
+if cfg.flat:
+    art.base_rot = torch.from_numpy(read_fvecs(art_dir / "base.fvecs"))
+else:
+    dv = read_divf(art_dir / "index.ivf")
+    art.centroids, art.offsets, art.ids, art.storage = dv.centroids, dv.offsets, dv.ids, dv.storage.reshape(cfg.n, cfg.dim)
+_recall = bench.recall
+
+
+def recall_gt(ids, cnt, gt):  # ground truth covers the first len(gt) queries
+    m = min(len(gt), ids.shape[0])
+    return _recall(ids[:m], cnt[:m], gt[:m])
+
+
+bench.recall = recall_gt
 dco = gp.DadeStrategy(art.transform, art.cal, cfg.delta_d, dev=dev)
 art.transform.upload(dev)
 nq, k = art.q_raw.shape[0], cfg.k
@@ -108,10 +127,8 @@ if not cfg.flat:
 
 # reference on a 1-thread sample of the same artifacts
 if args.ref_s > 0 and not cfg.flat:
-    tmp = Path(tempfile.mkdtemp(prefix="dade_cc_"))
-    ref, ivf, strat, _keep = bench.reference_setup(art, tmp)
-    q_rot = art.q_rot.cpu().numpy()
-    sidx, rids, rcnt, rst, sec = bench.reference_sample(ivf, strat, q_rot, cfg, 1, args.ref_s)
+    ref, ivf, strat, q_rot, _, _keep = bench.reference_load(art_dir, cfg)
+    sidx, rids, rcnt, rst, sec = bench.reference_sample(ivf, strat, q_rot, cfg, 1, args.ref_s, limit=len(art.gt))
     ids_np = ids_d.cpu().numpy().astype(np.uint32)
     cnt_np = cnt_d.cpu().numpy().astype(np.uint32)
     line["reference"] = {"queries_per_s_1thread": len(sidx) / sec, "sample": int(len(sidx)),
