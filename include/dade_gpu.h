@@ -28,6 +28,9 @@
  *   dade_gpu_partial_sums    partial_sqdist at every checkpoint
  *                                                       proj/src/estimator.cpp:74-82
  *   dade_gpu_calibrate       calibrate                  proj/src/calibration.cpp:109-146
+ *   dade_gpu_comm_create / dade_gpu_sharded_ivf_search / _flat_search
+ *                            IvfIndex::search / linear_scan over list / row shards,
+ *                            NCCL exchange
  *   dade_gpu_covariance      compute_covariance         proj/src/transform.cpp:68-95
  *   dade_gpu_kmeans          kmeans                     proj/src/ivf.cpp:24-143
  *   dade_gpu_ivf_build       IvfIndex::build            proj/src/ivf.cpp:145-192
@@ -91,6 +94,11 @@ int dade_gpu_destroy(dade_gpu_ctx* ctx);
 /* Work on a caller-owned cudaStream_t (NULL = the handle's own stream). */
 int dade_gpu_set_stream(dade_gpu_ctx* ctx, void* cuda_stream);
 int dade_gpu_synchronize(dade_gpu_ctx* ctx);
+/* The stream the handle's work runs on (its own, or the one set_stream gave). */
+int dade_gpu_get_stream(dade_gpu_ctx* ctx, void** cuda_stream);
+/* Dim of the uploaded IVF index / flat base (nullable outputs; CONFIG_ERROR when
+ * a requested one is absent). */
+int dade_gpu_index_dims(dade_gpu_ctx* ctx, uint32_t* ivf_dim, uint32_t* base_dim);
 
 /* Column-major f64 D x D matrix (column k = k-th direction) + nonincreasing
  * variances; the lambda prefix sums are derived exactly as on load
@@ -279,6 +287,41 @@ int dade_gpu_ivf_build(dade_gpu_ctx* ctx, const float* data, uint32_t n, uint32_
  * (k <= 2048). out_ids [nq x k]. Pointers: device if DEVICE_PTRS, else host. */
 int dade_gpu_ground_truth(dade_gpu_ctx* ctx, const float* base, uint32_t n, const float* queries, uint32_t nq,
                           uint32_t dim, uint32_t k, uint32_t flags, uint32_t* out_ids);
+
+/* ---- multi-GPU over NCCL (SURVEY.md §8b init_nccl / sharded_*, §8e) --------
+ * One process (or host thread) per GPU, one handle + one communicator each.
+ * libnccl is resolved at run time: the copy already in the process, else
+ * libnccl.so.2. Rank 0 creates the unique id, the host distributes it (MPI,
+ * torch.distributed, a file ...), every rank creates its communicator on its
+ * handle. */
+#define DADE_GPU_NCCL_ID_BYTES 128
+typedef struct dade_gpu_comm dade_gpu_comm;
+int dade_gpu_nccl_unique_id(uint8_t* id_out /* [DADE_GPU_NCCL_ID_BYTES] */);
+int dade_gpu_comm_create(dade_gpu_ctx* ctx, int nranks, int rank, const uint8_t* id, dade_gpu_comm** out);
+int dade_gpu_comm_destroy(dade_gpu_comm* comm);
+
+/* List-sharded IvfIndex::search, query-owner scheme: every rank's handle holds
+ * the replicated centroids + transform + strategy and its shard of the lists
+ * (dade_gpu_set_ivf + dade_gpu_set_ivf_shard); every rank passes its own nq
+ * queries (the same nq on all ranks) and receives their top-k, bit-identical
+ * in FD mode to an unsharded search. Steps: coarse ranking of the own queries,
+ * NCCL all-gather of rotated queries + probes, phase 1 (the shard owning a
+ * query's nearest list seeds it), NCCL all-reduce(MIN) of the per-query
+ * radius, phase 2 (the other local lists), NCCL send/recv of each query's
+ * per-shard top-k to its owner, device merge. Host buffers unless
+ * DEVICE_PTRS; QUERIES_RAW rotates first. stats: this rank's DcoStats. */
+int dade_gpu_sharded_ivf_search(dade_gpu_comm* comm, const float* queries, uint32_t nq, uint32_t k,
+                                uint32_t n_probe, uint32_t flags, uint32_t* out_ids, float* out_dists,
+                                uint32_t* out_counts, dade_gpu_stats* stats);
+
+/* Row-sharded linear_scan: every rank's handle holds a contiguous row block
+ * (dade_gpu_set_base with id_base = its first row); the same nq queries on
+ * every rank; every rank receives the global top-k. Radius seed per shard,
+ * NCCL all-reduce(MIN) of the radius, the streaming passes, NCCL all-gather
+ * of the key blocks, device merge. */
+int dade_gpu_sharded_flat_search(dade_gpu_comm* comm, const float* queries, uint32_t nq, uint32_t k,
+                                 uint32_t flags, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
+                                 dade_gpu_stats* stats);
 
 /* Number of CUDA kernels this handle launched so far (bench evidence). */
 uint64_t dade_gpu_launch_count(dade_gpu_ctx* ctx);

@@ -22,6 +22,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -399,6 +400,13 @@ public:
         return out;
     }
 
+    // Keep only the lists with mask[c] != 0 on this device (list sharding).
+    void shard(const std::vector<std::uint8_t>& mask) const {
+        if (mask.size() != n_clusters_) throw InvalidInput("IvfIndex::shard: one mask byte per list");
+        check(dade_gpu_set_ivf_shard(dev_->get(), mask.data()));
+    }
+    const Device& device() const { return *dev_; }
+
 private:
     explicit IvfIndex(const Device& d) : dev_(&d) {}
     const Device* dev_;
@@ -432,6 +440,57 @@ public:
 private:
     const Device* dev_;
     std::uint32_t dim_;
+};
+
+// One NCCL communicator per GPU (dade_gpu_comm) and the sharded searches over it:
+// IvfIndex::search over list shards (each rank its own queries) and linear_scan
+// over row shards (the same queries on every rank). Rank 0 makes the unique id,
+// the host hands it to every rank (MPI, a file, ...).
+class Communicator {
+public:
+    using Id = std::array<std::uint8_t, DADE_GPU_NCCL_ID_BYTES>;
+    static Id unique_id() {
+        Id id{};
+        check(dade_gpu_nccl_unique_id(id.data()));
+        return id;
+    }
+    Communicator(const Device& d, int nranks, int rank, const Id& id) : dev_(&d) {
+        check(dade_gpu_comm_create(d.get(), nranks, rank, id.data(), &comm_));
+    }
+    ~Communicator() {
+        if (comm_) dade_gpu_comm_destroy(comm_);
+    }
+    Communicator(const Communicator&) = delete;
+    Communicator& operator=(const Communicator&) = delete;
+
+    std::vector<SearchResult> ivf_search(const float* queries, std::uint32_t nq, std::uint32_t k, std::uint32_t n_probe,
+                                         const DcoStrategy& dco, DcoStats* stats = nullptr, bool raw = false) const {
+        dco.use(*dev_);
+        return run([&](std::uint32_t* i, float* d, std::uint32_t* c, dade_gpu_stats* st) {
+            return dade_gpu_sharded_ivf_search(comm_, queries, nq, k, n_probe, raw ? DADE_GPU_QUERIES_RAW : 0u, i, d, c, st);
+        }, nq, k, stats);
+    }
+    std::vector<SearchResult> flat_search(const float* queries, std::uint32_t nq, std::uint32_t k,
+                                          const DcoStrategy& dco, DcoStats* stats = nullptr, bool raw = false) const {
+        dco.use(*dev_);
+        return run([&](std::uint32_t* i, float* d, std::uint32_t* c, dade_gpu_stats* st) {
+            return dade_gpu_sharded_flat_search(comm_, queries, nq, k, raw ? DADE_GPU_QUERIES_RAW : 0u, i, d, c, st);
+        }, nq, k, stats);
+    }
+
+private:
+    template <class F>
+    std::vector<SearchResult> run(F&& f, std::uint32_t nq, std::uint32_t k, DcoStats* stats) const {
+        const std::uint32_t kk = k ? k : 1;
+        std::vector<std::uint32_t> ids(std::size_t(nq) * kk), cnt(nq);
+        std::vector<float> d(std::size_t(nq) * kk);
+        dade_gpu_stats st{};
+        check(f(ids.data(), d.data(), cnt.data(), &st));
+        if (stats) stats->add(st);
+        return detail::to_results(ids, d, cnt, nq, kk);
+    }
+    const Device* dev_;
+    dade_gpu_comm* comm_ = nullptr;
 };
 
 }  // namespace gpu

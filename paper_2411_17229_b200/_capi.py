@@ -89,6 +89,13 @@ def _load():
         "dade_gpu_last_seed_profile": ([P, P, P], I),
         "dade_gpu_set_estimate_dump": ([P, U32], I),
         "dade_gpu_last_union_profile": ([P, P, P], I),
+        "dade_gpu_get_stream": ([P, P], I),
+        "dade_gpu_index_dims": ([P, P, P], I),
+        "dade_gpu_nccl_unique_id": ([P], I),
+        "dade_gpu_comm_create": ([P, I, I, P, C.POINTER(P)], I),
+        "dade_gpu_comm_destroy": ([P], I),
+        "dade_gpu_sharded_ivf_search": ([P, P, U32, U32, U32, U32, P, P, P, P], I),
+        "dade_gpu_sharded_flat_search": ([P, P, U32, U32, U32, P, P, P, P], I),
         "dade_gpu_covariance": ([P, P, U32, U32, U32, P, P], I),
         "dade_gpu_kmeans": ([P, P, U32, U32, U32, U32, U64, U32, P, P, P], I),
         "dade_gpu_ivf_build": ([P, P, U32, U32, U32, U32, U64, U32, P, P, P, P], I),
@@ -117,7 +124,9 @@ EXPORTED = [
     "dade_gpu_set_profiling", "dade_gpu_last_scan_profile", "dade_gpu_debug_counters",
     "dade_gpu_last_filter_profile", "dade_gpu_last_seed_profile", "dade_gpu_debug_radius",
     "dade_gpu_set_estimate_dump", "dade_gpu_get_estimate_dump", "dade_gpu_covariance", "dade_gpu_kmeans",
-    "dade_gpu_ivf_build", "dade_gpu_ground_truth", "dade_gpu_last_union_profile",
+    "dade_gpu_ivf_build", "dade_gpu_ground_truth", "dade_gpu_last_union_profile", "dade_gpu_get_stream",
+    "dade_gpu_index_dims", "dade_gpu_nccl_unique_id", "dade_gpu_comm_create", "dade_gpu_comm_destroy",
+    "dade_gpu_sharded_ivf_search", "dade_gpu_sharded_flat_search",
 ]
 
 

@@ -24,7 +24,7 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
     "-Xptxas", "-v", "--expt-relaxed-constexpr", "-cudart", "static",
 ]
-SOURCES = ["scan.cu", "filter.cu", "umma.cu", "coarse.cu", "prep.cu", "seed.cu", "build.cu", "capi.cu"]
+SOURCES = ["scan.cu", "filter.cu", "umma.cu", "coarse.cu", "prep.cu", "seed.cu", "build.cu", "capi.cu", "comm.cu"]
 
 
 def _run(cmd, log=None):
@@ -55,7 +55,7 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
             _run([NVCC, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / s), "-o", str(o)],
                  log=objdir / (s + ".log"))
             objs.append(str(o))
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *objs])
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *objs, "-ldl"])
     cpp_test = ROOT / "tests" / "cpp" / "host_api_test.cpp"
     if cpp_test.exists():
         exe = ROOT / "build" / "host_api_test"

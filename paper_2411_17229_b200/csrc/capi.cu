@@ -333,6 +333,10 @@ struct TmapCache {
 
 }  // namespace
 
+namespace dade_gpu {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace dade_gpu
+
 struct dade_gpu_ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
@@ -1767,6 +1771,27 @@ int dade_gpu_set_stream(dade_gpu_ctx* c, void* stream) {
     return guarded([&] {
         if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
         c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    });
+}
+
+int dade_gpu_get_stream(dade_gpu_ctx* c, void** stream) {
+    return guarded([&] {
+        if (!c || !stream) fail(DADE_GPU_INVALID_INPUT, "get_stream: null argument");
+        *stream = c->stream;
+    });
+}
+
+int dade_gpu_index_dims(dade_gpu_ctx* c, uint32_t* ivf_dim, uint32_t* base_dim) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (ivf_dim) {
+            if (!c->has_ivf) fail(DADE_GPU_CONFIG_ERROR, "IvfIndex::search: no ivf index uploaded");
+            *ivf_dim = c->dim;
+        }
+        if (base_dim) {
+            if (!c->has_base) fail(DADE_GPU_CONFIG_ERROR, "linear_scan: no base vectors uploaded");
+            *base_dim = c->b_dim;
+        }
     });
 }
 

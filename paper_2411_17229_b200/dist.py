@@ -165,3 +165,69 @@ def sharded_ivf_search(dev, group, d_queries, nq: int, k: int, n_probe: int, raw
     counts = torch.empty((nq,), dtype=torch.int32, device=dev_t)
     merge_keys_device(dev, recv, nq, k, ids, dists, counts)
     return ids, dists, counts
+
+
+# ---- the same protocols through the C ABI's own NCCL layer (csrc/comm.cu) ---------------
+class NcclComm:
+    """dade_gpu_comm: an NCCL communicator owned by libdade_gpu on a Device, for
+    dade_gpu_sharded_ivf_search / _flat_search (the C++ host's multi-GPU entry
+    points). The unique id comes from rank 0 and is broadcast over `group`
+    (torch.distributed, any backend), or passed in (`uid`, 128 bytes)."""
+
+    def __init__(self, dev, world: int, rank: int, group=None, uid: bytes | None = None):
+        if uid is None:
+            buf = (C.c_uint8 * 128)()
+            if rank == 0:
+                _capi.check(_capi.lib.dade_gpu_nccl_unique_id(buf))
+            if world > 1:
+                import torch
+                import torch.distributed as dist
+                t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+                dist.broadcast(t, 0, group=group)
+                buf = (C.c_uint8 * 128)(*t.tolist())
+            uid = bytes(buf)
+        self.dev, self.world, self.rank = dev, world, rank
+        h = C.c_void_p()
+        idb = (C.c_uint8 * 128)(*uid)
+        _capi.check(_capi.lib.dade_gpu_comm_create(dev.h, world, rank, idb, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            _capi.lib.dade_gpu_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _run(self, fn, args, nq, k, queries, flags, stats):
+        import torch
+        dev_t = queries.device if hasattr(queries, "device") and queries.is_cuda else None
+        if dev_t is not None:
+            ids = torch.empty((nq, k), dtype=torch.int32, device=dev_t)
+            dists = torch.empty((nq, k), dtype=torch.float32, device=dev_t)
+            counts = torch.empty((nq,), dtype=torch.int32, device=dev_t)
+            flags |= _capi.DEVICE_PTRS
+        else:
+            queries = np.ascontiguousarray(queries, np.float32)
+            ids, dists, counts = (np.zeros((nq, k), np.uint32), np.zeros((nq, k), np.float32),
+                                  np.zeros(nq, np.uint32))
+        st = _capi.Stats()
+        _capi.check(fn(self.h, _capi.ptr(queries), *args, flags, _capi.ptr(ids), _capi.ptr(dists),
+                       _capi.ptr(counts), C.byref(st)))
+        if stats is not None:
+            stats._add(st)
+        return ids, dists, counts
+
+    def ivf_search(self, queries, nq: int, k: int, n_probe: int, raw: bool = False, stats=None):
+        """dade_gpu_sharded_ivf_search: this rank's nq queries (host or CUDA)."""
+        return self._run(_capi.lib.dade_gpu_sharded_ivf_search, (nq, k, n_probe), nq, k, queries,
+                         _capi.QUERIES_RAW if raw else 0, stats)
+
+    def flat_search(self, queries, nq: int, k: int, raw: bool = False, stats=None):
+        """dade_gpu_sharded_flat_search: the same nq queries on every rank."""
+        return self._run(_capi.lib.dade_gpu_sharded_flat_search, (nq, k), nq, k, queries,
+                         _capi.QUERIES_RAW if raw else 0, stats)

@@ -79,6 +79,20 @@ int main(int argc, char** argv) {
         report(same && sb.total_dco == 2 * st.total_dco, "pipelined batches == single searches (FD), stats summed");
     }
 
+    {  // the NCCL layer with one rank: every protocol step runs, results equal the plain search
+        const Communicator comm(dev, 1, 0, Communicator::unique_id());
+        DcoStats sc;
+        const auto rc = comm.ivf_search(qs.data(), nq, 10, 3, fd, &sc);
+        bool same = rc.size() == res.size();
+        for (std::uint32_t q = 0; same && q < nq; ++q) {
+            same = rc[q].neighbors.size() == res[q].neighbors.size();
+            for (std::size_t i = 0; same && i < res[q].neighbors.size(); ++i)
+                same = rc[q].neighbors[i].id == res[q].neighbors[i].id &&
+                       rc[q].neighbors[i].distance == res[q].neighbors[i].distance;
+        }
+        report(same && sc.total_dco == st.total_dco, "sharded_ivf_search (1 rank, NCCL) == IvfIndex::search (FD)");
+    }
+
     const DadeStrategy dade(dev, t, cal, cal.delta_d);
     DcoStats sd;
     const auto rd = idx.search(qs.data(), 10, 3, dade, &sd);
