@@ -610,9 +610,10 @@ def run_ours_multi(args, cfg):
     idx.shard((owner == rank).astype(np.uint8))
     dev.apply(dco)
     dev.set_stream(stream.cuda_stream)
-    nq_loc = (q_all.shape[0] + world - 1) // world
-    q_loc = q_all[rank * nq_loc:min(q_all.shape[0], (rank + 1) * nq_loc)].contiguous()
-    nq_loc = q_loc.shape[0]
+    if q_all.shape[0] % world:
+        raise SystemExit(f"{q_all.shape[0]} queries do not split evenly over {world} ranks")
+    nq_loc = q_all.shape[0] // world  # strong scaling: the job's queries split over the ranks
+    q_loc = q_all[rank * nq_loc:(rank + 1) * nq_loc].contiguous()
 
     def step():
         return gdist.sharded_ivf_search(dev, None, q_loc, nq_loc, cfg.k, cfg.nprobe, raw=True)

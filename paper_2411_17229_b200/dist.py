@@ -205,7 +205,7 @@ class NcclComm:
 
     def _run(self, fn, args, nq, k, queries, flags, stats):
         import torch
-        dev_t = queries.device if hasattr(queries, "device") and queries.is_cuda else None
+        dev_t = queries.device if getattr(queries, "is_cuda", False) else None
         if dev_t is not None:
             ids = torch.empty((nq, k), dtype=torch.int32, device=dev_t)
             dists = torch.empty((nq, k), dtype=torch.float32, device=dev_t)
