@@ -78,28 +78,61 @@ __global__ void __launch_bounds__(kCovT * kCovT) covariance_kernel(const float* 
 // ---- k-means++ seeding (ivf.cpp:38-68) -----------------------------------------
 
 // l2_sq_double of rows [i0, i0 + 128) against one centroid, staged through
-// shared memory in 64-dim chunks (coalesced loads; each thread keeps its row's
-// sequential k order), then dist2[i] = min(dist2[i], d2) and the block's partial
-// sum of the updated dist2 (any order: the pick bounds its rounding).
-constexpr int kPpRows = 128, kPpChunk = 64;
+// shared memory in 64-dim chunks (16-byte loads, all in flight at once; each
+// thread then keeps its row's sequential k order), then dist2[i] = min(dist2[i],
+// d2) and the block's partial sum of the updated dist2 (any order: the pick
+// bounds its rounding).
+constexpr int kPpRows = 128, kPpChunk = 64, kPpPitch = kPpChunk + 1;
 __global__ void __launch_bounds__(kPpRows) kmpp_update_kernel(const float* __restrict__ x, uint32_t n, uint32_t dim,
                                                               const float* __restrict__ last, double* dist2,
                                                               double* block_sums) {
-    __shared__ float tile[kPpRows][kPpChunk + 1];
+    __shared__ float tile[kPpRows * kPpPitch];
+    __shared__ double lastc[kPpChunk];
     __shared__ double red[kPpRows / 32];
     const uint32_t i0 = blockIdx.x * kPpRows, t = threadIdx.x, i = i0 + t;
+    const bool vec = (dim & 3u) == 0;
     double acc = 0.0;
     for (uint32_t k0 = 0; k0 < dim; k0 += kPpChunk) {
         const uint32_t w = min((uint32_t)kPpChunk, dim - k0);
         __syncthreads();
-        for (uint32_t e = t; e < kPpRows * (uint32_t)kPpChunk; e += kPpRows) {
-            const uint32_t rr = e / kPpChunk, kk = e % kPpChunk;
-            tile[rr][kk] = (i0 + rr < n && kk < w) ? __ldg(x + (size_t)(i0 + rr) * dim + k0 + kk) : 0.f;
+        if (vec) {
+            constexpr int kV = kPpRows * kPpChunk / 4 / kPpRows;  // float4 per thread
+            float4 v[kV];
+#pragma unroll
+            for (int j = 0; j < kV; ++j) {
+                const uint32_t e = t + j * kPpRows, rr = e / (kPpChunk / 4), c4 = e % (kPpChunk / 4);
+                v[j] = (i0 + rr < n && 4 * c4 < w) ? __ldg(reinterpret_cast<const float4*>(x + (size_t)(i0 + rr) * dim + k0) + c4)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < kV; ++j) {
+                const uint32_t e = t + j * kPpRows, rr = e / (kPpChunk / 4), c4 = e % (kPpChunk / 4);
+                float* d = tile + rr * kPpPitch + 4 * c4;
+                d[0] = v[j].x;
+                d[1] = v[j].y;
+                d[2] = v[j].z;
+                d[3] = v[j].w;
+            }
+        } else {
+            for (uint32_t e = t; e < kPpRows * (uint32_t)kPpChunk; e += kPpRows) {
+                const uint32_t rr = e / kPpChunk, kk = e % kPpChunk;
+                tile[rr * kPpPitch + kk] = (i0 + rr < n && kk < w) ? __ldg(x + (size_t)(i0 + rr) * dim + k0 + kk) : 0.f;
+            }
         }
+        if (t < kPpChunk) lastc[t] = t < w ? (double)__ldg(last + k0 + t) : 0.0;
         __syncthreads();
-        for (uint32_t kk = 0; kk < w; ++kk) {
-            const double d = __dsub_rn((double)tile[t][kk], (double)__ldg(last + k0 + kk));
-            acc = __dadd_rn(acc, __dmul_rn(d, d));
+        const float* row = tile + t * kPpPitch;
+        if (w == (uint32_t)kPpChunk) {
+#pragma unroll 16
+            for (uint32_t kk = 0; kk < (uint32_t)kPpChunk; ++kk) {
+                const double d = __dsub_rn((double)row[kk], lastc[kk]);
+                acc = __dadd_rn(acc, __dmul_rn(d, d));
+            }
+        } else {
+            for (uint32_t kk = 0; kk < w; ++kk) {
+                const double d = __dsub_rn((double)row[kk], lastc[kk]);
+                acc = __dadd_rn(acc, __dmul_rn(d, d));
+            }
         }
     }
     double v = 0.0;
@@ -143,6 +176,7 @@ __device__ __forceinline__ uint64_t km_bounded(const uint64_t* raw, uint32_t* rn
 // when P_i <= lo. If the first index past `hi` has its predecessor <= lo the
 // pick is decided; otherwise (probability ~1e-4 per pick) thread 0 redoes the
 // reference's two sequential loops exactly.
+constexpr int kPickStage = 4096;  // doubles staged per round of the exact fallback
 __global__ void __launch_bounds__(1024) kmpp_pick_kernel(const float* __restrict__ x, uint32_t n, uint32_t dim,
                                                          const double* __restrict__ dist2,
                                                          const double* __restrict__ block_sums, uint32_t n_blocks,
@@ -150,7 +184,8 @@ __global__ void __launch_bounds__(1024) kmpp_pick_kernel(const float* __restrict
                                                          float* centroid_out, uint32_t* picks, uint32_t c,
                                                          uint32_t* err) {
     __shared__ double s_pref[1024];  // inclusive prefix of per-thread block-range sums
-    __shared__ uint32_t s_pick, s_mode;
+    __shared__ double s_stage[kPickStage];
+    __shared__ uint32_t s_pick, s_mode, s_first;
     __shared__ double s_lo, s_hi, s_base, s_u;
     __shared__ uint32_t s_blk;
     const uint32_t t = threadIdx.x;
@@ -160,6 +195,7 @@ __global__ void __launch_bounds__(1024) kmpp_pick_kernel(const float* __restrict
     double s = 0.0;
     for (uint32_t b = b0; b < b1; ++b) s = __dadd_rn(s, block_sums[b]);
     s_pref[t] = s;
+    if (t == 0) s_first = 1024;
     __syncthreads();
     for (uint32_t off = 1; off < 1024; off <<= 1) {
         const double v = t >= off ? s_pref[t - off] : 0.0;
@@ -189,59 +225,87 @@ __global__ void __launch_bounds__(1024) kmpp_pick_kernel(const float* __restrict
     }
     __syncthreads();
     if (s_mode == 1) {
-        // first thread range whose inclusive prefix exceeds hi, then its first block
-        if (t == 0) {
-            const double hi = s_hi;
-            uint32_t tt = 0;
-            while (tt < 1024 && !(s_pref[tt] > hi)) ++tt;
-            if (tt == 1024) {
-                s_mode = 3;  // nothing certainly past the target: exact fallback
-            } else {
+        // the first thread range whose inclusive prefix exceeds hi (parallel), its blocks and
+        // then the rows of the block that crosses it (staged, scanned by thread 0)
+        const double hi = s_hi;
+        // (the tree prefixes need not be monotone in fp: the smallest such t; any choice is
+        // verified below)
+        if (s_pref[t] > hi && (t == 0 || !(s_pref[t - 1] > hi))) atomicMin(&s_first, t);
+        __syncthreads();
+        const uint32_t tt = s_first;
+        if (tt == 1024) {
+            if (t == 0) s_mode = 3;  // nothing certainly past the target: exact fallback
+        } else {
+            const uint32_t bb0 = min(n_blocks, tt * per), bb1 = min(n_blocks, bb0 + per);
+            if (t < bb1 - bb0) s_stage[t] = block_sums[bb0 + t];
+            __syncthreads();
+            if (t == 0) {
                 double run = tt ? s_pref[tt - 1] : 0.0;
-                const uint32_t bb0 = min(n_blocks, tt * per), bb1 = min(n_blocks, bb0 + per);
                 uint32_t b = bb0;
                 for (; b < bb1; ++b) {
-                    const double nr = __dadd_rn(run, block_sums[b]);
+                    const double nr = __dadd_rn(run, s_stage[b - bb0]);
                     if (nr > hi) break;
                     run = nr;
                 }
                 s_blk = b;
                 s_base = run;  // prefix before block b
             }
-        }
-        __syncthreads();
-        if (s_mode == 1 && t == 0) {
-            // inside block s_blk: the first row whose prefix exceeds hi
-            const double lo = s_lo, hi = s_hi;
-            double run = s_base;
+            __syncthreads();
             const uint32_t r0 = s_blk * kPpRows, r1 = min(n, r0 + kPpRows);
-            uint32_t i = r0;
-            double prev = run;
-            for (; i < r1; ++i) {
-                prev = run;
-                run = __dadd_rn(run, dist2[i]);
-                if (run > hi) break;
+            if (r0 + t < r1) s_stage[t] = dist2[r0 + t];
+            __syncthreads();
+            if (t == 0) {
+                const double lo = s_lo;
+                double run = s_base, prev = run;
+                uint32_t i = r0;
+                for (; i < r1; ++i) {
+                    prev = run;
+                    run = __dadd_rn(run, s_stage[i - r0]);
+                    if (run > hi) break;
+                }
+                if (i < r1 && prev <= lo) s_pick = i;
+                else s_mode = 3;
             }
-            if (i < r1 && prev <= lo) s_pick = i;
-            else s_mode = 3;
         }
         __syncthreads();
     }
-    if (s_mode == 3 && t == 0) {
-        // exact: the reference's loops (ivf.cpp:47-61), sequentially
+    if (s_mode == 3) {
+        // exact: the reference's two loops (ivf.cpp:47-61), sequentially, the values
+        // staged through shared memory by the whole CTA
         double total = 0.0;
-        for (uint32_t i = 0; i < n; ++i) total = __dadd_rn(total, dist2[i]);
-        const double target = __dmul_rn(s_u, total);
+        for (uint32_t base = 0; base < n; base += kPickStage) {
+            const uint32_t m = min((uint32_t)kPickStage, n - base);
+            __syncthreads();
+            for (uint32_t e = t; e < m; e += blockDim.x) s_stage[e] = dist2[base + e];
+            __syncthreads();
+            if (t == 0)
+                for (uint32_t e = 0; e < m; ++e) total = __dadd_rn(total, s_stage[e]);
+        }
+        __shared__ double s_target;
+        __shared__ uint32_t s_done;
+        if (t == 0) {
+            s_target = __dmul_rn(s_u, total);
+            s_done = 0;
+            s_pick = n - 1;
+        }
         double run = 0.0;
-        uint32_t pick = n - 1;
-        for (uint32_t i = 0; i < n; ++i) {
-            run = __dadd_rn(run, dist2[i]);
-            if (run > target) {
-                pick = i;
-                break;
+        for (uint32_t base = 0; base < n; base += kPickStage) {
+            const uint32_t m = min((uint32_t)kPickStage, n - base);
+            __syncthreads();
+            if (s_done) break;
+            for (uint32_t e = t; e < m; e += blockDim.x) s_stage[e] = dist2[base + e];
+            __syncthreads();
+            if (t == 0) {
+                for (uint32_t e = 0; e < m; ++e) {
+                    run = __dadd_rn(run, s_stage[e]);
+                    if (run > s_target) {
+                        s_pick = base + e;
+                        s_done = 1;
+                        break;
+                    }
+                }
             }
         }
-        s_pick = pick;
     }
     __syncthreads();
     const uint32_t pick = s_pick;

@@ -391,6 +391,7 @@ struct dade_gpu_ctx {
     DevBuf seg_keys, seg_count, r_global, out_keys, out_count, out_ids, out_dists, out_counts, seed_keys, seed_count;
     DevBuf surv, surv_count, cand_q, cand_key, cand_count, q_count, q_off, q_cursor, bucket, surv_max, item_counter, seed_goff, seed_glist;
     DevBuf cnorm, qnorm, coarse_lo, coarse_overflow, q_norms, coarse_gmin;  // coarse_lo: p~ per (query, centroid)
+    DevBuf coarse_cand, coarse_cnt, coarse_t0;  // fused large-nlist selection
     bool coarse_force_exact = false, coarse_tc_used = false;
     int n_sms = 148;
     uint32_t surv_cap_hint = 0;
@@ -497,12 +498,16 @@ void set_tables(dade_gpu_ctx* c, uint32_t kind, uint32_t dim, std::vector<uint32
 bool coarse_tc_ok(dade_gpu_ctx* c, uint32_t n_probe) {
     return n_probe <= 256 && !c->coarse_force_exact;
 }
-// queries per coarse chunk: the p~ buffer holds chunk x n_clusters fp32 (<= 1 GB).
-// Large chunks keep the selection (a warp per query) at full occupancy: with
-// 2048-query chunks at nlist 16384 it ran at 21% achieved occupancy.
+// Above 1024 centroids the selection is fused with the GEMM (two tcgen05 passes:
+// group minima, then the candidates lo <= T0; p~ never reaches memory).
+constexpr uint32_t kCoarseFusedMin = 1024;
+constexpr uint32_t kCoarseCandCap = 512;  // candidates per query of the fused selection
+bool coarse_fused(const dade_gpu_ctx* c) { return c->n_clusters > kCoarseFusedMin && c->n_clusters <= 32768; }
+// queries per coarse chunk: the p~ buffer holds chunk x n_clusters fp32 (<= 1 GB);
+// the fused path's candidate lists chunk x 512 x 8 B.
 uint32_t coarse_tc_chunk(dade_gpu_ctx* c, uint32_t nq) {
-    return (uint32_t)std::max<uint64_t>(64, std::min<uint64_t>(std::max<uint32_t>(nq, 1),
-                                                               (1ull << 30) / (4ull * c->n_clusters)));
+    const uint64_t per_q = coarse_fused(c) ? 8ull * kCoarseCandCap : 4ull * c->n_clusters;
+    return (uint32_t)std::max<uint64_t>(64, std::min<uint64_t>(std::max<uint32_t>(nq, 1), (1ull << 30) / per_q));
 }
 // buffers for queries [0, nq) in chunks of coarse_tc_chunk(); overflow flag reset
 void coarse_tc_begin(dade_gpu_ctx* c, uint32_t nq, uint32_t n_probe) {
@@ -511,7 +516,13 @@ void coarse_tc_begin(dade_gpu_ctx* c, uint32_t nq, uint32_t n_probe) {
     c->probe_count.ensure((size_t)std::max<uint32_t>(nq, 1) * 4);
     c->cnorm.ensure((size_t)c->n_clusters * 4);
     c->qnorm.ensure((size_t)chunk * 4);
-    c->coarse_lo.ensure((size_t)chunk * c->n_clusters * 4);
+    if (coarse_fused(c)) {
+        c->coarse_cand.ensure((size_t)chunk * kCoarseCandCap * 8);
+        c->coarse_cnt.ensure((size_t)chunk * 4);
+        c->coarse_t0.ensure((size_t)chunk * 4);
+    } else {
+        c->coarse_lo.ensure((size_t)chunk * c->n_clusters * 4);
+    }
     c->coarse_overflow.ensure(8);  // [0] overflow flag, [1] candidate census (DADE_GPU_COARSE_CENSUS)
     cuda_check(cudaMemsetAsync(c->coarse_overflow.p, 0, 8, c->stream), "memset");
     c->coarse_tc_used = true;
@@ -532,13 +543,33 @@ void coarse_tc_range(dade_gpu_ctx* c, const float* d_q, uint32_t q0, uint32_t m,
         cuda_check(launch_coarse_norms(c->centroids.as<float>(), c->n_clusters, qc, m, c->dim, c->cnorm.as<float>(),
                                        c->qnorm.as<float>(), s),
                    "coarse norms");
-        // nlist > 1024: the GEMM epilogue also leaves the per-32-centroid minima of the
-        // upper bounds, the selection's first pass
-        uint32_t* gmin = nullptr;
-        if (c->n_clusters > 1024 && c->n_clusters <= 16384) {
-            c->coarse_gmin.ensure((size_t)coarse_tc_chunk(c, m) * ((c->n_clusters + 31) / 32) * 4);
-            gmin = c->coarse_gmin.as<uint32_t>();
+        if (coarse_fused(c)) {
+            // pass A: group minima of the upper bounds -> T0 per query; pass B: the same GEMM,
+            // candidates lo <= T0 listed per query; then B, exact l2_sq, (d^2, id) sort
+            c->coarse_gmin.ensure((size_t)m * ((c->n_clusters + 31) / 32) * 4);
+            uint32_t* gmin = c->coarse_gmin.as<uint32_t>();
+            cuda_check(launch_coarse_umma(*tmc, *tmq, q0, c->n_clusters, m, c->dim, c->cnorm.as<float>(),
+                                          c->qnorm.as<float>(), nullptr, s, gmin),
+                       "coarse gemm pass A (tcgen05)");
+            cuda_check(launch_coarse_t0(gmin, c->n_clusters, m, n_probe, c->coarse_t0.as<uint32_t>(), s), "coarse t0");
+            cuda_check(cudaMemsetAsync(c->coarse_cnt.p, 0, (size_t)m * 4, s), "memset");
+            CoarseFilter cf;
+            cf.t0 = c->coarse_t0.as<uint32_t>();
+            cf.cand = c->coarse_cand.as<uint64_t>();
+            cf.cnt = c->coarse_cnt.as<uint32_t>();
+            cf.cap = kCoarseCandCap;
+            cuda_check(launch_coarse_umma(*tmc, *tmq, q0, c->n_clusters, m, c->dim, c->cnorm.as<float>(),
+                                          c->qnorm.as<float>(), nullptr, s, nullptr, cf),
+                       "coarse gemm pass B (tcgen05)");
+            cuda_check(launch_coarse_finish(cf.cand, cf.cnt, cf.cap, c->cnorm.as<float>(), c->qnorm.as<float>(),
+                                            c->centroids.as<float>(), qc, m, c->dim, n_probe,
+                                            c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
+                                            c->coarse_overflow.as<uint32_t>(), s),
+                       "coarse finish");
+            c->launches += 5;
+            return;
         }
+        uint32_t* gmin = nullptr;
         cuda_check(launch_coarse_umma(*tmc, *tmq, q0, c->n_clusters, m, c->dim, c->cnorm.as<float>(),
                                       c->qnorm.as<float>(), c->coarse_lo.as<float>(), s, gmin),
                    "coarse gemm (tcgen05)");

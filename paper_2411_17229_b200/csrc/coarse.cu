@@ -458,6 +458,100 @@ __device__ __forceinline__ uint32_t warp_select_smem(const uint32_t* v, uint32_t
     return prefix;
 }
 
+// From the candidates (p~ bits << 32 | centroid, lower bound <= some T >= B) of
+// one query in shared memory: B = n_probe-th smallest upper bound among them,
+// keep lower bound <= B, exact sequential l2_sq, (acc, id) bitonic sort, first
+// n_probe -> probes. Warp-wide; hist / hv / rs / qs are this warp's scratch.
+__device__ void finish_from_candidates(uint64_t* cand, uint32_t n, const float* __restrict__ cnorm, float qn,
+                                       const float* __restrict__ cen, const float* __restrict__ qr, uint32_t dim,
+                                       uint32_t n_probe, uint64_t* __restrict__ probes_row, uint32_t* hist,
+                                       uint32_t* hv, float* rs, float* qs, int lane) {
+    __syncwarp();
+    for (uint32_t e = lane; e < n; e += 32) {
+        const uint64_t v = cand[e];
+        const uint32_t c = (uint32_t)v;
+        hv[e] = fkey(__fadd_rn(__uint_as_float((uint32_t)(v >> 32)), coarse_delta(cnorm[c], qn)));
+    }
+    __syncwarp();
+    const uint32_t B = warp_select_smem(hv, n, n_probe, hist, lane);
+    // candidates lo <= B, compacted in place (ids)
+    uint32_t m2 = 0;
+    for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        uint32_t c = 0;
+        bool is = false;
+        if (e < n) {
+            const uint64_t v = cand[e];
+            c = (uint32_t)v;
+            is = fkey(__fsub_rn(__uint_as_float((uint32_t)(v >> 32)), coarse_delta(cnorm[c], qn))) <= B;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, is);
+        __syncwarp();
+        if (is) cand[m2 + __popc(bal & ((1u << lane) - 1u))] = c;
+        m2 += __popc(bal);
+        __syncwarp();
+    }
+    n = m2;
+    __syncwarp();
+    // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43) of the candidates
+    for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const uint32_t my_c = e < n ? (uint32_t)cand[e] : 0u;
+        const uint32_t nv = min(32u, n - e0);
+        float acc = 0.f;
+        for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
+            const uint32_t w = min(32u, dim - k0);
+            const uint32_t sub = lane >> 3, c4 = lane & 7;
+            float4 v[8];
+#pragma unroll
+            for (int sg = 0; sg < 8; ++sg) {
+                const uint32_t sidx = 4 * sg + sub;
+                const uint32_t cc = __shfl_sync(0xffffffffu, my_c, sidx);
+                v[sg] = (sidx < nv && 4 * c4 < w) ? __ldg(reinterpret_cast<const float4*>(cen + (size_t)cc * dim + k0) + c4)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const float4 qv = (lane < 8 && 4u * lane < w) ? __ldg(reinterpret_cast<const float4*>(qr + k0) + lane)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            __syncwarp();
+#pragma unroll
+            for (int sg = 0; sg < 8; ++sg)
+                *reinterpret_cast<float4*>(rs + (4 * sg + sub) * kFsRS + 4 * c4) = v[sg];
+            if (lane < 8) *reinterpret_cast<float4*>(qs + 4 * lane) = qv;
+            __syncwarp();
+            if (e < n) {
+                const float* os = rs + lane * kFsRS;
+                for (uint32_t kk = 0; kk < w; kk += 4) {
+                    const float4 o4 = *reinterpret_cast<const float4*>(os + kk);
+                    const float4 q4 = *reinterpret_cast<const float4*>(qs + kk);
+                    acc = sq_step(acc, q4.x, o4.x);
+                    acc = sq_step(acc, q4.y, o4.y);
+                    acc = sq_step(acc, q4.z, o4.z);
+                    acc = sq_step(acc, q4.w, o4.w);
+                }
+            }
+        }
+        __syncwarp();
+        if (e < n) cand[e] = make_key(acc, my_c);
+    }
+    __syncwarp();
+    uint32_t m = 1;
+    while (m < n) m <<= 1;
+    for (uint32_t e = n + lane; e < m; e += 32) cand[e] = ~0ull;
+    __syncwarp();
+    uint64_t* kk = cand;
+    for (uint32_t size = 2; size <= m; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = lane; i < m / 2; i += 32) {
+                const uint32_t lo_i = 2 * i - (i & (stride - 1)), hi_i = lo_i + stride;
+                const bool up = (lo_i & size) == 0;
+                const uint64_t x = kk[lo_i], y = kk[hi_i];
+                if ((x > y) == up) { kk[lo_i] = y; kk[hi_i] = x; }
+            }
+            __syncwarp();
+        }
+    for (uint32_t i = lane; i < n_probe; i += 32) probes_row[i] = kk[i];
+}
+
 __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
     const float* __restrict__ pt, const float* __restrict__ cnorm, const float* __restrict__ qnorm,
     const float* __restrict__ cen, uint32_t n_cen, const float* __restrict__ q, uint32_t nq, uint32_t dim,
@@ -547,92 +641,81 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
         return;
     }
     __syncwarp();
-    for (uint32_t e = lane; e < n; e += 32) {
-        const uint64_t v = cand[warp][e];
-        const uint32_t c = (uint32_t)v;
-        hv[e] = fkey(__fadd_rn(__uint_as_float((uint32_t)(v >> 32)), coarse_delta(cnorm[c], qn)));
-    }
-    __syncwarp();
-    const uint32_t B = warp_select_smem(hv, n, n_probe, hist, lane);
-    // candidates lo <= B, compacted in place (ids)
-    uint32_t m2 = 0;
-    for (uint32_t e0 = 0; e0 < n; e0 += 32) {
-        const uint32_t e = e0 + lane;
-        uint32_t c = 0;
-        bool is = false;
-        if (e < n) {
-            const uint64_t v = cand[warp][e];
-            c = (uint32_t)v;
-            is = fkey(__fsub_rn(__uint_as_float((uint32_t)(v >> 32)), coarse_delta(cnorm[c], qn))) <= B;
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, is);
-        __syncwarp();
-        if (is) cand[warp][m2 + __popc(bal & ((1u << lane) - 1u))] = c;
-        m2 += __popc(bal);
-        __syncwarp();
-    }
-    n = m2;
-    __syncwarp();
-    // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43) of the candidates
-    const float* qr = q + (size_t)qi * dim;
-    float* rs = rows[warp];
-    float* qs = qch[warp];
-    for (uint32_t e0 = 0; e0 < n; e0 += 32) {
-        const uint32_t e = e0 + lane;
-        const uint32_t my_c = e < n ? (uint32_t)cand[warp][e] : 0u;
-        const uint32_t nv = min(32u, n - e0);
-        float acc = 0.f;
-        for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
-            const uint32_t w = min(32u, dim - k0);
-            const uint32_t sub = lane >> 3, c4 = lane & 7;
-            float4 v[8];
+    finish_from_candidates(cand[warp], n, cnorm, qn, cen, q + (size_t)qi * dim, dim, n_probe,
+                           probes + (size_t)qi * n_probe, hist, hv, rows[warp], qch[warp], lane);
+}
+
+// ---- fused large-nlist selection (p~ never in memory) -------------------------------
+// coarse_umma pass A leaves per query the minimum upper-bound key of every 32
+// centroids (gmin); T0 = the n_probe-th smallest of those minima >= B (they are
+// n_probe distinct upper bounds). Pass B (the GEMM again) lists every centroid
+// with lower bound <= T0 -- every exact top-n_probe centroid is among them --
+// and coarse_finish_kernel ends as coarse_select_wide_kernel does.
+__global__ void __launch_bounds__(kFsWarps * 32) coarse_t0_kernel(const uint32_t* __restrict__ gmin, uint32_t n_cen,
+                                                                  uint32_t nq, uint32_t n_probe, uint32_t* t0) {
+    __shared__ uint32_t hist[kFsWarps][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t qi = blockIdx.x * kFsWarps + warp;
+    if (qi >= nq) return;
+    const uint32_t ng = (n_cen + 31) / 32;
+    const uint32_t* gr = gmin + (size_t)qi * ng;
+    uint32_t gm[32];
 #pragma unroll
-            for (int sg = 0; sg < 8; ++sg) {
-                const uint32_t sidx = 4 * sg + sub;
-                const uint32_t cc = __shfl_sync(0xffffffffu, my_c, sidx);
-                v[sg] = (sidx < nv && 4 * c4 < w) ? __ldg(reinterpret_cast<const float4*>(cen + (size_t)cc * dim + k0) + c4)
-                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            const float4 qv = (lane < 8 && 4u * lane < w) ? __ldg(reinterpret_cast<const float4*>(qr + k0) + lane)
-                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t i = lane + 32u * j;
+        gm[j] = i < ng ? gr[i] : 0xffffffffu;
+    }
+    uint32_t kmin = 0xffffffffu, kmax = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        kmin = min(kmin, gm[j]);
+        if (gm[j] != 0xffffffffu) kmax = max(kmax, gm[j]);
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    uint32_t T0 = kmin;
+    if (kmax > kmin) {
+        const int top = (31 - __clz(kmin ^ kmax)) & ~7;
+        uint32_t mask = top >= 24 ? 0u : ~0u << (top + 8), rem = n_probe;
+        T0 = kmin & mask;
+        for (int shift = top; shift >= 0; shift -= 8) {
+            for (uint32_t j = lane; j < 256; j += 32) hist[warp][j] = 0;
             __syncwarp();
 #pragma unroll
-            for (int sg = 0; sg < 8; ++sg)
-                *reinterpret_cast<float4*>(rs + (4 * sg + sub) * kFsRS + 4 * c4) = v[sg];
-            if (lane < 8) *reinterpret_cast<float4*>(qs + 4 * lane) = qv;
+            for (int j = 0; j < 32; ++j)
+                if ((gm[j] & mask) == T0) atomicAdd(&hist[warp][(gm[j] >> shift) & 0xffu], 1u);
             __syncwarp();
-            if (e < n) {
-                const float* os = rs + lane * kFsRS;
-                for (uint32_t kk = 0; kk < w; kk += 4) {
-                    const float4 o4 = *reinterpret_cast<const float4*>(os + kk);
-                    const float4 q4 = *reinterpret_cast<const float4*>(qs + kk);
-                    acc = sq_step(acc, q4.x, o4.x);
-                    acc = sq_step(acc, q4.y, o4.y);
-                    acc = sq_step(acc, q4.z, o4.z);
-                    acc = sq_step(acc, q4.w, o4.w);
-                }
-            }
+            uint32_t d, before;
+            warp_hist_find(hist[warp], rem, lane, d, before);
+            rem -= before;
+            T0 |= d << shift;
+            mask |= 0xffu << shift;
+            __syncwarp();
         }
-        __syncwarp();
-        if (e < n) cand[warp][e] = make_key(acc, my_c);
     }
-    __syncwarp();
-    uint32_t m = 1;
-    while (m < n) m <<= 1;
-    for (uint32_t e = n + lane; e < m; e += 32) cand[warp][e] = ~0ull;
-    __syncwarp();
-    uint64_t* kk = cand[warp];
-    for (uint32_t size = 2; size <= m; size <<= 1)
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (uint32_t i = lane; i < m / 2; i += 32) {
-                const uint32_t lo_i = 2 * i - (i & (stride - 1)), hi_i = lo_i + stride;
-                const bool up = (lo_i & size) == 0;
-                const uint64_t x = kk[lo_i], y = kk[hi_i];
-                if ((x > y) == up) { kk[lo_i] = y; kk[hi_i] = x; }
-            }
-            __syncwarp();
-        }
-    for (uint32_t i = lane; i < n_probe; i += 32) probes[(size_t)qi * n_probe + i] = kk[i];
+    if (lane == 0) t0[qi] = T0;
+}
+
+__global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_finish_kernel(
+    const uint64_t* __restrict__ cand_g, const uint32_t* __restrict__ cnt, uint32_t cap,
+    const float* __restrict__ cnorm, const float* __restrict__ qnorm, const float* __restrict__ cen,
+    const float* __restrict__ q, uint32_t nq, uint32_t dim, uint32_t n_probe, uint64_t* __restrict__ probes,
+    uint32_t* __restrict__ overflow) {
+    __shared__ uint64_t cand[kFsWarps][kSelCap];
+    __shared__ __align__(16) float rows[kFsWarps][32 * kFsRS];
+    __shared__ __align__(16) float qch[kFsWarps][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t qi = blockIdx.x * kFsWarps + warp;
+    if (qi >= nq) return;
+    const uint32_t n = cnt[qi];
+    if (n > cap || n > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
+        if (lane == 0) atomicAdd(overflow, 1u);
+        return;
+    }
+    for (uint32_t e = lane; e < n; e += 32) cand[warp][e] = cand_g[(size_t)qi * cap + e];
+    uint32_t* hist = reinterpret_cast<uint32_t*>(rows[warp]);
+    finish_from_candidates(cand[warp], n, cnorm, qnorm[qi], cen, q + (size_t)qi * dim, dim, n_probe,
+                           probes + (size_t)qi * n_probe, hist, hist + 256, rows[warp], qch[warp], lane);
 }
 
 // the select kernel for n_cen centroids
@@ -686,6 +769,23 @@ cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const f
                                  const uint32_t* gmin) {
     if (nq == 0) return cudaSuccess;
     launch_select_any(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, s, gmin);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coarse_t0(const uint32_t* gmin, uint32_t n_cen, uint32_t nq, uint32_t n_probe, uint32_t* t0,
+                             cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    if ((n_cen + 31) / 32 > 1024) return cudaErrorInvalidValue;
+    coarse_t0_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(gmin, n_cen, nq, n_probe, t0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coarse_finish(const uint64_t* cand, const uint32_t* cnt, uint32_t cap, const float* cnorm,
+                                 const float* qnorm, const float* centroids, const float* queries, uint32_t nq,
+                                 uint32_t dim, uint32_t n_probe, uint64_t* probes, uint32_t* overflow, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    coarse_finish_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
+        cand, cnt, cap, cnorm, qnorm, centroids, queries, nq, dim, n_probe, probes, overflow);
     return cudaGetLastError();
 }
 

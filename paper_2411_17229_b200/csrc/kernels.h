@@ -92,9 +92,24 @@ cudaError_t launch_filter_umma(const FilterArgs& a, const CUtensorMap& tmap128, 
 // tcgen05 coarse GEMM: p~ [nq][n_cen] for queries [q0, q0 + nq) of the tm_q map (box {32, 256})
 // gmin (nullable) [nq][ceil(n_cen / 32)]: per query, the minimum coarse upper-bound key (fkey(p~ + delta))
 // of every 32 consecutive centroids (coarse_select_wide_kernel's group minima)
+// pass B of the fused large-nlist coarse selection: append (p~ bits << 32 | centroid) of every
+// pair with lower bound <= t0[q] to cand[q][0..cap), counts in cnt[q] (may exceed cap)
+struct CoarseFilter {
+    const uint32_t* t0 = nullptr;  // [nq] (chunk-relative), nullptr: pass A / p~ mode
+    uint64_t* cand = nullptr;      // [nq][cap]
+    uint32_t* cnt = nullptr;       // [nq], zeroed before the launch
+    uint32_t cap = 0;
+};
 cudaError_t launch_coarse_umma(const CUtensorMap& tm_cen, const CUtensorMap& tm_q, uint32_t q0, uint32_t n_cen,
                                uint32_t nq, uint32_t dim, const float* cnorm, const float* qnorm, float* p_out,
-                               cudaStream_t s, uint32_t* gmin = nullptr);
+                               cudaStream_t s, uint32_t* gmin = nullptr, const CoarseFilter& cf = CoarseFilter{});
+// the fused large-nlist selection around it (coarse.cu): T0 per query from the GEMM's group
+// minima, then (after pass B) B, the exact l2_sq of the candidates and the (d^2, id) sort
+cudaError_t launch_coarse_t0(const uint32_t* gmin, uint32_t n_cen, uint32_t nq, uint32_t n_probe, uint32_t* t0,
+                             cudaStream_t s);
+cudaError_t launch_coarse_finish(const uint64_t* cand, const uint32_t* cnt, uint32_t cap, const float* cnorm,
+                                 const float* qnorm, const float* centroids, const float* queries, uint32_t nq,
+                                 uint32_t dim, uint32_t n_probe, uint64_t* probes, uint32_t* overflow, cudaStream_t s);
 // coarse.cu pieces around it
 cudaError_t launch_coarse_norms(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
                                 float* cnorm, float* qnorm, cudaStream_t s);

@@ -572,10 +572,15 @@ namespace {
 constexpr int kCgM = 128, kCgN = 256, kCgStages = 2;  // 2 stages: 2 CTAs per SM, one in its epilogue while the other loads
 constexpr int kCgThreads = 160;
 
+// Fused-selection modes (CoarseFilter, large nlist): pass A writes only the
+// group minima (p_out == nullptr), pass B (t0 != nullptr) recomputes the same
+// tile and appends every (p~, centroid) whose lower bound is <= the query's T0
+// to the query's candidate list -- p~ never goes to memory.
 __global__ void __launch_bounds__(kCgThreads, 2)
 coarse_umma_kernel(const __grid_constant__ CUtensorMap tm_cen, const __grid_constant__ CUtensorMap tm_q, uint32_t q0,
                    uint32_t n_cen, uint32_t nq, uint32_t dim, const float* __restrict__ cnorm,
-                   const float* __restrict__ qnorm, float* __restrict__ p_out, uint32_t* __restrict__ gmin) {
+                   const float* __restrict__ qnorm, float* __restrict__ p_out, uint32_t* __restrict__ gmin,
+                   const CoarseFilter cf) {
     extern __shared__ unsigned char cg_raw[];
     unsigned char* sm = cg_raw + ((1024u - (su32(cg_raw) & 1023u)) & 1023u);
     constexpr uint32_t kABytes = kCgM * 128, kBBytes = kCgN * 128;
@@ -634,6 +639,37 @@ coarse_umma_kernel(const __grid_constant__ CUtensorMap tm_cen, const __grid_cons
             tc_commit(accf);
         }
         __syncwarp();
+    } else if (cf.t0) {
+        // pass B: candidates lo <= T0 per query column, appended warp-aggregated
+        mb_wait(accf, 0);
+        tc_fence_after();
+        const uint32_t c = c0 + warp * 32 + lane;
+        const float cn = c < n_cen ? cnorm[c] : 0.f;
+        for (uint32_t j = 0; j < (uint32_t)kCgN / 32; ++j) {
+            if (qt + j * 32 >= nq) break;
+            float v[32];
+            tc_ld32_nowait(tmem + ((warp * 32) << 16) + j * 32, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            const uint32_t myq = qt + j * 32 + lane;  // this lane's query column (T0 and qnorm loads)
+            const uint32_t t0_mine = myq < nq ? cf.t0[myq] : 0u;
+            const float qn_mine = myq < nq ? qnorm[myq] : 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const uint32_t qq = qt + j * 32 + i;
+                const uint32_t t0 = __shfl_sync(0xffffffffu, t0_mine, i);
+                const float qn = __shfl_sync(0xffffffffu, qn_mine, i);
+                const float p = fmaf(-2.f, v[i], cn + qn);
+                const bool is = c < n_cen && qq < nq && fkey(__fsub_rn(p, coarse_delta(cn, qn))) <= t0;
+                const uint32_t bal = __ballot_sync(0xffffffffu, is);
+                if (!bal) continue;
+                uint32_t base = 0;
+                if (lane == __ffs(bal) - 1) base = atomicAdd(cf.cnt + qq, (uint32_t)__popc(bal));
+                base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+                const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
+                if (is && pos < cf.cap)
+                    cf.cand[(size_t)qq * cf.cap + pos] = (static_cast<uint64_t>(__float_as_uint(p)) << 32) | c;
+            }
+        }
     } else {
         // epilogue: TMEM lane = centroid c0 + 32 warp + lane; columns = queries
         mb_wait(accf, 0);
@@ -652,7 +688,7 @@ coarse_umma_kernel(const __grid_constant__ CUtensorMap tm_cen, const __grid_cons
                 const uint32_t qq = qt + j * 32 + i;
                 const float qn = qq < nq ? qnorm[qq] : 0.f;
                 const float p = fmaf(-2.f, v[i], cn + qn);
-                if (c < n_cen && qq < nq) p_out[(size_t)qq * n_cen + c] = p;
+                if (p_out && c < n_cen && qq < nq) p_out[(size_t)qq * n_cen + c] = p;
                 if (gmin) {  // min upper-bound key of this warp's 32 centroids, per query column
                     const uint32_t m = __reduce_min_sync(
                         0xffffffffu, c < n_cen ? fkey(__fadd_rn(p, coarse_delta(cn, qn))) : 0xffffffffu);
@@ -679,12 +715,13 @@ size_t coarse_umma_smem_bytes() { return (size_t)kCgStages * (kCgM * 128 + kCgN 
 
 cudaError_t launch_coarse_umma(const CUtensorMap& tm_cen, const CUtensorMap& tm_q, uint32_t q0, uint32_t n_cen,
                                uint32_t nq, uint32_t dim, const float* cnorm, const float* qnorm, float* p_out,
-                               cudaStream_t s, uint32_t* gmin) {
+                               cudaStream_t s, uint32_t* gmin, const CoarseFilter& cf) {
     if (nq == 0 || n_cen == 0) return cudaSuccess;
     const size_t smem = coarse_umma_smem_bytes();
     DADE_CUDA_TRY(cudaFuncSetAttribute(coarse_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid((n_cen + kCgM - 1) / kCgM, (nq + kCgN - 1) / kCgN);
-    coarse_umma_kernel<<<grid, kCgThreads, smem, s>>>(tm_cen, tm_q, q0, n_cen, nq, dim, cnorm, qnorm, p_out, gmin);
+    coarse_umma_kernel<<<grid, kCgThreads, smem, s>>>(tm_cen, tm_q, q0, n_cen, nq, dim, cnorm, qnorm, p_out, gmin,
+                                                       cf);
     return cudaGetLastError();
 }
 
