@@ -412,6 +412,7 @@ struct dade_gpu_ctx {
     DevBuf counters, phase;
     TmapCache tm_centroids, tm_storage, tm_base;
     TmapCache tm_queries{256};  // rotated queries, {32 dims, 256 rows} boxes (tcgen05 coarse GEMM)
+    TmapCache tm_q128{128}, tm_c256{256};  // query-major fused coarse selection
     TmapCache tm32_storage{32}, tm32_base{32};
     RowNorms norms_storage, norms_base;
     RowAug aug_storage;
@@ -518,7 +519,7 @@ void coarse_tc_begin(dade_gpu_ctx* c, uint32_t nq, uint32_t n_probe) {
     c->qnorm.ensure((size_t)chunk * 4);
     if (coarse_fused(c)) {
         c->coarse_cand.ensure((size_t)chunk * kCoarseCandCap * 8);
-        c->coarse_cnt.ensure((size_t)chunk * 4);
+        c->coarse_cnt.ensure((size_t)chunk * 4 * kCoarseSelParts);
         c->coarse_t0.ensure((size_t)chunk * 4);
     } else {
         c->coarse_lo.ensure((size_t)chunk * c->n_clusters * 4);
@@ -543,9 +544,40 @@ void coarse_tc_range(dade_gpu_ctx* c, const float* d_q, uint32_t q0, uint32_t m,
         cuda_check(launch_coarse_norms(c->centroids.as<float>(), c->n_clusters, qc, m, c->dim, c->cnorm.as<float>(),
                                        c->qnorm.as<float>(), s),
                    "coarse norms");
+        bool tq128 = false, tc256 = false;
+        const CUtensorMap* mq = coarse_fused(c) && coarse_sel_umma_ok(c->dim)
+                                    ? &c->tm_q128.get(d_q, q0 + m, c->dim, tq128) : nullptr;
+        const CUtensorMap* mc = mq ? &c->tm_c256.get(c->centroids.as<float>(), c->n_clusters, c->dim, tc256) : nullptr;
+        if (mq && tq128 && tc256) {
+            // query-major fused selection (umma.cu coarse_sel_umma_kernel): pass A, group minima of
+            // the upper bounds -> T0 per query; pass B, the same GEMM, candidates lo <= T0 listed per
+            // query; then B, exact l2_sq, (d^2, id) sort. p~ never reaches memory.
+            c->coarse_gmin.ensure((size_t)m * ((c->n_clusters + 31) / 32) * 4);
+            uint32_t* gmin = c->coarse_gmin.as<uint32_t>();
+            CoarseFilter none;
+            cuda_check(launch_coarse_sel_umma(*mq, *mc, q0, c->n_clusters, m, c->dim, c->cnorm.as<float>(),
+                                              c->qnorm.as<float>(), gmin, none, s),
+                       "coarse selection pass A (tcgen05)");
+            cuda_check(launch_coarse_t0(gmin, c->n_clusters, m, n_probe, c->coarse_t0.as<uint32_t>(), s, true),
+                       "coarse t0");
+            CoarseFilter cf;  // (every thread writes its slice count: no memset)
+            cf.t0 = c->coarse_t0.as<uint32_t>();
+            cf.cand = c->coarse_cand.as<uint64_t>();
+            cf.cnt = c->coarse_cnt.as<uint32_t>();
+            cf.cap = kCoarseCandCap;
+            cuda_check(launch_coarse_sel_umma(*mq, *mc, q0, c->n_clusters, m, c->dim, c->cnorm.as<float>(),
+                                              c->qnorm.as<float>(), nullptr, cf, s),
+                       "coarse selection pass B (tcgen05)");
+            cuda_check(launch_coarse_finish(cf.cand, cf.cnt, cf.cap, c->cnorm.as<float>(), c->qnorm.as<float>(),
+                                            c->centroids.as<float>(), qc, m, c->dim, n_probe,
+                                            c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
+                                            c->coarse_overflow.as<uint32_t>(), s, kCoarseSelParts),
+                       "coarse finish");
+            c->launches += 5;
+            return;
+        }
         if (coarse_fused(c)) {
-            // pass A: group minima of the upper bounds -> T0 per query; pass B: the same GEMM,
-            // candidates lo <= T0 listed per query; then B, exact l2_sq, (d^2, id) sort
+            // centroid-major passes of coarse_umma_kernel (dims it cannot stage)
             c->coarse_gmin.ensure((size_t)m * ((c->n_clusters + 31) / 32) * 4);
             uint32_t* gmin = c->coarse_gmin.as<uint32_t>();
             cuda_check(launch_coarse_umma(*tmc, *tmq, q0, c->n_clusters, m, c->dim, c->cnorm.as<float>(),

@@ -652,18 +652,18 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_wide_kernel(
 // with lower bound <= T0 -- every exact top-n_probe centroid is among them --
 // and coarse_finish_kernel ends as coarse_select_wide_kernel does.
 __global__ void __launch_bounds__(kFsWarps * 32) coarse_t0_kernel(const uint32_t* __restrict__ gmin, uint32_t n_cen,
-                                                                  uint32_t nq, uint32_t n_probe, uint32_t* t0) {
+                                                                  uint32_t nq, uint32_t n_probe, uint32_t* t0,
+                                                                  bool transposed) {
     __shared__ uint32_t hist[kFsWarps][256];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t qi = blockIdx.x * kFsWarps + warp;
     if (qi >= nq) return;
     const uint32_t ng = (n_cen + 31) / 32;
-    const uint32_t* gr = gmin + (size_t)qi * ng;
     uint32_t gm[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         const uint32_t i = lane + 32u * j;
-        gm[j] = i < ng ? gr[i] : 0xffffffffu;
+        gm[j] = i < ng ? (transposed ? gmin[(size_t)i * nq + qi] : gmin[(size_t)qi * ng + i]) : 0xffffffffu;
     }
     uint32_t kmin = 0xffffffffu, kmax = 0;
 #pragma unroll
@@ -696,8 +696,10 @@ __global__ void __launch_bounds__(kFsWarps * 32) coarse_t0_kernel(const uint32_t
     if (lane == 0) t0[qi] = T0;
 }
 
+// parts > 1: the query's list is `parts` slices of cap / parts entries (query-major
+// pass B), counts cnt[q * parts + p]; parts == 1: one list, count cnt[q]
 __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_finish_kernel(
-    const uint64_t* __restrict__ cand_g, const uint32_t* __restrict__ cnt, uint32_t cap,
+    const uint64_t* __restrict__ cand_g, const uint32_t* __restrict__ cnt, uint32_t cap, uint32_t parts,
     const float* __restrict__ cnorm, const float* __restrict__ qnorm, const float* __restrict__ cen,
     const float* __restrict__ q, uint32_t nq, uint32_t dim, uint32_t n_probe, uint64_t* __restrict__ probes,
     uint32_t* __restrict__ overflow) {
@@ -707,12 +709,20 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_finish_kernel(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t qi = blockIdx.x * kFsWarps + warp;
     if (qi >= nq) return;
-    const uint32_t n = cnt[qi];
-    if (n > cap || n > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
+    const uint32_t pcap = cap / parts;
+    uint32_t n = 0;
+    bool over = false;
+    for (uint32_t p = 0; p < parts; ++p) {
+        const uint32_t np = cnt[(size_t)qi * parts + p];
+        over = over || np > pcap;
+        if (!over && n + np <= (uint32_t)kSelCap)
+            for (uint32_t e = lane; e < np; e += 32) cand[warp][n + e] = cand_g[(size_t)qi * cap + p * pcap + e];
+        n += np;
+    }
+    if (over || n > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
         if (lane == 0) atomicAdd(overflow, 1u);
         return;
     }
-    for (uint32_t e = lane; e < n; e += 32) cand[warp][e] = cand_g[(size_t)qi * cap + e];
     uint32_t* hist = reinterpret_cast<uint32_t*>(rows[warp]);
     finish_from_candidates(cand[warp], n, cnorm, qnorm[qi], cen, q + (size_t)qi * dim, dim, n_probe,
                            probes + (size_t)qi * n_probe, hist, hist + 256, rows[warp], qch[warp], lane);
@@ -773,19 +783,21 @@ cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const f
 }
 
 cudaError_t launch_coarse_t0(const uint32_t* gmin, uint32_t n_cen, uint32_t nq, uint32_t n_probe, uint32_t* t0,
-                             cudaStream_t s) {
+                             cudaStream_t s, bool transposed) {
     if (nq == 0) return cudaSuccess;
     if ((n_cen + 31) / 32 > 1024) return cudaErrorInvalidValue;
-    coarse_t0_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(gmin, n_cen, nq, n_probe, t0);
+    coarse_t0_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(gmin, n_cen, nq, n_probe, t0,
+                                                                             transposed);
     return cudaGetLastError();
 }
 
 cudaError_t launch_coarse_finish(const uint64_t* cand, const uint32_t* cnt, uint32_t cap, const float* cnorm,
                                  const float* qnorm, const float* centroids, const float* queries, uint32_t nq,
-                                 uint32_t dim, uint32_t n_probe, uint64_t* probes, uint32_t* overflow, cudaStream_t s) {
+                                 uint32_t dim, uint32_t n_probe, uint64_t* probes, uint32_t* overflow, cudaStream_t s,
+                                 uint32_t parts) {
     if (nq == 0) return cudaSuccess;
     coarse_finish_kernel<<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
-        cand, cnt, cap, cnorm, qnorm, centroids, queries, nq, dim, n_probe, probes, overflow);
+        cand, cnt, cap, parts, cnorm, qnorm, centroids, queries, nq, dim, n_probe, probes, overflow);
     return cudaGetLastError();
 }
 

@@ -103,13 +103,23 @@ struct CoarseFilter {
 cudaError_t launch_coarse_umma(const CUtensorMap& tm_cen, const CUtensorMap& tm_q, uint32_t q0, uint32_t n_cen,
                                uint32_t nq, uint32_t dim, const float* cnorm, const float* qnorm, float* p_out,
                                cudaStream_t s, uint32_t* gmin = nullptr, const CoarseFilter& cf = CoarseFilter{});
+// query-major fused selection (umma.cu): pass A (cf.t0 == nullptr) writes gmin_t
+// [ceil(n_cen / 32)][nq] (per query, the min upper-bound key of every 32 centroids); pass B
+// (cf.t0 set) lists the candidates. tm_q128: queries, box {32, 128}; tm_c256: centroids, box {32, 256}.
+bool coarse_sel_umma_ok(uint32_t dim);
+cudaError_t launch_coarse_sel_umma(const CUtensorMap& tm_q128, const CUtensorMap& tm_c256, uint32_t q0, uint32_t n_cen,
+                                   uint32_t nq, uint32_t dim, const float* cnorm, const float* qnorm, uint32_t* gmin_t,
+                                   const CoarseFilter& cf, cudaStream_t s);
 // the fused large-nlist selection around it (coarse.cu): T0 per query from the GEMM's group
 // minima, then (after pass B) B, the exact l2_sq of the candidates and the (d^2, id) sort
+// transposed: gmin[group][nq] (coarse_sel_umma pass A) instead of gmin[query][groups]
 cudaError_t launch_coarse_t0(const uint32_t* gmin, uint32_t n_cen, uint32_t nq, uint32_t n_probe, uint32_t* t0,
-                             cudaStream_t s);
+                             cudaStream_t s, bool transposed = false);
 cudaError_t launch_coarse_finish(const uint64_t* cand, const uint32_t* cnt, uint32_t cap, const float* cnorm,
                                  const float* qnorm, const float* centroids, const float* queries, uint32_t nq,
-                                 uint32_t dim, uint32_t n_probe, uint64_t* probes, uint32_t* overflow, cudaStream_t s);
+                                 uint32_t dim, uint32_t n_probe, uint64_t* probes, uint32_t* overflow, cudaStream_t s,
+                                 uint32_t parts = 1);
+constexpr uint32_t kCoarseSelParts = 4;  // list slices per query of the query-major pass B
 // coarse.cu pieces around it
 cudaError_t launch_coarse_norms(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
                                 float* cnorm, float* qnorm, cudaStream_t s);

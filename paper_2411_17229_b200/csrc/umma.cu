@@ -711,6 +711,194 @@ coarse_umma_kernel(const __grid_constant__ CUtensorMap tm_cen, const __grid_cons
 
 }  // namespace
 
+// ---- fused large-nlist coarse selection, query-major (tcgen05) -----------------------
+// One CTA per 128 queries (MMA M = queries: TMEM lane = query), the query block
+// staged once (TMA, SW128, all 32-dim atoms), the centroids streamed as 256-row
+// tiles (MMA N) through a 4-stage ring of 32-dim atoms (they stay L2-resident:
+// 8 MB at nlist 16384, D 128), two 256-column TMEM accumulators so the MMAs of
+// tile t+1 run under the epilogue of tile t. Eight epilogue warps: warp w reads
+// TMEM lanes 32 (w % 4).. and columns 128 (w / 4).. of each tile, one thread =
+// one query, no cross-lane traffic:
+//   pass A: per 32 centroids the minimum upper-bound key fkey(p~ + delta)
+//           -> gmin[group][query] (coalesced);
+//   pass B: every centroid with lower bound fkey(p~ - delta) <= t0[query]
+//           -> (p~ bits << 32 | centroid) appended to the query's list.
+// Same p~ = |c|^2 + |q|^2 - 2 q.c and bound as the other coarse kernels.
+constexpr int kSqM = 128, kSqN = 256, kSqStages = 4, kSqEpiWarps = 16;
+constexpr int kSqCols = kSqN / (kSqEpiWarps / 4);  // columns per epilogue warp (64)
+static_assert(kSqEpiWarps / 4 == (int)kCoarseSelParts, "one candidate-list slice per column part");
+constexpr int kSqThreads = (kSqEpiWarps + 1) * 32;
+constexpr uint32_t kSqAtomA = kSqM * 128, kSqAtomB = kSqN * 128;  // bytes per 32-dim atom
+
+struct SqLayout {
+    uint32_t a, ring, cn, bars, total;
+};
+__host__ __device__ inline SqLayout sq_layout(uint32_t dim) {
+    SqLayout L;
+    const uint32_t n_atoms = (dim + 31) / 32;
+    L.a = 0;
+    L.ring = L.a + n_atoms * kSqAtomA;
+    L.cn = L.ring + kSqStages * kSqAtomB;
+    L.bars = L.cn + 2 * kSqEpiWarps * kSqCols * 4;
+    L.total = L.bars + 16 * 8 + 16 + 1024;  // + alignment slack
+    return L;
+}
+
+template <bool kPassB>
+__global__ void __launch_bounds__(kSqThreads, 1)
+coarse_sel_umma_kernel(const __grid_constant__ CUtensorMap tm_q128, const __grid_constant__ CUtensorMap tm_c256,
+                       uint32_t q0, uint32_t n_cen, uint32_t nq, uint32_t dim, const float* __restrict__ cnorm,
+                       const float* __restrict__ qnorm, uint32_t* __restrict__ gmin_t, const CoarseFilter cf) {
+    extern __shared__ unsigned char sq_raw[];
+    unsigned char* sm = sq_raw + ((1024u - (su32(sq_raw) & 1023u)) & 1023u);
+    const SqLayout L = sq_layout(dim);
+    unsigned char* sa = sm + L.a;
+    unsigned char* ring = sm + L.ring;
+    float* cn_s = reinterpret_cast<float*>(sm + L.cn);  // [2][warp][128] centroid norms of each warp's columns
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
+    uint64_t* afull = bars;
+    uint64_t* full = bars + 1;                 // [kSqStages]
+    uint64_t* empty = full + kSqStages;        // [kSqStages]
+    uint64_t* accf = empty + kSqStages;        // [2]
+    uint64_t* acce = accf + 2;                 // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t qb = blockIdx.x * kSqM;
+    const uint32_t n_atoms = (dim + 31) / 32, n_tiles = (n_cen + kSqN - 1) / kSqN;
+    if (threadIdx.x == 0) {
+        mb_init(afull, 1);
+        for (int i = 0; i < kSqStages; ++i) {
+            mb_init(full + i, 1);
+            mb_init(empty + i, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mb_init(accf + b, 1);
+            mb_init(acce + b, kSqEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == kSqEpiWarps) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp == kSqEpiWarps) {
+        if (lane == 0) {
+            // the query block: every atom once
+            mb_arrive_tx(afull, n_atoms * kSqAtomA);
+            for (uint32_t k = 0; k < n_atoms; ++k) tma2d_u(sa + k * kSqAtomA, &tm_q128, (int)(k * 32), (int)(q0 + qb), afull);
+            const uint32_t total = n_tiles * n_atoms;
+            auto issue = [&](uint32_t i) {  // i-th (tile, atom) of the centroid stream
+                const uint32_t s = i % kSqStages;
+                if (i >= (uint32_t)kSqStages) mb_wait(empty + s, ((i / kSqStages) - 1) & 1);
+                mb_arrive_tx(full + s, kSqAtomB);
+                tma2d_u(ring + (size_t)s * kSqAtomB, &tm_c256, (int)((i % n_atoms) * 32), (int)((i / n_atoms) * kSqN),
+                        full + s);
+            };
+            uint32_t next = 0;
+            while (next < total && next < (uint32_t)kSqStages) issue(next++);
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kSqN >> 3) << 17) |
+                                   ((uint32_t)(kSqM >> 4) << 24);
+            mb_wait(afull, 0);
+            for (uint32_t t = 0; t < n_tiles; ++t) {
+                const uint32_t b = t & 1;
+                if (t >= 2) mb_wait(acce + b, ((t >> 1) - 1) & 1);
+                tc_fence_after();
+                for (uint32_t k = 0; k < n_atoms; ++k) {
+                    const uint32_t i = t * n_atoms + k, s = i % kSqStages;
+                    mb_wait(full + s, (i / kSqStages) & 1);
+                    tc_fence_after();
+                    const uint32_t a_addr = su32(sa + k * kSqAtomA), b_addr = su32(ring + (size_t)s * kSqAtomB);
+                    const int nk = min(4, (int)(dim - k * 32 + 7) / 8);
+                    for (int kk = 0; kk < nk; ++kk)
+                        tc_mma(tmem + b * kSqN, desc_sw128(a_addr + kk * 32), desc_sw128(b_addr + kk * 32), idesc,
+                               (k | kk) ? 1u : 0u);
+                    tc_commit(empty + s);
+                    if (next < total) issue(next++);
+                }
+                tc_commit(accf + b);
+            }
+        }
+        __syncwarp();
+    } else {
+        // epilogue: thread = query qb + 32 (warp % 4) + lane, columns [64 (warp / 4), +64) of each tile;
+        // bounds compared as floats (fkey is monotone): hi = p~ + delta, lo = p~ - delta
+        const uint32_t quarter = warp & 3, part = warp >> 2;
+        const uint32_t qq = qb + quarter * 32 + lane;
+        const bool qok = qq < nq;
+        const float qn = qok ? qnorm[qq] : 0.f;
+        // pass B: candidates of part p go to cand[q][p * part_cap ..], their count to cnt[q * 4 + p]
+        const uint32_t part_cap = cf.cap / (kSqEpiWarps / 4);
+        uint64_t* part_list = kPassB ? cf.cand + (size_t)qq * cf.cap + part * part_cap : nullptr;
+        uint32_t n_app = 0;
+        float t0f = 0.f;
+        if (kPassB && qok) {  // the float whose key is t0
+            const uint32_t k = cf.t0[qq];
+            t0f = __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+        }
+        for (uint32_t t = 0; t < n_tiles; ++t) {
+            const uint32_t b = t & 1, c_tile = t * kSqN;
+            float* cns = cn_s + (b * kSqEpiWarps + warp) * kSqCols;  // this warp's column norms
+#pragma unroll
+            for (int r = 0; r < kSqCols / 32; ++r) {
+                const uint32_t c = c_tile + part * kSqCols + r * 32 + lane;
+                cns[r * 32 + lane] = c < n_cen ? cnorm[c] : 0.f;
+            }
+            __syncwarp();
+            mb_wait(accf + b, (t >> 1) & 1);
+            tc_fence_after();
+            const uint32_t col0 = part * kSqCols;
+            float v[2][32];
+            tc_ld32_nowait(tmem + ((quarter * 32) << 16) + b * kSqN + col0, v[0]);
+            tc_ld32_nowait(tmem + ((quarter * 32) << 16) + b * kSqN + col0 + 32, v[1]);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive(acce + b);  // accumulator read: the MMAs of tile t + 2 may start
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t cb = c_tile + col0 + h * 32;
+                if (cb >= n_cen) break;
+                if (!kPassB) {
+                    float m[4] = {__int_as_float(0x7f800000), __int_as_float(0x7f800000), __int_as_float(0x7f800000),
+                                  __int_as_float(0x7f800000)};  // 4 independent chains
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float cn = cns[h * 32 + i];
+                        const float p = fmaf(-2.f, v[h][i], cn + qn);
+                        const float hi = __fadd_rn(p, coarse_delta(cn, qn));
+                        m[i & 3] = (cb + i < n_cen) ? fminf(m[i & 3], hi) : m[i & 3];
+                    }
+                    if (qok) gmin_t[(size_t)(cb / 32) * nq + qq] = fkey(fminf(fminf(m[0], m[1]), fminf(m[2], m[3])));
+                } else if (qok) {
+                    // this thread's own slice of the query's list (part p of kSqEpiWarps / 4): no atomics
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float cn = cns[h * 32 + i];
+                        const float p = fmaf(-2.f, v[h][i], cn + qn);
+                        if (__fsub_rn(p, coarse_delta(cn, qn)) <= t0f && cb + i < n_cen) {
+                            if (n_app < part_cap)
+                                part_list[n_app] = (static_cast<uint64_t>(__float_as_uint(p)) << 32) | (cb + i);
+                            ++n_app;
+                        }
+                    }
+                }
+            }
+        }
+        if (kPassB && qok) cf.cnt[(size_t)qq * (kSqEpiWarps / 4) + part] = n_app;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kSqEpiWarps) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+    }
+}
+
 size_t coarse_umma_smem_bytes() { return (size_t)kCgStages * (kCgM * 128 + kCgN * 128) + 8 * 8 + 1024; }
 
 cudaError_t launch_coarse_umma(const CUtensorMap& tm_cen, const CUtensorMap& tm_q, uint32_t q0, uint32_t n_cen,
@@ -722,6 +910,29 @@ cudaError_t launch_coarse_umma(const CUtensorMap& tm_cen, const CUtensorMap& tm_
     dim3 grid((n_cen + kCgM - 1) / kCgM, (nq + kCgN - 1) / kCgN);
     coarse_umma_kernel<<<grid, kCgThreads, smem, s>>>(tm_cen, tm_q, q0, n_cen, nq, dim, cnorm, qnorm, p_out, gmin,
                                                        cf);
+    return cudaGetLastError();
+}
+
+bool coarse_sel_umma_ok(uint32_t dim) { return dim % 4 == 0 && dim >= 32 && dim <= 256 && sq_layout(dim).total <= 227 * 1024; }
+
+cudaError_t launch_coarse_sel_umma(const CUtensorMap& tm_q128, const CUtensorMap& tm_c256, uint32_t q0, uint32_t n_cen,
+                                   uint32_t nq, uint32_t dim, const float* cnorm, const float* qnorm, uint32_t* gmin_t,
+                                   const CoarseFilter& cf, cudaStream_t s) {
+    if (nq == 0 || n_cen == 0) return cudaSuccess;
+    if (!coarse_sel_umma_ok(dim)) return cudaErrorInvalidValue;
+    const size_t smem = sq_layout(dim).total;
+    const dim3 grid((nq + kSqM - 1) / kSqM);
+    if (cf.t0) {
+        DADE_CUDA_TRY(cudaFuncSetAttribute(coarse_sel_umma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+        coarse_sel_umma_kernel<true><<<grid, kSqThreads, smem, s>>>(tm_q128, tm_c256, q0, n_cen, nq, dim, cnorm, qnorm,
+                                                                    gmin_t, cf);
+    } else {
+        DADE_CUDA_TRY(cudaFuncSetAttribute(coarse_sel_umma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+        coarse_sel_umma_kernel<false><<<grid, kSqThreads, smem, s>>>(tm_q128, tm_c256, q0, n_cen, nq, dim, cnorm,
+                                                                     qnorm, gmin_t, cf);
+    }
     return cudaGetLastError();
 }
 
