@@ -50,10 +50,12 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
     objdir.mkdir(parents=True, exist_ok=True)
     if force or _stale(LIB, deps):
         objs = []
+        headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "dade_gpu.h"]
         for s in SOURCES:
             o = objdir / (s + ".o")
-            _run([NVCC, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / s), "-o", str(o)],
-                 log=objdir / (s + ".log"))
+            if force or _stale(o, [CSRC / s, *headers, Path(__file__)]):
+                _run([NVCC, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / s), "-o", str(o)],
+                     log=objdir / (s + ".log"))
             objs.append(str(o))
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *objs, "-ldl"])
     cpp_test = ROOT / "tests" / "cpp" / "host_api_test.cpp"

@@ -12,87 +12,165 @@ namespace dade_gpu {
 namespace {
 
 // ---- K1: out[i][k] = (float) sum_r W[k*D + r] * in[i][r] --------------------
-// f64 accumulation in r order with separately rounded DMUL/DADD, exactly
-// OrthoTransform::transform_vector (proj/src/transform.cpp:221-228).
+// The reference's sum is a sequential chain of D rounded DMULs and DADDs
+// (proj/src/transform.cpp:221-228). The kernel computes the same dot products
+// on the FP64 tensor cores (mma.sync m8n8k4 f64, IEEE fp64 fused multiply-adds
+// in some order) and proves that both results round to the same float: with
+// S = sum_r |w_r x_r| <= |w| |x|, each of the two fp64 evaluations is within
+// gamma_D S of the real value (gamma_D = D u / (1 - D u), u = 2^-53), so the
+// reference's fp64 sum lies in [acc - E, acc + E], E = 2 gamma_D |w| |x|. When
+// both ends of that interval round to the same float (RN is monotone), that
+// float is the reference's output. Otherwise (a float rounding boundary inside
+// the interval: ~1e-4 of the elements, and every NaN) the element is recomputed
+// with the reference's exact DMUL/DADD chain, one lane per element after the
+// CTA's main loop, so every output is bit-identical to transform_vector.
+//
+// 64 rows x 64 output columns per CTA of 4 warps, 32 x 32 per warp (4 x 4
+// m8n8 tiles); x and W chunks of 16 r staged as fp64 ([row][r], [col][r],
+// stride 20 doubles: conflict-free fragment loads), prefetched one chunk ahead
+// in registers; the row / column norms are accumulated from the staged values.
+// (A 32 x 32 tile with the K range split over the warps measured 1.5x slower:
+// four times the staging per multiply-add.)
+constexpr int kRotT = 64;    // rows and columns per CTA
+constexpr int kRotK = 16;    // r chunk
+constexpr int kRotS = 20;    // staged row stride (doubles)
+constexpr int kRotFix = 512; // per-CTA list of elements to recompute exactly
 
-// 32 output columns x 64 rows per CTA, a 4-row x 2-column register block per
-// thread; W and x chunks staged transposed ([r][col], [r][row]) so each
-// thread's weights and inputs of one r are 16-byte loads. Every output element
-// is the reference's sequential fp64 sum over r = 0..D-1 (DMUL + DADD, no FMA).
-constexpr int kRotC = 32;   // columns per CTA
-constexpr int kRotR = 64;   // rows per CTA
-constexpr int kRotK = 32;   // r chunk
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
 
-__global__ void __launch_bounds__(256)
+__device__ __noinline__ float rotate_exact(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in,
+                                           uint32_t row, uint32_t col) {
+    const double* w = W + (size_t)col * dim;
+    const float* x = in + (size_t)row * dim;
+    double acc = 0.0;
+    for (uint32_t r = 0; r < dim; ++r) acc = __dadd_rn(acc, __dmul_rn(__ldg(w + r), (double)__ldg(x + r)));
+    return __double2float_rn(acc);
+}
+
+__global__ void __launch_bounds__(128)
 rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in, uint32_t n,
               float* __restrict__ out) {
-    __shared__ __align__(16) double ws[kRotK][kRotC + 2];
-    __shared__ __align__(16) double xs[kRotK][kRotR + 2];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tc = lane & 15;                    // columns 2 tc, 2 tc + 1
-    const int tr = warp * 2 + (lane >> 4);       // rows 4 tr .. 4 tr + 3
-    const uint32_t col0 = blockIdx.x * kRotC;
-    const uint32_t row0 = blockIdx.y * kRotR;
-    double acc[4][2];
+    __shared__ __align__(16) double xs[kRotT * kRotS];
+    __shared__ __align__(16) double ws[kRotT * kRotS];
+    __shared__ double wn[kRotT], xn[kRotT];
+    __shared__ uint32_t fix[kRotFix];
+    __shared__ uint32_t n_fix;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;          // mma fragment coordinates
+    const int wm = warp >> 1, wc = warp & 1;        // warp tile: rows 32 wm.., columns 32 wc..
+    const uint32_t col0 = blockIdx.x * kRotT, row0 = blockIdx.y * kRotT;
+    if (tid == 0) n_fix = 0;
+    double c[4][4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
-    // chunk r0's W / x values: this thread's 4 + 8 staging elements, loaded one
-    // chunk ahead into registers while the previous chunk is accumulated
-    constexpr int kWPer = kRotC * kRotK / 256, kXPer = kRotR * kRotK / 256;
-    double wreg[kWPer];
-    float xreg[kXPer];
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+    // staging: thread tid holds row / column tid >> 1, r = r0 + 8 (tid & 1) .. + 7
+    const uint32_t sr = tid >> 1, so = 8 * (tid & 1);
+    const uint32_t xrow = row0 + sr, wcol = col0 + sr;
+    const bool vec = dim % 4 == 0;
+    float xv[8];
+    double wv[8];
+    double xsq = 0.0, wsq = 0.0;
     auto load_chunk = [&](uint32_t r0) {
+        const uint32_t r = r0 + so;
+        if (vec && r + 8 <= dim) {
+            if (xrow < n) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(in + (size_t)xrow * dim + r));
+                const float4 b = __ldg(reinterpret_cast<const float4*>(in + (size_t)xrow * dim + r + 4));
+                xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
+                xv[4] = b.x; xv[5] = b.y; xv[6] = b.z; xv[7] = b.w;
+            } else {
 #pragma unroll
-        for (int u = 0; u < kWPer; ++u) {
-            const int idx = threadIdx.x + 256 * u, a = idx / kRotK, b = idx % kRotK;
-            const uint32_t col = col0 + a, r = r0 + b;
-            wreg[u] = (col < dim && r < dim) ? __ldg(W + (size_t)col * dim + r) : 0.0;
-        }
+                for (int e = 0; e < 8; ++e) xv[e] = 0.f;
+            }
+            if (wcol < dim) {
 #pragma unroll
-        for (int u = 0; u < kXPer; ++u) {
-            const int idx = threadIdx.x + 256 * u, a = idx / kRotK, b = idx % kRotK;
-            const uint32_t row = row0 + a, r = r0 + b;
-            xreg[u] = (row < n && r < dim) ? __ldg(in + (size_t)row * dim + r) : 0.f;
+                for (int e = 0; e < 8; e += 2) {
+                    const double2 v = __ldg(reinterpret_cast<const double2*>(W + (size_t)wcol * dim + r + e));
+                    wv[e] = v.x;
+                    wv[e + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) wv[e] = 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                xv[e] = (xrow < n && r + e < dim) ? __ldg(in + (size_t)xrow * dim + r + e) : 0.f;
+                wv[e] = (wcol < dim && r + e < dim) ? __ldg(W + (size_t)wcol * dim + r + e) : 0.0;
+            }
         }
     };
     load_chunk(0);
     for (uint32_t r0 = 0; r0 < dim; r0 += kRotK) {
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < kWPer; ++u) {
-            const int idx = threadIdx.x + 256 * u;
-            ws[idx % kRotK][idx / kRotK] = wreg[u];
-        }
-#pragma unroll
-        for (int u = 0; u < kXPer; ++u) {
-            const int idx = threadIdx.x + 256 * u;
-            xs[idx % kRotK][idx / kRotK] = (double)xreg[u];
+        for (int e = 0; e < 8; e += 2) {
+            const double x0 = (double)xv[e], x1 = (double)xv[e + 1];
+            *reinterpret_cast<double2*>(&xs[sr * kRotS + so + e]) = make_double2(x0, x1);
+            *reinterpret_cast<double2*>(&ws[sr * kRotS + so + e]) = make_double2(wv[e], wv[e + 1]);
+            xsq = fma(x0, x0, fma(x1, x1, xsq));
+            wsq = fma(wv[e], wv[e], fma(wv[e + 1], wv[e + 1], wsq));
         }
         __syncthreads();
         if (r0 + kRotK < dim) load_chunk(r0 + kRotK);
-        const int kmax = (int)min((uint32_t)kRotK, dim - r0);
-#pragma unroll 4
-        for (int b = 0; b < kmax; ++b) {
-            const double2 w = *reinterpret_cast<const double2*>(&ws[b][2 * tc]);
-            const double2 x01 = *reinterpret_cast<const double2*>(&xs[b][4 * tr]);
-            const double2 x23 = *reinterpret_cast<const double2*>(&xs[b][4 * tr + 2]);
-            const double x[4] = {x01.x, x01.y, x23.x, x23.y};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                acc[i][0] = __dadd_rn(acc[i][0], __dmul_rn(w.x, x[i]));
-                acc[i][1] = __dadd_rn(acc[i][1], __dmul_rn(w.y, x[i]));
-            }
+        for (int k0 = 0; k0 < kRotK; k0 += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = xs[(32 * wm + 8 * i + g) * kRotS + k0 + t];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = ws[(32 * wc + 8 * j + g) * kRotS + k0 + t];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(c[i][j], a[i], b[j]);
         }
     }
+    // norms (upper bounds after the 1.0001 margin below); lanes 2m, 2m + 1 share a row
+    xsq += __shfl_xor_sync(0xffffffffu, xsq, 1);
+    wsq += __shfl_xor_sync(0xffffffffu, wsq, 1);
+    if ((tid & 1) == 0) {
+        xn[sr] = sqrt(xsq);
+        wn[sr] = sqrt(wsq);
+    }
+    __syncthreads();
+    // E = 2 gamma_D |w| |x| with margin for the norms' own rounding
+    const double gam = (double)(dim + 2) * 0x1p-52 * 1.0001;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const uint32_t row = row0 + 4 * tr + i;
+        const uint32_t rl = 32 * wm + 8 * i + g, row = row0 + rl;
         if (row >= n) continue;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            const uint32_t col = col0 + 2 * tc + j;
-            if (col < dim) out[(size_t)row * dim + col] = __double2float_rn(acc[i][j]);
-        }
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t cl = 32 * wc + 8 * j + 2 * t + h, col = col0 + cl;
+                if (col >= dim) continue;
+                const double acc = c[i][j][h];
+                const double e = gam * wn[cl] * xn[rl];
+                const float lo = __double2float_rn(__dsub_rd(acc, e));
+                const float hi = __double2float_rn(__dadd_ru(acc, e));
+                if (__float_as_uint(lo) == __float_as_uint(hi) && !isnan(lo)) {
+                    out[(size_t)row * dim + col] = lo;
+                } else {
+                    const uint32_t slot = atomicAdd(&n_fix, 1u);
+                    if (slot < (uint32_t)kRotFix) fix[slot] = (rl << 8) | cl;
+                    else out[(size_t)row * dim + col] = rotate_exact(W, dim, in, row, col);
+                }
+            }
+    }
+    __syncthreads();
+    const uint32_t nf = min(n_fix, (uint32_t)kRotFix);
+    for (uint32_t e = tid; e < nf; e += blockDim.x) {
+        const uint32_t row = row0 + (fix[e] >> 8), col = col0 + (fix[e] & 0xffu);
+        out[(size_t)row * dim + col] = rotate_exact(W, dim, in, row, col);
     }
 }
 
@@ -784,8 +862,8 @@ cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s) {
 cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
                           cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    dim3 grid((dim + kRotC - 1) / kRotC, (n + kRotR - 1) / kRotR);
-    rotate_kernel<<<grid, 256, 0, s>>>(W, dim, in, n, out);
+    dim3 grid((dim + kRotT - 1) / kRotT, (n + kRotT - 1) / kRotT);
+    rotate_kernel<<<grid, 128, 0, s>>>(W, dim, in, n, out);
     return cudaGetLastError();
 }
 

@@ -337,3 +337,24 @@ def test_rotation_bit_exact_large(gp, dev, oracle_lib, ref_lib, dim, tmp_path):
     assert np.array_equal(bits(got), bits(oracle_lib.apply_transform(mat, raw)))
     write_transform(tmp_path / "t.dade", t)
     assert np.array_equal(bits(got), bits(ref_lib.load_transform(tmp_path / "t.dade").apply(raw)))
+
+
+@pytest.mark.parametrize("dim", [7, 64, 200])
+def test_rotation_verified_fast_path_edge_values(gp, dev, oracle_lib, dim):
+    """rotate_kernel's DFMA result is accepted only when it provably rounds to the
+    reference's float; inputs with a wide dynamic range (many outputs near a
+    float rounding boundary relative to the error bound), a non-orthogonal W,
+    zero rows and an inf row exercise the exact DMUL/DADD recompute path."""
+    g = np.random.default_rng(100 + dim)
+    mat = (g.standard_normal(dim * dim) * np.exp(g.uniform(-3, 3, dim * dim))).astype(np.float64)
+    raw = (g.standard_normal((3000, dim)) * np.exp(g.uniform(-12, 8, (3000, dim)))).astype(np.float32)
+    raw[5] = 0.0
+    raw[6, :] = np.float32(1e-30)
+    raw[7, dim // 2] = np.inf
+    raw[8] = np.float32(3e38)
+    t = gp.OrthoTransform(dim, 0, np.zeros(dim), np.ones(dim), mat)
+    got = t.apply(dev, raw)
+    want = oracle_lib.apply_transform(mat, raw)
+    nan_g, nan_w = np.isnan(got), np.isnan(want)
+    assert np.array_equal(nan_g, nan_w)
+    assert np.array_equal(bits(got)[~nan_g], bits(want)[~nan_w])
