@@ -271,6 +271,66 @@ __device__ __forceinline__ void cs_cp16(float* dst, const float* src) {
 }
 constexpr int kFsRS = 36;  // floats per staged row chunk (16-byte aligned, conflict-free LDS.128)
 
+// One round of exact sequential l2_sq (proj/include/dade/distance.hpp:36-43):
+// lane i advances candidate my_c of lane i (active lanes; nv = lanes holding a
+// candidate). Rows are staged 32 dims at a time through shared memory rs / qs
+// with coalesced 16-byte loads (8 lanes per 128-byte row chunk); the next
+// chunk's loads are issued before the current chunk is summed, so the L2
+// latency overlaps the arithmetic, and a full 32-dim chunk is summed unrolled.
+__device__ __forceinline__ float exact_l2_round(const float* __restrict__ cen, const float* __restrict__ qr,
+                                                uint32_t dim, uint32_t my_c, uint32_t nv, bool active, float* rs,
+                                                float* qs, int lane) {
+    const uint32_t sub = lane >> 3, c4 = lane & 7;
+    uint32_t cc[8];
+#pragma unroll
+    for (int sg = 0; sg < 8; ++sg) cc[sg] = __shfl_sync(0xffffffffu, my_c, 4 * sg + sub);
+    float4 v[8], qv;
+    auto load = [&](uint32_t k0) {
+        const uint32_t w = min(32u, dim - k0);
+#pragma unroll
+        for (int sg = 0; sg < 8; ++sg)
+            v[sg] = (4 * sg + sub < nv && 4 * c4 < w)
+                        ? __ldg(reinterpret_cast<const float4*>(cen + (size_t)cc[sg] * dim + k0) + c4)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        qv = (lane < 8 && 4u * lane < w) ? __ldg(reinterpret_cast<const float4*>(qr + k0) + lane)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    load(0);
+    float acc = 0.f;
+    const float* os = rs + lane * kFsRS;
+    for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
+        const uint32_t w = min(32u, dim - k0);
+        __syncwarp();  // previous chunk's readers done
+#pragma unroll
+        for (int sg = 0; sg < 8; ++sg) *reinterpret_cast<float4*>(rs + (4 * sg + sub) * kFsRS + 4 * c4) = v[sg];
+        if (lane < 8) *reinterpret_cast<float4*>(qs + 4 * lane) = qv;
+        __syncwarp();
+        if (k0 + 32 < dim) load(k0 + 32);
+        if (!active) continue;
+        if (w == 32) {
+#pragma unroll
+            for (uint32_t kk = 0; kk < 32; kk += 4) {
+                const float4 o4 = *reinterpret_cast<const float4*>(os + kk);
+                const float4 q4 = *reinterpret_cast<const float4*>(qs + kk);
+                acc = sq_step(acc, q4.x, o4.x);
+                acc = sq_step(acc, q4.y, o4.y);
+                acc = sq_step(acc, q4.z, o4.z);
+                acc = sq_step(acc, q4.w, o4.w);
+            }
+        } else {
+            for (uint32_t kk = 0; kk < w; kk += 4) {
+                const float4 o4 = *reinterpret_cast<const float4*>(os + kk);
+                const float4 q4 = *reinterpret_cast<const float4*>(qs + kk);
+                acc = sq_step(acc, q4.x, o4.x);
+                acc = sq_step(acc, q4.y, o4.y);
+                acc = sq_step(acc, q4.z, o4.z);
+                acc = sq_step(acc, q4.w, o4.w);
+            }
+        }
+    }
+    return acc;
+}
+
 // WPQ = 4 (small batches, where a warp per query leaves the GPU idle): the four
 // warps of a CTA select the same candidates redundantly (no synchronisation),
 // warp w runs the exact rounds w, w + 4, ... and writes its keys into warp 0's
@@ -358,38 +418,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
         const uint32_t e = e0 + lane;
         const uint32_t my_c = e < n ? (uint32_t)cand[warp][e] : 0u;
         const uint32_t nv = min(32u, n - e0);
-        float acc = 0.f;
-        for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
-            const uint32_t w = min(32u, dim - k0);
-            const uint32_t sub = lane >> 3, c4 = lane & 7;
-            float4 v[8];
-#pragma unroll
-            for (int sg = 0; sg < 8; ++sg) {
-                const uint32_t sidx = 4 * sg + sub;
-                const uint32_t cc = __shfl_sync(0xffffffffu, my_c, sidx);
-                v[sg] = (sidx < nv && 4 * c4 < w) ? __ldg(reinterpret_cast<const float4*>(cen + (size_t)cc * dim + k0) + c4)
-                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            const float4 qv = (lane < 8 && 4u * lane < w) ? __ldg(reinterpret_cast<const float4*>(qr + k0) + lane)
-                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-            __syncwarp();  // previous chunk's readers done
-#pragma unroll
-            for (int sg = 0; sg < 8; ++sg)
-                *reinterpret_cast<float4*>(rs + (4 * sg + sub) * kFsRS + 4 * c4) = v[sg];
-            if (lane < 8) *reinterpret_cast<float4*>(qs + 4 * lane) = qv;
-            __syncwarp();
-            if (e < n) {
-                const float* os = rs + lane * kFsRS;
-                for (uint32_t k = 0; k < w; k += 4) {
-                    const float4 o4 = *reinterpret_cast<const float4*>(os + k);
-                    const float4 q4 = *reinterpret_cast<const float4*>(qs + k);
-                    acc = sq_step(acc, q4.x, o4.x);
-                    acc = sq_step(acc, q4.y, o4.y);
-                    acc = sq_step(acc, q4.z, o4.z);
-                    acc = sq_step(acc, q4.w, o4.w);
-                }
-            }
-        }
+        const float acc = exact_l2_round(cen, qr, dim, my_c, nv, e < n, rs, qs, lane);
         __syncwarp();
         if (e < n) cand[WPQ == 1 ? warp : 0][e] = make_key(acc, my_c);
     }
@@ -498,38 +527,7 @@ __device__ void finish_from_candidates(uint64_t* cand, uint32_t n, const float* 
         const uint32_t e = e0 + lane;
         const uint32_t my_c = e < n ? (uint32_t)cand[e] : 0u;
         const uint32_t nv = min(32u, n - e0);
-        float acc = 0.f;
-        for (uint32_t k0 = 0; k0 < dim; k0 += 32) {
-            const uint32_t w = min(32u, dim - k0);
-            const uint32_t sub = lane >> 3, c4 = lane & 7;
-            float4 v[8];
-#pragma unroll
-            for (int sg = 0; sg < 8; ++sg) {
-                const uint32_t sidx = 4 * sg + sub;
-                const uint32_t cc = __shfl_sync(0xffffffffu, my_c, sidx);
-                v[sg] = (sidx < nv && 4 * c4 < w) ? __ldg(reinterpret_cast<const float4*>(cen + (size_t)cc * dim + k0) + c4)
-                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            const float4 qv = (lane < 8 && 4u * lane < w) ? __ldg(reinterpret_cast<const float4*>(qr + k0) + lane)
-                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-            __syncwarp();
-#pragma unroll
-            for (int sg = 0; sg < 8; ++sg)
-                *reinterpret_cast<float4*>(rs + (4 * sg + sub) * kFsRS + 4 * c4) = v[sg];
-            if (lane < 8) *reinterpret_cast<float4*>(qs + 4 * lane) = qv;
-            __syncwarp();
-            if (e < n) {
-                const float* os = rs + lane * kFsRS;
-                for (uint32_t kk = 0; kk < w; kk += 4) {
-                    const float4 o4 = *reinterpret_cast<const float4*>(os + kk);
-                    const float4 q4 = *reinterpret_cast<const float4*>(qs + kk);
-                    acc = sq_step(acc, q4.x, o4.x);
-                    acc = sq_step(acc, q4.y, o4.y);
-                    acc = sq_step(acc, q4.z, o4.z);
-                    acc = sq_step(acc, q4.w, o4.w);
-                }
-            }
-        }
+        const float acc = exact_l2_round(cen, qr, dim, my_c, nv, e < n, rs, qs, lane);
         __syncwarp();
         if (e < n) cand[e] = make_key(acc, my_c);
     }

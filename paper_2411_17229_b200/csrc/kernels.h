@@ -197,13 +197,9 @@ cudaError_t launch_coarse_tc(const float* centroids, uint32_t n_cen, const float
 // prep.cu
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s);
 // seed.cu: the list-major radius seed with a TMA/mbarrier pipeline (dim <= 256, K <= 128)
-// dims per TMA slice of the seed's ring (8: 32B-swizzled row segments, 2 stages in
-// the persistent kernel's 64 KB ring). 4 (16-byte segments, 4 stages) measured slower:
-// 364 -> 377 us, so the ring depth is not what holds the seed back
-#ifndef DADE_SEED_SLICE
-#define DADE_SEED_SLICE 8
-#endif
-constexpr int kSeedSlice = DADE_SEED_SLICE;
+// dims per TMA slice of the persistent seed's ring: {8 dims, 256 rows} boxes, 32-byte
+// row segments, 32B-swizzled (seed.cu)
+constexpr int kSeedSlice = 8;
 struct SeedListArgs {
     const uint32_t* counts;         // rank-bucket-0 query count per list (GroupArgs::counts)
     const uint32_t* bucket_off;

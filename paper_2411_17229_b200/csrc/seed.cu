@@ -1,116 +1,116 @@
-// Radius seed, TMA-pipelined variant of seed_radius_list_kernel (prep.cu) for
-// dim <= 256: one CTA per (nearest list, <= 16 of the queries whose nearest list
-// it is) scores the list's first S <= 1024 rows exactly, and its K best become
-// the queries' first results and radius (same output, bit for bit).
+// Radius seed (K4a), persistent and TMA-pipelined: per (nearest list, <= 16 of
+// the queries whose nearest list it is) the list's first S <= 1024 rows are
+// scored exactly, and each query's K best become its first results and radius
+// (bit for bit what seed_radius_list_kernel in prep.cu computes, which remains
+// for dims the TMA path cannot tile).
 //
-//   warp 8       producer: per 8-dim slice, TMA boxes of {8 dims, 256 rows}
-//                (32B-swizzled) into a 3-stage ring, full/empty mbarriers;
-//   warps 0-7    thread t advances rows t + 256 j (j < kR) x G queries of exact
-//                sequential fp32 sums with packed f32x2 arithmetic (two queries
-//                per instruction, the rounding of sq_step) from the ring slot and
-//                the group's queries (resident, [dim][16]); no CTA barrier inside
-//                the dimension loop, so warps drift and the producer runs ahead;
-//   then         one warp per query: radix-selected K-th distance, ties at it by
-//                id, 128-slot bitonic sort -> out_keys, atomicMin(r_global).
+// One CTA per SM walks the seed groups in the order a global counter hands them
+// out (costliest first, seed_order_kernel):
+//   warp 15       producer: next group id -> gid slot (4 slots, gfull/gempty),
+//                 then the group's 8-dim row slices by TMA ({8 dims, 256 rows}
+//                 32B-swizzled boxes) into a ring of full/empty mbarrier slots;
+//                 slice numbering continues across groups, so the ring stays
+//                 full across group boundaries;
+//   warps 0-7     thread t advances rows t + 256 j (j < kR) x G queries of exact
+//                 sequential fp32 sums with packed f32x2 arithmetic (two queries
+//                 per instruction, the rounding of sq_step) from the ring slot and
+//                 the group's queries (resident, [dim][16]), holding them in
+//                 registers until the group's last slice, then store them in the
+//                 sums buffer once the selection warps freed it (afree / aready);
+//   warps 8-14    selection of group i (one warp per query: radix-selected K-th
+//                 distance, ties at it by id, 128-slot bitonic sort -> out_keys,
+//                 atomicMin(r_global)) while the sum warps already run group i+1.
+//
+// Shared-memory geometry is chosen per launch (SpGeom): slots hold the slice of
+// up to slot_rows = S rounded up to 256, 512 or 1024 rows, so short seeds (256 rows above dim
+// 256) get 8 KB slots and a 16-deep ring, and the ring takes whatever the sums
+// buffer [16][slot_rows] and the resident queries [dim][16] leave: the seed
+// streams up to 1 MB per group with little arithmetic per byte when a group
+// holds few queries, so the bytes in flight per SM set its speed.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc.cuh"
 
 namespace dade_gpu {
 
 namespace {
 
-constexpr int kSdRows = 1024;         // max seeded rows
-constexpr int kSdT = 256;             // compute threads (8 warps)
-constexpr int kSdThreads = kSdT + 32; // + producer warp
-constexpr int kSdG = kSeedGroup;      // queries per CTA (16)
-constexpr int kSdSlice = kSeedSlice;  // dims per ring slot (one 16- or 32-byte row segment)
-constexpr int kSdStages = 24 / kSdSlice;  // 96 KB ring
+constexpr int kSdRowsMax = 1024;      // max seeded rows
 constexpr int kSdBox = 256;           // rows per TMA box
+constexpr int kSdG = kSeedGroup;      // queries per group (16)
+constexpr int kSdSlice = kSeedSlice;  // dims per ring slot (one 32-byte row segment)
 constexpr int kSdSmall = 128;         // sorted slots (K <= 128)
-constexpr int kSdMaxDim = 256;        // resident queries: [dim][16] fp32
+constexpr int kSdMaxDim = 1024;       // resident queries: [dim][16] fp32 <= 64 KB
+constexpr int kSpS = 8;               // sum warps
+constexpr int kSpL = 7;               // selection warps (16 warps in all: 4 per SM sub-partition)
+constexpr int kSpT = kSpS * 32;       // sum threads: rows t + kSpT j
+constexpr int kSpThreads = (kSpS + kSpL + 1) * 32;  // 512
+constexpr int kSpSlots = 4;           // group-id queue
+constexpr int kSpMaxStages = 32;
+constexpr uint32_t kSpEnd = 0xffffffffu;
+constexpr size_t kSpSmemMax = 232448 - 1024;  // opt-in maximum less the reserved 1 KB
 
-__device__ __forceinline__ uint32_t sd_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void sd_mb_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sd_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void sd_mb_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sd_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void sd_mb_arrive_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sd_u32(bar)), "r"(bytes) : "memory");
-}
-// try_wait with a suspend-time hint: a waiting warp sleeps instead of spinning
-__device__ __forceinline__ void sd_mb_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAITS_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-        "@!P1 bra WAITS_%=;\n"
-        "}\n" ::"r"(sd_u32(bar)),
-        "r"(parity), "r"(1000000u)
-        : "memory");
-}
-__device__ __forceinline__ void sd_tma2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-        "[%4];\n" ::"r"(sd_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(sd_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void sd_cp4(float* dst, const float* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sd_u32(dst)), "l"(src) : "memory");
-}
-
-struct SdLayout {
-    size_t ring, qres, bars, total;
+// per-launch shared-memory geometry (byte offsets from a 256-aligned base)
+struct SpGeom {
+    uint32_t slot_rows, slot_bytes, stages;
+    uint32_t ring, accs, qres, keys, hist, gid, bars, total;
 };
-__host__ __device__ inline SdLayout sd_layout() {
-    SdLayout L;
-    size_t off = 0;
-    L.ring = off; off += (size_t)kSdStages * kSdRows * kSdSlice * 4;  // 96 KB; reused for sums / keys / histograms
-    L.qres = off; off += (size_t)kSdMaxDim * kSdG * 4;                // 16 KB
-    L.bars = off; off += 8 * 2 * kSdStages;
-    L.total = off + 256;  // base alignment slack (32B-swizzled TMA destinations need 256 B)
-    return L;
+SpGeom sp_geom(uint32_t dim, uint32_t S) {
+    SpGeom g{};
+    g.slot_rows = S <= 256 ? 256 : S <= 512 ? 512 : 1024;  // the kernel's template instances
+    g.slot_bytes = g.slot_rows * kSdSlice * 4;
+    const uint32_t n_slices = (dim + kSdSlice - 1) / kSdSlice;
+    uint32_t off = 0;
+    const uint32_t accs = (uint32_t)kSdG * g.slot_rows * 4;
+    const uint32_t qres = n_slices * kSdSlice * kSdG * 4;
+    const uint32_t fixed = accs + qres + kSpL * kSdSmall * 8 + kSpL * 256 * 4 + 64 +
+                           8 * (2 * kSpMaxStages + 2 * kSpSlots + 2) + 256;
+    g.stages = fixed >= kSpSmemMax ? 0 : std::min<uint32_t>(kSpMaxStages, (uint32_t)((kSpSmemMax - fixed) / g.slot_bytes));
+    g.ring = off; off += g.stages * g.slot_bytes;
+    g.accs = off; off += accs;
+    g.qres = off; off += qres;
+    g.keys = off; off += kSpL * kSdSmall * 8;
+    g.hist = off; off += kSpL * 256 * 4;
+    g.gid = off; off += 64;
+    g.bars = off; off += 8 * (2 * kSpMaxStages + 2 * kSpSlots + 2);
+    g.total = off + 256;  // base alignment slack (32B-swizzled TMA destinations need 256 B)
+    return g;
 }
 
-// exact sums of rows (tid + 256 j, j < kR) x G queries -> accs[u][row].
-// Slices sl_base .. sl_base + n_slices - 1 of a kStages-deep ring (global slice
-// numbering: the persistent kernel's ring runs across groups). kPersist: the
-// sums go to a separate buffer once afree (if wait_free) completes, and every
-// thread arrives on aready; otherwise they overwrite the ring.
-template <int G, int kR, int kStages, bool kPersist, int kT = kSdT>
-__device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* qres, uint64_t* full, uint64_t* empty,
-                                        uint32_t sl_base, uint32_t n_slices, float* accs, uint64_t nz2,
-                                        uint64_t* afree = nullptr, bool wait_free = false, uint32_t free_parity = 0,
-                                        uint64_t* aready = nullptr) {
+// exact sums of rows (tid + kSpT j, j < kR) x G queries over slices sl_base ..
+// sl_base + n_slices - 1 of the ring (global slice numbering) -> accs[u][row]
+// (row stride slot_rows) once afree (if wait_free) completes; every thread then
+// arrives on aready.
+template <int G, int kR, int kSlotRows>
+__device__ __forceinline__ void sp_sums(const unsigned char* ring, const SpGeom& g, const float* qres,
+                                        uint64_t* full, uint64_t* empty, uint32_t sl_base, uint32_t n_slices,
+                                        float* accs, uint64_t nz2, uint64_t* afree, bool wait_free,
+                                        uint32_t free_parity, uint64_t* aready) {
     const uint32_t tid = threadIdx.x, lane = tid & 31;
     uint64_t acc[kR][G / 2];
 #pragma unroll
     for (int j = 0; j < kR; ++j)
 #pragma unroll
         for (int p = 0; p < G / 2; ++p) acc[j][p] = 0ull;
+    // ring slot and phase of slice sl_base, then advanced incrementally (no
+    // division by the runtime stage count inside the slice loop)
+    uint32_t s = sl_base % g.stages, ph = (sl_base / g.stages) & 1;
     for (uint32_t k = 0; k < n_slices; ++k) {
-        const uint32_t sl = sl_base + k;
-        const uint32_t s = sl % kStages;
-        sd_mb_wait(full + s, (sl / kStages) & 1);
-        const unsigned char* slot = ring + (size_t)s * kSdRows * kSdSlice * 4;
+        mb_wait(full + s, ph);
+        const unsigned char* slot = ring + (size_t)s * (kSlotRows * kSdSlice * 4);
         const float* qb = qres + (size_t)k * kSdSlice * kSdG;
 #pragma unroll
         for (int c = 0; c < kSdSlice / 4; ++c) {
             float o[kR][4];
 #pragma unroll
             for (int j = 0; j < kR; ++j) {
-                const uint32_t r = min(tid + j * kT, (uint32_t)kSdRows - 1);  // rows >= 1024 (kT = 384): never stored
-                // 4-dim slices: 16-byte rows, unswizzled; 8-dim: 32B-swizzled, 16-byte chunk c ^ row bit 2
-                const float4 x = kSdSlice == 4
-                                     ? *reinterpret_cast<const float4*>(slot + r * 16)
-                                     : *reinterpret_cast<const float4*>(slot + r * 32 + (((uint32_t)c ^ (r >> 2)) & 1u) * 16);
+                const uint32_t r = min(tid + j * kSpT, (uint32_t)kSlotRows - 1);
+                // 8-dim slices: 32-byte rows, 32B-swizzled (16-byte chunk c ^ row bit 2)
+                const float4 x = *reinterpret_cast<const float4*>(slot + r * 32 + (((uint32_t)c ^ (r >> 2)) & 1u) * 16);
                 o[j][0] = x.x;
                 o[j][1] = x.y;
                 o[j][2] = x.z;
@@ -133,26 +133,24 @@ __device__ __forceinline__ void sd_sums(const unsigned char* ring, const float* 
             }
         }
         __syncwarp();
-        if (lane == 0) sd_mb_arrive(empty + s);  // this warp is done with the slot
+        if (lane == 0) mb_arrive(empty + s);  // this warp is done with the slot
+        if (++s == g.stages) {
+            s = 0;
+            ph ^= 1;
+        }
     }
-    if (kPersist) {
-        if (wait_free) sd_mb_wait(afree, free_parity);
-    } else {
-        // the ring is reused for the sums: every warp must be past its last slot
-        asm volatile("bar.sync 1, %0;\n" ::"r"(kSdT));
-    }
+    if (wait_free) mb_wait(afree, free_parity);
 #pragma unroll
     for (int j = 0; j < kR; ++j)
 #pragma unroll
         for (int p = 0; p < G / 2; ++p) {
-            const uint32_t r = tid + j * kT;
-            if (kT * kR <= kSdRows || r < (uint32_t)kSdRows) {
-                accs[(2 * p) * kSdRows + r] = lo_f(acc[j][p]);
-                accs[(2 * p + 1) * kSdRows + r] = hi_f(acc[j][p]);
+            const uint32_t r = tid + j * kSpT;
+            if (kSpT * kR <= kSlotRows || r < (uint32_t)kSlotRows) {
+                accs[(2 * p) * kSlotRows + r] = lo_f(acc[j][p]);
+                accs[(2 * p + 1) * kSlotRows + r] = hi_f(acc[j][p]);
             }
         }
-    if (kPersist) sd_mb_arrive(aready);
-    else asm volatile("bar.sync 1, %0;\n" ::"r"(kSdT));
+    mb_arrive(aready);
 }
 
 template <int NV>
@@ -214,15 +212,15 @@ __device__ __forceinline__ void sd_bitonic(uint64_t* kk, uint32_t m, uint32_t la
 }
 
 // One warp: the K smallest exact sums of query q over rows [0, n) of the list at
-// start (acc[r]) by (sqrt distance, id) -> sorted keys out_keys[q], radius
-// atomicMin(r_global[q]). kk: 128 keys, hist: 256 words (per warp, shared).
-__device__ __forceinline__ void sd_finish_query(const SeedListArgs& a, uint32_t q, const float* accs, uint32_t u,
-                                             uint32_t n, uint32_t start, uint64_t* kk, uint32_t* hist) {
+// start (acc[r], row stride of the sums buffer) by (sqrt distance, id) -> sorted
+// keys out_keys[q], radius atomicMin(r_global[q]). kk: 128 keys, hist: 256
+// words (per warp, shared).
+__device__ __forceinline__ void sd_finish_query(const SeedListArgs& a, uint32_t q, const float* acc, uint32_t n,
+                                                uint32_t start, uint64_t* kk, uint32_t* hist) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t* row_ids = a.row_ids;
     const uint32_t K = a.K;
-    const float* acc = accs + u * kSdRows;
-    constexpr int kNV = kSdRows / 32;
+    constexpr int kNV = kSdRowsMax / 32;
     uint32_t dv[kNV];
 #pragma unroll
     for (int i = 0; i < kNV; ++i) {
@@ -269,46 +267,6 @@ __device__ __forceinline__ void sd_finish_query(const SeedListArgs& a, uint32_t 
     }
 }
 
-
-
-// ---- persistent, warp-specialised seed ------------------------------------------
-// One CTA per SM walks the seed groups in the order a global counter hands them
-// out (largest-first is not needed: a group is ~1/7 of a CTA's share):
-//   warp 15       producer: next group id -> gid slot (4 slots, gfull/gempty),
-//                 then its 8-dim slices by TMA into a 2-stage ring (full/empty,
-//                 slice numbering continues across groups);
-//   warps 0-7     sums (sd_sums, as seed_tma_kernel) into accs[i & 1] once the
-//                 selection warps freed it (afree), then aready;
-//   warps 8-14    selection (sd_finish_query) of group i while the sum warps
-//                 already run group i + 1, so the FMA pipe never idles on it.
-#ifndef DADE_SP_SUM_WARPS
-#define DADE_SP_SUM_WARPS 8
-#endif
-constexpr int kSpS = DADE_SP_SUM_WARPS;            // sum warps
-constexpr int kSpL = 15 - kSpS;                    // selection warps (16 warps in all: 4 per SM sub-partition)
-constexpr int kSpT = kSpS * 32;                    // sum threads: rows t + kSpT j
-constexpr int kSpThreads = (kSpS + kSpL + 1) * 32;  // 512
-constexpr int kSpStages = 16 / kSdSlice;  // 64 KB ring
-constexpr int kSpSlots = 4;
-constexpr uint32_t kSpEnd = 0xffffffffu;
-
-struct SpLayout {
-    size_t ring, accs, qres, keys, hist, gid, bars, total;
-};
-__host__ __device__ inline SpLayout sp_layout() {
-    SpLayout L;
-    size_t off = 0;
-    L.ring = off; off += (size_t)kSpStages * kSdRows * kSdSlice * 4;  // 64 KB
-    L.accs = off; off += 2ull * kSdG * kSdRows * 4;                   // 128 KB
-    L.qres = off; off += (size_t)kSdMaxDim * kSdG * 4;                // 16 KB
-    L.keys = off; off += (size_t)kSpL * kSdSmall * 8;
-    L.hist = off; off += (size_t)kSpL * 256 * 4;
-    L.gid = off; off += 64;
-    L.bars = off; off += 8 * (2 * kSpStages + 2 * kSpSlots + 4);
-    L.total = off + 256;
-    return L;
-}
-
 struct SpGroup {
     uint32_t start, n, ng;
     const uint32_t* qs;
@@ -325,44 +283,42 @@ __device__ __forceinline__ bool sp_group(const SeedListArgs& a, uint32_t b, SpGr
     G.ng = min((uint32_t)kSdG, cnt_all - g0);
     return true;
 }
-__device__ __forceinline__ int sp_rsel(uint32_t n) { return n > 2u * kSdT ? 4 : n > (uint32_t)kSdT ? 2 : 1; }
 __device__ __forceinline__ int sp_rows_per_thread(uint32_t n) { return (int)((n + kSpT - 1) / kSpT); }
 
-__global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedListArgs a,
+template <int kSlotRows>
+__global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedListArgs a, const SpGeom geom,
                                                                       const __grid_constant__ CUtensorMap tmap,
                                                                       uint32_t* work) {
     extern __shared__ unsigned char sd_raw[];
-    unsigned char* sm = sd_raw + ((256u - (sd_u32(sd_raw) & 255u)) & 255u);
-    const SpLayout L = sp_layout();
-    unsigned char* ring = sm + L.ring;
-    float* accs = reinterpret_cast<float*>(sm + L.accs);  // [2][16][1024]
-    float* qres = reinterpret_cast<float*>(sm + L.qres);  // [dim][16]
-    uint64_t* keys = reinterpret_cast<uint64_t*>(sm + L.keys);
-    uint32_t* hists = reinterpret_cast<uint32_t*>(sm + L.hist);
-    volatile uint32_t* gid = reinterpret_cast<volatile uint32_t*>(sm + L.gid);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + L.bars);
-    uint64_t* empty = full + kSpStages;
-    uint64_t* gfull = empty + kSpStages;
+    unsigned char* sm = sd_raw + ((256u - (su32(sd_raw) & 255u)) & 255u);
+    const SpGeom& g = geom;
+    unsigned char* ring = sm + g.ring;
+    float* accs = reinterpret_cast<float*>(sm + g.accs);  // [16][slot_rows]
+    float* qres = reinterpret_cast<float*>(sm + g.qres);  // [dim][16]
+    uint64_t* keys = reinterpret_cast<uint64_t*>(sm + g.keys);
+    uint32_t* hists = reinterpret_cast<uint32_t*>(sm + g.hist);
+    volatile uint32_t* gid = reinterpret_cast<volatile uint32_t*>(sm + g.gid);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + g.bars);
+    uint64_t* empty = full + kSpMaxStages;
+    uint64_t* gfull = empty + kSpMaxStages;
     uint64_t* gempty = gfull + kSpSlots;
     uint64_t* aready = gempty + kSpSlots;
-    uint64_t* afree = aready + 2;
+    uint64_t* afree = aready + 1;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t n_groups = a.seed_goff[a.n_lists];
     const uint32_t dim = a.dim;
     const uint32_t n_slices = (dim + kSdSlice - 1) / kSdSlice;
     if (tid == 0) {
-        for (int i = 0; i < kSpStages; ++i) {
-            sd_mb_init(full + i, 1);
-            sd_mb_init(empty + i, kSpS);
+        for (uint32_t i = 0; i < g.stages; ++i) {
+            mb_init(full + i, 1);
+            mb_init(empty + i, kSpS);
         }
         for (int j = 0; j < kSpSlots; ++j) {
-            sd_mb_init(gfull + j, 1);
-            sd_mb_init(gempty + j, kSpL);
+            mb_init(gfull + j, 1);
+            mb_init(gempty + j, kSpL);
         }
-        for (int b = 0; b < 2; ++b) {
-            sd_mb_init(aready + b, kSpT);
-            sd_mb_init(afree + b, kSpL);
-        }
+        mb_init(aready, kSpT);
+        mb_init(afree, kSpL);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -370,10 +326,10 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
     if (warp == kSpS + kSpL) {
         // ---- producer ----
         if (lane != 0) return;
-        uint32_t sl = 0;
+        uint32_t s = 0, ph = 0, used = 0;  // ring slot, its phase, slots filled so far (< stages: no wait)
         for (uint32_t i = 0;; ++i) {
             const uint32_t j = i % kSpSlots;
-            if (i >= (uint32_t)kSpSlots) sd_mb_wait(gempty + j, ((i / kSpSlots) - 1) & 1);
+            if (i >= (uint32_t)kSpSlots) mb_wait(gempty + j, ((i / kSpSlots) - 1) & 1);
             uint32_t b;
             SpGroup G;
             for (;;) {
@@ -382,20 +338,24 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
                 if (b >= n_groups || sp_group(a, b, G)) break;
             }
             gid[j] = b < n_groups ? b : kSpEnd;
-            sd_mb_arrive(gfull + j);
+            mb_arrive(gfull + j);
             if (b >= n_groups) return;
             if (a.census) atomicAdd(a.census, (unsigned long long)G.n * G.ng * dim);
             if (a.counters) atomicAdd(a.counters + 2, 4ull * G.n * dim);  // the group's rows, loaded once
-            const uint32_t n_boxes = (uint32_t)sp_rsel(G.n);
+            const uint32_t n_boxes = (G.n + kSdBox - 1) / kSdBox;
             const uint32_t bytes = n_boxes * kSdBox * kSdSlice * 4;
-            for (uint32_t k = 0; k < n_slices; ++k, ++sl) {
-                const uint32_t s = sl % kSpStages;
-                if (sl >= (uint32_t)kSpStages) sd_mb_wait(empty + s, ((sl / kSpStages) - 1) & 1);
-                sd_mb_arrive_tx(full + s, bytes);
-                unsigned char* slot = ring + (size_t)s * kSdRows * kSdSlice * 4;
+            for (uint32_t k = 0; k < n_slices; ++k) {
+                if (used >= g.stages) mb_wait(empty + s, ph ^ 1);  // the slot's previous fill consumed
+                else ++used;
+                mb_arrive_tx(full + s, bytes);
+                unsigned char* slot = ring + (size_t)s * g.slot_bytes;
                 for (uint32_t bx = 0; bx < n_boxes; ++bx)
-                    sd_tma2d(slot + (size_t)bx * kSdBox * kSdSlice * 4, &tmap, (int)(k * kSdSlice),
-                             (int)(G.start + bx * kSdBox), full + s);
+                    tma2d_u(slot + (size_t)bx * kSdBox * kSdSlice * 4, &tmap, (int)(k * kSdSlice),
+                            (int)(G.start + bx * kSdBox), full + s);
+                if (++s == g.stages) {
+                    s = 0;
+                    ph ^= 1;
+                }
             }
         }
     }
@@ -404,30 +364,32 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
         uint32_t sl = 0;
         for (uint32_t i = 0;; ++i) {
             const uint32_t j = i % kSpSlots;
-            sd_mb_wait(gfull + j, (i / kSpSlots) & 1);
+            mb_wait(gfull + j, (i / kSpSlots) & 1);
             const uint32_t b = gid[j];
             if (b == kSpEnd) return;
             SpGroup G;
             sp_group(a, b, G);
             // every sum warp is past the previous group's queries
-            asm volatile("bar.sync 1, %0;\n" ::"r"(kSpS * 32) : "memory");
-            for (uint32_t e = tid; e < dim * kSdG; e += kSpS * 32) {
+            asm volatile("bar.sync 1, %0;\n" ::"r"(kSpT) : "memory");
+            for (uint32_t e = tid; e < dim * kSdG; e += kSpT) {
                 const uint32_t k = e / kSdG, u = e % kSdG;
-                if (u < G.ng) sd_cp4(qres + e, a.queries + (size_t)G.qs[u] * dim + k);
-                else qres[e] = 0.f;
+                if (u < G.ng) {
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(su32(qres + e)),
+                                 "l"(a.queries + (size_t)G.qs[u] * dim + k)
+                                 : "memory");
+                } else {
+                    qres[e] = 0.f;
+                }
             }
-            for (uint32_t e = dim * kSdG + tid; e < n_slices * kSdSlice * kSdG; e += kSpS * 32) qres[e] = 0.f;
+            for (uint32_t e = dim * kSdG + tid; e < n_slices * kSdSlice * kSdG; e += kSpT) qres[e] = 0.f;
             asm volatile("cp.async.wait_all;\n" ::: "memory");
-            asm volatile("bar.sync 1, %0;\n" ::"r"(kSpS * 32) : "memory");
-            const uint32_t buf = i & 1;
-            float* acc = accs + (size_t)buf * kSdG * kSdRows;
-            const bool wf = i >= 2;
-            const uint32_t fp = ((i >> 1) - 1) & 1;
+            asm volatile("bar.sync 1, %0;\n" ::"r"(kSpT) : "memory");
+            const bool wf = i >= 1;
+            const uint32_t fp = (i - 1) & 1;
             const int rsel = sp_rows_per_thread(G.n);
             switch ((G.ng + 1) >> 1) {
-#define SP_R(P, R)                                                                                            \
-    sd_sums<2 * P, R, kSpStages, true, kSpT>(ring, qres, full, empty, sl, n_slices, acc, a.nz2, afree + buf, wf, fp, \
-                                             aready + buf)
+#define SP_R(P, R) \
+    sp_sums<2 * P, R, kSlotRows>(ring, g, qres, full, empty, sl, n_slices, accs, a.nz2, afree, wf, fp, aready)
 #define SP_G(P)                                                 \
     case P:                                                     \
         if (rsel >= 4) SP_R(P, 4);                              \
@@ -446,20 +408,19 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
     const uint32_t lw = warp - kSpS;
     for (uint32_t i = 0;; ++i) {
         const uint32_t j = i % kSpSlots;
-        sd_mb_wait(gfull + j, (i / kSpSlots) & 1);
+        mb_wait(gfull + j, (i / kSpSlots) & 1);
         const uint32_t b = gid[j];
         if (b == kSpEnd) return;
         SpGroup G;
         sp_group(a, b, G);
-        const uint32_t buf = i & 1;
-        sd_mb_wait(aready + buf, (i >> 1) & 1);
-        const float* acc = accs + (size_t)buf * kSdG * kSdRows;
+        mb_wait(aready, i & 1);
         for (uint32_t u = lw; u < G.ng; u += kSpL)
-            sd_finish_query(a, G.qs[u], acc, u, G.n, G.start, keys + lw * kSdSmall, hists + lw * 256);
+            sd_finish_query(a, G.qs[u], accs + (size_t)u * kSlotRows, G.n, G.start, keys + lw * kSdSmall,
+                            hists + lw * 256);
         __syncwarp();
         if (lane == 0) {
-            sd_mb_arrive(afree + buf);
-            sd_mb_arrive(gempty + j);
+            mb_arrive(afree);
+            mb_arrive(gempty + j);
         }
     }
 }
@@ -496,24 +457,32 @@ __global__ void __launch_bounds__(1024) seed_order_kernel(const SeedListArgs a, 
 
 }  // namespace
 
-bool seed_tma_ok(uint32_t dim, uint32_t K) { return dim <= (uint32_t)kSdMaxDim && dim % 4 == 0 && K <= (uint32_t)kSdSmall; }
+bool seed_tma_ok(uint32_t dim, uint32_t K) {
+    return dim <= (uint32_t)kSdMaxDim && dim % 4 == 0 && K <= (uint32_t)kSdSmall && sp_geom(dim, kSdRowsMax).stages >= 2;
+}
 
 cudaError_t launch_seed_tma(const SeedListArgs& a, const CUtensorMap& tmap, uint32_t max_groups, cudaStream_t s,
                             uint32_t* work) {
     if (a.n_lists == 0 || max_groups == 0) return cudaSuccess;
-    if (!work) return cudaErrorInvalidValue;  // the persistent kernel's group counter
-    static_assert((size_t)kSdStages * kSdRows * kSdSlice * 4 >=
-                      (size_t)kSdG * kSdRows * 4 + (kSdT / 32) * (kSdSmall * 8 + 256 * 4),
-                  "sums + keys + histograms must fit in the ring");
-    const size_t sp = sp_layout().total;
+    if (!work || a.S > (uint32_t)kSdRowsMax) return cudaErrorInvalidValue;  // the persistent kernel's group counter
+    const SpGeom g = sp_geom(a.dim, a.S);
+    if (g.stages < 2) return cudaErrorInvalidValue;
     int dev = 0, n_sm = 0;
     DADE_CUDA_TRY(cudaGetDevice(&dev));
     DADE_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-    DADE_CUDA_TRY(cudaFuncSetAttribute(seed_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp));
     DADE_CUDA_TRY(cudaMemsetAsync(work, 0, 4, s));
     if (a.order) seed_order_kernel<<<1, 1024, 0, s>>>(a, a.order);
-    seed_persist_kernel<<<std::min<uint32_t>(max_groups, (uint32_t)n_sm), kSpThreads, sp, s>>>(a, tmap, work);
-    return cudaGetLastError();
+    const uint32_t grid = std::min<uint32_t>(max_groups, (uint32_t)n_sm);
+    auto run = [&](auto kern) -> cudaError_t {
+        DADE_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.total));
+        kern<<<grid, kSpThreads, g.total, s>>>(a, g, tmap, work);
+        return cudaGetLastError();
+    };
+    // slot rows as a compile-time constant: the sums' row and slot arithmetic
+    // stays immediate (a runtime stride cost the D <= 256 seed 3%)
+    if (g.slot_rows <= 256) return run(seed_persist_kernel<256>);
+    if (g.slot_rows <= 512) return run(seed_persist_kernel<512>);
+    return run(seed_persist_kernel<1024>);
 }
 
 }  // namespace dade_gpu

@@ -24,7 +24,10 @@ def main(name="config1", warm=3):
     cfg = CONFIGS[name]
     art = ensure_artifacts(cfg, gt_queries=2000, log=lambda *a: print(*a, file=sys.stderr))
     dev = gp.Device(0)
-    idx = gp.IvfIndex.from_divf(dev, read_divf(art / "index.ivf"))
+    if cfg.flat:
+        idx = gp.FlatIndex(dev, read_fvecs(art / "base.fvecs"))
+    else:
+        idx = gp.IvfIndex.from_divf(dev, read_divf(art / "index.ivf"))
     dco = gp.DadeStrategy(read_transform(art / "t.dade"), read_cal(art / "c.cal"), cfg.delta_d, dev=dev)
     dev.apply(dco)
     q = torch.from_numpy(read_fvecs(art / "queries.fvecs")).cuda()
@@ -35,6 +38,11 @@ def main(name="config1", warm=3):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     def search():
+        if cfg.flat:
+            _capi.check(_capi.lib.dade_gpu_flat_search(dev.h, _capi.ptr(q), nq, k,
+                                                       _capi.QUERIES_RAW | _capi.DEVICE_PTRS, _capi.ptr(oi),
+                                                       _capi.ptr(od), _capi.ptr(oc), None))
+            return
         _capi.check(_capi.lib.dade_gpu_ivf_search(dev.h, _capi.ptr(q), nq, k, cfg.nprobe,
                                                   _capi.QUERIES_RAW | _capi.DEVICE_PTRS, _capi.ptr(oi),
                                                   _capi.ptr(od), _capi.ptr(oc), None))
