@@ -15,7 +15,9 @@ under /tmp; both arms load the same files):
   * N = 1: config 1 (1M x 256, 10k queries, nlist 1024, nprobe 32, K 100,
     dd 32, p_s .1). The same line carries a `config2` block (1M x 960, 1k
     queries, nprobe 64, K 20, dd 64, p_s .05), the long-vector config the
-    north_star's HBM target is about.
+    north_star's HBM target is about, and a `config4` block (the flat
+    exhaustive scan, 2M x 768, 4096 queries per batch, K 10) with the
+    reference's linear_scan timed on a query sample on all host threads.
   * N > 1 (one process per GPU; started here under torch.distributed.run when
     WORLD_SIZE is unset): config 3 (10M x 128, nlist 16384, 100k queries,
     nprobe 64, K 100) list-sharded over the N GPUs, strong scaling (the 100k
@@ -189,7 +191,10 @@ def ncu_scan_traffic(cfg_name: str):
     d = json.loads(p.read_text())
     ls = d["launches"]
     # one search: from its seed launch to the end of the list
-    starts = [i for i, x in enumerate(ls) if x["kernel"].startswith("seed_")]
+    starts = [i for i, x in enumerate(ls) if x["kernel"].startswith(("seed_order", "seed_persist", "seed_radius"))]
+    if starts:  # the seed order kernel (when present) directly precedes the seed
+        while starts[-1] > 0 and ls[starts[-1] - 1]["kernel"].startswith("seed_order"):
+            starts[-1] -= 1
     if starts:
         ls = ls[starts[-1]:]
     ls = [x for x in ls if x["kernel"].startswith(SCAN_KERNELS)]
@@ -525,6 +530,64 @@ def single_gpu_workload(args, cfg, dev, device, stream, flush, with_e2e=True, wi
     return out
 
 
+def flat_workload(args, cfg, dev, device, stream, flush):
+    """Config 4, the flat exhaustive DADE scan (dade_gpu_flat_search): device time
+    per 4096-query batch (raw queries resident, L2 flushed, CUDA events), recall,
+    and the reference's linear_scan (knn.cpp:31-41) on a bounded query sample
+    with all host threads, on the same rotated base, transform and calibration."""
+    import torch
+
+    import paper_2411_17229_b200 as gp
+    from oracle import RefLib, read_fvecs as ref_read_fvecs
+    from paper_2411_17229_b200 import _capi
+    from paper_2411_17229_b200.io import read_cal, read_fvecs, read_ivecs, read_transform
+    from paper_2411_17229_b200.workloads import artifact_dir, ensure_artifacts
+    art = artifact_dir(cfg)
+    if not (art / "DONE").exists():
+        art = ensure_artifacts(cfg, gt_queries=GT_SAMPLE, log=log)
+    base = read_fvecs(art / "base.fvecs")
+    idx = gp.FlatIndex(dev, base)
+    dco = gp.DadeStrategy(read_transform(art / "t.dade"), read_cal(art / "c.cal"), cfg.delta_d, dev=dev)
+    dev.apply(dco)
+    dev.set_stream(stream.cuda_stream)
+    q_raw = read_fvecs(art / "queries.fvecs")
+    q_dev = torch.from_numpy(q_raw).to(device)
+    gt = read_ivecs(art / "gt.ivecs").astype(np.uint32)
+    nq, k = q_dev.shape[0], cfg.k
+    out_ids = torch.empty((nq, k), dtype=torch.int32, device=device)
+    out_d = torch.empty((nq, k), dtype=torch.float32, device=device)
+    out_c = torch.empty((nq,), dtype=torch.int32, device=device)
+
+    def step():
+        _capi.check(_capi.lib.dade_gpu_flat_search(dev.h, _capi.ptr(q_dev), nq, k,
+                                                   _capi.QUERIES_RAW | _capi.DEVICE_PTRS, _capi.ptr(out_ids),
+                                                   _capi.ptr(out_d), _capi.ptr(out_c), None))
+    ms = time_device(step, stream, flush, min(args.steps, 5), min(args.warmup, 3))
+    mean_ms = float(np.mean(ms))
+    ids_np = out_ids.cpu().numpy().astype(np.uint32)
+    cnt_np = out_c.cpu().numpy().astype(np.uint32)
+    out = {"workload": cfg.describe(), "value": nq / (mean_ms / 1e3), "unit": UNIT, "ms_per_step": mean_ms,
+           "recall_at_k": recall(ids_np[:gt.shape[0]], cnt_np[:gt.shape[0]], gt),
+           "timing": "CUDA events, raw queries resident, L2 flushed, mean of the timed batches"}
+    try:
+        ref = RefLib()
+        t = ref.load_transform(art / "t.dade")
+        cal = ref.cal_load(art / "c.cal")
+        strat = ref.strategy_dade(t, cal, cfg.delta_d)
+        threads = os.cpu_count() or 1
+        m = min(gt.shape[0], max(2 * threads, 32))
+        q_rot = t.apply(ref_read_fvecs(art / "queries.fvecs")[:m])
+        rids, _, rcnt, _, sec = ref.linear_scan(base, strat, q_rot, k, threads=threads)
+        out["reference"] = {"value": m / sec, "unit": UNIT, "cores": threads, "kind": "reference",
+                            "sample": f"first {m} queries, linear_scan + DadeStrategy (oracle/_ref/libdade_ref.so) "
+                                      f"over the same rotated base, {threads} host threads",
+                            "recall_at_k_sample": recall(rids, rcnt, gt[:m]),
+                            "ours_recall_at_k_same_sample": recall(ids_np[:m], cnt_np[:m], gt[:m])}
+    except Exception as e:  # reported, never fatal to the GPU line
+        out["reference"] = {"value": None, "sample": f"failed: {e}"}
+    return out
+
+
 # ---- ours ------------------------------------------------------------------------------
 def run_ours_single(args, cfg):
     import torch
@@ -560,6 +623,12 @@ def run_ours_single(args, cfg):
                                "clocks": c2["clocks"]}
         except Exception as e:  # reported, never fatal to the headline line
             line["config2"] = {"error": repr(e)}
+    if not args.no_config4 and cfg.name == "config1":
+        try:
+            torch.cuda.empty_cache()
+            line["config4"] = flat_workload(args, CONFIGS["config4"], gp.Device(0), device, stream, flush)
+        except Exception as e:  # reported, never fatal to the headline line
+            line["config4"] = {"error": repr(e)}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -719,6 +788,7 @@ def main():
     ap.add_argument("--cpu-baseline-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=6.0)
     ap.add_argument("--no-config2", action="store_true")
+    ap.add_argument("--no-config4", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     n_gpus = max(args.gpus, world)
