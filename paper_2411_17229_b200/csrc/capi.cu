@@ -415,8 +415,6 @@ struct dade_gpu_ctx {
     TmapCache tm_q128{128}, tm_c256{256};  // query-major fused coarse selection
     TmapCache tm32_storage{32}, tm32_base{32};
     RowNorms norms_storage, norms_base;
-    RowNorms full_norms_storage, full_norms_base;  // |o|^2 over all dims (tensor-core seed bounds)
-    DevBuf seed_scratch;  // tensor-core seed: per-CTA [2][16][1024] exact sums
     RowAug aug_storage;
     SliceTmap seed_tm;
     DevBuf seed_work;  // persistent seed's group counter
@@ -908,13 +906,10 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             cuda_check(cudaMemsetAsync(c->row_dims.p, 0, (size_t)std::max<uint32_t>(n_rows, 1) * 4, s), "memset");
         }
         if (seed.on && !resume) {
-            // tensor-core-bounded seed (rows TMA-tiled for the tcgen05 filter, dim % 32 == 0, dim <= 256),
-            // else the dense persistent TMA seed, else the cp.async one; the same output bit for bit
-            const bool tc_seed = g && umma && k <= 128 && seed_tc_ok(a.dim, k) && !env_flag("DADE_GPU_SEED_DENSE");
             const CUtensorMap* stm =
-                (g && k <= 128 && !tc_seed && seed_tma_ok(a.dim, k)) ? c->seed_tm.get(rows, n_rows, a.dim) : nullptr;
-            seed_tma_ran = stm != nullptr || tc_seed;
-            if (stm || tc_seed) {
+                (g && k <= 128 && seed_tma_ok(a.dim, k)) ? c->seed_tm.get(rows, n_rows, a.dim) : nullptr;
+            seed_tma_ran = stm != nullptr;
+            if (stm) {
                 SeedListArgs sa{};
                 sa.counts = g->counts;
                 sa.bucket_off = g->bucket_off;
@@ -944,18 +939,8 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                     sa.census = c->seed_census.as<unsigned long long>();
                     cuda_check(cudaEventRecord(c->es[0], s), "event");
                 }
-                if (tc_seed) {
-                    RowNorms& fnc = flat ? c->full_norms_base : c->full_norms_storage;
-                    const float* fn = fnc.get(rows, n_rows, a.dim, a.dim, s);
-                    c->seed_scratch.ensure(seed_tc_scratch_bytes((uint32_t)c->n_sms));
-                    cuda_check(launch_seed_tc(sa, tm, fn, c->seed_scratch.as<float>(), nq / kSeedGroup + g->n_lists + 1,
-                                              s, c->seed_work.as<uint32_t>()),
-                               "seed radius (tcgen05 bounds)");
-                } else {
-                    cuda_check(launch_seed_tma(sa, *stm, nq / kSeedGroup + g->n_lists + 1, s,
-                                               c->seed_work.as<uint32_t>()),
-                               "seed radius (tma)");
-                }
+                cuda_check(launch_seed_tma(sa, *stm, nq / kSeedGroup + g->n_lists + 1, s, c->seed_work.as<uint32_t>()),
+                           "seed radius (tma)");
                 if (c->profiling) cuda_check(cudaEventRecord(c->es[1], s), "event");
             } else if (g && g->n_rb >= 1 && k <= 128)
                 cuda_check(launch_seed_radius_lists(g->counts, g->bucket_off, g->bucket_q, g->seed_goff, g->seed_glist,
@@ -1824,9 +1809,6 @@ int dade_gpu_destroy(dade_gpu_ctx* c) {
         if (c->h_batch) cudaFreeHost(c->h_batch);
         c->h_batch = nullptr;
         c->norms_storage.buf.release();
-        c->full_norms_storage.buf.release();
-        c->full_norms_base.buf.release();
-        c->seed_scratch.release();
         c->aug_storage.buf.release();
         c->aug_storage.rows = nullptr;
         c->norms_base.buf.release();
@@ -1944,7 +1926,6 @@ int dade_gpu_set_ivf(dade_gpu_ctx* c, uint32_t dim, uint32_t count, uint32_t n_c
         c->count = count;
         c->n_clusters = n_clusters;
         c->norms_storage.rows = nullptr;
-        c->full_norms_storage.rows = nullptr;
         c->aug_storage.rows = nullptr;
         c->h_offsets.assign(offsets, offsets + n_clusters + 1);
         c->dev_offsets = c->h_offsets;
@@ -2008,7 +1989,6 @@ int dade_gpu_set_base(dade_gpu_ctx* c, uint32_t dim, uint32_t count, const float
         upload(c->base, data, (size_t)count * dim * 4, c->stream);
         cuda_check(cudaStreamSynchronize(c->stream), "base upload");
         c->norms_base.rows = nullptr;
-        c->full_norms_base.rows = nullptr;
         c->b_dim = dim;
         c->b_count = count;
         c->b_id_base = id_base;

@@ -221,13 +221,6 @@ struct SeedListArgs {
     unsigned long long* counters;   // nullable: [2] += the rows' bytes each group loads (B_read)
 };
 bool seed_tma_ok(uint32_t dim, uint32_t K);
-// tensor-core-bounded seed (seed.cu seed_tc_kernel): dim % 32 == 0, dim <= 256; same output as launch_seed_tma.
-// tmap128: the rows' 128-row SW128 map (the tcgen05 filter's); full_norms: |o|^2 per row (fp32);
-// scratch: seed_tc_scratch_bytes(SM count) bytes
-bool seed_tc_ok(uint32_t dim, uint32_t K);
-size_t seed_tc_scratch_bytes(uint32_t n_sm);
-cudaError_t launch_seed_tc(const SeedListArgs& a, const CUtensorMap& tmap128, const float* full_norms, float* scratch,
-                           uint32_t max_groups, cudaStream_t s, uint32_t* work);
 // work: one zeroed-per-launch counter word (persistent variant); nullptr: one CTA per group
 cudaError_t launch_seed_tma(const SeedListArgs& a, const CUtensorMap& tmap, uint32_t max_groups, cudaStream_t s,
                             uint32_t* work = nullptr);

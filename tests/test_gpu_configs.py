@@ -289,46 +289,6 @@ def test_k100_d256_seed_persist_fd_exact(gp, oracle_lib, d256):
     assert_same_results(gi, gd, gc, oi, od, oc)
 
 
-@pytest.mark.parametrize("dim,k,nlist,dup", [(256, 100, 24, False), (128, 10, 40, True), (64, 128, 12, False),
-                                               (256, 20, 300, True)])
-def test_tensor_core_seed_matches_dense_seed(gp, oracle_lib, monkeypatch, dim, k, nlist, dup):
-    """seed_tc_kernel (tcgen05 bounds, exact sums only for candidate pairs) gives
-    the dense seed's output bit for bit: whole searches with a pruning strategy
-    (ADS) are identical under both seeds, and the unbounded DADE search equals the
-    oracle's FD search. Cases: lists longer than the seed (K 100, D 256), short
-    lists with partial 128-row blocks and duplicated rows (distance ties broken
-    by id), K = 128 (the largest the seed takes), many small lists."""
-    dev = gp.Device(0)
-    g = np.random.default_rng(dim * 7 + k)
-    n, nq = 30_000 if nlist < 100 else 40_000, 150
-    lam = np.arange(1, dim + 1) ** -1.1
-    centers = g.standard_normal((nlist, dim)) * 4
-    data = (centers[g.integers(0, nlist, n)] + g.standard_normal((n, dim)) * np.sqrt(lam * dim / lam.sum()))
-    data = data.astype(np.float32)
-    if dup:  # exact duplicates: equal distances inside a seed block
-        data[1::7] = data[0::7][: len(data[1::7])]
-    qs = (data[g.integers(0, n, nq)] + 0.3 * g.standard_normal((nq, dim))).astype(np.float32)
-    idx = gp.IvfIndex.build(dev, data, nlist, 8, 3)
-    npb = 5
-    ads = gp.AdsamplingStrategy(dim, 16, 2.1, dev=dev)
-    monkeypatch.setenv("DADE_GPU_SEED_DENSE", "1")
-    di, dd, dc = idx.search_batch(qs, k, npb, ads)
-    monkeypatch.delenv("DADE_GPU_SEED_DENSE")
-    ti, td, tc = idx.search_batch(qs, k, npb, ads)
-    assert_same_results(ti, td, tc, di, dd, dc)
-    t = gp.OrthoTransform(dim, 0, np.zeros(dim), np.linspace(2.0, 0.1, dim), np.eye(dim).reshape(-1))
-    unb = gp.DadeStrategy(t, gp.CalibrationTable.unbounded(dim, 16), 16, dev=dev)
-    dev.set_profiling(True)
-    try:
-        gi, gd, gc = idx.search_batch(qs, k, npb, unb)
-        seed_ms, seed_pd = dev.last_seed_profile()
-    finally:
-        dev.set_profiling(False)
-    assert seed_ms > 0 and seed_pd > 0, "the seed did not run"
-    oi, od, oc, _ = oracle_lib.ivf_search(idx.centroids, idx.offsets, idx.ids, idx.storage, qs, k, npb)
-    assert_same_results(gi, gd, gc, oi, od, oc)
-
-
 def test_hot_path_estimator_values(gp, oracle_lib, ref_lib, d256, monkeypatch, tmp_path):
     """Every checkpoint partial the survivor kernel evaluates (DADE_GPU_DEBUG=1
     sends every pair there, pruned-by-bound ones included) equals
