@@ -1,6 +1,5 @@
 """Seed kernel alone on a BASELINE workload: device time and scored pair-dims
-(dade_gpu_last_seed_profile) of one search, for the default seed and, with
-DADE_GPU_SEED_DENSE=1 in the environment, the dense one.
+(dade_gpu_last_seed_profile) of a few searches.
     python tools/seed_probe.py config1"""
 import sys
 from pathlib import Path
