@@ -386,7 +386,8 @@ def roofline_block(cfg, prof, d0, dim):
                                "definition": "2 * DCO pairs * d0 first-slice flops / filter time; peak = "
                                              f"{bf16_src} / 2 (TF32 dense)"}
     if prof["seed_ms"] > 0:
-        seed_bytes = ncu["per_kernel_bytes"].get("seed_persist_kernel") if ncu else None
+        seed_bytes = (sum(v for kname, v in ncu["per_kernel_bytes"].items() if kname.startswith("seed_persist"))
+                      or None) if ncu else None  # (template instances: seed_persist_kernel<rows>)
         roof["seed_view"] = {"kernel": "seed_persist_kernel", "ms_per_step": prof["seed_ms"],
                              "pair_dims_per_step": prof["seed_pair_dims"],
                              "ncu_dram_bytes": seed_bytes,
