@@ -433,7 +433,7 @@ struct dade_gpu_ctx {
     // profiling
     bool profiling = false;
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
-    cudaEvent_t ef[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // filter launches per pass
+    cudaEvent_t ef[12] = {};  // filter launch start / end per pass (up to the flat scan's six passes)
     cudaEvent_t es[2] = {nullptr, nullptr};  // the persistent seed launch
     bool seed_profiled = false;
     double last_seed_ms = 0, last_seed_pair_dims = 0;

@@ -41,7 +41,7 @@ constexpr int kFSlots = 2;          // private ring depth per warp (per dense bo
 constexpr int kFWarps = 8;
 constexpr int kFThreads = kFWarps * 32;
 constexpr int kFList = 128;         // kept-pair list per warp per round
-constexpr float kTcDeltaF = 4e-3f;  // same bound as scan.cu's kTcDelta
+constexpr float kTcDeltaF = 2.6e-3f;  // same bound as scan.cu's kTcDelta
 
 __device__ __forceinline__ uint32_t smem_u32f(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 

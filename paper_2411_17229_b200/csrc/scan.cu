@@ -47,8 +47,10 @@ constexpr int kNormWin = kRT + 4;  // 16-byte aligned window of row norms per bo
 // accumulation of 8-term steps and the fp32 norms / combination add < 1e-5;
 // the exact sequential fp32 partial differs from the real distance by
 // < 32 * 3 * 2^-24 relative (< 1e-5 of (|o| + |q|)^2). So
-// |p~ - acc| < 2 * 9.8e-4 + 3e-5 < 2.1e-3 of (|o|^2 + |q|^2); 4e-3 leaves ~2x.
-constexpr float kTcDelta = 4e-3f;
+// |p~ - acc| < 2 * 9.8e-4 + 3e-5 < 2.1e-3 of (|o|^2 + |q|^2) (d0 <= 64); 2.6e-3 leaves 24%
+// (4e-3 kept ~1.5x more pairs for the exact survivor pass: the band between the
+// bound and the threshold is what the survivor kernels spend their time on).
+constexpr float kTcDelta = 2.6e-3f;
 
 struct SmemLayout {
     size_t slots, norms, q_res, n_q, r_s, thr_s, qidx, slot, wl_meta, wl_acc, s2_meta, s2_acc, keys, mscratch, bars, total;

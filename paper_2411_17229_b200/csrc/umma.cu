@@ -54,7 +54,7 @@ constexpr int kUMma = kUEpiWarps + 2;     // warp index
 constexpr int kUThreads = (kUEpiWarps + 3) * 32;
 constexpr int kUNB = 2;                   // item (B) buffers
 constexpr uint32_t kUTmemCols = 512;      // 2 accumulator buffers x 256 columns
-constexpr float kUDelta = 4e-3f;          // same bound as filter.cu / scan.cu
+constexpr float kUDelta = 2.6e-3f;        // same bound as filter.cu / scan.cu
 constexpr uint32_t kUSentinel = 0xffffffffu;
 
 struct UItem {  // published by the stager in item buffer ib
