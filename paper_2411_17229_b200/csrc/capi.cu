@@ -1016,6 +1016,14 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 f.n_items = g->n_items + 1;
                 f.piece_lo = flat_lo[pass];
                 f.piece_hi = flat_hi[pass];
+                if (g->piece_major) {  // the pass's items are contiguous: no stager scans past the others
+                    const uint32_t nqc = (nq + g->q_chunk - 1) / g->q_chunk;
+                    const uint32_t skip = n_rows >= g->seed_min ? g->seed_skip : 0u;
+                    const uint32_t np = (n_rows - skip + g->max_item_rows - 1) / g->max_item_rows;
+                    f.range_lo = std::min(flat_lo[pass], np) * nqc;
+                    f.range_hi = std::min(flat_hi[pass], np) * nqc;
+                    if (f.range_hi == 0) f.range_lo = 0;  // (empty base: the counter path)
+                }
             } else if (two_pass) {
                 // pass 0: kFilterItemRows rows of each nearest list past the seed
                 const uint32_t p0 = std::max<uint32_t>(1, kFilterItemRows / rank0_item_rows(umma));
@@ -1308,6 +1316,7 @@ bool flat_stream(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t k, uin
     g.max_item_rows = kFilterItemRows;
     g.rank0_item_rows = 0;
     g.q_chunk = kUmmaQ;
+    g.piece_major = 1;
     g.seed_skip = std::min<uint32_t>(seed_rows(c, k, c->b_dim, true), c->b_count);
     g.seed_min = k;
     const size_t max_items = ((size_t)nq + kUmmaQ - 1) / kUmmaQ * ((c->b_count + kFilterItemRows - 1) / kFilterItemRows) + 1;

@@ -173,8 +173,9 @@ dco_filter_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap tmap) 
     unsigned long long st_dco = 0, st_dims = 0, st_bytes = 0, st_surv = 0, st_viol = 0;
     unsigned long long cs_tiles = 0, cs_ktiles = 0, cs_kept = 0;  // census (lane 0)
     uint32_t k_iter = 0;  // this warp's running ring position (mbarrier phases persist across items)
-    const uint32_t base = a.items ? (a.item_base ? *a.item_base : 0u) : 0u;
-    const uint32_t end = a.items ? *a.n_items : a.flat_qchunks * ((a.flat_rows + a.flat_block - 1) / a.flat_block);
+    const uint32_t base = a.items ? (a.range_hi ? a.range_lo : a.item_base ? *a.item_base : 0u) : 0u;
+    const uint32_t end = a.items ? (a.range_hi ? min(a.range_hi, *a.n_items) : *a.n_items)
+                                 : a.flat_qchunks * ((a.flat_rows + a.flat_block - 1) / a.flat_block);
     auto box = [&](uint32_t slot, int c) { return myboxes + ((size_t)slot * c_dense + c) * kFRows * kBox; };
 
     for (;;) {  // persistent: each warp pulls work items from a global counter

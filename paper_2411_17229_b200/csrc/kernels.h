@@ -76,6 +76,7 @@ struct FilterArgs {
     uint32_t* item_counter;       // persistent scheduling (zeroed before the launch)
     const float* row_norms;       // [rows + 32] first-slice |o|^2 per storage row
     uint32_t piece_lo, piece_hi;  // only items whose row piece is in [piece_lo, piece_hi)
+    uint32_t range_lo = 0, range_hi = 0;  // range_hi > 0: the pass's items are exactly [range_lo, range_hi) (flat, piece major)
     const uint32_t* b0_items;     // nullable: items below *b0_items (rank bucket 0) need piece >= b0_piece_lo
     uint32_t b0_piece_lo;         //   instead (the last IVF pass also takes the nearest lists' tails)
     int debug;                    // 1: re-check every filter prune exactly (counters[3] = violations)
@@ -260,6 +261,7 @@ struct GroupArgs {
     uint32_t rank0_item_rows;       // row piece of rank-bucket-0 entries (0: max_item_rows)
     uint32_t q_chunk;               // queries per work item (kQC; 32 for the streaming filter)
     uint32_t seed_skip, seed_min;   // rank-0 lists of >= seed_min rows skip their first seed_skip rows
+    uint32_t piece_major = 0;       // items ordered row piece major (the flat scan): shared pieces stay L2-hot
     uint32_t* seed_goff;            // nullable [n_lists + 1]: prefix of ceil(rank-0 count / kSeedGroup)
     uint32_t* seed_glist;           // nullable [seed groups]: the list of each seed group
 };

@@ -358,7 +358,12 @@ __global__ void __launch_bounds__(256) group_items_kernel(const GroupArgs g) {
     const uint32_t piece = pr ? pr : max(len, 1u);
     const uint32_t np = max(1u, (len + piece - 1) / piece);
     const uint32_t li = t - g.item_off[e];
-    const uint32_t tq = li / np, p = li - tq * np;  // query chunk major, row piece minor
+    // query chunk major, row piece minor; piece major for the flat scan, so the
+    // consecutive items (started together on different SMs) share one row piece
+    // and read it from HBM once for all query chunks
+    const uint32_t nqc = (c + g.q_chunk - 1) / g.q_chunk;
+    const uint32_t tq = g.piece_major ? li % nqc : li / np;
+    const uint32_t p = g.piece_major ? li / nqc : li - tq * np;
     WorkItem w;
     w.row_start = start + p * piece;
     w.row_count = min(piece, len - p * piece);

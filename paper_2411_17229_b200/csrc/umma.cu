@@ -139,8 +139,8 @@ dco_filter_umma_kernel(const FilterArgs a, const __grid_constant__ CUtensorMap t
 
     if (warp == kUStager) {
         // ============================ stager ============================
-        const uint32_t base = a.item_base ? *a.item_base : 0u;
-        const uint32_t end = *a.n_items;
+        const uint32_t base = a.range_hi ? a.range_lo : a.item_base ? *a.item_base : 0u;
+        const uint32_t end = a.range_hi ? min(a.range_hi, *a.n_items) : *a.n_items;
         long long tp_stage = 0, tp_items = 0;
         for (uint32_t k = 0;; ++k) {
             const uint32_t ib = k % kUNB;
