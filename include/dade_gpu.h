@@ -160,7 +160,10 @@ int dade_gpu_ivf_search_batches(dade_gpu_ctx* ctx, uint32_t n_batches, const flo
                                 uint32_t* const* out_ids, float* const* out_dists,
                                 uint32_t* const* out_counts, dade_gpu_stats* stats);
 
-/* Batched linear_scan over the flat base. */
+/* Batched linear_scan over the flat base. After dade_gpu_flat_partition the
+ * scan visits the base in data order (every partition probed, each query's
+ * nearest partition first), else in row order; either way every base row is a
+ * candidate and FD results are identical (ties by id). */
 int dade_gpu_flat_search(dade_gpu_ctx* ctx, const float* queries, uint32_t nq, uint32_t k,
                          uint32_t flags, uint32_t* out_ids, float* out_dists,
                          uint32_t* out_counts, dade_gpu_stats* stats);
@@ -330,6 +333,22 @@ uint64_t dade_gpu_launch_count(dade_gpu_ctx* ctx);
  * scores exactly; 0 restores the default (1024, ~1 MB of rows per IVF list above
  * dim 256). A tuning knob: fewer seeded rows give a looser first radius. */
 int dade_gpu_set_seed_rows(dade_gpu_ctx* ctx, uint32_t rows);
+
+/* Repeated IVF searches of one shape replay a captured CUDA graph of the search
+ * body (coarse ranking .. merges; the first call runs eagerly, the second is
+ * captured). 0 turns the capture off for this handle (every search eager),
+ * 1 (the default) back on. Results are identical either way. */
+int dade_gpu_set_graphs(dade_gpu_ctx* ctx, int on);
+
+/* Data-ordered flat scan: partitions the uploaded flat base (dade_gpu_set_base)
+ * into n_parts k-means cells on the GPU (kmeans of proj/src/ivf.cpp:24-143,
+ * max_iters, seed), which become this handle's IVF index (replacing any
+ * uploaded one); dade_gpu_flat_search then probes every cell, the query's
+ * nearest first, so its radius is tight from the first rows scanned. The
+ * visiting order of linear_scan (proj/src/knn.cpp:31-41) changes, the candidate
+ * set does not. n_parts = 0 drops the partition (row-order scan). A later
+ * dade_gpu_set_base / _set_ivf / _ivf_build drops it too. */
+int dade_gpu_flat_partition(dade_gpu_ctx* ctx, uint32_t n_parts, uint32_t max_iters, uint64_t seed);
 
 /* Measured device time (ms) of the DCO scan kernel(s) in the last search
  * call, via CUDA events on the launching stream, and its algorithmic bytes

@@ -74,6 +74,8 @@ def _load():
         "dade_gpu_coarse_probes": ([P, P, U32, U32, U32, P, P], I),
         "dade_gpu_flat_search_keys_begin": ([P, P, U32, U32, U32, P, P], I),
         "dade_gpu_set_seed_rows": ([P, U32], I),
+        "dade_gpu_set_graphs": ([P, I], I),
+        "dade_gpu_flat_partition": ([P, U32, U32, U64], I),
         "dade_gpu_ivf_search_keys_end": ([P, P, P], I),
         "dade_gpu_flat_search_keys": ([P, P, U32, U32, U32, P, P], I),
         "dade_gpu_merge_keys": ([P, P, U32, U32, U32, P, P, P], I),
@@ -118,7 +120,7 @@ EXPORTED = [
     "dade_gpu_set_strategy_dade", "dade_gpu_set_strategy_ads", "dade_gpu_rotate",
     "dade_gpu_ivf_search", "dade_gpu_ivf_search_batches", "dade_gpu_flat_search", "dade_gpu_ivf_search_keys",
     "dade_gpu_ivf_search_keys_begin", "dade_gpu_ivf_search_keys_end", "dade_gpu_coarse_probes",
-    "dade_gpu_flat_search_keys_begin", "dade_gpu_set_seed_rows",
+    "dade_gpu_flat_search_keys_begin", "dade_gpu_set_seed_rows", "dade_gpu_set_graphs", "dade_gpu_flat_partition",
     "dade_gpu_flat_search_keys", "dade_gpu_merge_keys", "dade_gpu_dco_evaluate",
     "dade_gpu_partial_sums", "dade_gpu_calibrate", "dade_gpu_launch_count",
     "dade_gpu_set_profiling", "dade_gpu_last_scan_profile", "dade_gpu_debug_counters",

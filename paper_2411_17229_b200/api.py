@@ -79,6 +79,10 @@ class Device:
     def set_profiling(self, on: bool):
         check(_capi.lib.dade_gpu_set_profiling(self.h, int(on)))
 
+    def set_graphs(self, on: bool):
+        """Replay captured CUDA graphs of repeated IVF searches (default on)."""
+        check(_capi.lib.dade_gpu_set_graphs(self.h, int(on)))
+
     def last_filter_profile(self):
         ms, n = C.c_double(), C.c_int()
         check(_capi.lib.dade_gpu_last_filter_profile(self.h, C.byref(ms), C.byref(n)))
@@ -495,7 +499,16 @@ class FlatIndex:
         if d.ndim != 2 or d.shape[1] == 0:
             raise InvalidInput("VectorSet: dim must be positive")
         self.dim, self.count = d.shape[1], d.shape[0]
+        self.parts = 0
         check(_capi.lib.dade_gpu_set_base(dev.h, self.dim, self.count, ptr(d), id_base))
+
+    def partition(self, n_parts: int, max_iters: int = 10, seed: int = 1):
+        """Data-ordered scan (dade_gpu_flat_partition): k-means cells of the base
+        on the GPU become the visiting order (every cell probed, each query's
+        nearest first). Replaces the Device's IVF index; 0 drops it."""
+        check(_capi.lib.dade_gpu_flat_partition(self.dev.h, int(n_parts), int(max_iters), int(seed)))
+        self.parts = int(n_parts)
+        return self
 
     def search_batch(self, queries, k: int, dco, stats: DcoStats | None = None, raw: bool = False):
         q = _f32(queries)

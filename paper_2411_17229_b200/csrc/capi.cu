@@ -8,6 +8,7 @@
 // so it is capturable in a CUDA graph; the host only synchronises when it has
 // to copy results or counters back.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <utility>
 #include <cmath>
@@ -68,11 +69,16 @@ int guarded(F&& f) {
     }
 }
 
+// Bumped on every device (re)allocation: a captured search graph bakes buffer
+// addresses into its launches, so its cache key carries this epoch.
+uint64_t g_alloc_epoch = 0;
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
     void* ensure(size_t bytes) {
         if (bytes <= cap && p) return p;
+        ++g_alloc_epoch;
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
@@ -84,7 +90,10 @@ struct DevBuf {
     template <class T>
     T* as() const { return static_cast<T*>(p); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            cudaFree(p);
+            ++g_alloc_epoch;
+        }
         p = nullptr;
         cap = 0;
     }
@@ -377,6 +386,7 @@ struct dade_gpu_ctx {
     bool has_base = false;
     uint32_t b_dim = 0, b_count = 0, b_id_base = 0;
     DevBuf base;
+    uint32_t flat_parts = 0;  // > 0: the IVF index holds the flat base in n k-means cells (dade_gpu_flat_partition)
 
     // strategy
     bool has_strategy = false;
@@ -448,6 +458,23 @@ struct dade_gpu_ctx {
     bool tl_on = false;
     double last_scan_ms = 0, last_bytes = 0, last_total_ms = 0, last_filter_ms = 0;
 
+    // CUDA graphs of the search body (search_graphed): key = everything its
+    // launches bake in (pointers, shapes, host-side decisions, allocation and
+    // configuration epochs); the host state the body leaves is replayed too
+    struct GraphEntry {
+        std::array<uint64_t, 14> key{};
+        cudaGraphExec_t exec = nullptr;
+        uint64_t launches = 0, lru = 0;
+        uint32_t surv_cap_used = 0;
+        int n_filter_passes = 0;
+        bool coarse_tc_used = false, fo_done = false;
+    };
+    std::vector<GraphEntry> graphs;
+    std::array<uint64_t, 14> graph_seen{};  // key of the last body run eagerly (captured on a repeat)
+    uint64_t cfg_epoch = 0, graph_tick = 0;
+    bool graphs_on = true;
+    void config_changed() { ++cfg_epoch; }
+
     void use_device() const { cuda_check(cudaSetDevice(device), "cudaSetDevice"); }
 };
 
@@ -494,6 +521,7 @@ void set_tables(dade_gpu_ctx* c, uint32_t kind, uint32_t dim, std::vector<uint32
     upload(c->d_scale, c->scale.data(), c->scale.size() * 8, c->stream);
     cuda_check(cudaStreamSynchronize(c->stream), "strategy upload");
     c->has_strategy = true;
+    c->config_changed();
 }
 
 bool coarse_tc_ok(dade_gpu_ctx* c, uint32_t n_probe) {
@@ -985,8 +1013,15 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         for (int pass = 0; pass < n_pass; ++pass) {
             if (resume && pass < split_pass) continue;  // phase 2: from the split pass on
             if (stop && pass == split_pass) break;      // phase 1: everything before it
-            if (pass == n_pass - 1 && c->qin_free_recorded)
-                cuda_check(cudaEventRecord(c->copy_ev[8], s), "event");
+            if (pass == n_pass - 1 && c->qin_free_recorded) {
+                // (inside a graph capture: an event-record node the next staging's copy stream waits on)
+                cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                cuda_check(cudaStreamIsCapturing(s, &cs), "capture status");
+                cuda_check(cs == cudaStreamCaptureStatusActive
+                               ? cudaEventRecordWithFlags(c->copy_ev[8], s, cudaEventRecordExternal)
+                               : cudaEventRecord(c->copy_ev[8], s),
+                           "event");
+            }
             cuda_check(cudaMemsetAsync(c->surv_count.p, 0, 4, s), "memset");
             FilterArgs f{};
             f.queries = d_q;
@@ -1569,10 +1604,104 @@ bool search_overflowed(dade_gpu_ctx* c) {
     return false;
 }
 
+// The search body (coarse ranking, grouping, the DCO scan, merges: ~30 launches
+// and memsets on one stream, no host sync) as a CUDA graph. The first run of a
+// key is eager (it sizes every workspace, tensor map and cached row operand),
+// a repeat is captured, later ones replay the instantiated graph: the GPU then
+// runs the launches back to back instead of waiting on each launch's issue.
+// Off for diagnostic runs (profiling, timeline, failure accounting, estimate
+// dumps, two-phase searches, DADE_GPU_DEBUG) and with DADE_GPU_NO_GRAPH=1.
+bool graph_usable(const dade_gpu_ctx* c) {
+    static const bool env_off = env_flag("DADE_GPU_NO_GRAPH") || std::getenv("DADE_GPU_DEBUG") ||
+                                std::getenv("DADE_GPU_SURV_CAP");
+    return c->graphs_on && !env_off && !c->profiling && !c->tl_on && !c->measure && !c->dump_cap && c->split == 0 &&
+           c->stream != nullptr && c->stream != cudaStreamLegacy && c->stream != cudaStreamPerThread;
+}
+
+void search_graphed(dade_gpu_ctx* c, uint64_t tag, const float* d_q, uint32_t nq, uint32_t k, uint64_t* ok,
+                    uint32_t* oc, const std::function<void(const float*, uint64_t*, uint32_t*)>& run) {
+    if (!tag || !graph_usable(c)) {
+        run(d_q, ok, oc);
+        return;
+    }
+    const std::array<uint64_t, 14> key = {
+        tag,
+        reinterpret_cast<uint64_t>(d_q),
+        reinterpret_cast<uint64_t>(ok),
+        reinterpret_cast<uint64_t>(oc),
+        reinterpret_cast<uint64_t>(c->fo.ids),
+        reinterpret_cast<uint64_t>(c->fo.dists),
+        reinterpret_cast<uint64_t>(c->fo.counts),
+        ((uint64_t)nq << 32) | k,
+        reinterpret_cast<uint64_t>(c->stream),
+        g_alloc_epoch,
+        c->cfg_epoch,
+        c->surv_cap_hint,
+        (uint64_t)c->probes_ready | ((uint64_t)c->coarse_force_exact << 1) | ((uint64_t)c->sharded << 2),
+        (uint64_t)c->seed_rows_set};
+    for (auto& e : c->graphs)
+        if (e.key == key) {
+            cuda_check(cudaGraphLaunch(e.exec, c->stream), "graph launch");
+            e.lru = ++c->graph_tick;
+            c->launches += e.launches;
+            c->surv_cap_used = e.surv_cap_used;
+            c->n_filter_passes = e.n_filter_passes;
+            c->coarse_tc_used = e.coarse_tc_used;
+            c->fo.done = e.fo_done;
+            c->probes_ready = false;
+            return;
+        }
+    if (c->graph_seen != key) {  // first sighting: eager
+        run(d_q, ok, oc);
+        c->graph_seen = key;
+        return;
+    }
+    const uint64_t l0 = c->launches;
+    cudaGraph_t g = nullptr;
+    cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+        run(d_q, ok, oc);
+    } catch (...) {
+        cudaStreamEndCapture(c->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        throw;
+    }
+    cuda_check(cudaStreamEndCapture(c->stream, &g), "end capture");
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t ie = g_alloc_epoch == key[9] ? cudaGraphInstantiate(&ex, g, 0) : cudaErrorInvalidValue;
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {  // (a workspace grew during the capture: run it eagerly, capture next time)
+        cudaGetLastError();
+        c->launches = l0;
+        run(d_q, ok, oc);
+        c->graph_seen = {};
+        return;
+    }
+    if (c->graphs.size() >= 6) {  // evict the least recently used
+        auto it = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                   [](const auto& a, const auto& b) { return a.lru < b.lru; });
+        cudaGraphExecDestroy(it->exec);
+        c->graphs.erase(it);
+    }
+    dade_gpu_ctx::GraphEntry e;
+    e.key = key;
+    e.exec = ex;
+    e.launches = c->launches - l0;
+    e.lru = ++c->graph_tick;
+    e.surv_cap_used = c->surv_cap_used;
+    e.n_filter_passes = c->n_filter_passes;
+    e.coarse_tc_used = c->coarse_tc_used;
+    e.fo_done = c->fo.done;
+    c->graphs.push_back(e);
+    cuda_check(cudaGraphLaunch(ex, c->stream), "graph launch");
+}
+
 // Common driver: results as ids/dists/counts (host or device).
 void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t dim, uint32_t k,
                    uint32_t flags, uint32_t* out_ids, float* out_dists, uint32_t* out_counts,
-                   dade_gpu_stats* stats, const std::function<void(const float*, uint64_t*, uint32_t*)>& run) {
+                   dade_gpu_stats* stats, const std::function<void(const float*, uint64_t*, uint32_t*)>& run,
+                   uint64_t graph_tag = 0) {
     c->use_device();
     cudaStream_t s = c->stream;
     c->counters.ensure(kCounterBytes);
@@ -1604,7 +1733,7 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     bool fused = false;
     {
         FusedOutputs scope(c, ids, dists, cnts);
-        run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
+        search_graphed(c, graph_tag, d_q, nq, k, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), run);
         fused = c->fo.done;
     }
     tl_mark(c, "searched", s);
@@ -1625,7 +1754,7 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
     enqueue_flags(c);
     wait_stream(s);
     if (search_overflowed(c)) {  // survivor worklist too small: redo with the observed size x2
-        search_common(c, queries, nq, dim, k, flags, out_ids, out_dists, out_counts, stats, run);
+        search_common(c, queries, nq, dim, k, flags, out_ids, out_dists, out_counts, stats, run, graph_tag);
         return;
     }
     if (c->coarse_tc_used) {
@@ -1635,7 +1764,7 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
         if (ov) {
             c->coarse_force_exact = true;
             try {
-                search_common(c, queries, nq, dim, k, flags, out_ids, out_dists, out_counts, stats, run);
+                search_common(c, queries, nq, dim, k, flags, out_ids, out_dists, out_counts, stats, run, graph_tag);
             } catch (...) {
                 c->coarse_force_exact = false;
                 throw;
@@ -1658,7 +1787,8 @@ void search_common(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint32_t 
 // search_common (same results as a sequence of single searches).
 void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, uint32_t nq, uint32_t dim, uint32_t k,
                     uint32_t flags, uint32_t* const* out_ids, float* const* out_dists, uint32_t* const* out_counts,
-                    dade_gpu_stats* stats, const std::function<void(const float*, uint64_t*, uint32_t*)>& run) {
+                    dade_gpu_stats* stats, const std::function<void(const float*, uint64_t*, uint32_t*)>& run,
+                    uint64_t graph_tag = 0) {
     c->use_device();
     if (nb == 0 || nq == 0) return;
     cudaStream_t s = c->stream;
@@ -1713,7 +1843,7 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
         {
             FusedOutputs scope(c, c->res_ids[j].as<uint32_t>(), c->res_dists[j].as<float>(),
                                c->res_counts[j].as<uint32_t>());
-            run(d_q, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>());
+            search_graphed(c, graph_tag, d_q, nq, k, c->out_keys.as<uint64_t>(), c->out_count.as<uint32_t>(), run);
             fused = c->fo.done;
         }
         cap_used[b] = c->surv_cap_used;
@@ -1753,7 +1883,7 @@ void search_batches(dade_gpu_ctx* c, uint32_t nb, const float* const* queries, u
         if (surv_over || (coarse_used[b] && (uint32_t)h[1])) {
             // the single-search driver redoes it (larger worklist / all-exact coarse ranking)
             search_common(c, queries[b], nq, dim, k, flags, out_ids[b], out_dists[b],
-                          out_counts ? out_counts[b] : nullptr, stats, run);
+                          out_counts ? out_counts[b] : nullptr, stats, run, graph_tag);
             continue;
         }
         if (stats) {
@@ -1834,6 +1964,8 @@ int dade_gpu_destroy(dade_gpu_ctx* c) {
         cudaEventDestroy(c->e2);
         cudaEventDestroy(c->e3);
         for (auto& e : c->ef) cudaEventDestroy(e);
+        for (auto& e : c->graphs) cudaGraphExecDestroy(e.exec);
+        c->graphs.clear();
         cudaStreamDestroy(c->own_stream);
         delete c;
     });
@@ -1891,6 +2023,7 @@ int dade_gpu_set_transform(dade_gpu_ctx* c, uint32_t dim, const double* matrix, 
         cuda_check(cudaStreamSynchronize(c->stream), "transform upload");
         c->t_dim = dim;
         c->lambda_prefix = std::move(pre);
+        c->config_changed();
     });
 }
 
@@ -1940,6 +2073,8 @@ int dade_gpu_set_ivf(dade_gpu_ctx* c, uint32_t dim, uint32_t count, uint32_t n_c
         c->dev_offsets = c->h_offsets;
         c->has_ivf = true;
         c->sharded = false;
+        c->flat_parts = 0;
+        c->config_changed();
     });
 }
 
@@ -1987,6 +2122,8 @@ int dade_gpu_set_ivf_shard(dade_gpu_ctx* c, const uint8_t* mask) {
         c->count = (uint32_t)rows;
         c->norms_storage.rows = nullptr;
         c->aug_storage.rows = nullptr;
+        c->flat_parts = 0;
+        c->config_changed();
     });
 }
 
@@ -2002,6 +2139,8 @@ int dade_gpu_set_base(dade_gpu_ctx* c, uint32_t dim, uint32_t count, const float
         c->b_count = count;
         c->b_id_base = id_base;
         c->has_base = true;
+        c->flat_parts = 0;
+        c->config_changed();
     });
 }
 
@@ -2140,7 +2279,8 @@ int dade_gpu_ivf_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uint
                               out_dists + (size_t)q0 * k, out_counts ? out_counts + q0 : nullptr, stats,
                               [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
                                   ivf_search_device(c, d_q, m, k, n_probe, ok, oc);
-                              });
+                              },
+                              ((uint64_t)n_probe << 8) | 1u);
                 if (nq == 0) break;
             }
         } catch (...) {
@@ -2168,7 +2308,8 @@ int dade_gpu_ivf_search_batches(dade_gpu_ctx* c, uint32_t n_batches, const float
             search_batches(c, n_batches, queries, nq, c->dim, k, flags, out_ids, out_dists, out_counts, stats,
                            [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
                                ivf_search_device(c, d_q, nq, k, n_probe, ok, oc);
-                           });
+                           },
+                           ((uint64_t)n_probe << 8) | 1u);
         } catch (...) {
             c->stage_n_probe = 0;
             throw;
@@ -2185,15 +2326,31 @@ int dade_gpu_flat_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uin
         const bool measure = flags & DADE_GPU_MEASURE_FAILURES;
         MeasureScope ms(c, measure);
         const uint32_t chunk = measure ? measure_chunk(c->b_count, nq) : nq;
-        for (uint32_t q0 = 0; q0 < nq || q0 == 0; q0 += chunk) {
-            const uint32_t m = std::min(chunk, nq - q0);
-            search_common(c, queries + (size_t)q0 * c->b_dim, m, c->b_dim, k, flags, out_ids + (size_t)q0 * k,
-                          out_dists + (size_t)q0 * k, out_counts ? out_counts + q0 : nullptr, stats,
-                          [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
-                              flat_search_device(c, d_q, m, k, ok, oc);
-                          });
-            if (nq == 0) break;
+        const uint32_t parts = c->flat_parts && c->has_ivf && c->dim == c->b_dim ? c->flat_parts : 0u;
+        c->stage_n_probe = parts;  // data-ordered: the staging may coarse-rank query chunks
+        try {
+            for (uint32_t q0 = 0; q0 < nq || q0 == 0; q0 += chunk) {
+                const uint32_t m = std::min(chunk, nq - q0);
+                if (parts)  // every cell probed, nearest first: the IVF search over the partitioned base
+                    search_common(c, queries + (size_t)q0 * c->b_dim, m, c->b_dim, k, flags, out_ids + (size_t)q0 * k,
+                                  out_dists + (size_t)q0 * k, out_counts ? out_counts + q0 : nullptr, stats,
+                                  [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
+                                      ivf_search_device(c, d_q, m, k, parts, ok, oc);
+                                  },
+                                  ((uint64_t)parts << 8) | 2u);
+                else
+                    search_common(c, queries + (size_t)q0 * c->b_dim, m, c->b_dim, k, flags, out_ids + (size_t)q0 * k,
+                                  out_dists + (size_t)q0 * k, out_counts ? out_counts + q0 : nullptr, stats,
+                                  [&](const float* d_q, uint64_t* ok, uint32_t* oc) {
+                                      flat_search_device(c, d_q, m, k, ok, oc);
+                                  });
+                if (nq == 0) break;
+            }
+        } catch (...) {
+            c->stage_n_probe = 0;
+            throw;
         }
+        c->stage_n_probe = 0;
     });
 }
 
@@ -2623,6 +2780,14 @@ int dade_gpu_set_seed_rows(dade_gpu_ctx* c, uint32_t rows) {
     return guarded([&] {
         if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
         c->seed_rows_set = rows;
+        c->config_changed();
+    });
+}
+
+int dade_gpu_set_graphs(dade_gpu_ctx* c, int on) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        c->graphs_on = on != 0;
     });
 }
 
@@ -2749,6 +2914,8 @@ uint32_t kmeans_device(dade_gpu_ctx* c, const float* d_x, uint32_t n, uint32_t d
     cudaStream_t s = c->stream;
     c->has_ivf = false;
     c->sharded = false;
+    c->flat_parts = 0;
+    c->config_changed();
     c->dim = dim;
     c->n_clusters = n_clusters;
     c->centroids.ensure((size_t)n_clusters * dim * 4);
@@ -2931,6 +3098,7 @@ int dade_gpu_ivf_build(dade_gpu_ctx* c, const float* data, uint32_t n, uint32_t 
         c->norms_storage.rows = nullptr;
         c->aug_storage.rows = nullptr;
         c->has_ivf = true;
+        c->config_changed();
         const cudaMemcpyKind kind = cudaMemcpyDefault;  // outputs: host or device memory (unified addressing)
         if (centroids)
             cuda_check(cudaMemcpyAsync(centroids, c->centroids.p, (size_t)n_clusters * dim * 4, kind, s), "copy");
@@ -2938,6 +3106,29 @@ int dade_gpu_ivf_build(dade_gpu_ctx* c, const float* data, uint32_t n, uint32_t 
         if (ids) cuda_check(cudaMemcpyAsync(ids, c->ids.p, (size_t)n * 4, kind, s), "copy");
         if (storage) cuda_check(cudaMemcpyAsync(storage, c->storage.p, (size_t)n * dim * 4, kind, s), "copy");
         cuda_check(cudaStreamSynchronize(s), "ivf_build");
+    });
+}
+
+int dade_gpu_flat_partition(dade_gpu_ctx* c, uint32_t n_parts, uint32_t max_iters, uint64_t seed) {
+    return guarded([&] {
+        if (!c) fail(DADE_GPU_INVALID_INPUT, "null handle");
+        if (n_parts == 0) {
+            c->flat_parts = 0;
+            c->config_changed();
+            return;
+        }
+        if (!c->has_base) fail(DADE_GPU_CONFIG_ERROR, "flat_partition: no base vectors uploaded");
+        const int rc = dade_gpu_ivf_build(c, c->base.as<float>(), c->b_count, c->b_dim, n_parts, max_iters, seed,
+                                          DADE_GPU_DEVICE_PTRS, nullptr, nullptr, nullptr, nullptr);
+        if (rc != DADE_GPU_OK) fail(rc, g_last_error);
+        if (c->b_id_base) {  // the cells hold row indices; the flat scan reports id_base + row
+            std::vector<uint32_t> h(c->b_count);
+            cuda_check(cudaMemcpy(h.data(), c->ids.p, (size_t)c->b_count * 4, cudaMemcpyDeviceToHost), "D2H ids");
+            for (uint32_t& v : h) v += c->b_id_base;
+            cuda_check(cudaMemcpy(c->ids.p, h.data(), (size_t)c->b_count * 4, cudaMemcpyHostToDevice), "H2D ids");
+        }
+        c->flat_parts = n_parts;
+        c->config_changed();
     });
 }
 
