@@ -403,6 +403,7 @@ struct dade_gpu_ctx {
     DevBuf cnorm, qnorm, coarse_lo, coarse_overflow, q_norms, coarse_gmin;  // coarse_lo: p~ per (query, centroid)
     DevBuf coarse_cand, coarse_cnt, coarse_t0;  // fused large-nlist selection
     bool coarse_force_exact = false, coarse_tc_used = false;
+    bool coarse_all = false;  // every centroid probed, no exact ranking (the data-ordered flat scan)
     int n_sms = 148;
     uint32_t surv_cap_hint = 0;
     uint32_t surv_cap_used = 0;     // worklist capacity of the last streaming search (0: none)
@@ -633,6 +634,13 @@ void coarse_tc_range(dade_gpu_ctx* c, const float* d_q, uint32_t q0, uint32_t m,
         cuda_check(launch_coarse_umma(*tmc, *tmq, q0, c->n_clusters, m, c->dim, c->cnorm.as<float>(),
                                       c->qnorm.as<float>(), c->coarse_lo.as<float>(), s, gmin),
                    "coarse gemm (tcgen05)");
+        if (c->coarse_all && n_probe == c->n_clusters) {  // data-ordered flat scan: order only
+            cuda_check(launch_coarse_all(c->coarse_lo.as<float>(), c->n_clusters, m,
+                                         c->probes.as<uint64_t>() + (size_t)q0 * n_probe, s),
+                       "coarse order");
+            c->launches += 3;
+            return;
+        }
         cuda_check(launch_coarse_select(c->centroids.as<float>(), c->n_clusters, qc, m, c->dim, n_probe,
                                         c->cnorm.as<float>(), c->qnorm.as<float>(), c->coarse_lo.as<float>(),
                                         c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
@@ -1637,7 +1645,8 @@ void search_graphed(dade_gpu_ctx* c, uint64_t tag, const float* d_q, uint32_t nq
         g_alloc_epoch,
         c->cfg_epoch,
         c->surv_cap_hint,
-        (uint64_t)c->probes_ready | ((uint64_t)c->coarse_force_exact << 1) | ((uint64_t)c->sharded << 2),
+        (uint64_t)c->probes_ready | ((uint64_t)c->coarse_force_exact << 1) | ((uint64_t)c->sharded << 2) |
+            ((uint64_t)c->coarse_all << 3),
         (uint64_t)c->seed_rows_set};
     for (auto& e : c->graphs)
         if (e.key == key) {
@@ -2328,6 +2337,7 @@ int dade_gpu_flat_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uin
         const uint32_t chunk = measure ? measure_chunk(c->b_count, nq) : nq;
         const uint32_t parts = c->flat_parts && c->has_ivf && c->dim == c->b_dim ? c->flat_parts : 0u;
         c->stage_n_probe = parts;  // data-ordered: the staging may coarse-rank query chunks
+        c->coarse_all = parts != 0;
         try {
             for (uint32_t q0 = 0; q0 < nq || q0 == 0; q0 += chunk) {
                 const uint32_t m = std::min(chunk, nq - q0);
@@ -2348,9 +2358,11 @@ int dade_gpu_flat_search(dade_gpu_ctx* c, const float* queries, uint32_t nq, uin
             }
         } catch (...) {
             c->stage_n_probe = 0;
+            c->coarse_all = false;
             throw;
         }
         c->stage_n_probe = 0;
+        c->coarse_all = false;
     });
 }
 

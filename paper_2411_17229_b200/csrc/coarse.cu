@@ -771,6 +771,48 @@ cudaError_t launch_coarse_norms(const float* centroids, uint32_t n_cen, const fl
     return cudaGetLastError();
 }
 
+namespace {
+// Every centroid probed (the data-ordered flat scan, dade_gpu_flat_partition):
+// the nearest by p~ first, the others in id order. No exact ranking: any order
+// visits the same candidates; the first cell only seeds the radius. Warp per query.
+__global__ void __launch_bounds__(128) coarse_all_kernel(const float* __restrict__ pt, uint32_t n_cen, uint32_t nq,
+                                                         uint64_t* __restrict__ probes) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t qi = blockIdx.x * 4 + warp;
+    if (qi >= nq) return;
+    const float* prow = pt + (size_t)qi * n_cen;
+    float best = __int_as_float(0x7f800000);
+    uint32_t bi = 0xffffffffu;
+    for (uint32_t c = lane; c < n_cen; c += 32) {
+        const float v = prow[c];
+        if (v < best || bi == 0xffffffffu) {
+            best = v;
+            bi = c;
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (oi != 0xffffffffu && (bi == 0xffffffffu || ov < best || (ov == best && oi < bi))) {
+            best = ov;
+            bi = oi;
+        }
+    }
+    if (bi == 0xffffffffu) bi = 0;  // (all NaN)
+    uint64_t* out = probes + (size_t)qi * n_cen;
+    for (uint32_t i = lane; i < n_cen; i += 32) {
+        const uint32_t j = i == 0 ? bi : (i - 1 < bi ? i - 1 : i);
+        out[i] = make_key(fmaxf(prow[j], 0.f), j);
+    }
+}
+}  // namespace
+
+cudaError_t launch_coarse_all(const float* pt, uint32_t n_cen, uint32_t nq, uint64_t* probes, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    coarse_all_kernel<<<(nq + 3) / 4, 128, 0, s>>>(pt, n_cen, nq, probes);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq,
                                  uint32_t dim, uint32_t n_probe, const float* cnorm, const float* qnorm,
                                  const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s,

@@ -124,6 +124,8 @@ constexpr uint32_t kCoarseSelParts = 4;  // list slices per query of the query-m
 // coarse.cu pieces around it
 cudaError_t launch_coarse_norms(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq, uint32_t dim,
                                 float* cnorm, float* qnorm, cudaStream_t s);
+// Every centroid probed: p~-nearest first, the rest in id order (data-ordered flat scan).
+cudaError_t launch_coarse_all(const float* pt, uint32_t n_cen, uint32_t nq, uint64_t* probes, cudaStream_t s);
 cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq,
                                  uint32_t dim, uint32_t n_probe, const float* cnorm, const float* qnorm,
                                  const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s,
