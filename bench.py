@@ -531,7 +531,7 @@ def single_gpu_workload(args, cfg, dev, device, stream, flush, with_e2e=True, wi
     return out
 
 
-FLAT_PARTS, FLAT_PART_ITERS = 256, 10
+FLAT_PARTS, FLAT_PART_ITERS = 512, 10
 
 
 def flat_workload(args, cfg, dev, device, stream, flush):

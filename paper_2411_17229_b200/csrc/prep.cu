@@ -26,20 +26,30 @@ namespace {
 // CTA's main loop, so every output is bit-identical to transform_vector.
 //
 // 64 rows x 64 output columns per CTA of 4 warps, 32 x 32 per warp (4 x 4
-// m8n8 tiles); x and W chunks of 16 r staged as fp64 ([row][r], [col][r],
-// stride 20 doubles: conflict-free fragment loads), prefetched one chunk ahead
-// in registers; the row / column norms are accumulated from the staged values.
+// m8n8 tiles). Chunks of 16 r are staged by cp.async into double buffers (x as
+// fp32 [row][r], stride 20 floats; W as fp64 [col][r], stride 20 doubles:
+// conflict-free fragment loads), the next chunk in flight while the current one
+// is multiplied; x is widened to fp64 at the fragment load. With no register
+// staging the kernel fits 5 CTAs per SM, so 148 x 5 tiles run in one wave
+// (config 1's 628 tiles took two waves at 4 per SM). The row / column norms are
+// accumulated from the staged values.
 // (A 32 x 32 tile with the K range split over the warps measured 1.5x slower:
 // four times the staging per multiply-add.)
 constexpr int kRotT = 64;    // rows and columns per CTA
 constexpr int kRotK = 16;    // r chunk
-constexpr int kRotS = 20;    // staged row stride (doubles)
+constexpr int kRotS = 20;    // staged row stride (doubles / floats)
 constexpr int kRotFix = 512; // per-CTA list of elements to recompute exactly
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                  : "+d"(c[0]), "+d"(c[1])
                  : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void rot_cp16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
 }
 
 __device__ __noinline__ float rotate_exact(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in,
@@ -51,11 +61,11 @@ __device__ __noinline__ float rotate_exact(const double* __restrict__ W, uint32_
     return __double2float_rn(acc);
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 5)
 rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in, uint32_t n,
               float* __restrict__ out) {
-    __shared__ __align__(16) double xs[kRotT * kRotS];
-    __shared__ __align__(16) double ws[kRotT * kRotS];
+    __shared__ __align__(16) float xs[2][kRotT * kRotS];
+    __shared__ __align__(16) double ws[2][kRotT * kRotS];
     __shared__ double wn[kRotT], xn[kRotT];
     __shared__ uint32_t fix[kRotFix];
     __shared__ uint32_t n_fix;
@@ -69,69 +79,74 @@ rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restric
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = 0.0;
-    // staging: thread tid holds row / column tid >> 1, r = r0 + 8 (tid & 1) .. + 7
+    // staging: thread tid owns row / column tid >> 1, r = r0 + 8 (tid & 1) .. + 7
     const uint32_t sr = tid >> 1, so = 8 * (tid & 1);
     const uint32_t xrow = row0 + sr, wcol = col0 + sr;
     const bool vec = dim % 4 == 0;
-    float xv[8];
-    double wv[8];
     double xsq = 0.0, wsq = 0.0;
-    auto load_chunk = [&](uint32_t r0) {
+    auto stage = [&](uint32_t r0, int b) {
         const uint32_t r = r0 + so;
+        float* xd = &xs[b][sr * kRotS + so];
+        double* wd = &ws[b][sr * kRotS + so];
         if (vec && r + 8 <= dim) {
             if (xrow < n) {
-                const float4 a = __ldg(reinterpret_cast<const float4*>(in + (size_t)xrow * dim + r));
-                const float4 b = __ldg(reinterpret_cast<const float4*>(in + (size_t)xrow * dim + r + 4));
-                xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
-                xv[4] = b.x; xv[5] = b.y; xv[6] = b.z; xv[7] = b.w;
+                rot_cp16(xd, in + (size_t)xrow * dim + r);
+                rot_cp16(xd + 4, in + (size_t)xrow * dim + r + 4);
             } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) xv[e] = 0.f;
+                *reinterpret_cast<float4*>(xd) = make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(xd + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             if (wcol < dim) {
 #pragma unroll
-                for (int e = 0; e < 8; e += 2) {
-                    const double2 v = __ldg(reinterpret_cast<const double2*>(W + (size_t)wcol * dim + r + e));
-                    wv[e] = v.x;
-                    wv[e + 1] = v.y;
-                }
+                for (int e = 0; e < 8; e += 2) rot_cp16(wd + e, W + (size_t)wcol * dim + r + e);
             } else {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) wv[e] = 0.0;
+                for (int e = 0; e < 8; e += 2) *reinterpret_cast<double2*>(wd + e) = make_double2(0.0, 0.0);
             }
         } else {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                xv[e] = (xrow < n && r + e < dim) ? __ldg(in + (size_t)xrow * dim + r + e) : 0.f;
-                wv[e] = (wcol < dim && r + e < dim) ? __ldg(W + (size_t)wcol * dim + r + e) : 0.0;
+                xd[e] = (xrow < n && r + e < dim) ? __ldg(in + (size_t)xrow * dim + r + e) : 0.f;
+                wd[e] = (wcol < dim && r + e < dim) ? __ldg(W + (size_t)wcol * dim + r + e) : 0.0;
             }
         }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    load_chunk(0);
-    for (uint32_t r0 = 0; r0 < dim; r0 += kRotK) {
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-            const double x0 = (double)xv[e], x1 = (double)xv[e + 1];
-            *reinterpret_cast<double2*>(&xs[sr * kRotS + so + e]) = make_double2(x0, x1);
-            *reinterpret_cast<double2*>(&ws[sr * kRotS + so + e]) = make_double2(wv[e], wv[e + 1]);
-            xsq = fma(x0, x0, fma(x1, x1, xsq));
-            wsq = fma(wv[e], wv[e], fma(wv[e + 1], wv[e + 1], wsq));
+    stage(0, 0);
+    int b = 0;
+    for (uint32_t r0 = 0; r0 < dim; r0 += kRotK, b ^= 1) {
+        if (r0 + kRotK < dim) {
+            stage(r0 + kRotK, b ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         __syncthreads();
-        if (r0 + kRotK < dim) load_chunk(r0 + kRotK);
+        {  // this thread's row / column share of the norms
+            const float* xv = &xs[b][sr * kRotS + so];
+            const double* wv = &ws[b][sr * kRotS + so];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const double x = (double)xv[e];
+                xsq = fma(x, x, xsq);
+                wsq = fma(wv[e], wv[e], wsq);
+            }
+        }
+        const float* xb = xs[b];
+        const double* wb = ws[b];
 #pragma unroll
         for (int k0 = 0; k0 < kRotK; k0 += 4) {
-            double a[4], b[4];
+            double a[4], bb[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = xs[(32 * wm + 8 * i + g) * kRotS + k0 + t];
+            for (int i = 0; i < 4; ++i) a[i] = (double)xb[(32 * wm + 8 * i + g) * kRotS + k0 + t];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = ws[(32 * wc + 8 * j + g) * kRotS + k0 + t];
+            for (int j = 0; j < 4; ++j) bb[j] = wb[(32 * wc + 8 * j + g) * kRotS + k0 + t];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(c[i][j], a[i], b[j]);
+                for (int j = 0; j < 4; ++j) dmma(c[i][j], a[i], bb[j]);
         }
+        __syncthreads();  // buffer b is restaged two chunks on
     }
     // norms (upper bounds after the 1.0001 margin below); lanes 2m, 2m + 1 share a row
     xsq += __shfl_xor_sync(0xffffffffu, xsq, 1);
