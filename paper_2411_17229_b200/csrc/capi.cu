@@ -404,6 +404,7 @@ struct dade_gpu_ctx {
     DevBuf coarse_cand, coarse_cnt, coarse_t0;  // fused large-nlist selection
     bool coarse_force_exact = false, coarse_tc_used = false;
     bool coarse_all = false;  // every centroid probed, no exact ranking (the data-ordered flat scan)
+    bool coarse_exact_keys = false;  // probe keys exact and ascending (dade_gpu_coarse_probes), not only the set
     int n_sms = 148;
     uint32_t surv_cap_hint = 0;
     uint32_t surv_cap_used = 0;     // worklist capacity of the last streaming search (0: none)
@@ -646,7 +647,7 @@ void coarse_tc_range(dade_gpu_ctx* c, const float* d_q, uint32_t q0, uint32_t m,
         cuda_check(launch_coarse_select(c->centroids.as<float>(), c->n_clusters, qc, m, c->dim, n_probe,
                                         c->cnorm.as<float>(), c->qnorm.as<float>(), c->coarse_lo.as<float>(),
                                         c->probes.as<uint64_t>() + (size_t)q0 * n_probe,
-                                        c->coarse_overflow.as<uint32_t>(), s, gmin),
+                                        c->coarse_overflow.as<uint32_t>(), s, gmin, c->coarse_exact_keys),
                    "coarse select");
         c->launches += 3;
         return;
@@ -1648,7 +1649,7 @@ void search_graphed(dade_gpu_ctx* c, uint64_t tag, const float* d_q, uint32_t nq
         c->cfg_epoch,
         c->surv_cap_hint,
         (uint64_t)c->probes_ready | ((uint64_t)c->coarse_force_exact << 1) | ((uint64_t)c->sharded << 2) |
-            ((uint64_t)c->coarse_all << 3),
+            ((uint64_t)c->coarse_all << 3) | ((uint64_t)c->coarse_exact_keys << 4),
         (uint64_t)c->seed_rows_set};
     for (auto& e : c->graphs)
         if (e.key == key) {
@@ -2409,6 +2410,11 @@ int dade_gpu_coarse_probes(dade_gpu_ctx* c, const float* d_queries, uint32_t nq,
         if (nq && (!d_queries || !d_probes)) fail(DADE_GPU_INVALID_INPUT, "coarse_probes: null argument");
         c->use_device();
         if (nq == 0) return;
+        struct ExactKeys {  // this entry point's keys are exact l2_sq, ascending (dade_gpu.h)
+            dade_gpu_ctx* c;
+            ~ExactKeys() { c->coarse_exact_keys = false; }
+        } exact_keys{c};
+        c->coarse_exact_keys = true;
         const float* d_q = stage_queries(c, d_queries, nq, c->dim, flags);
         coarse_rank(c, d_q, nq, n_probe);
         if (c->coarse_tc_used) {  // boundary-candidate overflow (pathological ties): all-exact ranking

@@ -339,7 +339,8 @@ template <int WPQ>
 __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
     const float* __restrict__ pt, const float* __restrict__ cnorm, const float* __restrict__ qnorm,
     const float* __restrict__ cen, uint32_t n_cen, const float* __restrict__ q, uint32_t nq, uint32_t dim,
-    uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow, uint32_t* census = nullptr) {
+    uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow, uint32_t* census = nullptr,
+    bool exact_all = true) {
     __shared__ uint64_t cand[kFsWarps][kSelCap];
     __shared__ __align__(16) float rows[kFsWarps][32 * kFsRS];
     __shared__ __align__(16) float qch[kFsWarps][32];
@@ -409,18 +410,75 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
         n = kSelCap;
     }
     __syncwarp();
+    // Sure members: a candidate c with hi_c <= B that fewer than n_probe other
+    // candidates can beat (lo_c' <= hi_c: every centroid with a smaller exact
+    // (l2_sq, id) key is such a candidate) is in the probe set whatever the exact
+    // values are; only the rest (U) get the exact l2_sq, and their (l2_sq, id)
+    // order fills the slots the sure members leave. Sure keys carry p~ (the probe
+    // order after the nearest matters to no consumer); U keys are flagged with
+    // the top bit so the sort puts the sure members first. exact_all (the
+    // coarse_probes entry point, whose keys are documented exact): every
+    // candidate is in U, i.e. the previous all-exact selection.
+    uint32_t nS = 0;
+    if (!exact_all) {
+        uint32_t* klo = reinterpret_cast<uint32_t*>(rows[warp]);  // free until the exact rounds
+        uint32_t* khi = klo + kSelCap;                             // (2 x 512 <= 32 x 36 words)
+        for (uint32_t e = lane; e < n; e += 32) {
+            const uint32_t c = (uint32_t)cand[warp][e];
+            const float p = prow[c], d = coarse_delta(cnorm[c], qn);
+            klo[e] = fkey(__fsub_rn(p, d));
+            khi[e] = fkey(__fadd_rn(p, d));
+        }
+        __syncwarp();
+        constexpr int kG = kSelCap / 32;
+        uint32_t ids[kG];
+        uint32_t smask = 0;
+        const uint32_t ng = (n + 31) / 32;
+#pragma unroll
+        for (int i = 0; i < kG; ++i) {
+            if ((uint32_t)i >= ng) break;
+            const uint32_t e = lane + 32u * i;
+            ids[i] = e < n ? (uint32_t)cand[warp][e] : 0u;
+            if (e < n) {
+                const uint32_t h = khi[e];
+                if (h <= B) {
+                    uint32_t cnt = 0;
+                    for (uint32_t e2 = 0; e2 < n && cnt < n_probe; ++e2) cnt += (e2 != e && klo[e2] <= h) ? 1u : 0u;
+                    if (cnt < n_probe) smask |= 1u << i;
+                }
+            }
+        }
+        __syncwarp();
+        uint32_t nU = 0;
+#pragma unroll
+        for (int i = 0; i < kG; ++i) {
+            if ((uint32_t)i >= ng) break;
+            const uint32_t e = lane + 32u * i;
+            const bool sure = (smask >> i) & 1u, unsure = e < n && !sure;
+            const uint32_t bs = __ballot_sync(0xffffffffu, sure), bu = __ballot_sync(0xffffffffu, unsure);
+            const uint32_t lt = (1u << lane) - 1u;
+            // sure keys from the front, U ids after them (positions settled below)
+            if (sure) cand[warp][nS + __popc(bs & lt)] = make_key(fmaxf(prow[ids[i]], 0.f), ids[i]);
+            if (unsure) reinterpret_cast<uint32_t*>(rows[warp])[nU + __popc(bu & lt)] = ids[i];
+            nS += __popc(bs);
+            nU += __popc(bu);
+        }
+        __syncwarp();
+        for (uint32_t e = lane; e < nU; e += 32) cand[warp][nS + e] = reinterpret_cast<uint32_t*>(rows[warp])[e];
+    }
+    __syncwarp();
     if (WPQ > 1) __syncthreads();  // every warp's id list is written before keys land in warp 0's
-    // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43) of the candidates
+    // exact sequential l2_sq (proj/include/dade/distance.hpp:36-43) of the U candidates
     const float* qr = q + (size_t)qi * dim;
     float* rs = rows[warp];
     float* qs = qch[warp];
-    for (uint32_t e0 = 32 * (warp % WPQ); e0 < n; e0 += 32 * WPQ) {
+    for (uint32_t e0 = nS + 32 * (warp % WPQ); e0 < n; e0 += 32 * WPQ) {
         const uint32_t e = e0 + lane;
         const uint32_t my_c = e < n ? (uint32_t)cand[warp][e] : 0u;
         const uint32_t nv = min(32u, n - e0);
         const float acc = exact_l2_round(cen, qr, dim, my_c, nv, e < n, rs, qs, lane);
         __syncwarp();
-        if (e < n) cand[WPQ == 1 ? warp : 0][e] = make_key(acc, my_c);
+        if (e < n) cand[WPQ == 1 ? warp : 0][e] = make_key(acc, my_c) | 0x8000000000000000ull;
     }
     if (WPQ == 1) {
         __syncwarp();
@@ -428,7 +486,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
         __syncthreads();
         if (warp != 0) return;
     }
-    // pad and bitonic-sort the candidate keys
+    // pad and bitonic-sort the candidate keys (sure members first)
     uint32_t m = 1;
     while (m < n) m <<= 1;
     for (uint32_t e = n + lane; e < m; e += 32) cand[warp][e] = ~0ull;
@@ -444,7 +502,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
             }
             __syncwarp();
         }
-    for (uint32_t i = lane; i < n_probe; i += 32) probes[(size_t)qi * n_probe + i] = kk[i];
+    for (uint32_t i = lane; i < n_probe; i += 32) probes[(size_t)qi * n_probe + i] = kk[i] & 0x7fffffffffffffffull;
 }
 
 // Large-nlist path (1024 < n_cen <= 16384, dim % 4 == 0), warp per query:
@@ -729,15 +787,16 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_finish_kernel(
 // the select kernel for n_cen centroids
 void launch_select_any(const float* pt, const float* cnorm, const float* qnorm, const float* centroids, uint32_t n_cen,
                        const float* queries, uint32_t nq, uint32_t dim, uint32_t n_probe, uint64_t* probes,
-                       uint32_t* overflow, cudaStream_t s, const uint32_t* gmin = nullptr) {
+                       uint32_t* overflow, cudaStream_t s, const uint32_t* gmin = nullptr, bool exact_all = true) {
     if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap) {
         uint32_t* census = nullptr;
         if (nq <= 4096 && n_probe > 32)  // > 1 exact round
+            // (warps split the exact rounds: skipping the sure members saves no latency here)
             coarse_select_fast_kernel<kFsWarps><<<nq, kFsWarps * 32, 0, s>>>(
-                pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, census);
+                pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, census, true);
         else
             coarse_select_fast_kernel<1><<<(nq + kFsWarps - 1) / kFsWarps, kFsWarps * 32, 0, s>>>(
-                pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, census);
+                pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, census, exact_all);
         return;
     }
     if (n_cen <= 32u * kWdChunk && dim % 4 == 0 && n_probe <= kSelCap && !std::getenv("DADE_GPU_SELECT_WARP")) {
@@ -816,9 +875,10 @@ cudaError_t launch_coarse_all(const float* pt, uint32_t n_cen, uint32_t nq, uint
 cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq,
                                  uint32_t dim, uint32_t n_probe, const float* cnorm, const float* qnorm,
                                  const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s,
-                                 const uint32_t* gmin) {
+                                 const uint32_t* gmin, bool exact_keys) {
     if (nq == 0) return cudaSuccess;
-    launch_select_any(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, s, gmin);
+    launch_select_any(pt, cnorm, qnorm, centroids, n_cen, queries, nq, dim, n_probe, probes, overflow, s, gmin,
+                      exact_keys);
     return cudaGetLastError();
 }
 

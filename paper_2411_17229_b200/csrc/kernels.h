@@ -126,10 +126,12 @@ cudaError_t launch_coarse_norms(const float* centroids, uint32_t n_cen, const fl
                                 float* cnorm, float* qnorm, cudaStream_t s);
 // Every centroid probed: p~-nearest first, the rest in id order (data-ordered flat scan).
 cudaError_t launch_coarse_all(const float* pt, uint32_t n_cen, uint32_t nq, uint64_t* probes, cudaStream_t s);
+// exact_keys: every probe key carries the exact l2_sq (else only the probe set is exact,
+// the order after the nearest approximate)
 cudaError_t launch_coarse_select(const float* centroids, uint32_t n_cen, const float* queries, uint32_t nq,
                                  uint32_t dim, uint32_t n_probe, const float* cnorm, const float* qnorm,
                                  const float* pt, uint64_t* probes, uint32_t* overflow, cudaStream_t s,
-                                 const uint32_t* gmin = nullptr);
+                                 const uint32_t* gmin = nullptr, bool exact_keys = true);
 // per-row extra operand [n][8] = (-h hi, -h lo, 1, 1, 0, 0, 0, 0) from first-slice norms
 cudaError_t launch_row_aug(const float* norms, uint32_t n, float* out, cudaStream_t s);
 

@@ -189,6 +189,156 @@ rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restric
     }
 }
 
+// Small batches (fewer 64 x 64 tiles than two per SM: configs 0 and 2, 1000
+// queries) leave most SMs idle, so their rotation runs 32 x 32 output tiles with
+// the r range split over the CTA's four warps: each warp stages its own r chunks
+// (cp.async, warp-private double buffers) into its own 32 x 32 accumulator; the
+// partial sums and partial norms are added in warp order (deterministic) and the
+// same rounding proof applies (any summation order stays within gamma_{D+2}).
+constexpr int kRkT = 32;                       // rows and columns per CTA
+constexpr int kRkWarp = 2 * kRkT * kRotS * 12; // bytes per warp: x [2][32][20] f32 + W [2][32][20] f64
+
+__global__ void __launch_bounds__(128, 4)
+rotate_ksplit_kernel(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in, uint32_t n,
+                     float* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char rk_smem[];
+    __shared__ double wn[kRkT], xn[kRkT];
+    __shared__ uint32_t fix[kRotFix];
+    __shared__ uint32_t n_fix;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t col0 = blockIdx.x * kRkT, row0 = blockIdx.y * kRkT;
+    float* xs = reinterpret_cast<float*>(rk_smem + (size_t)warp * kRkWarp);            // [2][32][20]
+    double* ws = reinterpret_cast<double*>(rk_smem + (size_t)warp * kRkWarp + 2 * kRkT * kRotS * 4);  // [2][32][20]
+    if (tid == 0) n_fix = 0;
+    double c[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+    const uint32_t nch = (dim + kRotK - 1) / kRotK;
+    const uint32_t ch0 = warp * nch / 4, ch1 = (warp + 1) * nch / 4;
+    const uint32_t xrow = row0 + lane, wcol = col0 + lane;
+    const bool vec = dim % 4 == 0;
+    double xsq = 0.0, wsq = 0.0;
+    auto stage = [&](uint32_t ch, int b) {  // lane: row / column lane, r = 16 ch .. + 15
+        const uint32_t r = ch * kRotK;
+        float* xd = xs + b * kRkT * kRotS + lane * kRotS;
+        double* wd = ws + b * kRkT * kRotS + lane * kRotS;
+        if (vec && r + kRotK <= dim) {
+#pragma unroll
+            for (int e = 0; e < kRotK; e += 4) {
+                if (xrow < n) rot_cp16(xd + e, in + (size_t)xrow * dim + r + e);
+                else *reinterpret_cast<float4*>(xd + e) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int e = 0; e < kRotK; e += 2) {
+                if (wcol < dim) rot_cp16(wd + e, W + (size_t)wcol * dim + r + e);
+                else *reinterpret_cast<double2*>(wd + e) = make_double2(0.0, 0.0);
+            }
+        } else {
+            for (int e = 0; e < kRotK; ++e) {
+                xd[e] = (xrow < n && r + e < dim) ? __ldg(in + (size_t)xrow * dim + r + e) : 0.f;
+                wd[e] = (wcol < dim && r + e < dim) ? __ldg(W + (size_t)wcol * dim + r + e) : 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    if (ch0 < ch1) stage(ch0, 0);
+    int b = 0;
+    for (uint32_t ch = ch0; ch < ch1; ++ch, b ^= 1) {
+        if (ch + 1 < ch1) {
+            stage(ch + 1, b ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncwarp();
+        const float* xb = xs + b * kRkT * kRotS;
+        const double* wb = ws + b * kRkT * kRotS;
+#pragma unroll
+        for (int e = 0; e < kRotK; ++e) {
+            const double x = (double)xb[lane * kRotS + e];
+            xsq = fma(x, x, xsq);
+            wsq = fma(wb[lane * kRotS + e], wb[lane * kRotS + e], wsq);
+        }
+#pragma unroll
+        for (int k0 = 0; k0 < kRotK; k0 += 4) {
+            double a[4], bb[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = (double)xb[(8 * i + g) * kRotS + k0 + t];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bb[j] = wb[(8 * j + g) * kRotS + k0 + t];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(c[i][j], a[i], bb[j]);
+        }
+        __syncwarp();  // buffer b is restaged two chunks on
+    }
+    __syncthreads();  // every warp done with its staging: reuse it for the partials
+    double* part = reinterpret_cast<double*>(rk_smem);  // [3][32 x 32] of warps 1-3, then norms [3][2][32]
+    double* pnorm = part + 3 * kRkT * kRkT;
+    if (warp > 0) {
+        double* pw = part + (warp - 1) * kRkT * kRkT;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) pw[(8 * i + g) * kRkT + 8 * j + 2 * t + h] = c[i][j][h];
+        pnorm[(warp - 1) * 2 * kRkT + lane] = xsq;
+        pnorm[(warp - 1) * 2 * kRkT + kRkT + lane] = wsq;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (int w = 0; w < 3; ++w) {
+            const double* pw = part + w * kRkT * kRkT;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) c[i][j][h] += pw[(8 * i + g) * kRkT + 8 * j + 2 * t + h];
+            xsq += pnorm[w * 2 * kRkT + lane];
+            wsq += pnorm[w * 2 * kRkT + kRkT + lane];
+        }
+        xn[lane] = sqrt(xsq);
+        wn[lane] = sqrt(wsq);
+        __syncwarp();
+        const double gam = (double)(dim + 2) * 0x1p-52 * 1.0001;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t rl = 8 * i + g, row = row0 + rl;
+            if (row >= n) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t cl = 8 * j + 2 * t + h, col = col0 + cl;
+                    if (col >= dim) continue;
+                    const double acc = c[i][j][h];
+                    const double e = gam * wn[cl] * xn[rl];
+                    const float lo = __double2float_rn(__dsub_rd(acc, e));
+                    const float hi = __double2float_rn(__dadd_ru(acc, e));
+                    if (__float_as_uint(lo) == __float_as_uint(hi) && !isnan(lo)) {
+                        out[(size_t)row * dim + col] = lo;
+                    } else {
+                        const uint32_t slot = atomicAdd(&n_fix, 1u);
+                        if (slot < (uint32_t)kRotFix) fix[slot] = (rl << 8) | cl;
+                        else out[(size_t)row * dim + col] = rotate_exact(W, dim, in, row, col);
+                    }
+                }
+        }
+    }
+    __syncthreads();
+    const uint32_t nf = min(n_fix, (uint32_t)kRotFix);
+    for (uint32_t e = tid; e < nf; e += blockDim.x) {
+        const uint32_t row = row0 + (fix[e] >> 8), col = col0 + (fix[e] & 0xffu);
+        out[(size_t)row * dim + col] = rotate_exact(W, dim, in, row, col);
+    }
+}
+
 // ---- K3: grouping ------------------------------------------------------------
 __device__ __forceinline__ uint32_t rank_bucket(const GroupArgs& g, uint32_t p) {
     uint32_t b = 0;
@@ -882,6 +1032,20 @@ cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s) {
 cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
                           cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            n_sm = 148;
+    }
+    const uint64_t tiles64 = (uint64_t)((dim + kRotT - 1) / kRotT) * ((n + kRotT - 1) / kRotT);
+    if (tiles64 < 2ull * n_sm && dim >= 4 * kRotK) {  // small batch: 32 x 32 tiles, r split over the warps
+        const size_t smem = 4 * (size_t)kRkWarp;
+        DADE_CUDA_TRY(cudaFuncSetAttribute(rotate_ksplit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid((dim + kRkT - 1) / kRkT, (n + kRkT - 1) / kRkT);
+        rotate_ksplit_kernel<<<grid, 128, smem, s>>>(W, dim, in, n, out);
+        return cudaGetLastError();
+    }
     dim3 grid((dim + kRotT - 1) / kRotT, (n + kRotT - 1) / kRotT);
     rotate_kernel<<<grid, 128, 0, s>>>(W, dim, in, n, out);
     return cudaGetLastError();
