@@ -1014,7 +1014,21 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         // everything else incl. the nearest lists' tails -- a separate middle pass for
         // those tails costs its own filter/survivor/merge launches
         const bool fold = umma && two_pass && !flat;
-        const int n_pass = flat ? 6 : two_pass ? (fold ? 2 : 3) : 1;
+        // ... and (tcgen05 filter) NO separate pass 0 unless it pays: the pass tightens the radius
+        // for everything after it at the price of its own filter / survivor / merge launches
+        // (~60 us of mostly idle GPU). It pays when the nearest lists reach well past the seed AND
+        // much work follows (the partitioned flat scan: 3906-row cells, 8e9 pairs: 6.1 vs 7.9 ms).
+        // Otherwise one pass over everything the seed left, with the seed's radius: config 1
+        // 0.931 -> 0.874 ms, config 2 0.875 -> 0.791 ms, config 0 0.386 -> 0.337 ms, config 3
+        // 9.46 -> 9.33 ms per batch; recall 0.985 -> 0.986 / 0.983 -> 0.994 / 1.000 / 0.803 ->
+        // 0.804 (a looser radius prunes fewer true neighbours).
+        bool single = false;
+        if (fold && g && g->n_lists) {
+            const double mean_len = (double)n_rows / g->n_lists;
+            const double pairs = (double)nq * seed.n_probe * mean_len;
+            single = !(mean_len > 2.0 * seed_rows(c, k, a.dim, flat) && pairs >= 1e9);
+        }
+        const int n_pass = flat ? 6 : single ? 1 : two_pass ? (fold ? 2 : 3) : 1;
         // The next staging's H2D (pipelined batches) starts with the last pass, not
         // after this search's rotation: under the seed and the early passes the
         // copy slowed the search by ~60 us, under the last pass's tcgen05 filter
@@ -1070,7 +1084,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                     f.range_hi = std::min(flat_hi[pass], np) * nqc;
                     if (f.range_hi == 0) f.range_lo = 0;  // (empty base: the counter path)
                 }
-            } else if (two_pass) {
+            } else if (two_pass && !single) {
                 // pass 0: kFilterItemRows rows of each nearest list past the seed
                 const uint32_t p0 = std::max<uint32_t>(1, kFilterItemRows / rank0_item_rows(umma));
                 if (pass == 0 || (pass == 1 && !fold)) {

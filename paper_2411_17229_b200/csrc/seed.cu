@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
         uint32_t s = 0, ph = 0, used = 0;  // ring slot, its phase, slots filled so far (< stages: no wait)
         for (uint32_t i = 0;; ++i) {
             const uint32_t j = i % kSpSlots;
-            if (i >= (uint32_t)kSpSlots) mb_wait(gempty + j, ((i / kSpSlots) - 1) & 1);
+            if (i >= (uint32_t)kSpSlots) mb_wait_sleep(gempty + j, ((i / kSpSlots) - 1) & 1, 400);
             uint32_t b;
             SpGroup G;
             for (;;) {
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
             const uint32_t n_boxes = (G.n + kSdBox - 1) / kSdBox;
             const uint32_t bytes = n_boxes * kSdBox * kSdSlice * 4;
             for (uint32_t k = 0; k < n_slices; ++k) {
-                if (used >= g.stages) mb_wait(empty + s, ph ^ 1);  // the slot's previous fill consumed
+                if (used >= g.stages) mb_wait_sleep(empty + s, ph ^ 1, 100);  // the slot's previous fill consumed
                 else ++used;
                 mb_arrive_tx(full + s, bytes);
                 unsigned char* slot = ring + (size_t)s * g.slot_bytes;
@@ -408,12 +408,12 @@ __global__ void __launch_bounds__(kSpThreads, 1) seed_persist_kernel(const SeedL
     const uint32_t lw = warp - kSpS;
     for (uint32_t i = 0;; ++i) {
         const uint32_t j = i % kSpSlots;
-        mb_wait(gfull + j, (i / kSpSlots) & 1);
+        mb_wait_sleep(gfull + j, (i / kSpSlots) & 1, 400);
         const uint32_t b = gid[j];
         if (b == kSpEnd) return;
         SpGroup G;
         sp_group(a, b, G);
-        mb_wait(aready, i & 1);
+        mb_wait_sleep(aready, i & 1, 400);
         for (uint32_t u = lw; u < G.ng; u += kSpL)
             sd_finish_query(a, G.qs[u], accs + (size_t)u * kSlotRows, G.n, G.start, keys + lw * kSdSmall,
                             hists + lw * 256);

@@ -33,6 +33,27 @@ __device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity), "r"(1000000u)
         : "memory");
 }
+// Long waits of role warps that are off the critical path (a selection warp
+// waiting for the next group's sums, a producer waiting for a ring slot): the
+// try_wait above wakes every few dozen cycles and its retry loop still takes
+// issue slots from the arithmetic warps on the same scheduler; sleeping between
+// polls does not.
+__device__ __forceinline__ void mb_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    for (;;) {
+        uint32_t done;
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(su32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        __nanosleep(ns);
+    }
+}
 __device__ __forceinline__ void tma2d_u(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "

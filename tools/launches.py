@@ -3,7 +3,7 @@
 import csv, re, sys
 
 rows = list(csv.reader(open(sys.argv[1])))
-anchor = sys.argv[2] if len(sys.argv) > 2 else "rotate_kernel"
+anchor = sys.argv[2] if len(sys.argv) > 2 else "rotate"
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 h = rows[hi]
 ki, vi = h.index("Kernel Name"), h.index("Metric Value")
