@@ -37,6 +37,9 @@ def main(parts=(256,), iters=10):
         torch.cuda.synchronize()
         bt = time.time() - t0
         dev.apply(dco)
+        import os
+        if os.environ.get("SEED_ROWS"):
+            _capi.check(_capi.lib.dade_gpu_set_seed_rows(dev.h, int(os.environ["SEED_ROWS"])))
 
         def search():
             _capi.check(_capi.lib.dade_gpu_flat_search(dev.h, _capi.ptr(q), nq, k, _capi.QUERIES_RAW | _capi.DEVICE_PTRS,

@@ -14,7 +14,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def main(name="config1", warm=3):
+def main(name="config1", warm=3, parts=0):
     import torch
 
     import paper_2411_17229_b200 as gp
@@ -26,6 +26,8 @@ def main(name="config1", warm=3):
     dev = gp.Device(0)
     if cfg.flat:
         idx = gp.FlatIndex(dev, read_fvecs(art / "base.fvecs"))
+        if parts:  # the data-ordered scan (dade_gpu_flat_partition), as bench.py's config4 block runs it
+            idx.partition(parts, 10, 1)
     else:
         idx = gp.IvfIndex.from_divf(dev, read_divf(art / "index.ivf"))
     dco = gp.DadeStrategy(read_transform(art / "t.dade"), read_cal(art / "c.cal"), cfg.delta_d, dev=dev)
@@ -57,4 +59,4 @@ def main(name="config1", warm=3):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["config1"]))
+    main(sys.argv[1] if len(sys.argv) > 1 else "config1", parts=int(sys.argv[2]) if len(sys.argv) > 2 else 0)
