@@ -530,7 +530,7 @@ void set_tables(dade_gpu_ctx* c, uint32_t kind, uint32_t dim, std::vector<uint32
 bool coarse_tc_ok(dade_gpu_ctx* c, uint32_t n_probe) {
     // (the data-ordered flat scan probes every cell in any order: no selection cap)
     return (n_probe <= 256 || (c->coarse_all && n_probe == c->n_clusters && c->n_clusters <= 1024)) &&
-           !c->coarse_force_exact;
+           !c->coarse_force_exact && c->dim <= kCoarseTcMaxDim;  // (the bound's error budget, common.cuh)
 }
 // Above 1024 centroids the selection is fused with the GEMM (two tcgen05 passes:
 // group minima, then the candidates lo <= T0; p~ never reaches memory).

@@ -130,8 +130,14 @@ __device__ __forceinline__ void warp_hist_find(const uint32_t* hist, uint32_t ra
     before = __shfl_sync(0xffffffffu, b, src);
 }
 
-// Coarse ranking bound (coarse.cu): |p~ - l2_sq| <= kCoarseDelta (|q|^2 + |c|^2)
-constexpr float kCoarseDelta = 4e-3f;
+// Coarse ranking bound (coarse.cu): |p~ - l2_sq| <= kCoarseDelta (|q|^2 + |c|^2). Budget, in units of
+// |q|^2 + |c|^2, for dim <= kCoarseTcMaxDim = 2048: TF32 operands (fp32 bits, low 13 mantissa bits ignored:
+// < 2^-10 relative each) put 2 c.q off by < 2^-9 + 2^-20 = 1.95e-3; the tensor core's fp32 accumulation over
+// dim / 8 steps < 6e-5; the fp32 norms < gamma_dim = 1.2e-4; the reference's sequential fp32 l2_sq differs from
+// the real value by < gamma_dim d^2 <= 2.4e-4. Sum < 2.37e-3 (2.16e-3 up to dim 1024): 2.6e-3 holds with margin
+// (4e-3 until round 2; the tighter bound leaves a third fewer uncertain centroids for the exact rounds).
+constexpr float kCoarseDelta = 2.6e-3f;
+constexpr uint32_t kCoarseTcMaxDim = 2048;  // longer vectors rank with the exact kernels
 // the bound's half-width and the upper / lower keys, with explicit roundings so every
 // kernel that forms them (GEMM epilogue, selections) gets the same bits
 __device__ __forceinline__ float coarse_delta(float cn, float qn) { return __fmul_rn(kCoarseDelta, __fadd_rn(cn, qn)); }
