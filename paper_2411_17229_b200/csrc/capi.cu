@@ -897,9 +897,9 @@ bool umma_ok(dade_gpu_ctx* c, const ChunkTable& ct, bool tma128) {
     return d0 % 8 == 0 && d0 <= 2 * kBox;
 }
 
-// Streaming passes: [nearest lists], [the rest] (or one flat pass). Each pass =
-// tensor-core filter -> survivor kernel -> candidate buckets -> merge into the
-// running top-K; between passes every query's radius is tightened from it.
+// Streaming passes after the radius seed (their number and row ranges are chosen
+// below). Each pass = tensor-core filter -> survivor kernel -> candidate buckets ->
+// merge into the running top-K; between passes every query's radius is tightened from it.
 struct SeedArgs {
     bool on;
     const uint64_t* probes;
@@ -1006,11 +1006,10 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
         if (!resume && c->dump_cap)
             cuda_check(cudaMemsetAsync(c->dump_count.p, 0, 4, s), "memset");
         tl_mark(c, "seeded", s);
-        // passes: nearest lists' first row piece, their remaining pieces, all other
-        // lists (IVF); or one flat pass. The radius is tightened after each.
-        // IVF: nearest lists' first pieces, their other pieces, the other lists.
-        // Flat (one list holding the whole base, every query on it): row ranges
-        // of 1024-row pieces growing 4x per pass, the radius tightened between.
+        // Each pass = filter -> survivors -> merge; the radius is tightened after each.
+        // IVF (mma.sync / SIMT filters): nearest lists' first pieces, their other pieces, the
+        // other lists. Flat (one list holding the whole base, every query on it): row ranges
+        // of 1024-row pieces growing 4x per pass.
         static const uint32_t flat_lo[6] = {0, 2, 8, 32, 128, 512};
         static const uint32_t flat_hi[6] = {2, 8, 32, 128, 512, 0xffffffffu};
         // IVF: pass 0 = the nearest lists' next rows, then (tcgen05 filter) one pass over
