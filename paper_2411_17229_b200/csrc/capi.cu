@@ -1029,6 +1029,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
             const double mean_len = (double)n_rows / g->n_lists;
             const double pairs = (double)nq * seed.n_probe * mean_len;
             single = !(mean_len > 2.0 * seed_rows(c, k, a.dim, flat) && pairs >= 1e9);
+            if (env_flag("DADE_GPU_TWO_PASS")) single = false;  // test hook: the two-pass structure at test sizes
         }
         const int n_pass = flat ? 6 : single ? 1 : two_pass ? (fold ? 2 : 3) : 1;
         // The next staging's H2D (pipelined batches) starts with the last pass, not

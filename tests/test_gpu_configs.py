@@ -289,6 +289,36 @@ def test_k100_d256_seed_persist_fd_exact(gp, oracle_lib, d256):
     assert_same_results(gi, gd, gc, oi, od, oc)
 
 
+@pytest.mark.parametrize("two_pass", ["0", "1"])
+def test_k100_d256_pass_structures(gp, oracle_lib, d256, monkeypatch, two_pass):
+    """The streaming scan after the seed runs as ONE pass when a separate pass over the nearest
+    lists' next rows does not pay (capi.cu stream_passes: the default at these sizes) and as two
+    (nearest lists' next 1024 rows, radius tightened, then everything else) where it does --
+    DADE_GPU_TWO_PASS=1 forces that structure here. Both must return the oracle's FD answer under
+    an unbounded DADE table (every pair survives every checkpoint), and exact ascending distances
+    under a pruning one."""
+    dev = d256["dev"]
+    idx, qs, dim = d256["idx"], d256["qs"], d256["dim"]
+    monkeypatch.setenv("DADE_GPU_TWO_PASS", two_pass)
+    dev.set_graphs(False)
+    try:
+        oi, od, oc, _ = oracle_lib.ivf_search(idx.centroids, idx.offsets, idx.ids, idx.storage, qs, 100, 6)
+        t = gp.OrthoTransform(dim, 0, np.zeros(dim), np.linspace(2.0, 0.1, dim), np.eye(dim).reshape(-1))
+        unb = gp.DadeStrategy(t, gp.CalibrationTable.unbounded(dim, 32), 32, dev=dev)
+        gi, gd, gc = idx.search_batch(qs, 100, 6, unb)
+        assert_same_results(gi, gd, gc, oi, od, oc)
+        ads = gp.AdsamplingStrategy(dim, 32, 2.1, dev=dev)
+        ai, ad, ac = idx.search_batch(qs, 100, 6, ads)
+        data = d256["data"]
+        for q in range(0, len(qs), 17):
+            for j in range(ac[q]):
+                ex = math.sqrt(oracle_lib.partial_sqdist(data[ai[q, j]], qs[q], 0, dim))
+                assert np.float32(ex) == ad[q, j]
+            assert np.all(np.diff(ad[q, :ac[q]]) >= 0)
+    finally:
+        dev.set_graphs(True)
+
+
 def test_hot_path_estimator_values(gp, oracle_lib, ref_lib, d256, monkeypatch, tmp_path):
     """Every checkpoint partial the survivor kernel evaluates (DADE_GPU_DEBUG=1
     sends every pair there, pruned-by-bound ones included) equals
