@@ -1,7 +1,8 @@
 """Config 4 through the product's data-ordered flat scan (FlatIndex.partition ->
 dade_gpu_flat_partition, then dade_gpu_flat_search): partition build time,
 device time per 4096-query batch, recall, for each cell count given.
-    python tools/flat_ordered_probe.py [n_parts ...] [--iters N]"""
+    python tools/flat_ordered_probe.py [n_parts ...] [--iters N]
+SEED_ROWS=N in the environment overrides the seeded rows (dade_gpu_set_seed_rows)."""
 import sys
 import time
 from pathlib import Path
