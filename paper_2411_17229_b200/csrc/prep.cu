@@ -61,6 +61,33 @@ __device__ __noinline__ float rotate_exact(const double* __restrict__ W, uint32_
     return __double2float_rn(acc);
 }
 
+// The same element by one warp (the kernels' fix lists): the products fl(w_r x_r) do not depend on the
+// running sum, so the lanes form them 256 at a time from coalesced loads into shared memory (prod: 256
+// doubles, warp-private) and lane 0 alone runs the reference's DADD chain over them, in r order. A single
+// lane doing loads and chain (rotate_exact) waits one L2 round trip per r: ~150 us for one element at
+// dim 960, which the whole CTA -- and at a one-wave grid the whole kernel -- then waits for.
+__device__ __forceinline__ void rotate_exact_warp(const double* __restrict__ W, uint32_t dim,
+                                                  const float* __restrict__ in, uint32_t row, uint32_t col,
+                                                  double* prod, float* dst) {
+    const uint32_t lane = threadIdx.x & 31;
+    const double* w = W + (size_t)col * dim;
+    const float* x = in + (size_t)row * dim;
+    double acc = 0.0;
+    for (uint32_t r0 = 0; r0 < dim; r0 += 256) {
+        const uint32_t m = min(256u, dim - r0);
+        __syncwarp();
+#pragma unroll
+        for (uint32_t i = 0; i < 256; i += 32)
+            if (i + lane < m) prod[i + lane] = __dmul_rn(__ldg(w + r0 + i + lane), (double)__ldg(x + r0 + i + lane));
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll 8
+            for (uint32_t i = 0; i < m; ++i) acc = __dadd_rn(acc, prod[i]);
+        }
+    }
+    if (lane == 0) *dst = __double2float_rn(acc);
+}
+
 __global__ void __launch_bounds__(128, 5)
 rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in, uint32_t n,
               float* __restrict__ out) {
@@ -181,11 +208,11 @@ rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restric
                 }
             }
     }
-    __syncthreads();
+    __syncthreads();  // (the staging buffers are free: ws[0] holds the warps' product blocks)
     const uint32_t nf = min(n_fix, (uint32_t)kRotFix);
-    for (uint32_t e = tid; e < nf; e += blockDim.x) {
+    for (uint32_t e = warp; e < nf; e += blockDim.x / 32) {
         const uint32_t row = row0 + (fix[e] >> 8), col = col0 + (fix[e] & 0xffu);
-        out[(size_t)row * dim + col] = rotate_exact(W, dim, in, row, col);
+        rotate_exact_warp(W, dim, in, row, col, &ws[0][warp * 256], out + (size_t)row * dim + col);
     }
 }
 
@@ -331,11 +358,12 @@ rotate_ksplit_kernel(const double* __restrict__ W, uint32_t dim, const float* __
                 }
         }
     }
-    __syncthreads();
+    __syncthreads();  // (the staging buffers are free: rk_smem holds the warps' product blocks)
     const uint32_t nf = min(n_fix, (uint32_t)kRotFix);
-    for (uint32_t e = tid; e < nf; e += blockDim.x) {
+    for (uint32_t e = warp; e < nf; e += blockDim.x / 32) {
         const uint32_t row = row0 + (fix[e] >> 8), col = col0 + (fix[e] & 0xffu);
-        out[(size_t)row * dim + col] = rotate_exact(W, dim, in, row, col);
+        rotate_exact_warp(W, dim, in, row, col, reinterpret_cast<double*>(rk_smem) + warp * 256,
+                          out + (size_t)row * dim + col);
     }
 }
 
