@@ -431,6 +431,7 @@ struct dade_gpu_ctx {
     RowAug aug_storage;
     SliceTmap seed_tm;
     DevBuf seed_work;  // persistent seed's group counter
+    DevBuf rot_fix;    // rotation: launch-wide list of undecided elements [cap] uint2 + its counter
     DevBuf seed_order; // persistent seed's costliest-first group order
     DevBuf qslots;     // per-query candidate slots [nq][kQSlots] of a streaming pass
     DevBuf cand_total; // candidates of a pass (census, qslots mode)
@@ -883,6 +884,18 @@ __global__ void min_u32_kernel(uint32_t* r, const uint32_t* other, uint32_t n) {
 
 // The streaming tensor-core path applies when the first checkpoint is a
 // multiple of 8 dims (MMA k) within two 32-dim TMA boxes.
+constexpr uint32_t kRotFixCap = 1u << 20;  // undecided rotation outputs per launch handled by rotate_fix_kernel
+cudaError_t rotate_on(dade_gpu_ctx* c, uint32_t dim, const float* in, uint32_t n, float* out) {
+    // Long vectors only: the undecided share grows with dim (1e-4 at dim 256, ~1% at dim 960, where the
+    // in-CTA recompute was a third of the kernel: config 2 170.6 -> 129.5 + 13 us); at dim 256 the few
+    // in-CTA recomputes cost less than a second launch (config 1 77.7 vs 77.2 + 7.2 us).
+    if (dim < 512) return launch_rotate(c->W.as<double>(), dim, in, n, out, c->stream);
+    c->rot_fix.ensure((size_t)kRotFixCap * 8 + 16);
+    uint2* fix = c->rot_fix.as<uint2>();
+    return launch_rotate(c->W.as<double>(), dim, in, n, out, c->stream, fix,
+                         reinterpret_cast<uint32_t*>(fix + kRotFixCap), kRotFixCap);
+}
+
 bool filter_ok(dade_gpu_ctx* c, const ChunkTable& ct, uint32_t dim) {
     if (!ct.use_tc || !ct.use_tma || ct.n_ckpt > 63) return false;
     const uint32_t d0 = ct.end[ct.n_dense - 1];
@@ -1542,8 +1555,7 @@ const float* stage_queries_overlapped(dade_gpu_ctx* c, const float* queries, uin
     for (uint32_t i = 0, q0 = 0; i < nch; q0 += sizes[i], ++i) {
         const uint32_t m = sizes[i];
         cuda_check(cudaStreamWaitEvent(c->stream, c->copy_ev[i], 0), "wait");
-        cuda_check(launch_rotate(c->W.as<double>(), dim, c->q_in.as<float>() + (size_t)q0 * dim, m,
-                                 c->q_rot.as<float>() + (size_t)q0 * dim, c->stream),
+        cuda_check(rotate_on(c, dim, c->q_in.as<float>() + (size_t)q0 * dim, m, c->q_rot.as<float>() + (size_t)q0 * dim),
                    "rotate");
         ++c->launches;
         if (coarse) coarse_tc_range(c, c->q_rot.as<float>(), q0, m, n_probe);
@@ -1572,7 +1584,7 @@ const float* stage_queries(dade_gpu_ctx* c, const float* queries, uint32_t nq, u
     if (flags & DADE_GPU_QUERIES_RAW) {
         if (c->t_dim != dim) fail(DADE_GPU_CONFIG_ERROR, "raw queries need a transform of the index dim");
         c->q_rot.ensure(bytes);
-        cuda_check(launch_rotate(c->W.as<double>(), dim, d_in, nq, c->q_rot.as<float>(), c->stream), "rotate");
+        cuda_check(rotate_on(c, dim, d_in, nq, c->q_rot.as<float>()), "rotate");
         ++c->launches;
         return c->q_rot.as<float>();
     }
@@ -2253,15 +2265,14 @@ int dade_gpu_rotate(dade_gpu_ctx* c, const float* in, uint32_t n, float* out, ui
         c->use_device();
         const size_t bytes = (size_t)n * c->t_dim * 4;
         if (flags & DADE_GPU_DEVICE_PTRS) {
-            cuda_check(launch_rotate(c->W.as<double>(), c->t_dim, in, n, out, c->stream), "rotate");
+            cuda_check(rotate_on(c, c->t_dim, in, n, out), "rotate");
             ++c->launches;
             return;
         }
         c->q_in.ensure(bytes);
         c->q_rot.ensure(bytes);
         cuda_check(cudaMemcpyAsync(c->q_in.p, in, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
-        cuda_check(launch_rotate(c->W.as<double>(), c->t_dim, c->q_in.as<float>(), n, c->q_rot.as<float>(), c->stream),
-                   "rotate");
+        cuda_check(rotate_on(c, c->t_dim, c->q_in.as<float>(), n, c->q_rot.as<float>()), "rotate");
         ++c->launches;
         cuda_check(cudaMemcpyAsync(out, c->q_rot.p, bytes, cudaMemcpyDeviceToHost, c->stream), "D2H");
         cuda_check(cudaStreamSynchronize(c->stream), "rotate");

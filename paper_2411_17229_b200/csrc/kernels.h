@@ -241,8 +241,10 @@ cudaError_t launch_seed_radius(const uint64_t* probes, uint32_t n_probe, const u
                                const float* storage, const uint32_t* row_ids, uint32_t dim, const float* queries,
                                uint32_t nq, uint32_t K, uint32_t S, uint32_t* r_global, uint64_t* out_keys,
                                uint32_t* out_count, cudaStream_t s);
+// fix / fix_n / fix_cap (nullable): a launch-wide list for the elements whose rounding the tensor-core
+// sum cannot decide; a second kernel recomputes them one warp each (else each CTA recomputes its own)
 cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
-                          cudaStream_t s);
+                          cudaStream_t s, uint2* fix = nullptr, uint32_t* fix_n = nullptr, uint32_t fix_cap = 0);
 // Probe grouping (K3): probe keys [nq x nprobe] (low 32 bits = list id) ->
 // per (rank bucket, list) query buckets and work items, ordered by rank bucket.
 struct GroupArgs {

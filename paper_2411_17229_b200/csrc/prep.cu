@@ -90,7 +90,7 @@ __device__ __forceinline__ void rotate_exact_warp(const double* __restrict__ W, 
 
 __global__ void __launch_bounds__(128, 5)
 rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in, uint32_t n,
-              float* __restrict__ out) {
+              float* __restrict__ out, uint2* __restrict__ gfix, uint32_t* __restrict__ gfix_n, uint32_t gfix_cap) {
     __shared__ __align__(16) float xs[2][kRotT * kRotS];
     __shared__ __align__(16) double ws[2][kRotT * kRotS];
     __shared__ double wn[kRotT], xn[kRotT];
@@ -201,6 +201,10 @@ rotate_kernel(const double* __restrict__ W, uint32_t dim, const float* __restric
                 const float hi = __double2float_rn(__dadd_ru(acc, e));
                 if (__float_as_uint(lo) == __float_as_uint(hi) && !isnan(lo)) {
                     out[(size_t)row * dim + col] = lo;
+                } else if (gfix) {  // the launch-wide list: rotate_fix_kernel spreads these over the GPU
+                    const uint32_t gs = atomicAdd(gfix_n, 1u);
+                    if (gs < gfix_cap) gfix[gs] = make_uint2(row, col);
+                    else out[(size_t)row * dim + col] = rotate_exact(W, dim, in, row, col);
                 } else {
                     const uint32_t slot = atomicAdd(&n_fix, 1u);
                     if (slot < (uint32_t)kRotFix) fix[slot] = (rl << 8) | cl;
@@ -227,7 +231,8 @@ constexpr int kRkWarp = 2 * kRkT * kRotS * 12; // bytes per warp: x [2][32][20] 
 
 __global__ void __launch_bounds__(128, 4)
 rotate_ksplit_kernel(const double* __restrict__ W, uint32_t dim, const float* __restrict__ in, uint32_t n,
-                     float* __restrict__ out) {
+                     float* __restrict__ out, uint2* __restrict__ gfix, uint32_t* __restrict__ gfix_n,
+                     uint32_t gfix_cap) {
     extern __shared__ __align__(16) unsigned char rk_smem[];
     __shared__ double wn[kRkT], xn[kRkT];
     __shared__ uint32_t fix[kRotFix];
@@ -350,6 +355,10 @@ rotate_ksplit_kernel(const double* __restrict__ W, uint32_t dim, const float* __
                     const float hi = __double2float_rn(__dadd_ru(acc, e));
                     if (__float_as_uint(lo) == __float_as_uint(hi) && !isnan(lo)) {
                         out[(size_t)row * dim + col] = lo;
+                    } else if (gfix) {
+                        const uint32_t gs = atomicAdd(gfix_n, 1u);
+                        if (gs < gfix_cap) gfix[gs] = make_uint2(row, col);
+                        else out[(size_t)row * dim + col] = rotate_exact(W, dim, in, row, col);
                     } else {
                         const uint32_t slot = atomicAdd(&n_fix, 1u);
                         if (slot < (uint32_t)kRotFix) fix[slot] = (rl << 8) | cl;
@@ -1057,8 +1066,24 @@ cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, size_t n, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// The undecided elements of a rotation launch (rotate_kernel / rotate_ksplit_kernel append them to fix),
+// one warp per element over the whole GPU: at dim 960 about 1% of the outputs are undecided, and
+// recomputing them inside the CTA that found them left every CTA with a ~12 us serial tail.
+__global__ void __launch_bounds__(128) rotate_fix_kernel(const double* __restrict__ W, uint32_t dim,
+                                                         const float* __restrict__ in, float* __restrict__ out,
+                                                         const uint2* __restrict__ fix, const uint32_t* __restrict__ fix_n,
+                                                         uint32_t fix_cap) {
+    __shared__ double prod[4][256];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t n = min(*fix_n, fix_cap);
+    for (uint32_t e = blockIdx.x * 4 + warp; e < n; e += gridDim.x * 4) {
+        const uint2 rc = fix[e];
+        rotate_exact_warp(W, dim, in, rc.x, rc.y, prod[warp], out + (size_t)rc.x * dim + rc.y);
+    }
+}
+
 cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32_t n, float* out,
-                          cudaStream_t s) {
+                          cudaStream_t s, uint2* fix, uint32_t* fix_n, uint32_t fix_cap) {
     if (n == 0) return cudaSuccess;
     static int n_sm = 0;
     if (!n_sm) {
@@ -1066,16 +1091,25 @@ cudaError_t launch_rotate(const double* W, uint32_t dim, const float* in, uint32
         if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
             n_sm = 148;
     }
+    if (!fix || !fix_n || !fix_cap) {
+        fix = nullptr;
+        fix_n = nullptr;
+        fix_cap = 0;
+    } else {
+        DADE_CUDA_TRY(cudaMemsetAsync(fix_n, 0, 4, s));
+    }
     const uint64_t tiles64 = (uint64_t)((dim + kRotT - 1) / kRotT) * ((n + kRotT - 1) / kRotT);
     if (tiles64 < 2ull * n_sm && dim >= 4 * kRotK) {  // small batch: 32 x 32 tiles, r split over the warps
         const size_t smem = 4 * (size_t)kRkWarp;
         DADE_CUDA_TRY(cudaFuncSetAttribute(rotate_ksplit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dim3 grid((dim + kRkT - 1) / kRkT, (n + kRkT - 1) / kRkT);
-        rotate_ksplit_kernel<<<grid, 128, smem, s>>>(W, dim, in, n, out);
-        return cudaGetLastError();
+        rotate_ksplit_kernel<<<grid, 128, smem, s>>>(W, dim, in, n, out, fix, fix_n, fix_cap);
+    } else {
+        dim3 grid((dim + kRotT - 1) / kRotT, (n + kRotT - 1) / kRotT);
+        rotate_kernel<<<grid, 128, 0, s>>>(W, dim, in, n, out, fix, fix_n, fix_cap);
     }
-    dim3 grid((dim + kRotT - 1) / kRotT, (n + kRotT - 1) / kRotT);
-    rotate_kernel<<<grid, 128, 0, s>>>(W, dim, in, n, out);
+    DADE_CUDA_TRY(cudaGetLastError());
+    if (fix) rotate_fix_kernel<<<n_sm * 16, 128, 0, s>>>(W, dim, in, out, fix, fix_n, fix_cap);  // all resident
     return cudaGetLastError();
 }
 
