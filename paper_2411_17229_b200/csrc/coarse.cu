@@ -264,6 +264,10 @@ __global__ void __launch_bounds__(128) coarse_select_kernel(const float* __restr
 //     row chunk), each lane then advancing its candidate's sequential fp32 sum;
 //   * (acc, id) bitonic sort of the candidates, first n_probe -> probes.
 constexpr int kFsWarps = 4;
+// candidates per query of coarse_select_fast_kernel: 384 keeps a CTA under 32 KB of shared memory, so seven
+// CTAs fit an SM and a 1000-query batch (one CTA per query) is ONE wave of 1036 slots instead of a full wave of
+// 888 and a tail of 112 (config 2: the kernel took two per-query latencies)
+constexpr int kFsCap = 384;
 __device__ __forceinline__ void cs_cp16(float* dst, const float* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
                  "l"(src)
@@ -336,12 +340,12 @@ __device__ __forceinline__ float exact_l2_round(const float* __restrict__ cen, c
 // warp w runs the exact rounds w, w + 4, ... and writes its keys into warp 0's
 // list, which warp 0 sorts after the CTA barrier.
 template <int WPQ>
-__global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
+__global__ void __launch_bounds__(kFsWarps * 32, WPQ == 1 ? 6 : 7) coarse_select_fast_kernel(
     const float* __restrict__ pt, const float* __restrict__ cnorm, const float* __restrict__ qnorm,
     const float* __restrict__ cen, uint32_t n_cen, const float* __restrict__ q, uint32_t nq, uint32_t dim,
     uint32_t n_probe, uint64_t* __restrict__ probes, uint32_t* __restrict__ overflow, uint32_t* census = nullptr,
     bool exact_all = true) {
-    __shared__ uint64_t cand[kFsWarps][kSelCap];
+    __shared__ uint64_t cand[kFsWarps][kFsCap];
     __shared__ __align__(16) float rows[kFsWarps][32 * kFsRS];
     __shared__ __align__(16) float qch[kFsWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -401,13 +405,13 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
         const bool is = lk[j] <= B && (lane + 32u * j) < n_cen;
         const uint32_t bal = __ballot_sync(0xffffffffu, is);
         const uint32_t pos = n + __popc(bal & ((1u << lane) - 1u));
-        if (is && pos < (uint32_t)kSelCap) cand[warp][pos] = lane + 32u * j;
+        if (is && pos < (uint32_t)kFsCap) cand[warp][pos] = lane + 32u * j;
         n += __popc(bal);
     }
     if (census && lane == 0 && (WPQ == 1 || warp == 0)) atomicAdd(census, n);  // DADE_GPU_COARSE_CENSUS
-    if (n > (uint32_t)kSelCap) {  // pathological ties: the host redoes the search all-exact
+    if (n > (uint32_t)kFsCap) {  // pathological ties: the host redoes the search all-exact
         if (lane == 0) atomicAdd(overflow, 1u);
-        n = kSelCap;
+        n = kFsCap;
     }
     __syncwarp();
     // Sure members: a candidate c with hi_c <= B that fewer than n_probe other
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
     uint32_t nS = 0;
     if (!exact_all) {
         uint32_t* klo = reinterpret_cast<uint32_t*>(rows[warp]);  // free until the exact rounds
-        uint32_t* khi = klo + kSelCap;                             // (2 x 512 <= 32 x 36 words)
+        uint32_t* khi = klo + kFsCap;                             // (2 x 384 <= 32 x 36 words)
         for (uint32_t e = lane; e < n; e += 32) {
             const uint32_t c = (uint32_t)cand[warp][e];
             const float p = prow[c], d = coarse_delta(cnorm[c], qn);
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_select_fast_kernel(
             khi[e] = fkey(__fadd_rn(p, d));
         }
         __syncwarp();
-        constexpr int kG = kSelCap / 32;
+        constexpr int kG = kFsCap / 32;
         uint32_t ids[kG];
         uint32_t smask = 0;
         const uint32_t ng = (n + 31) / 32;
@@ -788,7 +792,7 @@ __global__ void __launch_bounds__(kFsWarps * 32, 6) coarse_finish_kernel(
 void launch_select_any(const float* pt, const float* cnorm, const float* qnorm, const float* centroids, uint32_t n_cen,
                        const float* queries, uint32_t nq, uint32_t dim, uint32_t n_probe, uint64_t* probes,
                        uint32_t* overflow, cudaStream_t s, const uint32_t* gmin = nullptr, bool exact_all = true) {
-    if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kSelCap) {
+    if (n_cen <= 1024 && dim % 4 == 0 && n_probe <= kFsCap) {
         uint32_t* census = nullptr;
         if (nq <= 4096 && n_probe > 32)  // > 1 exact round
             // (warps split the exact rounds: skipping the sure members saves no latency here)
