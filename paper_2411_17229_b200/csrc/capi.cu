@@ -730,8 +730,12 @@ constexpr uint32_t kFilterQ = 32;           // queries per streaming work item (
 // Pass 0 takes the pieces covering the first kFilterItemRows rows.
 constexpr uint32_t kUmmaQ = 256;            // queries per tcgen05 work item (MMA N)
 constexpr uint32_t kQSlots = 256;           // per-query candidate slots of a streaming pass
-uint32_t rank0_item_rows(bool umma) {
-    return umma ? 128 : 32;  // one tile: a nearest list's heavy rows spread over every SM / warp
+uint32_t rank0_item_rows(bool umma, bool dense_groups) {
+    // one tile: a nearest list's heavy rows spread over every SM / warp -- when the list has several queries.
+    // With about one query per nearest list (config 2: 1000 queries on 1024 lists) short pieces only multiply
+    // the items (six 128-row items of ONE query per list, each paying its staging and pipeline fill).
+    if (umma && !dense_groups) return kFilterItemRows;
+    return umma ? 128 : 32;
 }
 constexpr uint32_t kSeedRowsDefault = 1024;  // rows of the nearest list used by the radius seed
 
@@ -1102,7 +1106,7 @@ void stream_passes(dade_gpu_ctx* c, const ScanArgs& a, const ChunkTable& ct, con
                 }
             } else if (two_pass && !single) {
                 // pass 0: kFilterItemRows rows of each nearest list past the seed
-                const uint32_t p0 = std::max<uint32_t>(1, kFilterItemRows / rank0_item_rows(umma));
+                const uint32_t p0 = std::max<uint32_t>(1, kFilterItemRows / rank0_item_rows(umma, c->dense_groups));
                 if (pass == 0 || (pass == 1 && !fold)) {
                     f.n_items = g->n_items + 1;  // rank-bucket-0 items: every query's nearest list
                     f.piece_lo = pass == 0 ? 0u : p0;
@@ -1258,7 +1262,7 @@ void ivf_search_device(dade_gpu_ctx* c, const float* d_q, uint32_t nq, uint32_t 
         g.rb_end[1] = n_probe;
         g.n_rb = nrb = 2;
     }
-    g.rank0_item_rows = use_filter && nrb > 1 ? rank0_item_rows(umma) : 0;
+    g.rank0_item_rows = use_filter && nrb > 1 ? rank0_item_rows(umma, c->dense_groups) : 0;
     g.q_chunk = umma ? kUmmaQ : use_filter ? kFilterQ : (uint32_t)kQC;
     const bool seeded = n_probe > 1 && k <= 512;
     if (use_filter && seeded) {  // the seed's rows of every nearest list are final results already
